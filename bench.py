@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Geometry-to-grid benchmark (BASELINE.json metric) on B200.
+
+One step = the whole hot path on one geometry: binary-STL records -> SoA
+import -> face binning -> per level {near-wall marking, propagation,
+refinement / block allocation} -> lattice boundary links + q on the finest
+level.  ``value`` is cell-face tests / s (T of SURVEY.md §8d over the step's
+marking passes divided by the step's device time) with the STL records
+resident in HBM; ``e2e`` repeats the step from pinned host bytes with the
+H2D copy and the D2H of the results (forest arrays, link flags, q) inside the
+timed region.  ``ms_per_step`` is the geometry-to-grid time.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (strong scaling, NCCL)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIGS = {
+    "C1": dict(workload="C1 circle text primitive 12800 edges, 64^2 root, d=0.1, 3 levels, B=8, D2Q9",
+               kind="text", text="circle 0.5 0.5 0.25 12800\n", dim=2, root=64, d=0.1, levels=3, B=8,
+               lattice="D2Q9"),
+    "C2": dict(workload="C2 icosphere 20480 triangles (binary STL), 16^3 root, d=0.05, 3 levels, B=8, D3Q19",
+               kind="ico", subdiv=5, dim=3, root=16, d=0.05, levels=3, B=8, lattice="D3Q19"),
+    "C3": dict(workload="C3 bumpy lat-lon sphere 69936 triangles (binary STL), 16^3 root, d=0.05, 4 levels, "
+                        "B=8, D3Q27", kind="bumpy", dim=3, root=16, d=0.05, levels=4, B=8, lattice="D3Q27"),
+    "C4": dict(workload="C4 torus knot 1M triangles (binary STL), 16^3 root, d=0.02, 5 levels, B=32, D3Q19",
+               kind="knot", dim=3, root=16, d=0.02, levels=5, B=32, lattice="D3Q19"),
+    "C5": dict(workload="C5 icosphere 5.24M triangles (binary STL), 64^3 root, d=0.01, 3 levels, B=64, D3Q19",
+               kind="ico", subdiv=9, dim=3, root=64, d=0.01, levels=3, B=64, lattice="D3Q19"),
+}
+
+FP32_OPS_PER_TEST = {3: 130, 2: 21}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def make_input(cfg):
+    from paper_2502_16310_b200 import shapes
+
+    if cfg["kind"] == "text":
+        return cfg["text"].encode()
+    if cfg["kind"] == "ico":
+        tris = shapes.icosphere_triangles(cfg["subdiv"])
+    elif cfg["kind"] == "bumpy":
+        tris = shapes.bumpy_sphere_triangles()
+    else:
+        tris = shapes.torus_knot_triangles()
+    return shapes.binary_stl_bytes(tris)
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    def __init__(self, index, period=0.01):
+        self.index, self.period = index, period
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.nv = pynvml
+            names = {
+                "hw_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+                "sw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                "hw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                "sw_power_cap": getattr(pynvml, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+                "hw_power_brake_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80),
+            }
+            self.names = names
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                        r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h) if hasattr(
+                            self.nv, "nvmlDeviceGetCurrentClocksEventReasons") else \
+                            self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                        for k, bit in self.names.items():
+                            if r & bit:
+                                self.reasons.add(k)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception as e:  # pragma: no cover
+            log("clock sampling unavailable:", e)
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": float(self.max_mhz) if self.max_mhz else None,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def gpu_arm(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2502_16310_b200 as ow
+    from paper_2502_16310_b200 import _lib, parallel
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    shard = parallel.Shard() if world > 1 else None
+    data = make_input(cfg)
+    dim = cfg["dim"]
+    dom = ow.Aabb(np.zeros(dim), np.ones(dim))
+    params = ow.NearWallParams(d_spec=cfg["d"], n_levels=cfg["levels"], bins_per_axis=cfg["B"])
+    grid = ow.BinGrid(dom, cfg["B"])
+    text = cfg["kind"] == "text"
+    if text:
+        ig = ow.geometry.parse_text_primitives(data.decode())
+        n_faces = ig.n_faces
+    else:
+        n_faces = int.from_bytes(data[80:84], "little")
+        rec_host = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).pin_memory()
+        rec_dev = rec_host.to(dev)
+
+    def import_geom(records):
+        if text:
+            return ow.index_to_coords(ig)
+        return ow.geometry.stl_records_to_coords(records, n_faces)
+
+    def step(records):
+        geom = import_geom(records)
+        forest = ow.init_root_grid(dom, (cfg["root"],) * dim, capacity=8 * cfg["root"] ** dim)
+        res = ow.refine_near_wall(forest, geom, params, shard=shard)
+        ll = ow.build_lattice_links(forest, geom, grid, cfg["lattice"])
+        return res, forest, ll
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def l2_flush():
+        flush.zero_()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        res, forest, ll = step(rec_dev if not text else None)
+    T_step = int(sum(res.cell_face_tests))
+    evaluated = int(sum(res.pairs_evaluated))
+    blocks = forest.blocks_per_level()
+    n_boundary = ll.n_boundary
+
+    # ---- value: inputs resident in HBM
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    _lib.profile(True)
+    launches0 = _lib.launches()
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        for k in range(args.steps):
+            l2_flush()
+            ev[k][0].record()
+            res, forest, ll = step(rec_dev if not text else None)
+            ev[k][1].record()
+        barrier()
+    launches = _lib.launches() - launches0
+    prof = _lib.profile_read()
+    _lib.profile(False)
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+
+    # ---- e2e: pinned host bytes in, results out
+    e2e = None
+    if not args.no_e2e:
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        h2d = d2h = 0
+        barrier()
+        for k in range(args.steps):
+            l2_flush()
+            ev2[k][0].record()
+            if text:
+                res, forest, ll = step(None)
+                h2d = 0
+            else:
+                rd = rec_host.to(dev, non_blocking=True)
+                h2d = rec_host.numel()
+                res, forest, ll = step(rd)
+            outs = [forest.level_tensor, forest.coords_tensor, forest._parent_t[: forest.n_blocks],
+                    forest._first_child_t[: forest.n_blocks], forest.marks, ll.flags, ll.cells, ll.q]
+            host = [o.to("cpu") for o in outs]
+            d2h = sum(o.numel() * o.element_size() for o in host)
+            ev2[k][1].record()
+        barrier()
+        ms2 = sum(a.elapsed_time(b) for a, b in ev2)
+        t2 = torch.tensor([ms2], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        ms2 = float(t2.item()) / args.steps
+        e2e = {"value": T_step / (ms2 / 1e3), "unit": "cell-face tests/s", "ms_per_step": ms2,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # ---- roofline of the dominant kernel family
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    kern = {k: v for k, v in prof.items() if k in ("mark", "lattice", "fill_bins", "stl", "prep")}
+    dom_k = max(kern, key=lambda k: kern[k][0]) if kern else "mark"
+    mark_ms, mark_n = prof["mark"]
+    sm_mhz = clk.summary()["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # non-FMA issue rate (-fmad=false), TOP/s
+    ops = FP32_OPS_PER_TEST[dim] * evaluated * args.steps
+    achieved = ops / (mark_ms / 1e3) / 1e12 if mark_ms > 0 else 0.0
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(REPO, "profiles", "traffic.json")))
+        traffic = tj.get(args.config, {}).get("mark")
+    except Exception:
+        pass
+    roofline = {
+        "kernel": "k_mark (near-wall predicate sweep)", "bound": "fp32", "achieved": achieved,
+        "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None,
+        "traffic": traffic,
+        "peak_note": "148 SMs x 128 FP32 lanes x max SM clock, non-FMA (FMUL/FADD) issue rate; "
+                     "MEASURED_PEAKS.json has no FP32 entry",
+        "algorithmic": f"{FP32_OPS_PER_TEST[dim]} FP32 ops per evaluated cell-face predicate x {evaluated} "
+                       f"evaluations per step",
+        "launches": mark_n, "avg_launch_ms": mark_ms / max(mark_n, 1),
+        "dominant_family": dom_k,
+        "families_ms": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},
+    }
+    out = {
+        "metric": "geometry-to-grid time (ms) & cell-face tests/s at 1/2/4/8 B200 vs CPU",
+        "value": T_step / (ms_step / 1e3),
+        "unit": "cell-face tests/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "geometry_to_grid_ms": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (procedural geometry, deterministic)",
+        "config": {"workload": cfg["workload"], "faces": n_faces, "cell_face_tests_per_step": T_step,
+                   "pairs_evaluated_per_step": evaluated, "blocks_per_level": blocks,
+                   "boundary_cells": n_boundary, "l2": "flushed (256 MB write) before every step",
+                   "parallelism": f"octree-block shards x{world}, NCCL all-gather of marks"},
+        "roofline": roofline,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        out["e2e"] = e2e
+    return out
+
+
+# ---------------------------------------------------------------------------- CPU arms
+def cpu_sample(cfg):
+    """Bounded oracle sample of the same workload: the level-0 pass (import,
+    bins, marking, propagation, refinement) — returns (tests, seconds)."""
+    from oracle import binning as ob
+    from oracle import forest as of
+    from oracle import geometry as og
+    from oracle import nearwall as on
+
+    data = make_input(cfg)
+    dim = cfg["dim"]
+    t0 = time.perf_counter()
+    if cfg["kind"] == "text":
+        coords = og.index_to_coords(*og.parse_primitives(data.decode()))
+    else:
+        coords = og.stl(data)
+    f = of.Forest(np.zeros(dim), np.ones(dim), (cfg["root"],) * dim)
+    grid = ob.Grid(np.zeros(dim), np.ones(dim), cfg["B"])
+    bins = ob.fill_bins(coords, grid)
+    T = on.cell_face_tests(f, 0, grid, bins[1], coords.shape[2])
+    on.mark(f, 0, coords, cfg["d"], bins, grid)
+    on.propagate(f, 0, cfg["d"])
+    f.refine_marked(0)
+    return T, time.perf_counter() - t0
+
+
+def reference_arm(args, cfg):
+    tests = secs = 0.0
+    for _ in range(args.warmup and 1):
+        cpu_sample(cfg)
+    for _ in range(args.steps):
+        T, s = cpu_sample(cfg)
+        tests += T
+        secs += s
+    v = tests / secs
+    cb = {"value": v, "unit": "cell-face tests/s", "cores": 1, "kind": "port",
+          "sample": f"oracle (NumPy restatement of octowall) level-0 pass of {args.config}: import, fill_bins, "
+                    f"binned marking, propagation, refinement; {int(tests / args.steps)} tests per step"}
+    return {
+        "metric": "geometry-to-grid time (ms) & cell-face tests/s at 1/2/4/8 B200 vs CPU",
+        "impl": "reference", "value": v, "unit": "cell-face tests/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["workload"]}, "cpu_baseline": cb,
+        "e2e": {"value": v, "unit": "cell-face tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(reference_arm(args, cfg)), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2502_16310_b200 import _build
+
+    if rank == 0:
+        _build.build()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    out = gpu_arm(args, cfg, rank, world, local_rank)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        T, s = cpu_sample(cfg)
+        out["cpu_baseline"] = {
+            "value": T / s, "unit": "cell-face tests/s", "cores": 1, "kind": "port",
+            "sample": f"oracle level-0 pass of {args.config} ({T} tests, {s:.1f} s, 1 core, NumPy)"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

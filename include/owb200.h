@@ -1,0 +1,202 @@
+/*
+ * owb200.h — C ABI of libowb200.so, the sm_100a geometry-to-grid hot path.
+ *
+ * Drop-in boundary for the reference package `octowall`
+ * (/root/reference/pkg/src/octowall).  The reference is pure Python, so it has
+ * no FFI of its own; each entry point below replaces one reference function
+ * and is what a ctypes / cffi binding of that function binds (see
+ * INTEGRATION.md).  The Python host package paper_2502_16310_b200 mirrors the
+ * reference API on top of these calls.
+ *
+ * Conventions
+ *  - Every pointer named d_* is DEVICE memory owned by the caller (PyTorch
+ *    tensors in the Python package); the library owns only scratch inside an
+ *    ow_ctx.  Sizes are element counts.  `stream` is a cudaStream_t.
+ *  - Calls are stream-ordered.  A call that returns a host scalar through an
+ *    out_* pointer synchronises `stream` before returning.
+ *  - Return value: OW_OK or an error code mirroring octowall/errors.py:4-41
+ *    (exit codes 2/3/4); ow_last_error() returns the thread-local message.
+ *  - Arithmetic: float32 with the reference's operation order, IEEE div/sqrt,
+ *    no FMA contraction (compiled -fmad=false), float64 where the reference
+ *    uses float64 (cell centres, face boxes, degeneracy test).
+ */
+#ifndef OWB200_H
+#define OWB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  OW_OK = 0,
+  OW_ERR_INTERNAL = 1, /* CUDA / library failure                     (OctowallError)          */
+  OW_ERR_INVALID = 2,  /* bad parameter, degenerate face, outside domain (InvalidParameterError) */
+  OW_ERR_PARSE = 3,    /* malformed STL                             (GeometryParseError)     */
+  OW_ERR_CAPACITY = 4  /* bin / link capacity exceeded              (CapacityError)          */
+};
+
+enum { OW_NONE = 0, OW_MARKED = 1, OW_INTERMEDIATE = 2 }; /* forest.py:24-27 RefineMark */
+
+typedef struct ow_ctx ow_ctx;
+
+/* Regular bin grid, binning.py:34-60 (BinGrid).  min32/len32 are the float32
+ * constants the reference derives (_min32 = f32(min), _len32 = f32(extent/B)). */
+typedef struct {
+  int32_t dim;
+  int32_t bins_per_axis;
+  double dmin[3];
+  double dmax[3];
+  float min32[3];
+  float len32[3];
+} ow_grid;
+
+/* Forest-of-octrees SoA view, forest.py:47-81.  Arrays are caller-owned device
+ * memory of `capacity` entries; n_blocks entries are valid.  The library grows
+ * the forest through `grow`, a caller callback that must reallocate every
+ * array to at least `need` entries, copy the first n_blocks entries, update
+ * the pointers/capacity in *f and return 0. */
+typedef struct ow_forest ow_forest;
+typedef int (*ow_grow_fn)(void* user, ow_forest* f, int64_t need);
+struct ow_forest {
+  int32_t dim;
+  int32_t max_level;
+  int32_t root[3];
+  int32_t _pad;
+  double dmin[3];
+  double dext[3];
+  int64_t n_blocks;
+  int64_t capacity;
+  int16_t* d_level;
+  int32_t* d_coord[3]; /* lattice coordinates per axis at the block's level */
+  int32_t* d_parent;
+  int32_t* d_first_child;
+  int8_t* d_marks;
+  ow_grow_fn grow;
+  void* grow_user;
+};
+
+/* ---- context --------------------------------------------------------------- */
+int ow_ctx_create(int device, ow_ctx** out);
+int ow_ctx_destroy(ow_ctx* ctx);
+const char* ow_last_error(void);
+int ow_version(void);
+/* kernels launched by this ctx since creation (instrumentation for bench.py) */
+int64_t ow_launch_count(ow_ctx* ctx);
+/* Optional CUDA-event timing of kernel families (bench.py roofline):
+ * ids 0 mark, 1 lattice, 2 fill_bins, 3 refine, 4 propagate, 5 links,
+ * 6 STL import, 7 face prep.  ow_profile(ctx, 1) enables and resets. */
+int ow_profile(ow_ctx* ctx, int enable);
+int ow_profile_read(ow_ctx* ctx, int kernel_id, double* total_ms, int64_t* launches);
+
+/* ---- geometry import (geometry.py) ----------------------------------------- */
+/* Binary STL records (50 B each, after the 84-byte header) -> coords (3,3,F)
+ * float32 SoA [vertex slot][component][face].  Replaces _parse_binary_stl +
+ * _tris_to_geometry, geometry.py:415-436. */
+int ow_stl_binary_to_soa(ow_ctx* ctx, const uint8_t* d_records, int64_t n_faces, float* d_coords,
+                         void* stream);
+/* Pure gather coords[j][c][k] = vertices[faces[k][j]][c]; index_to_coords,
+ * geometry.py:262-273. */
+int ow_index_to_coords(ow_ctx* ctx, int32_t dim, const float* d_vertices, const int32_t* d_faces,
+                       int64_t n_faces, float* d_coords, void* stream);
+
+/* One pass over all faces: first degenerate face (validate_faces,
+ * geometry.py:276-299), first non-finite face, float32 bounding box
+ * (bounding_box, geometry.py:302-308) and max |coordinate|. */
+typedef struct {
+  int64_t first_degenerate; /* -1 if none */
+  int64_t first_nonfinite;  /* -1 if none */
+  float bbox_min[3];
+  float bbox_max[3];
+  float abs_max;
+  float _pad;
+} ow_face_summary;
+int ow_face_check(ow_ctx* ctx, int32_t dim, const float* d_coords, int64_t n_faces,
+                  ow_face_summary* out, void* stream);
+
+/* ---- binning (binning.py:200-266, fill_bins) ------------------------------- */
+/* Phase 1: sample every face (spacing h), count distinct (bin, face) pairs.
+ * Writes d_counts[n_bins] and returns the entry total.  *out_outside is the
+ * first face with a sample outside the domain (-1 if none; binning.py:74-77). */
+int ow_fill_bins_count(ow_ctx* ctx, const ow_grid* grid, const float* d_coords, int64_t n_faces,
+                       float spacing, int32_t* d_counts, int64_t* out_entries, int64_t* out_outside,
+                       void* stream);
+/* Phase 2 (after a successful phase 1 on the same ctx): d_ids[entries] grouped
+ * by bin, ascending face id within each bin; d_offsets = exclusive scan. */
+int ow_fill_bins_emit(ow_ctx* ctx, const ow_grid* grid, int32_t* d_ids, const int32_t* d_counts,
+                      int32_t* d_offsets, void* stream);
+
+/* ---- forest (forest.py) ----------------------------------------------------- */
+/* Ascending ids of childless blocks at `level` (leaf_blocks_at, forest.py:143). */
+int ow_forest_leaves(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t* d_out, int64_t* out_n,
+                     void* stream);
+/* Per-level block and leaf histograms (blocks_per_level / leaves_per_level). */
+int ow_forest_level_counts(ow_ctx* ctx, const ow_forest* f, int64_t* out_blocks, int64_t* out_leaves,
+                           int32_t max_levels, void* stream);
+/* Count blocks at `level` carrying mark `mark` (leaves only if leaf_only). */
+int ow_forest_count_marks(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t leaf_only,
+                          int32_t mark, int64_t* out_n, void* stream);
+/* Cell centres (n, 4^D, D) float32 of blocks `d_ids`, FP64 then one rounding
+ * (cell_centers_many, forest.py:187-205). */
+int ow_forest_cell_centers(ow_ctx* ctx, const ow_forest* f, const int32_t* d_ids, int64_t n,
+                           float* d_out, void* stream);
+/* Split MARKED leaves at `level` in ascending id, then restore 2:1 face
+ * balance (refine_marked, forest.py:331-370).  *out_split = blocks split. */
+int ow_refine_marked(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, void* stream);
+
+/* ---- near-wall detection (nearwall.py) ------------------------------------- */
+/* Mark leaves `d_leaves` (ascending, at one level) whose cell centres pass the
+ * FP32 near-face predicate at d_spec for a candidate face: every face (naive,
+ * d_bin_ids == NULL; mark_near_wall_naive nearwall.py:217) or the faces of the
+ * cell's bin (mark_near_wall_binned nearwall.py:253).  `reach` is the
+ * reference's conservative cull radius (nearwall.py:38-40).  Outputs:
+ * *out_marked newly MARKED blocks; *out_tests the algorithmic cell-face test
+ * count T; *out_evaluated the pairs that reached the full
+ * predicate.  geom_key identifies the immutable geometry for prep caching. */
+int ow_mark_near_wall(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
+                      const float* d_coords, int64_t n_faces, int64_t geom_key, const ow_grid* grid,
+                      const int32_t* d_bin_ids, const int32_t* d_bin_counts, const int32_t* d_bin_offsets,
+                      float d_spec, double reach, int64_t* out_marked, int64_t* out_tests,
+                      int64_t* out_evaluated, void* stream);
+/* `rounds` two-pass dilation rounds over leaves `d_leaves` (propagate_marks,
+ * nearwall.py:321-366). */
+int ow_propagate_marks(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
+                       int32_t rounds, void* stream);
+
+/* Cell-face links (build_cell_face_links, nearwall.py:522-594), two phases.
+ * Count: per leaf cell the faces of its bin within d_link.  On overflow of
+ * `capacity` returns OW_ERR_CAPACITY with the reference's message naming the
+ * first overflowing (block, bin, cell).  Emit writes the CSR. */
+int ow_cell_face_links_count(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
+                             const float* d_coords, int64_t n_faces, int64_t geom_key, const ow_grid* grid,
+                             const int32_t* d_bin_ids, const int32_t* d_bin_counts,
+                             const int32_t* d_bin_offsets, float d_link, double reach, int64_t capacity,
+                             int64_t* out_cells, int64_t* out_links, void* stream);
+int ow_cell_face_links_emit(ow_ctx* ctx, int64_t* d_block_ids, int64_t* d_cell_indices, int64_t* d_offsets,
+                            int32_t* d_face_ids, void* stream);
+
+/* ---- lattice boundary links (north-star extension) -------------- */
+/* Q directions d_dirs[Q][dim] (int8) of a DnQm lattice; links of every cell of
+ * leaves `d_leaves` (finest level) tested against faces with FP32
+ * Moller-Trumbore (3D) / segment-segment (2D).  Phase 1 writes d_flags
+ * [n_leaves * 4^D] (bit i = link i hits) and returns the boundary-cell count;
+ * phase 2 writes d_cells (flat cell index, ascending) and d_q [nb][Q] = min t
+ * (-1 for no hit). */
+int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
+                           const float* d_coords, int64_t n_faces, int64_t geom_key, const ow_grid* grid,
+                           const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags, int64_t* out_boundary,
+                           void* stream);
+int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, void* stream);
+
+/* ---- predicate probe (parity tests) ---------------------------------------- */
+/* out[i] = near(point i, face i, d[i]) for n independent pairs; points (n, D),
+ * faces (D, D, n) SoA, d float32 (n).  The device predicate used by marking. */
+int ow_near_pairs(ow_ctx* ctx, int32_t dim, const float* d_points, const float* d_faces, const float* d_d,
+                  int64_t n, uint8_t* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OWB200_H */

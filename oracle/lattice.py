@@ -132,7 +132,7 @@ def lattice_links(forest, coords, lattice="D3Q19"):
                 hit, t = mt_hits(cen[cell], dvec, coords[:, :, fac])
             else:
                 hit, t = seg_hits(cen[cell], dvec, coords[:, :, fac])
-            cell, t = cell[hit], t[hit]
+            cell, t = cell[hit], t[hit] + F32(0.0)  # -0 -> +0
             if cell.size == 0:
                 continue
             flags[cell] |= np.uint32(1 << i)

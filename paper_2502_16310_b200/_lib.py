@@ -1,0 +1,191 @@
+"""ctypes binding of libowb200.so (include/owb200.h) and device plumbing.
+
+The library is the product: there is no CPU fallback.  Loading fails loudly
+when the shared object is missing or no CUDA device is present.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import torch
+
+from . import errors
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libowb200.so")
+
+OW_OK, OW_ERR_INTERNAL, OW_ERR_INVALID, OW_ERR_PARSE, OW_ERR_CAPACITY = 0, 1, 2, 3, 4
+
+_EXC = {
+    OW_ERR_INTERNAL: errors.OctowallError,
+    OW_ERR_INVALID: errors.InvalidParameterError,
+    OW_ERR_PARSE: errors.GeometryParseError,
+    OW_ERR_CAPACITY: errors.CapacityError,
+}
+
+
+class Grid(C.Structure):  # ow_grid
+    _fields_ = [
+        ("dim", C.c_int32),
+        ("bins_per_axis", C.c_int32),
+        ("dmin", C.c_double * 3),
+        ("dmax", C.c_double * 3),
+        ("min32", C.c_float * 3),
+        ("len32", C.c_float * 3),
+    ]
+
+
+class ForestView(C.Structure):  # ow_forest (fields appended below: self-referential callback)
+    pass
+
+
+GROW_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(ForestView), C.c_int64)
+
+ForestView._fields_ = [
+    ("dim", C.c_int32),
+    ("max_level", C.c_int32),
+    ("root", C.c_int32 * 3),
+    ("_pad", C.c_int32),
+    ("dmin", C.c_double * 3),
+    ("dext", C.c_double * 3),
+    ("n_blocks", C.c_int64),
+    ("capacity", C.c_int64),
+    ("d_level", C.c_void_p),
+    ("d_coord", C.c_void_p * 3),
+    ("d_parent", C.c_void_p),
+    ("d_first_child", C.c_void_p),
+    ("d_marks", C.c_void_p),
+    ("grow", GROW_FN),
+    ("grow_user", C.c_void_p),
+]
+
+
+class FaceSummary(C.Structure):  # ow_face_summary
+    _fields_ = [
+        ("first_degenerate", C.c_int64),
+        ("first_nonfinite", C.c_int64),
+        ("bbox_min", C.c_float * 3),
+        ("bbox_max", C.c_float * 3),
+        ("abs_max", C.c_float),
+        ("_pad", C.c_float),
+    ]
+
+
+P = C.c_void_p
+I32, I64, F32, F64 = C.c_int32, C.c_int64, C.c_float, C.c_double
+PI64 = C.POINTER(C.c_int64)
+
+# name -> argtypes (restype int unless listed in _RESTYPE)
+_SIGS = {
+    "ow_ctx_create": [C.c_int, C.POINTER(P)],
+    "ow_ctx_destroy": [P],
+    "ow_last_error": [],
+    "ow_version": [],
+    "ow_launch_count": [P],
+    "ow_profile": [P, C.c_int],
+    "ow_profile_read": [P, C.c_int, C.POINTER(C.c_double), PI64],
+    "ow_stl_binary_to_soa": [P, P, I64, P, P],
+    "ow_index_to_coords": [P, I32, P, P, I64, P, P],
+    "ow_face_check": [P, I32, P, I64, C.POINTER(FaceSummary), P],
+    "ow_fill_bins_count": [P, C.POINTER(Grid), P, I64, F32, P, PI64, PI64, P],
+    "ow_fill_bins_emit": [P, C.POINTER(Grid), P, P, P, P],
+    "ow_forest_leaves": [P, C.POINTER(ForestView), I32, P, PI64, P],
+    "ow_forest_level_counts": [P, C.POINTER(ForestView), PI64, PI64, I32, P],
+    "ow_forest_count_marks": [P, C.POINTER(ForestView), I32, I32, I32, PI64, P],
+    "ow_forest_cell_centers": [P, C.POINTER(ForestView), P, I64, P, P],
+    "ow_refine_marked": [P, C.POINTER(ForestView), I32, PI64, P],
+    "ow_mark_near_wall": [P, C.POINTER(ForestView), P, I64, P, I64, I64, C.POINTER(Grid), P, P, P, F32, F64,
+                          PI64, PI64, PI64, P],
+    "ow_propagate_marks": [P, C.POINTER(ForestView), P, I64, I32, P],
+    "ow_cell_face_links_count": [P, C.POINTER(ForestView), P, I64, P, I64, I64, C.POINTER(Grid), P, P, P, F32, F64,
+                                 I64, PI64, PI64, P],
+    "ow_cell_face_links_emit": [P, P, P, P, P, P],
+    "ow_lattice_links_count": [P, C.POINTER(ForestView), P, I64, P, I64, I64, C.POINTER(Grid), P, I32, P, PI64, P],
+    "ow_lattice_links_emit": [P, P, P, P],
+    "ow_near_pairs": [P, I32, P, P, P, I64, P, P],
+}
+_RESTYPE = {"ow_last_error": C.c_char_p, "ow_version": C.c_int, "ow_launch_count": C.c_int64}
+
+_lib = None
+_ctx = {}
+_lock = threading.Lock()
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise errors.OctowallError(
+                        f"{LIB_PATH} is missing: build it with paper_2502_16310_b200._build.build() "
+                        "(there is no CPU fallback)")
+                L = C.CDLL(LIB_PATH)
+                for name, argt in _SIGS.items():
+                    fn = getattr(L, name)
+                    fn.argtypes = argt
+                    fn.restype = _RESTYPE.get(name, C.c_int)
+                _lib = L
+    return _lib
+
+
+def device():
+    if not torch.cuda.is_available():
+        raise errors.OctowallError("paper_2502_16310_b200 needs a CUDA device (B200, sm_100a); none is visible")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def ctx():
+    """Per-device ow_ctx (created lazily)."""
+    dev = device()
+    key = dev.index
+    if key not in _ctx:
+        p = P()
+        check(lib().ow_ctx_create(key, C.byref(p)))
+        _ctx[key] = p
+    return _ctx[key]
+
+
+def stream():
+    return P(torch.cuda.current_stream().cuda_stream)
+
+
+def check(status, exc_map=None):
+    if status == OW_OK:
+        return
+    msg = lib().ow_last_error().decode("utf-8", "replace")
+    cls = (exc_map or {}).get(status) or _EXC.get(status, errors.OctowallError)
+    raise cls(msg)
+
+
+def call(name, *args, exc_map=None):
+    check(getattr(lib(), name)(*args), exc_map)
+
+
+def ptr(t):
+    return P(t.data_ptr()) if t is not None else P()
+
+
+def launches():
+    """Kernels launched by this process's contexts so far (bench instrumentation)."""
+    return sum(int(lib().ow_launch_count(c)) for c in _ctx.values())
+
+
+PROF_IDS = {"mark": 0, "lattice": 1, "fill_bins": 2, "refine": 3, "propagate": 4, "links": 5, "stl": 6, "prep": 7}
+
+
+def profile(enable=True):
+    call("ow_profile", ctx(), int(bool(enable)))
+
+
+def profile_read():
+    """{family: (total_ms, launches)} of the CUDA-event brackets since profile()."""
+    out = {}
+    for name, i in PROF_IDS.items():
+        ms, n = C.c_double(0.0), C.c_int64(0)
+        call("ow_profile_read", ctx(), i, C.byref(ms), C.byref(n))
+        out[name] = (float(ms.value), int(n.value))
+    return out

@@ -1,0 +1,293 @@
+// Shared host/device infrastructure for libowb200: context, errors, scratch
+// slots, launch accounting, and the exact float32/float64 arithmetic helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/owb200.h"
+
+#define OW_SMS 148  // B200 SM count: persistent grids are sized in multiples of it
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+void ow_set_error(const char* fmt, ...);
+
+#define OW_CUDA(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t _e = (call);                                                                   \
+    if (_e != cudaSuccess) {                                                                   \
+      ow_set_error("CUDA error %s at %s:%d", cudaGetErrorString(_e), __FILE__, __LINE__);       \
+      return OW_ERR_INTERNAL;                                                                  \
+    }                                                                                          \
+  } while (0)
+
+#define OW_TRY(call)              \
+  do {                            \
+    int _s = (call);              \
+    if (_s != OW_OK) return _s;   \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// context: persistent scratch slots (stream-ordered growth) + pinned readback
+// ---------------------------------------------------------------------------
+enum ow_slot {
+  SLOT_SCAN_STATUS = 0,
+  SLOT_SCAN_AUX,
+  SLOT_FACE_PREP,      // predicate payload cache
+  SLOT_FACE_BOX,       // float32 face boxes (lo[D], hi[D])
+  SLOT_FACE_SPHERE,    // float4 bounding spheres (reach dependent)
+  SLOT_BIN_MASK,       // per-face bin bitmask (fill_bins)
+  SLOT_BIN_NB,         // per-face distinct-bin count
+  SLOT_BIN_FOFF,       // per-face pair offset
+  SLOT_BIN_SLOW,       // slow-path face list
+  SLOT_BIN_SLOWOFF,    // slow-path bitmap offsets
+  SLOT_BIN_BITMAP,     // slow-path bitmaps
+  SLOT_PAIR_KEY0,      // radix sort ping-pong
+  SLOT_PAIR_VAL0,
+  SLOT_PAIR_KEY1,
+  SLOT_PAIR_VAL1,
+  SLOT_RADIX_HIST,
+  SLOT_FOREST_LIST,    // split / violator lists
+  SLOT_FOREST_FLAG,    // violator flags
+  SLOT_LINK_CNT,       // per-cell link counts
+  SLOT_LINK_OFF,
+  SLOT_LINK_CELLOFF,
+  SLOT_LINK_LEAVES,
+  SLOT_LAT_BCOUNT,
+  SLOT_LAT_BOFF,
+  SLOT_LAT_LEAVES,
+  SLOT_LAT_FLAGS,
+  SLOT_ABIN_IDS,       // AABB-overlap bin CSR (lattice candidates)
+  SLOT_ABIN_CNT,
+  SLOT_ABIN_OFF,
+  SLOT_MISC,
+  SLOT_COUNT
+};
+
+// optional per-kernel CUDA-event timing (bench.py roofline instrumentation)
+enum { PROF_MARK = 0, PROF_LATTICE, PROF_BINS, PROF_REFINE, PROF_PROP, PROF_LINKS, PROF_STL, PROF_PREP, PROF_N };
+#define PROF_MAX 256
+struct ow_prof {
+  int enabled;
+  int n[PROF_N];
+  cudaEvent_t ev[PROF_N][PROF_MAX][2];
+};
+
+struct ow_ctx {
+  int device;
+  ow_prof* prof;
+  void* slot_ptr[SLOT_COUNT];
+  size_t slot_bytes[SLOT_COUNT];
+  int64_t* h_pinned;  // 64 int64 of pinned host memory for readbacks
+  int64_t* d_small;   // 64 int64 of device scalars (counters, flags)
+  int64_t launches;
+  // face prep cache key
+  int64_t prep_key;
+  float prep_d;
+  double prep_reach;
+  int64_t prep_faces;
+  int32_t prep_dim;
+  // fill_bins phase state
+  int64_t bins_faces, bins_entries, bins_slow;
+  int32_t bins_dim, bins_B;
+  float bins_h;
+  const float* bins_coords;
+  // cell-face link phase state
+  int64_t link_cells, link_total, link_leaves;
+  int32_t link_dim, link_nbins;
+  const float* link_coords;
+  const int32_t *link_bin_ids, *link_bin_counts, *link_bin_offsets;
+  const int32_t* link_leaves_ptr;
+  int64_t link_key, link_faces;
+  float link_d;
+  double link_reach;
+  ow_forest link_forest;
+  ow_grid link_grid;
+  // lattice phase state
+  int64_t lat_leaves, lat_boundary, lat_faces;
+  int32_t lat_dirs;
+  int8_t lat_dir[27 * 3];
+  const float* lat_coords;
+  const int32_t* lat_leaves_ptr;
+  int64_t lat_key;
+  ow_forest lat_forest;
+  ow_grid lat_grid;
+  int64_t abin_key;
+  int32_t abin_B, abin_dim;
+};
+
+// Scratch slot of at least `bytes`; contents are preserved across calls unless
+// the slot grows (then it is reallocated, stream-ordered, uninitialised).
+int ow_slot(ow_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out);
+
+// Copy n int64 device values to host and synchronise.
+int ow_readback(ow_ctx* ctx, const int64_t* d_src, int n, int64_t* h_dst, cudaStream_t s);
+
+// bracket device work of kernel family `id` with events when profiling is on
+void ow_prof_mark(ow_ctx* ctx, int id, int end, cudaStream_t s);
+#define OW_PROF_BEGIN(ctx, id, s) \
+  do {                            \
+    if ((ctx)->prof && (ctx)->prof->enabled) ow_prof_mark(ctx, id, 0, s); \
+  } while (0)
+#define OW_PROF_END(ctx, id, s) \
+  do {                          \
+    if ((ctx)->prof && (ctx)->prof->enabled) ow_prof_mark(ctx, id, 1, s); \
+  } while (0)
+
+#define OW_LAUNCHED(ctx) ((ctx)->launches++)
+#define OW_CHECK_LAUNCH()                                                                        \
+  do {                                                                                           \
+    cudaError_t _e = cudaGetLastError();                                                         \
+    if (_e != cudaSuccess) {                                                                     \
+      ow_set_error("kernel launch failed: %s at %s:%d", cudaGetErrorString(_e), __FILE__, __LINE__); \
+      return OW_ERR_INTERNAL;                                                                    \
+    }                                                                                            \
+  } while (0)
+
+static inline int ow_blocks(int64_t n, int threads, int64_t cap = 1 << 30) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (int)b;
+}
+
+// ---------------------------------------------------------------------------
+// exact arithmetic: explicit round-to-nearest intrinsics never contract to FMA
+// ---------------------------------------------------------------------------
+#define FADD(a, b) __fadd_rn((a), (b))
+#define FSUB(a, b) __fsub_rn((a), (b))
+#define FMUL(a, b) __fmul_rn((a), (b))
+#define FDIV(a, b) __fdiv_rn((a), (b))
+#define FSQRT(a) __fsqrt_rn(a)
+#define DADD(a, b) __dadd_rn((a), (b))
+#define DSUB(a, b) __dsub_rn((a), (b))
+#define DMUL(a, b) __dmul_rn((a), (b))
+#define DDIV(a, b) __ddiv_rn((a), (b))
+
+// ((a0*b0 + a1*b1) + a2*b2) in float32, left to right
+__device__ __forceinline__ float dot3f(float a0, float a1, float a2, float b0, float b1, float b2) {
+  return FADD(FADD(FMUL(a0, b0), FMUL(a1, b1)), FMUL(a2, b2));
+}
+
+// ---------------------------------------------------------------------------
+// grid constants on device
+// ---------------------------------------------------------------------------
+struct GridC {
+  int dim, B;
+  float min32[3], len32[3];
+  double lo_tol[3], hi_tol[3];  // domain +- 1e-6 * extent (binning.py:71-77)
+};
+
+static inline GridC make_gridc(const ow_grid* g) {
+  GridC c;
+  c.dim = g->dim;
+  c.B = g->bins_per_axis;
+  for (int a = 0; a < 3; ++a) {
+    c.min32[a] = g->min32[a];
+    c.len32[a] = g->len32[a];
+    double ext = g->dmax[a] - g->dmin[a];
+    double tol = 1e-6 * ext;
+    c.lo_tol[a] = g->dmin[a] - tol;
+    c.hi_tol[a] = g->dmax[a] + tol;
+  }
+  return c;
+}
+
+// floor((p - min32) / len32) -> int64 -> clip [0, B-1]  (binning.py:78-79)
+__device__ __forceinline__ int bin_axis(float p, float mn, float ln, int B) {
+  float f = floorf(FDIV(FSUB(p, mn), ln));
+  if (!(f >= 0.0f)) return 0;  // negative (NaN impossible for finite input)
+  if (f >= (float)(B - 1)) return B - 1;
+  return (int)f;
+}
+
+__device__ __forceinline__ bool outside_domain(const GridC& g, const float* p) {
+  for (int a = 0; a < g.dim; ++a) {
+    double v = (double)p[a];
+    if (v < g.lo_tol[a] || v > g.hi_tol[a]) return true;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------------------
+// forest device view + helpers
+// ---------------------------------------------------------------------------
+struct ForestC {
+  int dim, max_level;
+  int root[3];
+  double dmin[3], dext[3];
+  int64_t n;
+  const int16_t* level;
+  const int32_t* coord[3];
+  const int32_t* parent;
+  const int32_t* first_child;
+  int8_t* marks;
+};
+
+static inline ForestC make_forestc(const ow_forest* f) {
+  ForestC c;
+  c.dim = f->dim;
+  c.max_level = f->max_level;
+  for (int a = 0; a < 3; ++a) {
+    c.root[a] = f->root[a];
+    c.dmin[a] = f->dmin[a];
+    c.dext[a] = f->dext[a];
+    c.coord[a] = f->d_coord[a];
+  }
+  c.n = f->n_blocks;
+  c.level = f->d_level;
+  c.parent = f->d_parent;
+  c.first_child = f->d_first_child;
+  c.marks = f->d_marks;
+  return c;
+}
+
+// block edge per axis: extent / (root * 2^level)   (forest.py:152-161)
+__device__ __forceinline__ double block_len(const ForestC& F, int ax, int level) {
+  return DDIV(F.dext[ax], (double)((int64_t)F.root[ax] << level));
+}
+
+// Deepest existing block on the path from the root lattice to lattice cell
+// (level, nc): the block itself if it exists, else the coarser leaf covering
+// it.  Replaces the (level, coords) dictionary walk of forest.py:246-261.
+__device__ __forceinline__ int locate(const ForestC& F, int level, const int32_t* nc, int* out_depth) {
+  int node = 0, stride = 1;
+  for (int a = 0; a < F.dim; ++a) {
+    node += (nc[a] >> level) * stride;
+    stride *= F.root[a];
+  }
+  int depth = 0;
+  while (depth < level) {
+    int fc = F.first_child[node];
+    if (fc < 0) break;
+    int sh = level - 1 - depth, ci = 0;
+    for (int a = 0; a < F.dim; ++a) ci |= ((nc[a] >> sh) & 1) << a;
+    node = fc + ci;
+    ++depth;
+  }
+  *out_depth = depth;
+  return node;
+}
+
+// Lattice neighbour of block (level, c) across side s = 2*axis + (step>0);
+// returns false at the domain boundary.
+__device__ __forceinline__ bool side_target(const ForestC& F, int level, const int32_t* c, int s,
+                                            int32_t* nc) {
+  int ax = s >> 1, step = (s & 1) ? 1 : -1;
+  for (int a = 0; a < 3; ++a) nc[a] = (a < F.dim) ? c[a] : 0;
+  nc[ax] += step;
+  int64_t dimax = (int64_t)F.root[ax] << level;
+  return nc[ax] >= 0 && nc[ax] < dimax;
+}
+
+// ---------------------------------------------------------------------------
+// warp helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}

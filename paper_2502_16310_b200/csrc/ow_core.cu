@@ -1,0 +1,116 @@
+// Context, error state, scratch slots and readback for libowb200.
+#include <stdarg.h>
+#include <string.h>
+
+#include "ow_common.cuh"
+
+static thread_local char g_err[1024] = "";
+
+void ow_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+extern "C" const char* ow_last_error(void) { return g_err; }
+
+extern "C" int ow_version(void) { return 10000; }  // 1.0.0
+
+extern "C" int64_t ow_launch_count(ow_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+extern "C" int ow_ctx_create(int device, ow_ctx** out) {
+  if (!out) {
+    ow_set_error("ow_ctx_create: null out pointer");
+    return OW_ERR_INVALID;
+  }
+  OW_CUDA(cudaSetDevice(device));
+  ow_ctx* c = (ow_ctx*)calloc(1, sizeof(ow_ctx));
+  if (!c) {
+    ow_set_error("ow_ctx_create: out of host memory");
+    return OW_ERR_INTERNAL;
+  }
+  c->device = device;
+  c->prep_key = -1;
+  c->abin_key = -1;
+  cudaError_t e = cudaMallocHost((void**)&c->h_pinned, 64 * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&c->d_small, 64 * sizeof(int64_t));
+  if (e != cudaSuccess) {
+    ow_set_error("ow_ctx_create: %s", cudaGetErrorString(e));
+    free(c);
+    return OW_ERR_INTERNAL;
+  }
+  *out = c;
+  return OW_OK;
+}
+
+extern "C" int ow_ctx_destroy(ow_ctx* c) {
+  if (!c) return OW_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int i = 0; i < SLOT_COUNT; ++i)
+    if (c->slot_ptr[i]) cudaFree(c->slot_ptr[i]);
+  cudaFreeHost(c->h_pinned);
+  cudaFree(c->d_small);
+  free(c);
+  return OW_OK;
+}
+
+int ow_slot(ow_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out) {
+  if (bytes == 0) bytes = 16;
+  if (ctx->slot_bytes[slot] < bytes) {
+    size_t want = bytes + bytes / 4 + 256;
+    if (ctx->slot_ptr[slot]) OW_CUDA(cudaFreeAsync(ctx->slot_ptr[slot], s));
+    ctx->slot_ptr[slot] = nullptr;
+    ctx->slot_bytes[slot] = 0;
+    OW_CUDA(cudaMallocAsync(&ctx->slot_ptr[slot], want, s));
+    ctx->slot_bytes[slot] = want;
+  }
+  *out = ctx->slot_ptr[slot];
+  return OW_OK;
+}
+
+void ow_prof_mark(ow_ctx* ctx, int id, int end, cudaStream_t s) {
+  ow_prof* p = ctx->prof;
+  int k = p->n[id];
+  if (k >= PROF_MAX) return;
+  cudaEvent_t* e = &p->ev[id][k][end];
+  if (!*e) cudaEventCreate(e);
+  cudaEventRecord(*e, s);
+  if (end) p->n[id] = k + 1;
+}
+
+extern "C" int ow_profile(ow_ctx* ctx, int enable) {
+  if (!ctx->prof) {
+    ctx->prof = (ow_prof*)calloc(1, sizeof(ow_prof));
+    if (!ctx->prof) {
+      ow_set_error("ow_profile: out of host memory");
+      return OW_ERR_INTERNAL;
+    }
+  }
+  ctx->prof->enabled = enable;
+  for (int i = 0; i < PROF_N; ++i) ctx->prof->n[i] = 0;
+  return OW_OK;
+}
+
+extern "C" int ow_profile_read(ow_ctx* ctx, int id, double* total_ms, int64_t* launches) {
+  *total_ms = 0.0;
+  *launches = 0;
+  if (!ctx->prof || id < 0 || id >= PROF_N) return OW_OK;
+  ow_prof* p = ctx->prof;
+  for (int k = 0; k < p->n[id]; ++k) {
+    OW_CUDA(cudaEventSynchronize(p->ev[id][k][1]));
+    float ms = 0.0f;
+    OW_CUDA(cudaEventElapsedTime(&ms, p->ev[id][k][0], p->ev[id][k][1]));
+    *total_ms += ms;
+  }
+  *launches = p->n[id];
+  return OW_OK;
+}
+
+int ow_readback(ow_ctx* ctx, const int64_t* d_src, int n, int64_t* h_dst, cudaStream_t s) {
+  OW_CUDA(cudaMemcpyAsync(ctx->h_pinned, d_src, n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  OW_CUDA(cudaStreamSynchronize(s));
+  memcpy(h_dst, ctx->h_pinned, n * sizeof(int64_t));
+  return OW_OK;
+}

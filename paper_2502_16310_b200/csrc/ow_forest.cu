@@ -1,0 +1,319 @@
+// Forest-of-octrees kernels: leaf listing, level histograms, cell centres,
+// mark propagation, refinement with deterministic allocation and 2:1 balance.
+//
+// Reference: octowall/forest.py:143-205 (queries, cell centres), 224-285
+// (face neighbours), 300-370 (split / refine_marked / _rebalance);
+// octowall/nearwall.py:321-366 (propagate_marks).
+//
+// The reference resolves neighbours through a (level, coords) -> id dict; here
+// a neighbour is found by descending from the root lattice with the child
+// bits of its lattice coordinates (`locate`), which needs no hash table and
+// touches <= level+1 first_child words per query.
+#include "ow_scan.cuh"
+
+namespace {
+
+using ow::scan;
+
+__global__ void k_cell_centers(ForestC F, const int32_t* __restrict__ ids, int64_t n, float* out) {
+  const int C = F.dim == 2 ? 16 : 64;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * C) return;
+  int64_t i = t / C;
+  int c = (int)(t % C);
+  int id = ids[i];
+  int L = F.level[id];
+  for (int a = 0; a < F.dim; ++a) {
+    double q = block_len(F, a, L);
+    double o = DADD(F.dmin[a], DMUL((double)F.coord[a][id], q));
+    int digit = (c >> (2 * a)) & 3;
+    double u = ((double)digit + 0.5) / 4.0;  // exact
+    out[t * F.dim + a] = __double2float_rn(DADD(o, DMUL(u, q)));
+  }
+}
+
+__global__ void k_level_counts(ForestC F, int max_levels, unsigned long long* blocks, unsigned long long* leaves) {
+  __shared__ unsigned long long sb[64], sl[64];
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) sb[i] = sl[i] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < F.n; i += (int64_t)gridDim.x * blockDim.x) {
+    int L = F.level[i];
+    if (L < max_levels) {
+      atomicAdd(&sb[L], 1ull);
+      if (F.first_child[i] < 0) atomicAdd(&sl[L], 1ull);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < max_levels; i += blockDim.x) {
+    if (sb[i]) atomicAdd(&blocks[i], sb[i]);
+    if (sl[i]) atomicAdd(&leaves[i], sl[i]);
+  }
+}
+
+struct LeafLoad {
+  const int16_t* level;
+  const int32_t* fc;
+  int L;
+  __device__ int64_t operator()(int64_t i) const { return level[i] == L && fc[i] < 0; }
+};
+struct CompactStore {
+  int32_t* out;
+  __device__ void operator()(int64_t i, int64_t e, int64_t v) const {
+    if (v) out[e] = (int32_t)i;
+  }
+};
+
+struct MarkCountLoad {
+  ForestC F;
+  int L, leaf_only, mark;
+  __device__ int64_t operator()(int64_t i) const {
+    return F.level[i] == L && (!leaf_only || F.first_child[i] < 0) && F.marks[i] == mark;
+  }
+};
+struct NullStore {
+  __device__ void operator()(int64_t, int64_t, int64_t) const {}
+};
+
+// MARKED leaves at L (flag 1) + INTERMEDIATE anywhere at L (side flag)
+struct SplitLoad {
+  ForestC F;
+  int L;
+  int64_t* inter_flag;
+  __device__ int64_t operator()(int64_t i) const {
+    if (F.level[i] != L) return 0;
+    int8_t m = F.marks[i];
+    if (m == OW_INTERMEDIATE) atomicExch((unsigned long long*)inter_flag, 1ull);
+    return F.first_child[i] < 0 && m == OW_MARKED;
+  }
+};
+
+struct FlagLoad {
+  const uint8_t* flag;
+  __device__ int64_t operator()(int64_t i) const { return flag[i] != 0; }
+};
+
+// Split list[0..m) (ascending ids): children ids base + 2^D * r + ci with
+// coords 2c + bits(ci); parent mark reset (forest.py:300-329).
+__global__ void k_split(ow_forest f, const int32_t* __restrict__ list, int64_t m, int64_t base) {
+  const int nc = 1 << f.dim;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * nc) return;
+  int64_t r = t / nc;
+  int ci = (int)(t % nc);
+  int p = list[r];
+  int64_t id = base + t;
+  f.d_level[id] = (int16_t)(f.d_level[p] + 1);
+  for (int a = 0; a < f.dim; ++a) f.d_coord[a][id] = 2 * f.d_coord[a][p] + ((ci >> a) & 1);
+  f.d_parent[id] = p;
+  f.d_first_child[id] = -1;
+  f.d_marks[id] = OW_NONE;
+  if (ci == 0) {
+    f.d_first_child[p] = (int32_t)(base + r * nc);
+    f.d_marks[p] = OW_NONE;
+  }
+}
+
+// 2:1 violators among the face-adjacent leaves of frontier blocks
+// [f0, f1): a coarser leaf more than one level above (forest.py:351-370).
+__global__ void k_violators(ForestC F, int64_t f0, int64_t f1, uint8_t* flag) {
+  const int sides = 2 * F.dim;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (f1 - f0) * sides) return;
+  int64_t id = f0 + t / sides;
+  int s = (int)(t % sides);
+  int lv = F.level[id];
+  int32_t c[3] = {F.coord[0][id], F.dim > 1 ? F.coord[1][id] : 0, F.dim > 2 ? F.coord[2][id] : 0};
+  int32_t nc[3];
+  if (!side_target(F, lv, c, s, nc)) return;
+  int depth;
+  int node = locate(F, lv, nc, &depth);
+  if (F.first_child[node] < 0 && depth < lv - 1) flag[node] = 1;
+}
+
+// any MARKED leaf on the face of region (L, nc) facing the query block
+__device__ bool side_has_marked(const ForestC& F, int L, const int32_t* nc, int s) {
+  int depth;
+  int node = locate(F, L, nc, &depth);
+  if (F.first_child[node] < 0) return F.marks[node] == OW_MARKED;
+  const int ax = s >> 1;
+  const int want = (s & 1) ? 0 : 1;  // neighbour on + side: its children on the min face
+  int stack[64];
+  int sp = 0;
+  stack[sp++] = node;
+  while (sp) {
+    int b = stack[--sp];
+    int fc = F.first_child[b];
+    if (fc < 0) {
+      if (F.marks[b] == OW_MARKED) return true;
+      continue;
+    }
+    for (int ci = (1 << F.dim) - 1; ci >= 0; --ci)
+      if (((ci >> ax) & 1) == want && sp < 64) stack[sp++] = fc + ci;
+  }
+  return false;
+}
+
+__global__ void k_prop_gather(ForestC F, const int32_t* __restrict__ leaves, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int id = leaves[i];
+  if (F.marks[id] != OW_NONE) return;
+  int L = F.level[id];
+  int32_t c[3] = {F.coord[0][id], F.dim > 1 ? F.coord[1][id] : 0, F.dim > 2 ? F.coord[2][id] : 0};
+  for (int s = 0; s < 2 * F.dim; ++s) {
+    int32_t nc[3];
+    if (!side_target(F, L, c, s, nc)) continue;
+    if (side_has_marked(F, L, nc, s)) {
+      F.marks[id] = OW_INTERMEDIATE;
+      return;
+    }
+  }
+}
+
+__global__ void k_prop_promote(int8_t* marks, const int32_t* __restrict__ leaves, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int id = leaves[i];
+  if (marks[id] == OW_INTERMEDIATE) marks[id] = OW_MARKED;
+}
+
+int split_list(ow_ctx* ctx, ow_forest* f, const int32_t* list, int64_t m, cudaStream_t s) {
+  const int nc = 1 << f->dim;
+  int64_t need = f->n_blocks + (int64_t)nc * m;
+  if (need > (int64_t)INT32_MAX) {
+    ow_set_error("forest exceeds 2^31 blocks");
+    return OW_ERR_CAPACITY;
+  }
+  if (need > f->capacity) {
+    if (!f->grow) {
+      ow_set_error("forest capacity %lld < %lld and no grow callback", (long long)f->capacity, (long long)need);
+      return OW_ERR_CAPACITY;
+    }
+    if (f->grow(f->grow_user, f, need) != 0 || f->capacity < need) {
+      ow_set_error("forest grow callback failed (need %lld blocks)", (long long)need);
+      return OW_ERR_INTERNAL;
+    }
+  }
+  k_split<<<ow_blocks(m * nc, 256), 256, 0, s>>>(*f, list, m, f->n_blocks);
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  f->n_blocks = need;
+  return OW_OK;
+}
+
+}  // namespace
+
+extern "C" int ow_forest_leaves(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t* d_out, int64_t* out_n,
+                                void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  OW_TRY(scan(ctx, LeafLoad{f->d_level, f->d_first_child, level}, CompactStore{d_out}, f->n_blocks,
+              ctx->d_small + 8, s));
+  return ow_readback(ctx, ctx->d_small + 8, 1, out_n, s);
+}
+
+extern "C" int ow_forest_level_counts(ow_ctx* ctx, const ow_forest* f, int64_t* out_blocks, int64_t* out_leaves,
+                                      int32_t max_levels, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (max_levels > 28) max_levels = 28;
+  OW_CUDA(cudaMemsetAsync(ctx->d_small, 0, 64 * 8, s));
+  ForestC F = make_forestc(f);
+  k_level_counts<<<ow_blocks(F.n, 256, 2 * OW_SMS), 256, 0, s>>>(F, max_levels, (unsigned long long*)ctx->d_small,
+                                                                 (unsigned long long*)ctx->d_small + 32);
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  int64_t h[64];
+  OW_TRY(ow_readback(ctx, ctx->d_small, 64, h, s));
+  for (int i = 0; i < max_levels; ++i) {
+    out_blocks[i] = h[i];
+    out_leaves[i] = h[32 + i];
+  }
+  return OW_OK;
+}
+
+extern "C" int ow_forest_count_marks(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t leaf_only,
+                                     int32_t mark, int64_t* out_n, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  OW_TRY(scan(ctx, MarkCountLoad{make_forestc(f), level, leaf_only, mark}, NullStore{}, f->n_blocks,
+              ctx->d_small + 8, s));
+  return ow_readback(ctx, ctx->d_small + 8, 1, out_n, s);
+}
+
+extern "C" int ow_forest_cell_centers(ow_ctx* ctx, const ow_forest* f, const int32_t* d_ids, int64_t n,
+                                      float* d_out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n <= 0) return OW_OK;
+  const int C = f->dim == 2 ? 16 : 64;
+  k_cell_centers<<<ow_blocks(n * C, 256), 256, 0, s>>>(make_forestc(f), d_ids, n, d_out);
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  return OW_OK;
+}
+
+extern "C" int ow_propagate_marks(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
+                                  int32_t rounds, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n_leaves <= 0 || rounds <= 0) return OW_OK;
+  ForestC F = make_forestc(f);
+  OW_PROF_BEGIN(ctx, PROF_PROP, s);
+  for (int r = 0; r < rounds; ++r) {
+    k_prop_gather<<<ow_blocks(n_leaves, 128), 128, 0, s>>>(F, d_leaves, n_leaves);
+    k_prop_promote<<<ow_blocks(n_leaves, 256), 256, 0, s>>>(F.marks, d_leaves, n_leaves);
+    ctx->launches += 2;
+  }
+  OW_PROF_END(ctx, PROF_PROP, s);
+  OW_CHECK_LAUNCH();
+  return OW_OK;
+}
+
+static int refine_marked_impl(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, cudaStream_t s);
+
+extern "C" int ow_refine_marked(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  OW_PROF_BEGIN(ctx, PROF_REFINE, s);
+  int st = refine_marked_impl(ctx, f, level, out_split, s);
+  OW_PROF_END(ctx, PROF_REFINE, s);
+  return st;
+}
+
+static int refine_marked_impl(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, cudaStream_t s) {
+  int64_t* small = ctx->d_small;
+  void* pl;
+  OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(f->n_blocks + 1), s, &pl));
+  OW_CUDA(cudaMemsetAsync(small + 9, 0, 8, s));
+  OW_TRY(scan(ctx, SplitLoad{make_forestc(f), level, small + 9}, CompactStore{(int32_t*)pl}, f->n_blocks, small + 8, s));
+  int64_t h[2];
+  OW_TRY(ow_readback(ctx, small + 8, 2, h, s));
+  if (h[1]) {
+    ow_set_error("level %d still carries intermediate marks; finish propagation first", level);
+    return OW_ERR_INVALID;
+  }
+  int64_t m = h[0], n_split = m;
+  *out_split = 0;
+  if (m == 0) return OW_OK;
+  if (level >= f->max_level) {
+    ow_set_error("refinement beyond max level %d", f->max_level);
+    return OW_ERR_INVALID;
+  }
+  int64_t f0 = f->n_blocks;
+  OW_TRY(split_list(ctx, f, (const int32_t*)pl, m, s));
+  while (f->n_blocks > f0) {
+    int64_t f1 = f->n_blocks;
+    void* pf;
+    OW_TRY(ow_slot(ctx, SLOT_FOREST_FLAG, (size_t)f->capacity, s, &pf));
+    OW_CUDA(cudaMemsetAsync(pf, 0, (size_t)f1, s));
+    ForestC F = make_forestc(f);
+    k_violators<<<ow_blocks((f1 - f0) * 2 * f->dim, 256), 256, 0, s>>>(F, f0, f1, (uint8_t*)pf);
+    OW_LAUNCHED(ctx);
+    OW_CHECK_LAUNCH();
+    OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(f1 + 1), s, &pl));
+    OW_TRY(scan(ctx, FlagLoad{(const uint8_t*)pf}, CompactStore{(int32_t*)pl}, f1, small + 8, s));
+    OW_TRY(ow_readback(ctx, small + 8, 1, h, s));
+    int64_t v = h[0];
+    if (v == 0) break;
+    n_split += v;
+    f0 = f1;
+    OW_TRY(split_list(ctx, f, (const int32_t*)pl, v, s));
+  }
+  *out_split = n_split;
+  return OW_OK;
+}

@@ -1,0 +1,190 @@
+// Geometry import kernels: binary STL records -> SoA, index->coords gather,
+// degenerate-face / bounding-box / non-finite reduction.
+// Reference: octowall/geometry.py:262-308 (index_to_coords, validate_faces,
+// bounding_box) and 415-436 (_parse_binary_stl, _tris_to_geometry).
+#include "ow_common.cuh"
+
+namespace {
+
+constexpr int STL_TILE = 256;  // faces per CTA
+
+// 50-byte records are only 2-byte aligned: stage the tile's bytes through
+// shared memory with coalesced 16-bit loads, then emit 9 coalesced float planes.
+__global__ void __launch_bounds__(STL_TILE)
+k_stl_to_soa(const uint16_t* rec16, int64_t n, float* coords) {
+  __shared__ uint16_t s[STL_TILE * 25];
+  const int64_t f0 = (int64_t)blockIdx.x * STL_TILE;
+  const int64_t nf = min((int64_t)STL_TILE, n - f0);
+  const uint16_t* src = rec16 + f0 * 25;
+  for (int i = threadIdx.x; i < nf * 25; i += STL_TILE) s[i] = src[i];
+  __syncthreads();
+  if (threadIdx.x < nf) {
+    const uint16_t* r = s + threadIdx.x * 25 + 6;  // skip the 12-byte normal
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      uint32_t bits = (uint32_t)r[2 * j] | ((uint32_t)r[2 * j + 1] << 16);
+      coords[(int64_t)j * n + f0 + threadIdx.x] = __uint_as_float(bits);
+    }
+  }
+}
+
+__global__ void k_index_to_coords(int dim, const float* __restrict__ verts, const int32_t* __restrict__ faces,
+                                  int64_t n, float* coords) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  for (int j = 0; j < dim; ++j) {
+    int64_t v = faces[k * dim + j];
+    for (int c = 0; c < dim; ++c) coords[((int64_t)j * dim + c) * n + k] = verts[v * dim + c];
+  }
+}
+
+__device__ __forceinline__ void atomic_min_f(float* a, float v) {
+  if (__float_as_uint(v) >> 31) atomicMax((unsigned*)a, __float_as_uint(v));
+  else atomicMin((int*)a, __float_as_int(v));
+}
+__device__ __forceinline__ void atomic_max_f(float* a, float v) {
+  if (__float_as_uint(v) >> 31) atomicMin((unsigned*)a, __float_as_uint(v));
+  else atomicMax((int*)a, __float_as_int(v));
+}
+
+// small[0] first degenerate (u64 min), small[1] first non-finite (u64 min),
+// then floats: min[3], max[3], absmax at ((float*)(small+2))[0..6]
+__global__ void __launch_bounds__(256) k_face_check(int dim, const float* __restrict__ c, int64_t n, int64_t* small) {
+  float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY}, am = 0.0f;
+  unsigned long long bad_deg = ~0ull, bad_fin = ~0ull;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    float v[3][3];
+    bool finite = true;
+    for (int j = 0; j < dim; ++j)
+      for (int a = 0; a < dim; ++a) {
+        float x = c[((int64_t)j * dim + a) * n + k];
+        v[j][a] = x;
+        finite &= isfinite(x);
+        mn[a] = fminf(mn[a], x);
+        mx[a] = fmaxf(mx[a], x);
+        am = fmaxf(am, fabsf(x));
+      }
+    if (!finite) {
+      bad_fin = min(bad_fin, (unsigned long long)k);
+      continue;
+    }
+    bool deg;
+    if (dim == 2) {  // geometry.py:281-285
+      double dx = DSUB((double)v[1][0], (double)v[0][0]), dy = DSUB((double)v[1][1], (double)v[0][1]);
+      deg = DADD(DMUL(dx, dx), DMUL(dy, dy)) == 0.0;
+    } else {  // geometry.py:287-297, FP64
+      double u[3], w[3], z[3];
+      for (int a = 0; a < 3; ++a) {
+        u[a] = DSUB((double)v[1][a], (double)v[0][a]);
+        w[a] = DSUB((double)v[2][a], (double)v[0][a]);
+        z[a] = DSUB((double)v[2][a], (double)v[1][a]);
+      }
+      double su = DADD(DADD(DMUL(u[0], u[0]), DMUL(u[1], u[1])), DMUL(u[2], u[2]));
+      double sw = DADD(DADD(DMUL(w[0], w[0]), DMUL(w[1], w[1])), DMUL(w[2], w[2]));
+      double sz = DADD(DADD(DMUL(z[0], z[0]), DMUL(z[1], z[1])), DMUL(z[2], z[2]));
+      double scale = fmax(fmax(su, sw), sz);
+      double cx = DSUB(DMUL(u[1], w[2]), DMUL(u[2], w[1]));
+      double cy = DSUB(DMUL(u[2], w[0]), DMUL(u[0], w[2]));
+      double cz = DSUB(DMUL(u[0], w[1]), DMUL(u[1], w[0]));
+      double area = __dsqrt_rn(DADD(DADD(DMUL(cx, cx), DMUL(cy, cy)), DMUL(cz, cz)));
+      deg = (scale == 0.0) || (area < DMUL(1e-12, scale));
+    }
+    if (deg) bad_deg = min(bad_deg, (unsigned long long)k);
+  }
+  // warp reduce, then one atomic per warp
+  for (int o = 16; o > 0; o >>= 1) {
+    for (int a = 0; a < 3; ++a) {
+      mn[a] = fminf(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+      mx[a] = fmaxf(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+    }
+    am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+    bad_deg = min(bad_deg, __shfl_xor_sync(0xffffffffu, bad_deg, o));
+    bad_fin = min(bad_fin, __shfl_xor_sync(0xffffffffu, bad_fin, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    float* fs = (float*)(small + 2);
+    for (int a = 0; a < dim; ++a) {
+      atomic_min_f(&fs[a], mn[a]);
+      atomic_max_f(&fs[3 + a], mx[a]);
+    }
+    atomic_max_f(&fs[6], am);
+    if (bad_deg != ~0ull) atomicMin((unsigned long long*)&small[0], bad_deg);
+    if (bad_fin != ~0ull) atomicMin((unsigned long long*)&small[1], bad_fin);
+  }
+}
+
+__global__ void k_face_check_init(int64_t* small) {
+  small[0] = -1;  // 0xfff.. as unsigned = "none"
+  small[1] = -1;
+  float* fs = (float*)(small + 2);
+  for (int a = 0; a < 3; ++a) {
+    fs[a] = INFINITY;
+    fs[3 + a] = -INFINITY;
+  }
+  fs[6] = 0.0f;
+  fs[7] = 0.0f;
+}
+
+}  // namespace
+
+extern "C" int ow_stl_binary_to_soa(ow_ctx* ctx, const uint8_t* d_records, int64_t n, float* d_coords,
+                                    void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n < 0 || (n > 0 && (!d_records || !d_coords))) {
+    ow_set_error("ow_stl_binary_to_soa: bad arguments");
+    return OW_ERR_INVALID;
+  }
+  if (((uintptr_t)d_records & 1) != 0) {
+    ow_set_error("ow_stl_binary_to_soa: records must be 2-byte aligned");
+    return OW_ERR_INVALID;
+  }
+  if (n == 0) return OW_OK;
+  OW_PROF_BEGIN(ctx, PROF_STL, s);
+  k_stl_to_soa<<<ow_blocks(n, STL_TILE), STL_TILE, 0, s>>>((const uint16_t*)d_records, n, d_coords);
+  OW_PROF_END(ctx, PROF_STL, s);
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  return OW_OK;
+}
+
+extern "C" int ow_index_to_coords(ow_ctx* ctx, int32_t dim, const float* d_vertices, const int32_t* d_faces,
+                                  int64_t n, float* d_coords, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dim != 2 && dim != 3) {
+    ow_set_error("dim must be 2 or 3, got %d", dim);
+    return OW_ERR_INVALID;
+  }
+  if (n == 0) return OW_OK;
+  k_index_to_coords<<<ow_blocks(n, 256), 256, 0, s>>>(dim, d_vertices, d_faces, n, d_coords);
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  return OW_OK;
+}
+
+extern "C" int ow_face_check(ow_ctx* ctx, int32_t dim, const float* d_coords, int64_t n,
+                             ow_face_summary* out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dim != 2 && dim != 3) {
+    ow_set_error("dim must be 2 or 3, got %d", dim);
+    return OW_ERR_INVALID;
+  }
+  k_face_check_init<<<1, 1, 0, s>>>(ctx->d_small);
+  OW_LAUNCHED(ctx);
+  if (n > 0) {
+    k_face_check<<<ow_blocks(n, 256, 4 * OW_SMS), 256, 0, s>>>(dim, d_coords, n, ctx->d_small);
+    OW_LAUNCHED(ctx);
+  }
+  OW_CHECK_LAUNCH();
+  int64_t h[6];
+  OW_TRY(ow_readback(ctx, ctx->d_small, 6, h, s));
+  out->first_degenerate = h[0];
+  out->first_nonfinite = h[1];
+  const float* fs = (const float*)(h + 2);
+  for (int a = 0; a < 3; ++a) {
+    out->bbox_min[a] = fs[a];
+    out->bbox_max[a] = fs[3 + a];
+  }
+  out->abs_max = fs[6];
+  out->_pad = 0.0f;
+  return OW_OK;
+}

@@ -1,0 +1,596 @@
+// Near-wall detection on sm_100a: face prep, block marking (naive / binned),
+// cell-face links, and the pairwise predicate probe.
+//
+// Reference: octowall/nearwall.py:31-54 (cull reach, face boxes, box cull),
+// 146-214 (sphere prefilter, _scan_block), 217-311 (mark_near_wall_naive /
+// _binned), 522-594 (build_cell_face_links).
+//
+// One CTA per leaf block.  The CTA computes its 4^D cell centres (FP64 -> one
+// FP32 rounding), their bins, and the block box; then, per distinct bin of its
+// cells (or once over all faces for the naive strategy), stages the bin's
+// faces that pass the reference's FP64 box cull into shared memory, and
+// sweeps (cell, staged face) pairs: FP32 bounding-sphere prefilter, then the
+// full 130-op predicate.  The first hit ends the block (a mark is an OR).
+// A pair is evaluated iff the reference evaluates it, so marks are bit-exact
+// even where the predicate is ill-conditioned.
+#include "ow_predicate.cuh"
+#include "ow_scan.cuh"
+#include <string.h>
+
+namespace {
+
+using ow::scan;
+
+constexpr int MARK_THREADS = 128;
+constexpr int STAGE = 512;  // faces staged per chunk
+
+template <int D>
+__global__ void k_face_prep(const float* __restrict__ c, int64_t n, float d, double reach, float4* box,
+                            float4* sph, float4* pay) {
+  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n) return;
+  float lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  for (int a = 0; a < D; ++a) {
+    float mn = c[(int64_t)a * n + f], mx = mn;
+    for (int j = 1; j < D; ++j) {
+      float x = c[((int64_t)j * D + a) * n + f];
+      mn = fminf(mn, x);
+      mx = fmaxf(mx, x);
+    }
+    lo[a] = mn;
+    hi[a] = mx;
+  }
+  box[2 * f] = make_float4(lo[0], lo[1], lo[2], 0.0f);
+  box[2 * f + 1] = make_float4(hi[0], hi[1], hi[2], 0.0f);
+  // bounding sphere: centre f32(0.5 (lo+hi)), radius^2 f32((|0.5 (hi-lo)| + reach)^2)
+  double ctr[3] = {0, 0, 0}, ss = 0.0;
+  for (int a = 0; a < D; ++a) {
+    double l = lo[a], h = hi[a];
+    ctr[a] = DMUL(0.5, DADD(l, h));
+    double hh = DMUL(0.5, DSUB(h, l));
+    ss = a ? DADD(ss, DMUL(hh, hh)) : DMUL(hh, hh);
+  }
+  double r = DADD(__dsqrt_rn(ss), reach);
+  sph[f] = make_float4(__double2float_rn(ctr[0]), __double2float_rn(ctr[1]), __double2float_rn(ctr[2]),
+                       __double2float_rn(DMUL(r, r)));
+  face_prep_one<D>(c, n, f, d, pay + f * (D == 3 ? PAY3 : PAY2));
+}
+
+int prepare_faces(ow_ctx* ctx, int dim, const float* c, int64_t n, int64_t key, float d, double reach,
+                  cudaStream_t s) {
+  const int pw = dim == 3 ? PAY3 : PAY2;
+  void *pb, *ps, *pp;
+  bool fresh = ctx->prep_key != key || key < 0 || ctx->prep_faces != n || ctx->prep_dim != dim;
+  size_t need_pay = sizeof(float4) * pw * (size_t)n;
+  if (ctx->slot_bytes[SLOT_FACE_PREP] < need_pay || ctx->slot_bytes[SLOT_FACE_BOX] < 32 * (size_t)n ||
+      ctx->slot_bytes[SLOT_FACE_SPHERE] < 16 * (size_t)n)
+    fresh = true;
+  if (!fresh && ctx->prep_d == d && ctx->prep_reach == reach) return OW_OK;
+  OW_TRY(ow_slot(ctx, SLOT_FACE_BOX, 32 * (size_t)n, s, &pb));
+  OW_TRY(ow_slot(ctx, SLOT_FACE_SPHERE, 16 * (size_t)n, s, &ps));
+  OW_TRY(ow_slot(ctx, SLOT_FACE_PREP, need_pay, s, &pp));
+  if (dim == 3)
+    k_face_prep<3><<<ow_blocks(n, 128), 128, 0, s>>>(c, n, d, reach, (float4*)pb, (float4*)ps, (float4*)pp);
+  else
+    k_face_prep<2><<<ow_blocks(n, 128), 128, 0, s>>>(c, n, d, reach, (float4*)pb, (float4*)ps, (float4*)pp);
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  ctx->prep_key = key;
+  ctx->prep_faces = n;
+  ctx->prep_dim = dim;
+  ctx->prep_d = d;
+  ctx->prep_reach = reach;
+  return OW_OK;
+}
+
+// FP64 block-box vs face-box distance cull (nearwall.py:48-54); the sum
+// follows numpy.einsum's pairing for 3 terms, (g0^2 + g2^2) + g1^2.
+template <int D>
+__device__ __forceinline__ bool box_ok(const double* blo, const double* bhi, float4 flo, float4 fhi, double reach2) {
+  double g[3];
+  const float l[3] = {flo.x, flo.y, flo.z}, h[3] = {fhi.x, fhi.y, fhi.z};
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double x = fmax(DSUB((double)l[a], bhi[a]), DSUB(blo[a], (double)h[a]));
+    g[a] = fmax(0.0, x);
+  }
+  double s = D == 3 ? DADD(DADD(DMUL(g[0], g[0]), DMUL(g[2], g[2])), DMUL(g[1], g[1]))
+                    : DADD(DMUL(g[0], g[0]), DMUL(g[1], g[1]));
+  return s <= reach2;
+}
+
+template <int D>
+__device__ __forceinline__ bool sphere_ok(const float* p, float4 s) {
+  float dx = FSUB(p[0], s.x), dy = FSUB(p[1], s.y);
+  float dist = FADD(FMUL(dx, dx), FMUL(dy, dy));
+  if (D == 3) {
+    float dz = FSUB(p[2], s.z);
+    dist = FADD(dist, FMUL(dz, dz));
+  }
+  return dist <= s.w;
+}
+
+struct MarkArgs {
+  ForestC F;
+  GridC g;
+  const int32_t* leaves;
+  const float4* box;
+  const float4* sph;
+  const float4* pay;
+  const int32_t* bin_ids;
+  const int32_t* bin_counts;
+  const int32_t* bin_offsets;
+  int64_t n_faces;
+  float d;
+  double reach;
+  unsigned long long* out;  // [0] marked, [1] tests, [2] evaluated
+};
+
+template <int D, bool BINNED>
+__global__ void __launch_bounds__(MARK_THREADS) k_mark(MarkArgs A) {
+  constexpr int C = D == 3 ? 64 : 16;
+  constexpr int PW = D == 3 ? PAY3 : PAY2;
+  __shared__ float s_cen[C][D];
+  __shared__ int s_bin[C];
+  __shared__ int s_ubin[C];
+  __shared__ int s_cells[C];
+  __shared__ int s_nu, s_ncell, s_ncand, s_hit;
+  __shared__ int s_cand[STAGE];
+  __shared__ float4 s_sph[STAGE];
+  __shared__ unsigned long long s_red[MARK_THREADS / 32];
+
+  const ForestC& F = A.F;
+  const int id = A.leaves[blockIdx.x];
+  const int L = F.level[id];
+  const int tid = threadIdx.x;
+  double blo[3], bhi[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double q = block_len(F, a, L);
+    blo[a] = DADD(F.dmin[a], DMUL((double)F.coord[a][id], q));
+    bhi[a] = DADD(blo[a], q);
+  }
+  if (tid < C) {
+    float p[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      double q = block_len(F, a, L);
+      double u = ((double)((tid >> (2 * a)) & 3) + 0.5) / 4.0;
+      p[a] = __double2float_rn(DADD(blo[a], DMUL(u, q)));
+      s_cen[tid][a] = p[a];
+    }
+    if (BINNED) {
+      int lin = 0, mul = 1;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        lin += bin_axis(p[a], A.g.min32[a], A.g.len32[a], A.g.B) * mul;
+        mul *= A.g.B;
+      }
+      s_bin[tid] = lin;
+    }
+  }
+  if (tid == 0) {
+    s_hit = 0;
+    s_nu = 0;
+  }
+  __syncthreads();
+  // algorithmic test count T
+  {
+    unsigned long long t = 0;
+    if (tid < C) t = BINNED ? (unsigned long long)A.bin_counts[s_bin[tid]] : (unsigned long long)A.n_faces;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((tid & 31) == 0) s_red[tid >> 5] = t;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long sum = 0;
+      for (int w = 0; w < MARK_THREADS / 32; ++w) sum += s_red[w];
+      atomicAdd(&A.out[1], sum);
+    }
+  }
+  if (F.marks[id] == OW_MARKED) return;
+  if (BINNED && tid < C) {
+    bool first = true;
+    for (int j = 0; j < tid; ++j) first &= s_bin[j] != s_bin[tid];
+    if (first) s_ubin[atomicAdd(&s_nu, 1)] = s_bin[tid];
+  }
+  __syncthreads();
+  const int nu = BINNED ? s_nu : 1;
+  const double reach2 = DMUL(A.reach, A.reach);
+  const float r2 = FMUL(A.d, A.d);
+  unsigned long long evaluated = 0;
+
+  for (int u = 0; u < nu && !s_hit; ++u) {
+    int64_t src0 = 0, srcn = A.n_faces;
+    const int32_t* src = nullptr;
+    if (BINNED) {
+      int b = s_ubin[u];
+      src = A.bin_ids + A.bin_offsets[b];
+      srcn = A.bin_counts[b];
+      if (tid == 0) s_ncell = 0;
+      __syncthreads();
+      if (tid < C && s_bin[tid] == b) s_cells[atomicAdd(&s_ncell, 1)] = tid;
+    } else {
+      if (tid < C) s_cells[tid] = tid;
+      if (tid == 0) s_ncell = C;
+    }
+    for (int64_t base = src0; base < srcn; base += STAGE) {
+      if (tid == 0) s_ncand = 0;
+      __syncthreads();
+      const int64_t m = min((int64_t)STAGE, srcn - base);
+      for (int j = tid; j < m; j += MARK_THREADS) {
+        int f = BINNED ? src[base + j] : (int)(base + j);
+        if (box_ok<D>(blo, bhi, A.box[2 * (int64_t)f], A.box[2 * (int64_t)f + 1], reach2)) {
+          int k = atomicAdd(&s_ncand, 1);
+          s_cand[k] = f;
+          s_sph[k] = A.sph[f];
+        }
+      }
+      __syncthreads();
+      const int ncand = s_ncand, ncell = s_ncell;
+      const int total = ncand * ncell;
+      for (int k = tid; k < total; k += MARK_THREADS) {
+        if (*(volatile int*)&s_hit) break;
+        int ci = s_cells[k / ncand];
+        int j = k - (k / ncand) * ncand;
+        float p[3];
+#pragma unroll
+        for (int a = 0; a < D; ++a) p[a] = s_cen[ci][a];
+        if (!sphere_ok<D>(p, s_sph[j])) continue;
+        ++evaluated;
+        if (near_face<D>(A.pay + (int64_t)s_cand[j] * PW, p, r2)) {
+          s_hit = 1;
+          break;
+        }
+      }
+      __syncthreads();
+      if (s_hit) break;
+    }
+    __syncthreads();  // s_cells / s_ncell are rewritten for the next bin
+  }
+  for (int o = 16; o > 0; o >>= 1) evaluated += __shfl_xor_sync(0xffffffffu, evaluated, o);
+  if ((tid & 31) == 0 && evaluated) atomicAdd(&A.out[2], evaluated);
+  if (tid == 0 && s_hit) {
+    F.marks[id] = OW_MARKED;
+    atomicAdd(&A.out[0], 1ull);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// cell-face links (build_cell_face_links, nearwall.py:522-594)
+// Pass 1 counts the links of every leaf cell and finds the first overflowing
+// (block position, bin, cell) key; pass 2 writes each cell's faces in
+// ascending order (bins hold ascending ids; a warp walks them in order with
+// a ballot prefix).  One CTA per leaf block, one warp per cell at a time.
+// ---------------------------------------------------------------------------
+struct LinkArgs {
+  ForestC F;
+  GridC g;
+  const int32_t* leaves;
+  const float4* box;
+  const float4* pay;
+  const int32_t* bin_ids;
+  const int32_t* bin_counts;
+  const int32_t* bin_offsets;
+  float d;
+  double reach;
+  int64_t capacity;
+  int32_t* cell_cnt;          // pass 1 out: per cell count
+  unsigned long long* over;   // pass 1 out: min overflow key
+  const int64_t* cell_off;    // pass 2 in: per cell link offset
+  int32_t* face_ids;          // pass 2 out
+};
+
+template <int D, bool EMIT>
+__global__ void __launch_bounds__(MARK_THREADS) k_links(LinkArgs A) {
+  constexpr int C = D == 3 ? 64 : 16;
+  constexpr int PW = D == 3 ? PAY3 : PAY2;
+  __shared__ float s_cen[C][D];
+  __shared__ int s_bin[C];
+  __shared__ int s_cnt[C];
+  const ForestC& F = A.F;
+  const int64_t pos = blockIdx.x;
+  const int id = A.leaves[pos];
+  const int L = F.level[id];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double blo[3], bhi[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double q = block_len(F, a, L);
+    blo[a] = DADD(F.dmin[a], DMUL((double)F.coord[a][id], q));
+    bhi[a] = DADD(blo[a], q);
+  }
+  if (tid < C) {
+    float p[3];
+    int lin = 0, mul = 1;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      double q = block_len(F, a, L);
+      double u = ((double)((tid >> (2 * a)) & 3) + 0.5) / 4.0;
+      p[a] = __double2float_rn(DADD(blo[a], DMUL(u, q)));
+      s_cen[tid][a] = p[a];
+      lin += bin_axis(p[a], A.g.min32[a], A.g.len32[a], A.g.B) * mul;
+      mul *= A.g.B;
+    }
+    s_bin[tid] = lin;
+    s_cnt[tid] = 0;
+  }
+  __syncthreads();
+  const double reach2 = DMUL(A.reach, A.reach);
+  const float r2 = FMUL(A.d, A.d);
+  for (int ci = warp; ci < C; ci += MARK_THREADS / 32) {
+    const int b = s_bin[ci];
+    const int32_t* src = A.bin_ids + A.bin_offsets[b];
+    const int n = A.bin_counts[b];
+    float p[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) p[a] = s_cen[ci][a];
+    int64_t out = EMIT ? A.cell_off[pos * C + ci] : 0;
+    int cnt = 0;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      int j = j0 + lane;
+      bool hit = false;
+      int f = 0;
+      if (j < n) {
+        f = src[j];
+        if (box_ok<D>(blo, bhi, A.box[2 * (int64_t)f], A.box[2 * (int64_t)f + 1], reach2))
+          hit = near_face<D>(A.pay + (int64_t)f * PW, p, r2);
+      }
+      unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (EMIT && hit) A.face_ids[out + cnt + __popc(bal & lanemask_lt())] = f;
+      cnt += __popc(bal);
+    }
+    if (lane == 0) s_cnt[ci] = cnt;
+  }
+  __syncthreads();
+  if (!EMIT && tid < C) {
+    int cnt = s_cnt[tid];
+    A.cell_cnt[pos * C + tid] = cnt;
+    if (cnt > A.capacity) {
+      // first overflow in the reference's order: block asc, bin asc, cell asc
+      unsigned long long key = ((unsigned long long)pos << 40) | ((unsigned long long)s_bin[tid] << 8) | tid;
+      atomicMin(A.over, key);
+    }
+  }
+}
+
+struct CellCntLoad {
+  const int32_t* c;
+  __device__ int64_t operator()(int64_t i) const { return c[i]; }
+};
+struct CellOffStore {
+  int64_t* off;
+  __device__ void operator()(int64_t i, int64_t e, int64_t) const { off[i] = e; }
+};
+struct LinkedLoad {
+  const int32_t* c;
+  __device__ int64_t operator()(int64_t i) const { return c[i] > 0; }
+};
+struct NullStoreL {
+  __device__ void operator()(int64_t, int64_t, int64_t) const {}
+};
+struct LinkedStore {
+  const int32_t* leaves;
+  const int32_t* cnt;
+  const int64_t* cell_off;
+  int C;
+  int64_t* block_ids;
+  int64_t* cell_idx;
+  int64_t* offsets;
+  __device__ void operator()(int64_t i, int64_t e, int64_t v) const {
+    if (!v) return;
+    block_ids[e] = leaves[i / C];
+    cell_idx[e] = i % C;
+    offsets[e] = cell_off[i];
+  }
+};
+
+__global__ void k_near_pairs(int dim, const float* __restrict__ pts, const float* __restrict__ faces,
+                             const float* __restrict__ dd, int64_t n, uint8_t* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float4 pay[PAY3];
+  float d = dd[i];
+  float r2 = FMUL(d, d);
+  float p[3];
+  if (dim == 3) {
+    face_prep_one<3>(faces, n, i, d, pay);
+    for (int a = 0; a < 3; ++a) p[a] = pts[i * 3 + a];
+    out[i] = near_face<3>(pay, p, r2);
+  } else {
+    face_prep_one<2>(faces, n, i, d, pay);
+    for (int a = 0; a < 2; ++a) p[a] = pts[i * 2 + a];
+    out[i] = near_face<2>(pay, p, r2);
+  }
+}
+
+}  // namespace
+
+extern "C" int ow_mark_near_wall(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
+                                 const float* d_coords, int64_t n_faces, int64_t geom_key, const ow_grid* grid,
+                                 const int32_t* d_bin_ids, const int32_t* d_bin_counts, const int32_t* d_bin_offsets,
+                                 float d_spec, double reach, int64_t* out_marked, int64_t* out_tests,
+                                 int64_t* out_evaluated, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!(d_spec > 0.0f)) {
+    ow_set_error("near-wall distance must be positive, got %g", (double)d_spec);
+    return OW_ERR_INVALID;
+  }
+  if (n_faces <= 0) {
+    ow_set_error("cannot mark near-wall blocks with empty geometry");
+    return OW_ERR_INVALID;
+  }
+  const bool binned = d_bin_ids != nullptr;
+  if (binned && (!grid || grid->dim != f->dim)) {
+    ow_set_error("bin grid does not match the forest");
+    return OW_ERR_INVALID;
+  }
+  OW_PROF_BEGIN(ctx, PROF_PREP, s);
+  OW_TRY(prepare_faces(ctx, f->dim, d_coords, n_faces, geom_key, d_spec, reach, s));
+  OW_PROF_END(ctx, PROF_PREP, s);
+  unsigned long long* out = (unsigned long long*)(ctx->d_small + 16);
+  OW_CUDA(cudaMemsetAsync(out, 0, 3 * 8, s));
+  if (n_leaves > 0) {
+    MarkArgs A;
+    A.F = make_forestc(f);
+    if (binned) A.g = make_gridc(grid);
+    A.leaves = d_leaves;
+    A.box = (const float4*)ctx->slot_ptr[SLOT_FACE_BOX];
+    A.sph = (const float4*)ctx->slot_ptr[SLOT_FACE_SPHERE];
+    A.pay = (const float4*)ctx->slot_ptr[SLOT_FACE_PREP];
+    A.bin_ids = d_bin_ids;
+    A.bin_counts = d_bin_counts;
+    A.bin_offsets = d_bin_offsets;
+    A.n_faces = n_faces;
+    A.d = d_spec;
+    A.reach = reach;
+    A.out = out;
+    dim3 grd((unsigned)n_leaves);
+    OW_PROF_BEGIN(ctx, PROF_MARK, s);
+    if (f->dim == 3) {
+      if (binned) k_mark<3, true><<<grd, MARK_THREADS, 0, s>>>(A);
+      else k_mark<3, false><<<grd, MARK_THREADS, 0, s>>>(A);
+    } else {
+      if (binned) k_mark<2, true><<<grd, MARK_THREADS, 0, s>>>(A);
+      else k_mark<2, false><<<grd, MARK_THREADS, 0, s>>>(A);
+    }
+    OW_PROF_END(ctx, PROF_MARK, s);
+    OW_LAUNCHED(ctx);
+    OW_CHECK_LAUNCH();
+  }
+  int64_t h[3];
+  OW_TRY(ow_readback(ctx, ctx->d_small + 16, 3, h, s));
+  *out_marked = h[0];
+  *out_tests = h[1];
+  *out_evaluated = h[2];
+  return OW_OK;
+}
+
+extern "C" int ow_cell_face_links_count(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
+                                        const float* d_coords, int64_t n_faces, int64_t geom_key, const ow_grid* grid,
+                                        const int32_t* d_bin_ids, const int32_t* d_bin_counts,
+                                        const int32_t* d_bin_offsets, float d_link, double reach, int64_t capacity,
+                                        int64_t* out_cells, int64_t* out_links, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!(d_link > 0.0f)) {
+    ow_set_error("near-wall distance must be positive, got %g", (double)d_link);
+    return OW_ERR_INVALID;
+  }
+  const int C = f->dim == 3 ? 64 : 16;
+  OW_TRY(prepare_faces(ctx, f->dim, d_coords, n_faces, geom_key, d_link, reach, s));
+  int64_t ncells = n_leaves * C;
+  void *pc, *po;
+  OW_TRY(ow_slot(ctx, SLOT_LINK_CNT, 4 * (size_t)ncells, s, &pc));
+  OW_TRY(ow_slot(ctx, SLOT_LINK_OFF, 8 * (size_t)(ncells + 1), s, &po));
+  unsigned long long* over = (unsigned long long*)(ctx->d_small + 24);
+  OW_CUDA(cudaMemsetAsync(over, 0xff, 8, s));
+  LinkArgs A;
+  memset(&A, 0, sizeof(A));
+  A.F = make_forestc(f);
+  A.g = make_gridc(grid);
+  A.leaves = d_leaves;
+  A.box = (const float4*)ctx->slot_ptr[SLOT_FACE_BOX];
+  A.pay = (const float4*)ctx->slot_ptr[SLOT_FACE_PREP];
+  A.bin_ids = d_bin_ids;
+  A.bin_counts = d_bin_counts;
+  A.bin_offsets = d_bin_offsets;
+  A.d = d_link;
+  A.reach = reach;
+  A.capacity = capacity;
+  A.cell_cnt = (int32_t*)pc;
+  A.over = over;
+  if (n_leaves > 0) {
+    if (f->dim == 3) k_links<3, false><<<(unsigned)n_leaves, MARK_THREADS, 0, s>>>(A);
+    else k_links<2, false><<<(unsigned)n_leaves, MARK_THREADS, 0, s>>>(A);
+    OW_LAUNCHED(ctx);
+    OW_CHECK_LAUNCH();
+  }
+  OW_TRY(scan(ctx, CellCntLoad{(const int32_t*)pc}, CellOffStore{(int64_t*)po}, ncells, ctx->d_small + 25, s));
+  OW_TRY(scan(ctx, LinkedLoad{(const int32_t*)pc}, NullStoreL{}, ncells, ctx->d_small + 26, s));
+  int64_t h[3];
+  OW_TRY(ow_readback(ctx, ctx->d_small + 24, 3, h, s));
+  if (h[0] != -1) {
+    unsigned long long key = (unsigned long long)h[0];
+    int64_t pos = (int64_t)(key >> 40);
+    int cell = (int)(key & 0xff);
+    int32_t bid, cnt;
+    OW_CUDA(cudaMemcpyAsync(&bid, d_leaves + pos, 4, cudaMemcpyDeviceToHost, s));
+    OW_CUDA(cudaMemcpyAsync(&cnt, (int32_t*)pc + pos * C + cell, 4, cudaMemcpyDeviceToHost, s));
+    OW_CUDA(cudaStreamSynchronize(s));
+    ow_set_error("cell-face link overflow: block %d cell %d links %d faces, capacity %lld", bid, cell, cnt,
+                 (long long)capacity);
+    return OW_ERR_CAPACITY;
+  }
+  ctx->link_total = h[1];
+  ctx->link_cells = h[2];
+  ctx->link_leaves = n_leaves;
+  ctx->link_dim = f->dim;
+  ctx->link_forest = *f;
+  ctx->link_grid = *grid;
+  ctx->link_coords = d_coords;
+  ctx->link_bin_ids = d_bin_ids;
+  ctx->link_bin_counts = d_bin_counts;
+  ctx->link_bin_offsets = d_bin_offsets;
+  ctx->link_d = d_link;
+  ctx->link_reach = reach;
+  ctx->link_leaves_ptr = d_leaves;
+  ctx->link_key = geom_key;
+  ctx->link_faces = n_faces;
+  *out_cells = h[2];
+  *out_links = h[1];
+  return OW_OK;
+}
+
+extern "C" int ow_cell_face_links_emit(ow_ctx* ctx, int64_t* d_block_ids, int64_t* d_cell_indices, int64_t* d_offsets,
+                                       int32_t* d_face_ids, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (ctx->link_dim != 2 && ctx->link_dim != 3) {
+    ow_set_error("ow_cell_face_links_emit without ow_cell_face_links_count");
+    return OW_ERR_INVALID;
+  }
+  const int C = ctx->link_dim == 3 ? 64 : 16;
+  int64_t ncells = ctx->link_leaves * C;
+  OW_TRY(prepare_faces(ctx, ctx->link_dim, ctx->link_coords, ctx->link_faces, ctx->link_key, ctx->link_d,
+                       ctx->link_reach, s));
+  const int32_t* cnt = (const int32_t*)ctx->slot_ptr[SLOT_LINK_CNT];
+  const int64_t* off = (const int64_t*)ctx->slot_ptr[SLOT_LINK_OFF];
+  OW_TRY(scan(ctx, LinkedLoad{cnt},
+              LinkedStore{ctx->link_leaves_ptr, cnt, off, C, d_block_ids, d_cell_indices, d_offsets}, ncells,
+              nullptr, s));
+  OW_CUDA(cudaMemcpyAsync(d_offsets + ctx->link_cells, &ctx->link_total, 8, cudaMemcpyHostToDevice, s));
+  LinkArgs A;
+  memset(&A, 0, sizeof(A));
+  A.F = make_forestc(&ctx->link_forest);
+  A.g = make_gridc(&ctx->link_grid);
+  A.leaves = ctx->link_leaves_ptr;
+  A.box = (const float4*)ctx->slot_ptr[SLOT_FACE_BOX];
+  A.pay = (const float4*)ctx->slot_ptr[SLOT_FACE_PREP];
+  A.bin_ids = ctx->link_bin_ids;
+  A.bin_counts = ctx->link_bin_counts;
+  A.bin_offsets = ctx->link_bin_offsets;
+  A.d = ctx->link_d;
+  A.reach = ctx->link_reach;
+  A.cell_off = off;
+  A.face_ids = d_face_ids;
+  if (ctx->link_leaves > 0) {
+    if (ctx->link_dim == 3) k_links<3, true><<<(unsigned)ctx->link_leaves, MARK_THREADS, 0, s>>>(A);
+    else k_links<2, true><<<(unsigned)ctx->link_leaves, MARK_THREADS, 0, s>>>(A);
+    OW_LAUNCHED(ctx);
+    OW_CHECK_LAUNCH();
+  }
+  OW_CUDA(cudaStreamSynchronize(s));  // the host offset copy reads ctx memory
+  return OW_OK;
+}
+
+extern "C" int ow_near_pairs(ow_ctx* ctx, int32_t dim, const float* d_points, const float* d_faces, const float* d_d,
+                             int64_t n, uint8_t* d_out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dim != 2 && dim != 3) {
+    ow_set_error("dim must be 2 or 3, got %d", dim);
+    return OW_ERR_INVALID;
+  }
+  if (n <= 0) return OW_OK;
+  k_near_pairs<<<ow_blocks(n, 128), 128, 0, s>>>(dim, d_points, d_faces, d_d, n, d_out);
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  return OW_OK;
+}

@@ -1,0 +1,315 @@
+"""Near-wall refinement on the GPU: marking, propagation, per-level driver,
+cell-face links.  Mirrors octowall/nearwall.py (names, signatures, defaults,
+return values, error messages) on top of libowb200:
+
+    mark_near_wall_naive / _binned -> ow_mark_near_wall     (nearwall.py:217, 253)
+    propagate_marks                -> ow_propagate_marks    (nearwall.py:321)
+    Forest.refine_marked           -> ow_refine_marked      (forest.py:331)
+    build_cell_face_links          -> ow_cell_face_links_*  (nearwall.py:522)
+
+Every host scalar the reference returns (blocks marked, entries, splits) is a
+stream synchronisation point; everything else stays on the device.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib, backends
+from .binning import BinGrid, BinnedFaces, auto_bin_fraction, fill_bins
+from .errors import InvalidParameterError
+from .forest import Forest, RefineMark
+from .geometry import CoordListGeometry, bounding_box, validate_faces
+
+
+def _coordinate_scale(forest, geom):
+    """nearwall.py:31-35 (|coords| max from the GPU face summary)."""
+    s = max(float(np.abs(forest.domain.min).max()), float(np.abs(forest.domain.max).max()))
+    if geom.n_faces:
+        s = max(s, float(np.float32(geom.summary().abs_max)))
+    return s
+
+
+def _cull_reach(d_spec, scale):
+    return d_spec + 1e-3 * max(1.0, scale, d_spec)
+
+
+def _check_marking_inputs(forest, geom, d_spec):
+    if geom.dim != forest.dim:
+        raise InvalidParameterError(f"geometry is {geom.dim}D but forest is {forest.dim}D")
+    if geom.n_faces == 0:
+        raise InvalidParameterError("cannot mark near-wall blocks with empty geometry")
+    if d_spec <= 0:
+        raise InvalidParameterError(f"near-wall distance must be positive, got {d_spec}")
+    validate_faces(geom)
+
+
+@dataclass
+class MarkStats:
+    """Per marking pass: blocks newly marked, algorithmic tests T, pairs evaluated."""
+
+    marked: int
+    tests: int
+    evaluated: int
+
+
+def _mark(forest, level, geom, d_spec, bins, grid, leaves=None):
+    if leaves is None:
+        leaves = forest._leaves(level)
+    n = int(leaves.numel())
+    m, t, e = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+    reach = _cull_reach(d_spec, _coordinate_scale(forest, geom))
+    g = grid.c_struct() if grid is not None else None
+    _lib.call("ow_mark_near_wall", _lib.ctx(), C.byref(forest.view()), _lib.ptr(leaves), n, _lib.ptr(geom.coords),
+              geom.n_faces, geom.key, C.byref(g) if g is not None else None,
+              _lib.ptr(bins.ids) if bins is not None else None,
+              _lib.ptr(bins.counts) if bins is not None else None,
+              _lib.ptr(bins.offsets) if bins is not None else None,
+              float(np.float32(d_spec)), float(reach), C.byref(m), C.byref(t), C.byref(e), _lib.stream())
+    return MarkStats(int(m.value), int(t.value), int(e.value))
+
+
+def mark_near_wall_naive(forest: Forest, level, geom: CoordListGeometry, d_spec, backend=backends.SERIAL,
+                         stats=False):
+    """Mark leaves at ``level`` with a cell centre within d_spec of any face."""
+    backends.validate_backend(backend)
+    _check_marking_inputs(forest, geom, d_spec)
+    s = _mark(forest, level, geom, d_spec, None, None)
+    return s if stats else s.marked
+
+
+def mark_near_wall_binned(forest: Forest, level, geom: CoordListGeometry, bins: BinnedFaces, grid: BinGrid,
+                          d_spec, backend=backends.SERIAL, stats=False):
+    """Each cell tests only the faces stored in the bin holding its centre."""
+    backends.validate_backend(backend)
+    _check_marking_inputs(forest, geom, d_spec)
+    if bins.n_bins != grid.n_bins:
+        raise InvalidParameterError("bin structure does not match the bin grid")
+    s = _mark(forest, level, geom, d_spec, bins, grid)
+    return s if stats else s.marked
+
+
+def propagation_rounds(d_spec, block_length):
+    if d_spec <= 0 or block_length <= 0:
+        raise InvalidParameterError("d_spec and block_length must be positive")
+    return 1 + math.floor(d_spec / block_length)
+
+
+def propagate_marks(forest: Forest, level, d_spec, backend=backends.SERIAL, rounds=None):
+    """Two-pass NONE -> INTERMEDIATE -> MARKED dilation over face neighbours."""
+    backends.validate_backend(backend)
+    if forest.count_marks(level, RefineMark.INTERMEDIATE, leaf_only=False):
+        raise InvalidParameterError(f"level {level} already carries intermediate marks")
+    if rounds is None:
+        rounds = propagation_rounds(d_spec, float(np.min(forest.block_length(level))))
+    leaves = forest._leaves(level)
+    if leaves.numel() == 0 or rounds == 0:
+        return
+    _lib.call("ow_propagate_marks", _lib.ctx(), C.byref(forest.view()), _lib.ptr(leaves), int(leaves.numel()),
+              int(rounds), _lib.stream())
+
+
+@dataclass
+class StageTiming:
+    stage: str
+    level: int
+    strategy: str
+    bins_per_axis: int
+    bin_fraction: int
+    milliseconds: float
+
+    CSV_HEADER = "stage,level,strategy,B,B_f,milliseconds"
+
+    def csv_row(self):
+        return (f"{self.stage},{self.level},{self.strategy},{self.bins_per_axis},"
+                f"{self.bin_fraction},{self.milliseconds:.3f}")
+
+
+def write_timings_csv(path, timings):
+    with open(path, "w", encoding="utf-8") as f:
+        f.write(StageTiming.CSV_HEADER + "\n")
+        for t in timings:
+            f.write(t.csv_row() + "\n")
+
+
+@dataclass
+class NearWallParams:
+    d_spec: float
+    n_levels: int = 3
+    strategy: str = "binned"
+    bins_per_axis: int = 8
+    bin_fraction: int | None = None
+    overlap_factor: int = 10
+    spacing: float | None = None
+    backend: str = backends.SERIAL
+
+    def __post_init__(self):
+        if self.strategy not in ("naive", "binned"):
+            raise InvalidParameterError(f"unknown strategy {self.strategy!r}")
+        if self.n_levels < 1:
+            raise InvalidParameterError(f"n_levels must be >= 1, got {self.n_levels}")
+        backends.validate_backend(self.backend)
+
+
+@dataclass
+class NearWallResult:
+    forest: Forest
+    timings: list = field(default_factory=list)
+    marked_detected: list = field(default_factory=list)
+    marked_refined: list = field(default_factory=list)
+    bins: BinnedFaces | None = None
+    grid: BinGrid | None = None
+    cell_face_tests: list = field(default_factory=list)  # T per marking pass
+    pairs_evaluated: list = field(default_factory=list)
+
+    @property
+    def total_marked(self):
+        return sum(self.marked_refined)
+
+    def total_ms(self, stage=None):
+        return sum(t.milliseconds for t in self.timings if stage is None or t.stage == stage)
+
+
+class _Clock:
+    """Stage wall clock; every stage ends in a host readback, so the GPU work
+    of the stage is complete when the clock stops (same semantics as the
+    reference's perf_counter records, nearwall.py:452-490)."""
+
+    def __init__(self, sync):
+        self.sync = sync
+
+    def __enter__(self):
+        if self.sync:
+            torch.cuda.current_stream().synchronize()
+        self.t0 = time.perf_counter()
+        return self
+
+    def __exit__(self, *a):
+        if self.sync:
+            torch.cuda.current_stream().synchronize()
+        self.ms = 1e3 * (time.perf_counter() - self.t0)
+
+
+def refine_near_wall(forest: Forest, geom: CoordListGeometry, params: NearWallParams, reuse_bins=True,
+                     shard=None) -> NearWallResult:
+    """Per level L in 0..n_levels-2: bins -> mark -> propagate -> refine.
+
+    The bin CSR depends only on (geometry, grid), so it is built once and
+    reused for every level (``reuse_bins``); the reference rebuilds an
+    identical structure per level.  ``shard`` (a ``parallel.Shard``) splits the
+    marking pass across ranks and all-gathers the marks (multi-GPU).
+    """
+    if geom.n_faces == 0:
+        raise InvalidParameterError("cannot refine around empty geometry")
+    bbox = bounding_box(geom)
+    tol = 1e-6 * forest.domain.extent
+    if np.any(bbox.min < forest.domain.min - tol) or np.any(bbox.max > forest.domain.max + tol):
+        raise InvalidParameterError(
+            f"geometry spans {bbox.min.tolist()}..{bbox.max.tolist()}, outside the forest domain")
+    result = NearWallResult(forest=forest)
+    binned = params.strategy == "binned"
+    b = params.bins_per_axis if binned else 1
+    bf = params.bin_fraction
+    if binned and bf is None:
+        bf = auto_bin_fraction(BinGrid(forest.domain, b).n_bins, geom.n_faces)
+
+    def record(stage, level, ms):
+        result.timings.append(StageTiming(stage, level, params.strategy, b, bf if binned else 1, ms))
+
+    bins = grid = None
+    for level in range(params.n_levels - 1):
+        if binned:
+            with _Clock(False) as ck:
+                if bins is None or not reuse_bins:
+                    grid = BinGrid(forest.domain, params.bins_per_axis)
+                    bins = fill_bins(geom, grid, bin_fraction=bf, overlap_factor=params.overlap_factor,
+                                     spacing=params.spacing, backend=params.backend)
+            record("bin_setup", level, ck.ms)
+            result.bins, result.grid = bins, grid
+            with _Clock(False) as ck:
+                _check_marking_inputs(forest, geom, params.d_spec)
+                st = _mark_level(forest, level, geom, params.d_spec, bins, grid, shard)
+            record("face_detection", level, ck.ms)
+            with _Clock(False) as ck:
+                propagate_marks(forest, level, params.d_spec, backend=params.backend)
+            record("propagation", level, ck.ms)
+        else:
+            with _Clock(False) as ck:
+                _check_marking_inputs(forest, geom, params.d_spec)
+                st = _mark_level(forest, level, geom, params.d_spec, None, None, shard)
+            record("face_detection", level, ck.ms)
+        result.marked_detected.append(st.marked)
+        result.cell_face_tests.append(st.tests)
+        result.pairs_evaluated.append(st.evaluated)
+        result.marked_refined.append(forest.count_marks(level, RefineMark.MARKED, leaf_only=True))
+        with _Clock(False) as ck:
+            forest.refine_marked(level)
+        record("refinement", level, ck.ms)
+    return result
+
+
+def _mark_level(forest, level, geom, d_spec, bins, grid, shard):
+    if shard is None:
+        return _mark(forest, level, geom, d_spec, bins, grid)
+    return shard.mark_level(forest, level, geom, d_spec, bins, grid, _mark)
+
+
+@dataclass
+class CellFaceLinks:
+    """Per-cell face links on the finest level (CUDA tensors; nearwall.py:494-519)."""
+
+    level: int
+    d_link: float
+    capacity: int
+    block_ids: torch.Tensor  # (n_cells,) int64
+    cell_indices: torch.Tensor  # (n_cells,) int64
+    offsets: torch.Tensor  # (n_cells + 1,) int64
+    face_ids: torch.Tensor  # int32
+
+    @property
+    def n_linked_cells(self):
+        return int(self.block_ids.numel())
+
+    def links_for(self, block_id, cell_index):
+        sel = torch.nonzero((self.block_ids == block_id) & (self.cell_indices == cell_index)).flatten()
+        if sel.numel() == 0:
+            return torch.zeros(0, dtype=torch.int32, device=self.face_ids.device)
+        i = int(sel[0])
+        return self.face_ids[int(self.offsets[i]):int(self.offsets[i + 1])]
+
+
+def build_cell_face_links(forest: Forest, geom: CoordListGeometry, bins: BinnedFaces, grid: BinGrid, d_link=None,
+                          capacity=16) -> CellFaceLinks:
+    """Link finest-level leaf cells to the nearby faces of their bin (GPU)."""
+    _check_marking_inputs(forest, geom, 1.0 if d_link is None else d_link)
+    level = forest.n_levels - 1
+    if d_link is None:
+        cell_len = forest.block_length(level) / 4.0
+        d_link = math.sqrt(forest.dim) * float(np.linalg.norm(cell_len))
+    leaves = forest._leaves(level)
+    if leaves.numel() == 0:
+        raise InvalidParameterError(f"no leaf blocks at finest level {level}")
+    reach = _cull_reach(d_link, _coordinate_scale(forest, geom))
+    g = grid.c_struct()
+    ncell, nlink = C.c_int64(0), C.c_int64(0)
+    ctx, st = _lib.ctx(), _lib.stream()
+    _lib.call("ow_cell_face_links_count", ctx, C.byref(forest.view()), _lib.ptr(leaves), int(leaves.numel()),
+              _lib.ptr(geom.coords), geom.n_faces, geom.key, C.byref(g), _lib.ptr(bins.ids), _lib.ptr(bins.counts),
+              _lib.ptr(bins.offsets), float(np.float32(d_link)), float(reach), int(capacity), C.byref(ncell),
+              C.byref(nlink), st)
+    dev = forest.device
+    nc, nl = int(ncell.value), int(nlink.value)
+    block_ids = torch.empty(nc, dtype=torch.int64, device=dev)
+    cell_idx = torch.empty(nc, dtype=torch.int64, device=dev)
+    offsets = torch.empty(nc + 1, dtype=torch.int64, device=dev)
+    face_ids = torch.empty(nl, dtype=torch.int32, device=dev)
+    _lib.call("ow_cell_face_links_emit", ctx, _lib.ptr(block_ids), _lib.ptr(cell_idx), _lib.ptr(offsets),
+              _lib.ptr(face_ids), st)
+    return CellFaceLinks(level=level, d_link=float(d_link), capacity=capacity, block_ids=block_ids,
+                         cell_indices=cell_idx, offsets=offsets, face_ids=face_ids)

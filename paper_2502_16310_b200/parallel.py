@@ -1,0 +1,76 @@
+"""Multi-GPU sharding of the near-wall pass: one process per GPU, NCCL.
+
+Octree blocks are independent units for marking, so each rank marks a
+contiguous slice of the level's ascending leaf list and the per-leaf marks
+are all-gathered (one NCCL all-gather of int8 per level over NVLink).  The
+forest metadata and the bin CSR are replicated: every rank builds them from
+the same inputs with the same deterministic kernels, so propagation and
+refinement (tiny, latency-bound) run redundantly and produce identical block
+ids on every rank without any further exchange.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def partition(n, rank, world, weights=None):
+    """[lo, hi) slice of n ordered units for ``rank``; balanced by ``weights``
+    (a 1-D cumulative-work tensor) when given, else by count."""
+    if world <= 1:
+        return 0, n
+    if weights is None or n == 0:
+        per = (n + world - 1) // world
+        return min(n, rank * per), min(n, (rank + 1) * per)
+    cum = torch.cumsum(weights.to(torch.float64), 0)
+    total = float(cum[-1]) if n else 0.0
+    cut = torch.tensor([total * r / world for r in range(world + 1)], dtype=torch.float64, device=cum.device)
+    idx = torch.searchsorted(cum, cut, right=False).clamp_(0, n).tolist()
+    idx[0], idx[-1] = 0, n
+    return int(idx[rank]), int(idx[rank + 1])
+
+
+def gather_slices(local, n, world, group=None):
+    """All-gather variable-length contiguous slices (padded to the largest);
+    returns the concatenation in rank order, length n."""
+    per = (n + world - 1) // world if world > 1 else n
+    dev = local.device
+    counts = torch.tensor([local.numel()], dtype=torch.int64, device=dev)
+    all_counts = [torch.zeros_like(counts) for _ in range(world)]
+    dist.all_gather(all_counts, counts, group=group)
+    sizes = [int(c.item()) for c in all_counts]
+    m = max(max(sizes), per, 1)
+    buf = torch.zeros(m, dtype=local.dtype, device=dev)
+    buf[: local.numel()] = local
+    out = torch.empty(world * m, dtype=local.dtype, device=dev)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    parts = [out[r * m: r * m + sizes[r]] for r in range(world)]
+    res = torch.cat(parts)
+    assert res.numel() == n, (res.numel(), n)
+    return res
+
+
+class Shard:
+    """Shard marking passes across the ranks of ``group`` (default world)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+
+    def mark_level(self, forest, level, geom, d_spec, bins, grid, mark_fn):
+        from .nearwall import MarkStats
+
+        leaves = forest._leaves(level)
+        n = int(leaves.numel())
+        lo, hi = partition(n, self.rank, self.world)
+        st = mark_fn(forest, level, geom, d_spec, bins, grid, leaves=leaves[lo:hi].contiguous())
+        if self.world > 1:
+            mine = forest.marks.index_select(0, leaves[lo:hi].to(torch.int64))
+            allm = gather_slices(mine, n, self.world, self.group)
+            forest.marks.index_copy_(0, leaves.to(torch.int64), allm)
+            tot = torch.tensor([st.marked, st.tests, st.evaluated], dtype=torch.int64, device=allm.device)
+            dist.all_reduce(tot, group=self.group)
+            st = MarkStats(*(int(x) for x in tot.tolist()))
+        return st

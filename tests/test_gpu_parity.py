@@ -1,0 +1,316 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden fixtures and the CPU oracle, bit-exact for every integer / boolean
+output (bins, marks, forest arrays, links, flags) and float32-exact for q."""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_util as gu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ow():
+    import paper_2502_16310_b200 as m
+    from paper_2502_16310_b200 import _build
+
+    _build.build()
+    return m
+
+
+def domain(ow, dim):
+    return ow.Aabb(np.zeros(dim), np.ones(dim))
+
+
+def geom_of(ow, g):
+    c = gu.geometry(g)
+    return ow.CoordListGeometry(c.shape[0], c)
+
+
+# --------------------------------------------------------------------------- predicate
+def test_predicate_triangle_bitexact(ow):
+    g = gu.load(gu.files("pred_tri")[0])
+    faces = np.ascontiguousarray(np.transpose(g["tri"], (1, 2, 0)))
+    from paper_2502_16310_b200.distance import near_pairs
+
+    got = near_pairs(g["pts"], faces, g["d"].astype(np.float32)).cpu().numpy()
+    np.testing.assert_array_equal(got, g["mask"])
+
+
+def test_predicate_edge_bitexact(ow):
+    g = gu.load(gu.files("pred_edge")[0])
+    faces = np.ascontiguousarray(np.transpose(g["seg"], (1, 2, 0)))
+    from paper_2502_16310_b200.distance import near_pairs
+
+    got = near_pairs(g["pts"], faces, g["d"].astype(np.float32)).cpu().numpy()
+    np.testing.assert_array_equal(got, g["mask"])
+
+
+# --------------------------------------------------------------------------- bins
+@pytest.mark.parametrize("path", gu.files("bins_"), ids=gu.ids(gu.files("bins_")))
+def test_fill_bins_bitexact(ow, path):
+    g = gu.load(path)
+    geom = geom_of(ow, g)
+    grid = ow.BinGrid(domain(ow, geom.dim), int(g["bins_per_axis"]))
+    h = None if np.isnan(g["spacing"]) else float(g["spacing"])
+    bins = ow.fill_bins(geom, grid, spacing=h, overlap_factor=10 ** 6)
+    ids, counts, offsets = bins.numpy()
+    np.testing.assert_array_equal(counts, g["counts"])
+    np.testing.assert_array_equal(offsets, g["offsets"])
+    np.testing.assert_array_equal(ids, g["ids"])
+
+
+# --------------------------------------------------------------------------- marking
+@pytest.mark.parametrize("path", gu.files("mark_"), ids=gu.ids(gu.files("mark_")))
+def test_marking_bitexact(ow, path):
+    g = gu.load(path)
+    geom = geom_of(ow, g)
+    dim = geom.dim
+    f = ow.init_root_grid(domain(ow, dim), (int(g["root"]),) * dim)
+    b = int(g["bins_per_axis"])
+    if b < 0:
+        n = ow.mark_near_wall_naive(f, 0, geom, float(g["d_spec"]))
+    else:
+        grid = ow.BinGrid(domain(ow, dim), b)
+        n = ow.mark_near_wall_binned(f, 0, geom, ow.fill_bins(geom, grid), grid, float(g["d_spec"]))
+    assert n == int(g["n_marked"])
+    np.testing.assert_array_equal(f.marks.cpu().numpy(), g["marks"])
+
+
+# --------------------------------------------------------------------------- pipelines
+@pytest.mark.parametrize("path", gu.files("pipe_"), ids=gu.ids(gu.files("pipe_")))
+def test_refine_near_wall_bitexact(ow, path):
+    g = gu.load(path)
+    geom = geom_of(ow, g)
+    dim = geom.dim
+    f = ow.init_root_grid(domain(ow, dim), (int(g["root"]),) * dim)
+    params = ow.NearWallParams(d_spec=float(g["d_spec"]), n_levels=int(g["n_levels"]),
+                               strategy=str(g["strategy"]), bins_per_axis=int(g["bins_per_axis"]))
+    res = ow.refine_near_wall(f, geom, params)
+    assert res.marked_detected == g["marked_detected"].tolist()
+    assert res.marked_refined == g["marked_refined"].tolist()
+    assert [t.stage for t in res.timings] == g["stages"].tolist()
+    assert f.n_blocks == int(g["n_blocks"])
+    np.testing.assert_array_equal(f._level, g["level"])
+    np.testing.assert_array_equal(f._coords, g["coords"])
+    np.testing.assert_array_equal(f._parent, g["parent"])
+    np.testing.assert_array_equal(f._first_child, g["first_child"])
+    np.testing.assert_array_equal(f.marks.cpu().numpy(), g["marks"])
+    assert f.blocks_per_level() == g["blocks_per_level"].tolist()
+    assert f.leaves_per_level() == g["leaves_per_level"].tolist()
+    if "bin_ids" in g:
+        ids, counts, offsets = res.bins.numpy()
+        np.testing.assert_array_equal(ids, g["bin_ids"])
+        np.testing.assert_array_equal(counts, g["bin_counts"])
+
+
+# --------------------------------------------------------------------------- forest units
+def test_forest_units_bitexact(ow):
+    g = gu.load(gu.files("forest_units")[0])
+    f = ow.init_root_grid(domain(ow, 2), (8, 8))
+    f.marks[[3, 17, 44]] = int(ow.RefineMark.MARKED)
+    ow.propagate_marks(f, 0, d_spec=0.3)
+    np.testing.assert_array_equal(f.marks.cpu().numpy(), g["prop8_marks"])
+
+    f = ow.init_root_grid(domain(ow, 3), (4, 4, 4))
+    f.marks[[5, 21, 42]] = int(ow.RefineMark.MARKED)
+    f.refine_marked(0)
+    lv1 = f.leaf_blocks_at(1)
+    f.marks[lv1[::5]] = int(ow.RefineMark.MARKED)
+    f.marks[[0, 63]] = int(ow.RefineMark.MARKED)
+    ow.propagate_marks(f, 0, d_spec=0.3, rounds=2)
+    np.testing.assert_array_equal(f.marks.cpu().numpy(), g["prop3d_marks"])
+    np.testing.assert_array_equal(f._coords, g["prop3d_coords"])
+
+    for dim, seed, rounds, root in ((2, 1, 3, 4), (2, 3, 4, 4), (3, 5, 3, 3), (3, 8, 4, 2)):
+        rng = np.random.default_rng(seed)
+        f = ow.init_root_grid(domain(ow, dim), (root,) * dim)
+        splits = []
+        for lv in range(rounds):
+            leaves = f.leaf_blocks_at(lv).cpu().numpy()
+            if len(leaves) == 0:
+                break
+            pick = leaves[rng.random(len(leaves)) < 0.4]
+            f.marks[torch.as_tensor(pick, device=f.device)] = int(ow.RefineMark.MARKED)
+            splits.append(f.refine_marked(lv))
+        p = f"rand{dim}d_s{seed}_"
+        assert splits == g[p + "splits"].tolist()
+        np.testing.assert_array_equal(f._level, g[p + "level"])
+        np.testing.assert_array_equal(f._coords, g[p + "coords"])
+        np.testing.assert_array_equal(f._parent, g[p + "parent"])
+        np.testing.assert_array_equal(f._first_child, g[p + "first_child"])
+
+
+def test_forest_growth_callback(ow):
+    """Capacity growth through the C callback keeps ids/coords intact."""
+    f = ow.Forest(domain(ow, 3), (2, 2, 2), capacity=8)
+    assert f.capacity >= 8
+    for lv in range(4):
+        leaves = f.leaf_blocks_at(lv)
+        f.marks[leaves] = int(ow.RefineMark.MARKED)
+        f.refine_marked(lv)
+    assert f.blocks_per_level() == [8, 64, 512, 4096, 32768]
+    assert f.capacity >= f.n_blocks
+
+
+# --------------------------------------------------------------------------- links
+@pytest.mark.parametrize("path", gu.files("links_"), ids=gu.ids(gu.files("links_")))
+def test_cell_face_links_bitexact(ow, path):
+    g = gu.load(path)
+    geom = geom_of(ow, g)
+    dim = geom.dim
+    f = ow.init_root_grid(domain(ow, dim), (int(g["root"]),) * dim)
+    if int(g["n_levels"]) > 1:
+        ow.refine_near_wall(f, geom, ow.NearWallParams(d_spec=float(g["d_spec"]), n_levels=int(g["n_levels"]),
+                                                       bins_per_axis=int(g["bins_refine"])))
+    np.testing.assert_array_equal(f._coords, g["coords"])
+    grid = ow.BinGrid(domain(ow, dim), int(g["bins_per_axis"]))
+    bins = ow.fill_bins(geom, grid)
+    dl = None if np.isnan(g["d_link_arg"]) else float(g["d_link_arg"])
+    err = str(g["error"])
+    if err:
+        with pytest.raises(ow.CapacityError) as ei:
+            ow.build_cell_face_links(f, geom, bins, grid, d_link=dl, capacity=int(g["capacity"]))
+        assert str(ei.value) == err
+        return
+    links = ow.build_cell_face_links(f, geom, bins, grid, d_link=dl, capacity=int(g["capacity"]))
+    assert links.d_link == float(g["d_link"])
+    np.testing.assert_array_equal(links.block_ids.cpu().numpy(), g["block_ids"])
+    np.testing.assert_array_equal(links.cell_indices.cpu().numpy(), g["cell_indices"])
+    np.testing.assert_array_equal(links.offsets.cpu().numpy(), g["offsets"])
+    np.testing.assert_array_equal(links.face_ids.cpu().numpy(), g["face_ids"])
+
+
+# --------------------------------------------------------------------------- STL import
+def test_stl_binary_and_ascii_import(ow, tmp_path):
+    from paper_2502_16310_b200 import shapes
+    from oracle import geometry as og
+
+    tris = shapes.icosphere_triangles(3)
+    data = shapes.binary_stl_bytes(tris)
+    got = ow.import_stl_bytes(data).coords_numpy()
+    np.testing.assert_array_equal(got, og.stl(data))
+    # ASCII round trip of the unit cube (test_acceptance.py criterion 10)
+    cube = np.array([[[0, 0, 0], [0, 1, 0], [1, 1, 0]], [[0, 0, 0], [1, 1, 0], [1, 0, 0]]], np.float64)
+    lines = ["solid c"]
+    for t in cube:
+        lines += ["facet normal 0 0 1", "outer loop"] + [f"vertex {p[0]} {p[1]} {p[2]}" for p in t]
+        lines += ["endloop", "endfacet"]
+    lines.append("endsolid c")
+    a = ow.import_stl_bytes("\n".join(lines).encode())
+    np.testing.assert_array_equal(a.coords_numpy(), np.transpose(cube.astype(np.float32), (1, 2, 0)))
+    with pytest.raises(ow.GeometryParseError):
+        ow.import_stl_bytes(data[:-25])
+
+
+def test_index_to_coords_gather(ow):
+    from oracle import geometry as og
+
+    ig = ow.generate_sphere((0.5, 0.5, 0.5), 0.3, 15, 18)
+    v, fc = og.latlon_sphere(0.5, 0.5, 0.5, 0.3, 15, 18)
+    np.testing.assert_array_equal(ig.vertices, v)
+    np.testing.assert_array_equal(ow.index_to_coords(ig).coords_numpy(), og.index_to_coords(v, fc))
+
+
+# --------------------------------------------------------------------------- errors
+def test_error_behaviour(ow):
+    c = np.zeros((2, 2, 1), np.float32)
+    c[0, :, 0], c[1, :, 0] = (0.01, 0.5), (0.99, 0.5)
+    g = ow.CoordListGeometry(2, c)
+    with pytest.raises(ow.CapacityError, match="overlap_factor"):
+        ow.fill_bins(g, ow.BinGrid(domain(ow, 2), 16), overlap_factor=10)
+    c[0, :, 0], c[1, :, 0] = (0.5, 0.5), (1.5, 0.5)
+    with pytest.raises(ow.InvalidParameterError, match="outside"):
+        ow.fill_bins(ow.CoordListGeometry(2, c), ow.BinGrid(domain(ow, 2), 2))
+    c[0, :, 0], c[1, :, 0] = (0.5, 0.5), (0.5, 0.5)
+    with pytest.raises(ow.InvalidParameterError, match="degenerate"):
+        ow.fill_bins(ow.CoordListGeometry(2, c), ow.BinGrid(domain(ow, 2), 2))
+    f = ow.init_root_grid(domain(ow, 2), (1, 1), max_level=1)
+    f.marks[0] = int(ow.RefineMark.MARKED)
+    f.refine_marked(0)
+    f.marks[f.leaf_blocks_at(1)] = int(ow.RefineMark.MARKED)
+    with pytest.raises(ow.InvalidParameterError, match="max level"):
+        f.refine_marked(1)
+    f = ow.init_root_grid(domain(ow, 2), (4, 4))
+    f.marks[3] = int(ow.RefineMark.INTERMEDIATE)
+    with pytest.raises(ow.InvalidParameterError, match="intermediate"):
+        f.refine_marked(0)
+    with pytest.raises(ow.InvalidParameterError):
+        ow.propagate_marks(f, 0, d_spec=0.1)
+
+
+def test_known_answers(ow):
+    f = ow.init_root_grid(domain(ow, 2), (4, 4))
+    assert f.face_neighbors(5) == [(4,), (6,), (1,), (9,)]
+    f.marks[5] = int(ow.RefineMark.MARKED)
+    assert f.refine_marked(0) == 1
+    assert list(f.block(5).children) == [16, 17, 18, 19]
+    assert f.face_neighbors(6)[0] == (17, 19)
+    assert f.face_neighbors(17)[1] == (6,)
+    c = f.cell_centers(0).cpu().numpy()
+    np.testing.assert_array_equal(c[:4, 0], np.array([0.03125, 0.09375, 0.15625, 0.21875], np.float32))
+    assert ow.check_near_triangle((0.5, 0.25, 0.05), (0, 0, 0), (1, 0, 0), (0, 1, 0), 0.1)
+    assert not ow.check_near_triangle((2, 2, 2), (0, 0, 0), (1, 0, 0), (0, 1, 0), 0.1)
+    assert ow.check_near_edge((0.5, 0.05), (0, 0), (1, 0), 0.1)
+
+
+# --------------------------------------------------------------------------- oracle-vs-GPU at other sizes
+@pytest.mark.parametrize("dim,seed,n_faces,root,d,B", [
+    (2, 101, 300, 8, 0.05, 4), (2, 102, 500, 16, 0.02, 16), (3, 103, 300, 6, 0.07, 3), (3, 104, 800, 8, 0.04, 8),
+])
+def test_pipeline_random_soups_vs_oracle(ow, dim, seed, n_faces, root, d, B):
+    from oracle import forest as of
+    from oracle import nearwall as on
+
+    rng = np.random.default_rng(seed)
+    anchors = rng.uniform(0.1, 0.9, (n_faces, dim))
+    coords = np.empty((dim, dim, n_faces), np.float32)
+    for j in range(dim):
+        coords[j] = (anchors + (rng.uniform(-0.04, 0.04, (n_faces, dim)) if j else 0.0)).T.astype(np.float32)
+    from oracle.geometry import first_degenerate
+
+    while first_degenerate(coords) >= 0:
+        coords[:, :, first_degenerate(coords)] += np.float32(1e-3)
+    fo = of.Forest(np.zeros(dim), np.ones(dim), (root,) * dim)
+    ro = on.refine_near_wall(fo, coords, d, n_levels=3, bins_per_axis=B)
+    geom = ow.CoordListGeometry(dim, coords)
+    fg = ow.init_root_grid(domain(ow, dim), (root,) * dim)
+    rg = ow.refine_near_wall(fg, geom, ow.NearWallParams(d_spec=d, n_levels=3, bins_per_axis=B))
+    assert rg.marked_detected == ro["marked_detected"]
+    assert rg.cell_face_tests == ro["cell_face_tests"]
+    np.testing.assert_array_equal(fg._coords, fo.coords)
+    np.testing.assert_array_equal(fg._first_child, fo.first_child)
+
+
+# --------------------------------------------------------------------------- lattice links vs oracle
+@pytest.mark.parametrize("case", ["circle", "icosphere"])
+def test_lattice_links_vs_oracle(ow, case):
+    from oracle import forest as of
+    from oracle import lattice as ol
+    from oracle import nearwall as on
+    from paper_2502_16310_b200 import shapes
+
+    if case == "circle":
+        ig = ow.generate_circle((0.5, 0.5), 0.25, 200)
+        coords = ow.index_to_coords(ig).coords_numpy()
+        dim, root, d, lat = 2, 8, 0.1, "D2Q9"
+    elif case == "icosphere":
+        coords = np.ascontiguousarray(np.transpose(shapes.icosphere_triangles(3).astype(np.float32), (1, 2, 0)))
+        dim, root, d, lat = 3, 4, 0.08, "D3Q19"
+    else:
+        from golden.make_golden import cube_triangles  # noqa: F401  (recipe only; reference not imported)
+        raise pytest.skip("covered by icosphere/circle")
+    fo = of.Forest(np.zeros(dim), np.ones(dim), (root,) * dim)
+    on.refine_near_wall(fo, coords, d, n_levels=3, bins_per_axis=4)
+    ref = ol.lattice_links(fo, coords, lat)
+    geom = ow.CoordListGeometry(dim, coords)
+    fg = ow.init_root_grid(domain(ow, dim), (root,) * dim)
+    ow.refine_near_wall(fg, geom, ow.NearWallParams(d_spec=d, n_levels=3, bins_per_axis=4))
+    ll = ow.build_lattice_links(fg, geom, ow.BinGrid(domain(ow, dim), 4), lat)
+    np.testing.assert_array_equal(ll.leaves.cpu().numpy(), ref["leaves"])
+    np.testing.assert_array_equal(ll.flags.cpu().numpy().view(np.uint32), ref["flags"])
+    np.testing.assert_array_equal(ll.cells.cpu().numpy(), ref["boundary"])
+    np.testing.assert_array_equal(ll.q.cpu().numpy(), ref["q"])
+    assert ll.n_boundary > 0
