@@ -100,7 +100,10 @@ class Forest:
 
     def _grow(self, _user, view_p, need):
         try:
-            n = self._n
+            # the C side may already have appended blocks during this refine
+            # call: its view holds the live count, not self._n
+            n = int(view_p.contents.n_blocks)
+            self._n = n
             new_cap = max(int(need), 2 * self._cap)
             old = (self._level_t, self._coord, self._parent_t, self._first_child_t, self._marks)
             self._alloc(new_cap)
