@@ -66,60 +66,59 @@ def make_input(cfg):
 
 # ---------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """NVML sampling of SM clock + throttle reasons during the timed region."""
+    """SM clock + throttle reasons sampled by an ``nvidia-smi -lms`` child
+    process during the timed region (a separate process: no GIL contention
+    with the host side of the pipeline being timed)."""
 
-    def __init__(self, index, period=0.01):
-        self.index, self.period = index, period
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index, period_ms=20):
+        self.index, self.period_ms = index, period_ms
         self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._stop = threading.Event()
-        self._t = None
+        self.proc = None
 
     def __enter__(self):
+        import subprocess
+        import tempfile
+
+        self.out = tempfile.TemporaryFile(mode="w+")
         try:
-            import pynvml
-
-            pynvml.nvmlInit()
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self.nv = pynvml
-            names = {
-                "hw_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
-                "sw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
-                "hw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
-                "sw_power_cap": getattr(pynvml, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
-                "hw_power_brake_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80),
-            }
-            self.names = names
-
-            def run():
-                while not self._stop.is_set():
-                    try:
-                        self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                        r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h) if hasattr(
-                            self.nv, "nvmlDeviceGetCurrentClocksEventReasons") else \
-                            self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
-                        for k, bit in self.names.items():
-                            if r & bit:
-                                self.reasons.add(k)
-                    except Exception:
-                        pass
-                    time.sleep(self.period)
-
-            self._t = threading.Thread(target=run, daemon=True)
-            self._t.start()
+            dev = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[self.index] \
+                if os.environ.get("CUDA_VISIBLE_DEVICES") else str(self.index)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", dev, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 f"-lms={self.period_ms}"], stdout=self.out, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)  # let the sampler start before the timed region
         except Exception as e:  # pragma: no cover
             log("clock sampling unavailable:", e)
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join()
+        if self.proc:
+            time.sleep(0.05)
+            self.proc.terminate()
+            self.proc.wait()
+            self.out.seek(0)
+            for line in self.out.read().splitlines():
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) != 6:
+                    continue
+                try:
+                    self.samples.append(float(parts[0]))
+                    self.max_mhz = float(parts[1])
+                except ValueError:
+                    continue
+                for name, v in zip(self.NAMES, parts[2:]):
+                    if v.lower().startswith("active"):
+                        self.reasons.add(name)
 
     def summary(self):
         return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
-                "sm_max_mhz": float(self.max_mhz) if self.max_mhz else None,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "sampler": f"nvidia-smi -lms {self.period_ms} (child process) over the timed region"}
 
 
 # ---------------------------------------------------------------------------- GPU arm
@@ -156,7 +155,7 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         geom = import_geom(records)
         forest = ow.init_root_grid(dom, (cfg["root"],) * dim, capacity=8 * cfg["root"] ** dim)
         res = ow.refine_near_wall(forest, geom, params, shard=shard)
-        ll = ow.build_lattice_links(forest, geom, grid, cfg["lattice"])
+        ll = ow.build_lattice_links(forest, geom, None, cfg["lattice"])
         return res, forest, ll
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
@@ -189,6 +188,8 @@ def gpu_arm(args, cfg, rank, world, local_rank):
             ev[k][1].record()
         barrier()
     launches = _lib.launches() - launches0
+    for s in res.timings:
+        log("stage", s.csv_row())
     prof = _lib.profile_read()
     _lib.profile(False)
     ms = sum(a.elapsed_time(b) for a, b in ev)
@@ -204,10 +205,12 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
         h2d = d2h = 0
+        pinned = []
         barrier()
-        for k in range(args.steps):
+        for k in range(-1, args.steps):  # k = -1: untimed, sizes the pinned result buffers
             l2_flush()
-            ev2[k][0].record()
+            if k >= 0:
+                ev2[k][0].record()
             if text:
                 res, forest, ll = step(None)
                 h2d = 0
@@ -217,9 +220,19 @@ def gpu_arm(args, cfg, rank, world, local_rank):
                 res, forest, ll = step(rd)
             outs = [forest.level_tensor, forest.coords_tensor, forest._parent_t[: forest.n_blocks],
                     forest._first_child_t[: forest.n_blocks], forest.marks, ll.flags, ll.cells, ll.q]
-            host = [o.to("cpu") for o in outs]
-            d2h = sum(o.numel() * o.element_size() for o in host)
-            ev2[k][1].record()
+            d2h = 0
+            for i, o in enumerate(outs):  # pinned host result buffers, reused across steps
+                nbytes = o.numel() * o.element_size()
+                if i >= len(pinned) or pinned[i].numel() < nbytes:
+                    if i < len(pinned):
+                        pinned[i] = torch.empty(2 * nbytes, dtype=torch.uint8, pin_memory=True)
+                    else:
+                        pinned.append(torch.empty(2 * nbytes + 64, dtype=torch.uint8, pin_memory=True))
+                pinned[i][:nbytes].copy_(o.contiguous().view(-1).view(torch.uint8), non_blocking=True)
+                d2h += nbytes
+            torch.cuda.current_stream().synchronize()
+            if k >= 0:
+                ev2[k][1].record()
         barrier()
         ms2 = sum(a.elapsed_time(b) for a, b in ev2)
         t2 = torch.tensor([ms2], dtype=torch.float64, device=dev)

@@ -63,6 +63,10 @@ enum ow_slot {
   SLOT_ABIN_IDS,       // AABB-overlap bin CSR (lattice candidates)
   SLOT_ABIN_CNT,
   SLOT_ABIN_OFF,
+  SLOT_LAT_REC,        // packed 64-byte face records (lattice candidates)
+  SLOT_LAT_CCNT,       // candidates per finest block
+  SLOT_LAT_BOFFS,      // boundary-row offsets per candidate block
+  SLOT_LAT_TEMP,       // q rows staging
   SLOT_MISC,
   SLOT_COUNT
 };
@@ -112,7 +116,8 @@ struct ow_ctx {
   int8_t lat_dir[27 * 3];
   const float* lat_coords;
   const int32_t* lat_leaves_ptr;
-  int64_t lat_key;
+  uint32_t* lat_flags;
+  int64_t lat_key, lat_ncb;
   ow_forest lat_forest;
   ow_grid lat_grid;
   int64_t abin_key;

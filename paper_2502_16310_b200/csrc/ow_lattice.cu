@@ -3,13 +3,18 @@
 // checker and DESIGN.md §Lattice links the definition).
 //
 // Candidates come from an AABB-overlap bin CSR (a face is stored in every bin
-// its float32 AABB touches), built once per (geometry, grid).  A CTA per
-// finest leaf block gathers the faces of the bins under its box grown by two
-// cells, visiting each face once (in the first bin of the overlap range), and
-// tests every (cell, direction, face) triple: exact float32 link-AABB overlap,
-// then Moller-Trumbore (3D) / segment-segment (2D) with a fixed op order.
-// Pass 1 writes the per-cell flag words and per-block boundary counts; pass 2
-// re-runs the blocks holding boundary cells and writes q rows in cell order.
+// its float32 AABB touches) plus a packed 64-byte record per face (v0, edge
+// vectors, float32 box, first bin), built once per (geometry, grid).
+//   k_lat_count : warp per finest leaf block, counts the faces whose box meets
+//                 the block box grown by two cells (each face once: in the
+//                 first bin of its range ∩ the block's range).
+//   scan        : compacts the blocks with candidates (typically ~1/4).
+//   k_lattice   : CTA per candidate block; stages the candidates in shared
+//                 memory and sweeps every (cell, direction) link: exact float32
+//                 link-AABB overlap, then Moller-Trumbore (3D) / segment-
+//                 segment (2D) with a fixed op order; writes flag words, the
+//                 block's boundary-cell count and its q rows to a staging area.
+//   scan + k_lat_emit : boundary rows compacted in (block, cell) order.
 #include "ow_scan.cuh"
 #include <string.h>
 
@@ -18,30 +23,38 @@ namespace {
 using ow::scan;
 
 constexpr int LAT_THREADS = 256;
-constexpr int LAT_STAGE = 256;
 constexpr int QMAX = 27;
+constexpr int LAT_CAP = 512;  // staged faces per sweep
+constexpr int LAT_ITEMS = (64 * (QMAX - 1) + LAT_THREADS - 1) / LAT_THREADS;
+constexpr int CNT_WARPS = 8;
 
 struct Dirs {
   int8_t c[QMAX][3];
 };
 
 template <int D>
-__device__ __forceinline__ void face_box(const float* __restrict__ c, int64_t n, int64_t f, float* lo, float* hi) {
+__device__ __forceinline__ void face_verts(const float* __restrict__ c, int64_t n, int64_t f, float v[3][3]) {
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+#pragma unroll
+    for (int a = 0; a < D; ++a) v[j][a] = c[((int64_t)j * D + a) * n + f];
+}
+
+template <int D>
+__device__ __forceinline__ void vert_box(const float v[3][3], float* lo, float* hi) {
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    float mn = c[(int64_t)a * n + f], mx = mn;
+    lo[a] = v[0][a];
+    hi[a] = v[0][a];
 #pragma unroll
     for (int j = 1; j < D; ++j) {
-      float x = c[((int64_t)j * D + a) * n + f];
-      mn = fminf(mn, x);
-      mx = fmaxf(mx, x);
+      lo[a] = fminf(lo[a], v[j][a]);
+      hi[a] = fmaxf(hi[a], v[j][a]);
     }
-    lo[a] = mn;
-    hi[a] = mx;
   }
 }
 
-// ---- AABB-overlap bin CSR -------------------------------------------------
+// ---- AABB-overlap bin CSR + packed face records ------------------------------
 template <int D>
 __device__ __forceinline__ int64_t abin_range(const GridC& g, const float* lo, const float* hi, int* blo, int* ext) {
   int64_t v = 1;
@@ -60,24 +73,43 @@ struct AbinCountLoad {
   const float* c;
   int64_t n;
   __device__ int64_t operator()(int64_t f) const {
-    float lo[3], hi[3];
+    float v[3][3], lo[3], hi[3];
     int bl[3], ex[3];
-    face_box<D>(c, n, f, lo, hi);
+    face_verts<D>(c, n, f, v);
+    vert_box<D>(v, lo, hi);
     return abin_range<D>(g, lo, hi, bl, ex);
   }
 };
 
+// record layout (float4 x 4):
+//  3D: [v0.xyz lo.x] [e1.xyz lo.y] [e2.xyz lo.z] [hi.xyz binlo]
+//  2D: [a.xy s.xy]   [lo.xy hi.xy] [binlo 0 0 0] [0 0 0 0]
+// binlo packs the face's first bin per axis, 10 bits each (B <= 1024).
 template <int D>
 __global__ void k_abin_emit(GridC g, const float* __restrict__ c, int64_t n, const int64_t* foff, uint32_t* keys,
-                            int32_t* vals, int32_t* counts) {
+                            int32_t* vals, int32_t* counts, float4* rec) {
   int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= n) return;
-  float lo[3], hi[3];
-  int bl[3], ex[3];
-  face_box<D>(c, n, f, lo, hi);
-  int64_t v = abin_range<D>(g, lo, hi, bl, ex);
+  float v[3][3], lo[3], hi[3];
+  int bl[3] = {0, 0, 0}, ex[3];
+  face_verts<D>(c, n, f, v);
+  vert_box<D>(v, lo, hi);
+  int64_t cnt = abin_range<D>(g, lo, hi, bl, ex);
+  unsigned packed = (unsigned)bl[0] | ((unsigned)bl[1] << 10) | ((unsigned)(D == 3 ? bl[2] : 0) << 20);
+  float pk = __uint_as_float(packed);
+  if (D == 3) {
+    rec[4 * f + 0] = make_float4(v[0][0], v[0][1], v[0][2], lo[0]);
+    rec[4 * f + 1] = make_float4(FSUB(v[1][0], v[0][0]), FSUB(v[1][1], v[0][1]), FSUB(v[1][2], v[0][2]), lo[1]);
+    rec[4 * f + 2] = make_float4(FSUB(v[2][0], v[0][0]), FSUB(v[2][1], v[0][1]), FSUB(v[2][2], v[0][2]), lo[2]);
+    rec[4 * f + 3] = make_float4(hi[0], hi[1], hi[2], pk);
+  } else {
+    rec[4 * f + 0] = make_float4(v[0][0], v[0][1], FSUB(v[1][0], v[0][0]), FSUB(v[1][1], v[0][1]));
+    rec[4 * f + 1] = make_float4(lo[0], lo[1], hi[0], hi[1]);
+    rec[4 * f + 2] = make_float4(pk, 0.0f, 0.0f, 0.0f);
+    rec[4 * f + 3] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  }
   int64_t pos = foff[f];
-  for (int64_t k = 0; k < v; ++k) {
+  for (int64_t k = 0; k < cnt; ++k) {
     int64_t rem = k, lin = 0, mul = 1;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
@@ -95,8 +127,12 @@ template <int D>
 int build_abins(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, int64_t key, cudaStream_t s) {
   int64_t nb = 1;
   for (int a = 0; a < D; ++a) nb *= g.B;
+  if (g.B > 1024) {
+    ow_set_error("lattice candidate grid limited to 1024 bins per axis");
+    return OW_ERR_INVALID;
+  }
   if (key >= 0 && ctx->abin_key == key && ctx->abin_B == g.B && ctx->abin_dim == D) return OW_OK;
-  void *pfo, *pcnt, *poff;
+  void *pfo, *pcnt, *poff, *prec;
   OW_TRY(ow_slot(ctx, SLOT_LAT_BOFF, 8 * (size_t)(n + 1), s, &pfo));
   OW_TRY(scan(ctx, AbinCountLoad<D>{g, c, n}, ow::StoreExcl<int64_t>{(int64_t*)pfo}, n, ctx->d_small + 32, s));
   int64_t E;
@@ -112,9 +148,10 @@ int build_abins(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, int64_t 
   OW_TRY(ow_slot(ctx, SLOT_PAIR_VAL1, 4 * (size_t)E, s, &pv1));
   OW_TRY(ow_slot(ctx, SLOT_ABIN_CNT, 4 * (size_t)nb, s, &pcnt));
   OW_TRY(ow_slot(ctx, SLOT_ABIN_OFF, 4 * (size_t)nb, s, &poff));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_REC, 64 * (size_t)n, s, &prec));
   OW_CUDA(cudaMemsetAsync(pcnt, 0, 4 * (size_t)nb, s));
   k_abin_emit<D><<<ow_blocks(n, 256), 256, 0, s>>>(g, c, n, (const int64_t*)pfo, (uint32_t*)pk0, (int32_t*)pv0,
-                                                  (int32_t*)pcnt);
+                                                  (int32_t*)pcnt, (float4*)prec);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   int bits = 0;
@@ -132,30 +169,123 @@ int build_abins(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, int64_t 
   return OW_OK;
 }
 
-// ---- link kernel -------------------------------------------------------------
+// ---- shared geometry of one finest block ---------------------------------------
+struct BlockFrame {
+  double blo[3];
+  float h32[3], glo[3], ghi[3];  // cell size, outward-rounded box grown by two cells
+  int rlo[3], rhi[3];            // bin range of the grown box
+};
+
+template <int D>
+__device__ __forceinline__ BlockFrame block_frame(const ForestC& F, const GridC& g, int id) {
+  BlockFrame b;
+  const int L = F.level[id];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    b.h32[a] = b.glo[a] = b.ghi[a] = 0.0f;
+    b.rlo[a] = b.rhi[a] = 0;
+    b.blo[a] = 0.0;
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double q = block_len(F, a, L);
+    b.blo[a] = DADD(F.dmin[a], DMUL((double)F.coord[a][id], q));
+    double bhi = DADD(b.blo[a], q);
+    double h64 = q / 4.0;  // exact (power-of-two scale)
+    b.h32[a] = __double2float_rn(h64);
+    b.glo[a] = __double2float_rd(b.blo[a] - 2.0 * h64);
+    b.ghi[a] = __double2float_ru(bhi + 2.0 * h64);
+    b.rlo[a] = bin_axis(b.glo[a], g.min32[a], g.len32[a], g.B);
+    b.rhi[a] = bin_axis(b.ghi[a], g.min32[a], g.len32[a], g.B);
+  }
+  return b;
+}
+
+// candidate test on a packed record: face box meets the grown box, and this
+// is the face's first bin inside the block's range
+template <int D>
+__device__ __forceinline__ bool is_candidate(const float4* __restrict__ rec, int f, const BlockFrame& b,
+                                             const int* bx) {
+  float lo[3], hi[3];
+  unsigned pk;
+  if (D == 3) {
+    float4 r0 = rec[4 * f], r1 = rec[4 * f + 1], r2 = rec[4 * f + 2], r3 = rec[4 * f + 3];
+    lo[0] = r0.w, lo[1] = r1.w, lo[2] = r2.w;
+    hi[0] = r3.x, hi[1] = r3.y, hi[2] = r3.z;
+    pk = __float_as_uint(r3.w);
+  } else {
+    float4 r1 = rec[4 * f + 1], r2 = rec[4 * f + 2];
+    lo[0] = r1.x, lo[1] = r1.y, hi[0] = r1.z, hi[1] = r1.w;
+    pk = __float_as_uint(r2.x);
+  }
+  bool ok = true;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    int fl = (int)((pk >> (10 * a)) & 1023u);
+    ok &= lo[a] <= b.ghi[a] && hi[a] >= b.glo[a] && max(fl, b.rlo[a]) == bx[a];
+  }
+  return ok;
+}
+
 struct LatArgs {
   ForestC F;
   GridC g;
   Dirs dirs;
   int nq;
   const int32_t* leaves;
-  const float* c;
-  int64_t n;
+  int64_t n_leaves;
+  const float4* rec;
   const int32_t* ab_ids;
   const int32_t* ab_cnt;
   const int32_t* ab_off;
-  uint32_t* flags;    // pass 1 out [n_leaves * C]
-  int32_t* bcount;    // pass 1 out [n_leaves]
-  const int64_t* boff;  // pass 2 in
-  int64_t* cells_out;   // pass 2 out
-  float* q_out;         // pass 2 out
+  int32_t* cand_cnt;       // [n_leaves]
+  int32_t* cand_blocks;    // [n_leaves] compacted positions
+  const int64_t* n_cb;     // device scalar
+  uint32_t* flags;         // [n_leaves * C]
+  int32_t* bcount;         // [n_leaves] boundary cells per candidate block
+  const int64_t* boff;     // [n_leaves]
+  float* temp;             // [n_cb * C * nq] q rows (staging)
+  int64_t* cells_out;
+  float* q_out;
 };
 
-// Moller-Trumbore, fixed op order (oracle/lattice.py:mt_hits)
-__device__ __forceinline__ bool mt_hit(const float* x, const float* dv, const float* v0, const float* v1,
-                                       const float* v2, float* tout) {
-  float e1[3] = {FSUB(v1[0], v0[0]), FSUB(v1[1], v0[1]), FSUB(v1[2], v0[2])};
-  float e2[3] = {FSUB(v2[0], v0[0]), FSUB(v2[1], v0[1]), FSUB(v2[2], v0[2])};
+template <int D>
+__global__ void __launch_bounds__(CNT_WARPS * 32) k_lat_count(LatArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t pos = (int64_t)blockIdx.x * CNT_WARPS + (threadIdx.x >> 5);
+  if (pos >= A.n_leaves) return;
+  const BlockFrame b = block_frame<D>(A.F, A.g, A.leaves[pos]);
+  int count = 0;
+  for (int bz = b.rlo[2]; bz <= b.rhi[2]; ++bz)
+    for (int by = b.rlo[1]; by <= b.rhi[1]; ++by)
+      for (int bx0 = b.rlo[0]; bx0 <= b.rhi[0]; ++bx0) {
+        int bx[3] = {bx0, by, bz};
+        int64_t lin = bx0 + (int64_t)A.g.B * (by + (int64_t)A.g.B * bz);
+        const int32_t* src = A.ab_ids + A.ab_off[lin];
+        const int cnt = A.ab_cnt[lin];
+        for (int j0 = 0; j0 < cnt; j0 += 32) {
+          bool ok = j0 + lane < cnt && is_candidate<D>(A.rec, src[j0 + lane], b, bx);
+          count += __popc(__ballot_sync(0xffffffffu, ok));
+        }
+      }
+  if (lane == 0) A.cand_cnt[pos] = count;
+}
+
+struct CandLoad {
+  const int32_t* c;
+  __device__ int64_t operator()(int64_t i) const { return c[i] > 0; }
+};
+struct CandStore {
+  int32_t* out;
+  __device__ void operator()(int64_t i, int64_t e, int64_t v) const {
+    if (v) out[e] = (int32_t)i;
+  }
+};
+
+// Moller-Trumbore, fixed op order (oracle/lattice.py:mt_hits); e1 = v1 - v0,
+// e2 = v2 - v0 were formed by the same float32 subtractions at packing time.
+__device__ __forceinline__ bool mt_hit_e(const float* x, const float* dv, const float* v0, const float* e1,
+                                         const float* e2, float* tout) {
   float px = FSUB(FMUL(dv[1], e2[2]), FMUL(dv[2], e2[1]));
   float py = FSUB(FMUL(dv[2], e2[0]), FMUL(dv[0], e2[2]));
   float pz = FSUB(FMUL(dv[0], e2[1]), FMUL(dv[1], e2[0]));
@@ -175,148 +305,212 @@ __device__ __forceinline__ bool mt_hit(const float* x, const float* dv, const fl
   return true;
 }
 
-// segment-segment (oracle/lattice.py:seg_hits)
-__device__ __forceinline__ bool seg_hit(const float* x, const float* dv, const float* a, const float* b, float* tout) {
-  float sx = FSUB(b[0], a[0]), sy = FSUB(b[1], a[1]);
-  float den = FSUB(FMUL(dv[0], sy), FMUL(dv[1], sx));
+// segment-segment (oracle/lattice.py:seg_hits) with s = b - a pre-formed
+__device__ __forceinline__ bool seg_hit_s(const float* x, const float* dv, const float* a, const float* sv,
+                                          float* tout) {
+  float den = FSUB(FMUL(dv[0], sv[1]), FMUL(dv[1], sv[0]));
   if (den == 0.0f) return false;
   float qx = FSUB(a[0], x[0]), qy = FSUB(a[1], x[1]);
-  float t = FDIV(FSUB(FMUL(qx, sy), FMUL(qy, sx)), den);
+  float t = FDIV(FSUB(FMUL(qx, sv[1]), FMUL(qy, sv[0])), den);
   float s = FDIV(FSUB(FMUL(qx, dv[1]), FMUL(qy, dv[0])), den);
   if (!(t >= 0.0f) || !(t <= 1.0f) || !(s >= 0.0f) || !(s <= 1.0f)) return false;
   *tout = t;
   return true;
 }
 
-template <int D, bool EMIT>
+template <int D>
 __global__ void __launch_bounds__(LAT_THREADS) k_lattice(LatArgs A) {
   constexpr int C = D == 3 ? 64 : 16;
+  constexpr int NF = D == 3 ? 15 : 8;  // staged floats per face: v0|a, e1|s, (e2), lo, hi
   __shared__ float s_cen[C][D];
-  __shared__ float s_h[3];
-  __shared__ int s_cand[LAT_STAGE];
+  __shared__ float s_dv[QMAX][D];
+  __shared__ float s_fv[NF][LAT_CAP];
   __shared__ int s_ncand;
   __shared__ unsigned s_flag[C];
-  __shared__ unsigned s_q[C][QMAX];  // float bits of min t (t >= 0 => int order)
-  const ForestC& F = A.F;
-  const int64_t pos = blockIdx.x;
-  if (EMIT && A.bcount[pos] == 0) return;
+  const int64_t r = blockIdx.x;
+  if (r >= *A.n_cb) return;
+  const int64_t pos = A.cand_blocks[r];
   const int id = A.leaves[pos];
+  const ForestC& F = A.F;
   const int L = F.level[id];
   const int tid = threadIdx.x;
-  double blo[3], bhi[3], h64[3];
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    double q = block_len(F, a, L);
-    blo[a] = DADD(F.dmin[a], DMUL((double)F.coord[a][id], q));
-    bhi[a] = DADD(blo[a], q);
-    h64[a] = q / 4.0;  // exact (power-of-two scale)
-  }
+  const BlockFrame b = block_frame<D>(F, A.g, id);
+  const int nq = A.nq, nd = nq - 1, work = C * nd;
   if (tid < C) {
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       double q = block_len(F, a, L);
       double u = ((double)((tid >> (2 * a)) & 3) + 0.5) / 4.0;
-      s_cen[tid][a] = __double2float_rn(DADD(blo[a], DMUL(u, q)));
+      s_cen[tid][a] = __double2float_rn(DADD(b.blo[a], DMUL(u, q)));
     }
     s_flag[tid] = 0u;
-    for (int i = 0; i < QMAX; ++i) s_q[tid][i] = 0x7f800000u;  // +inf
   }
-  if (tid < D) s_h[tid] = __double2float_rn(h64[tid]);
-  // grown block box (two cells) and its bin range, padded by one bin
-  double glo[3], ghi[3];
-  int rlo[3], rhi[3];
+  if (tid < nq) {
 #pragma unroll
-  for (int a = 0; a < D; ++a) {
-    glo[a] = blo[a] - 2.0 * h64[a];
-    ghi[a] = bhi[a] + 2.0 * h64[a];
-    rlo[a] = max(bin_axis(__double2float_rd(glo[a]), A.g.min32[a], A.g.len32[a], A.g.B) - 1, 0);
-    rhi[a] = min(bin_axis(__double2float_ru(ghi[a]), A.g.min32[a], A.g.len32[a], A.g.B) + 1, A.g.B - 1);
+    for (int a = 0; a < D; ++a) s_dv[tid][a] = FMUL((float)A.dirs.c[tid][a], b.h32[a]);  // exact: c in {-1,0,1}
+  }
+  if (tid == 0) s_ncand = 0;
+  // this thread's links (cell, direction), packed cell * 32 + direction
+  const float inv_nd = 1.0f / (float)nd;
+  int item[LAT_ITEMS];
+  float tmin[LAT_ITEMS];
+  unsigned hitmask = 0;
+#pragma unroll
+  for (int k = 0; k < LAT_ITEMS; ++k) {
+    const int it = tid + k * LAT_THREADS;
+    const int ci = (int)(((float)it + 0.5f) * inv_nd);  // exact for it < 2^16
+    item[k] = it < work ? ci * 32 + 1 + (it - ci * nd) : -1;
+    tmin[k] = INFINITY;
   }
   __syncthreads();
-  const int nq = A.nq;
-  const int work_cd = C * (nq - 1);
-  int bx[3];
-  const int nx = rhi[0] - rlo[0] + 1, ny = rhi[1] - rlo[1] + 1, nz = D == 3 ? rhi[2] - rlo[2] + 1 : 1;
-  for (int bk = 0; bk < nx * ny * nz; ++bk) {
-    bx[0] = rlo[0] + bk % nx;
-    bx[1] = rlo[1] + (bk / nx) % ny;
-    bx[2] = D == 3 ? rlo[2] + bk / (nx * ny) : 0;
-    int64_t lin = bx[0] + (int64_t)A.g.B * (bx[1] + (int64_t)A.g.B * bx[2]);
-    const int32_t* src = A.ab_ids + A.ab_off[lin];
-    const int cnt = A.ab_cnt[lin];
-    for (int base = 0; base < cnt; base += LAT_STAGE) {
-      if (tid == 0) s_ncand = 0;
-      __syncthreads();
-      for (int j = base + tid; j < min(cnt, base + LAT_STAGE); j += LAT_THREADS) {
-        int f = src[j];
-        float lo[3], hi[3];
-        face_box<D>(A.c, A.n, f, lo, hi);
-        bool ok = true, first = true;
+
+  auto sweep = [&](int ncand) {
 #pragma unroll
-        for (int a = 0; a < D; ++a) {
-          ok &= (double)lo[a] <= ghi[a] && (double)hi[a] >= glo[a];
-          // visit the face only in the first bin of (its bin range ∩ ours)
-          int fl = max(bin_axis(lo[a], A.g.min32[a], A.g.len32[a], A.g.B), rlo[a]);
-          first &= fl == bx[a];
-        }
-        if (ok && first) s_cand[atomicAdd(&s_ncand, 1)] = f;
+    for (int k = 0; k < LAT_ITEMS; ++k) {
+      if (item[k] < 0) break;
+      const int ci = item[k] >> 5, di = item[k] & 31;
+      float x[3], dv[3], llo[3], lhi[3];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        x[a] = s_cen[ci][a];
+        dv[a] = s_dv[di][a];
+        float e = FADD(x[a], dv[a]);
+        llo[a] = fminf(x[a], e);
+        lhi[a] = fmaxf(x[a], e);
       }
-      __syncthreads();
-      const int ncand = s_ncand;
-      for (int k = tid; k < work_cd * ncand; k += LAT_THREADS) {
-        int cd = k / ncand, j = k - cd * ncand;
-        int ci = cd / (nq - 1), di = 1 + cd % (nq - 1);
-        int f = s_cand[j];
-        float x[3], dv[3], lo[3], hi[3];
+      for (int j = 0; j < ncand; ++j) {
         bool ov = true;
-        face_box<D>(A.c, A.n, f, lo, hi);
+#pragma unroll
+        for (int a = 0; a < D; ++a) ov &= s_fv[NF - 2 * D + a][j] <= lhi[a] && s_fv[NF - D + a][j] >= llo[a];
+        if (!ov) continue;
+        float v0[3], e1[3], e2[3], t;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
-          x[a] = s_cen[ci][a];
-          dv[a] = FMUL((float)A.dirs.c[di][a], s_h[a]);
-          float e = FADD(x[a], dv[a]);
-          float l = fminf(x[a], e), u = fmaxf(x[a], e);
-          ov &= lo[a] <= u && hi[a] >= l;
+          v0[a] = s_fv[a][j];
+          e1[a] = s_fv[D + a][j];
+          if (D == 3) e2[a] = s_fv[6 + a][j];
         }
-        if (!ov) continue;
-        float v[3][3];
-#pragma unroll
-        for (int jj = 0; jj < D; ++jj)
-#pragma unroll
-          for (int a = 0; a < D; ++a) v[jj][a] = A.c[((int64_t)jj * D + a) * A.n + f];
-        float t;
-        bool hit = D == 3 ? mt_hit(x, dv, v[0], v[1], v[2], &t) : seg_hit(x, dv, v[0], v[1], &t);
+        bool hit = D == 3 ? mt_hit_e(x, dv, v0, e1, e2, &t) : seg_hit_s(x, dv, v0, e1, &t);
         if (hit) {
           t = FADD(t, 0.0f);  // -0 -> +0
-          atomicOr(&s_flag[ci], 1u << di);
-          if (EMIT) atomicMin(&s_q[ci][di], __float_as_uint(t));
+          hitmask |= 1u << k;
+          tmin[k] = fminf(tmin[k], t);
         }
       }
-      __syncthreads();
     }
+  };
+
+  for (int bz = b.rlo[2]; bz <= b.rhi[2]; ++bz)
+    for (int by = b.rlo[1]; by <= b.rhi[1]; ++by)
+      for (int bx0 = b.rlo[0]; bx0 <= b.rhi[0]; ++bx0) {
+        int bx[3] = {bx0, by, bz};
+        int64_t lin = bx0 + (int64_t)A.g.B * (by + (int64_t)A.g.B * bz);
+        const int32_t* src = A.ab_ids + A.ab_off[lin];
+        const int cnt = A.ab_cnt[lin];
+        for (int base = 0; base < cnt; base += LAT_THREADS) {
+          if (s_ncand > LAT_CAP - LAT_THREADS) {  // uniform: read after a barrier
+            sweep(s_ncand);
+            __syncthreads();
+            if (tid == 0) s_ncand = 0;
+            __syncthreads();
+          }
+          const int j = base + tid;
+          if (j < cnt) {
+            const int f = src[j];
+            if (is_candidate<D>(A.rec, f, b, bx)) {
+              const int k = atomicAdd(&s_ncand, 1);
+              const float4* R = A.rec + 4 * (int64_t)f;
+              if (D == 3) {
+                float4 r0 = R[0], r1 = R[1], r2 = R[2], r3 = R[3];
+                float fv[15] = {r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r2.x, r2.y, r2.z,
+                                r0.w, r1.w, r2.w, r3.x, r3.y, r3.z};
+#pragma unroll
+                for (int q = 0; q < NF; ++q) s_fv[q][k] = fv[q];
+              } else {
+                float4 r0 = R[0], r1 = R[1];
+                float fv[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+                for (int q = 0; q < NF; ++q) s_fv[q][k] = fv[q];
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+  if (s_ncand > 0) sweep(s_ncand);
+#pragma unroll
+  for (int k = 0; k < LAT_ITEMS; ++k) {
+    if (item[k] < 0 || !((hitmask >> k) & 1)) continue;
+    atomicOr(&s_flag[item[k] >> 5], 1u << (item[k] & 31));
   }
-  if (!EMIT) {
-    if (tid < C) A.flags[pos * C + tid] = s_flag[tid];
-    if (tid < 32) {
-      int nb = 0;
-      for (int c0 = tid; c0 < C; c0 += 32) nb += s_flag[c0] != 0;
-      for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
-      if (tid == 0) A.bcount[pos] = nb;
-    }
-    return;
+  __syncthreads();
+  // q rows of this block (staging, all Q entries of boundary cells)
+#pragma unroll
+  for (int k = 0; k < LAT_ITEMS; ++k) {
+    if (item[k] < 0) break;
+    const int ci = item[k] >> 5, di = item[k] & 31;
+    if (s_flag[ci]) A.temp[((int64_t)r * C + ci) * nq + di] = ((hitmask >> k) & 1) ? tmin[k] : -1.0f;
   }
-  // emit rows in cell order
   if (tid < C) {
-    unsigned fl = s_flag[tid];
-    int rank = 0;
-    for (int c0 = 0; c0 < tid; ++c0) rank += s_flag[c0] != 0;
-    if (fl) {
-      int64_t row = A.boff[pos] + rank;
-      A.cells_out[row] = pos * C + tid;
-      for (int i = 0; i < nq; ++i)
-        A.q_out[row * nq + i] = ((fl >> i) & 1) ? __uint_as_float(s_q[tid][i]) : -1.0f;
-    }
+    A.flags[pos * C + tid] = s_flag[tid];
+    if (s_flag[tid]) A.temp[((int64_t)r * C + tid) * nq] = -1.0f;  // rest direction
   }
+  if (tid < 32) {
+    int nb = 0;
+    for (int c0 = tid; c0 < C; c0 += 32) nb += s_flag[c0] != 0;
+    for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    if (tid == 0) A.bcount[r] = nb;
+  }
+}
+
+// boundary rows in (block, cell) order: CTA of C threads per candidate block
+template <int D>
+__global__ void k_lat_emit(LatArgs A) {
+  constexpr int C = D == 3 ? 64 : 16;
+  const int64_t r = blockIdx.x;
+  if (r >= *A.n_cb || A.bcount[r] == 0) return;
+  const int64_t pos = A.cand_blocks[r];
+  const int c = threadIdx.x;
+  const unsigned fl = A.flags[pos * C + c];
+  __shared__ int s_b[C];
+  s_b[c] = fl != 0;
+  __syncthreads();
+  if (!fl) return;
+  int rank = 0;
+  for (int c0 = 0; c0 < c; ++c0) rank += s_b[c0];
+  const int64_t row = A.boff[r] + rank;
+  A.cells_out[row] = pos * C + c;
+  for (int i = 0; i < A.nq; ++i) A.q_out[row * A.nq + i] = A.temp[((int64_t)r * C + c) * A.nq + i];
+}
+
+struct BcountLoad {
+  const int32_t* b;
+  const int64_t* n_cb;
+  __device__ int64_t operator()(int64_t i) const { return i < *n_cb ? b[i] : 0; }
+};
+
+LatArgs make_args(ow_ctx* ctx, const ow_forest* f, const ow_grid* grid, const int8_t* dirs, int nq,
+                  const int32_t* leaves, int64_t n_leaves) {
+  LatArgs A;
+  memset(&A, 0, sizeof(A));
+  A.F = make_forestc(f);
+  A.g = make_gridc(grid);
+  for (int i = 0; i < nq; ++i)
+    for (int a = 0; a < 3; ++a) A.dirs.c[i][a] = a < f->dim ? dirs[i * 3 + a] : 0;
+  A.nq = nq;
+  A.leaves = leaves;
+  A.n_leaves = n_leaves;
+  A.rec = (const float4*)ctx->slot_ptr[SLOT_LAT_REC];
+  A.ab_ids = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_IDS];
+  A.ab_cnt = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_CNT];
+  A.ab_off = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_OFF];
+  A.cand_cnt = (int32_t*)ctx->slot_ptr[SLOT_LAT_CCNT];
+  A.cand_blocks = (int32_t*)ctx->slot_ptr[SLOT_LAT_LEAVES];
+  A.n_cb = ctx->d_small + 34;
+  A.bcount = (int32_t*)ctx->slot_ptr[SLOT_LAT_BCOUNT];
+  A.boff = (const int64_t*)ctx->slot_ptr[SLOT_LAT_BOFFS];
+  A.temp = (float*)ctx->slot_ptr[SLOT_LAT_TEMP];
+  return A;
 }
 
 }  // namespace
@@ -334,51 +528,61 @@ extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, const int
     ow_set_error("lattice: empty geometry");
     return OW_ERR_INVALID;
   }
+  const int D = f->dim, C = D == 3 ? 64 : 16;
   GridC g = make_gridc(grid);
   OW_PROF_BEGIN(ctx, PROF_PREP, s);
-  OW_TRY(f->dim == 3 ? build_abins<3>(ctx, g, d_coords, n_faces, geom_key, s)
-                     : build_abins<2>(ctx, g, d_coords, n_faces, geom_key, s));
-  void* pbc;
-  OW_TRY(ow_slot(ctx, SLOT_LAT_BCOUNT, 4 * (size_t)(n_leaves + 1), s, &pbc));
-  LatArgs A;
-  memset(&A, 0, sizeof(A));
-  A.F = make_forestc(f);
-  A.g = g;
+  OW_TRY(D == 3 ? build_abins<3>(ctx, g, d_coords, n_faces, geom_key, s)
+                : build_abins<2>(ctx, g, d_coords, n_faces, geom_key, s));
+  OW_PROF_END(ctx, PROF_PREP, s);
+  void* p;
+  const int64_t nl = n_leaves > 0 ? n_leaves : 1;
+  OW_TRY(ow_slot(ctx, SLOT_LAT_CCNT, 4 * (size_t)nl, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_LEAVES, 4 * (size_t)nl, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_BCOUNT, 4 * (size_t)nl, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_BOFFS, 8 * (size_t)nl, s, &p));
+  int8_t dirs3[QMAX * 3];
+  memset(dirs3, 0, sizeof(dirs3));
   for (int i = 0; i < n_dirs; ++i)
-    for (int a = 0; a < 3; ++a) A.dirs.c[i][a] = a < f->dim ? h_dirs[i * f->dim + a] : 0;
-  A.nq = n_dirs;
-  A.leaves = d_leaves;
-  A.c = d_coords;
-  A.n = n_faces;
-  A.ab_ids = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_IDS];
-  A.ab_cnt = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_CNT];
-  A.ab_off = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_OFF];
-  A.flags = d_flags;
-  A.bcount = (int32_t*)pbc;
-  if (n_leaves > 0) {
-    OW_PROF_END(ctx, PROF_PREP, s);
-    OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
-    if (f->dim == 3) k_lattice<3, false><<<(unsigned)n_leaves, LAT_THREADS, 0, s>>>(A);
-    else k_lattice<2, false><<<(unsigned)n_leaves, LAT_THREADS, 0, s>>>(A);
-    OW_PROF_END(ctx, PROF_LATTICE, s);
-    OW_LAUNCHED(ctx);
-    OW_CHECK_LAUNCH();
-  }
-  void* pofs;
-  OW_TRY(ow_slot(ctx, SLOT_LAT_LEAVES, 8 * (size_t)(n_leaves + 1), s, &pofs));
-  OW_TRY(scan(ctx, ow::LoadArr<int32_t>{(const int32_t*)pbc}, ow::StoreExcl<int64_t>{(int64_t*)pofs}, n_leaves,
-              ctx->d_small + 33, s));
-  int64_t nb;
-  OW_TRY(ow_readback(ctx, ctx->d_small + 33, 1, &nb, s));
+    for (int a = 0; a < D; ++a) dirs3[i * 3 + a] = h_dirs[i * D + a];
   ctx->lat_leaves = n_leaves;
-  ctx->lat_boundary = nb;
+  ctx->lat_boundary = 0;
   ctx->lat_dirs = n_dirs;
-  memcpy(ctx->lat_dir, &A.dirs, sizeof(A.dirs) < sizeof(ctx->lat_dir) ? sizeof(A.dirs) : sizeof(ctx->lat_dir));
+  memcpy(ctx->lat_dir, dirs3, sizeof(dirs3));
   ctx->lat_coords = d_coords;
   ctx->lat_faces = n_faces;
   ctx->lat_leaves_ptr = d_leaves;
   ctx->lat_forest = *f;
   ctx->lat_grid = *grid;
+  ctx->lat_flags = d_flags;
+  *out_boundary = 0;
+  if (n_leaves <= 0) return OW_OK;
+  OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
+  LatArgs A = make_args(ctx, f, grid, dirs3, n_dirs, d_leaves, n_leaves);
+  if (D == 3) k_lat_count<3><<<ow_blocks(n_leaves, CNT_WARPS), CNT_WARPS * 32, 0, s>>>(A);
+  else k_lat_count<2><<<ow_blocks(n_leaves, CNT_WARPS), CNT_WARPS * 32, 0, s>>>(A);
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  OW_TRY(scan(ctx, CandLoad{A.cand_cnt}, CandStore{A.cand_blocks}, n_leaves, ctx->d_small + 34, s));
+  int64_t n_cb;
+  OW_TRY(ow_readback(ctx, ctx->d_small + 34, 1, &n_cb, s));
+  ctx->lat_ncb = n_cb;
+  OW_CUDA(cudaMemsetAsync(d_flags, 0, 4 * (size_t)n_leaves * C, s));
+  A.flags = d_flags;
+  if (n_cb > 0) {
+    // q rows of the candidate blocks (boundary cells only are written)
+    OW_TRY(ow_slot(ctx, SLOT_LAT_TEMP, 4 * (size_t)n_cb * C * n_dirs, s, &p));
+    A.temp = (float*)p;
+    if (D == 3) k_lattice<3><<<(unsigned)n_cb, LAT_THREADS, 0, s>>>(A);
+    else k_lattice<2><<<(unsigned)n_cb, LAT_THREADS, 0, s>>>(A);
+    OW_LAUNCHED(ctx);
+    OW_CHECK_LAUNCH();
+  }
+  OW_TRY(scan(ctx, BcountLoad{A.bcount, A.n_cb}, ow::StoreExcl<int64_t>{(int64_t*)A.boff}, n_cb,
+              ctx->d_small + 35, s));
+  OW_PROF_END(ctx, PROF_LATTICE, s);
+  int64_t nb;
+  OW_TRY(ow_readback(ctx, ctx->d_small + 35, 1, &nb, s));
+  ctx->lat_boundary = nb;
   *out_boundary = nb;
   return OW_OK;
 }
@@ -390,25 +594,15 @@ extern "C" int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, 
     return OW_ERR_INVALID;
   }
   if (ctx->lat_boundary == 0 || ctx->lat_leaves == 0) return OW_OK;
-  LatArgs A;
-  memset(&A, 0, sizeof(A));
-  A.F = make_forestc(&ctx->lat_forest);
-  A.g = make_gridc(&ctx->lat_grid);
-  memcpy(&A.dirs, ctx->lat_dir, sizeof(A.dirs) < sizeof(ctx->lat_dir) ? sizeof(A.dirs) : sizeof(ctx->lat_dir));
-  A.nq = ctx->lat_dirs;
-  A.leaves = ctx->lat_leaves_ptr;
-  A.c = ctx->lat_coords;
-  A.n = ctx->lat_faces;
-  A.ab_ids = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_IDS];
-  A.ab_cnt = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_CNT];
-  A.ab_off = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_OFF];
-  A.bcount = (int32_t*)ctx->slot_ptr[SLOT_LAT_BCOUNT];
-  A.boff = (const int64_t*)ctx->slot_ptr[SLOT_LAT_LEAVES];
+  LatArgs A = make_args(ctx, &ctx->lat_forest, &ctx->lat_grid, ctx->lat_dir, ctx->lat_dirs, ctx->lat_leaves_ptr,
+                        ctx->lat_leaves);
+  A.flags = ctx->lat_flags;
   A.cells_out = d_cells;
   A.q_out = d_q;
+  const int C = ctx->lat_forest.dim == 3 ? 64 : 16;
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
-  if (ctx->lat_forest.dim == 3) k_lattice<3, true><<<(unsigned)ctx->lat_leaves, LAT_THREADS, 0, s>>>(A);
-  else k_lattice<2, true><<<(unsigned)ctx->lat_leaves, LAT_THREADS, 0, s>>>(A);
+  if (ctx->lat_forest.dim == 3) k_lat_emit<3><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
+  else k_lat_emit<2><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
   OW_PROF_END(ctx, PROF_LATTICE, s);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();

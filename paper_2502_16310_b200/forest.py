@@ -85,18 +85,37 @@ class Forest:
         self._marks[:r] = 0
         self._n = r
         self._n_levels = 1
+        self._version = 0
+        self._leaf_cache = {}
         self._view_struct = _lib.ForestView()
         self._grow_cb = _lib.GROW_FN(self._grow)
 
     # ------------------------------------------------------------------ storage
     def _alloc(self, cap):
+        # entries past n_blocks are never read: the split kernel writes every
+        # field of each block it appends, so the storage is left uninitialised
         dev = self.device
         self._cap = cap
-        self._level_t = torch.zeros(cap, dtype=torch.int16, device=dev)
-        self._coord = [torch.zeros(cap, dtype=torch.int32, device=dev) for _ in range(self.dim)]
-        self._parent_t = torch.full((cap,), -1, dtype=torch.int32, device=dev)
-        self._first_child_t = torch.full((cap,), -1, dtype=torch.int32, device=dev)
-        self._marks = torch.zeros(cap, dtype=torch.int8, device=dev)
+        self._level_t = torch.empty(cap, dtype=torch.int16, device=dev)
+        self._coord = [torch.empty(cap, dtype=torch.int32, device=dev) for _ in range(self.dim)]
+        self._parent_t = torch.empty(cap, dtype=torch.int32, device=dev)
+        self._first_child_t = torch.empty(cap, dtype=torch.int32, device=dev)
+        self._marks = torch.empty(cap, dtype=torch.int8, device=dev)
+
+    def _resize(self, new_cap, n):
+        old = (self._level_t, self._coord, self._parent_t, self._first_child_t, self._marks)
+        self._alloc(new_cap)
+        self._level_t[:n] = old[0][:n]
+        for ax in range(self.dim):
+            self._coord[ax][:n] = old[1][ax][:n]
+        self._parent_t[:n] = old[2][:n]
+        self._first_child_t[:n] = old[3][:n]
+        self._marks[:n] = old[4][:n]
+
+    def reserve(self, n_blocks):
+        """Make room for ``n_blocks`` blocks (geometric growth, one copy)."""
+        if n_blocks > self._cap:
+            self._resize(max(int(n_blocks), 2 * self._cap), self._n)
 
     def _grow(self, _user, view_p, need):
         try:
@@ -104,15 +123,7 @@ class Forest:
             # call: its view holds the live count, not self._n
             n = int(view_p.contents.n_blocks)
             self._n = n
-            new_cap = max(int(need), 2 * self._cap)
-            old = (self._level_t, self._coord, self._parent_t, self._first_child_t, self._marks)
-            self._alloc(new_cap)
-            self._level_t[:n] = old[0][:n]
-            for ax in range(self.dim):
-                self._coord[ax][:n] = old[1][ax][:n]
-            self._parent_t[:n] = old[2][:n]
-            self._first_child_t[:n] = old[3][:n]
-            self._marks[:n] = old[4][:n]
+            self._resize(max(int(need), 2 * self._cap), n)
             self._fill_view(view_p.contents)
             return 0
         except Exception:  # pragma: no cover - reported by the C side as a failed grow
@@ -205,12 +216,23 @@ class Forest:
         return self.level_counts()[1]
 
     def _leaves(self, level):
-        """Ascending leaf ids at ``level`` as an int32 CUDA tensor (hot path)."""
+        """Ascending leaf ids at ``level`` as an int32 CUDA tensor (hot path).
+
+        Cached until the block structure changes (refine_marked); marks do
+        not change the leaf set."""
+        key = (self._version, int(level))
+        hit = self._leaf_cache.get(key)
+        if hit is not None:
+            return hit
         out = torch.empty(max(self._n, 1), dtype=torch.int32, device=self.device)
         n = C.c_int64(0)
         _lib.call("ow_forest_leaves", _lib.ctx(), C.byref(self.view()), int(level), _lib.ptr(out), C.byref(n),
                   _lib.stream())
-        return out[: n.value]
+        res = out[: n.value]
+        if len(self._leaf_cache) > 8:
+            self._leaf_cache.clear()
+        self._leaf_cache[key] = res
+        return res
 
     def leaf_blocks_at(self, level):
         if level < 0 or level >= self._n_levels:
@@ -328,6 +350,8 @@ class Forest:
             _lib.call("ow_refine_marked", _lib.ctx(), C.byref(v), int(level), C.byref(out), _lib.stream())
         finally:
             self._sync_from_view()
+            self._version += 1
+            self._leaf_cache.clear()
         n = int(out.value)
         if n > 0:
             self._n_levels = max(self._n_levels, int(level) + 2)

@@ -70,8 +70,24 @@ class LatticeLinks:
         return int(sum(((f >> i) & 1).sum().item() for i in range(1, 27)))
 
 
-def build_lattice_links(forest: Forest, geom: CoordListGeometry, grid: BinGrid, lattice="D3Q19") -> LatticeLinks:
+def candidate_grid(forest: Forest):
+    """Candidate-bin grid sized to the finest level: bin edge ~ two finest blocks.
+
+    The candidate bins only prune work — the link set does not depend on them —
+    so the grid is chosen for speed (capped so the bin arrays stay small)."""
+    level = forest.n_levels - 1
+    b = max(1, max((r << level) // 2 for r in forest.root_dims))
+    cap = 160 if forest.dim == 3 else 2048
+    return BinGrid(forest.domain, min(b, cap))
+
+
+def build_lattice_links(forest: Forest, geom: CoordListGeometry, grid: BinGrid | None = None,
+                        lattice="D3Q19") -> LatticeLinks:
+    """Boundary links of the finest level; ``grid`` only chooses the candidate
+    bins (None: sized to the finest level) and never changes the result."""
     dirs = lattice_directions(lattice)
+    if grid is None:
+        grid = candidate_grid(forest)
     if dirs.shape[1] != forest.dim or geom.dim != forest.dim:
         raise InvalidParameterError(f"lattice {lattice} does not match a {forest.dim}D forest")
     if geom.n_faces == 0:

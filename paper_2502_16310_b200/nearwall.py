@@ -247,8 +247,12 @@ def refine_near_wall(forest: Forest, geom: CoordListGeometry, params: NearWallPa
         result.marked_detected.append(st.marked)
         result.cell_face_tests.append(st.tests)
         result.pairs_evaluated.append(st.evaluated)
-        result.marked_refined.append(forest.count_marks(level, RefineMark.MARKED, leaf_only=True))
+        n_marked = forest.count_marks(level, RefineMark.MARKED, leaf_only=True)
+        result.marked_refined.append(n_marked)
         with _Clock(False) as ck:
+            # pre-size for the marked splits plus rebalance slack, so the C
+            # side rarely needs its grow callback mid-refinement
+            forest.reserve(forest.n_blocks + forest.n_children * (n_marked + n_marked // 2 + 64))
             forest.refine_marked(level)
         record("refinement", level, ck.ms)
     return result

@@ -308,9 +308,11 @@ def test_lattice_links_vs_oracle(ow, case):
     geom = ow.CoordListGeometry(dim, coords)
     fg = ow.init_root_grid(domain(ow, dim), (root,) * dim)
     ow.refine_near_wall(fg, geom, ow.NearWallParams(d_spec=d, n_levels=3, bins_per_axis=4))
-    ll = ow.build_lattice_links(fg, geom, ow.BinGrid(domain(ow, dim), 4), lat)
-    np.testing.assert_array_equal(ll.leaves.cpu().numpy(), ref["leaves"])
-    np.testing.assert_array_equal(ll.flags.cpu().numpy().view(np.uint32), ref["flags"])
-    np.testing.assert_array_equal(ll.cells.cpu().numpy(), ref["boundary"])
-    np.testing.assert_array_equal(ll.q.cpu().numpy(), ref["q"])
-    assert ll.n_boundary > 0
+    # the candidate grid only prunes work: explicit coarse bins and the auto grid agree
+    for grid in (ow.BinGrid(domain(ow, dim), 4), None, ow.BinGrid(domain(ow, dim), 1)):
+        ll = ow.build_lattice_links(fg, geom, grid, lat)
+        np.testing.assert_array_equal(ll.leaves.cpu().numpy(), ref["leaves"])
+        np.testing.assert_array_equal(ll.flags.cpu().numpy().view(np.uint32), ref["flags"])
+        np.testing.assert_array_equal(ll.cells.cpu().numpy(), ref["boundary"])
+        np.testing.assert_array_equal(ll.q.cpu().numpy(), ref["q"])
+        assert ll.n_boundary > 0
