@@ -15,6 +15,7 @@ Layout (HBM, struct of arrays, `capacity` entries each):
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass
 from enum import IntEnum
 
@@ -88,7 +89,16 @@ class Forest:
         self._version = 0
         self._leaf_cache = {}
         self._view_struct = _lib.ForestView()
-        self._grow_cb = _lib.GROW_FN(self._grow)
+        # the callback holds the forest weakly: a bound method would form a
+        # reference cycle that keeps every forest (and its HBM) alive until
+        # the cyclic GC runs
+        ref = weakref.ref(self)
+
+        def grow(user, view_p, need):
+            f = ref()
+            return 1 if f is None else f._grow(user, view_p, need)
+
+        self._grow_cb = _lib.GROW_FN(grow)
 
     # ------------------------------------------------------------------ storage
     def _alloc(self, cap):

@@ -36,11 +36,53 @@ def step():
 for _ in range(3):
     step()
 torch.cuda.synchronize()
+
+# log slow torch.empty calls (size, caller) during a few steps
+import time as _t  # noqa: E402
+import traceback  # noqa: E402
+
+_orig_empty = torch.empty
+slow = []
+
+
+def _timed_empty(*a, **k):
+    t0 = _t.perf_counter()
+    r = _orig_empty(*a, **k)
+    dt = _t.perf_counter() - t0
+    if dt > 50e-6:
+        fr = traceback.extract_stack(limit=3)[0]
+        slow.append((round(dt * 1e6), tuple(r.shape), str(r.dtype), f"{os.path.basename(fr.filename)}:{fr.lineno}"))
+    return r
+
+
+torch.empty = _timed_empty
+for _ in range(5):
+    step()
+torch.cuda.synchronize()
+torch.empty = _orig_empty
+for s in slow:
+    print("slow empty", s)
+m0 = torch.cuda.memory_stats()
 pr = cProfile.Profile()
 pr.enable()
 for _ in range(steps):
     step()
 torch.cuda.synchronize()
 pr.disable()
+m1 = torch.cuda.memory_stats()
+for k in ("num_device_alloc", "num_device_free", "num_alloc_retries", "num_sync_all_streams"):
+    print(k, m1.get(k, 0) - m0.get(k, 0))
+import time  # noqa: E402
+
+sizes = [(32768, torch.int16), (32768, torch.int32), (121632, torch.int32), (4435968, torch.int32),
+         (191360 * 19, torch.float32), (24806, torch.int32), (69312, torch.int32)]
+for nel, dt in sizes:
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(100):
+        x = torch.empty(nel, dtype=dt, device="cuda")
+        del x
+    t1 = time.perf_counter()
+    print(f"empty({nel}, {dt}) {1e6 * (t1 - t0) / 100:.1f} us")
 st = pstats.Stats(pr)
 st.sort_stats("tottime").print_stats(25)
