@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(LAT_THREADS) k_lattice(LatArgs A) {
   __shared__ float s_fv[NF][LAT_CAP];
   __shared__ int s_ncand;
   __shared__ unsigned s_flag[C];
+  __shared__ unsigned s_mask[C][LAT_CAP / 32];
   const int64_t r = blockIdx.x;
   if (r >= *A.n_cb) return;
   const int64_t pos = A.cand_blocks[r];
@@ -364,7 +365,29 @@ __global__ void __launch_bounds__(LAT_THREADS) k_lattice(LatArgs A) {
   }
   __syncthreads();
 
+  // Phase A: per cell, which staged faces meet its "star" box
+  // [fl(x - h), fl(x + h)] — the union of all its link boxes, since every link
+  // end point is x, fl(x + h) or fl(x - h) per axis.  Phase B: each link
+  // tests only those faces.
   auto sweep = [&](int ncand) {
+    const int lane = tid & 31, warp = tid >> 5, nw = (ncand + 31) >> 5;
+    for (int c = warp; c < C; c += LAT_THREADS / 32) {
+      float slo[3], shi[3];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        slo[a] = FADD(s_cen[c][a], -b.h32[a]);
+        shi[a] = FADD(s_cen[c][a], b.h32[a]);
+      }
+      for (int w = 0; w < nw; ++w) {
+        const int j = w * 32 + lane;
+        bool ov = j < ncand;
+#pragma unroll
+        for (int a = 0; a < D; ++a) ov = ov && s_fv[NF - 2 * D + a][j] <= shi[a] && s_fv[NF - D + a][j] >= slo[a];
+        const unsigned m = __ballot_sync(0xffffffffu, ov);
+        if (lane == 0) s_mask[c][w] = m;
+      }
+    }
+    __syncthreads();
 #pragma unroll
     for (int k = 0; k < LAT_ITEMS; ++k) {
       if (item[k] < 0) break;
@@ -378,7 +401,9 @@ __global__ void __launch_bounds__(LAT_THREADS) k_lattice(LatArgs A) {
         llo[a] = fminf(x[a], e);
         lhi[a] = fmaxf(x[a], e);
       }
-      for (int j = 0; j < ncand; ++j) {
+      for (int w = 0; w < nw; ++w)
+      for (unsigned m = s_mask[ci][w]; m; m &= m - 1) {
+        const int j = w * 32 + __ffs(m) - 1;
         bool ov = true;
 #pragma unroll
         for (int a = 0; a < D; ++a) ov &= s_fv[NF - 2 * D + a][j] <= lhi[a] && s_fv[NF - D + a][j] >= llo[a];

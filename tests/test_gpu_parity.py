@@ -316,3 +316,26 @@ def test_lattice_links_vs_oracle(ow, case):
         np.testing.assert_array_equal(ll.cells.cpu().numpy(), ref["boundary"])
         np.testing.assert_array_equal(ll.q.cpu().numpy(), ref["q"])
         assert ll.n_boundary > 0
+
+
+@pytest.mark.parametrize("case", ["wall_between", "wall_on_centres", "wall_at_link_end", "square2d"])
+def test_lattice_known_answers_on_gpu(ow, case):
+    from oracle import forest as of
+    from oracle import lattice as ol
+
+    from test_oracle_lattice import _wall_z
+
+    if case == "square2d":
+        sq = np.array([[[0.3, 0.3], [0.7, 0.3]], [[0.7, 0.3], [0.7, 0.7]], [[0.7, 0.7], [0.3, 0.7]],
+                       [[0.3, 0.7], [0.3, 0.3]]], np.float32)
+        coords, dim, lat = np.ascontiguousarray(np.transpose(sq, (1, 2, 0))), 2, "D2Q9"
+    else:
+        z = {"wall_between": 0.2, "wall_on_centres": 0.125, "wall_at_link_end": 0.375}[case]
+        coords, dim, lat = _wall_z(np.float32(z)), 3, "D3Q27"
+    fo = of.Forest(np.zeros(dim), np.ones(dim), (1,) * dim)
+    ref = ol.lattice_links(fo, coords, lat)
+    fg = ow.init_root_grid(domain(ow, dim), (1,) * dim)
+    ll = ow.build_lattice_links(fg, ow.CoordListGeometry(dim, coords), None, lat)
+    np.testing.assert_array_equal(ll.flags.cpu().numpy().view(np.uint32), ref["flags"])
+    np.testing.assert_array_equal(ll.cells.cpu().numpy(), ref["boundary"])
+    np.testing.assert_array_equal(ll.q.cpu().numpy(), ref["q"])
