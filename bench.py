@@ -188,6 +188,7 @@ def gpu_arm(args, cfg, rank, world, local_rank):
             ev[k][1].record()
         barrier()
     launches = _lib.launches() - launches0
+    lat_stats = _lib.lattice_stats()
     for s in res.timings:
         log("stage", s.csv_row())
     prof = _lib.profile_read()
@@ -248,31 +249,38 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    kern = {k: v for k, v in prof.items() if k in ("mark", "lattice", "fill_bins", "stl", "prep")}
-    dom_k = max(kern, key=lambda k: kern[k][0]) if kern else "mark"
-    mark_ms, mark_n = prof["mark"]
     sm_mhz = clk.summary()["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # non-FMA issue rate (-fmad=false), TOP/s
-    ops = FP32_OPS_PER_TEST[dim] * evaluated * args.steps
-    achieved = ops / (mark_ms / 1e3) / 1e12 if mark_ms > 0 else 0.0
-    traffic = None
+    traffic = {}
     try:
-        tj = json.load(open(os.path.join(REPO, "profiles", "traffic.json")))
-        traffic = tj.get(args.config, {}).get("mark")
+        traffic = json.load(open(os.path.join(REPO, "profiles", "traffic.json"))).get(args.config, {})
     except Exception:
         pass
-    roofline = {
-        "kernel": "k_mark (near-wall predicate sweep)", "bound": "fp32", "achieved": achieved,
-        "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None,
-        "traffic": traffic,
-        "peak_note": "148 SMs x 128 FP32 lanes x max SM clock, non-FMA (FMUL/FADD) issue rate; "
-                     "MEASURED_PEAKS.json has no FP32 entry",
-        "algorithmic": f"{FP32_OPS_PER_TEST[dim]} FP32 ops per evaluated cell-face predicate x {evaluated} "
-                       f"evaluations per step",
-        "launches": mark_n, "avg_launch_ms": mark_ms / max(mark_n, 1),
-        "dominant_family": dom_k,
-        "families_ms": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},
-    }
+    peak_note = ("148 SMs x 128 FP32 lanes x max SM clock = non-FMA (FMUL/FADD/FSETP) issue rate; "
+                 "MEASURED_PEAKS.json has no FP32 entry")
+
+    def entry(kernel, ms, n, ops, algorithmic, tkey):
+        achieved = ops / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+        t = traffic.get(tkey)
+        return {"kernel": kernel, "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak if fp32_peak else None, "traffic": t, "traffic_unit": "bytes/launch",
+                "algorithmic": algorithmic, "launches": n, "avg_launch_ms": ms / max(n, 1), "peak_note": peak_note}
+
+    mark_ms, mark_n = prof["mark"]
+    mark = entry("k_mark (near-wall predicate sweep)", mark_ms, mark_n,
+                 FP32_OPS_PER_TEST[dim] * evaluated * args.steps,
+                 f"{FP32_OPS_PER_TEST[dim]} FP32 ops per evaluated cell-face predicate x {evaluated} per step "
+                 f"(pairs surviving the reference's box + sphere culls)", "mark")
+    sw_ms, sw_n = prof["lattice_sweep"]
+    star, box, mt = lat_stats
+    lat_ops = (6 * star + 6 * box + 45 * mt) if dim == 3 else (4 * star + 4 * box + 13 * mt)
+    lattice = entry("k_lattice (boundary-link sweep)", sw_ms, sw_n, lat_ops * args.steps,
+                    f"per step: {star} star-box tests x 6 cmp + {box} link-box tests x 6 cmp + {mt} "
+                    f"Moller-Trumbore tests x 45 FP32 ops", "lattice")
+    dominant = lattice if sw_ms >= mark_ms else mark
+    roofline = dict(dominant)
+    roofline["secondary"] = mark if dominant is lattice else lattice
+    roofline["families_ms"] = {k: round(v[0] / args.steps, 4) for k, v in prof.items()}
     out = {
         "metric": "geometry-to-grid time (ms) & cell-face tests/s at 1/2/4/8 B200 vs CPU",
         "value": T_step / (ms_step / 1e3),

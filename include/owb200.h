@@ -87,7 +87,8 @@ int ow_version(void);
 int64_t ow_launch_count(ow_ctx* ctx);
 /* Optional CUDA-event timing of kernel families (bench.py roofline):
  * ids 0 mark, 1 lattice, 2 fill_bins, 3 refine, 4 propagate, 5 links,
- * 6 STL import, 7 face prep.  ow_profile(ctx, 1) enables and resets. */
+ * 6 STL import, 7 face prep, 8 lattice sweep kernel alone.
+ * ow_profile(ctx, 1) enables and resets. */
 int ow_profile(ow_ctx* ctx, int enable);
 int ow_profile_read(ow_ctx* ctx, int kernel_id, double* total_ms, int64_t* launches);
 
@@ -189,6 +190,9 @@ int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, const int32_t* d_lea
                            const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags, int64_t* out_boundary,
                            void* stream);
 int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, void* stream);
+/* Work counters of the last ow_lattice_links_count: [0] star-box tests,
+ * [1] link-AABB tests, [2] Moller-Trumbore / segment tests (roofline). */
+int ow_lattice_stats(ow_ctx* ctx, int64_t* out3, void* stream);
 
 /* ---- predicate probe (parity tests) ---------------------------------------- */
 /* out[i] = near(point i, face i, d[i]) for n independent pairs; points (n, D),

@@ -105,6 +105,7 @@ _SIGS = {
     "ow_cell_face_links_emit": [P, P, P, P, P, P],
     "ow_lattice_links_count": [P, C.POINTER(ForestView), P, I64, P, I64, I64, C.POINTER(Grid), P, I32, P, PI64, P],
     "ow_lattice_links_emit": [P, P, P, P],
+    "ow_lattice_stats": [P, PI64, P],
     "ow_near_pairs": [P, I32, P, P, P, I64, P, P],
 }
 _RESTYPE = {"ow_last_error": C.c_char_p, "ow_version": C.c_int, "ow_launch_count": C.c_int64}
@@ -174,7 +175,15 @@ def launches():
     return sum(int(lib().ow_launch_count(c)) for c in _ctx.values())
 
 
-PROF_IDS = {"mark": 0, "lattice": 1, "fill_bins": 2, "refine": 3, "propagate": 4, "links": 5, "stl": 6, "prep": 7}
+PROF_IDS = {"mark": 0, "lattice": 1, "fill_bins": 2, "refine": 3, "propagate": 4, "links": 5, "stl": 6, "prep": 7,
+            "lattice_sweep": 8}
+
+
+def lattice_stats():
+    """(star-box, link-box, intersection) test counts of the last lattice call."""
+    out = (C.c_int64 * 3)()
+    call("ow_lattice_stats", ctx(), out, stream())
+    return tuple(int(x) for x in out)
 
 
 def profile(enable=True):

@@ -67,12 +67,17 @@ enum ow_slot {
   SLOT_LAT_CCNT,       // candidates per finest block
   SLOT_LAT_BOFFS,      // boundary-row offsets per candidate block
   SLOT_LAT_TEMP,       // q rows staging
+  SLOT_LAT_COFF,       // packed pair offset / candidate-block rank per finest block
+  SLOT_LAT_PFACE,      // (block, face) pairs: face
+  SLOT_LAT_PBLK,       // (block, face) pairs: block position
+  SLOT_LAT_STAR,       // (pair, cell) items passing the star-box test
   SLOT_MISC,
   SLOT_COUNT
 };
 
 // optional per-kernel CUDA-event timing (bench.py roofline instrumentation)
-enum { PROF_MARK = 0, PROF_LATTICE, PROF_BINS, PROF_REFINE, PROF_PROP, PROF_LINKS, PROF_STL, PROF_PREP, PROF_N };
+enum { PROF_MARK = 0, PROF_LATTICE, PROF_BINS, PROF_REFINE, PROF_PROP, PROF_LINKS, PROF_STL, PROF_PREP,
+       PROF_LAT_SWEEP, PROF_N };
 #define PROF_MAX 256
 struct ow_prof {
   int enabled;
@@ -117,7 +122,7 @@ struct ow_ctx {
   const float* lat_coords;
   const int32_t* lat_leaves_ptr;
   uint32_t* lat_flags;
-  int64_t lat_key, lat_ncb;
+  int64_t lat_key, lat_ncb, lat_pairs;
   ow_forest lat_forest;
   ow_grid lat_grid;
   int64_t abin_key;

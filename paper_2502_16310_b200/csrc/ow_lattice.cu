@@ -5,16 +5,19 @@
 // Candidates come from an AABB-overlap bin CSR (a face is stored in every bin
 // its float32 AABB touches) plus a packed 64-byte record per face (v0, edge
 // vectors, float32 box, first bin), built once per (geometry, grid).
+// The work is flattened into three independent item lists so every stage
+// runs at full occupancy without per-block serial latency:
 //   k_lat_count : warp per finest leaf block, counts the faces whose box meets
 //                 the block box grown by two cells (each face once: in the
 //                 first bin of its range ∩ the block's range).
-//   scan        : compacts the blocks with candidates (typically ~1/4).
-//   k_lattice   : CTA per candidate block; stages the candidates in shared
-//                 memory and sweeps every (cell, direction) link: exact float32
-//                 link-AABB overlap, then Moller-Trumbore (3D) / segment-
-//                 segment (2D) with a fixed op order; writes flag words, the
-//                 block's boundary-cell count and its q rows to a staging area.
-//   scan + k_lat_emit : boundary rows compacted in (block, cell) order.
+//   scan        : pair offsets + candidate-block ranks (one packed scan).
+//   k_lat_pairs : (block, face) candidate pairs.
+//   k_lat_star  : (pair, cell) items whose cell star box — the union of its
+//                 link boxes — meets the face box.
+//   k_lat_links : per item, every direction: exact float32 link-AABB test,
+//                 then Moller-Trumbore (3D) / segment-segment (2D) with a fixed
+//                 op order; atomicOr flag bits, atomicMin q bits.
+//   k_lat_bcount + scan + k_lat_emit : boundary rows in (block, cell) order.
 #include "ow_scan.cuh"
 #include <string.h>
 
@@ -24,8 +27,6 @@ using ow::scan;
 
 constexpr int LAT_THREADS = 256;
 constexpr int QMAX = 27;
-constexpr int LAT_CAP = 512;  // staged faces per sweep
-constexpr int LAT_ITEMS = (64 * (QMAX - 1) + LAT_THREADS - 1) / LAT_THREADS;
 constexpr int CNT_WARPS = 8;
 
 struct Dirs {
@@ -238,15 +239,22 @@ struct LatArgs {
   const int32_t* ab_ids;
   const int32_t* ab_cnt;
   const int32_t* ab_off;
-  int32_t* cand_cnt;       // [n_leaves]
-  int32_t* cand_blocks;    // [n_leaves] compacted positions
-  const int64_t* n_cb;     // device scalar
-  uint32_t* flags;         // [n_leaves * C]
-  int32_t* bcount;         // [n_leaves] boundary cells per candidate block
-  const int64_t* boff;     // [n_leaves]
-  float* temp;             // [n_cb * C * nq] q rows (staging)
+  int32_t* cand_cnt;        // [n_leaves] candidate faces per finest block
+  int64_t* cand_off;        // [n_leaves] packed: pair offset << 32 | candidate-block rank
+  int32_t* cand_blocks;     // [n_cb] position of each candidate block
+  int32_t* pair_face;       // [P] candidate face of each (block, face) pair
+  int32_t* pair_blk;        // [P] leaf position of each pair
+  int64_t n_pairs;
+  uint32_t* star;           // [<= P*C] (pair << shift | cell) passing the star-box test
+  unsigned long long* n_star;
+  uint32_t* flags;          // [n_leaves * C]
+  unsigned* qbits;          // [n_cb * C * nq] min-t float bits (+inf init)
+  int32_t* bcount;          // [n_cb]
+  const int64_t* boff;      // [n_cb]
+  int64_t n_cb;
   int64_t* cells_out;
   float* q_out;
+  unsigned long long* stats;  // [0] star-box, [1] link-box, [2] intersection tests
 };
 
 template <int D>
@@ -271,16 +279,110 @@ __global__ void __launch_bounds__(CNT_WARPS * 32) k_lat_count(LatArgs A) {
   if (lane == 0) A.cand_cnt[pos] = count;
 }
 
+// one scan gives both the pair offset (high word) and the candidate-block rank (low word)
 struct CandLoad {
   const int32_t* c;
-  __device__ int64_t operator()(int64_t i) const { return c[i] > 0; }
-};
-struct CandStore {
-  int32_t* out;
-  __device__ void operator()(int64_t i, int64_t e, int64_t v) const {
-    if (v) out[e] = (int32_t)i;
+  __device__ int64_t operator()(int64_t i) const {
+    int64_t n = c[i];
+    return (n << 32) | (n > 0 ? 1 : 0);
   }
 };
+struct CandStore {
+  int64_t* off;
+  int32_t* blocks;
+  __device__ void operator()(int64_t i, int64_t e, int64_t v) const {
+    off[i] = e;
+    if (v) blocks[e & 0xffffffffll] = (int32_t)i;
+  }
+};
+
+// warp per candidate block: write its (block, face) pairs
+template <int D>
+__global__ void __launch_bounds__(CNT_WARPS * 32) k_lat_pairs(LatArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * CNT_WARPS + (threadIdx.x >> 5);
+  if (r >= A.n_cb) return;
+  const int pos = A.cand_blocks[r];
+  const BlockFrame b = block_frame<D>(A.F, A.g, A.leaves[pos]);
+  int64_t out = A.cand_off[pos] >> 32;
+  for (int bz = b.rlo[2]; bz <= b.rhi[2]; ++bz)
+    for (int by = b.rlo[1]; by <= b.rhi[1]; ++by)
+      for (int bx0 = b.rlo[0]; bx0 <= b.rhi[0]; ++bx0) {
+        int bx[3] = {bx0, by, bz};
+        int64_t lin = bx0 + (int64_t)A.g.B * (by + (int64_t)A.g.B * bz);
+        const int32_t* src = A.ab_ids + A.ab_off[lin];
+        const int cnt = A.ab_cnt[lin];
+        for (int j0 = 0; j0 < cnt; j0 += 32) {
+          const int f = j0 + lane < cnt ? src[j0 + lane] : 0;
+          const bool ok = j0 + lane < cnt && is_candidate<D>(A.rec, f, b, bx);
+          const unsigned m = __ballot_sync(0xffffffffu, ok);
+          if (ok) {
+            const int64_t k = out + __popc(m & lanemask_lt());
+            A.pair_face[k] = f;
+            A.pair_blk[k] = pos;
+          }
+          out += __popc(m);
+        }
+      }
+}
+
+// cell centre (FP64 -> one FP32 rounding) and cell size of cell c of block id
+template <int D>
+__device__ __forceinline__ void cell_center(const ForestC& F, int id, int c, float* x, float* h) {
+  const int L = F.level[id];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double q = block_len(F, a, L);
+    double o = DADD(F.dmin[a], DMUL((double)F.coord[a][id], q));
+    double u = ((double)((c >> (2 * a)) & 3) + 0.5) / 4.0;
+    x[a] = __double2float_rn(DADD(o, DMUL(u, q)));
+    h[a] = __double2float_rn(q / 4.0);
+  }
+}
+
+__device__ __forceinline__ void face_lohi(const float4* __restrict__ rec, int f, int D, float* lo, float* hi) {
+  if (D == 3) {
+    float4 r0 = rec[4 * f], r1 = rec[4 * f + 1], r2 = rec[4 * f + 2], r3 = rec[4 * f + 3];
+    lo[0] = r0.w, lo[1] = r1.w, lo[2] = r2.w, hi[0] = r3.x, hi[1] = r3.y, hi[2] = r3.z;
+  } else {
+    float4 r1 = rec[4 * f + 1];
+    lo[0] = r1.x, lo[1] = r1.y, hi[0] = r1.z, hi[1] = r1.w;
+  }
+}
+
+// (pair, cell) items whose cell "star" box [fl(x-h), fl(x+h)] — the union of
+// all its link boxes — meets the face box; appended with warp-aggregated atomics
+template <int D>
+__global__ void __launch_bounds__(256) k_lat_star(LatArgs A) {
+  constexpr int SH = D == 3 ? 6 : 4;  // log2 cells per block
+  const int64_t total = A.n_pairs << SH;
+  const int lane = threadIdx.x & 31;
+  unsigned long long tests = 0;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = base + threadIdx.x;
+    bool ok = false;
+    if (t < total) {
+      const int64_t p = t >> SH;
+      const int c = (int)(t & ((1 << SH) - 1));
+      float x[3], h[3], lo[3], hi[3];
+      cell_center<D>(A.F, A.leaves[A.pair_blk[p]], c, x, h);
+      face_lohi(A.rec, A.pair_face[p], D, lo, hi);
+      ok = true;
+#pragma unroll
+      for (int a = 0; a < D; ++a) ok = ok && lo[a] <= FADD(x[a], h[a]) && hi[a] >= FADD(x[a], -h[a]);
+      ++tests;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if (m) {
+      unsigned long long w = 0;
+      if (lane == 0) w = atomicAdd(A.n_star, (unsigned long long)__popc(m));
+      w = __shfl_sync(0xffffffffu, w, 0);
+      if (ok) A.star[w + __popc(m & lanemask_lt())] = (uint32_t)t;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) tests += __shfl_xor_sync(0xffffffffu, tests, o);
+  if (lane == 0 && tests) atomicAdd(&A.stats[0], tests);
+}
 
 // Moller-Trumbore, fixed op order (oracle/lattice.py:mt_hits); e1 = v1 - v0,
 // e2 = v2 - v0 were formed by the same float32 subtractions at packing time.
@@ -318,174 +420,78 @@ __device__ __forceinline__ bool seg_hit_s(const float* x, const float* dv, const
   return true;
 }
 
+// every link of a (cell, face) item: exact link-AABB test, then the
+// intersection test; hits update the cell's flag word and min-t
 template <int D>
-__global__ void __launch_bounds__(LAT_THREADS) k_lattice(LatArgs A) {
+__global__ void __launch_bounds__(256) k_lat_links(LatArgs A) {
+  constexpr int SH = D == 3 ? 6 : 4;
+  constexpr int C = 1 << SH;
+  const int64_t total = (int64_t)*A.n_star;
+  unsigned long long nbox = 0, nmt = 0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = A.star[e];
+    const int64_t p = t >> SH;
+    const int c = (int)(t & (C - 1));
+    const int pos = A.pair_blk[p], f = A.pair_face[p];
+    float x[3], h[3], lo[3], hi[3], v0[3], e1[3], e2[3];
+    cell_center<D>(A.F, A.leaves[pos], c, x, h);
+    const float4* R = A.rec + 4 * (int64_t)f;
+    if (D == 3) {
+      float4 r0 = R[0], r1 = R[1], r2 = R[2], r3 = R[3];
+      v0[0] = r0.x, v0[1] = r0.y, v0[2] = r0.z, e1[0] = r1.x, e1[1] = r1.y, e1[2] = r1.z;
+      e2[0] = r2.x, e2[1] = r2.y, e2[2] = r2.z;
+      lo[0] = r0.w, lo[1] = r1.w, lo[2] = r2.w, hi[0] = r3.x, hi[1] = r3.y, hi[2] = r3.z;
+    } else {
+      float4 r0 = R[0], r1 = R[1];
+      v0[0] = r0.x, v0[1] = r0.y, e1[0] = r0.z, e1[1] = r0.w;
+      lo[0] = r1.x, lo[1] = r1.y, hi[0] = r1.z, hi[1] = r1.w;
+    }
+    const int64_t cell = (int64_t)pos * C + c;
+    const int64_t qrow = ((int64_t)(A.cand_off[pos] & 0xffffffffll) * C + c) * A.nq;
+    unsigned fl = 0;
+    for (int d = 1; d < A.nq; ++d) {
+      float dv[3];
+      bool ov = true;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        dv[a] = FMUL((float)A.dirs.c[d][a], h[a]);  // exact: c in {-1,0,1}
+        const float en = FADD(x[a], dv[a]);
+        ov = ov && lo[a] <= fmaxf(x[a], en) && hi[a] >= fminf(x[a], en);
+      }
+      ++nbox;
+      if (!ov) continue;
+      ++nmt;
+      float tt;
+      const bool hit = D == 3 ? mt_hit_e(x, dv, v0, e1, e2, &tt) : seg_hit_s(x, dv, v0, e1, &tt);
+      if (hit) {
+        fl |= 1u << d;
+        atomicMin(&A.qbits[qrow + d], __float_as_uint(FADD(tt, 0.0f)));  // -0 -> +0; t >= 0
+      }
+    }
+    if (fl) atomicOr(&A.flags[cell], fl);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    nbox += __shfl_xor_sync(0xffffffffu, nbox, o);
+    nmt += __shfl_xor_sync(0xffffffffu, nmt, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (nbox) atomicAdd(&A.stats[1], nbox);
+    if (nmt) atomicAdd(&A.stats[2], nmt);
+  }
+}
+
+// boundary cells per candidate block (warp per block)
+template <int D>
+__global__ void k_lat_bcount(LatArgs A) {
   constexpr int C = D == 3 ? 64 : 16;
-  constexpr int NF = D == 3 ? 15 : 8;  // staged floats per face: v0|a, e1|s, (e2), lo, hi
-  __shared__ float s_cen[C][D];
-  __shared__ float s_dv[QMAX][D];
-  __shared__ float s_fv[NF][LAT_CAP];
-  __shared__ int s_ncand;
-  __shared__ unsigned s_flag[C];
-  __shared__ unsigned s_mask[C][LAT_CAP / 32];
-  const int64_t r = blockIdx.x;
-  if (r >= *A.n_cb) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= A.n_cb) return;
   const int64_t pos = A.cand_blocks[r];
-  const int id = A.leaves[pos];
-  const ForestC& F = A.F;
-  const int L = F.level[id];
-  const int tid = threadIdx.x;
-  const BlockFrame b = block_frame<D>(F, A.g, id);
-  const int nq = A.nq, nd = nq - 1, work = C * nd;
-  if (tid < C) {
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      double q = block_len(F, a, L);
-      double u = ((double)((tid >> (2 * a)) & 3) + 0.5) / 4.0;
-      s_cen[tid][a] = __double2float_rn(DADD(b.blo[a], DMUL(u, q)));
-    }
-    s_flag[tid] = 0u;
-  }
-  if (tid < nq) {
-#pragma unroll
-    for (int a = 0; a < D; ++a) s_dv[tid][a] = FMUL((float)A.dirs.c[tid][a], b.h32[a]);  // exact: c in {-1,0,1}
-  }
-  if (tid == 0) s_ncand = 0;
-  // this thread's links (cell, direction), packed cell * 32 + direction
-  const float inv_nd = 1.0f / (float)nd;
-  int item[LAT_ITEMS];
-  float tmin[LAT_ITEMS];
-  unsigned hitmask = 0;
-#pragma unroll
-  for (int k = 0; k < LAT_ITEMS; ++k) {
-    const int it = tid + k * LAT_THREADS;
-    const int ci = (int)(((float)it + 0.5f) * inv_nd);  // exact for it < 2^16
-    item[k] = it < work ? ci * 32 + 1 + (it - ci * nd) : -1;
-    tmin[k] = INFINITY;
-  }
-  __syncthreads();
-
-  // Phase A: per cell, which staged faces meet its "star" box
-  // [fl(x - h), fl(x + h)] — the union of all its link boxes, since every link
-  // end point is x, fl(x + h) or fl(x - h) per axis.  Phase B: each link
-  // tests only those faces.
-  auto sweep = [&](int ncand) {
-    const int lane = tid & 31, warp = tid >> 5, nw = (ncand + 31) >> 5;
-    for (int c = warp; c < C; c += LAT_THREADS / 32) {
-      float slo[3], shi[3];
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        slo[a] = FADD(s_cen[c][a], -b.h32[a]);
-        shi[a] = FADD(s_cen[c][a], b.h32[a]);
-      }
-      for (int w = 0; w < nw; ++w) {
-        const int j = w * 32 + lane;
-        bool ov = j < ncand;
-#pragma unroll
-        for (int a = 0; a < D; ++a) ov = ov && s_fv[NF - 2 * D + a][j] <= shi[a] && s_fv[NF - D + a][j] >= slo[a];
-        const unsigned m = __ballot_sync(0xffffffffu, ov);
-        if (lane == 0) s_mask[c][w] = m;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < LAT_ITEMS; ++k) {
-      if (item[k] < 0) break;
-      const int ci = item[k] >> 5, di = item[k] & 31;
-      float x[3], dv[3], llo[3], lhi[3];
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        x[a] = s_cen[ci][a];
-        dv[a] = s_dv[di][a];
-        float e = FADD(x[a], dv[a]);
-        llo[a] = fminf(x[a], e);
-        lhi[a] = fmaxf(x[a], e);
-      }
-      for (int w = 0; w < nw; ++w)
-      for (unsigned m = s_mask[ci][w]; m; m &= m - 1) {
-        const int j = w * 32 + __ffs(m) - 1;
-        bool ov = true;
-#pragma unroll
-        for (int a = 0; a < D; ++a) ov &= s_fv[NF - 2 * D + a][j] <= lhi[a] && s_fv[NF - D + a][j] >= llo[a];
-        if (!ov) continue;
-        float v0[3], e1[3], e2[3], t;
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          v0[a] = s_fv[a][j];
-          e1[a] = s_fv[D + a][j];
-          if (D == 3) e2[a] = s_fv[6 + a][j];
-        }
-        bool hit = D == 3 ? mt_hit_e(x, dv, v0, e1, e2, &t) : seg_hit_s(x, dv, v0, e1, &t);
-        if (hit) {
-          t = FADD(t, 0.0f);  // -0 -> +0
-          hitmask |= 1u << k;
-          tmin[k] = fminf(tmin[k], t);
-        }
-      }
-    }
-  };
-
-  for (int bz = b.rlo[2]; bz <= b.rhi[2]; ++bz)
-    for (int by = b.rlo[1]; by <= b.rhi[1]; ++by)
-      for (int bx0 = b.rlo[0]; bx0 <= b.rhi[0]; ++bx0) {
-        int bx[3] = {bx0, by, bz};
-        int64_t lin = bx0 + (int64_t)A.g.B * (by + (int64_t)A.g.B * bz);
-        const int32_t* src = A.ab_ids + A.ab_off[lin];
-        const int cnt = A.ab_cnt[lin];
-        for (int base = 0; base < cnt; base += LAT_THREADS) {
-          if (s_ncand > LAT_CAP - LAT_THREADS) {  // uniform: read after a barrier
-            sweep(s_ncand);
-            __syncthreads();
-            if (tid == 0) s_ncand = 0;
-            __syncthreads();
-          }
-          const int j = base + tid;
-          if (j < cnt) {
-            const int f = src[j];
-            if (is_candidate<D>(A.rec, f, b, bx)) {
-              const int k = atomicAdd(&s_ncand, 1);
-              const float4* R = A.rec + 4 * (int64_t)f;
-              if (D == 3) {
-                float4 r0 = R[0], r1 = R[1], r2 = R[2], r3 = R[3];
-                float fv[15] = {r0.x, r0.y, r0.z, r1.x, r1.y, r1.z, r2.x, r2.y, r2.z,
-                                r0.w, r1.w, r2.w, r3.x, r3.y, r3.z};
-#pragma unroll
-                for (int q = 0; q < NF; ++q) s_fv[q][k] = fv[q];
-              } else {
-                float4 r0 = R[0], r1 = R[1];
-                float fv[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-#pragma unroll
-                for (int q = 0; q < NF; ++q) s_fv[q][k] = fv[q];
-              }
-            }
-          }
-          __syncthreads();
-        }
-      }
-  if (s_ncand > 0) sweep(s_ncand);
-#pragma unroll
-  for (int k = 0; k < LAT_ITEMS; ++k) {
-    if (item[k] < 0 || !((hitmask >> k) & 1)) continue;
-    atomicOr(&s_flag[item[k] >> 5], 1u << (item[k] & 31));
-  }
-  __syncthreads();
-  // q rows of this block (staging, all Q entries of boundary cells)
-#pragma unroll
-  for (int k = 0; k < LAT_ITEMS; ++k) {
-    if (item[k] < 0) break;
-    const int ci = item[k] >> 5, di = item[k] & 31;
-    if (s_flag[ci]) A.temp[((int64_t)r * C + ci) * nq + di] = ((hitmask >> k) & 1) ? tmin[k] : -1.0f;
-  }
-  if (tid < C) {
-    A.flags[pos * C + tid] = s_flag[tid];
-    if (s_flag[tid]) A.temp[((int64_t)r * C + tid) * nq] = -1.0f;  // rest direction
-  }
-  if (tid < 32) {
-    int nb = 0;
-    for (int c0 = tid; c0 < C; c0 += 32) nb += s_flag[c0] != 0;
-    for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
-    if (tid == 0) A.bcount[r] = nb;
-  }
+  int nb = 0;
+  for (int c = lane; c < C; c += 32) nb += A.flags[pos * C + c] != 0;
+  for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+  if (lane == 0) A.bcount[r] = nb;
 }
 
 // boundary rows in (block, cell) order: CTA of C threads per candidate block
@@ -493,7 +499,7 @@ template <int D>
 __global__ void k_lat_emit(LatArgs A) {
   constexpr int C = D == 3 ? 64 : 16;
   const int64_t r = blockIdx.x;
-  if (r >= *A.n_cb || A.bcount[r] == 0) return;
+  if (r >= A.n_cb || A.bcount[r] == 0) return;
   const int64_t pos = A.cand_blocks[r];
   const int c = threadIdx.x;
   const unsigned fl = A.flags[pos * C + c];
@@ -505,14 +511,9 @@ __global__ void k_lat_emit(LatArgs A) {
   for (int c0 = 0; c0 < c; ++c0) rank += s_b[c0];
   const int64_t row = A.boff[r] + rank;
   A.cells_out[row] = pos * C + c;
-  for (int i = 0; i < A.nq; ++i) A.q_out[row * A.nq + i] = A.temp[((int64_t)r * C + c) * A.nq + i];
+  const unsigned* q = A.qbits + (r * C + c) * A.nq;
+  for (int i = 0; i < A.nq; ++i) A.q_out[row * A.nq + i] = ((fl >> i) & 1) ? __uint_as_float(q[i]) : -1.0f;
 }
-
-struct BcountLoad {
-  const int32_t* b;
-  const int64_t* n_cb;
-  __device__ int64_t operator()(int64_t i) const { return i < *n_cb ? b[i] : 0; }
-};
 
 LatArgs make_args(ow_ctx* ctx, const ow_forest* f, const ow_grid* grid, const int8_t* dirs, int nq,
                   const int32_t* leaves, int64_t n_leaves) {
@@ -530,11 +531,18 @@ LatArgs make_args(ow_ctx* ctx, const ow_forest* f, const ow_grid* grid, const in
   A.ab_cnt = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_CNT];
   A.ab_off = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_OFF];
   A.cand_cnt = (int32_t*)ctx->slot_ptr[SLOT_LAT_CCNT];
+  A.cand_off = (int64_t*)ctx->slot_ptr[SLOT_LAT_COFF];
   A.cand_blocks = (int32_t*)ctx->slot_ptr[SLOT_LAT_LEAVES];
-  A.n_cb = ctx->d_small + 34;
+  A.pair_face = (int32_t*)ctx->slot_ptr[SLOT_LAT_PFACE];
+  A.pair_blk = (int32_t*)ctx->slot_ptr[SLOT_LAT_PBLK];
+  A.star = (uint32_t*)ctx->slot_ptr[SLOT_LAT_STAR];
+  A.n_star = (unsigned long long*)(ctx->d_small + 37);
   A.bcount = (int32_t*)ctx->slot_ptr[SLOT_LAT_BCOUNT];
   A.boff = (const int64_t*)ctx->slot_ptr[SLOT_LAT_BOFFS];
-  A.temp = (float*)ctx->slot_ptr[SLOT_LAT_TEMP];
+  A.qbits = (unsigned*)ctx->slot_ptr[SLOT_LAT_TEMP];
+  A.stats = (unsigned long long*)(ctx->d_small + 40);
+  A.n_cb = ctx->lat_ncb;
+  A.n_pairs = ctx->lat_pairs;
   return A;
 }
 
@@ -562,15 +570,16 @@ extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, const int
   void* p;
   const int64_t nl = n_leaves > 0 ? n_leaves : 1;
   OW_TRY(ow_slot(ctx, SLOT_LAT_CCNT, 4 * (size_t)nl, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_COFF, 8 * (size_t)nl, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_LEAVES, 4 * (size_t)nl, s, &p));
-  OW_TRY(ow_slot(ctx, SLOT_LAT_BCOUNT, 4 * (size_t)nl, s, &p));
-  OW_TRY(ow_slot(ctx, SLOT_LAT_BOFFS, 8 * (size_t)nl, s, &p));
   int8_t dirs3[QMAX * 3];
   memset(dirs3, 0, sizeof(dirs3));
   for (int i = 0; i < n_dirs; ++i)
     for (int a = 0; a < D; ++a) dirs3[i * 3 + a] = h_dirs[i * D + a];
   ctx->lat_leaves = n_leaves;
   ctx->lat_boundary = 0;
+  ctx->lat_ncb = 0;
+  ctx->lat_pairs = 0;
   ctx->lat_dirs = n_dirs;
   memcpy(ctx->lat_dir, dirs3, sizeof(dirs3));
   ctx->lat_coords = d_coords;
@@ -580,6 +589,8 @@ extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, const int
   ctx->lat_grid = *grid;
   ctx->lat_flags = d_flags;
   *out_boundary = 0;
+  OW_CUDA(cudaMemsetAsync(ctx->d_small + 37, 0, 8, s));
+  OW_CUDA(cudaMemsetAsync(ctx->d_small + 40, 0, 3 * 8, s));
   if (n_leaves <= 0) return OW_OK;
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
   LatArgs A = make_args(ctx, f, grid, dirs3, n_dirs, d_leaves, n_leaves);
@@ -587,23 +598,48 @@ extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, const int
   else k_lat_count<2><<<ow_blocks(n_leaves, CNT_WARPS), CNT_WARPS * 32, 0, s>>>(A);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
-  OW_TRY(scan(ctx, CandLoad{A.cand_cnt}, CandStore{A.cand_blocks}, n_leaves, ctx->d_small + 34, s));
-  int64_t n_cb;
-  OW_TRY(ow_readback(ctx, ctx->d_small + 34, 1, &n_cb, s));
-  ctx->lat_ncb = n_cb;
+  OW_TRY(scan(ctx, CandLoad{A.cand_cnt}, CandStore{A.cand_off, A.cand_blocks}, n_leaves, ctx->d_small + 34, s));
   OW_CUDA(cudaMemsetAsync(d_flags, 0, 4 * (size_t)n_leaves * C, s));
-  A.flags = d_flags;
-  if (n_cb > 0) {
-    // q rows of the candidate blocks (boundary cells only are written)
-    OW_TRY(ow_slot(ctx, SLOT_LAT_TEMP, 4 * (size_t)n_cb * C * n_dirs, s, &p));
-    A.temp = (float*)p;
-    if (D == 3) k_lattice<3><<<(unsigned)n_cb, LAT_THREADS, 0, s>>>(A);
-    else k_lattice<2><<<(unsigned)n_cb, LAT_THREADS, 0, s>>>(A);
-    OW_LAUNCHED(ctx);
-    OW_CHECK_LAUNCH();
+  int64_t tot;
+  OW_TRY(ow_readback(ctx, ctx->d_small + 34, 1, &tot, s));
+  const int64_t n_pairs = tot >> 32, n_cb = tot & 0xffffffffll;
+  ctx->lat_ncb = n_cb;
+  ctx->lat_pairs = n_pairs;
+  if (n_pairs * C >= (int64_t(1) << 32)) {
+    ow_set_error("lattice: %lld candidate pairs exceed the 32-bit item encoding", (long long)n_pairs);
+    return OW_ERR_CAPACITY;
   }
-  OW_TRY(scan(ctx, BcountLoad{A.bcount, A.n_cb}, ow::StoreExcl<int64_t>{(int64_t*)A.boff}, n_cb,
-              ctx->d_small + 35, s));
+  if (n_cb > 0) {
+    OW_TRY(ow_slot(ctx, SLOT_LAT_PFACE, 4 * (size_t)n_pairs, s, &p));
+    OW_TRY(ow_slot(ctx, SLOT_LAT_PBLK, 4 * (size_t)n_pairs, s, &p));
+    OW_TRY(ow_slot(ctx, SLOT_LAT_STAR, 4 * (size_t)n_pairs * C, s, &p));
+    OW_TRY(ow_slot(ctx, SLOT_LAT_TEMP, 4 * (size_t)n_cb * C * n_dirs, s, &p));
+    OW_TRY(ow_slot(ctx, SLOT_LAT_BCOUNT, 4 * (size_t)n_cb, s, &p));
+    OW_TRY(ow_slot(ctx, SLOT_LAT_BOFFS, 8 * (size_t)n_cb, s, &p));
+    A = make_args(ctx, f, grid, dirs3, n_dirs, d_leaves, n_leaves);
+    A.flags = d_flags;
+    OW_CUDA(cudaMemsetAsync(A.qbits, 0x7f, 4 * (size_t)n_cb * C * n_dirs, s));  // 3.39e38 > any t <= 1
+    OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
+    const int grid_items = 8 * OW_SMS;
+    if (D == 3) {
+      k_lat_pairs<3><<<ow_blocks(n_cb, CNT_WARPS), CNT_WARPS * 32, 0, s>>>(A);
+      k_lat_star<3><<<ow_blocks(n_pairs * C, 256, grid_items), 256, 0, s>>>(A);
+      k_lat_links<3><<<grid_items, 256, 0, s>>>(A);
+      k_lat_bcount<3><<<ow_blocks(n_cb, 8), 256, 0, s>>>(A);
+    } else {
+      k_lat_pairs<2><<<ow_blocks(n_cb, CNT_WARPS), CNT_WARPS * 32, 0, s>>>(A);
+      k_lat_star<2><<<ow_blocks(n_pairs * C, 256, grid_items), 256, 0, s>>>(A);
+      k_lat_links<2><<<grid_items, 256, 0, s>>>(A);
+      k_lat_bcount<2><<<ow_blocks(n_cb, 8), 256, 0, s>>>(A);
+    }
+    OW_PROF_END(ctx, PROF_LAT_SWEEP, s);
+    ctx->launches += 4;
+    OW_CHECK_LAUNCH();
+    OW_TRY(scan(ctx, ow::LoadArr<int32_t>{A.bcount}, ow::StoreExcl<int64_t>{(int64_t*)A.boff}, n_cb,
+                ctx->d_small + 35, s));
+  } else {
+    OW_CUDA(cudaMemsetAsync(ctx->d_small + 35, 0, 8, s));
+  }
   OW_PROF_END(ctx, PROF_LATTICE, s);
   int64_t nb;
   OW_TRY(ow_readback(ctx, ctx->d_small + 35, 1, &nb, s));
@@ -618,7 +654,7 @@ extern "C" int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, 
     ow_set_error("ow_lattice_links_emit without ow_lattice_links_count");
     return OW_ERR_INVALID;
   }
-  if (ctx->lat_boundary == 0 || ctx->lat_leaves == 0) return OW_OK;
+  if (ctx->lat_boundary == 0 || ctx->lat_ncb == 0) return OW_OK;
   LatArgs A = make_args(ctx, &ctx->lat_forest, &ctx->lat_grid, ctx->lat_dir, ctx->lat_dirs, ctx->lat_leaves_ptr,
                         ctx->lat_leaves);
   A.flags = ctx->lat_flags;
@@ -632,4 +668,8 @@ extern "C" int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, 
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;
+}
+
+extern "C" int ow_lattice_stats(ow_ctx* ctx, int64_t* out3, void* stream) {
+  return ow_readback(ctx, ctx->d_small + 40, 3, out3, (cudaStream_t)stream);
 }
