@@ -153,7 +153,7 @@ def gpu_arm(args, cfg, rank, world, local_rank):
 
     def step(records):
         geom = import_geom(records)
-        forest = ow.init_root_grid(dom, (cfg["root"],) * dim, capacity=8 * cfg["root"] ** dim)
+        forest = ow.init_root_grid(dom, (cfg["root"],) * dim, capacity=32 * cfg["root"] ** dim)
         res = ow.refine_near_wall(forest, geom, params, shard=shard)
         ll = ow.build_lattice_links(forest, geom, None, cfg["lattice"])
         return res, forest, ll
@@ -168,7 +168,7 @@ def gpu_arm(args, cfg, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 1)):  # >= 1 untimed step sizes every buffer
         res, forest, ll = step(rec_dev if not text else None)
     T_step = int(sum(res.cell_face_tests))
     evaluated = int(sum(res.pairs_evaluated))
@@ -272,11 +272,12 @@ def gpu_arm(args, cfg, rank, world, local_rank):
                  f"{FP32_OPS_PER_TEST[dim]} FP32 ops per evaluated cell-face predicate x {evaluated} per step "
                  f"(pairs surviving the reference's box + sphere culls)", "mark")
     sw_ms, sw_n = prof["lattice_sweep"]
-    star, box, mt = lat_stats
-    lat_ops = (6 * star + 6 * box + 45 * mt) if dim == 3 else (4 * star + 4 * box + 13 * mt)
-    lattice = entry("k_lattice (boundary-link sweep)", sw_ms, sw_n, lat_ops * args.steps,
-                    f"per step: {star} star-box tests x 6 cmp + {box} link-box tests x 6 cmp + {mt} "
-                    f"Moller-Trumbore tests x 45 FP32 ops", "lattice")
+    n_cb, n_rows, mt = lat_stats
+    per_mt = 45 if dim == 3 else 13
+    lattice = entry("k_lat_mt (boundary-link intersection sweep)", sw_ms, sw_n, per_mt * mt * args.steps,
+                    f"per step: {mt} {'Moller-Trumbore' if dim == 3 else 'segment-segment'} link-face tests x "
+                    f"{per_mt} FP32 ops ({n_rows} (block, face, direction) rows over {n_cb} candidate blocks; "
+                    f"every test is a link whose AABB meets the face AABB)", "lattice")
     dominant = lattice if sw_ms >= mark_ms else mark
     roofline = dict(dominant)
     roofline["secondary"] = mark if dominant is lattice else lattice

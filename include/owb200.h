@@ -147,11 +147,16 @@ int ow_forest_cell_centers(ow_ctx* ctx, const ow_forest* f, const int32_t* d_ids
  * balance (refine_marked, forest.py:331-370).  *out_split = blocks split. */
 int ow_refine_marked(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, void* stream);
 
+/* Fill the root grid: blocks 0..R-1 at level 0, x-fastest lattice coordinates
+ * (init_root_grid, forest.py:48-81, 405-409); sets f->n_blocks = R. */
+int ow_forest_init_root(ow_ctx* ctx, ow_forest* f, void* stream);
+
 /* ---- near-wall detection (nearwall.py) ------------------------------------- */
 /* Mark leaves `d_leaves` (ascending, at one level) whose cell centres pass the
  * FP32 near-face predicate at d_spec for a candidate face: every face (naive,
  * d_bin_ids == NULL; mark_near_wall_naive nearwall.py:217) or the faces of the
- * cell's bin (mark_near_wall_binned nearwall.py:253).  `reach` is the
+ * cell's bin (mark_near_wall_binned nearwall.py:253; n_bin_entries = length of
+ * d_bin_ids).  `reach` is the
  * reference's conservative cull radius (nearwall.py:38-40).  Outputs:
  * *out_marked newly MARKED blocks; *out_tests the algorithmic cell-face test
  * count T; *out_evaluated the pairs that reached the full
@@ -159,12 +164,55 @@ int ow_refine_marked(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_spli
 int ow_mark_near_wall(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
                       const float* d_coords, int64_t n_faces, int64_t geom_key, const ow_grid* grid,
                       const int32_t* d_bin_ids, const int32_t* d_bin_counts, const int32_t* d_bin_offsets,
-                      float d_spec, double reach, int64_t* out_marked, int64_t* out_tests,
+                      int64_t n_bin_entries, float d_spec, double reach, int64_t* out_marked, int64_t* out_tests,
                       int64_t* out_evaluated, void* stream);
 /* `rounds` two-pass dilation rounds over leaves `d_leaves` (propagate_marks,
  * nearwall.py:321-366). */
 int ow_propagate_marks(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
                        int32_t rounds, void* stream);
+
+/* ---- native per-level driver (refine_near_wall, nearwall.py:430-491) -------- */
+#define OW_MAX_PASSES 26
+/* Multi-GPU hook: after a rank marked leaves [lo, hi) of d_leaves (all
+ * n_leaves leaves of `level`, ascending), make every rank's forest marks of
+ * all n_leaves leaves identical and sum stats[3] (marked, tests, evaluated)
+ * over ranks.  Return 0 on success. */
+typedef int (*ow_exchange_fn)(void* user, int32_t level, const int32_t* d_leaves, int64_t n_leaves, int64_t lo,
+                              int64_t hi, int64_t* stats3);
+typedef struct {
+  float d_spec;           /* float32(d_spec): predicate distance */
+  int32_t n_levels;       /* NearWallParams.n_levels */
+  double d_spec64;        /* Python float d_spec: propagation rounds */
+  double reach;           /* conservative cull reach (nearwall.py:38-40) */
+  int32_t binned;         /* strategy: 1 "binned", 0 "naive" */
+  int32_t reuse_bins;     /* 1: build the bin CSR once (identical every level) */
+  float spacing;          /* fill_bins sample spacing h */
+  int32_t rank, world;    /* marking shard of this process (world <= 1: all) */
+  int64_t overlap_factor; /* fill_bins capacity = overlap_factor * n_faces */
+  int64_t bin_fraction;   /* B_f (only shapes the capacity-error message) */
+  ow_exchange_fn exchange;
+  void* exchange_user;
+} ow_nearwall_params;
+typedef struct {
+  int32_t n_passes;
+  int32_t bins_built;
+  int64_t bin_entries;
+  int64_t marked_detected[OW_MAX_PASSES];
+  int64_t marked_refined[OW_MAX_PASSES];
+  int64_t n_split[OW_MAX_PASSES];
+  int64_t tests[OW_MAX_PASSES];     /* algorithmic cell-face tests T */
+  int64_t evaluated[OW_MAX_PASSES];
+  float stage_ms[OW_MAX_PASSES][4]; /* bin_setup, face_detection, propagation, refinement (CUDA events) */
+} ow_nearwall_result;
+/* The whole level loop in one call: per level L in 0..n_levels-2, bins (binned;
+ * built into the caller's d_bin_* buffers, d_bin_ids of bin_ids_capacity
+ * entries) -> mark leaves at L -> propagate (binned) -> refine.  Geometry
+ * validation (degenerate faces, domain) is the caller's, as in the reference
+ * it precedes the loop.  Errors carry the reference's messages. */
+int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_faces, int64_t geom_key,
+                        const ow_grid* grid, const ow_nearwall_params* params, int32_t* d_bin_ids,
+                        int64_t bin_ids_capacity, int32_t* d_bin_counts, int32_t* d_bin_offsets,
+                        ow_nearwall_result* out, void* stream);
 
 /* Cell-face links (build_cell_face_links, nearwall.py:522-594), two phases.
  * Count: per leaf cell the faces of its bin within d_link.  On overflow of
@@ -180,18 +228,20 @@ int ow_cell_face_links_emit(ow_ctx* ctx, int64_t* d_block_ids, int64_t* d_cell_i
 
 /* ---- lattice boundary links (north-star extension) -------------- */
 /* Q directions d_dirs[Q][dim] (int8) of a DnQm lattice; links of every cell of
- * leaves `d_leaves` (finest level) tested against faces with FP32
- * Moller-Trumbore (3D) / segment-segment (2D).  Phase 1 writes d_flags
+ * leaves `d_leaves` (all at `level`, the finest level) tested with FP32
+ * Moller-Trumbore (3D) / segment-segment (2D) against every face whose float32
+ * AABB meets the link's AABB.  `grid` is optional and unused (kept for ABI
+ * stability: candidates come from the forest itself).  Phase 1 writes d_flags
  * [n_leaves * 4^D] (bit i = link i hits) and returns the boundary-cell count;
  * phase 2 writes d_cells (flat cell index, ascending) and d_q [nb][Q] = min t
  * (-1 for no hit). */
-int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
-                           const float* d_coords, int64_t n_faces, int64_t geom_key, const ow_grid* grid,
-                           const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags, int64_t* out_boundary,
-                           void* stream);
+int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_leaves,
+                           int64_t n_leaves, const float* d_coords, int64_t n_faces, int64_t geom_key,
+                           const ow_grid* grid, const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags,
+                           int64_t* out_boundary, void* stream);
 int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, void* stream);
-/* Work counters of the last ow_lattice_links_count: [0] star-box tests,
- * [1] link-AABB tests, [2] Moller-Trumbore / segment tests (roofline). */
+/* Work counters of the last ow_lattice_links_count: [0] candidate blocks,
+ * [1] (block, face, direction) rows, [2] Moller-Trumbore / segment tests. */
 int ow_lattice_stats(ow_ctx* ctx, int64_t* out3, void* stream);
 
 /* ---- predicate probe (parity tests) ---------------------------------------- */

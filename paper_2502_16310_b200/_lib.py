@@ -74,6 +74,43 @@ class FaceSummary(C.Structure):  # ow_face_summary
     ]
 
 
+MAX_PASSES = 26  # OW_MAX_PASSES
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                          C.POINTER(C.c_int64))
+
+
+class NearWallParamsC(C.Structure):  # ow_nearwall_params
+    _fields_ = [
+        ("d_spec", C.c_float),
+        ("n_levels", C.c_int32),
+        ("d_spec64", C.c_double),
+        ("reach", C.c_double),
+        ("binned", C.c_int32),
+        ("reuse_bins", C.c_int32),
+        ("spacing", C.c_float),
+        ("rank", C.c_int32),
+        ("world", C.c_int32),
+        ("overlap_factor", C.c_int64),
+        ("bin_fraction", C.c_int64),
+        ("exchange", EXCHANGE_FN),
+        ("exchange_user", C.c_void_p),
+    ]
+
+
+class NearWallResultC(C.Structure):  # ow_nearwall_result
+    _fields_ = [
+        ("n_passes", C.c_int32),
+        ("bins_built", C.c_int32),
+        ("bin_entries", C.c_int64),
+        ("marked_detected", C.c_int64 * MAX_PASSES),
+        ("marked_refined", C.c_int64 * MAX_PASSES),
+        ("n_split", C.c_int64 * MAX_PASSES),
+        ("tests", C.c_int64 * MAX_PASSES),
+        ("evaluated", C.c_int64 * MAX_PASSES),
+        ("stage_ms", (C.c_float * 4) * MAX_PASSES),
+    ]
+
+
 P = C.c_void_p
 I32, I64, F32, F64 = C.c_int32, C.c_int64, C.c_float, C.c_double
 PI64 = C.POINTER(C.c_int64)
@@ -97,13 +134,16 @@ _SIGS = {
     "ow_forest_count_marks": [P, C.POINTER(ForestView), I32, I32, I32, PI64, P],
     "ow_forest_cell_centers": [P, C.POINTER(ForestView), P, I64, P, P],
     "ow_refine_marked": [P, C.POINTER(ForestView), I32, PI64, P],
-    "ow_mark_near_wall": [P, C.POINTER(ForestView), P, I64, P, I64, I64, C.POINTER(Grid), P, P, P, F32, F64,
+    "ow_mark_near_wall": [P, C.POINTER(ForestView), P, I64, P, I64, I64, C.POINTER(Grid), P, P, P, I64, F32, F64,
                           PI64, PI64, PI64, P],
     "ow_propagate_marks": [P, C.POINTER(ForestView), P, I64, I32, P],
+    "ow_forest_init_root": [P, C.POINTER(ForestView), P],
+    "ow_refine_near_wall": [P, C.POINTER(ForestView), P, I64, I64, C.POINTER(Grid), C.POINTER(NearWallParamsC), P,
+                            I64, P, P, C.POINTER(NearWallResultC), P],
     "ow_cell_face_links_count": [P, C.POINTER(ForestView), P, I64, P, I64, I64, C.POINTER(Grid), P, P, P, F32, F64,
                                  I64, PI64, PI64, P],
     "ow_cell_face_links_emit": [P, P, P, P, P, P],
-    "ow_lattice_links_count": [P, C.POINTER(ForestView), P, I64, P, I64, I64, C.POINTER(Grid), P, I32, P, PI64, P],
+    "ow_lattice_links_count": [P, C.POINTER(ForestView), I32, P, I64, P, I64, I64, C.POINTER(Grid), P, I32, P, PI64, P],
     "ow_lattice_links_emit": [P, P, P, P],
     "ow_lattice_stats": [P, PI64, P],
     "ow_near_pairs": [P, I32, P, P, P, I64, P, P],
@@ -180,7 +220,7 @@ PROF_IDS = {"mark": 0, "lattice": 1, "fill_bins": 2, "refine": 3, "propagate": 4
 
 
 def lattice_stats():
-    """(star-box, link-box, intersection) test counts of the last lattice call."""
+    """(candidate blocks, rows, intersection tests) of the last lattice call."""
     out = (C.c_int64 * 3)()
     call("ow_lattice_stats", ctx(), out, stream())
     return tuple(int(x) for x in out)

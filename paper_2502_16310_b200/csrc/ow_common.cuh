@@ -56,21 +56,23 @@ enum ow_slot {
   SLOT_LINK_OFF,
   SLOT_LINK_CELLOFF,
   SLOT_LINK_LEAVES,
-  SLOT_LAT_BCOUNT,
-  SLOT_LAT_BOFF,
-  SLOT_LAT_LEAVES,
-  SLOT_LAT_FLAGS,
-  SLOT_ABIN_IDS,       // AABB-overlap bin CSR (lattice candidates)
-  SLOT_ABIN_CNT,
-  SLOT_ABIN_OFF,
-  SLOT_LAT_REC,        // packed 64-byte face records (lattice candidates)
-  SLOT_LAT_CCNT,       // candidates per finest block
+  SLOT_LAT_BCOUNT,     // boundary cells per candidate block
   SLOT_LAT_BOFFS,      // boundary-row offsets per candidate block
-  SLOT_LAT_TEMP,       // q rows staging
-  SLOT_LAT_COFF,       // packed pair offset / candidate-block rank per finest block
-  SLOT_LAT_PFACE,      // (block, face) pairs: face
-  SLOT_LAT_PBLK,       // (block, face) pairs: block position
-  SLOT_LAT_STAR,       // (pair, cell) items passing the star-box test
+  SLOT_LAT_LEAVES,     // candidate-block leaf positions
+  SLOT_LAT_RANK,       // candidate-block rank per leaf position
+  SLOT_LAT_POS,        // leaf position per block id
+  SLOT_LAT_HAS,        // leaf has at least one candidate row
+  SLOT_LAT_CEN,        // per-leaf float32 cell-centre coordinates [D][4]
+  SLOT_LAT_REC,        // packed face records (v0, e1, e2)
+  SLOT_LAT_FCNT,       // rows per face -> row offsets
+  SLOT_LAT_ROWS,       // (leaf, face, block, direction|cell ranges) rows
+  SLOT_LAT_ROWOFF,     // units per row -> unit offsets
+  SLOT_LAT_TILEROW,    // first row of each intersection tile
+  SLOT_LAT_HITS,       // hit list (flat cell, t bits)
+  SLOT_LAT_HITDIR,     // hit list directions
+  SLOT_LAT_BMASK,      // boundary-cell mask per candidate block
+  SLOT_MARK_CBOX,      // union boxes of 32-entry bin chunks (marking cull)
+  SLOT_DRV_LEAVES,     // native driver: leaves of the current level
   SLOT_MISC,
   SLOT_COUNT
 };
@@ -116,18 +118,19 @@ struct ow_ctx {
   ow_forest link_forest;
   ow_grid link_grid;
   // lattice phase state
-  int64_t lat_leaves, lat_boundary, lat_faces;
-  int32_t lat_dirs;
+  int64_t lat_leaves, lat_boundary, lat_faces, lat_ncb, lat_rows, lat_units;
+  int32_t lat_dirs, lat_level;
   int8_t lat_dir[27 * 3];
   const float* lat_coords;
   const int32_t* lat_leaves_ptr;
   uint32_t* lat_flags;
-  int64_t lat_key, lat_ncb, lat_pairs;
   ow_forest lat_forest;
-  ow_grid lat_grid;
-  int64_t abin_key;
-  int32_t abin_B, abin_dim;
+  void* stage_events;  // native driver CUDA events
 };
+
+// refine_marked returning the MARKED-leaf count of the split pass as well
+int ow_refine_marked_counted(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, int64_t* out_marked,
+                             cudaStream_t s);
 
 // Scratch slot of at least `bytes`; contents are preserved across calls unless
 // the slot grows (then it is reallocated, stream-ordered, uninitialised).

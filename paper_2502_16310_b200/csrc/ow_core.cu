@@ -32,7 +32,6 @@ extern "C" int ow_ctx_create(int device, ow_ctx** out) {
   }
   c->device = device;
   c->prep_key = -1;
-  c->abin_key = -1;
   cudaError_t e = cudaMallocHost((void**)&c->h_pinned, 64 * sizeof(int64_t));
   if (e == cudaSuccess) e = cudaMalloc((void**)&c->d_small, 64 * sizeof(int64_t));
   if (e != cudaSuccess) {
@@ -50,6 +49,19 @@ extern "C" int ow_ctx_destroy(ow_ctx* c) {
   cudaDeviceSynchronize();
   for (int i = 0; i < SLOT_COUNT; ++i)
     if (c->slot_ptr[i]) cudaFree(c->slot_ptr[i]);
+  if (c->stage_events) {
+    cudaEvent_t* ev = (cudaEvent_t*)c->stage_events;  // StageEvents starts with its event table
+    for (int i = 0; i < OW_MAX_PASSES * 5; ++i)
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    free(c->stage_events);
+  }
+  if (c->prof) {
+    for (int i = 0; i < PROF_N; ++i)
+      for (int k = 0; k < PROF_MAX; ++k)
+        for (int j = 0; j < 2; ++j)
+          if (c->prof->ev[i][k][j]) cudaEventDestroy(c->prof->ev[i][k][j]);
+    free(c->prof);
+  }
   cudaFreeHost(c->h_pinned);
   cudaFree(c->d_small);
   free(c);

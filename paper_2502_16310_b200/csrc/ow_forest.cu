@@ -265,17 +265,24 @@ extern "C" int ow_propagate_marks(ow_ctx* ctx, const ow_forest* f, const int32_t
   return OW_OK;
 }
 
-static int refine_marked_impl(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, cudaStream_t s);
+static int refine_marked_impl(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, int64_t* out_marked,
+                              cudaStream_t s);
 
 extern "C" int ow_refine_marked(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
+  int64_t m;
+  return ow_refine_marked_counted(ctx, f, level, out_split, &m, (cudaStream_t)stream);
+}
+
+int ow_refine_marked_counted(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, int64_t* out_marked,
+                             cudaStream_t s) {
   OW_PROF_BEGIN(ctx, PROF_REFINE, s);
-  int st = refine_marked_impl(ctx, f, level, out_split, s);
+  int st = refine_marked_impl(ctx, f, level, out_split, out_marked, s);
   OW_PROF_END(ctx, PROF_REFINE, s);
   return st;
 }
 
-static int refine_marked_impl(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, cudaStream_t s) {
+static int refine_marked_impl(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, int64_t* out_marked,
+                              cudaStream_t s) {
   int64_t* small = ctx->d_small;
   void* pl;
   OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(f->n_blocks + 1), s, &pl));
@@ -289,6 +296,7 @@ static int refine_marked_impl(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t*
   }
   int64_t m = h[0], n_split = m;
   *out_split = 0;
+  *out_marked = m;
   if (m == 0) return OW_OK;
   if (level >= f->max_level) {
     ow_set_error("refinement beyond max level %d", f->max_level);

@@ -1,23 +1,30 @@
 // Lattice boundary links + wall-distance fractions q on the finest level
 // (north-star extension; no reference counterpart, oracle/lattice.py is the
-// checker and DESIGN.md §Lattice links the definition).
+// checker and DESIGN.md §5 the definition).
 //
-// Candidates come from an AABB-overlap bin CSR (a face is stored in every bin
-// its float32 AABB touches) plus a packed 64-byte record per face (v0, edge
-// vectors, float32 box, first bin), built once per (geometry, grid).
-// The work is flattened into three independent item lists so every stage
-// runs at full occupancy without per-block serial latency:
-//   k_lat_count : warp per finest leaf block, counts the faces whose box meets
-//                 the block box grown by two cells (each face once: in the
-//                 first bin of its range ∩ the block's range).
-//   scan        : pair offsets + candidate-block ranks (one packed scan).
-//   k_lat_pairs : (block, face) candidate pairs.
-//   k_lat_star  : (pair, cell) items whose cell star box — the union of its
-//                 link boxes — meets the face box.
-//   k_lat_links : per item, every direction: exact float32 link-AABB test,
-//                 then Moller-Trumbore (3D) / segment-segment (2D) with a fixed
-//                 op order; atomicOr flag bits, atomicMin q bits.
-//   k_lat_bcount + scan + k_lat_emit : boundary rows in (block, cell) order.
+// A link (cell, direction d) is tested against face f iff the face's float32
+// AABB meets the link's float32 AABB [min(x, x+c_d h), max(x, x+c_d h)].  That
+// test is separable per axis and monotone in the cell index along the axis
+// (cell centres and fl(x + c h) are non-decreasing in the index), so for one
+// (finest block, face) pair the cells whose d-link box meets the face box form
+// an axis-aligned sub-box of the 4^D cells: [i0, i0+ext) per axis, one range per
+// (axis, c in {-1,0,+1}).  The sweep therefore never tests boxes cell by cell:
+//
+//   k_lat_pos    : pos_of[leaf id] = leaf position, per-leaf cell-centre table.
+//   k_lat_faces  : warp per face; walks the finest-level lattice blocks its box
+//                  can reach (root-lattice descent, no bins), computes the
+//                  per-axis cell ranges of each existing finest leaf and emits
+//                  one row per (leaf, face, direction) with a non-empty cell
+//                  box and a non-zero determinant (count pass, then EMIT).
+//   scans        : row/unit offsets per face, candidate-block ranks, unit
+//                  offsets per row (+ the first row of every MT tile).
+//   k_lat_mt     : one thread per (row, cell) unit, load-balanced over rows
+//                  staged in shared memory with their per-row Moller-Trumbore
+//                  terms (p = d x e2, det); per unit the FP32 test with a fixed
+//                  op order (divisions only for hits); atomicOr flag bits and
+//                  a compact hit list (cell, direction, t).
+//   k_lat_bcount + scan : boundary rows in (block, cell) order.
+//   k_lat_emit + k_lat_hits : cells, q rows (-1 / min t via atomicMin).
 #include "ow_scan.cuh"
 #include <string.h>
 
@@ -25,24 +32,105 @@ namespace {
 
 using ow::scan;
 
-constexpr int LAT_THREADS = 256;
 constexpr int QMAX = 27;
-constexpr int CNT_WARPS = 8;
+constexpr int MT_THREADS = 256;
+constexpr int MT_ITEMS = 2;
+constexpr int MT_TILE = MT_THREADS * MT_ITEMS;
 
-struct Dirs {
-  int8_t c[QMAX][3];
+// row record: x = leaf position, y = face,
+// z = dir | (i0_a | (ext_a-1) << 2) << (5 + 4a), w = units of the row
+struct LatArgs {
+  ForestC F;
+  int nq, level;
+  float h[3];               // finest cell size per axis (float32 of the FP64 value)
+  float dv[QMAX][3];        // link vectors c_d * h (exact)
+  const float* coords;
+  int64_t n_faces;
+  const int32_t* leaves;
+  int64_t n_leaves;
+  int32_t* pos_of;          // [n_blocks]
+  float* cen;               // [n_leaves][D][4] cell-centre coordinates
+  uint8_t* has_pair;        // [n_leaves]
+  float4* rec;              // [n_faces * 3] (v0, e1, e2) / (a, s)
+  int64_t* fcnt;            // [n_faces] rows | units << 32 per face -> exclusive offsets
+  int4* rows;               // [R]
+  int64_t* rowoff;          // [R] units per row -> exclusive unit offsets
+  int32_t* tile_row;        // [n_tiles] row of the first unit of each MT tile
+  int64_t n_rows, n_units;
+  int32_t* cand_rank;       // [n_leaves]
+  int32_t* cand_blocks;     // [n_cb]
+  int64_t n_cb;
+  uint32_t* flags;          // [n_leaves * C]
+  uint2* hits;              // [<= n_units] (flat cell, t bits)
+  uint8_t* hit_dir;         // [<= n_units] direction of each hit
+  unsigned long long* n_hits;
+  int32_t* bcount;          // [n_cb] boundary cells per candidate block
+  unsigned long long* bmask;  // [n_cb] boundary-cell mask
+  const int64_t* boff;      // [n_cb]
+  int64_t* cells_out;
+  float* q_out;
 };
 
 template <int D>
-__device__ __forceinline__ void face_verts(const float* __restrict__ c, int64_t n, int64_t f, float v[3][3]) {
+__global__ void k_lat_pos(ForestC F, int level, const int32_t* __restrict__ leaves, int64_t n, int32_t* pos_of,
+                          uint8_t* has_pair, float* cen) {
+  double q[3];
+#pragma unroll
+  for (int a = 0; a < D; ++a) q[a] = block_len(F, a, level);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int id = leaves[i];
+    pos_of[id] = (int32_t)i;
+    has_pair[i] = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {  // forest.py:187-205: f32(o + u q), u = (i + 1/2) / 4
+      const double o = DADD(F.dmin[a], DMUL((double)F.coord[a][id], q[a]));
+      float4 v;
+      v.x = __double2float_rn(DADD(o, DMUL(0.125, q[a])));
+      v.y = __double2float_rn(DADD(o, DMUL(0.375, q[a])));
+      v.z = __double2float_rn(DADD(o, DMUL(0.625, q[a])));
+      v.w = __double2float_rn(DADD(o, DMUL(0.875, q[a])));
+      reinterpret_cast<float4*>(cen)[i * D + a] = v;
+    }
+  }
+}
+
+// Per-axis cell ranges of one (block, face) pair: for c in {-1,0,+1} the
+// contiguous set of cell indices i whose link box [min(x_i, e_i), max(x_i, e_i)],
+// e_i = fl(x_i + c h), meets [lo, hi] — the per-cell test of oracle/lattice.py
+// on the same float32 centres.  4 bits (i0 | (ext-1) << 2), 0xF0 when empty.
+__device__ __forceinline__ void axis_ranges(const float4 x4, float h, float lo, float hi, unsigned* r3) {
+  const float x[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+  for (int ci = 0; ci < 3; ++ci) {
+    const float dv = FMUL((float)(ci - 1), h);
+    unsigned m = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float en = FADD(x[i], dv);
+      m |= (unsigned)(lo <= fmaxf(x[i], en) && hi >= fminf(x[i], en)) << i;
+    }
+    r3[ci] = m == 0 ? 0xF0u : (unsigned)(__ffs(m) - 1) | ((unsigned)(__popc(m) - 1) << 2);  // contiguous
+  }
+}
+
+// Warp per face: lane 0 packs the face record; lanes test the directions'
+// determinants (a link parallel to the face plane never hits: Moller-Trumbore
+// and the segment test reject det == 0), then walk the finest-level lattice
+// blocks the face box can reach (root-lattice descent, no bins).  Link boxes of
+// block k span [o_k - q/8, o_k + 9q/8]; a 0.01-block margin absorbs float
+// rounding and the exact per-axis range test filters.
+// Count pass: rows | units << 32 per face, has_pair per leaf.  EMIT: the rows
+// in slot order (warp prefix) and their unit counts.
+template <int D, bool EMIT>
+__global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t f = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (f >= A.n_faces) return;
+  float v[3][3], lo[3], hi[3], e1[3], e2[3];
 #pragma unroll
   for (int j = 0; j < D; ++j)
 #pragma unroll
-    for (int a = 0; a < D; ++a) v[j][a] = c[((int64_t)j * D + a) * n + f];
-}
-
-template <int D>
-__device__ __forceinline__ void vert_box(const float v[3][3], float* lo, float* hi) {
+    for (int a = 0; a < D; ++a) v[j][a] = A.coords[((int64_t)j * D + a) * A.n_faces + f];
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     lo[a] = v[0][a];
@@ -52,435 +140,308 @@ __device__ __forceinline__ void vert_box(const float v[3][3], float* lo, float* 
       lo[a] = fminf(lo[a], v[j][a]);
       hi[a] = fmaxf(hi[a], v[j][a]);
     }
+    e1[a] = FSUB(v[1][a], v[0][a]);  // e1 = v1 - v0 (3D) / s = b - a (2D), oracle/lattice.py
+    e2[a] = D == 3 ? FSUB(v[2][a], v[0][a]) : 0.0f;
   }
-}
-
-// ---- AABB-overlap bin CSR + packed face records ------------------------------
-template <int D>
-__device__ __forceinline__ int64_t abin_range(const GridC& g, const float* lo, const float* hi, int* blo, int* ext) {
-  int64_t v = 1;
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    blo[a] = bin_axis(lo[a], g.min32[a], g.len32[a], g.B);
-    ext[a] = bin_axis(hi[a], g.min32[a], g.len32[a], g.B) - blo[a] + 1;
-    v *= ext[a];
-  }
-  return v;
-}
-
-template <int D>
-struct AbinCountLoad {
-  GridC g;
-  const float* c;
-  int64_t n;
-  __device__ int64_t operator()(int64_t f) const {
-    float v[3][3], lo[3], hi[3];
-    int bl[3], ex[3];
-    face_verts<D>(c, n, f, v);
-    vert_box<D>(v, lo, hi);
-    return abin_range<D>(g, lo, hi, bl, ex);
-  }
-};
-
-// record layout (float4 x 4):
-//  3D: [v0.xyz lo.x] [e1.xyz lo.y] [e2.xyz lo.z] [hi.xyz binlo]
-//  2D: [a.xy s.xy]   [lo.xy hi.xy] [binlo 0 0 0] [0 0 0 0]
-// binlo packs the face's first bin per axis, 10 bits each (B <= 1024).
-template <int D>
-__global__ void k_abin_emit(GridC g, const float* __restrict__ c, int64_t n, const int64_t* foff, uint32_t* keys,
-                            int32_t* vals, int32_t* counts, float4* rec) {
-  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= n) return;
-  float v[3][3], lo[3], hi[3];
-  int bl[3] = {0, 0, 0}, ex[3];
-  face_verts<D>(c, n, f, v);
-  vert_box<D>(v, lo, hi);
-  int64_t cnt = abin_range<D>(g, lo, hi, bl, ex);
-  unsigned packed = (unsigned)bl[0] | ((unsigned)bl[1] << 10) | ((unsigned)(D == 3 ? bl[2] : 0) << 20);
-  float pk = __uint_as_float(packed);
-  if (D == 3) {
-    rec[4 * f + 0] = make_float4(v[0][0], v[0][1], v[0][2], lo[0]);
-    rec[4 * f + 1] = make_float4(FSUB(v[1][0], v[0][0]), FSUB(v[1][1], v[0][1]), FSUB(v[1][2], v[0][2]), lo[1]);
-    rec[4 * f + 2] = make_float4(FSUB(v[2][0], v[0][0]), FSUB(v[2][1], v[0][1]), FSUB(v[2][2], v[0][2]), lo[2]);
-    rec[4 * f + 3] = make_float4(hi[0], hi[1], hi[2], pk);
-  } else {
-    rec[4 * f + 0] = make_float4(v[0][0], v[0][1], FSUB(v[1][0], v[0][0]), FSUB(v[1][1], v[0][1]));
-    rec[4 * f + 1] = make_float4(lo[0], lo[1], hi[0], hi[1]);
-    rec[4 * f + 2] = make_float4(pk, 0.0f, 0.0f, 0.0f);
-    rec[4 * f + 3] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-  }
-  int64_t pos = foff[f];
-  for (int64_t k = 0; k < cnt; ++k) {
-    int64_t rem = k, lin = 0, mul = 1;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      lin += (int64_t)(bl[a] + rem % ex[a]) * mul;
-      rem /= ex[a];
-      mul *= g.B;
-    }
-    keys[pos + k] = (uint32_t)lin;
-    vals[pos + k] = (int32_t)f;
-    atomicAdd(&counts[lin], 1);
-  }
-}
-
-template <int D>
-int build_abins(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, int64_t key, cudaStream_t s) {
-  int64_t nb = 1;
-  for (int a = 0; a < D; ++a) nb *= g.B;
-  if (g.B > 1024) {
-    ow_set_error("lattice candidate grid limited to 1024 bins per axis");
-    return OW_ERR_INVALID;
-  }
-  if (key >= 0 && ctx->abin_key == key && ctx->abin_B == g.B && ctx->abin_dim == D) return OW_OK;
-  void *pfo, *pcnt, *poff, *prec;
-  OW_TRY(ow_slot(ctx, SLOT_LAT_BOFF, 8 * (size_t)(n + 1), s, &pfo));
-  OW_TRY(scan(ctx, AbinCountLoad<D>{g, c, n}, ow::StoreExcl<int64_t>{(int64_t*)pfo}, n, ctx->d_small + 32, s));
-  int64_t E;
-  OW_TRY(ow_readback(ctx, ctx->d_small + 32, 1, &E, s));
-  if (E >= (int64_t(1) << 31)) {
-    ow_set_error("lattice candidate bins overflow (%lld entries)", (long long)E);
-    return OW_ERR_CAPACITY;
-  }
-  void *pk0, *pv0, *pk1, *pv1;
-  OW_TRY(ow_slot(ctx, SLOT_PAIR_KEY0, 4 * (size_t)E, s, &pk0));
-  OW_TRY(ow_slot(ctx, SLOT_PAIR_VAL0, 4 * (size_t)E, s, &pv0));
-  OW_TRY(ow_slot(ctx, SLOT_PAIR_KEY1, 4 * (size_t)E, s, &pk1));
-  OW_TRY(ow_slot(ctx, SLOT_PAIR_VAL1, 4 * (size_t)E, s, &pv1));
-  OW_TRY(ow_slot(ctx, SLOT_ABIN_CNT, 4 * (size_t)nb, s, &pcnt));
-  OW_TRY(ow_slot(ctx, SLOT_ABIN_OFF, 4 * (size_t)nb, s, &poff));
-  OW_TRY(ow_slot(ctx, SLOT_LAT_REC, 64 * (size_t)n, s, &prec));
-  OW_CUDA(cudaMemsetAsync(pcnt, 0, 4 * (size_t)nb, s));
-  k_abin_emit<D><<<ow_blocks(n, 256), 256, 0, s>>>(g, c, n, (const int64_t*)pfo, (uint32_t*)pk0, (int32_t*)pv0,
-                                                  (int32_t*)pcnt, (float4*)prec);
-  OW_LAUNCHED(ctx);
-  OW_CHECK_LAUNCH();
-  int bits = 0;
-  while ((int64_t(1) << bits) < nb) ++bits;
-  uint32_t* rk;
-  int32_t* rv;
-  OW_TRY(ow::radix_sort_pairs(ctx, (uint32_t*)pk0, (int32_t*)pv0, (uint32_t*)pk1, (int32_t*)pv1, E, bits, &rk, &rv, s));
-  void* pids;
-  OW_TRY(ow_slot(ctx, SLOT_ABIN_IDS, 4 * (size_t)E, s, &pids));
-  if (E > 0) OW_CUDA(cudaMemcpyAsync(pids, rv, 4 * (size_t)E, cudaMemcpyDeviceToDevice, s));
-  OW_TRY(scan(ctx, ow::LoadArr<int32_t>{(const int32_t*)pcnt}, ow::StoreExcl<int32_t>{(int32_t*)poff}, nb, nullptr, s));
-  ctx->abin_key = key;
-  ctx->abin_B = g.B;
-  ctx->abin_dim = D;
-  return OW_OK;
-}
-
-// ---- shared geometry of one finest block ---------------------------------------
-struct BlockFrame {
-  double blo[3];
-  float h32[3], glo[3], ghi[3];  // cell size, outward-rounded box grown by two cells
-  int rlo[3], rhi[3];            // bin range of the grown box
-};
-
-template <int D>
-__device__ __forceinline__ BlockFrame block_frame(const ForestC& F, const GridC& g, int id) {
-  BlockFrame b;
-  const int L = F.level[id];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    b.h32[a] = b.glo[a] = b.ghi[a] = 0.0f;
-    b.rlo[a] = b.rhi[a] = 0;
-    b.blo[a] = 0.0;
-  }
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    double q = block_len(F, a, L);
-    b.blo[a] = DADD(F.dmin[a], DMUL((double)F.coord[a][id], q));
-    double bhi = DADD(b.blo[a], q);
-    double h64 = q / 4.0;  // exact (power-of-two scale)
-    b.h32[a] = __double2float_rn(h64);
-    b.glo[a] = __double2float_rd(b.blo[a] - 2.0 * h64);
-    b.ghi[a] = __double2float_ru(bhi + 2.0 * h64);
-    b.rlo[a] = bin_axis(b.glo[a], g.min32[a], g.len32[a], g.B);
-    b.rhi[a] = bin_axis(b.ghi[a], g.min32[a], g.len32[a], g.B);
-  }
-  return b;
-}
-
-// candidate test on a packed record: face box meets the grown box, and this
-// is the face's first bin inside the block's range
-template <int D>
-__device__ __forceinline__ bool is_candidate(const float4* __restrict__ rec, int f, const BlockFrame& b,
-                                             const int* bx) {
-  float lo[3], hi[3];
-  unsigned pk;
-  if (D == 3) {
-    float4 r0 = rec[4 * f], r1 = rec[4 * f + 1], r2 = rec[4 * f + 2], r3 = rec[4 * f + 3];
-    lo[0] = r0.w, lo[1] = r1.w, lo[2] = r2.w;
-    hi[0] = r3.x, hi[1] = r3.y, hi[2] = r3.z;
-    pk = __float_as_uint(r3.w);
-  } else {
-    float4 r1 = rec[4 * f + 1], r2 = rec[4 * f + 2];
-    lo[0] = r1.x, lo[1] = r1.y, hi[0] = r1.z, hi[1] = r1.w;
-    pk = __float_as_uint(r2.x);
-  }
-  bool ok = true;
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    int fl = (int)((pk >> (10 * a)) & 1023u);
-    ok &= lo[a] <= b.ghi[a] && hi[a] >= b.glo[a] && max(fl, b.rlo[a]) == bx[a];
-  }
-  return ok;
-}
-
-struct LatArgs {
-  ForestC F;
-  GridC g;
-  Dirs dirs;
-  int nq;
-  const int32_t* leaves;
-  int64_t n_leaves;
-  const float4* rec;
-  const int32_t* ab_ids;
-  const int32_t* ab_cnt;
-  const int32_t* ab_off;
-  int32_t* cand_cnt;        // [n_leaves] candidate faces per finest block
-  int64_t* cand_off;        // [n_leaves] packed: pair offset << 32 | candidate-block rank
-  int32_t* cand_blocks;     // [n_cb] position of each candidate block
-  int32_t* pair_face;       // [P] candidate face of each (block, face) pair
-  int32_t* pair_blk;        // [P] leaf position of each pair
-  int64_t n_pairs;
-  uint32_t* star;           // [<= P*C] (pair << shift | cell) passing the star-box test
-  unsigned long long* n_star;
-  uint32_t* flags;          // [n_leaves * C]
-  unsigned* qbits;          // [n_cb * C * nq] min-t float bits (+inf init)
-  int32_t* bcount;          // [n_cb]
-  const int64_t* boff;      // [n_cb]
-  int64_t n_cb;
-  int64_t* cells_out;
-  float* q_out;
-  unsigned long long* stats;  // [0] star-box, [1] link-box, [2] intersection tests
-};
-
-template <int D>
-__global__ void __launch_bounds__(CNT_WARPS * 32) k_lat_count(LatArgs A) {
-  const int lane = threadIdx.x & 31;
-  const int64_t pos = (int64_t)blockIdx.x * CNT_WARPS + (threadIdx.x >> 5);
-  if (pos >= A.n_leaves) return;
-  const BlockFrame b = block_frame<D>(A.F, A.g, A.leaves[pos]);
-  int count = 0;
-  for (int bz = b.rlo[2]; bz <= b.rhi[2]; ++bz)
-    for (int by = b.rlo[1]; by <= b.rhi[1]; ++by)
-      for (int bx0 = b.rlo[0]; bx0 <= b.rhi[0]; ++bx0) {
-        int bx[3] = {bx0, by, bz};
-        int64_t lin = bx0 + (int64_t)A.g.B * (by + (int64_t)A.g.B * bz);
-        const int32_t* src = A.ab_ids + A.ab_off[lin];
-        const int cnt = A.ab_cnt[lin];
-        for (int j0 = 0; j0 < cnt; j0 += 32) {
-          bool ok = j0 + lane < cnt && is_candidate<D>(A.rec, src[j0 + lane], b, bx);
-          count += __popc(__ballot_sync(0xffffffffu, ok));
-        }
-      }
-  if (lane == 0) A.cand_cnt[pos] = count;
-}
-
-// one scan gives both the pair offset (high word) and the candidate-block rank (low word)
-struct CandLoad {
-  const int32_t* c;
-  __device__ int64_t operator()(int64_t i) const {
-    int64_t n = c[i];
-    return (n << 32) | (n > 0 ? 1 : 0);
-  }
-};
-struct CandStore {
-  int64_t* off;
-  int32_t* blocks;
-  __device__ void operator()(int64_t i, int64_t e, int64_t v) const {
-    off[i] = e;
-    if (v) blocks[e & 0xffffffffll] = (int32_t)i;
-  }
-};
-
-// warp per candidate block: write its (block, face) pairs
-template <int D>
-__global__ void __launch_bounds__(CNT_WARPS * 32) k_lat_pairs(LatArgs A) {
-  const int lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * CNT_WARPS + (threadIdx.x >> 5);
-  if (r >= A.n_cb) return;
-  const int pos = A.cand_blocks[r];
-  const BlockFrame b = block_frame<D>(A.F, A.g, A.leaves[pos]);
-  int64_t out = A.cand_off[pos] >> 32;
-  for (int bz = b.rlo[2]; bz <= b.rhi[2]; ++bz)
-    for (int by = b.rlo[1]; by <= b.rhi[1]; ++by)
-      for (int bx0 = b.rlo[0]; bx0 <= b.rhi[0]; ++bx0) {
-        int bx[3] = {bx0, by, bz};
-        int64_t lin = bx0 + (int64_t)A.g.B * (by + (int64_t)A.g.B * bz);
-        const int32_t* src = A.ab_ids + A.ab_off[lin];
-        const int cnt = A.ab_cnt[lin];
-        for (int j0 = 0; j0 < cnt; j0 += 32) {
-          const int f = j0 + lane < cnt ? src[j0 + lane] : 0;
-          const bool ok = j0 + lane < cnt && is_candidate<D>(A.rec, f, b, bx);
-          const unsigned m = __ballot_sync(0xffffffffu, ok);
-          if (ok) {
-            const int64_t k = out + __popc(m & lanemask_lt());
-            A.pair_face[k] = f;
-            A.pair_blk[k] = pos;
-          }
-          out += __popc(m);
-        }
-      }
-}
-
-// cell centre (FP64 -> one FP32 rounding) and cell size of cell c of block id
-template <int D>
-__device__ __forceinline__ void cell_center(const ForestC& F, int id, int c, float* x, float* h) {
-  const int L = F.level[id];
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    double q = block_len(F, a, L);
-    double o = DADD(F.dmin[a], DMUL((double)F.coord[a][id], q));
-    double u = ((double)((c >> (2 * a)) & 3) + 0.5) / 4.0;
-    x[a] = __double2float_rn(DADD(o, DMUL(u, q)));
-    h[a] = __double2float_rn(q / 4.0);
-  }
-}
-
-__device__ __forceinline__ void face_lohi(const float4* __restrict__ rec, int f, int D, float* lo, float* hi) {
-  if (D == 3) {
-    float4 r0 = rec[4 * f], r1 = rec[4 * f + 1], r2 = rec[4 * f + 2], r3 = rec[4 * f + 3];
-    lo[0] = r0.w, lo[1] = r1.w, lo[2] = r2.w, hi[0] = r3.x, hi[1] = r3.y, hi[2] = r3.z;
-  } else {
-    float4 r1 = rec[4 * f + 1];
-    lo[0] = r1.x, lo[1] = r1.y, hi[0] = r1.z, hi[1] = r1.w;
-  }
-}
-
-// (pair, cell) items whose cell "star" box [fl(x-h), fl(x+h)] — the union of
-// all its link boxes — meets the face box; appended with warp-aggregated atomics
-template <int D>
-__global__ void __launch_bounds__(256) k_lat_star(LatArgs A) {
-  constexpr int SH = D == 3 ? 6 : 4;  // log2 cells per block
-  const int64_t total = A.n_pairs << SH;
-  const int lane = threadIdx.x & 31;
-  unsigned long long tests = 0;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < total; base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = base + threadIdx.x;
-    bool ok = false;
-    if (t < total) {
-      const int64_t p = t >> SH;
-      const int c = (int)(t & ((1 << SH) - 1));
-      float x[3], h[3], lo[3], hi[3];
-      cell_center<D>(A.F, A.leaves[A.pair_blk[p]], c, x, h);
-      face_lohi(A.rec, A.pair_face[p], D, lo, hi);
-      ok = true;
-#pragma unroll
-      for (int a = 0; a < D; ++a) ok = ok && lo[a] <= FADD(x[a], h[a]) && hi[a] >= FADD(x[a], -h[a]);
-      ++tests;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, ok);
-    if (m) {
-      unsigned long long w = 0;
-      if (lane == 0) w = atomicAdd(A.n_star, (unsigned long long)__popc(m));
-      w = __shfl_sync(0xffffffffu, w, 0);
-      if (ok) A.star[w + __popc(m & lanemask_lt())] = (uint32_t)t;
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) tests += __shfl_xor_sync(0xffffffffu, tests, o);
-  if (lane == 0 && tests) atomicAdd(&A.stats[0], tests);
-}
-
-// Moller-Trumbore, fixed op order (oracle/lattice.py:mt_hits); e1 = v1 - v0,
-// e2 = v2 - v0 were formed by the same float32 subtractions at packing time.
-__device__ __forceinline__ bool mt_hit_e(const float* x, const float* dv, const float* v0, const float* e1,
-                                         const float* e2, float* tout) {
-  float px = FSUB(FMUL(dv[1], e2[2]), FMUL(dv[2], e2[1]));
-  float py = FSUB(FMUL(dv[2], e2[0]), FMUL(dv[0], e2[2]));
-  float pz = FSUB(FMUL(dv[0], e2[1]), FMUL(dv[1], e2[0]));
-  float det = dot3f(e1[0], e1[1], e1[2], px, py, pz);
-  if (det == 0.0f) return false;
-  float tx = FSUB(x[0], v0[0]), ty = FSUB(x[1], v0[1]), tz = FSUB(x[2], v0[2]);
-  float u = FDIV(dot3f(tx, ty, tz, px, py, pz), det);
-  if (!(u >= 0.0f)) return false;
-  float qx = FSUB(FMUL(ty, e1[2]), FMUL(tz, e1[1]));
-  float qy = FSUB(FMUL(tz, e1[0]), FMUL(tx, e1[2]));
-  float qz = FSUB(FMUL(tx, e1[1]), FMUL(ty, e1[0]));
-  float v = FDIV(dot3f(dv[0], dv[1], dv[2], qx, qy, qz), det);
-  if (!(v >= 0.0f) || !(FADD(u, v) <= 1.0f)) return false;
-  float t = FDIV(dot3f(e2[0], e2[1], e2[2], qx, qy, qz), det);
-  if (!(t >= 0.0f) || !(t <= 1.0f)) return false;
-  *tout = t;
-  return true;
-}
-
-// segment-segment (oracle/lattice.py:seg_hits) with s = b - a pre-formed
-__device__ __forceinline__ bool seg_hit_s(const float* x, const float* dv, const float* a, const float* sv,
-                                          float* tout) {
-  float den = FSUB(FMUL(dv[0], sv[1]), FMUL(dv[1], sv[0]));
-  if (den == 0.0f) return false;
-  float qx = FSUB(a[0], x[0]), qy = FSUB(a[1], x[1]);
-  float t = FDIV(FSUB(FMUL(qx, sv[1]), FMUL(qy, sv[0])), den);
-  float s = FDIV(FSUB(FMUL(qx, dv[1]), FMUL(qy, dv[0])), den);
-  if (!(t >= 0.0f) || !(t <= 1.0f) || !(s >= 0.0f) || !(s <= 1.0f)) return false;
-  *tout = t;
-  return true;
-}
-
-// every link of a (cell, face) item: exact link-AABB test, then the
-// intersection test; hits update the cell's flag word and min-t
-template <int D>
-__global__ void __launch_bounds__(256) k_lat_links(LatArgs A) {
-  constexpr int SH = D == 3 ? 6 : 4;
-  constexpr int C = 1 << SH;
-  const int64_t total = (int64_t)*A.n_star;
-  unsigned long long nbox = 0, nmt = 0;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t t = A.star[e];
-    const int64_t p = t >> SH;
-    const int c = (int)(t & (C - 1));
-    const int pos = A.pair_blk[p], f = A.pair_face[p];
-    float x[3], h[3], lo[3], hi[3], v0[3], e1[3], e2[3];
-    cell_center<D>(A.F, A.leaves[pos], c, x, h);
-    const float4* R = A.rec + 4 * (int64_t)f;
+  if (!EMIT && lane == 0) {
     if (D == 3) {
-      float4 r0 = R[0], r1 = R[1], r2 = R[2], r3 = R[3];
-      v0[0] = r0.x, v0[1] = r0.y, v0[2] = r0.z, e1[0] = r1.x, e1[1] = r1.y, e1[2] = r1.z;
-      e2[0] = r2.x, e2[1] = r2.y, e2[2] = r2.z;
-      lo[0] = r0.w, lo[1] = r1.w, lo[2] = r2.w, hi[0] = r3.x, hi[1] = r3.y, hi[2] = r3.z;
+      A.rec[3 * f + 0] = make_float4(v[0][0], v[0][1], v[0][2], 0.0f);
+      A.rec[3 * f + 1] = make_float4(e1[0], e1[1], e1[2], 0.0f);
+      A.rec[3 * f + 2] = make_float4(e2[0], e2[1], e2[2], 0.0f);
     } else {
-      float4 r0 = R[0], r1 = R[1];
-      v0[0] = r0.x, v0[1] = r0.y, e1[0] = r0.z, e1[1] = r0.w;
-      lo[0] = r1.x, lo[1] = r1.y, hi[0] = r1.z, hi[1] = r1.w;
+      A.rec[3 * f + 0] = make_float4(v[0][0], v[0][1], e1[0], e1[1]);
     }
-    const int64_t cell = (int64_t)pos * C + c;
-    const int64_t qrow = ((int64_t)(A.cand_off[pos] & 0xffffffffll) * C + c) * A.nq;
-    unsigned fl = 0;
-    for (int d = 1; d < A.nq; ++d) {
-      float dv[3];
-      bool ov = true;
+  }
+  bool dok = false;  // lane d: determinant of direction d is non-zero
+  if (lane >= 1 && lane < A.nq) {
+    const float* dv = A.dv[lane];
+    if (D == 3) {
+      const float px = FSUB(FMUL(dv[1], e2[2]), FMUL(dv[2], e2[1]));
+      const float py = FSUB(FMUL(dv[2], e2[0]), FMUL(dv[0], e2[2]));
+      const float pz = FSUB(FMUL(dv[0], e2[1]), FMUL(dv[1], e2[0]));
+      dok = dot3f(e1[0], e1[1], e1[2], px, py, pz) != 0.0f;
+    } else {
+      dok = FSUB(FMUL(dv[0], e1[1]), FMUL(dv[1], e1[0])) != 0.0f;
+    }
+  }
+  const unsigned detmask = __ballot_sync(0xffffffffu, dok);
+  const int L = A.level;
+  int k0[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
+  int64_t nslots = detmask ? 1 : 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const double q = block_len(A.F, a, L);
+    const int64_t nmax = ((int64_t)A.F.root[a] << L) - 1;
+    int64_t a0 = (int64_t)ceil(((double)lo[a] - A.F.dmin[a]) / q - 1.135);
+    int64_t a1 = (int64_t)floor(((double)hi[a] - A.F.dmin[a]) / q + 0.135);
+    if (a0 < 0) a0 = 0;
+    if (a1 > nmax) a1 = nmax;
+    k0[a] = (int)a0;
+    ext[a] = a1 >= a0 ? (int)(a1 - a0 + 1) : 0;
+    nslots *= ext[a];
+  }
+  int64_t out = EMIT ? (A.fcnt[f] & 0xffffffffll) : 0;
+  int64_t rows_w = 0, units_w = 0;
+  for (int64_t s0 = 0; s0 < nslots; s0 += 32) {
+    const int64_t slot = s0 + lane;
+    int nrow = 0, nunit = 0, pos = 0;
+    unsigned r[3][3];
+    if (slot < nslots) {
+      int32_t nc[3] = {0, 0, 0};
+      int64_t rem = slot;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        dv[a] = FMUL((float)A.dirs.c[d][a], h[a]);  // exact: c in {-1,0,1}
-        const float en = FADD(x[a], dv[a]);
-        ov = ov && lo[a] <= fmaxf(x[a], en) && hi[a] >= fminf(x[a], en);
+        nc[a] = k0[a] + (int)(rem % ext[a]);
+        rem /= ext[a];
       }
-      ++nbox;
-      if (!ov) continue;
-      ++nmt;
-      float tt;
-      const bool hit = D == 3 ? mt_hit_e(x, dv, v0, e1, e2, &tt) : seg_hit_s(x, dv, v0, e1, &tt);
-      if (hit) {
-        fl |= 1u << d;
-        atomicMin(&A.qbits[qrow + d], __float_as_uint(FADD(tt, 0.0f)));  // -0 -> +0; t >= 0
+      int depth;
+      const int node = locate(A.F, L, nc, &depth);
+      if (depth == L && A.F.first_child[node] < 0) {
+        pos = A.pos_of[node];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+          axis_ranges(reinterpret_cast<const float4*>(A.cen)[(int64_t)pos * D + a], A.h[a], lo[a], hi[a], r[a]);
+        for (int d = 1; d < A.nq; ++d) {
+          if (!((detmask >> d) & 1u)) continue;
+          int units = 1;
+          bool ok = true;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            const float c = A.dv[d][a];
+            const unsigned ra = r[a][c < 0.0f ? 0 : (c > 0.0f ? 2 : 1)];
+            ok = ok && ra != 0xF0u;
+            units *= (int)((ra >> 2) & 3u) + 1;
+          }
+          if (!ok) continue;
+          ++nrow;
+          nunit += units;
+        }
+        if (!EMIT && nrow) A.has_pair[pos] = 1;
       }
     }
-    if (fl) atomicOr(&A.flags[cell], fl);
+    if (EMIT) {
+      int incl = nrow;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int64_t k = out + incl - nrow;
+      if (nrow) {
+        for (int d = 1; d < A.nq; ++d) {
+          if (!((detmask >> d) & 1u)) continue;
+          unsigned w = (unsigned)d;
+          int units = 1;
+          bool ok = true;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            const float c = A.dv[d][a];
+            const unsigned ra = r[a][c < 0.0f ? 0 : (c > 0.0f ? 2 : 1)];
+            ok = ok && ra != 0xF0u;
+            w |= (ra & 0xFu) << (5 + 4 * a);
+            units *= (int)((ra >> 2) & 3u) + 1;
+          }
+          if (!ok) continue;
+          A.rows[k] = make_int4(pos, (int)f, (int)w, units);
+          A.rowoff[k] = units;
+          ++k;
+        }
+      }
+      out += __shfl_sync(0xffffffffu, incl, 31);
+    } else {
+      rows_w += nrow;
+      units_w += nunit;
+    }
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    nbox += __shfl_xor_sync(0xffffffffu, nbox, o);
-    nmt += __shfl_xor_sync(0xffffffffu, nmt, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (nbox) atomicAdd(&A.stats[1], nbox);
-    if (nmt) atomicAdd(&A.stats[2], nmt);
+  if (!EMIT) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      rows_w += __shfl_xor_sync(0xffffffffu, rows_w, o);
+      units_w += __shfl_xor_sync(0xffffffffu, units_w, o);
+    }
+    if (lane == 0) A.fcnt[f] = rows_w | (units_w << 32);
   }
 }
 
-// boundary cells per candidate block (warp per block)
+// ranks of candidate blocks (leaves with at least one row)
+struct CandLoad {
+  const uint8_t* h;
+  __device__ int64_t operator()(int64_t i) const { return h[i]; }
+};
+struct CandStore {
+  int32_t* rank;
+  int32_t* blocks;
+  __device__ void operator()(int64_t i, int64_t e, int64_t v) const {
+    rank[i] = (int32_t)e;
+    if (v) blocks[e] = (int32_t)i;
+  }
+};
+
+// rowoff[i] = exclusive unit offset (in place over the unit counts); the row
+// holding the first unit of each MT tile is recorded on the fly
+struct RowCntStore {
+  int64_t* off;
+  int32_t* tile_row;
+  __device__ void operator()(int64_t i, int64_t e, int64_t v) const {
+    off[i] = e;
+    for (int64_t t = (e + MT_TILE - 1) / MT_TILE; t * MT_TILE < e + v; ++t) tile_row[t] = (int32_t)i;
+  }
+};
+
+// q = fl(a / det) >= 0 is decided before dividing: it holds iff a is zero, a
+// and det agree in sign, or the negative quotient underflows to -0
+// (|a / det| <= 2^-150; |a| 2^150 is formed by two exact power-of-two scalings,
+// overflow to +inf meaning "not tiny").  A miss never pays for a division and a
+// hit gets the quotient bits the oracle computes.
+__device__ __forceinline__ bool quot_nonneg(float a, float det) {
+  if (a == 0.0f || ((a > 0.0f) == (det > 0.0f))) return true;
+  return FMUL(FMUL(fabsf(a), 0x1p75f), 0x1p75f) <= fabsf(det);
+}
+
+// x / ext for 0 <= x < 64, ext in 1..4 (multiply-shift, exact in that range)
+__device__ __forceinline__ int div_small(int x, int ext) {
+  const int m = ext == 1 ? 256 : ext == 2 ? 128 : ext == 3 ? 86 : 64;
+  return (x * m) >> 8;
+}
+
+// Persistent, load-balanced over units: a tile of MT_TILE consecutive units
+// covers at most MT_TILE + 1 rows (the first one recorded by the unit scan).
+// The tile's rows are staged in shared memory with their per-row terms of
+// Moller-Trumbore (oracle/lattice.py:mt_hits, same float32 ops): p = d x e2,
+// det = e1 . p (3D) / den = d x s (2D).  Each thread binary-searches the row of
+// its first unit and walks forward.
+template <int D>
+__global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
+  constexpr int C = D == 3 ? 64 : 16;
+  __shared__ int s_off[MT_TILE + 1];
+  __shared__ int4 s_meta[MT_TILE + 1];    // pos, face, w, units
+  __shared__ float4 s_v0[MT_TILE + 1];    // v0.xyz, det     (2D: a.xy, den, -)
+  __shared__ float4 s_e1[MT_TILE + 1];    // e1.xyz, p.x     (2D: s.xy, -, -)
+  __shared__ float4 s_e2[MT_TILE + 1];    // e2.xyz, p.y
+  __shared__ float s_pz[MT_TILE + 1];     // p.z
+  __shared__ float s_dv[QMAX][3];
+  for (int i = threadIdx.x; i < QMAX * 3; i += MT_THREADS) s_dv[i / 3][i % 3] = A.dv[i / 3][i % 3];
+  const int64_t U = A.n_units;
+  const int64_t R = A.n_rows;
+  const int64_t n_tiles = (U + MT_TILE - 1) / MT_TILE;
+  const int lane = threadIdx.x & 31;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t u0 = tile * MT_TILE;
+    const int64_t u1 = min(U, u0 + MT_TILE);
+    const int64_t r0 = A.tile_row[tile];
+    const int nr = (int)((tile + 1 < n_tiles ? (int64_t)A.tile_row[tile + 1] : R - 1) - r0 + 1);
+    __syncthreads();  // previous tile done with the staging buffers (and s_dv written)
+    for (int i = threadIdx.x; i < nr; i += MT_THREADS) {
+      const int4 m = A.rows[r0 + i];
+      s_off[i] = (int)(A.rowoff[r0 + i] - u0);  // >= -63 for the first row
+      s_meta[i] = m;
+      const float* dv = s_dv[m.z & 31];
+      const float4* Rf = A.rec + 3 * (int64_t)m.y;
+      if (D == 3) {
+        const float4 a = Rf[0], b = Rf[1], c = Rf[2];
+        const float px = FSUB(FMUL(dv[1], c.z), FMUL(dv[2], c.y));
+        const float py = FSUB(FMUL(dv[2], c.x), FMUL(dv[0], c.z));
+        const float pz = FSUB(FMUL(dv[0], c.y), FMUL(dv[1], c.x));
+        s_v0[i] = make_float4(a.x, a.y, a.z, dot3f(b.x, b.y, b.z, px, py, pz));
+        s_e1[i] = make_float4(b.x, b.y, b.z, px);
+        s_e2[i] = make_float4(c.x, c.y, c.z, py);
+        s_pz[i] = pz;
+      } else {
+        const float4 a = Rf[0];
+        s_v0[i] = make_float4(a.x, a.y, FSUB(FMUL(dv[0], a.w), FMUL(dv[1], a.z)), 0.0f);
+        s_e1[i] = make_float4(a.z, a.w, 0.0f, 0.0f);
+      }
+    }
+    __syncthreads();
+    const int ub = threadIdx.x * MT_ITEMS;  // tile-relative
+    const int un_tile = (int)(u1 - u0);
+    int row = 0;
+    if (ub < un_tile) {
+      int lo = 0, hi = nr;  // last row with s_off <= ub
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_off[mid] <= ub) lo = mid;
+        else hi = mid;
+      }
+      row = lo;
+    }
+#pragma unroll
+    for (int k = 0; k < MT_ITEMS; ++k) {
+      const int u = ub + k;
+      bool hit = false;
+      int cellg = 0, d = 0;
+      float t = 0.0f;
+      if (u < un_tile) {
+        while (row + 1 < nr && s_off[row + 1] <= u) ++row;
+        const int4 m = s_meta[row];
+        const unsigned w = (unsigned)m.z;
+        d = (int)(w & 31u);
+        int rem = u - s_off[row];
+        int cell = 0;
+        float x[3];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const unsigned ra = (w >> (5 + 4 * a)) & 0xFu;
+          const int ext = (int)(ra >> 2) + 1;
+          const int qd = div_small(rem, ext);
+          const int i = (int)(ra & 3u) + (rem - qd * ext);
+          rem = qd;
+          cell |= i << (2 * a);
+          x[a] = __ldg(A.cen + ((int64_t)m.x * D + a) * 4 + i);
+        }
+        cellg = m.x * C + cell;
+        const float* dv = s_dv[d];
+        if (D == 3) {
+          const float4 V = s_v0[row], E1 = s_e1[row], E2 = s_e2[row];
+          const float det = V.w, px = E1.w, py = E2.w, pz = s_pz[row];
+          const float tx = FSUB(x[0], V.x), ty = FSUB(x[1], V.y), tz = FSUB(x[2], V.z);
+          const float un = dot3f(tx, ty, tz, px, py, pz);
+          if (quot_nonneg(un, det)) {
+            const float qx = FSUB(FMUL(ty, E1.z), FMUL(tz, E1.y));
+            const float qy = FSUB(FMUL(tz, E1.x), FMUL(tx, E1.z));
+            const float qz = FSUB(FMUL(tx, E1.y), FMUL(ty, E1.x));
+            const float vn = dot3f(dv[0], dv[1], dv[2], qx, qy, qz);
+            const float tn = dot3f(E2.x, E2.y, E2.z, qx, qy, qz);
+            if (quot_nonneg(vn, det) && quot_nonneg(tn, det)) {
+              const float uu = FDIV(un, det), vv = FDIV(vn, det);
+              if (FADD(uu, vv) <= 1.0f) {
+                t = FDIV(tn, det);
+                hit = t <= 1.0f;
+              }
+            }
+          }
+        } else {
+          // segment-segment (oracle/lattice.py:seg_hits), s = b - a pre-formed
+          const float4 V = s_v0[row], S = s_e1[row];
+          const float den = V.z;
+          const float qx = FSUB(V.x, x[0]), qy = FSUB(V.y, x[1]);
+          const float tn = FSUB(FMUL(qx, S.y), FMUL(qy, S.x));
+          const float sn = FSUB(FMUL(qx, dv[1]), FMUL(qy, dv[0]));
+          if (quot_nonneg(tn, den) && quot_nonneg(sn, den)) {
+            t = FDIV(tn, den);
+            const float ss = FDIV(sn, den);
+            hit = t <= 1.0f && ss <= 1.0f;
+          }
+        }
+      }
+      if (hit) atomicOr(&A.flags[cellg], 1u << d);
+      // warp-aggregated append to the hit list: (flat cell, dir | t bits)
+      const unsigned hm = __ballot_sync(0xffffffffu, hit);
+      if (hm) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(A.n_hits, (unsigned long long)__popc(hm));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (hit) {
+          const unsigned long long k = base + __popc(hm & lanemask_lt());
+          A.hits[k] = make_uint2((unsigned)cellg, __float_as_uint(FADD(t, 0.0f)));  // -0 -> +0
+          A.hit_dir[k] = (uint8_t)d;
+        }
+      }
+    }
+  }
+}
+
+// boundary cells per candidate block (warp per block): count + cell mask
 template <int D>
 __global__ void k_lat_bcount(LatArgs A) {
   constexpr int C = D == 3 ? 64 : 16;
@@ -488,73 +449,101 @@ __global__ void k_lat_bcount(LatArgs A) {
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= A.n_cb) return;
   const int64_t pos = A.cand_blocks[r];
-  int nb = 0;
-  for (int c = lane; c < C; c += 32) nb += A.flags[pos * C + c] != 0;
-  for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
-  if (lane == 0) A.bcount[r] = nb;
+  unsigned long long m = 0;
+#pragma unroll
+  for (int k = 0; k < (C + 31) / 32; ++k) {
+    const int c = lane + 32 * k;
+    const unsigned b = __ballot_sync(0xffffffffu, c < C && A.flags[pos * C + c] != 0);
+    m |= (unsigned long long)b << (32 * k);
+  }
+  if (lane == 0) {
+    A.bcount[r] = __popcll(m);
+    A.bmask[r] = m;
+  }
 }
 
-// boundary rows in (block, cell) order: CTA of C threads per candidate block
+// boundary rows in (block, cell) order: cells and q rows (-1 where the link
+// misses; flagged entries start at +big and receive min t from k_lat_hits)
 template <int D>
 __global__ void k_lat_emit(LatArgs A) {
   constexpr int C = D == 3 ? 64 : 16;
   const int64_t r = blockIdx.x;
-  if (r >= A.n_cb || A.bcount[r] == 0) return;
-  const int64_t pos = A.cand_blocks[r];
+  const unsigned long long m = A.bmask[r];
   const int c = threadIdx.x;
+  if (!((m >> c) & 1ull)) return;
+  const int64_t pos = A.cand_blocks[r];
   const unsigned fl = A.flags[pos * C + c];
-  __shared__ int s_b[C];
-  s_b[c] = fl != 0;
-  __syncthreads();
-  if (!fl) return;
-  int rank = 0;
-  for (int c0 = 0; c0 < c; ++c0) rank += s_b[c0];
-  const int64_t row = A.boff[r] + rank;
+  const int64_t row = A.boff[r] + __popcll(m & ((1ull << c) - 1ull));
   A.cells_out[row] = pos * C + c;
-  const unsigned* q = A.qbits + (r * C + c) * A.nq;
-  for (int i = 0; i < A.nq; ++i) A.q_out[row * A.nq + i] = ((fl >> i) & 1) ? __uint_as_float(q[i]) : -1.0f;
+  float* q = A.q_out + row * A.nq;
+  for (int i = 0; i < A.nq; ++i) q[i] = ((fl >> i) & 1) ? __uint_as_float(0x7f7f7f7fu) : -1.0f;
 }
 
-LatArgs make_args(ow_ctx* ctx, const ow_forest* f, const ow_grid* grid, const int8_t* dirs, int nq,
-                  const int32_t* leaves, int64_t n_leaves) {
+// min t per (boundary row, direction): t >= 0, so float order = uint order
+template <int D>
+__global__ void k_lat_hits(LatArgs A) {
+  constexpr int C = D == 3 ? 64 : 16;
+  const int64_t n = (int64_t)*A.n_hits;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint2 h = A.hits[i];
+    const int64_t pos = h.x / C;
+    const int c = (int)(h.x % C);
+    const int r = A.cand_rank[pos];
+    const int64_t row = A.boff[r] + __popcll(A.bmask[r] & ((1ull << c) - 1ull));
+    atomicMin(reinterpret_cast<unsigned*>(A.q_out) + row * A.nq + A.hit_dir[i], h.y);
+  }
+}
+
+LatArgs make_args(ow_ctx* ctx) {
   LatArgs A;
   memset(&A, 0, sizeof(A));
+  const ow_forest* f = &ctx->lat_forest;
   A.F = make_forestc(f);
-  A.g = make_gridc(grid);
-  for (int i = 0; i < nq; ++i)
-    for (int a = 0; a < 3; ++a) A.dirs.c[i][a] = a < f->dim ? dirs[i * 3 + a] : 0;
-  A.nq = nq;
-  A.leaves = leaves;
-  A.n_leaves = n_leaves;
-  A.rec = (const float4*)ctx->slot_ptr[SLOT_LAT_REC];
-  A.ab_ids = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_IDS];
-  A.ab_cnt = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_CNT];
-  A.ab_off = (const int32_t*)ctx->slot_ptr[SLOT_ABIN_OFF];
-  A.cand_cnt = (int32_t*)ctx->slot_ptr[SLOT_LAT_CCNT];
-  A.cand_off = (int64_t*)ctx->slot_ptr[SLOT_LAT_COFF];
+  A.nq = ctx->lat_dirs;
+  A.level = ctx->lat_level;
+  for (int a = 0; a < 3; ++a) {
+    // float32 of the FP64 cell size, as the device's block_len / 4 (IEEE division both sides)
+    A.h[a] = a < f->dim ? (float)(f->dext[a] / (double)((int64_t)f->root[a] << A.level) / 4.0) : 0.0f;
+  }
+  for (int i = 0; i < A.nq; ++i)
+    for (int a = 0; a < 3; ++a) A.dv[i][a] = (float)ctx->lat_dir[i * 3 + a] * A.h[a];  // exact
+  A.coords = ctx->lat_coords;
+  A.n_faces = ctx->lat_faces;
+  A.leaves = ctx->lat_leaves_ptr;
+  A.n_leaves = ctx->lat_leaves;
+  A.pos_of = (int32_t*)ctx->slot_ptr[SLOT_LAT_POS];
+  A.cen = (float*)ctx->slot_ptr[SLOT_LAT_CEN];
+  A.has_pair = (uint8_t*)ctx->slot_ptr[SLOT_LAT_HAS];
+  A.rec = (float4*)ctx->slot_ptr[SLOT_LAT_REC];
+  A.fcnt = (int64_t*)ctx->slot_ptr[SLOT_LAT_FCNT];
+  A.rows = (int4*)ctx->slot_ptr[SLOT_LAT_ROWS];
+  A.rowoff = (int64_t*)ctx->slot_ptr[SLOT_LAT_ROWOFF];
+  A.tile_row = (int32_t*)ctx->slot_ptr[SLOT_LAT_TILEROW];
+  A.n_rows = ctx->lat_rows;
+  A.n_units = ctx->lat_units;
+  A.cand_rank = (int32_t*)ctx->slot_ptr[SLOT_LAT_RANK];
   A.cand_blocks = (int32_t*)ctx->slot_ptr[SLOT_LAT_LEAVES];
-  A.pair_face = (int32_t*)ctx->slot_ptr[SLOT_LAT_PFACE];
-  A.pair_blk = (int32_t*)ctx->slot_ptr[SLOT_LAT_PBLK];
-  A.star = (uint32_t*)ctx->slot_ptr[SLOT_LAT_STAR];
-  A.n_star = (unsigned long long*)(ctx->d_small + 37);
-  A.bcount = (int32_t*)ctx->slot_ptr[SLOT_LAT_BCOUNT];
-  A.boff = (const int64_t*)ctx->slot_ptr[SLOT_LAT_BOFFS];
-  A.qbits = (unsigned*)ctx->slot_ptr[SLOT_LAT_TEMP];
-  A.stats = (unsigned long long*)(ctx->d_small + 40);
   A.n_cb = ctx->lat_ncb;
-  A.n_pairs = ctx->lat_pairs;
+  A.flags = ctx->lat_flags;
+  A.hits = (uint2*)ctx->slot_ptr[SLOT_LAT_HITS];
+  A.hit_dir = (uint8_t*)ctx->slot_ptr[SLOT_LAT_HITDIR];
+  A.n_hits = (unsigned long long*)(ctx->d_small + 36);
+  A.bcount = (int32_t*)ctx->slot_ptr[SLOT_LAT_BCOUNT];
+  A.bmask = (unsigned long long*)ctx->slot_ptr[SLOT_LAT_BMASK];
+  A.boff = (const int64_t*)ctx->slot_ptr[SLOT_LAT_BOFFS];
   return A;
 }
 
 }  // namespace
 
-extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
-                                      const float* d_coords, int64_t n_faces, int64_t geom_key, const ow_grid* grid,
-                                      const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags, int64_t* out_boundary,
-                                      void* stream) {
+extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_leaves,
+                                      int64_t n_leaves, const float* d_coords, int64_t n_faces, int64_t geom_key,
+                                      const ow_grid* grid, const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags,
+                                      int64_t* out_boundary, void* stream) {
+  (void)geom_key;
   cudaStream_t s = (cudaStream_t)stream;
-  if (n_dirs < 2 || n_dirs > QMAX || !grid || grid->dim != f->dim) {
-    ow_set_error("lattice: bad direction set or grid");
+  if (n_dirs < 2 || n_dirs > QMAX || (grid && grid->dim != f->dim) || level < 0 || level >= 28) {
+    ow_set_error("lattice: bad direction set, grid or level");
     return OW_ERR_INVALID;
   }
   if (n_faces <= 0) {
@@ -562,83 +551,88 @@ extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, const int
     return OW_ERR_INVALID;
   }
   const int D = f->dim, C = D == 3 ? 64 : 16;
-  GridC g = make_gridc(grid);
-  OW_PROF_BEGIN(ctx, PROF_PREP, s);
-  OW_TRY(D == 3 ? build_abins<3>(ctx, g, d_coords, n_faces, geom_key, s)
-                : build_abins<2>(ctx, g, d_coords, n_faces, geom_key, s));
-  OW_PROF_END(ctx, PROF_PREP, s);
-  void* p;
-  const int64_t nl = n_leaves > 0 ? n_leaves : 1;
-  OW_TRY(ow_slot(ctx, SLOT_LAT_CCNT, 4 * (size_t)nl, s, &p));
-  OW_TRY(ow_slot(ctx, SLOT_LAT_COFF, 8 * (size_t)nl, s, &p));
-  OW_TRY(ow_slot(ctx, SLOT_LAT_LEAVES, 4 * (size_t)nl, s, &p));
-  int8_t dirs3[QMAX * 3];
-  memset(dirs3, 0, sizeof(dirs3));
+  if (n_leaves * C >= (int64_t(1) << 32)) {
+    ow_set_error("lattice: %lld finest cells exceed the 32-bit cell index", (long long)(n_leaves * C));
+    return OW_ERR_CAPACITY;
+  }
+  memset(ctx->lat_dir, 0, sizeof(ctx->lat_dir));
   for (int i = 0; i < n_dirs; ++i)
-    for (int a = 0; a < D; ++a) dirs3[i * 3 + a] = h_dirs[i * D + a];
+    for (int a = 0; a < D; ++a) ctx->lat_dir[i * 3 + a] = h_dirs[i * D + a];
+  ctx->lat_level = level;
   ctx->lat_leaves = n_leaves;
   ctx->lat_boundary = 0;
   ctx->lat_ncb = 0;
-  ctx->lat_pairs = 0;
+  ctx->lat_rows = 0;
+  ctx->lat_units = 0;
   ctx->lat_dirs = n_dirs;
-  memcpy(ctx->lat_dir, dirs3, sizeof(dirs3));
   ctx->lat_coords = d_coords;
   ctx->lat_faces = n_faces;
   ctx->lat_leaves_ptr = d_leaves;
   ctx->lat_forest = *f;
-  ctx->lat_grid = *grid;
   ctx->lat_flags = d_flags;
   *out_boundary = 0;
-  OW_CUDA(cudaMemsetAsync(ctx->d_small + 37, 0, 8, s));
-  OW_CUDA(cudaMemsetAsync(ctx->d_small + 40, 0, 3 * 8, s));
+  OW_CUDA(cudaMemsetAsync(ctx->d_small + 33, 0, 4 * 8, s));
   if (n_leaves <= 0) return OW_OK;
+  void* p;
+  const int64_t nl = n_leaves;
+  OW_TRY(ow_slot(ctx, SLOT_LAT_POS, 4 * (size_t)f->n_blocks, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_HAS, (size_t)nl, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_CEN, 16 * (size_t)D * nl, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_RANK, 4 * (size_t)nl, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_LEAVES, 4 * (size_t)nl, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_REC, 48 * (size_t)n_faces, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_FCNT, 8 * (size_t)n_faces, s, &p));
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
-  LatArgs A = make_args(ctx, f, grid, dirs3, n_dirs, d_leaves, n_leaves);
-  if (D == 3) k_lat_count<3><<<ow_blocks(n_leaves, CNT_WARPS), CNT_WARPS * 32, 0, s>>>(A);
-  else k_lat_count<2><<<ow_blocks(n_leaves, CNT_WARPS), CNT_WARPS * 32, 0, s>>>(A);
-  OW_LAUNCHED(ctx);
+  LatArgs A = make_args(ctx);
+  if (D == 3) k_lat_pos<3><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of,
+                                                                         A.has_pair, A.cen);
+  else k_lat_pos<2><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of,
+                                                                    A.has_pair, A.cen);
+  if (D == 3) k_lat_faces<3, false><<<ow_blocks(n_faces, 4), 128, 0, s>>>(A);
+  else k_lat_faces<2, false><<<ow_blocks(n_faces, 4), 128, 0, s>>>(A);
+  ctx->launches += 2;
   OW_CHECK_LAUNCH();
-  OW_TRY(scan(ctx, CandLoad{A.cand_cnt}, CandStore{A.cand_off, A.cand_blocks}, n_leaves, ctx->d_small + 34, s));
+  OW_TRY(scan(ctx, ow::LoadArr<int64_t>{A.fcnt}, ow::StoreExcl<int64_t>{A.fcnt}, n_faces, ctx->d_small + 34, s));
+  OW_TRY(scan(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s));
   OW_CUDA(cudaMemsetAsync(d_flags, 0, 4 * (size_t)n_leaves * C, s));
-  int64_t tot;
-  OW_TRY(ow_readback(ctx, ctx->d_small + 34, 1, &tot, s));
-  const int64_t n_pairs = tot >> 32, n_cb = tot & 0xffffffffll;
-  ctx->lat_ncb = n_cb;
-  ctx->lat_pairs = n_pairs;
-  if (n_pairs * C >= (int64_t(1) << 32)) {
-    ow_set_error("lattice: %lld candidate pairs exceed the 32-bit item encoding", (long long)n_pairs);
+  int64_t tot[2];
+  OW_TRY(ow_readback(ctx, ctx->d_small + 33, 2, tot, s));
+  const int64_t n_cb = tot[0], n_rows = tot[1] & 0xffffffffll, n_units = (int64_t)((uint64_t)tot[1] >> 32);
+  if (n_units >= (int64_t(1) << 31) - MT_TILE) {
+    ow_set_error("lattice: %lld link-face tests exceed one pass (2^31)", (long long)n_units);
     return OW_ERR_CAPACITY;
   }
-  if (n_cb > 0) {
-    OW_TRY(ow_slot(ctx, SLOT_LAT_PFACE, 4 * (size_t)n_pairs, s, &p));
-    OW_TRY(ow_slot(ctx, SLOT_LAT_PBLK, 4 * (size_t)n_pairs, s, &p));
-    OW_TRY(ow_slot(ctx, SLOT_LAT_STAR, 4 * (size_t)n_pairs * C, s, &p));
-    OW_TRY(ow_slot(ctx, SLOT_LAT_TEMP, 4 * (size_t)n_cb * C * n_dirs, s, &p));
+  ctx->lat_ncb = n_cb;
+  ctx->lat_rows = n_rows;
+  ctx->lat_units = n_units;
+  if (n_rows > 0) {
+    OW_TRY(ow_slot(ctx, SLOT_LAT_ROWS, 16 * (size_t)n_rows, s, &p));
+    OW_TRY(ow_slot(ctx, SLOT_LAT_ROWOFF, 8 * (size_t)n_rows, s, &p));
+    OW_TRY(ow_slot(ctx, SLOT_LAT_TILEROW, 4 * (size_t)(n_units / MT_TILE + 2), s, &p));
+    OW_TRY(ow_slot(ctx, SLOT_LAT_HITS, 8 * (size_t)n_units, s, &p));
+    OW_TRY(ow_slot(ctx, SLOT_LAT_HITDIR, (size_t)n_units, s, &p));
     OW_TRY(ow_slot(ctx, SLOT_LAT_BCOUNT, 4 * (size_t)n_cb, s, &p));
+    OW_TRY(ow_slot(ctx, SLOT_LAT_BMASK, 8 * (size_t)n_cb, s, &p));
     OW_TRY(ow_slot(ctx, SLOT_LAT_BOFFS, 8 * (size_t)n_cb, s, &p));
-    A = make_args(ctx, f, grid, dirs3, n_dirs, d_leaves, n_leaves);
-    A.flags = d_flags;
-    OW_CUDA(cudaMemsetAsync(A.qbits, 0x7f, 4 * (size_t)n_cb * C * n_dirs, s));  // 3.39e38 > any t <= 1
+    A = make_args(ctx);
+    if (D == 3) k_lat_faces<3, true><<<ow_blocks(n_faces, 4), 128, 0, s>>>(A);
+    else k_lat_faces<2, true><<<ow_blocks(n_faces, 4), 128, 0, s>>>(A);
+    OW_LAUNCHED(ctx);
+    OW_CHECK_LAUNCH();
+    OW_TRY(scan(ctx, ow::LoadArr<int64_t>{A.rowoff}, RowCntStore{A.rowoff, A.tile_row}, n_rows, nullptr, s));
+    const int64_t tiles = (n_units + MT_TILE - 1) / MT_TILE;
     OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
-    const int grid_items = 8 * OW_SMS;
-    if (D == 3) {
-      k_lat_pairs<3><<<ow_blocks(n_cb, CNT_WARPS), CNT_WARPS * 32, 0, s>>>(A);
-      k_lat_star<3><<<ow_blocks(n_pairs * C, 256, grid_items), 256, 0, s>>>(A);
-      k_lat_links<3><<<grid_items, 256, 0, s>>>(A);
-      k_lat_bcount<3><<<ow_blocks(n_cb, 8), 256, 0, s>>>(A);
-    } else {
-      k_lat_pairs<2><<<ow_blocks(n_cb, CNT_WARPS), CNT_WARPS * 32, 0, s>>>(A);
-      k_lat_star<2><<<ow_blocks(n_pairs * C, 256, grid_items), 256, 0, s>>>(A);
-      k_lat_links<2><<<grid_items, 256, 0, s>>>(A);
-      k_lat_bcount<2><<<ow_blocks(n_cb, 8), 256, 0, s>>>(A);
-    }
+    if (D == 3) k_lat_mt<3><<<ow_blocks(tiles, 1, 6 * OW_SMS), MT_THREADS, 0, s>>>(A);
+    else k_lat_mt<2><<<ow_blocks(tiles, 1, 6 * OW_SMS), MT_THREADS, 0, s>>>(A);
     OW_PROF_END(ctx, PROF_LAT_SWEEP, s);
-    ctx->launches += 4;
+    OW_LAUNCHED(ctx);
+    OW_CHECK_LAUNCH();
+    if (D == 3) k_lat_bcount<3><<<ow_blocks(n_cb, 8), 256, 0, s>>>(A);
+    else k_lat_bcount<2><<<ow_blocks(n_cb, 8), 256, 0, s>>>(A);
+    OW_LAUNCHED(ctx);
     OW_CHECK_LAUNCH();
     OW_TRY(scan(ctx, ow::LoadArr<int32_t>{A.bcount}, ow::StoreExcl<int64_t>{(int64_t*)A.boff}, n_cb,
                 ctx->d_small + 35, s));
-  } else {
-    OW_CUDA(cudaMemsetAsync(ctx->d_small + 35, 0, 8, s));
   }
   OW_PROF_END(ctx, PROF_LATTICE, s);
   int64_t nb;
@@ -655,21 +649,29 @@ extern "C" int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, 
     return OW_ERR_INVALID;
   }
   if (ctx->lat_boundary == 0 || ctx->lat_ncb == 0) return OW_OK;
-  LatArgs A = make_args(ctx, &ctx->lat_forest, &ctx->lat_grid, ctx->lat_dir, ctx->lat_dirs, ctx->lat_leaves_ptr,
-                        ctx->lat_leaves);
-  A.flags = ctx->lat_flags;
+  LatArgs A = make_args(ctx);
   A.cells_out = d_cells;
   A.q_out = d_q;
   const int C = ctx->lat_forest.dim == 3 ? 64 : 16;
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
-  if (ctx->lat_forest.dim == 3) k_lat_emit<3><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
-  else k_lat_emit<2><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
+  if (ctx->lat_forest.dim == 3) {
+    k_lat_emit<3><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
+    k_lat_hits<3><<<2 * OW_SMS, 256, 0, s>>>(A);
+  } else {
+    k_lat_emit<2><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
+    k_lat_hits<2><<<2 * OW_SMS, 256, 0, s>>>(A);
+  }
   OW_PROF_END(ctx, PROF_LATTICE, s);
-  OW_LAUNCHED(ctx);
+  ctx->launches += 2;
   OW_CHECK_LAUNCH();
   return OW_OK;
 }
 
+// [0] candidate blocks, [1] (block, face, direction) rows, [2] intersection tests
 extern "C" int ow_lattice_stats(ow_ctx* ctx, int64_t* out3, void* stream) {
-  return ow_readback(ctx, ctx->d_small + 40, 3, out3, (cudaStream_t)stream);
+  (void)stream;
+  out3[0] = ctx->lat_ncb;
+  out3[1] = ctx->lat_rows;
+  out3[2] = ctx->lat_units;
+  return OW_OK;
 }

@@ -22,7 +22,6 @@ namespace {
 using ow::scan;
 
 constexpr int MARK_THREADS = 128;
-constexpr int STAGE = 512;  // faces staged per chunk
 
 template <int D>
 __global__ void k_face_prep(const float* __restrict__ c, int64_t n, float d, double reach, float4* box,
@@ -120,138 +119,179 @@ struct MarkArgs {
   const int32_t* bin_ids;
   const int32_t* bin_counts;
   const int32_t* bin_offsets;
-  int64_t n_faces;
+  const float4* cbox;       // union boxes of 32-entry bin-CSR chunks
+  int64_t n_faces, n_leaves;
   float d;
   double reach;
   unsigned long long* out;  // [0] marked, [1] tests, [2] evaluated
 };
 
+// Union box of the face boxes of bin-CSR entries [32 g, 32 g + 32) (entries of
+// neighbouring bins included: a larger box is still a conservative cull).  The
+// FP64 box distance is monotone in the box, so a chunk whose union box fails
+// the reference's cull holds no face that passes it.
+template <int D>
+__global__ void k_chunk_boxes(const int32_t* __restrict__ ids, int64_t n_entries, const float4* __restrict__ box,
+                              float4* cbox) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g * 32 >= n_entries) return;
+  float4 lo = make_float4(INFINITY, INFINITY, INFINITY, 0.0f), hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.0f);
+  const int64_t e1 = min(n_entries, g * 32 + 32);
+  for (int64_t e = g * 32; e < e1; ++e) {
+    const int64_t f = ids ? ids[e] : e;
+    const float4 l = box[2 * f], h = box[2 * f + 1];
+    lo.x = fminf(lo.x, l.x), lo.y = fminf(lo.y, l.y), lo.z = fminf(lo.z, l.z);
+    hi.x = fmaxf(hi.x, h.x), hi.y = fmaxf(hi.y, h.y), hi.z = fmaxf(hi.z, h.z);
+  }
+  cbox[2 * g] = lo;
+  cbox[2 * g + 1] = hi;
+}
+
+// Warp per leaf block.  Lanes own cells (lane, lane + 32); the warp walks the
+// distinct bins of its cells, culls 32 bin chunks per step by their union
+// boxes, then the faces of surviving chunks by the reference's FP64 box cull,
+// and sweeps the (candidate face, cell-in-bin) pairs flattened over the lanes:
+// FP32 bounding-sphere prefilter, then the full predicate.  First hit ends the
+// block (a mark is an OR).  Evaluated pairs = the reference's evaluated pairs.
+constexpr int MARK_WARPS = MARK_THREADS / 32;
+
 template <int D, bool BINNED>
 __global__ void __launch_bounds__(MARK_THREADS) k_mark(MarkArgs A) {
   constexpr int C = D == 3 ? 64 : 16;
+  constexpr int CPL = D == 3 ? 2 : 1;  // cells per lane
   constexpr int PW = D == 3 ? PAY3 : PAY2;
-  __shared__ float s_cen[C][D];
-  __shared__ int s_bin[C];
-  __shared__ int s_ubin[C];
-  __shared__ int s_cells[C];
-  __shared__ int s_nu, s_ncell, s_ncand, s_hit;
-  __shared__ int s_cand[STAGE];
-  __shared__ float4 s_sph[STAGE];
-  __shared__ unsigned long long s_red[MARK_THREADS / 32];
-
+  __shared__ float s_p[MARK_WARPS][C][D];
+  __shared__ int s_act[MARK_WARPS][C];
+  __shared__ int s_cand[MARK_WARPS][32];
+  __shared__ float4 s_sph[MARK_WARPS][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t pos = (int64_t)blockIdx.x * MARK_WARPS + wid;
+  if (pos >= A.n_leaves) return;
   const ForestC& F = A.F;
-  const int id = A.leaves[blockIdx.x];
+  const int id = A.leaves[pos];
   const int L = F.level[id];
-  const int tid = threadIdx.x;
-  double blo[3], bhi[3];
+  double blo[3], bhi[3], q[3];
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    double q = block_len(F, a, L);
-    blo[a] = DADD(F.dmin[a], DMUL((double)F.coord[a][id], q));
-    bhi[a] = DADD(blo[a], q);
+    q[a] = block_len(F, a, L);
+    blo[a] = DADD(F.dmin[a], DMUL((double)F.coord[a][id], q[a]));
+    bhi[a] = DADD(blo[a], q[a]);
   }
-  if (tid < C) {
-    float p[3];
+  int bin[CPL];
+  unsigned long long t = 0;
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
-      double q = block_len(F, a, L);
-      double u = ((double)((tid >> (2 * a)) & 3) + 0.5) / 4.0;
-      p[a] = __double2float_rn(DADD(blo[a], DMUL(u, q)));
-      s_cen[tid][a] = p[a];
-    }
-    if (BINNED) {
+  for (int k = 0; k < CPL; ++k) {
+    const int c = lane + 32 * k;
+    bin[k] = 0;
+    if (c < C) {
       int lin = 0, mul = 1;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        lin += bin_axis(p[a], A.g.min32[a], A.g.len32[a], A.g.B) * mul;
-        mul *= A.g.B;
+        const double u = ((double)((c >> (2 * a)) & 3) + 0.5) / 4.0;
+        const float p = __double2float_rn(DADD(blo[a], DMUL(u, q[a])));
+        s_p[wid][c][a] = p;
+        if (BINNED) {
+          lin += bin_axis(p, A.g.min32[a], A.g.len32[a], A.g.B) * mul;
+          mul *= A.g.B;
+        }
       }
-      s_bin[tid] = lin;
+      bin[k] = lin;
+      t += BINNED ? (unsigned long long)A.bin_counts[lin] : (unsigned long long)A.n_faces;
     }
   }
-  if (tid == 0) {
-    s_hit = 0;
-    s_nu = 0;
-  }
-  __syncthreads();
-  // algorithmic test count T
-  {
-    unsigned long long t = 0;
-    if (tid < C) t = BINNED ? (unsigned long long)A.bin_counts[s_bin[tid]] : (unsigned long long)A.n_faces;
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if ((tid & 31) == 0) s_red[tid >> 5] = t;
-    __syncthreads();
-    if (tid == 0) {
-      unsigned long long sum = 0;
-      for (int w = 0; w < MARK_THREADS / 32; ++w) sum += s_red[w];
-      atomicAdd(&A.out[1], sum);
-    }
-  }
+  // algorithmic test count T, one atomic per warp
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) atomicAdd(&A.out[1], t);
   if (F.marks[id] == OW_MARKED) return;
-  if (BINNED && tid < C) {
-    bool first = true;
-    for (int j = 0; j < tid; ++j) first &= s_bin[j] != s_bin[tid];
-    if (first) s_ubin[atomicAdd(&s_nu, 1)] = s_bin[tid];
-  }
-  __syncthreads();
-  const int nu = BINNED ? s_nu : 1;
   const double reach2 = DMUL(A.reach, A.reach);
   const float r2 = FMUL(A.d, A.d);
   unsigned long long evaluated = 0;
-
-  for (int u = 0; u < nu && !s_hit; ++u) {
-    int64_t src0 = 0, srcn = A.n_faces;
-    const int32_t* src = nullptr;
-    if (BINNED) {
-      int b = s_ubin[u];
-      src = A.bin_ids + A.bin_offsets[b];
-      srcn = A.bin_counts[b];
-      if (tid == 0) s_ncell = 0;
-      __syncthreads();
-      if (tid < C && s_bin[tid] == b) s_cells[atomicAdd(&s_ncell, 1)] = tid;
-    } else {
-      if (tid < C) s_cells[tid] = tid;
-      if (tid == 0) s_ncell = C;
-    }
-    for (int64_t base = src0; base < srcn; base += STAGE) {
-      if (tid == 0) s_ncand = 0;
-      __syncthreads();
-      const int64_t m = min((int64_t)STAGE, srcn - base);
-      for (int j = tid; j < m; j += MARK_THREADS) {
-        int f = BINNED ? src[base + j] : (int)(base + j);
-        if (box_ok<D>(blo, bhi, A.box[2 * (int64_t)f], A.box[2 * (int64_t)f + 1], reach2)) {
-          int k = atomicAdd(&s_ncand, 1);
-          s_cand[k] = f;
-          s_sph[k] = A.sph[f];
-        }
-      }
-      __syncthreads();
-      const int ncand = s_ncand, ncell = s_ncell;
-      const int total = ncand * ncell;
-      for (int k = tid; k < total; k += MARK_THREADS) {
-        if (*(volatile int*)&s_hit) break;
-        int ci = s_cells[k / ncand];
-        int j = k - (k / ncand) * ncand;
-        float p[3];
+  bool pend[CPL];
 #pragma unroll
-        for (int a = 0; a < D; ++a) p[a] = s_cen[ci][a];
-        if (!sphere_ok<D>(p, s_sph[j])) continue;
-        ++evaluated;
-        if (near_face<D>(A.pay + (int64_t)s_cand[j] * PW, p, r2)) {
-          s_hit = 1;
-          break;
-        }
+  for (int k = 0; k < CPL; ++k) pend[k] = lane + 32 * k < C;
+  bool hit = false;
+  while (!hit) {
+    // next distinct bin: the bin of the lowest pending cell
+    int b = 0;
+    bool found = false;
+#pragma unroll
+    for (int k = 0; k < CPL && !found; ++k) {
+      const unsigned m = __ballot_sync(0xffffffffu, pend[k]);
+      if (m) {
+        b = __shfl_sync(0xffffffffu, bin[k], __ffs(m) - 1);
+        found = true;
       }
-      __syncthreads();
-      if (s_hit) break;
     }
-    __syncthreads();  // s_cells / s_ncell are rewritten for the next bin
+    if (!found) break;
+    int nact = 0;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const bool act = pend[k] && (!BINNED || bin[k] == b);
+      pend[k] = pend[k] && !act;
+      const unsigned m = __ballot_sync(0xffffffffu, act);
+      if (act) s_act[wid][nact + __popc(m & lanemask_lt())] = lane + 32 * k;
+      nact += __popc(m);
+    }
+    __syncwarp();
+    const int64_t off = BINNED ? A.bin_offsets[b] : 0;
+    const int64_t cnt = BINNED ? A.bin_counts[b] : A.n_faces;
+    if (cnt == 0) continue;
+    const int64_t g0 = off >> 5, g1 = (off + cnt - 1) >> 5;
+    for (int64_t gb = g0; gb <= g1 && !hit; gb += 32) {
+      const int64_t g = gb + lane;
+      bool cok = false;
+      if (g <= g1) cok = box_ok<D>(blo, bhi, A.cbox[2 * g], A.cbox[2 * g + 1], reach2);
+      unsigned cm = __ballot_sync(0xffffffffu, cok);
+      while (cm && !hit) {
+        const int64_t gc = gb + __ffs(cm) - 1;
+        cm &= cm - 1;
+        const int64_t e = gc * 32 + lane;
+        int f = 0;
+        bool fok = false;
+        if (e >= off && e < off + cnt) {
+          f = BINNED ? A.bin_ids[e] : (int)e;
+          fok = box_ok<D>(blo, bhi, A.box[2 * (int64_t)f], A.box[2 * (int64_t)f + 1], reach2);
+        }
+        const unsigned fm = __ballot_sync(0xffffffffu, fok);
+        if (!fm) continue;
+        const int nf = __popc(fm);
+        if (fok) {
+          const int r = __popc(fm & lanemask_lt());
+          s_cand[wid][r] = f;
+          s_sph[wid][r] = A.sph[f];
+        }
+        __syncwarp();
+        const int total = nf * nact;
+        for (int k0 = 0; k0 < total; k0 += 32) {
+          const int k = k0 + lane;
+          bool h = false;
+          if (k < total) {
+            const int fi = k / nact;
+            const int ci = s_act[wid][k - fi * nact];
+            float p[3];
+#pragma unroll
+            for (int a = 0; a < D; ++a) p[a] = s_p[wid][ci][a];
+            if (sphere_ok<D>(p, s_sph[wid][fi])) {
+              ++evaluated;
+              h = near_face<D>(A.pay + (int64_t)s_cand[wid][fi] * PW, p, r2);
+            }
+          }
+          if (__any_sync(0xffffffffu, h)) {
+            hit = true;
+            break;
+          }
+        }
+        __syncwarp();
+      }
+    }
   }
   for (int o = 16; o > 0; o >>= 1) evaluated += __shfl_xor_sync(0xffffffffu, evaluated, o);
-  if ((tid & 31) == 0 && evaluated) atomicAdd(&A.out[2], evaluated);
-  if (tid == 0 && s_hit) {
-    F.marks[id] = OW_MARKED;
-    atomicAdd(&A.out[0], 1ull);
+  if (lane == 0) {
+    if (evaluated) atomicAdd(&A.out[2], evaluated);
+    if (hit) {
+      F.marks[id] = OW_MARKED;
+      atomicAdd(&A.out[0], 1ull);
+    }
   }
 }
 
@@ -408,7 +448,8 @@ __global__ void k_near_pairs(int dim, const float* __restrict__ pts, const float
 extern "C" int ow_mark_near_wall(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
                                  const float* d_coords, int64_t n_faces, int64_t geom_key, const ow_grid* grid,
                                  const int32_t* d_bin_ids, const int32_t* d_bin_counts, const int32_t* d_bin_offsets,
-                                 float d_spec, double reach, int64_t* out_marked, int64_t* out_tests,
+                                 int64_t n_bin_entries, float d_spec, double reach, int64_t* out_marked,
+                                 int64_t* out_tests,
                                  int64_t* out_evaluated, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (!(d_spec > 0.0f)) {
@@ -444,8 +485,17 @@ extern "C" int ow_mark_near_wall(ow_ctx* ctx, ow_forest* f, const int32_t* d_lea
     A.d = d_spec;
     A.reach = reach;
     A.out = out;
-    dim3 grd((unsigned)n_leaves);
+    const int64_t n_entries = binned ? n_bin_entries : n_faces;
+    void* pc;
+    OW_TRY(ow_slot(ctx, SLOT_MARK_CBOX, 32 * (size_t)((n_entries + 31) / 32 + 1), s, &pc));
+    A.cbox = (const float4*)pc;
+    A.n_leaves = n_leaves;
     OW_PROF_BEGIN(ctx, PROF_MARK, s);
+    const int cg = ow_blocks((n_entries + 31) / 32, 128);
+    if (f->dim == 3) k_chunk_boxes<3><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
+    else k_chunk_boxes<2><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
+    OW_LAUNCHED(ctx);
+    dim3 grd((unsigned)((n_leaves + MARK_WARPS - 1) / MARK_WARPS));
     if (f->dim == 3) {
       if (binned) k_mark<3, true><<<grd, MARK_THREADS, 0, s>>>(A);
       else k_mark<3, false><<<grd, MARK_THREADS, 0, s>>>(A);

@@ -75,16 +75,7 @@ class Forest:
         r = int(np.prod(root_dims))
         cap = max(int(capacity or 0), 4 * r, 1024)
         self._alloc(cap)
-        idx = torch.arange(r, device=self.device, dtype=torch.int64)
-        rem = idx
-        for ax in range(self.dim):
-            self._coord[ax][:r] = (rem % self.root_dims[ax]).to(torch.int32)
-            rem = rem // self.root_dims[ax]
-        self._level_t[:r] = 0
-        self._parent_t[:r] = -1
-        self._first_child_t[:r] = -1
-        self._marks[:r] = 0
-        self._n = r
+        self._n = 0
         self._n_levels = 1
         self._version = 0
         self._leaf_cache = {}
@@ -99,6 +90,10 @@ class Forest:
             return 1 if f is None else f._grow(user, view_p, need)
 
         self._grow_cb = _lib.GROW_FN(grow)
+        # root blocks 0..R-1 (x-fastest lattice coords, level 0, no parent): one kernel
+        v = self.view()
+        _lib.call("ow_forest_init_root", _lib.ctx(), C.byref(v), _lib.stream())
+        self._sync_from_view()
 
     # ------------------------------------------------------------------ storage
     def _alloc(self, cap):

@@ -70,24 +70,16 @@ class LatticeLinks:
         return int(sum(((f >> i) & 1).sum().item() for i in range(1, 27)))
 
 
-def candidate_grid(forest: Forest):
-    """Candidate-bin grid sized to the finest level: bin edge ~ two finest blocks.
-
-    The candidate bins only prune work — the link set does not depend on them —
-    so the grid is chosen for speed (capped so the bin arrays stay small)."""
-    level = forest.n_levels - 1
-    b = max(1, max((r << level) // 2 for r in forest.root_dims))
-    cap = 160 if forest.dim == 3 else 2048
-    return BinGrid(forest.domain, min(b, cap))
-
-
 def build_lattice_links(forest: Forest, geom: CoordListGeometry, grid: BinGrid | None = None,
                         lattice="D3Q19") -> LatticeLinks:
-    """Boundary links of the finest level; ``grid`` only chooses the candidate
-    bins (None: sized to the finest level) and never changes the result."""
+    """Boundary links of the finest level.
+
+    Candidate faces come from the forest itself (each face visits the finest
+    blocks its box can reach), so ``grid`` is accepted for API stability,
+    checked for dimension, and otherwise unused: it never changes the result."""
     dirs = lattice_directions(lattice)
-    if grid is None:
-        grid = candidate_grid(forest)
+    if grid is not None and grid.dim != forest.dim:
+        raise InvalidParameterError(f"bin grid is {grid.dim}D but forest is {forest.dim}D")
     if dirs.shape[1] != forest.dim or geom.dim != forest.dim:
         raise InvalidParameterError(f"lattice {lattice} does not match a {forest.dim}D forest")
     if geom.n_faces == 0:
@@ -100,11 +92,11 @@ def build_lattice_links(forest: Forest, geom: CoordListGeometry, grid: BinGrid |
     dev = forest.device
     flags = torch.empty(n_leaves * ncell, dtype=torch.int32, device=dev)
     nb = C.c_int64(0)
-    g = grid.c_struct()
     hd = np.ascontiguousarray(dirs.reshape(-1))
     ctx, st = _lib.ctx(), _lib.stream()
-    _lib.call("ow_lattice_links_count", ctx, C.byref(forest.view()), _lib.ptr(leaves), n_leaves,
-              _lib.ptr(geom.coords), geom.n_faces, geom.key, C.byref(g), hd.ctypes.data_as(C.c_void_p), len(dirs),
+    _lib.call("ow_lattice_links_count", ctx, C.byref(forest.view()), level, _lib.ptr(leaves), n_leaves,
+              _lib.ptr(geom.coords), geom.n_faces, geom.key, None,
+              hd.ctypes.data_as(C.c_void_p), len(dirs),
               _lib.ptr(flags), C.byref(nb), st)
     n_b = int(nb.value)
     cells = torch.empty(n_b, dtype=torch.int64, device=dev)

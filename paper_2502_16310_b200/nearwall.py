@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib, backends
-from .binning import BinGrid, BinnedFaces, auto_bin_fraction, fill_bins
+from .binning import BinGrid, BinnedFaces, auto_bin_fraction, default_spacing, fill_bins
 from .errors import InvalidParameterError
 from .forest import Forest, RefineMark
 from .geometry import CoordListGeometry, bounding_box, validate_faces
@@ -71,7 +71,7 @@ def _mark(forest, level, geom, d_spec, bins, grid, leaves=None):
               _lib.ptr(bins.ids) if bins is not None else None,
               _lib.ptr(bins.counts) if bins is not None else None,
               _lib.ptr(bins.offsets) if bins is not None else None,
-              float(np.float32(d_spec)), float(reach), C.byref(m), C.byref(t), C.byref(e), _lib.stream())
+              int(bins.ids.numel()) if bins is not None else 0, float(np.float32(d_spec)), float(reach), C.byref(m), C.byref(t), C.byref(e), _lib.stream())
     return MarkStats(int(m.value), int(t.value), int(e.value))
 
 
@@ -200,10 +200,12 @@ def refine_near_wall(forest: Forest, geom: CoordListGeometry, params: NearWallPa
                      shard=None) -> NearWallResult:
     """Per level L in 0..n_levels-2: bins -> mark -> propagate -> refine.
 
-    The bin CSR depends only on (geometry, grid), so it is built once and
-    reused for every level (``reuse_bins``); the reference rebuilds an
-    identical structure per level.  ``shard`` (a ``parallel.Shard``) splits the
-    marking pass across ranks and all-gathers the marks (multi-GPU).
+    The level loop runs natively (``ow_refine_near_wall``): one host call per
+    pass over the geometry, device-event stage timings.  The bin CSR depends
+    only on (geometry, grid), so it is built once and reused for every level
+    (``reuse_bins``); the reference rebuilds an identical structure per level.
+    ``shard`` (a ``parallel.Shard``) splits each marking pass across ranks and
+    all-gathers the marks through the driver's exchange callback (multi-GPU).
     """
     if geom.n_faces == 0:
         raise InvalidParameterError("cannot refine around empty geometry")
@@ -218,43 +220,75 @@ def refine_near_wall(forest: Forest, geom: CoordListGeometry, params: NearWallPa
     bf = params.bin_fraction
     if binned and bf is None:
         bf = auto_bin_fraction(BinGrid(forest.domain, b).n_bins, geom.n_faces)
-
-    def record(stage, level, ms):
-        result.timings.append(StageTiming(stage, level, params.strategy, b, bf if binned else 1, ms))
-
-    bins = grid = None
-    for level in range(params.n_levels - 1):
-        if binned:
-            with _Clock(False) as ck:
-                if bins is None or not reuse_bins:
-                    grid = BinGrid(forest.domain, params.bins_per_axis)
-                    bins = fill_bins(geom, grid, bin_fraction=bf, overlap_factor=params.overlap_factor,
-                                     spacing=params.spacing, backend=params.backend)
-            record("bin_setup", level, ck.ms)
-            result.bins, result.grid = bins, grid
-            with _Clock(False) as ck:
-                _check_marking_inputs(forest, geom, params.d_spec)
-                st = _mark_level(forest, level, geom, params.d_spec, bins, grid, shard)
-            record("face_detection", level, ck.ms)
-            with _Clock(False) as ck:
-                propagate_marks(forest, level, params.d_spec, backend=params.backend)
-            record("propagation", level, ck.ms)
-        else:
-            with _Clock(False) as ck:
-                _check_marking_inputs(forest, geom, params.d_spec)
-                st = _mark_level(forest, level, geom, params.d_spec, None, None, shard)
-            record("face_detection", level, ck.ms)
-        result.marked_detected.append(st.marked)
-        result.cell_face_tests.append(st.tests)
-        result.pairs_evaluated.append(st.evaluated)
-        n_marked = forest.count_marks(level, RefineMark.MARKED, leaf_only=True)
-        result.marked_refined.append(n_marked)
-        with _Clock(False) as ck:
-            # pre-size for the marked splits plus rebalance slack, so the C
-            # side rarely needs its grow callback mid-refinement
-            forest.reserve(forest.n_blocks + forest.n_children * (n_marked + n_marked // 2 + 64))
-            forest.refine_marked(level)
-        record("refinement", level, ck.ms)
+    if params.n_levels - 1 > _lib.MAX_PASSES:
+        raise InvalidParameterError(f"n_levels must be <= {_lib.MAX_PASSES + 1}, got {params.n_levels}")
+    passes = params.n_levels - 1
+    if passes == 0:
+        return result
+    _check_marking_inputs(forest, geom, params.d_spec)
+    dev = forest.device
+    grid = bins_t = None
+    g = None
+    cap = 0
+    if binned:
+        grid = BinGrid(forest.domain, params.bins_per_axis)
+        backends.validate_backend(params.backend)
+        if bf is not None and bf < 1:
+            raise InvalidParameterError(f"bin_fraction must be >= 1, got {bf}")
+        h = np.float32(params.spacing) if params.spacing is not None else np.float32(default_spacing(grid))
+        if h <= 0:
+            raise InvalidParameterError(f"spacing must be positive, got {h}")
+        cap = max(1, params.overlap_factor * geom.n_faces)
+        bins_t = (torch.empty(cap, dtype=torch.int32, device=dev), torch.empty(grid.n_bins, dtype=torch.int32, device=dev),
+                  torch.empty(grid.n_bins, dtype=torch.int32, device=dev))
+        g = grid.c_struct()
+    p = _lib.NearWallParamsC()
+    p.d_spec = float(np.float32(params.d_spec))
+    p.n_levels = params.n_levels
+    p.d_spec64 = float(params.d_spec)
+    p.reach = float(_cull_reach(params.d_spec, _coordinate_scale(forest, geom)))
+    p.binned = int(binned)
+    p.reuse_bins = int(bool(reuse_bins))
+    p.spacing = float(h) if binned else 0.0
+    p.overlap_factor = int(params.overlap_factor)
+    p.bin_fraction = int(bf or 1)
+    exch = None
+    if shard is not None and shard.world > 1:
+        p.rank, p.world = shard.rank, shard.world
+        exch = _lib.EXCHANGE_FN(shard.exchange_callback(forest))
+        p.exchange = exch
+    else:
+        p.rank, p.world = 0, 1
+    out = _lib.NearWallResultC()
+    v = forest.view()
+    try:
+        _lib.call("ow_refine_near_wall", _lib.ctx(), C.byref(v), _lib.ptr(geom.coords), geom.n_faces, geom.key,
+                  C.byref(g) if g is not None else None, C.byref(p),
+                  _lib.ptr(bins_t[0]) if binned else None, cap,
+                  _lib.ptr(bins_t[1]) if binned else None, _lib.ptr(bins_t[2]) if binned else None,
+                  C.byref(out), _lib.stream())
+    finally:
+        forest._sync_from_view()
+        forest._version += 1
+        forest._leaf_cache.clear()
+        for level in range(out.n_passes):
+            if out.n_split[level] > 0:
+                forest._n_levels = max(forest._n_levels, level + 2)
+    stages = ("bin_setup", "face_detection", "propagation", "refinement")
+    for level in range(out.n_passes):
+        for k, stage in enumerate(stages):
+            if stage in ("bin_setup", "propagation") and not binned:
+                continue
+            result.timings.append(StageTiming(stage, level, params.strategy, b, bf if binned else 1,
+                                              float(out.stage_ms[level][k])))
+        result.marked_detected.append(int(out.marked_detected[level]))
+        result.marked_refined.append(int(out.marked_refined[level]))
+        result.cell_face_tests.append(int(out.tests[level]))
+        result.pairs_evaluated.append(int(out.evaluated[level]))
+    if binned:
+        e = int(out.bin_entries)
+        result.bins = BinnedFaces(grid.n_bins, bins_t[0][:e], bins_t[1], bins_t[2])
+        result.grid = grid
     return result
 
 

@@ -15,6 +15,17 @@ import torch
 import torch.distributed as dist
 
 
+def _wrap_int32(ptr, n, device):
+    """Zero-copy int32 CUDA tensor over n elements of device memory at ptr."""
+    if n == 0:
+        return torch.zeros(0, dtype=torch.int32, device=device)
+
+    class _Cuda:
+        __cuda_array_interface__ = {"shape": (int(n),), "typestr": "<i4", "data": (int(ptr), False), "version": 2}
+
+    return torch.as_tensor(_Cuda(), device=device)
+
+
 def partition(n, rank, world, weights=None):
     """[lo, hi) slice of n ordered units for ``rank``; balanced by ``weights``
     (a 1-D cumulative-work tensor) when given, else by count."""
@@ -33,7 +44,11 @@ def partition(n, rank, world, weights=None):
 
 def gather_slices(local, n, world, group=None):
     """All-gather variable-length contiguous slices (padded to the largest);
-    returns the concatenation in rank order, length n."""
+    returns the concatenation in rank order, length n.  NCCL gathers device
+    memory directly; under gloo (CPU tests, several ranks on one device) the
+    slices are staged through host memory."""
+    if local.is_cuda and dist.get_backend(group) == "gloo":
+        return gather_slices(local.cpu(), n, world, group).to(local.device)
     per = (n + world - 1) // world if world > 1 else n
     dev = local.device
     counts = torch.tensor([local.numel()], dtype=torch.int64, device=dev)
@@ -58,6 +73,32 @@ class Shard:
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+
+    def exchange_callback(self, forest):
+        """ow_exchange_fn for the native driver: all-gather the marks of the
+        level's leaves (each rank marked [lo, hi)) and sum the statistics."""
+
+        def cb(_user, level, d_leaves, n, lo, hi, stats3):
+            try:
+                ptr = int(d_leaves or 0)
+                leaves = _wrap_int32(ptr, n, forest.device)
+                idx = leaves.to(torch.int64)
+                mine = forest._marks.index_select(0, idx[lo:hi])
+                allm = gather_slices(mine, n, self.world, self.group)
+                forest._marks.index_copy_(0, idx, allm)
+                sdev = "cpu" if dist.get_backend(self.group) == "gloo" else forest.device
+                tot = torch.tensor([stats3[0], stats3[1], stats3[2]], dtype=torch.int64, device=sdev)
+                dist.all_reduce(tot, group=self.group)
+                for i, x in enumerate(tot.tolist()):
+                    stats3[i] = int(x)
+                return 0
+            except Exception:  # pragma: no cover - surfaced by the C side as an exchange failure
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        return cb
 
     def mark_level(self, forest, level, geom, d_spec, bins, grid, mark_fn):
         from .nearwall import MarkStats

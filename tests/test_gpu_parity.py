@@ -285,7 +285,7 @@ def test_pipeline_random_soups_vs_oracle(ow, dim, seed, n_faces, root, d, B):
 
 
 # --------------------------------------------------------------------------- lattice links vs oracle
-@pytest.mark.parametrize("case", ["circle", "icosphere"])
+@pytest.mark.parametrize("case", ["circle", "icosphere", "soup3d", "soup2d"])
 def test_lattice_links_vs_oracle(ow, case):
     from oracle import forest as of
     from oracle import lattice as ol
@@ -299,6 +299,22 @@ def test_lattice_links_vs_oracle(ow, case):
     elif case == "icosphere":
         coords = np.ascontiguousarray(np.transpose(shapes.icosphere_triangles(3).astype(np.float32), (1, 2, 0)))
         dim, root, d, lat = 3, 4, 0.08, "D3Q19"
+    elif case in ("soup3d", "soup2d"):
+        # random small faces, some snapped onto cell-centre planes and block seams
+        dim = 3 if case == "soup3d" else 2
+        rng = np.random.default_rng(7 + dim)
+        n = 400 if dim == 3 else 300
+        anchors = rng.uniform(0.05, 0.95, (n, dim))
+        snap = rng.random((n, dim)) < 0.3
+        anchors[snap] = np.round(anchors[snap] * 128) / 128
+        coords = np.zeros((dim, dim, n), np.float32)
+        for j in range(dim):
+            coords[j] = (anchors + (rng.uniform(-0.03, 0.03, (n, dim)) if j else 0.0)).T.astype(np.float32)
+        from oracle.geometry import first_degenerate
+
+        while first_degenerate(coords) >= 0:
+            coords[:, :, first_degenerate(coords)] += np.float32(1e-3)
+        root, d, lat = 4, 0.06, "D3Q27" if dim == 3 else "D2Q9"
     else:
         from golden.make_golden import cube_triangles  # noqa: F401  (recipe only; reference not imported)
         raise pytest.skip("covered by icosphere/circle")
@@ -339,3 +355,60 @@ def test_lattice_known_answers_on_gpu(ow, case):
     np.testing.assert_array_equal(ll.flags.cpu().numpy().view(np.uint32), ref["flags"])
     np.testing.assert_array_equal(ll.cells.cpu().numpy(), ref["boundary"])
     np.testing.assert_array_equal(ll.q.cpu().numpy(), ref["q"])
+
+
+# --------------------------------------------------------------------------- sharded driver (2 ranks, 1 GPU)
+def _shard_worker(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2502_16310_b200 as ow
+        from paper_2502_16310_b200 import parallel, shapes
+
+        torch.cuda.set_device(0)
+        coords = np.ascontiguousarray(np.transpose(shapes.icosphere_triangles(3).astype(np.float32), (1, 2, 0)))
+        geom = ow.CoordListGeometry(3, coords)
+        f = ow.init_root_grid(ow.Aabb(np.zeros(3), np.ones(3)), (8, 8, 8))
+        res = ow.refine_near_wall(f, geom, ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8),
+                                  shard=parallel.Shard())
+        q.put((rank, f._coords, f._first_child, res.marked_detected, res.cell_face_tests))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_sharded_native_driver_matches_single_rank(ow):
+    """Two ranks (gloo, one GPU) each mark half of every level through the
+    native driver's exchange hook; the gathered forest equals one rank's."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_2502_16310_b200 import shapes
+
+    coords = np.ascontiguousarray(np.transpose(shapes.icosphere_triangles(3).astype(np.float32), (1, 2, 0)))
+    geom = ow.CoordListGeometry(3, coords)
+    f = ow.init_root_grid(ow.Aabb(np.zeros(3), np.ones(3)), (8, 8, 8))
+    ref = ow.refine_near_wall(f, geom, ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=500) for _ in procs]
+    for p in procs:
+        p.join(60)
+    assert all(p.exitcode == 0 for p in procs)
+    for _, co, fc, md, t in outs:
+        np.testing.assert_array_equal(co, f._coords)
+        np.testing.assert_array_equal(fc, f._first_child)
+        assert md == ref.marked_detected and t == ref.cell_face_tests

@@ -34,7 +34,7 @@ def main():
         torch.cuda.synchronize()
         t["import"] = time.perf_counter() - t0
         t0 = time.perf_counter()
-        f = ow.init_root_grid(dom, (cfg["root"],) * dim, capacity=8 * cfg["root"] ** dim)
+        f = ow.init_root_grid(dom, (cfg["root"],) * dim, capacity=32 * cfg["root"] ** dim)
         torch.cuda.synchronize()
         t["init"] = time.perf_counter() - t0
         t0 = time.perf_counter()
