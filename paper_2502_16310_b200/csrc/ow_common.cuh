@@ -70,8 +70,11 @@ enum ow_slot {
   SLOT_LAT_TILEROW,    // first row of each intersection tile
   SLOT_LAT_HITS,       // hit list (flat cell, t bits)
   SLOT_LAT_HITDIR,     // hit list directions
+  SLOT_LAT_TILEHITS,   // hits per intersection tile
   SLOT_LAT_BMASK,      // boundary-cell mask per candidate block
   SLOT_MARK_CBOX,      // union boxes of 32-entry bin chunks (marking cull)
+  SLOT_MARK_ITEMS,     // (block, chunk, bin) marking items
+  SLOT_MARK_HIT,       // per-leaf hit words of a marking pass
   SLOT_DRV_LEAVES,     // native driver: leaves of the current level
   SLOT_MISC,
   SLOT_COUNT
@@ -126,6 +129,8 @@ struct ow_ctx {
   uint32_t* lat_flags;
   ow_forest lat_forest;
   void* stage_events;  // native driver CUDA events
+  int64_t mark_item_cap;
+  bool mark_rerun;
 };
 
 // refine_marked returning the MARKED-leaf count of the split pass as well

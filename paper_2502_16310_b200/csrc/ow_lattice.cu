@@ -63,7 +63,7 @@ struct LatArgs {
   uint32_t* flags;          // [n_leaves * C]
   uint2* hits;              // [<= n_units] (flat cell, t bits)
   uint8_t* hit_dir;         // [<= n_units] direction of each hit
-  unsigned long long* n_hits;
+  int32_t* tile_hits;       // [n_tiles] hits of each MT tile
   int32_t* bcount;          // [n_cb] boundary cells per candidate block
   unsigned long long* bmask;  // [n_cb] boundary-cell mask
   const int64_t* boff;      // [n_cb]
@@ -294,8 +294,8 @@ struct RowCntStore {
 // overflow to +inf meaning "not tiny").  A miss never pays for a division and a
 // hit gets the quotient bits the oracle computes.
 __device__ __forceinline__ bool quot_nonneg(float a, float det) {
-  if (a == 0.0f || ((a > 0.0f) == (det > 0.0f))) return true;
-  return FMUL(FMUL(fabsf(a), 0x1p75f), 0x1p75f) <= fabsf(det);
+  // branch-free: evaluated for every unit of the sweep
+  return (a == 0.0f) | ((a > 0.0f) == (det > 0.0f)) | (FMUL(FMUL(fabsf(a), 0x1p75f), 0x1p75f) <= fabsf(det));
 }
 
 // x / ext for 0 <= x < 64, ext in 1..4 (multiply-shift, exact in that range)
@@ -320,7 +320,9 @@ __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
   __shared__ float4 s_e2[MT_TILE + 1];    // e2.xyz, p.y
   __shared__ float s_pz[MT_TILE + 1];     // p.z
   __shared__ float s_dv[QMAX][3];
+  __shared__ int s_nh;
   for (int i = threadIdx.x; i < QMAX * 3; i += MT_THREADS) s_dv[i / 3][i % 3] = A.dv[i / 3][i % 3];
+  if (threadIdx.x == 0) s_nh = 0;
   const int64_t U = A.n_units;
   const int64_t R = A.n_rows;
   const int64_t n_tiles = (U + MT_TILE - 1) / MT_TILE;
@@ -396,19 +398,15 @@ __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
           const float det = V.w, px = E1.w, py = E2.w, pz = s_pz[row];
           const float tx = FSUB(x[0], V.x), ty = FSUB(x[1], V.y), tz = FSUB(x[2], V.z);
           const float un = dot3f(tx, ty, tz, px, py, pz);
-          if (quot_nonneg(un, det)) {
-            const float qx = FSUB(FMUL(ty, E1.z), FMUL(tz, E1.y));
-            const float qy = FSUB(FMUL(tz, E1.x), FMUL(tx, E1.z));
-            const float qz = FSUB(FMUL(tx, E1.y), FMUL(ty, E1.x));
-            const float vn = dot3f(dv[0], dv[1], dv[2], qx, qy, qz);
-            const float tn = dot3f(E2.x, E2.y, E2.z, qx, qy, qz);
-            if (quot_nonneg(vn, det) && quot_nonneg(tn, det)) {
-              const float uu = FDIV(un, det), vv = FDIV(vn, det);
-              if (FADD(uu, vv) <= 1.0f) {
-                t = FDIV(tn, det);
-                hit = t <= 1.0f;
-              }
-            }
+          const float qx = FSUB(FMUL(ty, E1.z), FMUL(tz, E1.y));
+          const float qy = FSUB(FMUL(tz, E1.x), FMUL(tx, E1.z));
+          const float qz = FSUB(FMUL(tx, E1.y), FMUL(ty, E1.x));
+          const float vn = dot3f(dv[0], dv[1], dv[2], qx, qy, qz);
+          const float tn = dot3f(E2.x, E2.y, E2.z, qx, qy, qz);
+          if (quot_nonneg(un, det) & quot_nonneg(vn, det) & quot_nonneg(tn, det)) {
+            const float uu = FDIV(un, det), vv = FDIV(vn, det);
+            t = FDIV(tn, det);
+            hit = (FADD(uu, vv) <= 1.0f) & (t <= 1.0f);
           }
         } else {
           // segment-segment (oracle/lattice.py:seg_hits), s = b - a pre-formed
@@ -424,19 +422,25 @@ __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
           }
         }
       }
-      if (hit) atomicOr(&A.flags[cellg], 1u << d);
-      // warp-aggregated append to the hit list: (flat cell, dir | t bits)
+      // hits of this tile go to its own slots [u0, u0 + n) of the hit list
+      // (a tile has at most MT_TILE hits): shared-memory append, no global counter
       const unsigned hm = __ballot_sync(0xffffffffu, hit);
       if (hm) {
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(A.n_hits, (unsigned long long)__popc(hm));
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&s_nh, __popc(hm));
         base = __shfl_sync(0xffffffffu, base, 0);
         if (hit) {
-          const unsigned long long k = base + __popc(hm & lanemask_lt());
+          atomicOr(&A.flags[cellg], 1u << d);
+          const int64_t k = u0 + base + __popc(hm & lanemask_lt());
           A.hits[k] = make_uint2((unsigned)cellg, __float_as_uint(FADD(t, 0.0f)));  // -0 -> +0
           A.hit_dir[k] = (uint8_t)d;
         }
       }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      A.tile_hits[tile] = s_nh;
+      s_nh = 0;
     }
   }
 }
@@ -479,18 +483,25 @@ __global__ void k_lat_emit(LatArgs A) {
   for (int i = 0; i < A.nq; ++i) q[i] = ((fl >> i) & 1) ? __uint_as_float(0x7f7f7f7fu) : -1.0f;
 }
 
-// min t per (boundary row, direction): t >= 0, so float order = uint order
+// min t per (boundary row, direction): t >= 0, so float order = uint order.
+// Warp per MT tile over that tile's hit slots.
 template <int D>
 __global__ void k_lat_hits(LatArgs A) {
   constexpr int C = D == 3 ? 64 : 16;
-  const int64_t n = (int64_t)*A.n_hits;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint2 h = A.hits[i];
-    const int64_t pos = h.x / C;
-    const int c = (int)(h.x % C);
-    const int r = A.cand_rank[pos];
-    const int64_t row = A.boff[r] + __popcll(A.bmask[r] & ((1ull << c) - 1ull));
-    atomicMin(reinterpret_cast<unsigned*>(A.q_out) + row * A.nq + A.hit_dir[i], h.y);
+  const int64_t n_tiles = (A.n_units + MT_TILE - 1) / MT_TILE;
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_tiles;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int n = A.tile_hits[t];
+    for (int j = lane; j < n; j += 32) {
+      const int64_t i = t * MT_TILE + j;
+      const uint2 h = A.hits[i];
+      const int64_t pos = h.x / C;
+      const int c = (int)(h.x % C);
+      const int r = A.cand_rank[pos];
+      const int64_t row = A.boff[r] + __popcll(A.bmask[r] & ((1ull << c) - 1ull));
+      atomicMin(reinterpret_cast<unsigned*>(A.q_out) + row * A.nq + A.hit_dir[i], h.y);
+    }
   }
 }
 
@@ -527,7 +538,7 @@ LatArgs make_args(ow_ctx* ctx) {
   A.flags = ctx->lat_flags;
   A.hits = (uint2*)ctx->slot_ptr[SLOT_LAT_HITS];
   A.hit_dir = (uint8_t*)ctx->slot_ptr[SLOT_LAT_HITDIR];
-  A.n_hits = (unsigned long long*)(ctx->d_small + 36);
+  A.tile_hits = (int32_t*)ctx->slot_ptr[SLOT_LAT_TILEHITS];
   A.bcount = (int32_t*)ctx->slot_ptr[SLOT_LAT_BCOUNT];
   A.bmask = (unsigned long long*)ctx->slot_ptr[SLOT_LAT_BMASK];
   A.boff = (const int64_t*)ctx->slot_ptr[SLOT_LAT_BOFFS];
@@ -611,6 +622,7 @@ extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, int32_t l
     OW_TRY(ow_slot(ctx, SLOT_LAT_TILEROW, 4 * (size_t)(n_units / MT_TILE + 2), s, &p));
     OW_TRY(ow_slot(ctx, SLOT_LAT_HITS, 8 * (size_t)n_units, s, &p));
     OW_TRY(ow_slot(ctx, SLOT_LAT_HITDIR, (size_t)n_units, s, &p));
+    OW_TRY(ow_slot(ctx, SLOT_LAT_TILEHITS, 4 * (size_t)(n_units / MT_TILE + 2), s, &p));
     OW_TRY(ow_slot(ctx, SLOT_LAT_BCOUNT, 4 * (size_t)n_cb, s, &p));
     OW_TRY(ow_slot(ctx, SLOT_LAT_BMASK, 8 * (size_t)n_cb, s, &p));
     OW_TRY(ow_slot(ctx, SLOT_LAT_BOFFS, 8 * (size_t)n_cb, s, &p));

@@ -147,151 +147,281 @@ __global__ void k_chunk_boxes(const int32_t* __restrict__ ids, int64_t n_entries
   cbox[2 * g + 1] = hi;
 }
 
-// Warp per leaf block.  Lanes own cells (lane, lane + 32); the warp walks the
-// distinct bins of its cells, culls 32 bin chunks per step by their union
-// boxes, then the faces of surviving chunks by the reference's FP64 box cull,
-// and sweeps the (candidate face, cell-in-bin) pairs flattened over the lanes:
-// FP32 bounding-sphere prefilter, then the full predicate.  First hit ends the
-// block (a mark is an OR).  Evaluated pairs = the reference's evaluated pairs.
+// Marking, two flat passes so no block's work is one long serial chain:
+//  k_mark_blocks : warp per leaf block.  Cell centres (FP64 -> one FP32
+//                  rounding) and bins, the algorithmic test count T; per
+//                  distinct bin of its cells, the 32-entry bin chunks whose union
+//                  box passes the reference's FP64 box cull.  The first CG
+//                  surviving chunks are swept inline (most near-wall blocks hit
+//                  there and stop: a mark is an OR); the rest become
+//                  (block, chunk, bin) items.
+//  k_mark_items  : warp per item, skipped once its block is hit.  Blocks that
+//                  reach this pass are mostly undecided ones that must test
+//                  every candidate, so flattening them costs no early exits.
+// Per chunk: its faces passing the box cull are staged, and the (candidate
+// face, cell-in-bin) pairs are swept flattened over the lanes: FP32
+// bounding-sphere prefilter, then the full predicate.  Every evaluated pair
+// is one the reference evaluates (same culls), so marks are bit-exact even
+// where the predicate is ill-conditioned.
 constexpr int MARK_WARPS = MARK_THREADS / 32;
+constexpr int CG = 4;  // chunks swept inline by the block pass
 
+struct MarkItems {
+  int4* items;                  // (leaf position, chunk, bin, 0)
+  unsigned long long* n_items;  // device counter
+  int64_t cap;
+  unsigned* hit;                // [n_leaves] block hit words
+};
+
+template <int D>
+struct MarkSmem {
+  static constexpr int C = D == 3 ? 64 : 16;
+  float p[MARK_WARPS][C][D];
+  int act[MARK_WARPS][C];
+  int cand[MARK_WARPS][32 * CG];
+  float4 sph[MARK_WARPS][32 * CG];
+};
+
+// cell centres + bins of the lane's cells (c = lane, lane + 32), block box
 template <int D, bool BINNED>
-__global__ void __launch_bounds__(MARK_THREADS) k_mark(MarkArgs A) {
+__device__ __forceinline__ void block_cells(const MarkArgs& A, int id, int lane, double* blo, double* bhi,
+                                            float (*p)[3], int* bin) {
   constexpr int C = D == 3 ? 64 : 16;
-  constexpr int CPL = D == 3 ? 2 : 1;  // cells per lane
-  constexpr int PW = D == 3 ? PAY3 : PAY2;
-  __shared__ float s_p[MARK_WARPS][C][D];
-  __shared__ int s_act[MARK_WARPS][C];
-  __shared__ int s_cand[MARK_WARPS][32];
-  __shared__ float4 s_sph[MARK_WARPS][32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t pos = (int64_t)blockIdx.x * MARK_WARPS + wid;
-  if (pos >= A.n_leaves) return;
-  const ForestC& F = A.F;
-  const int id = A.leaves[pos];
-  const int L = F.level[id];
-  double blo[3], bhi[3], q[3];
+  constexpr int CPL = D == 3 ? 2 : 1;
+  const int L = A.F.level[id];
+  double q[3];
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    q[a] = block_len(F, a, L);
-    blo[a] = DADD(F.dmin[a], DMUL((double)F.coord[a][id], q[a]));
+    q[a] = block_len(A.F, a, L);
+    blo[a] = DADD(A.F.dmin[a], DMUL((double)A.F.coord[a][id], q[a]));
     bhi[a] = DADD(blo[a], q[a]);
   }
-  int bin[CPL];
-  unsigned long long t = 0;
 #pragma unroll
   for (int k = 0; k < CPL; ++k) {
     const int c = lane + 32 * k;
-    bin[k] = 0;
+    bin[k] = -1;
     if (c < C) {
       int lin = 0, mul = 1;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         const double u = ((double)((c >> (2 * a)) & 3) + 0.5) / 4.0;
-        const float p = __double2float_rn(DADD(blo[a], DMUL(u, q[a])));
-        s_p[wid][c][a] = p;
+        p[k][a] = __double2float_rn(DADD(blo[a], DMUL(u, q[a])));
         if (BINNED) {
-          lin += bin_axis(p, A.g.min32[a], A.g.len32[a], A.g.B) * mul;
+          lin += bin_axis(p[k][a], A.g.min32[a], A.g.len32[a], A.g.B) * mul;
           mul *= A.g.B;
         }
       }
       bin[k] = lin;
-      t += BINNED ? (unsigned long long)A.bin_counts[lin] : (unsigned long long)A.n_faces;
     }
   }
+}
+
+// stage the lane's cells of bin b (all cells for the naive strategy)
+template <int D, bool BINNED>
+__device__ __forceinline__ int stage_cells(MarkSmem<D>& S, int wid, int lane, const float (*p)[3], const int* bin,
+                                           int b) {
+  constexpr int CPL = D == 3 ? 2 : 1;
+  int nact = 0;
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    const bool act = bin[k] >= 0 && (!BINNED || bin[k] == b);
+    const unsigned m = __ballot_sync(0xffffffffu, act);
+    if (act) {
+      const int c = lane + 32 * k;
+      S.act[wid][nact + __popc(m & lanemask_lt())] = c;
+#pragma unroll
+      for (int a = 0; a < D; ++a) S.p[wid][c][a] = p[k][a];
+    }
+    nact += __popc(m);
+  }
+  __syncwarp();
+  return nact;
+}
+
+// box-cull the entries of up to CG chunks gc[] (of bin range [off, off+cnt)),
+// stage the survivors, sweep (face, cell) pairs; true on a hit
+template <int D, bool BINNED>
+__device__ __forceinline__ bool sweep_chunks(const MarkArgs& A, MarkSmem<D>& S, int wid, int lane, const int64_t* gc,
+                                             int64_t off, int64_t cnt, const double* blo, const double* bhi,
+                                             double reach2, float r2, int nact, unsigned magic,
+                                             unsigned long long& evaluated) {
+  constexpr int PW = D == 3 ? PAY3 : PAY2;
+  int fv[CG];
+  bool fok[CG];
+#pragma unroll
+  for (int j = 0; j < CG; ++j) {  // independent loads: the id -> box chains overlap
+    const int64_t e = gc[j] * 32 + lane;
+    fok[j] = gc[j] >= 0 && e >= off && e < off + cnt;
+    fv[j] = fok[j] ? (BINNED ? A.bin_ids[e] : (int)e) : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < CG; ++j)
+    if (fok[j]) fok[j] = box_ok<D>(blo, bhi, A.box[2 * (int64_t)fv[j]], A.box[2 * (int64_t)fv[j] + 1], reach2);
+  int nf = 0;
+#pragma unroll
+  for (int j = 0; j < CG; ++j) {
+    const unsigned fm = __ballot_sync(0xffffffffu, fok[j]);
+    if (fok[j]) {
+      const int r = nf + __popc(fm & lanemask_lt());
+      S.cand[wid][r] = fv[j];
+      S.sph[wid][r] = A.sph[fv[j]];
+    }
+    nf += __popc(fm);
+  }
+  if (!nf) return false;
+  __syncwarp();
+  const int total = nf * nact;
+  bool hit = false;
+  for (int k0 = 0; k0 < total && !hit; k0 += 32) {
+    const int k = k0 + lane;
+    bool h = false;
+    if (k < total) {
+      const int fi = (int)__umulhi((unsigned)k, magic);  // k / nact (exact: k < 2^13, nact <= 64)
+      const int ci = S.act[wid][k - fi * nact];
+      float pp[3];
+#pragma unroll
+      for (int a = 0; a < D; ++a) pp[a] = S.p[wid][ci][a];
+      if (sphere_ok<D>(pp, S.sph[wid][fi])) {
+        ++evaluated;
+        h = near_face<D>(A.pay + (int64_t)S.cand[wid][fi] * PW, pp, r2);
+      }
+    }
+    hit = __any_sync(0xffffffffu, h);
+  }
+  __syncwarp();
+  return hit;
+}
+
+__device__ __forceinline__ unsigned div_magic(int n) { return (unsigned)((0x100000000ull + n - 1) / n); }
+
+template <int D, bool BINNED>
+__global__ void __launch_bounds__(MARK_THREADS) k_mark_blocks(MarkArgs A, MarkItems M) {
+  constexpr int CPL = D == 3 ? 2 : 1;
+  __shared__ MarkSmem<D> S;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t pos = (int64_t)blockIdx.x * MARK_WARPS + wid;
+  if (pos >= A.n_leaves) return;
+  const int id = A.leaves[pos];
+  double blo[3], bhi[3];
+  float p[CPL][3];
+  int bin[CPL];
+  block_cells<D, BINNED>(A, id, lane, blo, bhi, p, bin);
+  unsigned long long t = 0;
+#pragma unroll
+  for (int k = 0; k < CPL; ++k)
+    if (bin[k] >= 0) t += BINNED ? (unsigned long long)A.bin_counts[bin[k]] : (unsigned long long)A.n_faces;
   // algorithmic test count T, one atomic per warp
   for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
   if (lane == 0) atomicAdd(&A.out[1], t);
-  if (F.marks[id] == OW_MARKED) return;
+  if (A.F.marks[id] == OW_MARKED) return;
   const double reach2 = DMUL(A.reach, A.reach);
   const float r2 = FMUL(A.d, A.d);
   unsigned long long evaluated = 0;
   bool pend[CPL];
 #pragma unroll
-  for (int k = 0; k < CPL; ++k) pend[k] = lane + 32 * k < C;
-  bool hit = false;
+  for (int k = 0; k < CPL; ++k) pend[k] = bin[k] >= 0;
+  bool hit = false, inline_left = true;
   while (!hit) {
-    // next distinct bin: the bin of the lowest pending cell
-    int b = 0;
+    int b = 0;  // next distinct bin: the bin of the lowest pending cell
     bool found = false;
 #pragma unroll
-    for (int k = 0; k < CPL && !found; ++k) {
+    for (int k = 0; k < CPL; ++k) {
       const unsigned m = __ballot_sync(0xffffffffu, pend[k]);
-      if (m) {
+      if (m && !found) {
         b = __shfl_sync(0xffffffffu, bin[k], __ffs(m) - 1);
         found = true;
       }
     }
     if (!found) break;
-    int nact = 0;
 #pragma unroll
-    for (int k = 0; k < CPL; ++k) {
-      const bool act = pend[k] && (!BINNED || bin[k] == b);
-      pend[k] = pend[k] && !act;
-      const unsigned m = __ballot_sync(0xffffffffu, act);
-      if (act) s_act[wid][nact + __popc(m & lanemask_lt())] = lane + 32 * k;
-      nact += __popc(m);
-    }
-    __syncwarp();
+    for (int k = 0; k < CPL; ++k) pend[k] = pend[k] && !(!BINNED || bin[k] == b);
     const int64_t off = BINNED ? A.bin_offsets[b] : 0;
     const int64_t cnt = BINNED ? A.bin_counts[b] : A.n_faces;
     if (cnt == 0) continue;
+    int nact = -1;
+    unsigned magic = 0;
     const int64_t g0 = off >> 5, g1 = (off + cnt - 1) >> 5;
     for (int64_t gb = g0; gb <= g1 && !hit; gb += 32) {
       const int64_t g = gb + lane;
       bool cok = false;
       if (g <= g1) cok = box_ok<D>(blo, bhi, A.cbox[2 * g], A.cbox[2 * g + 1], reach2);
       unsigned cm = __ballot_sync(0xffffffffu, cok);
-      while (cm && !hit) {
-        const int64_t gc = gb + __ffs(cm) - 1;
-        cm &= cm - 1;
-        const int64_t e = gc * 32 + lane;
-        int f = 0;
-        bool fok = false;
-        if (e >= off && e < off + cnt) {
-          f = BINNED ? A.bin_ids[e] : (int)e;
-          fok = box_ok<D>(blo, bhi, A.box[2 * (int64_t)f], A.box[2 * (int64_t)f + 1], reach2);
-        }
-        const unsigned fm = __ballot_sync(0xffffffffu, fok);
-        if (!fm) continue;
-        const int nf = __popc(fm);
-        if (fok) {
-          const int r = __popc(fm & lanemask_lt());
-          s_cand[wid][r] = f;
-          s_sph[wid][r] = A.sph[f];
-        }
-        __syncwarp();
-        const int total = nf * nact;
-        for (int k0 = 0; k0 < total; k0 += 32) {
-          const int k = k0 + lane;
-          bool h = false;
-          if (k < total) {
-            const int fi = k / nact;
-            const int ci = s_act[wid][k - fi * nact];
-            float p[3];
+      if (cm && inline_left) {
+        inline_left = false;
+        int64_t gc[CG];
 #pragma unroll
-            for (int a = 0; a < D; ++a) p[a] = s_p[wid][ci][a];
-            if (sphere_ok<D>(p, s_sph[wid][fi])) {
-              ++evaluated;
-              h = near_face<D>(A.pay + (int64_t)s_cand[wid][fi] * PW, p, r2);
-            }
-          }
-          if (__any_sync(0xffffffffu, h)) {
-            hit = true;
-            break;
+        for (int j = 0; j < CG; ++j) {
+          gc[j] = -1;
+          if (cm) {
+            gc[j] = gb + __ffs(cm) - 1;
+            cm &= cm - 1;
           }
         }
-        __syncwarp();
+        if (nact < 0) {
+          nact = stage_cells<D, BINNED>(S, wid, lane, p, bin, b);
+          magic = div_magic(nact);
+        }
+        hit = sweep_chunks<D, BINNED>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, nact, magic, evaluated);
+        if (hit) break;
+      }
+      if (cm) {  // the rest: (block, chunk, bin) items for the flat pass
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(M.n_items, (unsigned long long)__popc(cm));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if ((cm >> lane) & 1u) {
+          const unsigned long long k = base + __popc(cm & lanemask_lt());
+          if ((int64_t)k < M.cap) M.items[k] = make_int4((int)pos, (int)(gb + lane), b, 0);
+        }
       }
     }
   }
   for (int o = 16; o > 0; o >>= 1) evaluated += __shfl_xor_sync(0xffffffffu, evaluated, o);
   if (lane == 0) {
     if (evaluated) atomicAdd(&A.out[2], evaluated);
-    if (hit) {
-      F.marks[id] = OW_MARKED;
+    if (hit && atomicOr(&M.hit[pos], 1u) == 0u) {
+      A.F.marks[id] = OW_MARKED;
       atomicAdd(&A.out[0], 1ull);
     }
+  }
+}
+
+template <int D, bool BINNED>
+__global__ void __launch_bounds__(MARK_THREADS) k_mark_items(MarkArgs A, MarkItems M) {
+  constexpr int CPL = D == 3 ? 2 : 1;
+  __shared__ MarkSmem<D> S;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t n = (int64_t)*M.n_items;
+  if (n > M.cap) return;  // overflowed: the host re-runs the pass with a larger list
+  const double reach2 = DMUL(A.reach, A.reach);
+  const float r2 = FMUL(A.d, A.d);
+  unsigned long long evaluated = 0, marked = 0;
+  for (int64_t it = (int64_t)blockIdx.x * MARK_WARPS + wid; it < n; it += (int64_t)gridDim.x * MARK_WARPS) {
+    const int4 item = M.items[it];
+    const int pos = item.x;
+    if (*(volatile unsigned*)&M.hit[pos]) continue;  // block already marked
+    const int id = A.leaves[pos];
+    const int b = item.z;
+    double blo[3], bhi[3];
+    float p[CPL][3];
+    int bin[CPL];
+    block_cells<D, BINNED>(A, id, lane, blo, bhi, p, bin);
+    const int nact = stage_cells<D, BINNED>(S, wid, lane, p, bin, b);
+    const int64_t off = BINNED ? A.bin_offsets[b] : 0;
+    const int64_t cnt = BINNED ? A.bin_counts[b] : A.n_faces;
+    int64_t gc[CG];
+#pragma unroll
+    for (int j = 0; j < CG; ++j) gc[j] = j == 0 ? (int64_t)item.y : -1;
+    const bool hit =
+        sweep_chunks<D, BINNED>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, nact, div_magic(nact), evaluated);
+    if (hit && lane == 0 && atomicOr(&M.hit[pos], 1u) == 0u) {
+      A.F.marks[id] = OW_MARKED;
+      ++marked;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) evaluated += __shfl_xor_sync(0xffffffffu, evaluated, o);
+  if (lane == 0) {
+    if (evaluated) atomicAdd(&A.out[2], evaluated);
+    if (marked) atomicAdd(&A.out[0], marked);
   }
 }
 
@@ -469,7 +599,11 @@ extern "C" int ow_mark_near_wall(ow_ctx* ctx, ow_forest* f, const int32_t* d_lea
   OW_TRY(prepare_faces(ctx, f->dim, d_coords, n_faces, geom_key, d_spec, reach, s));
   OW_PROF_END(ctx, PROF_PREP, s);
   unsigned long long* out = (unsigned long long*)(ctx->d_small + 16);
-  OW_CUDA(cudaMemsetAsync(out, 0, 3 * 8, s));
+  // a re-run after an item-list overflow keeps the blocks (and the count)
+  // marked by the first attempt: they are skipped as already MARKED
+  const bool rerun = ctx->mark_rerun;
+  ctx->mark_rerun = false;
+  OW_CUDA(cudaMemsetAsync(rerun ? out + 1 : out, 0, (rerun ? 2 : 3) * 8, s));
   if (n_leaves > 0) {
     MarkArgs A;
     A.F = make_forestc(f);
@@ -486,29 +620,63 @@ extern "C" int ow_mark_near_wall(ow_ctx* ctx, ow_forest* f, const int32_t* d_lea
     A.reach = reach;
     A.out = out;
     const int64_t n_entries = binned ? n_bin_entries : n_faces;
-    void* pc;
+    void *pc, *pi, *ph;
     OW_TRY(ow_slot(ctx, SLOT_MARK_CBOX, 32 * (size_t)((n_entries + 31) / 32 + 1), s, &pc));
+    // (block, chunk) items: 16 per leaf by default (grown and re-run on overflow)
+    const int64_t cap0 = 16 * n_leaves + 256;
+    const int64_t cap = ctx->mark_item_cap > cap0 ? ctx->mark_item_cap : cap0;
+    OW_TRY(ow_slot(ctx, SLOT_MARK_ITEMS, 16 * (size_t)cap, s, &pi));
+    OW_TRY(ow_slot(ctx, SLOT_MARK_HIT, 4 * (size_t)n_leaves, s, &ph));
     A.cbox = (const float4*)pc;
     A.n_leaves = n_leaves;
+    MarkItems M;
+    M.items = (int4*)pi;
+    M.n_items = (unsigned long long*)(ctx->d_small + 19);
+    M.cap = cap;
+    M.hit = (unsigned*)ph;
+    if (!rerun) OW_CUDA(cudaMemsetAsync(ph, 0, 4 * (size_t)n_leaves, s));
+    OW_CUDA(cudaMemsetAsync(M.n_items, 0, 8, s));
     OW_PROF_BEGIN(ctx, PROF_MARK, s);
     const int cg = ow_blocks((n_entries + 31) / 32, 128);
-    if (f->dim == 3) k_chunk_boxes<3><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
-    else k_chunk_boxes<2><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
-    OW_LAUNCHED(ctx);
-    dim3 grd((unsigned)((n_leaves + MARK_WARPS - 1) / MARK_WARPS));
-    if (f->dim == 3) {
-      if (binned) k_mark<3, true><<<grd, MARK_THREADS, 0, s>>>(A);
-      else k_mark<3, false><<<grd, MARK_THREADS, 0, s>>>(A);
-    } else {
-      if (binned) k_mark<2, true><<<grd, MARK_THREADS, 0, s>>>(A);
-      else k_mark<2, false><<<grd, MARK_THREADS, 0, s>>>(A);
+    if (!rerun) {
+      if (f->dim == 3) k_chunk_boxes<3><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
+      else k_chunk_boxes<2><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
+      OW_LAUNCHED(ctx);
     }
+    dim3 grd((unsigned)((n_leaves + MARK_WARPS - 1) / MARK_WARPS));
+    const int gi = 8 * OW_SMS;
+    if (f->dim == 3) {
+      if (binned) {
+        k_mark_blocks<3, true><<<grd, MARK_THREADS, 0, s>>>(A, M);
+        k_mark_items<3, true><<<gi, MARK_THREADS, 0, s>>>(A, M);
+      } else {
+        k_mark_blocks<3, false><<<grd, MARK_THREADS, 0, s>>>(A, M);
+        k_mark_items<3, false><<<gi, MARK_THREADS, 0, s>>>(A, M);
+      }
+    } else {
+      if (binned) {
+        k_mark_blocks<2, true><<<grd, MARK_THREADS, 0, s>>>(A, M);
+        k_mark_items<2, true><<<gi, MARK_THREADS, 0, s>>>(A, M);
+      } else {
+        k_mark_blocks<2, false><<<grd, MARK_THREADS, 0, s>>>(A, M);
+        k_mark_items<2, false><<<gi, MARK_THREADS, 0, s>>>(A, M);
+      }
+    }
+    ctx->launches += 2;
     OW_PROF_END(ctx, PROF_MARK, s);
     OW_LAUNCHED(ctx);
     OW_CHECK_LAUNCH();
   }
-  int64_t h[3];
-  OW_TRY(ow_readback(ctx, ctx->d_small + 16, 3, h, s));
+  int64_t h[4];
+  OW_TRY(ow_readback(ctx, ctx->d_small + 16, 4, h, s));
+  if (n_leaves > 0 && h[3] > ctx->mark_item_cap && h[3] > 16 * n_leaves + 256) {
+    // item list overflowed (the item pass did nothing): grow and run again
+    ctx->mark_item_cap = h[3] + h[3] / 4;
+    ctx->mark_rerun = true;
+    return ow_mark_near_wall(ctx, f, d_leaves, n_leaves, d_coords, n_faces, geom_key, grid, d_bin_ids,
+                             d_bin_counts, d_bin_offsets, n_bin_entries, d_spec, reach, out_marked, out_tests,
+                             out_evaluated, stream);
+  }
   *out_marked = h[0];
   *out_tests = h[1];
   *out_evaluated = h[2];

@@ -412,3 +412,30 @@ def test_sharded_native_driver_matches_single_rank(ow):
         np.testing.assert_array_equal(co, f._coords)
         np.testing.assert_array_equal(fc, f._first_child)
         assert md == ref.marked_detected and t == ref.cell_face_tests
+
+
+def test_marking_dense_soup_single_root(ow):
+    """One root block next to 12 000 faces: hundreds of bin chunks survive the
+    union-box cull per block (grouped chunk rounds); the forest equals the
+    oracle's for binned and naive marking."""
+    from oracle import forest as of
+    from oracle import nearwall as on
+
+    rng = np.random.default_rng(11)
+    n = 12000
+    anchors = rng.uniform(0.3, 0.7, (n, 3))
+    coords = np.zeros((3, 3, n), np.float32)
+    for j in range(3):
+        coords[j] = (anchors + (rng.uniform(-0.01, 0.01, (n, 3)) if j else 0.0)).T.astype(np.float32)
+    from oracle.geometry import first_degenerate
+
+    while first_degenerate(coords) >= 0:
+        coords[:, :, first_degenerate(coords)] += np.float32(1e-3)
+    for strategy, B in (("binned", 2), ("naive", 1)):
+        fo = of.Forest(np.zeros(3), np.ones(3), (1, 1, 1))
+        ro = on.refine_near_wall(fo, coords, 0.05, n_levels=3, bins_per_axis=B, strategy=strategy)
+        fg = ow.init_root_grid(domain(ow, 3), (1, 1, 1))
+        rg = ow.refine_near_wall(fg, ow.CoordListGeometry(3, coords),
+                                 ow.NearWallParams(d_spec=0.05, n_levels=3, bins_per_axis=B, strategy=strategy))
+        assert rg.marked_detected == ro["marked_detected"]
+        np.testing.assert_array_equal(fg._coords, fo.coords)
