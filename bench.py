@@ -146,17 +146,20 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         rec_host = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).pin_memory()
         rec_dev = rec_host.to(dev)
 
-    def import_geom(records):
-        if text:
-            return ow.index_to_coords(ig)
-        return ow.geometry.stl_records_to_coords(records, n_faces)
+    from paper_2502_16310_b200 import pipeline
+
+    plan = pipeline.GridPlan(dom, (cfg["root"],) * dim, params, cfg["lattice"]) if not text else None
 
     def step(records):
-        geom = import_geom(records)
-        forest = ow.init_root_grid(dom, (cfg["root"],) * dim, capacity=32 * cfg["root"] ** dim)
-        res = ow.refine_near_wall(forest, geom, params, shard=shard)
-        ll = ow.build_lattice_links(forest, geom, None, cfg["lattice"])
-        return res, forest, ll
+        if text or shard is not None:  # per-function path (reference call sequence, cli.py:87-113)
+            geom = ow.index_to_coords(ig) if text else ow.geometry.stl_records_to_coords(records, n_faces)
+            forest = ow.init_root_grid(dom, (cfg["root"],) * dim, capacity=32 * cfg["root"] ** dim)
+            res = ow.refine_near_wall(forest, geom, params, shard=shard)
+            ll = ow.build_lattice_links(forest, geom, None, cfg["lattice"])
+            return res, forest, ll
+        # fused native pass: STL records in HBM -> grid -> lattice links (ow_geometry_to_grid)
+        gp = plan.run(records, n_faces)
+        return gp.result, gp.forest, gp.links
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 

@@ -214,6 +214,39 @@ int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_
                         int64_t bin_ids_capacity, int32_t* d_bin_counts, int32_t* d_bin_offsets,
                         ow_nearwall_result* out, void* stream);
 
+/* ---- one native geometry-to-grid pass -------------------------------------- */
+/* Output allocator: return 0 and set *out to `bytes` of device memory owned by
+ * the caller (kept alive by it), for output `what`. */
+typedef int (*ow_alloc_fn)(void* user, int32_t what, int64_t bytes, void** out);
+enum { OW_OUT_LEAVES = 0, OW_OUT_FLAGS = 1, OW_OUT_CELLS = 2, OW_OUT_Q = 3 };
+typedef struct {
+  ow_nearwall_params nw;    /* reach <= 0: derived as nearwall.py:31-40 */
+  int32_t lattice_q;        /* directions of the lattice (0: no lattice links) */
+  int8_t lattice_dirs[27 * 3];
+  ow_alloc_fn alloc;
+  void* alloc_user;
+  void* out_buf[4];         /* optional caller buffers per OW_OUT_*: used when */
+  int64_t out_cap[4];       /* out_cap (bytes) covers the need, else alloc() */
+} ow_g2g_params;
+typedef struct {
+  ow_face_summary faces;
+  int32_t outside_domain;   /* 1: the bounding box left the forest domain */
+  int32_t finest_level;
+  ow_nearwall_result nw;
+  int64_t n_finest_leaves;
+  int64_t n_boundary;
+  int64_t lattice_stats[3];
+} ow_g2g_result;
+/* Binary STL records (or, with d_records NULL, coords already in d_coords) ->
+ * validated SoA geometry -> root grid in `f` (capacity preallocated, grown
+ * through f->grow) -> refine_near_wall -> finest-level leaves (int64), lattice
+ * flags, boundary cells and q through `alloc`.  Errors carry the reference's
+ * messages (degenerate face, outside domain, bin capacity). */
+int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces, int64_t geom_key,
+                        ow_forest* f, const ow_grid* grid, const ow_g2g_params* params, int32_t* d_bin_ids,
+                        int64_t bin_ids_capacity, int32_t* d_bin_counts, int32_t* d_bin_offsets,
+                        ow_g2g_result* out, void* stream);
+
 /* Cell-face links (build_cell_face_links, nearwall.py:522-594), two phases.
  * Count: per leaf cell the faces of its bin within d_link.  On overflow of
  * `capacity` returns OW_ERR_CAPACITY with the reference's message naming the

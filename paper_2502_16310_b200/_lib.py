@@ -111,6 +111,33 @@ class NearWallResultC(C.Structure):  # ow_nearwall_result
     ]
 
 
+ALLOC_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_int64, C.POINTER(C.c_void_p))
+
+
+class G2GParamsC(C.Structure):  # ow_g2g_params
+    _fields_ = [
+        ("nw", NearWallParamsC),
+        ("lattice_q", C.c_int32),
+        ("lattice_dirs", C.c_int8 * 81),
+        ("alloc", ALLOC_FN),
+        ("alloc_user", C.c_void_p),
+        ("out_buf", C.c_void_p * 4),
+        ("out_cap", C.c_int64 * 4),
+    ]
+
+
+class G2GResultC(C.Structure):  # ow_g2g_result
+    _fields_ = [
+        ("faces", FaceSummary),
+        ("outside_domain", C.c_int32),
+        ("finest_level", C.c_int32),
+        ("nw", NearWallResultC),
+        ("n_finest_leaves", C.c_int64),
+        ("n_boundary", C.c_int64),
+        ("lattice_stats", C.c_int64 * 3),
+    ]
+
+
 P = C.c_void_p
 I32, I64, F32, F64 = C.c_int32, C.c_int64, C.c_float, C.c_double
 PI64 = C.POINTER(C.c_int64)
@@ -138,6 +165,8 @@ _SIGS = {
                           PI64, PI64, PI64, P],
     "ow_propagate_marks": [P, C.POINTER(ForestView), P, I64, I32, P],
     "ow_forest_init_root": [P, C.POINTER(ForestView), P],
+    "ow_geometry_to_grid": [P, P, P, I64, I64, C.POINTER(ForestView), C.POINTER(Grid), C.POINTER(G2GParamsC), P, I64,
+                            P, P, C.POINTER(G2GResultC), P],
     "ow_refine_near_wall": [P, C.POINTER(ForestView), P, I64, I64, C.POINTER(Grid), C.POINTER(NearWallParamsC), P,
                             I64, P, P, C.POINTER(NearWallResultC), P],
     "ow_cell_face_links_count": [P, C.POINTER(ForestView), P, I64, P, I64, I64, C.POINTER(Grid), P, P, P, F32, F64,

@@ -9,6 +9,7 @@
 #include "../../include/owb200.h"
 
 #define OW_SMS 148  // B200 SM count: persistent grids are sized in multiples of it
+#define OW_PINNED_WORDS 256
 
 // ---------------------------------------------------------------------------
 // errors
@@ -76,6 +77,7 @@ enum ow_slot {
   SLOT_MARK_ITEMS,     // (block, chunk, bin) marking items
   SLOT_MARK_HIT,       // per-leaf hit words of a marking pass
   SLOT_DRV_LEAVES,     // native driver: leaves of the current level
+  SLOT_DRV_STATS,      // native driver: per-pass marking statistics
   SLOT_MISC,
   SLOT_COUNT
 };
@@ -95,7 +97,7 @@ struct ow_ctx {
   ow_prof* prof;
   void* slot_ptr[SLOT_COUNT];
   size_t slot_bytes[SLOT_COUNT];
-  int64_t* h_pinned;  // 64 int64 of pinned host memory for readbacks
+  int64_t* h_pinned;  // OW_PINNED_WORDS int64 of pinned host memory for readbacks
   int64_t* d_small;   // 64 int64 of device scalars (counters, flags)
   int64_t launches;
   // face prep cache key
@@ -129,9 +131,13 @@ struct ow_ctx {
   uint32_t* lat_flags;
   ow_forest lat_forest;
   void* stage_events;  // native driver CUDA events
-  int64_t mark_item_cap;
-  bool mark_rerun;
 };
+
+// one marking pass without a host round trip: stats accumulate in d_out[0..2]
+int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves, const float* d_coords,
+                   int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int32_t* d_bin_ids,
+                   const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,
+                   double reach, unsigned long long* d_out, cudaStream_t s);
 
 // refine_marked returning the MARKED-leaf count of the split pass as well
 int ow_refine_marked_counted(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, int64_t* out_marked,

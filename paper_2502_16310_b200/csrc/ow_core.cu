@@ -32,7 +32,7 @@ extern "C" int ow_ctx_create(int device, ow_ctx** out) {
   }
   c->device = device;
   c->prep_key = -1;
-  cudaError_t e = cudaMallocHost((void**)&c->h_pinned, 64 * sizeof(int64_t));
+  cudaError_t e = cudaMallocHost((void**)&c->h_pinned, OW_PINNED_WORDS * sizeof(int64_t));
   if (e == cudaSuccess) e = cudaMalloc((void**)&c->d_small, 64 * sizeof(int64_t));
   if (e != cudaSuccess) {
     ow_set_error("ow_ctx_create: %s", cudaGetErrorString(e));

@@ -44,6 +44,7 @@ struct LatArgs {
   int nq, level;
   float h[3];               // finest cell size per axis (float32 of the FP64 value)
   float dv[QMAX][3];        // link vectors c_d * h (exact)
+  int8_t dc[QMAX][3];       // lattice directions c_d
   const float* coords;
   int64_t n_faces;
   const int32_t* leaves;
@@ -97,9 +98,11 @@ __global__ void k_lat_pos(ForestC F, int level, const int32_t* __restrict__ leav
 // Per-axis cell ranges of one (block, face) pair: for c in {-1,0,+1} the
 // contiguous set of cell indices i whose link box [min(x_i, e_i), max(x_i, e_i)],
 // e_i = fl(x_i + c h), meets [lo, hi] — the per-cell test of oracle/lattice.py
-// on the same float32 centres.  4 bits (i0 | (ext-1) << 2), 0xF0 when empty.
-__device__ __forceinline__ void axis_ranges(const float4 x4, float h, float lo, float hi, unsigned* r3) {
+// on the same float32 centres.  Packed in one register: bits [4 ci, 4 ci + 4)
+// hold i0 | (ext-1) << 2 of c = ci - 1, bit 12 + ci marks an empty range.
+__device__ __forceinline__ unsigned axis_ranges(const float4 x4, float h, float lo, float hi) {
   const float x[4] = {x4.x, x4.y, x4.z, x4.w};
+  unsigned r = 0;
 #pragma unroll
   for (int ci = 0; ci < 3; ++ci) {
     const float dv = FMUL((float)(ci - 1), h);
@@ -109,8 +112,26 @@ __device__ __forceinline__ void axis_ranges(const float4 x4, float h, float lo, 
       const float en = FADD(x[i], dv);
       m |= (unsigned)(lo <= fmaxf(x[i], en) && hi >= fminf(x[i], en)) << i;
     }
-    r3[ci] = m == 0 ? 0xF0u : (unsigned)(__ffs(m) - 1) | ((unsigned)(__popc(m) - 1) << 2);  // contiguous
+    r |= m == 0 ? (1u << (12 + ci)) : (((unsigned)(__ffs(m) - 1) | ((unsigned)(__popc(m) - 1) << 2)) << (4 * ci));
   }
+  return r;  // contiguous by monotonicity
+}
+
+// row word of direction d from the packed axis ranges (0 when some axis is empty)
+template <int D>
+__device__ __forceinline__ unsigned row_word(const unsigned* R, const int8_t* c, int d, int* units) {
+  unsigned w = (unsigned)d;
+  int u = 1;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const int ci = c[a] + 1;
+    if ((R[a] >> (12 + ci)) & 1u) return 0u;
+    const unsigned ra = (R[a] >> (4 * ci)) & 0xFu;
+    w |= ra << (5 + 4 * a);
+    u *= (int)(ra >> 2) + 1;
+  }
+  *units = u;
+  return w;
 }
 
 // Warp per face: lane 0 packs the face record; lanes test the directions'
@@ -185,7 +206,7 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   for (int64_t s0 = 0; s0 < nslots; s0 += 32) {
     const int64_t slot = s0 + lane;
     int nrow = 0, nunit = 0, pos = 0;
-    unsigned r[3][3];
+    unsigned R[3] = {0u, 0u, 0u};
     if (slot < nslots) {
       int32_t nc[3] = {0, 0, 0};
       int64_t rem = slot;
@@ -200,19 +221,11 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
         pos = A.pos_of[node];
 #pragma unroll
         for (int a = 0; a < D; ++a)
-          axis_ranges(reinterpret_cast<const float4*>(A.cen)[(int64_t)pos * D + a], A.h[a], lo[a], hi[a], r[a]);
+          R[a] = axis_ranges(reinterpret_cast<const float4*>(A.cen)[(int64_t)pos * D + a], A.h[a], lo[a], hi[a]);
         for (int d = 1; d < A.nq; ++d) {
           if (!((detmask >> d) & 1u)) continue;
-          int units = 1;
-          bool ok = true;
-#pragma unroll
-          for (int a = 0; a < D; ++a) {
-            const float c = A.dv[d][a];
-            const unsigned ra = r[a][c < 0.0f ? 0 : (c > 0.0f ? 2 : 1)];
-            ok = ok && ra != 0xF0u;
-            units *= (int)((ra >> 2) & 3u) + 1;
-          }
-          if (!ok) continue;
+          int units;
+          if (!row_word<D>(R, A.dc[d], d, &units)) continue;
           ++nrow;
           nunit += units;
         }
@@ -230,18 +243,9 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
       if (nrow) {
         for (int d = 1; d < A.nq; ++d) {
           if (!((detmask >> d) & 1u)) continue;
-          unsigned w = (unsigned)d;
-          int units = 1;
-          bool ok = true;
-#pragma unroll
-          for (int a = 0; a < D; ++a) {
-            const float c = A.dv[d][a];
-            const unsigned ra = r[a][c < 0.0f ? 0 : (c > 0.0f ? 2 : 1)];
-            ok = ok && ra != 0xF0u;
-            w |= (ra & 0xFu) << (5 + 4 * a);
-            units *= (int)((ra >> 2) & 3u) + 1;
-          }
-          if (!ok) continue;
+          int units;
+          const unsigned w = row_word<D>(R, A.dc[d], d, &units);
+          if (!w) continue;
           A.rows[k] = make_int4(pos, (int)f, (int)w, units);
           A.rowoff[k] = units;
           ++k;
@@ -517,7 +521,10 @@ LatArgs make_args(ow_ctx* ctx) {
     A.h[a] = a < f->dim ? (float)(f->dext[a] / (double)((int64_t)f->root[a] << A.level) / 4.0) : 0.0f;
   }
   for (int i = 0; i < A.nq; ++i)
-    for (int a = 0; a < 3; ++a) A.dv[i][a] = (float)ctx->lat_dir[i * 3 + a] * A.h[a];  // exact
+    for (int a = 0; a < 3; ++a) {
+      A.dc[i][a] = ctx->lat_dir[i * 3 + a];
+      A.dv[i][a] = (float)ctx->lat_dir[i * 3 + a] * A.h[a];  // exact
+    }
   A.coords = ctx->lat_coords;
   A.n_faces = ctx->lat_faces;
   A.leaves = ctx->lat_leaves_ptr;

@@ -368,9 +368,27 @@ __global__ void __launch_bounds__(MARK_THREADS) k_mark_blocks(MarkArgs A, MarkIt
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(M.n_items, (unsigned long long)__popc(cm));
         base = __shfl_sync(0xffffffffu, base, 0);
-        if ((cm >> lane) & 1u) {
-          const unsigned long long k = base + __popc(cm & lanemask_lt());
-          if ((int64_t)k < M.cap) M.items[k] = make_int4((int)pos, (int)(gb + lane), b, 0);
+        if ((int64_t)(base + __popc(cm)) <= M.cap) {
+          if ((cm >> lane) & 1u) M.items[base + __popc(cm & lanemask_lt())] = make_int4((int)pos, (int)(gb + lane), b, 0);
+        } else {
+          // item list full: this warp sweeps its remaining chunks itself
+          if (nact < 0) {
+            nact = stage_cells<D, BINNED>(S, wid, lane, p, bin, b);
+            magic = div_magic(nact);
+          }
+          while (cm && !hit) {
+            int64_t gc[CG];
+#pragma unroll
+            for (int j = 0; j < CG; ++j) {
+              gc[j] = -1;
+              if (cm) {
+                gc[j] = gb + __ffs(cm) - 1;
+                cm &= cm - 1;
+              }
+            }
+            hit = sweep_chunks<D, BINNED>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, nact, magic,
+                                          evaluated);
+          }
         }
       }
     }
@@ -390,8 +408,7 @@ __global__ void __launch_bounds__(MARK_THREADS) k_mark_items(MarkArgs A, MarkIte
   constexpr int CPL = D == 3 ? 2 : 1;
   __shared__ MarkSmem<D> S;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t n = (int64_t)*M.n_items;
-  if (n > M.cap) return;  // overflowed: the host re-runs the pass with a larger list
+  const int64_t n = min((int64_t)*M.n_items, M.cap);  // items past cap were swept by their block warp
   const double reach2 = DMUL(A.reach, A.reach);
   const float r2 = FMUL(A.d, A.d);
   unsigned long long evaluated = 0, marked = 0;
@@ -575,13 +592,13 @@ __global__ void k_near_pairs(int dim, const float* __restrict__ pts, const float
 
 }  // namespace
 
-extern "C" int ow_mark_near_wall(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
-                                 const float* d_coords, int64_t n_faces, int64_t geom_key, const ow_grid* grid,
-                                 const int32_t* d_bin_ids, const int32_t* d_bin_counts, const int32_t* d_bin_offsets,
-                                 int64_t n_bin_entries, float d_spec, double reach, int64_t* out_marked,
-                                 int64_t* out_tests,
-                                 int64_t* out_evaluated, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
+// Launch one marking pass; statistics accumulate into d_out[0..2] (marked,
+// tests, evaluated) on the device (no host round trip: the native driver reads
+// them once at the end).
+int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves, const float* d_coords,
+                   int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int32_t* d_bin_ids,
+                   const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,
+                   double reach, unsigned long long* out, cudaStream_t s) {
   if (!(d_spec > 0.0f)) {
     ow_set_error("near-wall distance must be positive, got %g", (double)d_spec);
     return OW_ERR_INVALID;
@@ -598,85 +615,78 @@ extern "C" int ow_mark_near_wall(ow_ctx* ctx, ow_forest* f, const int32_t* d_lea
   OW_PROF_BEGIN(ctx, PROF_PREP, s);
   OW_TRY(prepare_faces(ctx, f->dim, d_coords, n_faces, geom_key, d_spec, reach, s));
   OW_PROF_END(ctx, PROF_PREP, s);
-  unsigned long long* out = (unsigned long long*)(ctx->d_small + 16);
-  // a re-run after an item-list overflow keeps the blocks (and the count)
-  // marked by the first attempt: they are skipped as already MARKED
-  const bool rerun = ctx->mark_rerun;
-  ctx->mark_rerun = false;
-  OW_CUDA(cudaMemsetAsync(rerun ? out + 1 : out, 0, (rerun ? 2 : 3) * 8, s));
-  if (n_leaves > 0) {
-    MarkArgs A;
-    A.F = make_forestc(f);
-    if (binned) A.g = make_gridc(grid);
-    A.leaves = d_leaves;
-    A.box = (const float4*)ctx->slot_ptr[SLOT_FACE_BOX];
-    A.sph = (const float4*)ctx->slot_ptr[SLOT_FACE_SPHERE];
-    A.pay = (const float4*)ctx->slot_ptr[SLOT_FACE_PREP];
-    A.bin_ids = d_bin_ids;
-    A.bin_counts = d_bin_counts;
-    A.bin_offsets = d_bin_offsets;
-    A.n_faces = n_faces;
-    A.d = d_spec;
-    A.reach = reach;
-    A.out = out;
-    const int64_t n_entries = binned ? n_bin_entries : n_faces;
-    void *pc, *pi, *ph;
-    OW_TRY(ow_slot(ctx, SLOT_MARK_CBOX, 32 * (size_t)((n_entries + 31) / 32 + 1), s, &pc));
-    // (block, chunk) items: 16 per leaf by default (grown and re-run on overflow)
-    const int64_t cap0 = 16 * n_leaves + 256;
-    const int64_t cap = ctx->mark_item_cap > cap0 ? ctx->mark_item_cap : cap0;
-    OW_TRY(ow_slot(ctx, SLOT_MARK_ITEMS, 16 * (size_t)cap, s, &pi));
-    OW_TRY(ow_slot(ctx, SLOT_MARK_HIT, 4 * (size_t)n_leaves, s, &ph));
-    A.cbox = (const float4*)pc;
-    A.n_leaves = n_leaves;
-    MarkItems M;
-    M.items = (int4*)pi;
-    M.n_items = (unsigned long long*)(ctx->d_small + 19);
-    M.cap = cap;
-    M.hit = (unsigned*)ph;
-    if (!rerun) OW_CUDA(cudaMemsetAsync(ph, 0, 4 * (size_t)n_leaves, s));
-    OW_CUDA(cudaMemsetAsync(M.n_items, 0, 8, s));
-    OW_PROF_BEGIN(ctx, PROF_MARK, s);
-    const int cg = ow_blocks((n_entries + 31) / 32, 128);
-    if (!rerun) {
-      if (f->dim == 3) k_chunk_boxes<3><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
-      else k_chunk_boxes<2><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
-      OW_LAUNCHED(ctx);
-    }
-    dim3 grd((unsigned)((n_leaves + MARK_WARPS - 1) / MARK_WARPS));
-    const int gi = 8 * OW_SMS;
-    if (f->dim == 3) {
-      if (binned) {
-        k_mark_blocks<3, true><<<grd, MARK_THREADS, 0, s>>>(A, M);
-        k_mark_items<3, true><<<gi, MARK_THREADS, 0, s>>>(A, M);
-      } else {
-        k_mark_blocks<3, false><<<grd, MARK_THREADS, 0, s>>>(A, M);
-        k_mark_items<3, false><<<gi, MARK_THREADS, 0, s>>>(A, M);
-      }
+  if (n_leaves <= 0) return OW_OK;
+  MarkArgs A;
+  A.F = make_forestc(f);
+  if (binned) A.g = make_gridc(grid);
+  A.leaves = d_leaves;
+  A.box = (const float4*)ctx->slot_ptr[SLOT_FACE_BOX];
+  A.sph = (const float4*)ctx->slot_ptr[SLOT_FACE_SPHERE];
+  A.pay = (const float4*)ctx->slot_ptr[SLOT_FACE_PREP];
+  A.bin_ids = d_bin_ids;
+  A.bin_counts = d_bin_counts;
+  A.bin_offsets = d_bin_offsets;
+  A.n_faces = n_faces;
+  A.d = d_spec;
+  A.reach = reach;
+  A.out = out;
+  const int64_t n_entries = binned ? n_bin_entries : n_faces;
+  void *pc, *pi, *ph;
+  OW_TRY(ow_slot(ctx, SLOT_MARK_CBOX, 32 * (size_t)((n_entries + 31) / 32 + 1), s, &pc));
+  // (block, chunk) items: 16 per leaf; a block warp that finds the list full
+  // sweeps its remaining chunks itself
+  const int64_t cap = 16 * n_leaves + 256;
+  OW_TRY(ow_slot(ctx, SLOT_MARK_ITEMS, 16 * (size_t)cap, s, &pi));
+  OW_TRY(ow_slot(ctx, SLOT_MARK_HIT, 4 * (size_t)n_leaves + 8, s, &ph));
+  A.cbox = (const float4*)pc;
+  A.n_leaves = n_leaves;
+  MarkItems M;
+  M.items = (int4*)pi;
+  M.n_items = (unsigned long long*)((unsigned*)ph + n_leaves + (n_leaves & 1));  // after the hit words
+  M.cap = cap;
+  M.hit = (unsigned*)ph;
+  OW_CUDA(cudaMemsetAsync(ph, 0, 4 * (size_t)(n_leaves + (n_leaves & 1)) + 8, s));
+  OW_PROF_BEGIN(ctx, PROF_MARK, s);
+  const int cg = ow_blocks((n_entries + 31) / 32, 128);
+  if (f->dim == 3) k_chunk_boxes<3><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
+  else k_chunk_boxes<2><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
+  dim3 grd((unsigned)((n_leaves + MARK_WARPS - 1) / MARK_WARPS));
+  const int gi = 8 * OW_SMS;
+  if (f->dim == 3) {
+    if (binned) {
+      k_mark_blocks<3, true><<<grd, MARK_THREADS, 0, s>>>(A, M);
+      k_mark_items<3, true><<<gi, MARK_THREADS, 0, s>>>(A, M);
     } else {
-      if (binned) {
-        k_mark_blocks<2, true><<<grd, MARK_THREADS, 0, s>>>(A, M);
-        k_mark_items<2, true><<<gi, MARK_THREADS, 0, s>>>(A, M);
-      } else {
-        k_mark_blocks<2, false><<<grd, MARK_THREADS, 0, s>>>(A, M);
-        k_mark_items<2, false><<<gi, MARK_THREADS, 0, s>>>(A, M);
-      }
+      k_mark_blocks<3, false><<<grd, MARK_THREADS, 0, s>>>(A, M);
+      k_mark_items<3, false><<<gi, MARK_THREADS, 0, s>>>(A, M);
     }
-    ctx->launches += 2;
-    OW_PROF_END(ctx, PROF_MARK, s);
-    OW_LAUNCHED(ctx);
-    OW_CHECK_LAUNCH();
+  } else {
+    if (binned) {
+      k_mark_blocks<2, true><<<grd, MARK_THREADS, 0, s>>>(A, M);
+      k_mark_items<2, true><<<gi, MARK_THREADS, 0, s>>>(A, M);
+    } else {
+      k_mark_blocks<2, false><<<grd, MARK_THREADS, 0, s>>>(A, M);
+      k_mark_items<2, false><<<gi, MARK_THREADS, 0, s>>>(A, M);
+    }
   }
-  int64_t h[4];
-  OW_TRY(ow_readback(ctx, ctx->d_small + 16, 4, h, s));
-  if (n_leaves > 0 && h[3] > ctx->mark_item_cap && h[3] > 16 * n_leaves + 256) {
-    // item list overflowed (the item pass did nothing): grow and run again
-    ctx->mark_item_cap = h[3] + h[3] / 4;
-    ctx->mark_rerun = true;
-    return ow_mark_near_wall(ctx, f, d_leaves, n_leaves, d_coords, n_faces, geom_key, grid, d_bin_ids,
-                             d_bin_counts, d_bin_offsets, n_bin_entries, d_spec, reach, out_marked, out_tests,
-                             out_evaluated, stream);
-  }
+  ctx->launches += 3;
+  OW_PROF_END(ctx, PROF_MARK, s);
+  OW_CHECK_LAUNCH();
+  return OW_OK;
+}
+
+extern "C" int ow_mark_near_wall(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves,
+                                 const float* d_coords, int64_t n_faces, int64_t geom_key, const ow_grid* grid,
+                                 const int32_t* d_bin_ids, const int32_t* d_bin_counts, const int32_t* d_bin_offsets,
+                                 int64_t n_bin_entries, float d_spec, double reach, int64_t* out_marked,
+                                 int64_t* out_tests, int64_t* out_evaluated, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* out = (unsigned long long*)(ctx->d_small + 16);
+  OW_CUDA(cudaMemsetAsync(out, 0, 3 * 8, s));
+  OW_TRY(ow_mark_launch(ctx, f, d_leaves, n_leaves, d_coords, n_faces, geom_key, grid, d_bin_ids, d_bin_counts,
+                        d_bin_offsets, n_bin_entries, d_spec, reach, out, s));
+  int64_t h[3];
+  OW_TRY(ow_readback(ctx, ctx->d_small + 16, 3, h, s));
   *out_marked = h[0];
   *out_tests = h[1];
   *out_evaluated = h[2];

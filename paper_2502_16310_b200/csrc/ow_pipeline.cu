@@ -103,6 +103,9 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
   bool have_bins = false;
   int64_t E = 0;
   const int passes = p->n_levels - 1;
+  void* stats;
+  OW_TRY(ow_slot(ctx, SLOT_DRV_STATS, 24 * (size_t)passes, s, &stats));
+  OW_CUDA(cudaMemsetAsync(stats, 0, 24 * (size_t)passes, s));
   for (int level = 0; level < passes; ++level) {
     // ---- bin_setup
     OW_TRY(record(se, level, 0, s));
@@ -147,12 +150,15 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
       lo = per * p->rank < n_leaves ? per * p->rank : n_leaves;
       hi = per * (p->rank + 1) < n_leaves ? per * (p->rank + 1) : n_leaves;
     }
-    int64_t st[3] = {0, 0, 0};
-    OW_TRY(ow_mark_near_wall(ctx, f, (const int32_t*)pl + lo, hi - lo, d_coords, n_faces, geom_key,
-                             p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
-                             p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
-                             p->binned ? E : 0, p->d_spec, p->reach, &st[0], &st[1], &st[2], s));
+    // marking statistics stay on the device (per-pass slots, one readback at the end)
+    unsigned long long* dst = (unsigned long long*)stats + 3 * level;
+    OW_TRY(ow_mark_launch(ctx, f, (const int32_t*)pl + lo, hi - lo, d_coords, n_faces, geom_key,
+                          p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
+                          p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
+                          p->binned ? E : 0, p->d_spec, p->reach, dst, s));
     if (p->world > 1) {
+      int64_t st[3];
+      OW_TRY(ow_readback(ctx, (const int64_t*)dst, 3, st, s));
       if (!p->exchange) {
         ow_set_error("refine_near_wall: world > 1 needs an exchange callback");
         return OW_ERR_INVALID;
@@ -161,10 +167,9 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
         ow_set_error("refine_near_wall: mark exchange failed at level %d", level);
         return OW_ERR_INTERNAL;
       }
+      OW_CUDA(cudaMemcpyAsync(dst, st, 24, cudaMemcpyHostToDevice, s));
+      OW_CUDA(cudaStreamSynchronize(s));  // st is a host stack buffer
     }
-    out->marked_detected[level] = st[0];
-    out->tests[level] = st[1];
-    out->evaluated[level] = st[2];
     // ---- propagation (binned only): 1 + floor(d / min block length)
     OW_TRY(record(se, level, 2, s));
     if (p->binned && n_leaves > 0) {
@@ -185,6 +190,15 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
     OW_TRY(record(se, level, 4, s));
     out->n_passes = level + 1;
   }
+  if (passes > 0) {
+    int64_t h[3 * OW_MAX_PASSES];
+    OW_TRY(ow_readback(ctx, (const int64_t*)stats, 3 * passes, h, s));
+    for (int level = 0; level < out->n_passes; ++level) {
+      out->marked_detected[level] = h[3 * level];
+      out->tests[level] = h[3 * level + 1];
+      out->evaluated[level] = h[3 * level + 2];
+    }
+  }
   OW_CUDA(cudaStreamSynchronize(s));
   for (int level = 0; level < out->n_passes; ++level)
     for (int k = 0; k < 4; ++k) {
@@ -193,5 +207,102 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
         OW_CUDA(cudaEventElapsedTime(&ms, se->ev[level][k], se->ev[level][k + 1]));
       out->stage_ms[level][k] = ms;
     }
+  return OW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// One geometry-to-grid pass in one host call: import (binary STL records ->
+// SoA) -> face validation / bounding box -> root grid -> refine_near_wall ->
+// lattice links on the finest level.  Output buffers whose size is only known
+// on the device (finest leaves, flags, boundary cells, q) are requested from
+// the caller through `alloc`, so the caller's allocator (PyTorch) owns them.
+// ---------------------------------------------------------------------------
+namespace {
+int out_buffer(const ow_g2g_params* p, int what, int64_t bytes, void** out) {
+  if (p->out_buf[what] && p->out_cap[what] >= bytes) {
+    *out = p->out_buf[what];
+    return 0;
+  }
+  return p->alloc(p->alloc_user, what, bytes, out);
+}
+
+__global__ void k_widen(const int32_t* __restrict__ in, int64_t n, int64_t* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+}  // namespace
+
+extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces,
+                                   int64_t geom_key, ow_forest* f, const ow_grid* grid, const ow_g2g_params* p,
+                                   int32_t* d_bin_ids, int64_t bin_ids_capacity, int32_t* d_bin_counts,
+                                   int32_t* d_bin_offsets, ow_g2g_result* out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  memset(out, 0, sizeof(*out));
+  out->faces.first_degenerate = out->faces.first_nonfinite = -1;
+  const int D = f->dim;
+  if (n_faces <= 0) {
+    ow_set_error("cannot refine around empty geometry");
+    return OW_ERR_INVALID;
+  }
+  if (d_records) OW_TRY(ow_stl_binary_to_soa(ctx, d_records, n_faces, d_coords, stream));
+  OW_TRY(ow_face_check(ctx, D, d_coords, n_faces, &out->faces, stream));
+  if (out->faces.first_nonfinite >= 0) {
+    ow_set_error("geometry has non-finite coordinates");
+    return OW_ERR_INVALID;
+  }
+  if (out->faces.first_degenerate >= 0) {
+    ow_set_error(D == 2 ? "degenerate edge (identical endpoints) at face %lld"
+                        : "degenerate triangle (zero area) at face %lld",
+                 (long long)out->faces.first_degenerate);
+    return OW_ERR_INVALID;
+  }
+  double scale = 0.0;  // nearwall.py:31-35: max |coordinate| of domain and geometry
+  for (int a = 0; a < D; ++a) {
+    const double lo = f->dmin[a], hi = f->dmin[a] + f->dext[a], tol = 1e-6 * f->dext[a];
+    if ((double)out->faces.bbox_min[a] < lo - tol || (double)out->faces.bbox_max[a] > hi + tol) {
+      out->outside_domain = 1;
+      ow_set_error("geometry outside the forest domain");
+      return OW_ERR_INVALID;
+    }
+    scale = fmax(scale, fmax(fabs(lo), fabs(hi)));
+  }
+  scale = fmax(scale, (double)out->faces.abs_max);
+  OW_TRY(ow_forest_init_root(ctx, f, stream));
+  ow_nearwall_params nw = p->nw;
+  if (!(nw.reach > 0.0)) nw.reach = nw.d_spec64 + 1e-3 * fmax(1.0, fmax(scale, nw.d_spec64));  // nearwall.py:38-40
+  OW_TRY(ow_refine_near_wall(ctx, f, d_coords, n_faces, geom_key, grid, &nw, d_bin_ids, bin_ids_capacity,
+                             d_bin_counts, d_bin_offsets, &out->nw, stream));
+  int finest = 0;
+  for (int l = 0; l < out->nw.n_passes; ++l)
+    if (out->nw.n_split[l] > 0) finest = l + 1;
+  out->finest_level = finest;
+  if (p->lattice_q < 2 || !p->alloc) return OW_OK;
+  void* pl;
+  OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(f->n_blocks + 1), s, &pl));
+  int64_t nl = 0;
+  OW_TRY(ow_forest_leaves(ctx, f, finest, (int32_t*)pl, &nl, stream));
+  out->n_finest_leaves = nl;
+  const int C = D == 3 ? 64 : 16;
+  void *leaves64, *flags;
+  if (out_buffer(p, OW_OUT_LEAVES, 8 * nl, &leaves64) || out_buffer(p, OW_OUT_FLAGS, 4 * nl * C, &flags)) {
+    ow_set_error("geometry_to_grid: output allocation failed");
+    return OW_ERR_INTERNAL;
+  }
+  if (nl > 0) {
+    k_widen<<<ow_blocks(nl, 256), 256, 0, s>>>((const int32_t*)pl, nl, (int64_t*)leaves64);
+    OW_LAUNCHED(ctx);
+    OW_CHECK_LAUNCH();
+  }
+  int64_t nb = 0;
+  OW_TRY(ow_lattice_links_count(ctx, f, finest, (const int32_t*)pl, nl, d_coords, n_faces, geom_key, grid,
+                                p->lattice_dirs, p->lattice_q, (uint32_t*)flags, &nb, stream));
+  out->n_boundary = nb;
+  void *cells, *q;
+  if (out_buffer(p, OW_OUT_CELLS, 8 * nb, &cells) || out_buffer(p, OW_OUT_Q, 4 * nb * p->lattice_q, &q)) {
+    ow_set_error("geometry_to_grid: output allocation failed");
+    return OW_ERR_INTERNAL;
+  }
+  OW_TRY(ow_lattice_links_emit(ctx, (int64_t*)cells, (float*)q, stream));
+  OW_TRY(ow_lattice_stats(ctx, out->lattice_stats, stream));
   return OW_OK;
 }

@@ -53,7 +53,7 @@ class Block:
 
 
 class Forest:
-    def __init__(self, domain: Aabb, root_dims, max_level=DEFAULT_MAX_LEVEL, capacity=None):
+    def __init__(self, domain: Aabb, root_dims, max_level=DEFAULT_MAX_LEVEL, capacity=None, _init_root=True):
         root_dims = np.asarray(root_dims, dtype=np.int64).reshape(-1)
         if root_dims.shape[0] != domain.dim:
             raise InvalidParameterError(f"root_dims has {root_dims.shape[0]} axes but domain is {domain.dim}D")
@@ -90,10 +90,12 @@ class Forest:
             return 1 if f is None else f._grow(user, view_p, need)
 
         self._grow_cb = _lib.GROW_FN(grow)
-        # root blocks 0..R-1 (x-fastest lattice coords, level 0, no parent): one kernel
-        v = self.view()
-        _lib.call("ow_forest_init_root", _lib.ctx(), C.byref(v), _lib.stream())
-        self._sync_from_view()
+        # root blocks 0..R-1 (x-fastest lattice coords, level 0, no parent): one
+        # kernel (ow_geometry_to_grid runs it itself: _init_root=False)
+        if _init_root:
+            v = self.view()
+            _lib.call("ow_forest_init_root", _lib.ctx(), C.byref(v), _lib.stream())
+            self._sync_from_view()
 
     # ------------------------------------------------------------------ storage
     def _alloc(self, cap):

@@ -122,6 +122,13 @@ class CoordListGeometry:
         if self.summary().first_nonfinite >= 0:
             raise InvalidParameterError("geometry has non-finite coordinates")
 
+    @classmethod
+    def _validated(cls, dim, coords, summary):
+        """Wrap device coords whose face summary the library already computed."""
+        g = cls.__new__(cls)
+        g.dim, g.coords, g.key, g._summary = int(dim), coords, next(_keys), summary
+        return g
+
     @property
     def n_faces(self):
         return int(self.coords.shape[2])

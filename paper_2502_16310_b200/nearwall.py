@@ -196,6 +196,85 @@ class _Clock:
         self.ms = 1e3 * (time.perf_counter() - self.t0)
 
 
+def _driver_setup(forest, n_faces, params, reuse_bins, shard):
+    """Bin buffers and the ow_nearwall_params struct of one driver call."""
+    binned = params.strategy == "binned"
+    b = params.bins_per_axis if binned else 1
+    bf = params.bin_fraction
+    if binned and bf is None:
+        bf = auto_bin_fraction(b ** forest.dim, n_faces)
+    if params.n_levels - 1 > _lib.MAX_PASSES:
+        raise InvalidParameterError(f"n_levels must be <= {_lib.MAX_PASSES + 1}, got {params.n_levels}")
+    if params.d_spec <= 0:
+        raise InvalidParameterError(f"near-wall distance must be positive, got {params.d_spec}")
+    backends.validate_backend(params.backend)
+    grid = bins_t = g = None
+    cap = 0
+    h = 0.0
+    if binned:
+        grid = BinGrid(forest.domain, params.bins_per_axis)
+        if bf < 1:
+            raise InvalidParameterError(f"bin_fraction must be >= 1, got {bf}")
+        h = np.float32(params.spacing) if params.spacing is not None else np.float32(default_spacing(grid))
+        if h <= 0:
+            raise InvalidParameterError(f"spacing must be positive, got {h}")
+        cap = max(1, params.overlap_factor * n_faces)
+        dev = forest.device
+        bins_t = (torch.empty(cap, dtype=torch.int32, device=dev), torch.empty(grid.n_bins, dtype=torch.int32, device=dev),
+                  torch.empty(grid.n_bins, dtype=torch.int32, device=dev))
+        g = grid.c_struct()
+    p = _lib.NearWallParamsC()
+    p.d_spec = float(np.float32(params.d_spec))
+    p.n_levels = params.n_levels
+    p.d_spec64 = float(params.d_spec)
+    p.reach = 0.0  # set by the caller (or derived natively)
+    p.binned = int(binned)
+    p.reuse_bins = int(bool(reuse_bins))
+    p.spacing = float(h)
+    p.overlap_factor = int(params.overlap_factor)
+    p.bin_fraction = int(bf or 1)
+    keep = None
+    if shard is not None and shard.world > 1:
+        p.rank, p.world = shard.rank, shard.world
+        keep = _lib.EXCHANGE_FN(shard.exchange_callback(forest))
+        p.exchange = keep
+    else:
+        p.rank, p.world = 0, 1
+    return dict(binned=binned, b=b, bf=bf, grid=grid, g=g, bins_t=bins_t, cap=cap, p=p, keep=keep)
+
+
+def _driver_done(forest, out):
+    forest._sync_from_view()
+    forest._version += 1
+    forest._leaf_cache.clear()
+    for level in range(out.n_passes):
+        if out.n_split[level] > 0:
+            forest._n_levels = max(forest._n_levels, level + 2)
+
+
+def _driver_result(forest, params, st, out) -> NearWallResult:
+    result = NearWallResult(forest=forest)
+    binned, b, bf = st["binned"], st["b"], st["bf"]
+    stages = ("bin_setup", "face_detection", "propagation", "refinement")
+    for level in range(out.n_passes):
+        for k, stage in enumerate(stages):
+            if stage in ("bin_setup", "propagation") and not binned:
+                continue
+            result.timings.append(StageTiming(stage, level, params.strategy, b, bf if binned else 1,
+                                              float(out.stage_ms[level][k])))
+    n = out.n_passes
+    result.marked_detected = list(out.marked_detected[:n])
+    result.marked_refined = list(out.marked_refined[:n])
+    result.cell_face_tests = list(out.tests[:n])
+    result.pairs_evaluated = list(out.evaluated[:n])
+    if binned:
+        e = int(out.bin_entries)
+        ids, counts, offsets = st["bins_t"]
+        result.bins = BinnedFaces(st["grid"].n_bins, ids[:e], counts, offsets)
+        result.grid = st["grid"]
+    return result
+
+
 def refine_near_wall(forest: Forest, geom: CoordListGeometry, params: NearWallParams, reuse_bins=True,
                      shard=None) -> NearWallResult:
     """Per level L in 0..n_levels-2: bins -> mark -> propagate -> refine.
@@ -214,82 +293,24 @@ def refine_near_wall(forest: Forest, geom: CoordListGeometry, params: NearWallPa
     if np.any(bbox.min < forest.domain.min - tol) or np.any(bbox.max > forest.domain.max + tol):
         raise InvalidParameterError(
             f"geometry spans {bbox.min.tolist()}..{bbox.max.tolist()}, outside the forest domain")
-    result = NearWallResult(forest=forest)
-    binned = params.strategy == "binned"
-    b = params.bins_per_axis if binned else 1
-    bf = params.bin_fraction
-    if binned and bf is None:
-        bf = auto_bin_fraction(BinGrid(forest.domain, b).n_bins, geom.n_faces)
-    if params.n_levels - 1 > _lib.MAX_PASSES:
-        raise InvalidParameterError(f"n_levels must be <= {_lib.MAX_PASSES + 1}, got {params.n_levels}")
-    passes = params.n_levels - 1
-    if passes == 0:
-        return result
+    if params.n_levels - 1 == 0:
+        return NearWallResult(forest=forest)
     _check_marking_inputs(forest, geom, params.d_spec)
-    dev = forest.device
-    grid = bins_t = None
-    g = None
-    cap = 0
-    if binned:
-        grid = BinGrid(forest.domain, params.bins_per_axis)
-        backends.validate_backend(params.backend)
-        if bf is not None and bf < 1:
-            raise InvalidParameterError(f"bin_fraction must be >= 1, got {bf}")
-        h = np.float32(params.spacing) if params.spacing is not None else np.float32(default_spacing(grid))
-        if h <= 0:
-            raise InvalidParameterError(f"spacing must be positive, got {h}")
-        cap = max(1, params.overlap_factor * geom.n_faces)
-        bins_t = (torch.empty(cap, dtype=torch.int32, device=dev), torch.empty(grid.n_bins, dtype=torch.int32, device=dev),
-                  torch.empty(grid.n_bins, dtype=torch.int32, device=dev))
-        g = grid.c_struct()
-    p = _lib.NearWallParamsC()
-    p.d_spec = float(np.float32(params.d_spec))
-    p.n_levels = params.n_levels
-    p.d_spec64 = float(params.d_spec)
+    st = _driver_setup(forest, geom.n_faces, params, reuse_bins, shard)
+    p = st["p"]
     p.reach = float(_cull_reach(params.d_spec, _coordinate_scale(forest, geom)))
-    p.binned = int(binned)
-    p.reuse_bins = int(bool(reuse_bins))
-    p.spacing = float(h) if binned else 0.0
-    p.overlap_factor = int(params.overlap_factor)
-    p.bin_fraction = int(bf or 1)
-    exch = None
-    if shard is not None and shard.world > 1:
-        p.rank, p.world = shard.rank, shard.world
-        exch = _lib.EXCHANGE_FN(shard.exchange_callback(forest))
-        p.exchange = exch
-    else:
-        p.rank, p.world = 0, 1
     out = _lib.NearWallResultC()
+    g, bins_t = st["g"], st["bins_t"]
     v = forest.view()
     try:
         _lib.call("ow_refine_near_wall", _lib.ctx(), C.byref(v), _lib.ptr(geom.coords), geom.n_faces, geom.key,
                   C.byref(g) if g is not None else None, C.byref(p),
-                  _lib.ptr(bins_t[0]) if binned else None, cap,
-                  _lib.ptr(bins_t[1]) if binned else None, _lib.ptr(bins_t[2]) if binned else None,
+                  _lib.ptr(bins_t[0]) if bins_t else None, st["cap"],
+                  _lib.ptr(bins_t[1]) if bins_t else None, _lib.ptr(bins_t[2]) if bins_t else None,
                   C.byref(out), _lib.stream())
     finally:
-        forest._sync_from_view()
-        forest._version += 1
-        forest._leaf_cache.clear()
-        for level in range(out.n_passes):
-            if out.n_split[level] > 0:
-                forest._n_levels = max(forest._n_levels, level + 2)
-    stages = ("bin_setup", "face_detection", "propagation", "refinement")
-    for level in range(out.n_passes):
-        for k, stage in enumerate(stages):
-            if stage in ("bin_setup", "propagation") and not binned:
-                continue
-            result.timings.append(StageTiming(stage, level, params.strategy, b, bf if binned else 1,
-                                              float(out.stage_ms[level][k])))
-        result.marked_detected.append(int(out.marked_detected[level]))
-        result.marked_refined.append(int(out.marked_refined[level]))
-        result.cell_face_tests.append(int(out.tests[level]))
-        result.pairs_evaluated.append(int(out.evaluated[level]))
-    if binned:
-        e = int(out.bin_entries)
-        result.bins = BinnedFaces(grid.n_bins, bins_t[0][:e], bins_t[1], bins_t[2])
-        result.grid = grid
-    return result
+        _driver_done(forest, out)
+    return _driver_result(forest, params, st, out)
 
 
 def _mark_level(forest, level, geom, d_spec, bins, grid, shard):

@@ -1,0 +1,155 @@
+"""One geometry-to-grid pass in one native call (``ow_geometry_to_grid``).
+
+The reference runs import -> refine_near_wall as separate Python calls
+(cli.py:87-113); each is available here with the reference's signature
+(``import_stl``, ``refine_near_wall``, ``build_lattice_links``).  This module
+adds the fused B200 path: binary STL records resident in HBM -> validated SoA
+geometry -> root grid -> per-level {bins, marking, propagation, refinement}
+-> lattice links + q on the finest level, driven from C++ with no Python
+between the stages.  Every returned array is an ordinary CUDA tensor: output
+buffers are allocated by PyTorch before the call (sized from the previous
+pass of the same plan) or, when a size is first learnt on the device, through
+an allocation callback.
+
+``GridPlan`` holds everything that does not depend on the geometry (bin grid,
+driver parameters, lattice directions, callbacks), so repeated passes — a
+time series of geometries, a benchmark loop — pay only for the call itself.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import InvalidParameterError
+from .forest import DEFAULT_MAX_LEVEL, Forest
+from .geometry import Aabb, CoordListGeometry
+from .geometry import _keys as _geom_keys
+from .lattice import LatticeLinks, lattice_directions
+from .nearwall import NearWallParams, NearWallResult, _driver_done, _driver_result, _driver_setup
+
+_OUT_DTYPES = (torch.int64, torch.int32, torch.int64, torch.float32)  # OW_OUT_LEAVES, FLAGS, CELLS, Q
+
+
+@dataclass
+class GridPass:
+    geometry: CoordListGeometry
+    forest: Forest
+    result: NearWallResult
+    links: LatticeLinks | None
+
+
+class GridPlan:
+    """Reusable setup of ``geometry_to_grid`` for one (domain, root grid,
+    NearWallParams, lattice)."""
+
+    def __init__(self, domain: Aabb, root_dims, params: NearWallParams, lattice: str | None = "D3Q19",
+                 capacity=None, max_level=DEFAULT_MAX_LEVEL):
+        self.domain = domain if isinstance(domain, Aabb) else Aabb(*domain)
+        self.dim = self.domain.dim
+        self.root_dims = tuple(int(v) for v in np.asarray(root_dims).reshape(-1))
+        self.params = params
+        self.lattice = lattice
+        self.max_level = max_level
+        r = int(np.prod(self.root_dims))
+        self.capacity = int(capacity or 32 * r)
+        self.dev = _lib.device()
+        self.dirs = None
+        if lattice:
+            self.dirs = lattice_directions(lattice)
+            if self.dirs.shape[1] != self.dim:
+                raise InvalidParameterError(f"lattice {lattice} does not match a {self.dim}D domain")
+        self._est = [0, 0, 0, 0]  # output bytes of the last pass (preallocation estimate)
+        self._outs = {}
+
+        def alloc(_user, what, nbytes, out_p):
+            try:
+                t = self._new_out(int(what), int(nbytes))
+                out_p[0] = t.data_ptr() if t.numel() else None
+                return 0
+            except Exception:  # pragma: no cover - reported by the C side as a failed allocation
+                return 1
+
+        self._alloc_cb = _lib.ALLOC_FN(alloc)
+
+    def _new_out(self, what, nbytes):
+        dt = _OUT_DTYPES[what]
+        t = torch.empty(max(nbytes, 0) // (8 if dt in (torch.int64,) else 4), dtype=dt, device=self.dev)
+        self._outs[what] = t
+        return t
+
+    def run(self, records: torch.Tensor | None = None, n_faces: int | None = None,
+            geometry: CoordListGeometry | None = None) -> GridPass:
+        """Binary STL records (device uint8, 50 bytes per face, after the
+        84-byte header) — or an existing ``geometry`` — to a refined forest and
+        its finest-level lattice links."""
+        if geometry is None and records is None:
+            raise InvalidParameterError("geometry_to_grid needs STL records or a geometry")
+        dim = self.dim
+        if geometry is not None:
+            if geometry.dim != dim:
+                raise InvalidParameterError(f"geometry is {geometry.dim}D but the domain is {dim}D")
+            coords = geometry.coords
+        else:
+            if dim != 3:
+                raise InvalidParameterError("binary STL records are 3D")
+            coords = torch.empty((3, 3, int(n_faces)), dtype=torch.float32, device=self.dev)
+        nf = int(coords.shape[2])
+        forest = Forest(self.domain, self.root_dims, max_level=self.max_level, capacity=self.capacity,
+                        _init_root=False)
+        st = _driver_setup(forest, nf, self.params, True, None)
+        gp = _lib.G2GParamsC()
+        gp.nw = st["p"]
+        self._outs = {}
+        if self.dirs is not None:
+            gp.lattice_q = len(self.dirs)
+            for i, v in enumerate(self.dirs.reshape(-1)):
+                gp.lattice_dirs[i] = int(v)
+            gp.alloc = self._alloc_cb
+            for what in range(4):  # fresh tensors sized from the last pass: no callback in steady state
+                if self._est[what]:
+                    t = self._new_out(what, self._est[what] + self._est[what] // 8 + 64)
+                    gp.out_buf[what] = t.data_ptr()
+                    gp.out_cap[what] = t.numel() * t.element_size()
+        out = _lib.G2GResultC()
+        g, bins_t = st["g"], st["bins_t"]
+        v = forest.view()
+        try:
+            _lib.call("ow_geometry_to_grid", _lib.ctx(), _lib.ptr(records) if geometry is None else None,
+                      _lib.ptr(coords), nf, next(_geom_keys), C.byref(v), C.byref(g) if g is not None else None,
+                      C.byref(gp), _lib.ptr(bins_t[0]) if bins_t else None, st["cap"],
+                      _lib.ptr(bins_t[1]) if bins_t else None, _lib.ptr(bins_t[2]) if bins_t else None,
+                      C.byref(out), _lib.stream())
+        except InvalidParameterError:
+            if out.outside_domain:
+                lo = np.array(out.faces.bbox_min[:dim], np.float32).astype(np.float64)
+                hi = np.array(out.faces.bbox_max[:dim], np.float32).astype(np.float64)
+                raise InvalidParameterError(
+                    f"geometry spans {lo.tolist()}..{hi.tolist()}, outside the forest domain") from None
+            raise
+        finally:
+            _driver_done(forest, out.nw)
+        geom = geometry if geometry is not None else CoordListGeometry._validated(dim, coords, out.faces)
+        result = _driver_result(forest, self.params, st, out.nw)
+        links = None
+        if self.dirs is not None:
+            nq, nl, nb = len(self.dirs), int(out.n_finest_leaves), int(out.n_boundary)
+            ncell = 4 ** dim
+            need = (8 * nl, 4 * nl * ncell, 8 * nb, 4 * nb * nq)
+            self._est = list(need)
+            o = self._outs
+            links = LatticeLinks(lattice=self.lattice, level=int(out.finest_level), leaves=o[0][:nl],
+                                 flags=o[1][: nl * ncell], cells=o[2][:nb], q=o[3][: nb * nq].view(nb, nq))
+        return GridPass(geom, forest, result, links)
+
+
+def geometry_to_grid(records: torch.Tensor | None, n_faces: int | None, domain: Aabb, root_dims,
+                     params: NearWallParams, lattice: str | None = "D3Q19", capacity=None,
+                     geometry: CoordListGeometry | None = None, max_level=DEFAULT_MAX_LEVEL) -> GridPass:
+    """One-shot ``GridPlan(...).run(...)``."""
+    return GridPlan(domain, root_dims, params, lattice, capacity=capacity, max_level=max_level).run(
+        records, n_faces, geometry)

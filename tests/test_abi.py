@@ -87,3 +87,29 @@ def test_no_gpu_means_loud_failure():
 
     with pytest.raises(ow.OctowallError, match="CUDA device"):
         ow.init_root_grid(ow.Aabb((0, 0), (1, 1)), (4, 4))
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """ctypes mirrors of the C structs have the C compiler's sizes/offsets."""
+    import ctypes as C
+    import shutil
+    import subprocess
+
+    from paper_2502_16310_b200 import _lib
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    src = tmp_path / "sz.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "owb200.h"\n'
+        "int main(){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(ow_grid), sizeof(ow_forest),"
+        " sizeof(ow_face_summary), sizeof(ow_nearwall_params), sizeof(ow_nearwall_result), sizeof(ow_g2g_params),"
+        " sizeof(ow_g2g_result), offsetof(ow_g2g_result, nw)); return 0;}\n")
+    exe = tmp_path / "sz"
+    subprocess.run([cc, "-I", os.path.join(REPO, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    want = [C.sizeof(_lib.Grid), C.sizeof(_lib.ForestView), C.sizeof(_lib.FaceSummary),
+            C.sizeof(_lib.NearWallParamsC), C.sizeof(_lib.NearWallResultC), C.sizeof(_lib.G2GParamsC),
+            C.sizeof(_lib.G2GResultC), _lib.G2GResultC.nw.offset]
+    assert got == want

@@ -439,3 +439,59 @@ def test_marking_dense_soup_single_root(ow):
                                  ow.NearWallParams(d_spec=0.05, n_levels=3, bins_per_axis=B, strategy=strategy))
         assert rg.marked_detected == ro["marked_detected"]
         np.testing.assert_array_equal(fg._coords, fo.coords)
+
+
+# --------------------------------------------------------------------------- fused native pass
+def test_geometry_to_grid_matches_per_function_path(ow):
+    """ow_geometry_to_grid (one native call from STL records) equals the
+    reference call sequence import_stl -> init_root_grid -> refine_near_wall
+    -> build_lattice_links, array for array."""
+    import torch
+
+    from paper_2502_16310_b200 import pipeline, shapes
+
+    tris = shapes.icosphere_triangles(3)
+    data = shapes.binary_stl_bytes(tris)
+    n = int.from_bytes(data[80:84], "little")
+    rec = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda()
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8)
+    plan = pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q27")
+    plan.run(rec, n)
+    gp = plan.run(rec, n)  # second pass: preallocated outputs sized from the first
+    geom = ow.import_stl_bytes(data)
+    f = ow.init_root_grid(dom, (8, 8, 8))
+    res = ow.refine_near_wall(f, geom, params)
+    ll = ow.build_lattice_links(f, geom, None, "D3Q27")
+    assert torch.equal(gp.geometry.coords, geom.coords)
+    assert gp.result.marked_detected == res.marked_detected and gp.result.cell_face_tests == res.cell_face_tests
+    assert gp.result.marked_refined == res.marked_refined
+    np.testing.assert_array_equal(gp.forest._coords, f._coords)
+    np.testing.assert_array_equal(gp.forest._first_child, f._first_child)
+    assert gp.forest.blocks_per_level() == f.blocks_per_level()
+    assert torch.equal(gp.result.bins.ids, res.bins.ids)
+    for name in ("leaves", "flags", "cells", "q"):
+        assert torch.equal(getattr(gp.links, name), getattr(ll, name)), name
+
+
+def test_geometry_to_grid_errors(ow):
+    import torch
+
+    from paper_2502_16310_b200 import pipeline, shapes
+
+    tris = shapes.icosphere_triangles(2).astype(np.float32)
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.06, n_levels=2, bins_per_axis=4)
+
+    def run(t):
+        data = shapes.binary_stl_bytes(t)
+        rec = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda()
+        return pipeline.geometry_to_grid(rec, len(t), dom, (4, 4, 4), params, "D3Q19")
+
+    bad = tris.copy()
+    bad[5, 1] = bad[5, 0]
+    with pytest.raises(ow.InvalidParameterError, match="degenerate triangle .* at face 5"):
+        run(bad)
+    out = tris + np.float32(0.9)
+    with pytest.raises(ow.InvalidParameterError, match="outside the forest domain"):
+        run(out)

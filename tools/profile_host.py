@@ -28,7 +28,7 @@ params = ow.NearWallParams(d_spec=cfg["d"], n_levels=cfg["levels"], bins_per_axi
 
 def step():
     geom = ow.geometry.stl_records_to_coords(rec, n)
-    f = ow.init_root_grid(dom, (cfg["root"],) * dim, capacity=8 * cfg["root"] ** dim)
+    f = ow.init_root_grid(dom, (cfg["root"],) * dim, capacity=32 * cfg["root"] ** dim)
     ow.refine_near_wall(f, geom, params)
     ow.build_lattice_links(f, geom, None, cfg["lattice"])
 
