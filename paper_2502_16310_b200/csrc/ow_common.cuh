@@ -65,7 +65,6 @@ enum ow_slot {
   SLOT_LAT_HAS,        // leaf has at least one candidate row
   SLOT_LAT_CEN,        // per-leaf float32 cell-centre coordinates [D][4]
   SLOT_LAT_REC,        // packed face records (v0, e1, e2)
-  SLOT_LAT_FCNT,       // rows per face -> row offsets
   SLOT_LAT_ROWS,       // (leaf, face, block, direction|cell ranges) rows
   SLOT_LAT_ROWOFF,     // units per row -> unit offsets
   SLOT_LAT_TILEROW,    // first row of each intersection tile
@@ -124,6 +123,7 @@ struct ow_ctx {
   ow_grid link_grid;
   // lattice phase state
   int64_t lat_leaves, lat_boundary, lat_faces, lat_ncb, lat_rows, lat_units;
+  int64_t lat_row_cap, lat_unit_cap;  // capacities of the single-pass row / unit lists
   int32_t lat_dirs, lat_level;
   int8_t lat_dir[27 * 3];
   const float* lat_coords;

@@ -53,14 +53,17 @@ struct LatArgs {
   float* cen;               // [n_leaves][D][4] cell-centre coordinates
   uint8_t* has_pair;        // [n_leaves]
   float4* rec;              // [n_faces * 3] (v0, e1, e2) / (a, s)
-  int64_t* fcnt;            // [n_faces] rows | units << 32 per face -> exclusive offsets
+  double q[3];              // finest block size per axis
   int4* rows;               // [R]
   int64_t* rowoff;          // [R] units per row -> exclusive unit offsets
   int32_t* tile_row;        // [n_tiles] row of the first unit of each MT tile
-  int64_t n_rows, n_units;
+  int64_t row_cap, unit_cap;
+  unsigned long long* n_rows_d;   // device row counter (may exceed row_cap: overflow)
+  const int64_t* n_units_d;       // device unit total
   int32_t* cand_rank;       // [n_leaves]
   int32_t* cand_blocks;     // [n_cb]
   int64_t n_cb;
+  const int64_t* n_cb_d;    // device candidate-block count
   uint32_t* flags;          // [n_leaves * C]
   uint2* hits;              // [<= n_units] (flat cell, t bits)
   uint8_t* hit_dir;         // [<= n_units] direction of each hit
@@ -139,10 +142,11 @@ __device__ __forceinline__ unsigned row_word(const unsigned* R, const int8_t* c,
 // and the segment test reject det == 0), then walk the finest-level lattice
 // blocks the face box can reach (root-lattice descent, no bins).  Link boxes of
 // block k span [o_k - q/8, o_k + 9q/8]; a 0.01-block margin absorbs float
-// rounding and the exact per-axis range test filters.
-// Count pass: rows | units << 32 per face, has_pair per leaf.  EMIT: the rows
-// in slot order (warp prefix) and their unit counts.
-template <int D, bool EMIT>
+// rounding and the exact per-axis range test filters.  Rows are appended in
+// one pass (warp-aggregated counter): their order is irrelevant, every hit is
+// combined with atomicOr / atomicMin.  Rows past `row_cap` are counted but not
+// written (the host re-runs with room for them).
+template <int D>
 __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   const int lane = threadIdx.x & 31;
   const int64_t f = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
     e1[a] = FSUB(v[1][a], v[0][a]);  // e1 = v1 - v0 (3D) / s = b - a (2D), oracle/lattice.py
     e2[a] = D == 3 ? FSUB(v[2][a], v[0][a]) : 0.0f;
   }
-  if (!EMIT && lane == 0) {
+  if (lane == 0) {
     if (D == 3) {
       A.rec[3 * f + 0] = make_float4(v[0][0], v[0][1], v[0][2], 0.0f);
       A.rec[3 * f + 1] = make_float4(e1[0], e1[1], e1[2], 0.0f);
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   int64_t nslots = detmask ? 1 : 0;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    const double q = block_len(A.F, a, L);
+    const double q = A.q[a];
     const int64_t nmax = ((int64_t)A.F.root[a] << L) - 1;
     int64_t a0 = (int64_t)ceil(((double)lo[a] - A.F.dmin[a]) / q - 1.135);
     int64_t a1 = (int64_t)floor(((double)hi[a] - A.F.dmin[a]) / q + 0.135);
@@ -201,11 +205,9 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
     ext[a] = a1 >= a0 ? (int)(a1 - a0 + 1) : 0;
     nslots *= ext[a];
   }
-  int64_t out = EMIT ? (A.fcnt[f] & 0xffffffffll) : 0;
-  int64_t rows_w = 0, units_w = 0;
   for (int64_t s0 = 0; s0 < nslots; s0 += 32) {
     const int64_t slot = s0 + lane;
-    int nrow = 0, nunit = 0, pos = 0;
+    int nrow = 0, pos = 0;
     unsigned R[3] = {0u, 0u, 0u};
     if (slot < nslots) {
       int32_t nc[3] = {0, 0, 0};
@@ -223,47 +225,37 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
         for (int a = 0; a < D; ++a)
           R[a] = axis_ranges(reinterpret_cast<const float4*>(A.cen)[(int64_t)pos * D + a], A.h[a], lo[a], hi[a]);
         for (int d = 1; d < A.nq; ++d) {
-          if (!((detmask >> d) & 1u)) continue;
           int units;
-          if (!row_word<D>(R, A.dc[d], d, &units)) continue;
-          ++nrow;
-          nunit += units;
+          if (((detmask >> d) & 1u) && row_word<D>(R, A.dc[d], d, &units)) ++nrow;
         }
-        if (!EMIT && nrow) A.has_pair[pos] = 1;
+        if (nrow) A.has_pair[pos] = 1;
       }
     }
-    if (EMIT) {
-      int incl = nrow;
+    int incl = nrow;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      int64_t k = out + incl - nrow;
-      if (nrow) {
-        for (int d = 1; d < A.nq; ++d) {
-          if (!((detmask >> d) & 1u)) continue;
-          int units;
-          const unsigned w = row_word<D>(R, A.dc[d], d, &units);
-          if (!w) continue;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (!tot) continue;
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(A.n_rows_d, (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    int64_t k = (int64_t)base + incl - nrow;
+    if (nrow) {
+      for (int d = 1; d < A.nq; ++d) {
+        if (!((detmask >> d) & 1u)) continue;
+        int units;
+        const unsigned w = row_word<D>(R, A.dc[d], d, &units);
+        if (!w) continue;
+        if (k < A.row_cap) {
           A.rows[k] = make_int4(pos, (int)f, (int)w, units);
           A.rowoff[k] = units;
-          ++k;
         }
+        ++k;
       }
-      out += __shfl_sync(0xffffffffu, incl, 31);
-    } else {
-      rows_w += nrow;
-      units_w += nunit;
     }
-  }
-  if (!EMIT) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      rows_w += __shfl_xor_sync(0xffffffffu, rows_w, o);
-      units_w += __shfl_xor_sync(0xffffffffu, units_w, o);
-    }
-    if (lane == 0) A.fcnt[f] = rows_w | (units_w << 32);
   }
 }
 
@@ -281,14 +273,38 @@ struct CandStore {
   }
 };
 
+// scans bounded by a device-side count (rows / candidate blocks are counted
+// on the device; the launch covers the host-known capacity)
+struct RowUnitsLoad {
+  const int64_t* units;
+  const unsigned long long* n;
+  int64_t cap;
+  __device__ int64_t operator()(int64_t i) const { return i < min((int64_t)*n, cap) ? units[i] : 0; }
+};
 // rowoff[i] = exclusive unit offset (in place over the unit counts); the row
 // holding the first unit of each MT tile is recorded on the fly
 struct RowCntStore {
   int64_t* off;
   int32_t* tile_row;
+  const unsigned long long* n;
+  int64_t row_cap, unit_cap;
   __device__ void operator()(int64_t i, int64_t e, int64_t v) const {
+    if (i >= min((int64_t)*n, row_cap)) return;
     off[i] = e;
-    for (int64_t t = (e + MT_TILE - 1) / MT_TILE; t * MT_TILE < e + v; ++t) tile_row[t] = (int32_t)i;
+    for (int64_t t = (e + MT_TILE - 1) / MT_TILE; t * MT_TILE < e + v && t * MT_TILE < unit_cap; ++t)
+      tile_row[t] = (int32_t)i;
+  }
+};
+struct BcountLoad {
+  const int32_t* c;
+  const int64_t* n;
+  __device__ int64_t operator()(int64_t i) const { return i < *n ? c[i] : 0; }
+};
+struct BoffStore {
+  int64_t* off;
+  const int64_t* n;
+  __device__ void operator()(int64_t i, int64_t e, int64_t) const {
+    if (i < *n) off[i] = e;
   }
 };
 
@@ -327,8 +343,9 @@ __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
   __shared__ int s_nh;
   for (int i = threadIdx.x; i < QMAX * 3; i += MT_THREADS) s_dv[i / 3][i % 3] = A.dv[i / 3][i % 3];
   if (threadIdx.x == 0) s_nh = 0;
-  const int64_t U = A.n_units;
-  const int64_t R = A.n_rows;
+  const int64_t U = *A.n_units_d;
+  const int64_t R = (int64_t)*A.n_rows_d;
+  if (R > A.row_cap || U > A.unit_cap) return;  // overflow: the host re-runs with room
   const int64_t n_tiles = (U + MT_TILE - 1) / MT_TILE;
   const int lane = threadIdx.x & 31;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -455,7 +472,7 @@ __global__ void k_lat_bcount(LatArgs A) {
   constexpr int C = D == 3 ? 64 : 16;
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (r >= A.n_cb) return;
+  if (r >= *A.n_cb_d) return;
   const int64_t pos = A.cand_blocks[r];
   unsigned long long m = 0;
 #pragma unroll
@@ -492,7 +509,9 @@ __global__ void k_lat_emit(LatArgs A) {
 template <int D>
 __global__ void k_lat_hits(LatArgs A) {
   constexpr int C = D == 3 ? 64 : 16;
-  const int64_t n_tiles = (A.n_units + MT_TILE - 1) / MT_TILE;
+  const int64_t U = *A.n_units_d;
+  if ((int64_t)*A.n_rows_d > A.row_cap || U > A.unit_cap) return;
+  const int64_t n_tiles = (U + MT_TILE - 1) / MT_TILE;
   const int lane = threadIdx.x & 31;
   for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_tiles;
        t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -518,7 +537,8 @@ LatArgs make_args(ow_ctx* ctx) {
   A.level = ctx->lat_level;
   for (int a = 0; a < 3; ++a) {
     // float32 of the FP64 cell size, as the device's block_len / 4 (IEEE division both sides)
-    A.h[a] = a < f->dim ? (float)(f->dext[a] / (double)((int64_t)f->root[a] << A.level) / 4.0) : 0.0f;
+    A.q[a] = a < f->dim ? f->dext[a] / (double)((int64_t)f->root[a] << A.level) : 1.0;
+    A.h[a] = a < f->dim ? (float)(A.q[a] / 4.0) : 0.0f;
   }
   for (int i = 0; i < A.nq; ++i)
     for (int a = 0; a < 3; ++a) {
@@ -533,15 +553,17 @@ LatArgs make_args(ow_ctx* ctx) {
   A.cen = (float*)ctx->slot_ptr[SLOT_LAT_CEN];
   A.has_pair = (uint8_t*)ctx->slot_ptr[SLOT_LAT_HAS];
   A.rec = (float4*)ctx->slot_ptr[SLOT_LAT_REC];
-  A.fcnt = (int64_t*)ctx->slot_ptr[SLOT_LAT_FCNT];
   A.rows = (int4*)ctx->slot_ptr[SLOT_LAT_ROWS];
   A.rowoff = (int64_t*)ctx->slot_ptr[SLOT_LAT_ROWOFF];
   A.tile_row = (int32_t*)ctx->slot_ptr[SLOT_LAT_TILEROW];
-  A.n_rows = ctx->lat_rows;
-  A.n_units = ctx->lat_units;
+  A.row_cap = ctx->lat_row_cap;
+  A.unit_cap = ctx->lat_unit_cap;
+  A.n_rows_d = (unsigned long long*)(ctx->d_small + 48);
+  A.n_units_d = ctx->d_small + 49;
   A.cand_rank = (int32_t*)ctx->slot_ptr[SLOT_LAT_RANK];
   A.cand_blocks = (int32_t*)ctx->slot_ptr[SLOT_LAT_LEAVES];
   A.n_cb = ctx->lat_ncb;
+  A.n_cb_d = ctx->d_small + 33;
   A.flags = ctx->lat_flags;
   A.hits = (uint2*)ctx->slot_ptr[SLOT_LAT_HITS];
   A.hit_dir = (uint8_t*)ctx->slot_ptr[SLOT_LAT_HITDIR];
@@ -589,8 +611,12 @@ extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, int32_t l
   ctx->lat_forest = *f;
   ctx->lat_flags = d_flags;
   *out_boundary = 0;
-  OW_CUDA(cudaMemsetAsync(ctx->d_small + 33, 0, 4 * 8, s));
   if (n_leaves <= 0) return OW_OK;
+  // row / unit capacities: last pass's sizes + 25 % (first pass: per-face guess);
+  // an overflow is detected at the single readback and the pass re-runs
+  if (ctx->lat_row_cap < 64 * n_faces + 1024) ctx->lat_row_cap = 64 * n_faces + 1024;
+  if (ctx->lat_unit_cap < 8 * ctx->lat_row_cap) ctx->lat_unit_cap = 8 * ctx->lat_row_cap;
+  const int64_t rcap = ctx->lat_row_cap, ucap = ctx->lat_unit_cap;
   void* p;
   const int64_t nl = n_leaves;
   OW_TRY(ow_slot(ctx, SLOT_LAT_POS, 4 * (size_t)f->n_blocks, s, &p));
@@ -599,63 +625,59 @@ extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, int32_t l
   OW_TRY(ow_slot(ctx, SLOT_LAT_RANK, 4 * (size_t)nl, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_LEAVES, 4 * (size_t)nl, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_REC, 48 * (size_t)n_faces, s, &p));
-  OW_TRY(ow_slot(ctx, SLOT_LAT_FCNT, 8 * (size_t)n_faces, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_ROWS, 16 * (size_t)rcap, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_ROWOFF, 8 * (size_t)rcap, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_TILEROW, 4 * (size_t)(ucap / MT_TILE + 2), s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_HITS, 8 * (size_t)ucap, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_HITDIR, (size_t)ucap, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_TILEHITS, 4 * (size_t)(ucap / MT_TILE + 2), s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_BCOUNT, 4 * (size_t)nl, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_BMASK, 8 * (size_t)nl, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_BOFFS, 8 * (size_t)nl, s, &p));
+  OW_CUDA(cudaMemsetAsync(ctx->d_small + 48, 0, 2 * 8, s));
+  OW_CUDA(cudaMemsetAsync(d_flags, 0, 4 * (size_t)n_leaves * C, s));
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
   LatArgs A = make_args(ctx);
-  if (D == 3) k_lat_pos<3><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of,
-                                                                         A.has_pair, A.cen);
-  else k_lat_pos<2><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of,
-                                                                    A.has_pair, A.cen);
-  if (D == 3) k_lat_faces<3, false><<<ow_blocks(n_faces, 4), 128, 0, s>>>(A);
-  else k_lat_faces<2, false><<<ow_blocks(n_faces, 4), 128, 0, s>>>(A);
+  if (D == 3) {
+    k_lat_pos<3><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
+    k_lat_faces<3><<<ow_blocks(n_faces, 4), 128, 0, s>>>(A);
+  } else {
+    k_lat_pos<2><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
+    k_lat_faces<2><<<ow_blocks(n_faces, 4), 128, 0, s>>>(A);
+  }
   ctx->launches += 2;
   OW_CHECK_LAUNCH();
-  OW_TRY(scan(ctx, ow::LoadArr<int64_t>{A.fcnt}, ow::StoreExcl<int64_t>{A.fcnt}, n_faces, ctx->d_small + 34, s));
   OW_TRY(scan(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s));
-  OW_CUDA(cudaMemsetAsync(d_flags, 0, 4 * (size_t)n_leaves * C, s));
-  int64_t tot[2];
-  OW_TRY(ow_readback(ctx, ctx->d_small + 33, 2, tot, s));
-  const int64_t n_cb = tot[0], n_rows = tot[1] & 0xffffffffll, n_units = (int64_t)((uint64_t)tot[1] >> 32);
-  if (n_units >= (int64_t(1) << 31) - MT_TILE) {
-    ow_set_error("lattice: %lld link-face tests exceed one pass (2^31)", (long long)n_units);
-    return OW_ERR_CAPACITY;
+  OW_TRY(scan(ctx, RowUnitsLoad{A.rowoff, A.n_rows_d, rcap}, RowCntStore{A.rowoff, A.tile_row, A.n_rows_d, rcap, ucap},
+              rcap, ctx->d_small + 49, s));
+  OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
+  const int64_t tiles_max = ucap / MT_TILE + 1;
+  if (D == 3) k_lat_mt<3><<<ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s>>>(A);
+  else k_lat_mt<2><<<ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s>>>(A);
+  OW_PROF_END(ctx, PROF_LAT_SWEEP, s);
+  if (D == 3) k_lat_bcount<3><<<ow_blocks(nl, 8), 256, 0, s>>>(A);
+  else k_lat_bcount<2><<<ow_blocks(nl, 8), 256, 0, s>>>(A);
+  ctx->launches += 2;
+  OW_CHECK_LAUNCH();
+  OW_TRY(scan(ctx, BcountLoad{A.bcount, A.n_cb_d}, BoffStore{(int64_t*)A.boff, A.n_cb_d}, nl, ctx->d_small + 35, s));
+  OW_PROF_END(ctx, PROF_LATTICE, s);
+  // single readback: candidate blocks, (scan scratch), boundary cells, rows, units
+  int64_t h[17];
+  OW_TRY(ow_readback(ctx, ctx->d_small + 33, 17, h, s));
+  const int64_t n_cb = h[0], nb = h[2], n_rows = h[15], n_units = h[16];
+  if (n_rows > rcap || n_units > ucap) {
+    ctx->lat_row_cap = n_rows + n_rows / 4 + 1024;
+    ctx->lat_unit_cap = n_units + n_units / 4 + 4096;
+    if (ctx->lat_unit_cap >= (int64_t(1) << 31)) {
+      ow_set_error("lattice: %lld link-face tests exceed one pass (2^31)", (long long)n_units);
+      return OW_ERR_CAPACITY;
+    }
+    return ow_lattice_links_count(ctx, f, level, d_leaves, n_leaves, d_coords, n_faces, geom_key, grid, h_dirs,
+                                  n_dirs, d_flags, out_boundary, stream);
   }
   ctx->lat_ncb = n_cb;
   ctx->lat_rows = n_rows;
   ctx->lat_units = n_units;
-  if (n_rows > 0) {
-    OW_TRY(ow_slot(ctx, SLOT_LAT_ROWS, 16 * (size_t)n_rows, s, &p));
-    OW_TRY(ow_slot(ctx, SLOT_LAT_ROWOFF, 8 * (size_t)n_rows, s, &p));
-    OW_TRY(ow_slot(ctx, SLOT_LAT_TILEROW, 4 * (size_t)(n_units / MT_TILE + 2), s, &p));
-    OW_TRY(ow_slot(ctx, SLOT_LAT_HITS, 8 * (size_t)n_units, s, &p));
-    OW_TRY(ow_slot(ctx, SLOT_LAT_HITDIR, (size_t)n_units, s, &p));
-    OW_TRY(ow_slot(ctx, SLOT_LAT_TILEHITS, 4 * (size_t)(n_units / MT_TILE + 2), s, &p));
-    OW_TRY(ow_slot(ctx, SLOT_LAT_BCOUNT, 4 * (size_t)n_cb, s, &p));
-    OW_TRY(ow_slot(ctx, SLOT_LAT_BMASK, 8 * (size_t)n_cb, s, &p));
-    OW_TRY(ow_slot(ctx, SLOT_LAT_BOFFS, 8 * (size_t)n_cb, s, &p));
-    A = make_args(ctx);
-    if (D == 3) k_lat_faces<3, true><<<ow_blocks(n_faces, 4), 128, 0, s>>>(A);
-    else k_lat_faces<2, true><<<ow_blocks(n_faces, 4), 128, 0, s>>>(A);
-    OW_LAUNCHED(ctx);
-    OW_CHECK_LAUNCH();
-    OW_TRY(scan(ctx, ow::LoadArr<int64_t>{A.rowoff}, RowCntStore{A.rowoff, A.tile_row}, n_rows, nullptr, s));
-    const int64_t tiles = (n_units + MT_TILE - 1) / MT_TILE;
-    OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
-    if (D == 3) k_lat_mt<3><<<ow_blocks(tiles, 1, 6 * OW_SMS), MT_THREADS, 0, s>>>(A);
-    else k_lat_mt<2><<<ow_blocks(tiles, 1, 6 * OW_SMS), MT_THREADS, 0, s>>>(A);
-    OW_PROF_END(ctx, PROF_LAT_SWEEP, s);
-    OW_LAUNCHED(ctx);
-    OW_CHECK_LAUNCH();
-    if (D == 3) k_lat_bcount<3><<<ow_blocks(n_cb, 8), 256, 0, s>>>(A);
-    else k_lat_bcount<2><<<ow_blocks(n_cb, 8), 256, 0, s>>>(A);
-    OW_LAUNCHED(ctx);
-    OW_CHECK_LAUNCH();
-    OW_TRY(scan(ctx, ow::LoadArr<int32_t>{A.bcount}, ow::StoreExcl<int64_t>{(int64_t*)A.boff}, n_cb,
-                ctx->d_small + 35, s));
-  }
-  OW_PROF_END(ctx, PROF_LATTICE, s);
-  int64_t nb;
-  OW_TRY(ow_readback(ctx, ctx->d_small + 35, 1, &nb, s));
   ctx->lat_boundary = nb;
   *out_boundary = nb;
   return OW_OK;
