@@ -77,6 +77,7 @@ enum ow_slot {
   SLOT_MARK_HIT,       // per-leaf hit words of a marking pass
   SLOT_DRV_LEAVES,     // native driver: leaves of the current level
   SLOT_DRV_STATS,      // native driver: per-pass marking statistics
+  SLOT_DRV_STATE,      // native driver: per-pass leaf count + refine state
   SLOT_MISC,
   SLOT_COUNT
 };
@@ -99,6 +100,7 @@ struct ow_ctx {
   int64_t* h_pinned;  // OW_PINNED_WORDS int64 of pinned host memory for readbacks
   int64_t* d_small;   // 64 int64 of device scalars (counters, flags)
   int64_t launches;
+  int64_t scan_epoch;  // epoch of the last scan (status words are epoch-tagged)
   // face prep cache key
   int64_t prep_key;
   float prep_d;
@@ -131,13 +133,25 @@ struct ow_ctx {
   uint32_t* lat_flags;
   ow_forest lat_forest;
   void* stage_events;  // native driver CUDA events
+  bool defer_stage_times;
 };
 
 // one marking pass without a host round trip: stats accumulate in d_out[0..2]
 int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves, const float* d_coords,
                    int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int32_t* d_bin_ids,
                    const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,
-                   double reach, unsigned long long* d_out, cudaStream_t s);
+                   double reach, unsigned long long* d_out, cudaStream_t s,
+                   const int64_t* d_n_leaves = nullptr);
+
+int ow_stage_times(ow_ctx* ctx, ow_nearwall_result* out);
+
+// device-driven forest steps of the native driver (ow_forest.cu)
+int ow_forest_leaves_dev(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t* d_out, int64_t* d_count,
+                         cudaStream_t s);
+int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, const int64_t* d_n, int64_t n_bound,
+                     int32_t rounds, cudaStream_t s);
+int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64_t* d_st, cudaStream_t s);
+int ow_rebalance_host(ow_ctx* ctx, ow_forest* f, int64_t f0, int64_t* n_split, cudaStream_t s);
 
 // refine_marked returning the MARKED-leaf count of the split pass as well
 int ow_refine_marked_counted(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* out_split, int64_t* out_marked,

@@ -325,3 +325,213 @@ static int refine_marked_impl(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t*
   *out_split = n_split;
   return OW_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Device-driven variants for the native driver: counts stay in device memory
+// (launches are sized from host upper bounds and read the exact count on the
+// device), so a whole level runs without a host round trip.
+// ---------------------------------------------------------------------------
+namespace {
+
+// refine state (int64, 64 words per pass): [0] intermediate-mark flag,
+// [1] capacity overflow, [2] MARKED leaves split, [3] blocks split in total,
+// [4] frontier start to resume from on the host, [5] MARKED list did not fit,
+// [RS_NR + k] block count before split k, [RS_CR + k] length of split list k
+enum { RS_INTER = 0, RS_OVER, RS_MARKED, RS_SPLITS, RS_RESUME, RS_OVER_FIRST, RS_NR = 8, RS_CR = 36, RS_WORDS = 64 };
+constexpr int RS_MAX_ITERS = 26;
+
+__global__ void k_rs_init(int64_t* st, int64_t n) {
+  for (int i = threadIdx.x; i < RS_WORDS; i += blockDim.x) st[i] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st[RS_NR] = n;
+    st[RS_RESUME] = n;
+  }
+}
+
+// Split k of a device-driven refine: list k (length cnt[k]) splits into ids
+// n[k] + 2^D r + ci; one thread publishes n[k+1].  A list that does not fit
+// the capacity is dropped (n[k+1] = n[k]) and the frontier to resume from is
+// recorded; the MARKED list (k = 0) is not split beyond max_level.
+__global__ void k_split_ring(ow_forest f, const int32_t* __restrict__ list, int64_t* st, int k, int beyond_max) {
+  const int nc = 1 << f.dim;
+  const int64_t base = st[RS_NR + k];
+  int64_t m = st[RS_CR + k];
+  const bool over = st[RS_OVER] || base + nc * m > f.capacity;
+  if (k == 0 && beyond_max) m = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (k == 0) st[RS_MARKED] = st[RS_CR];
+    if (over) {
+      if (m > 0 && !st[RS_OVER]) {
+        st[RS_OVER] = 1;
+        st[RS_OVER_FIRST] = k == 0;
+        st[RS_RESUME] = k > 0 ? st[RS_NR + k - 1] : base;
+      }
+      st[RS_NR + k + 1] = base;
+    } else {
+      st[RS_NR + k + 1] = base + nc * m;
+      st[RS_SPLITS] += m;
+      st[RS_RESUME] = base;  // frontier of the newest children
+    }
+  }
+  if (over) return;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m * nc; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / nc;
+    const int ci = (int)(t % nc);
+    const int p = list[r];
+    const int64_t id = base + t;
+    f.d_level[id] = (int16_t)(f.d_level[p] + 1);
+    for (int a = 0; a < f.dim; ++a) f.d_coord[a][id] = 2 * f.d_coord[a][p] + ((ci >> a) & 1);
+    f.d_parent[id] = p;
+    f.d_first_child[id] = -1;
+    f.d_marks[id] = OW_NONE;
+    if (ci == 0) {
+      f.d_first_child[p] = (int32_t)(base + r * nc);
+      f.d_marks[p] = OW_NONE;
+    }
+  }
+}
+
+// 2:1 violators around the frontier [n[k-1], n[k]) read on the device (grid-stride)
+__global__ void k_violators_dev(ForestC F, const int64_t* st, int k, uint8_t* flag) {
+  const int sides = 2 * F.dim;
+  const int64_t f0 = st[RS_NR + k - 1], f1 = st[RS_NR + k];
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (f1 - f0) * sides;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t id = f0 + t / sides;
+    const int s = (int)(t % sides);
+    const int lv = F.level[id];
+    int32_t c[3] = {F.coord[0][id], F.dim > 1 ? F.coord[1][id] : 0, F.dim > 2 ? F.coord[2][id] : 0};
+    int32_t nc[3];
+    if (!side_target(F, lv, c, s, nc)) continue;
+    int depth;
+    const int node = locate(F, lv, nc, &depth);
+    if (F.first_child[node] < 0 && depth < lv - 1) flag[node] = 1;
+  }
+}
+
+struct FlagLoadDev {  // violator flags of blocks [0, n), n on the device
+  const uint8_t* flag;
+  const int64_t* n;
+  __device__ int64_t operator()(int64_t i) const { return i < *n && flag[i] != 0; }
+};
+struct FlagCompactClear {  // compaction that also clears the flags it consumed
+  int32_t* out;
+  uint8_t* flag;
+  __device__ void operator()(int64_t i, int64_t e, int64_t v) const {
+    if (v) {
+      out[e] = (int32_t)i;
+      flag[i] = 0;
+    }
+  }
+};
+
+__global__ void k_prop_gather_dev(ForestC F, const int32_t* __restrict__ leaves, const int64_t* n) {
+  const int64_t nn = *n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
+    const int id = leaves[i];
+    if (F.marks[id] != OW_NONE) continue;
+    const int L = F.level[id];
+    int32_t c[3] = {F.coord[0][id], F.dim > 1 ? F.coord[1][id] : 0, F.dim > 2 ? F.coord[2][id] : 0};
+    for (int s = 0; s < 2 * F.dim; ++s) {
+      int32_t nc[3];
+      if (!side_target(F, L, c, s, nc)) continue;
+      if (side_has_marked(F, L, nc, s)) {
+        F.marks[id] = OW_INTERMEDIATE;
+        break;
+      }
+    }
+  }
+}
+
+__global__ void k_prop_promote_dev(int8_t* marks, const int32_t* __restrict__ leaves, const int64_t* n) {
+  const int64_t nn = *n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
+    const int id = leaves[i];
+    if (marks[id] == OW_INTERMEDIATE) marks[id] = OW_MARKED;
+  }
+}
+
+}  // namespace
+
+// leaves at `level` into d_out, count into *d_count (device; no readback)
+int ow_forest_leaves_dev(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t* d_out, int64_t* d_count,
+                         cudaStream_t s) {
+  return scan(ctx, LeafLoad{f->d_level, f->d_first_child, level}, CompactStore{d_out}, f->n_blocks, d_count, s);
+}
+
+int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, const int64_t* d_n, int64_t n_bound,
+                     int32_t rounds, cudaStream_t s) {
+  if (n_bound <= 0 || rounds <= 0) return OW_OK;
+  ForestC F = make_forestc(f);
+  OW_PROF_BEGIN(ctx, PROF_PROP, s);
+  for (int r = 0; r < rounds; ++r) {
+    k_prop_gather_dev<<<ow_blocks(n_bound, 128, 16 * OW_SMS), 128, 0, s>>>(F, d_leaves, d_n);
+    k_prop_promote_dev<<<ow_blocks(n_bound, 256, 8 * OW_SMS), 256, 0, s>>>(F.marks, d_leaves, d_n);
+    ctx->launches += 2;
+  }
+  OW_PROF_END(ctx, PROF_PROP, s);
+  OW_CHECK_LAUNCH();
+  return OW_OK;
+}
+
+// refine_marked + 2:1 rebalance (forest.py:300-370) without host round trips:
+// split the MARKED leaves at `level`, then `iters` violator sweeps (each
+// splits the coarser leaves more than one level above a new block).  The host
+// reads d_st afterwards: intermediate marks / beyond-max-level are errors; an
+// overflow or violators left after the last sweep are finished by
+// ow_rebalance_host from st[RS_RESUME] (or by a synchronous refine when the
+// MARKED list itself did not fit).
+int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64_t* d_st, cudaStream_t s) {
+  if (iters > RS_MAX_ITERS) iters = RS_MAX_ITERS;
+  const int nc = 1 << f->dim;
+  const int64_t n = f->n_blocks, cap = f->capacity;
+  void *pl, *pf;
+  OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(cap + 1), s, &pl));
+  OW_TRY(ow_slot(ctx, SLOT_FOREST_FLAG, (size_t)cap + 8, s, &pf));
+  OW_PROF_BEGIN(ctx, PROF_REFINE, s);
+  k_rs_init<<<1, 64, 0, s>>>(d_st, n);
+  OW_CUDA(cudaMemsetAsync(pf, 0, (size_t)cap, s));
+  OW_TRY(scan(ctx, SplitLoad{make_forestc(f), level, d_st + RS_INTER}, CompactStore{(int32_t*)pl}, n, d_st + RS_CR, s));
+  const ow_forest fv = *f;
+  const int sg = ow_blocks(cap * nc, 256, 8 * OW_SMS);
+  k_split_ring<<<sg, 256, 0, s>>>(fv, (const int32_t*)pl, d_st, 0, level >= f->max_level);
+  ctx->launches += 2;
+  ForestC F = make_forestc(f);
+  F.n = cap;
+  for (int k = 1; k <= iters; ++k) {
+    k_violators_dev<<<ow_blocks(cap * 2 * f->dim, 256, 8 * OW_SMS), 256, 0, s>>>(F, d_st, k, (uint8_t*)pf);
+    OW_TRY(scan(ctx, FlagLoadDev{(const uint8_t*)pf, d_st + RS_NR + k}, FlagCompactClear{(int32_t*)pl, (uint8_t*)pf},
+                cap, d_st + RS_CR + k, s));
+    k_split_ring<<<sg, 256, 0, s>>>(fv, (const int32_t*)pl, d_st, k, 0);
+    ctx->launches += 2;
+  }
+  OW_PROF_END(ctx, PROF_REFINE, s);
+  OW_CHECK_LAUNCH();
+  return OW_OK;
+}
+
+// finish a rebalance on the host loop from frontier [f0, n_blocks) (fallback of
+// ow_refine_dev after an overflow or a cascade deeper than its sweeps)
+int ow_rebalance_host(ow_ctx* ctx, ow_forest* f, int64_t f0, int64_t* n_split, cudaStream_t s) {
+  int64_t* small = ctx->d_small;
+  int64_t h[1];
+  while (f->n_blocks > f0) {
+    const int64_t f1 = f->n_blocks;
+    void *pf, *pl;
+    OW_TRY(ow_slot(ctx, SLOT_FOREST_FLAG, (size_t)f->capacity + 8, s, &pf));
+    OW_CUDA(cudaMemsetAsync(pf, 0, (size_t)f1, s));
+    ForestC F = make_forestc(f);
+    k_violators<<<ow_blocks((f1 - f0) * 2 * f->dim, 256), 256, 0, s>>>(F, f0, f1, (uint8_t*)pf);
+    OW_LAUNCHED(ctx);
+    OW_CHECK_LAUNCH();
+    OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(f1 + 1), s, &pl));
+    OW_TRY(scan(ctx, FlagLoad{(const uint8_t*)pf}, CompactStore{(int32_t*)pl}, f1, small + 8, s));
+    OW_TRY(ow_readback(ctx, small + 8, 1, h, s));
+    if (h[0] == 0) break;
+    *n_split += h[0];
+    f0 = f1;
+    OW_TRY(split_list(ctx, f, (const int32_t*)pl, h[0], s));
+  }
+  return OW_OK;
+}

@@ -45,6 +45,9 @@ struct LatArgs {
   float h[3];               // finest cell size per axis (float32 of the FP64 value)
   float dv[QMAX][3];        // link vectors c_d * h (exact)
   int8_t dc[QMAX][3];       // lattice directions c_d
+  uint8_t dir_combo[32];    // combination index sum_a (c_a + 1) 3^a of direction d
+  uint8_t combo_dir[27];    // direction of each combination (lattice subset)
+  unsigned spread[3][8];    // per-axis non-empty-c mask -> mask over combinations
   const float* coords;
   int64_t n_faces;
   const int32_t* leaves;
@@ -189,7 +192,8 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
       dok = FSUB(FMUL(dv[0], e1[1]), FMUL(dv[1], e1[0])) != 0.0f;
     }
   }
-  const unsigned detmask = __ballot_sync(0xffffffffu, dok);
+  // lattice directions with a non-zero determinant, over the 3^D combinations
+  const unsigned detmask = __reduce_or_sync(0xffffffffu, dok ? 1u << A.dir_combo[lane] : 0u);
   const int L = A.level;
   int k0[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
   int64_t nslots = detmask ? 1 : 0;
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   for (int64_t s0 = 0; s0 < nslots; s0 += 32) {
     const int64_t slot = s0 + lane;
     int nrow = 0, pos = 0;
-    unsigned R[3] = {0u, 0u, 0u};
+    unsigned R[3] = {0u, 0u, 0u}, valid = 0u;
     if (slot < nslots) {
       int32_t nc[3] = {0, 0, 0};
       int64_t rem = slot;
@@ -224,10 +228,12 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
 #pragma unroll
         for (int a = 0; a < D; ++a)
           R[a] = axis_ranges(reinterpret_cast<const float4*>(A.cen)[(int64_t)pos * D + a], A.h[a], lo[a], hi[a]);
-        for (int d = 1; d < A.nq; ++d) {
-          int units;
-          if (((detmask >> d) & 1u) && row_word<D>(R, A.dc[d], d, &units)) ++nrow;
-        }
+        // directions with a non-empty cell box on every axis, as a mask over the
+        // 3^D combinations c = (c_x, c_y[, c_z]) (outer product of per-axis masks)
+        valid = detmask;
+#pragma unroll
+        for (int a = 0; a < D; ++a) valid &= A.spread[a][(~R[a] >> 12) & 7u];
+        nrow = __popc(valid);
         if (nrow) A.has_pair[pos] = 1;
       }
     }
@@ -243,18 +249,23 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
     if (lane == 31) base = atomicAdd(A.n_rows_d, (unsigned long long)tot);
     base = __shfl_sync(0xffffffffu, base, 31);
     int64_t k = (int64_t)base + incl - nrow;
-    if (nrow) {
-      for (int d = 1; d < A.nq; ++d) {
-        if (!((detmask >> d) & 1u)) continue;
-        int units;
-        const unsigned w = row_word<D>(R, A.dc[d], d, &units);
-        if (!w) continue;
-        if (k < A.row_cap) {
-          A.rows[k] = make_int4(pos, (int)f, (int)w, units);
-          A.rowoff[k] = units;
-        }
-        ++k;
+    while (valid) {
+      const int ci = __ffs(valid) - 1;
+      valid &= valid - 1;
+      unsigned w = (unsigned)A.combo_dir[ci];
+      int units = 1, cc = ci;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const unsigned ra = (R[a] >> (4 * (cc % 3))) & 0xFu;
+        cc /= 3;
+        w |= ra << (5 + 4 * a);
+        units *= (int)(ra >> 2) + 1;
       }
+      if (k < A.row_cap) {
+        A.rows[k] = make_int4(pos, (int)f, (int)w, units);
+        A.rowoff[k] = units;
+      }
+      ++k;
     }
   }
 }
@@ -540,10 +551,26 @@ LatArgs make_args(ow_ctx* ctx) {
     A.q[a] = a < f->dim ? f->dext[a] / (double)((int64_t)f->root[a] << A.level) : 1.0;
     A.h[a] = a < f->dim ? (float)(A.q[a] / 4.0) : 0.0f;
   }
-  for (int i = 0; i < A.nq; ++i)
+  for (int i = 0; i < A.nq; ++i) {
+    int ci = 0, mul = 1;
     for (int a = 0; a < 3; ++a) {
       A.dc[i][a] = ctx->lat_dir[i * 3 + a];
       A.dv[i][a] = (float)ctx->lat_dir[i * 3 + a] * A.h[a];  // exact
+      if (a < f->dim) {
+        ci += (ctx->lat_dir[i * 3 + a] + 1) * mul;
+        mul *= 3;
+      }
+    }
+    A.dir_combo[i] = (uint8_t)ci;
+    A.combo_dir[ci] = (uint8_t)i;
+  }
+  for (int a = 0; a < 3; ++a)
+    for (int m = 0; m < 8; ++m) {
+      unsigned sp = 0;
+      int ncomb = f->dim == 3 ? 27 : 9, div = a == 0 ? 1 : (a == 1 ? 3 : 9);
+      for (int c = 0; c < ncomb; ++c)
+        if ((m >> ((c / div) % 3)) & 1) sp |= 1u << c;
+      A.spread[a][m] = a < f->dim ? sp : 0xffffffffu;
     }
   A.coords = ctx->lat_coords;
   A.n_faces = ctx->lat_faces;

@@ -121,6 +121,7 @@ struct MarkArgs {
   const int32_t* bin_offsets;
   const float4* cbox;       // union boxes of 32-entry bin-CSR chunks
   int64_t n_faces, n_leaves;
+  const int64_t* d_n;       // optional device leaf count (n_leaves is then an upper bound)
   float d;
   double reach;
   unsigned long long* out;  // [0] marked, [1] tests, [2] evaluated
@@ -295,12 +296,12 @@ __device__ __forceinline__ bool sweep_chunks(const MarkArgs& A, MarkSmem<D>& S, 
 __device__ __forceinline__ unsigned div_magic(int n) { return (unsigned)((0x100000000ull + n - 1) / n); }
 
 template <int D, bool BINNED>
-__global__ void __launch_bounds__(MARK_THREADS) k_mark_blocks(MarkArgs A, MarkItems M) {
+__global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_blocks(MarkArgs A, MarkItems M) {
   constexpr int CPL = D == 3 ? 2 : 1;
   __shared__ MarkSmem<D> S;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t pos = (int64_t)blockIdx.x * MARK_WARPS + wid;
-  if (pos >= A.n_leaves) return;
+  if (pos >= (A.d_n ? *A.d_n : A.n_leaves)) return;
   const int id = A.leaves[pos];
   double blo[3], bhi[3];
   float p[CPL][3];
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(MARK_THREADS) k_mark_blocks(MarkArgs A, MarkIt
 }
 
 template <int D, bool BINNED>
-__global__ void __launch_bounds__(MARK_THREADS) k_mark_items(MarkArgs A, MarkItems M) {
+__global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_items(MarkArgs A, MarkItems M) {
   constexpr int CPL = D == 3 ? 2 : 1;
   __shared__ MarkSmem<D> S;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -598,7 +599,7 @@ __global__ void k_near_pairs(int dim, const float* __restrict__ pts, const float
 int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves, const float* d_coords,
                    int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int32_t* d_bin_ids,
                    const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,
-                   double reach, unsigned long long* out, cudaStream_t s) {
+                   double reach, unsigned long long* out, cudaStream_t s, const int64_t* d_n_leaves) {
   if (!(d_spec > 0.0f)) {
     ow_set_error("near-wall distance must be positive, got %g", (double)d_spec);
     return OW_ERR_INVALID;
@@ -640,6 +641,7 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   OW_TRY(ow_slot(ctx, SLOT_MARK_HIT, 4 * (size_t)n_leaves + 8, s, &ph));
   A.cbox = (const float4*)pc;
   A.n_leaves = n_leaves;
+  A.d_n = d_n_leaves;
   MarkItems M;
   M.items = (int4*)pi;
   M.n_items = (unsigned long long*)((unsigned*)ph + n_leaves + (n_leaves & 1));  // after the hit words

@@ -103,8 +103,9 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
   bool have_bins = false;
   int64_t E = 0;
   const int passes = p->n_levels - 1;
-  void* stats;
+  void *stats, *drv;
   OW_TRY(ow_slot(ctx, SLOT_DRV_STATS, 24 * (size_t)passes, s, &stats));
+  OW_TRY(ow_slot(ctx, SLOT_DRV_STATE, 8 * 72 * (size_t)passes, s, &drv));
   OW_CUDA(cudaMemsetAsync(stats, 0, 24 * (size_t)passes, s));
   for (int level = 0; level < passes; ++level) {
     // ---- bin_setup
@@ -140,54 +141,87 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
     }
     // ---- face_detection
     OW_TRY(record(se, level, 1, s));
+    const int64_t n_host = f->n_blocks;
     void* pl;
-    OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(f->n_blocks + 1), s, &pl));
-    int64_t n_leaves = 0;
-    OW_TRY(ow_forest_leaves(ctx, f, level, (int32_t*)pl, &n_leaves, s));
-    int64_t lo = 0, hi = n_leaves;
-    if (p->world > 1) {  // contiguous count-balanced slice (parallel.partition)
-      const int64_t per = (n_leaves + p->world - 1) / p->world;
-      lo = per * p->rank < n_leaves ? per * p->rank : n_leaves;
-      hi = per * (p->rank + 1) < n_leaves ? per * (p->rank + 1) : n_leaves;
-    }
-    // marking statistics stay on the device (per-pass slots, one readback at the end)
+    OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(n_host + 1), s, &pl));
+    int64_t* dn = (int64_t*)drv + 72 * level;  // [0] leaves at level, [8..72) refine state
+    int64_t* rs = dn + 8;
     unsigned long long* dst = (unsigned long long*)stats + 3 * level;
-    OW_TRY(ow_mark_launch(ctx, f, (const int32_t*)pl + lo, hi - lo, d_coords, n_faces, geom_key,
-                          p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
-                          p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
-                          p->binned ? E : 0, p->d_spec, p->reach, dst, s));
     if (p->world > 1) {
-      int64_t st[3];
-      OW_TRY(ow_readback(ctx, (const int64_t*)dst, 3, st, s));
+      // sharded marking: each rank marks a contiguous slice, then the exchange
+      // callback all-gathers the marks (the slice needs the leaf count on the host)
+      int64_t n_leaves = 0;
+      OW_TRY(ow_forest_leaves(ctx, f, level, (int32_t*)pl, &n_leaves, s));
+      OW_CUDA(cudaMemcpyAsync(dn, &ctx->h_pinned[0], 8, cudaMemcpyHostToDevice, s));  // h_pinned[0] = n_leaves
+      const int64_t per = (n_leaves + p->world - 1) / p->world;
+      const int64_t lo = per * p->rank < n_leaves ? per * p->rank : n_leaves;
+      const int64_t hi = per * (p->rank + 1) < n_leaves ? per * (p->rank + 1) : n_leaves;
+      OW_TRY(ow_mark_launch(ctx, f, (const int32_t*)pl + lo, hi - lo, d_coords, n_faces, geom_key,
+                            p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
+                            p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
+                            p->binned ? E : 0, p->d_spec, p->reach, dst, s));
       if (!p->exchange) {
         ow_set_error("refine_near_wall: world > 1 needs an exchange callback");
         return OW_ERR_INVALID;
       }
+      int64_t st[3];
+      OW_TRY(ow_readback(ctx, (const int64_t*)dst, 3, st, s));
       if (p->exchange(p->exchange_user, level, (const int32_t*)pl, n_leaves, lo, hi, st) != 0) {
         ow_set_error("refine_near_wall: mark exchange failed at level %d", level);
         return OW_ERR_INTERNAL;
       }
-      OW_CUDA(cudaMemcpyAsync(dst, st, 24, cudaMemcpyHostToDevice, s));
-      OW_CUDA(cudaStreamSynchronize(s));  // st is a host stack buffer
+      for (int k = 0; k < 3; ++k) ctx->h_pinned[k] = st[k];
+      OW_CUDA(cudaMemcpyAsync(dst, ctx->h_pinned, 24, cudaMemcpyHostToDevice, s));
+      OW_CUDA(cudaStreamSynchronize(s));
+    } else {
+      // leaf count stays on the device: marking is launched for n_host blocks
+      // (an upper bound) and every warp checks the exact count
+      OW_TRY(ow_forest_leaves_dev(ctx, f, level, (int32_t*)pl, dn, s));
+      OW_TRY(ow_mark_launch(ctx, f, (const int32_t*)pl, n_host, d_coords, n_faces, geom_key,
+                            p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
+                            p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
+                            p->binned ? E : 0, p->d_spec, p->reach, dst, s, dn));
     }
     // ---- propagation (binned only): 1 + floor(d / min block length)
     OW_TRY(record(se, level, 2, s));
-    if (p->binned && n_leaves > 0) {
+    if (p->binned) {
       double bl = INFINITY;
       for (int a = 0; a < f->dim; ++a) {
         const double b = f->dext[a] / (double)((int64_t)f->root[a] << level);
         bl = b < bl ? b : bl;
       }
       const int rounds = 1 + (int)floor(p->d_spec64 / bl);
-      OW_TRY(ow_propagate_marks(ctx, f, (const int32_t*)pl, n_leaves, rounds, s));
+      OW_TRY(ow_propagate_dev(ctx, f, (const int32_t*)pl, dn, n_host, rounds, s));
     }
-    // ---- refinement: MARKED leaves at level = the split count of this pass
+    // ---- refinement on the device; one readback of its state per level
     OW_TRY(record(se, level, 3, s));
-    int64_t n_split = 0, n_marked = 0;
-    OW_TRY(ow_refine_marked_counted(ctx, f, level, &n_split, &n_marked, s));
+    // splits that would not fit the current capacity are detected on the device
+    // and finished below on the host path, which grows the forest
+    const int iters = level + 2;  // a cascade of splits descends at least one level per sweep
+    OW_TRY(ow_refine_dev(ctx, f, level, iters, rs, s));
+    OW_TRY(record(se, level, 4, s));
+    int64_t h[64];
+    OW_TRY(ow_readback(ctx, rs, 64, h, s));
+    if (h[0]) {
+      ow_set_error("level %d still carries intermediate marks; finish propagation first", level);
+      return OW_ERR_INVALID;
+    }
+    if (h[2] > 0 && level >= f->max_level) {
+      ow_set_error("refinement beyond max level %d", f->max_level);
+      return OW_ERR_INVALID;
+    }
+    int64_t n_split = h[3], n_marked = h[2];
+    const int64_t n_final = h[8 + iters + 1], last_cnt = h[36 + iters];
+    if (h[1] && h[5]) {
+      // the MARKED list itself did not fit: refine synchronously (grows the forest)
+      OW_TRY(ow_refine_marked_counted(ctx, f, level, &n_split, &n_marked, s));
+    } else {
+      f->n_blocks = n_final;
+      if (h[1] || last_cnt > 0)  // capacity overflow or a cascade deeper than the device sweeps
+        OW_TRY(ow_rebalance_host(ctx, f, h[4], &n_split, s));
+    }
     out->marked_refined[level] = n_marked;
     out->n_split[level] = n_split;
-    OW_TRY(record(se, level, 4, s));
     out->n_passes = level + 1;
   }
   if (passes > 0) {
@@ -199,7 +233,15 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
       out->evaluated[level] = h[3 * level + 2];
     }
   }
-  OW_CUDA(cudaStreamSynchronize(s));
+  if (!ctx->defer_stage_times) return ow_stage_times(ctx, out);
+  return OW_OK;
+}
+
+// stage times of the last driver pass from its CUDA events (all recorded
+// events precede the driver's final readback, so they are complete)
+int ow_stage_times(ow_ctx* ctx, ow_nearwall_result* out) {
+  StageEvents* se = (StageEvents*)ctx->stage_events;
+  if (!se) return OW_OK;
   for (int level = 0; level < out->n_passes; ++level)
     for (int k = 0; k < 4; ++k) {
       float ms = 0.0f;
@@ -270,13 +312,16 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
   OW_TRY(ow_forest_init_root(ctx, f, stream));
   ow_nearwall_params nw = p->nw;
   if (!(nw.reach > 0.0)) nw.reach = nw.d_spec64 + 1e-3 * fmax(1.0, fmax(scale, nw.d_spec64));  // nearwall.py:38-40
-  OW_TRY(ow_refine_near_wall(ctx, f, d_coords, n_faces, geom_key, grid, &nw, d_bin_ids, bin_ids_capacity,
-                             d_bin_counts, d_bin_offsets, &out->nw, stream));
+  ctx->defer_stage_times = true;  // read the stage events after the lattice work is queued
+  const int st = ow_refine_near_wall(ctx, f, d_coords, n_faces, geom_key, grid, &nw, d_bin_ids, bin_ids_capacity,
+                                     d_bin_counts, d_bin_offsets, &out->nw, stream);
+  ctx->defer_stage_times = false;
+  OW_TRY(st);
   int finest = 0;
   for (int l = 0; l < out->nw.n_passes; ++l)
     if (out->nw.n_split[l] > 0) finest = l + 1;
   out->finest_level = finest;
-  if (p->lattice_q < 2 || !p->alloc) return OW_OK;
+  if (p->lattice_q < 2 || !p->alloc) return ow_stage_times(ctx, &out->nw);
   void* pl;
   OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(f->n_blocks + 1), s, &pl));
   int64_t nl = 0;
@@ -304,5 +349,5 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
   }
   OW_TRY(ow_lattice_links_emit(ctx, (int64_t*)cells, (float*)q, stream));
   OW_TRY(ow_lattice_stats(ctx, out->lattice_stats, stream));
-  return OW_OK;
+  return ow_stage_times(ctx, &out->nw);  // host work overlapping the emit kernels
 }

@@ -10,9 +10,14 @@ namespace ow {
 constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+// Status words carry an epoch so the array never needs clearing between
+// scans: [63:62] flag (1 aggregate, 2 inclusive prefix), [61:46] epoch,
+// [45:0] value (sums < 2^46).  The tile-ticket counter is reset by the last
+// tile to finish.
 constexpr unsigned long long ST_AGG = 1ull << 62;
 constexpr unsigned long long ST_INC = 2ull << 62;
-constexpr unsigned long long ST_VAL = (1ull << 62) - 1;
+constexpr unsigned long long ST_VAL = (1ull << 46) - 1;
+constexpr int ST_EPOCH_SHIFT = 46;
 
 __device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -27,8 +32,8 @@ __device__ __forceinline__ unsigned long long ld_status(const unsigned long long
 // Store: void operator()(int64_t i, int64_t exclusive_prefix, int64_t value) const
 template <class Load, class Store>
 __global__ void __launch_bounds__(SCAN_THREADS)
-k_scan(Load load, Store store, int64_t n, int64_t n_tiles, unsigned long long* status,
-       unsigned int* tile_ctr, int64_t* total_out) {
+k_scan(Load load, Store store, int64_t n, int64_t n_tiles, unsigned long long* status, unsigned int* tile_ctr,
+       int64_t* total_out, unsigned long long epoch) {
   __shared__ int s_tile;
   __shared__ int64_t s_warp[SCAN_THREADS / 32];
   __shared__ int64_t s_prefix;
@@ -65,22 +70,22 @@ k_scan(Load load, Store store, int64_t n, int64_t n_tiles, unsigned long long* s
   __syncthreads();
   const int64_t agg = s_warp[SCAN_THREADS / 32 - 1];
   const int64_t thread_excl = (warp ? s_warp[warp - 1] : 0) + x - sum;
+  const unsigned long long tag = epoch << ST_EPOCH_SHIFT;
   if (threadIdx.x == 0) {
     int64_t prefix = 0;
     if (tile == 0) {
-      st_status(&status[0], ST_INC | (unsigned long long)agg);
+      st_status(&status[0], ST_INC | tag | (unsigned long long)agg);
     } else {
-      st_status(&status[tile], ST_AGG | (unsigned long long)agg);
+      st_status(&status[tile], ST_AGG | tag | (unsigned long long)agg);
       int64_t p = tile - 1;
       while (true) {
-        unsigned long long s = ld_status(&status[p]);
-        unsigned long long flag = s & ~ST_VAL;
-        if (flag == 0) continue;
-        prefix += (int64_t)(s & ST_VAL);
-        if (flag == ST_INC) break;
+        unsigned long long st = ld_status(&status[p]);
+        if ((st & ~(3ull << 62)) >> ST_EPOCH_SHIFT != epoch) continue;  // not yet published this scan
+        prefix += (int64_t)(st & ST_VAL);
+        if ((st >> 62) == 2) break;
         --p;
       }
-      st_status(&status[tile], ST_INC | (unsigned long long)(prefix + agg));
+      st_status(&status[tile], ST_INC | tag | (unsigned long long)(prefix + agg));
     }
     s_prefix = prefix;
     if (tile == n_tiles - 1 && total_out) *total_out = prefix + agg;
@@ -93,6 +98,13 @@ k_scan(Load load, Store store, int64_t n, int64_t n_tiles, unsigned long long* s
     if (i < n) store(i, run, v[k]);
     run += v[k];
   }
+  if (threadIdx.x == 0) {  // last tile out resets the ticket counters for the next scan
+    __threadfence();
+    if (atomicAdd(tile_ctr + 1, 1u) == (unsigned)(n_tiles - 1)) {
+      tile_ctr[0] = 0;
+      tile_ctr[1] = 0;
+    }
+  }
 }
 
 // Exclusive scan of load(0..n-1); *d_total (device) receives the sum.
@@ -103,11 +115,19 @@ int scan(ow_ctx* ctx, Load load, Store store, int64_t n, int64_t* d_total, cudaS
     return OW_OK;
   }
   int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  const size_t need = 8 * (size_t)(tiles + 1);
+  void* old = ctx->slot_ptr[SLOT_SCAN_STATUS];
+  const size_t old_bytes = ctx->slot_bytes[SLOT_SCAN_STATUS];
   void* p;
-  OW_TRY(ow_slot(ctx, SLOT_SCAN_STATUS, 8 * (size_t)(tiles + 1), s, &p));
-  OW_CUDA(cudaMemsetAsync(p, 0, 8 * (size_t)(tiles + 1), s));
-  unsigned long long* status = (unsigned long long*)p + 1;
-  k_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(load, store, n, tiles, status, (unsigned int*)p, d_total);
+  OW_TRY(ow_slot(ctx, SLOT_SCAN_STATUS, need, s, &p));
+  if (p != old || ctx->slot_bytes[SLOT_SCAN_STATUS] != old_bytes || ctx->scan_epoch >= 65535) {
+    // fresh (or wrapped) status array: clear once, epochs restart at 1
+    OW_CUDA(cudaMemsetAsync(p, 0, ctx->slot_bytes[SLOT_SCAN_STATUS], s));
+    ctx->scan_epoch = 0;
+  }
+  const unsigned long long epoch = (unsigned long long)(++ctx->scan_epoch);
+  unsigned long long* status = (unsigned long long*)p + 1;  // word 0: ticket counters
+  k_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(load, store, n, tiles, status, (unsigned int*)p, d_total, epoch);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;

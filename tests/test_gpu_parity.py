@@ -495,3 +495,24 @@ def test_geometry_to_grid_errors(ow):
     out = tris + np.float32(0.9)
     with pytest.raises(ow.InvalidParameterError, match="outside the forest domain"):
         run(out)
+
+
+def test_native_driver_capacity_fallbacks(ow):
+    """A forest created with the minimum capacity overflows inside the device
+    refinement: the driver finishes on the host path (grow + rebalance) and the
+    forest equals the oracle's."""
+    from oracle import forest as of
+    from oracle import nearwall as on
+    from paper_2502_16310_b200 import shapes
+
+    coords = np.ascontiguousarray(np.transpose(shapes.icosphere_triangles(3).astype(np.float32), (1, 2, 0)))
+    fo = of.Forest(np.zeros(3), np.ones(3), (4, 4, 4))
+    ro = on.refine_near_wall(fo, coords, 0.08, n_levels=3, bins_per_axis=4)
+    fg = ow.init_root_grid(domain(ow, 3), (4, 4, 4), capacity=1)  # minimum capacity (1024 blocks): overflows
+    rg = ow.refine_near_wall(fg, ow.CoordListGeometry(3, coords),
+                             ow.NearWallParams(d_spec=0.08, n_levels=3, bins_per_axis=4))
+    assert fg.n_blocks > 1024
+    assert rg.marked_detected == ro["marked_detected"]
+    assert rg.marked_refined == ro["marked_refined"]
+    np.testing.assert_array_equal(fg._coords, fo.coords)
+    np.testing.assert_array_equal(fg._first_child, fo.first_child)
