@@ -270,10 +270,13 @@ def gpu_arm(args, cfg, rank, world, local_rank):
                 "algorithmic": algorithmic, "launches": n, "avg_launch_ms": ms / max(n, 1), "peak_note": peak_note}
 
     mark_ms, mark_n = prof["mark"]
-    mark = entry("k_mark (near-wall predicate sweep)", mark_ms, mark_n,
-                 FP32_OPS_PER_TEST[dim] * evaluated * args.steps,
-                 f"{FP32_OPS_PER_TEST[dim]} FP32 ops per evaluated cell-face predicate x {evaluated} per step "
-                 f"(pairs surviving the reference's box + sphere culls)", "mark")
+    spheres = int(sum(res.sphere_tests))
+    sphere_ops = 8 if dim == 3 else 5  # (dx, dy[, dz]) sub, squares, sums
+    mark = entry("k_mark_blocks + k_mark_items (near-wall marking)", mark_ms, mark_n,
+                 (FP32_OPS_PER_TEST[dim] * evaluated + sphere_ops * spheres) * args.steps,
+                 f"per step: {spheres} cell-face bounding-sphere tests x {sphere_ops} FP32 ops + {evaluated} "
+                 f"full predicates x {FP32_OPS_PER_TEST[dim]} FP32 ops (the reference's _scan_block cascade on the "
+                 f"pairs surviving its FP64 box cull; {int(sum(res.box_culls))} FP64 box culls not counted)", "mark")
     sw_ms, sw_n = prof["lattice_sweep"]
     n_cb, n_rows, mt = lat_stats
     per_mt = 45 if dim == 3 else 13

@@ -201,7 +201,9 @@ typedef struct {
   int64_t marked_refined[OW_MAX_PASSES];
   int64_t n_split[OW_MAX_PASSES];
   int64_t tests[OW_MAX_PASSES];     /* algorithmic cell-face tests T */
-  int64_t evaluated[OW_MAX_PASSES];
+  int64_t evaluated[OW_MAX_PASSES];    /* pairs that reached the full predicate */
+  int64_t sphere_tests[OW_MAX_PASSES]; /* (cell, face) bounding-sphere prefilter tests */
+  int64_t box_culls[OW_MAX_PASSES];    /* FP64 block-box culls (bin chunks + faces) */
   float stage_ms[OW_MAX_PASSES][4]; /* bin_setup, face_detection, propagation, refinement (CUDA events) */
 } ow_nearwall_result;
 /* The whole level loop in one call: per level L in 0..n_levels-2, bins (binned;

@@ -107,6 +107,8 @@ class NearWallResultC(C.Structure):  # ow_nearwall_result
         ("n_split", C.c_int64 * MAX_PASSES),
         ("tests", C.c_int64 * MAX_PASSES),
         ("evaluated", C.c_int64 * MAX_PASSES),
+        ("sphere_tests", C.c_int64 * MAX_PASSES),
+        ("box_culls", C.c_int64 * MAX_PASSES),
         ("stage_ms", (C.c_float * 4) * MAX_PASSES),
     ]
 

@@ -124,7 +124,7 @@ struct MarkArgs {
   const int64_t* d_n;       // optional device leaf count (n_leaves is then an upper bound)
   float d;
   double reach;
-  unsigned long long* out;  // [0] marked, [1] tests, [2] evaluated
+  unsigned long long* out;  // [0] marked, [1] tests, [2] evaluated, [3] sphere tests, [4] box culls
 };
 
 // Union box of the face boxes of bin-CSR entries [32 g, 32 g + 32) (entries of
@@ -167,6 +167,10 @@ __global__ void k_chunk_boxes(const int32_t* __restrict__ ids, int64_t n_entries
 constexpr int MARK_WARPS = MARK_THREADS / 32;
 constexpr int CG = 4;  // chunks swept inline by the block pass
 
+struct MarkCounts {
+  unsigned long long evaluated = 0, spheres = 0, culls = 0;
+};
+
 struct MarkItems {
   int4* items;                  // (leaf position, chunk, bin, 0)
   unsigned long long* n_items;  // device counter
@@ -174,14 +178,49 @@ struct MarkItems {
   unsigned* hit;                // [n_leaves] block hit words
 };
 
+constexpr int PAIR_CAP = 256;  // sphere-passing (face, cell) pairs buffered per warp
+
 template <int D>
 struct MarkSmem {
   static constexpr int C = D == 3 ? 64 : 16;
-  float p[MARK_WARPS][C][D];
-  int act[MARK_WARPS][C];
   int cand[MARK_WARPS][32 * CG];
   float4 sph[MARK_WARPS][32 * CG];
+  float p[MARK_WARPS][C][D];                  // cell centres of the warp's block
+  unsigned short pair[MARK_WARPS][PAIR_CAP];  // face index << 6 | cell
 };
+
+// cell centres of the lane's cells into the warp's shared table
+template <int D>
+__device__ __forceinline__ void share_cells(MarkSmem<D>& S, int wid, int lane, const float (*p)[3]) {
+  constexpr int C = D == 3 ? 64 : 16;
+  constexpr int CPL = D == 3 ? 2 : 1;
+#pragma unroll
+  for (int k = 0; k < CPL; ++k)
+    if (lane + 32 * k < C)
+#pragma unroll
+      for (int a = 0; a < D; ++a) S.p[wid][lane + 32 * k][a] = p[k][a];
+  __syncwarp();
+}
+
+// full predicate on the buffered pairs, 32 in parallel (their payload loads
+// overlap); true on a hit
+template <int D>
+__device__ __forceinline__ bool eval_pairs(const MarkArgs& A, MarkSmem<D>& S, int wid, int lane, int npairs, float r2) {
+  constexpr int PW = D == 3 ? PAY3 : PAY2;
+  for (int k0 = 0; k0 < npairs; k0 += 32) {
+    bool h = false;
+    if (k0 + lane < npairs) {
+      const unsigned pr = S.pair[wid][k0 + lane];
+      const int c = (int)(pr & 63u);
+      float pp[3];
+#pragma unroll
+      for (int a = 0; a < D; ++a) pp[a] = S.p[wid][c][a];
+      h = near_face<D>(A.pay + (int64_t)S.cand[wid][pr >> 6] * PW, pp, r2);
+    }
+    if (__any_sync(0xffffffffu, h)) return true;
+  }
+  return false;
+}
 
 // cell centres + bins of the lane's cells (c = lane, lane + 32), block box
 template <int D, bool BINNED>
@@ -217,36 +256,18 @@ __device__ __forceinline__ void block_cells(const MarkArgs& A, int id, int lane,
   }
 }
 
-// stage the lane's cells of bin b (all cells for the naive strategy)
-template <int D, bool BINNED>
-__device__ __forceinline__ int stage_cells(MarkSmem<D>& S, int wid, int lane, const float (*p)[3], const int* bin,
-                                           int b) {
-  constexpr int CPL = D == 3 ? 2 : 1;
-  int nact = 0;
-#pragma unroll
-  for (int k = 0; k < CPL; ++k) {
-    const bool act = bin[k] >= 0 && (!BINNED || bin[k] == b);
-    const unsigned m = __ballot_sync(0xffffffffu, act);
-    if (act) {
-      const int c = lane + 32 * k;
-      S.act[wid][nact + __popc(m & lanemask_lt())] = c;
-#pragma unroll
-      for (int a = 0; a < D; ++a) S.p[wid][c][a] = p[k][a];
-    }
-    nact += __popc(m);
-  }
-  __syncwarp();
-  return nact;
-}
-
 // box-cull the entries of up to CG chunks gc[] (of bin range [off, off+cnt)),
-// stage the survivors, sweep (face, cell) pairs; true on a hit
+// stage the survivors, then sweep them face by face: every lane tests its own
+// cells (centres in registers, act = cell lies in this bin) against the
+// broadcast bounding sphere, and runs the full predicate on the survivors.
+// True on a hit (checked after every face: a mark is an OR).
 template <int D, bool BINNED>
 __device__ __forceinline__ bool sweep_chunks(const MarkArgs& A, MarkSmem<D>& S, int wid, int lane, const int64_t* gc,
                                              int64_t off, int64_t cnt, const double* blo, const double* bhi,
-                                             double reach2, float r2, int nact, unsigned magic,
-                                             unsigned long long& evaluated) {
+                                             double reach2, float r2, const float (*p)[3], const bool* act,
+                                             MarkCounts& cn) {
   constexpr int PW = D == 3 ? PAY3 : PAY2;
+  constexpr int CPL = D == 3 ? 2 : 1;
   int fv[CG];
   bool fok[CG];
 #pragma unroll
@@ -257,7 +278,10 @@ __device__ __forceinline__ bool sweep_chunks(const MarkArgs& A, MarkSmem<D>& S, 
   }
 #pragma unroll
   for (int j = 0; j < CG; ++j)
-    if (fok[j]) fok[j] = box_ok<D>(blo, bhi, A.box[2 * (int64_t)fv[j]], A.box[2 * (int64_t)fv[j] + 1], reach2);
+    if (fok[j]) {
+      ++cn.culls;
+      fok[j] = box_ok<D>(blo, bhi, A.box[2 * (int64_t)fv[j]], A.box[2 * (int64_t)fv[j] + 1], reach2);
+    }
   int nf = 0;
 #pragma unroll
   for (int j = 0; j < CG; ++j) {
@@ -271,29 +295,46 @@ __device__ __forceinline__ bool sweep_chunks(const MarkArgs& A, MarkSmem<D>& S, 
   }
   if (!nf) return false;
   __syncwarp();
-  const int total = nf * nact;
-  bool hit = false;
-  for (int k0 = 0; k0 < total && !hit; k0 += 32) {
-    const int k = k0 + lane;
-    bool h = false;
-    if (k < total) {
-      const int fi = (int)__umulhi((unsigned)k, magic);  // k / nact (exact: k < 2^13, nact <= 64)
-      const int ci = S.act[wid][k - fi * nact];
-      float pp[3];
+  // sphere prefilter over (face, own cell) with the sphere broadcast from shared
+  // memory; survivors are buffered and then evaluated 32 at a time
+  int npairs = 0;
+  for (int fi = 0; fi < nf; ++fi) {
+    const float4 sp = S.sph[wid][fi];
 #pragma unroll
-      for (int a = 0; a < D; ++a) pp[a] = S.p[wid][ci][a];
-      if (sphere_ok<D>(pp, S.sph[wid][fi])) {
-        ++evaluated;
-        h = near_face<D>(A.pay + (int64_t)S.cand[wid][fi] * PW, pp, r2);
-      }
+    for (int k = 0; k < CPL; ++k) {
+      const bool pass = act[k] && sphere_ok<D>(p[k], sp);
+      cn.spheres += act[k];
+      const unsigned m = __ballot_sync(0xffffffffu, pass);
+      if (pass) S.pair[wid][npairs + __popc(m & lanemask_lt())] = (unsigned short)((fi << 6) | (lane + 32 * k));
+      npairs += __popc(m);
     }
-    hit = __any_sync(0xffffffffu, h);
+    if (npairs > PAIR_CAP - 64) {  // buffer nearly full: evaluate what we have
+      __syncwarp();
+      cn.evaluated += lane == 0 ? npairs : 0;
+      if (eval_pairs<D>(A, S, wid, lane, npairs, r2)) return true;
+      npairs = 0;
+      __syncwarp();
+    }
   }
+  __syncwarp();
+  cn.evaluated += lane == 0 ? npairs : 0;
+  const bool hit = eval_pairs<D>(A, S, wid, lane, npairs, r2);
   __syncwarp();
   return hit;
 }
 
-__device__ __forceinline__ unsigned div_magic(int n) { return (unsigned)((0x100000000ull + n - 1) / n); }
+__device__ __forceinline__ void flush_counts(const MarkArgs& A, MarkCounts& cn, int lane) {
+  for (int o = 16; o > 0; o >>= 1) {
+    cn.evaluated += __shfl_xor_sync(0xffffffffu, cn.evaluated, o);
+    cn.spheres += __shfl_xor_sync(0xffffffffu, cn.spheres, o);
+    cn.culls += __shfl_xor_sync(0xffffffffu, cn.culls, o);
+  }
+  if (lane == 0) {
+    if (cn.evaluated) atomicAdd(&A.out[2], cn.evaluated);
+    if (cn.spheres) atomicAdd(&A.out[3], cn.spheres);
+    if (cn.culls) atomicAdd(&A.out[4], cn.culls);
+  }
+}
 
 template <int D, bool BINNED>
 __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_blocks(MarkArgs A, MarkItems M) {
@@ -307,6 +348,7 @@ __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_blocks(MarkArgs A, Mar
   float p[CPL][3];
   int bin[CPL];
   block_cells<D, BINNED>(A, id, lane, blo, bhi, p, bin);
+  share_cells<D>(S, wid, lane, p);
   unsigned long long t = 0;
 #pragma unroll
   for (int k = 0; k < CPL; ++k)
@@ -317,7 +359,7 @@ __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_blocks(MarkArgs A, Mar
   if (A.F.marks[id] == OW_MARKED) return;
   const double reach2 = DMUL(A.reach, A.reach);
   const float r2 = FMUL(A.d, A.d);
-  unsigned long long evaluated = 0;
+  MarkCounts cn;
   bool pend[CPL];
 #pragma unroll
   for (int k = 0; k < CPL; ++k) pend[k] = bin[k] >= 0;
@@ -339,13 +381,17 @@ __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_blocks(MarkArgs A, Mar
     const int64_t off = BINNED ? A.bin_offsets[b] : 0;
     const int64_t cnt = BINNED ? A.bin_counts[b] : A.n_faces;
     if (cnt == 0) continue;
-    int nact = -1;
-    unsigned magic = 0;
+    bool act[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) act[k] = bin[k] >= 0 && (!BINNED || bin[k] == b);
     const int64_t g0 = off >> 5, g1 = (off + cnt - 1) >> 5;
     for (int64_t gb = g0; gb <= g1 && !hit; gb += 32) {
       const int64_t g = gb + lane;
       bool cok = false;
-      if (g <= g1) cok = box_ok<D>(blo, bhi, A.cbox[2 * g], A.cbox[2 * g + 1], reach2);
+      if (g <= g1) {
+        ++cn.culls;
+        cok = box_ok<D>(blo, bhi, A.cbox[2 * g], A.cbox[2 * g + 1], reach2);
+      }
       unsigned cm = __ballot_sync(0xffffffffu, cok);
       if (cm && inline_left) {
         inline_left = false;
@@ -358,11 +404,7 @@ __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_blocks(MarkArgs A, Mar
             cm &= cm - 1;
           }
         }
-        if (nact < 0) {
-          nact = stage_cells<D, BINNED>(S, wid, lane, p, bin, b);
-          magic = div_magic(nact);
-        }
-        hit = sweep_chunks<D, BINNED>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, nact, magic, evaluated);
+        hit = sweep_chunks<D, BINNED>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, p, act, cn);
         if (hit) break;
       }
       if (cm) {  // the rest: (block, chunk, bin) items for the flat pass
@@ -373,10 +415,6 @@ __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_blocks(MarkArgs A, Mar
           if ((cm >> lane) & 1u) M.items[base + __popc(cm & lanemask_lt())] = make_int4((int)pos, (int)(gb + lane), b, 0);
         } else {
           // item list full: this warp sweeps its remaining chunks itself
-          if (nact < 0) {
-            nact = stage_cells<D, BINNED>(S, wid, lane, p, bin, b);
-            magic = div_magic(nact);
-          }
           while (cm && !hit) {
             int64_t gc[CG];
 #pragma unroll
@@ -387,16 +425,14 @@ __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_blocks(MarkArgs A, Mar
                 cm &= cm - 1;
               }
             }
-            hit = sweep_chunks<D, BINNED>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, nact, magic,
-                                          evaluated);
+            hit = sweep_chunks<D, BINNED>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, p, act, cn);
           }
         }
       }
     }
   }
-  for (int o = 16; o > 0; o >>= 1) evaluated += __shfl_xor_sync(0xffffffffu, evaluated, o);
+  flush_counts(A, cn, lane);
   if (lane == 0) {
-    if (evaluated) atomicAdd(&A.out[2], evaluated);
     if (hit && atomicOr(&M.hit[pos], 1u) == 0u) {
       A.F.marks[id] = OW_MARKED;
       atomicAdd(&A.out[0], 1ull);
@@ -412,7 +448,8 @@ __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_items(MarkArgs A, Mark
   const int64_t n = min((int64_t)*M.n_items, M.cap);  // items past cap were swept by their block warp
   const double reach2 = DMUL(A.reach, A.reach);
   const float r2 = FMUL(A.d, A.d);
-  unsigned long long evaluated = 0, marked = 0;
+  MarkCounts cn;
+  unsigned long long marked = 0;
   for (int64_t it = (int64_t)blockIdx.x * MARK_WARPS + wid; it < n; it += (int64_t)gridDim.x * MARK_WARPS) {
     const int4 item = M.items[it];
     const int pos = item.x;
@@ -423,24 +460,24 @@ __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_items(MarkArgs A, Mark
     float p[CPL][3];
     int bin[CPL];
     block_cells<D, BINNED>(A, id, lane, blo, bhi, p, bin);
-    const int nact = stage_cells<D, BINNED>(S, wid, lane, p, bin, b);
+    share_cells<D>(S, wid, lane, p);
+    bool act[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) act[k] = bin[k] >= 0 && (!BINNED || bin[k] == b);
     const int64_t off = BINNED ? A.bin_offsets[b] : 0;
     const int64_t cnt = BINNED ? A.bin_counts[b] : A.n_faces;
     int64_t gc[CG];
 #pragma unroll
     for (int j = 0; j < CG; ++j) gc[j] = j == 0 ? (int64_t)item.y : -1;
     const bool hit =
-        sweep_chunks<D, BINNED>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, nact, div_magic(nact), evaluated);
+        sweep_chunks<D, BINNED>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, p, act, cn);
     if (hit && lane == 0 && atomicOr(&M.hit[pos], 1u) == 0u) {
       A.F.marks[id] = OW_MARKED;
       ++marked;
     }
   }
-  for (int o = 16; o > 0; o >>= 1) evaluated += __shfl_xor_sync(0xffffffffu, evaluated, o);
-  if (lane == 0) {
-    if (evaluated) atomicAdd(&A.out[2], evaluated);
-    if (marked) atomicAdd(&A.out[0], marked);
-  }
+  flush_counts(A, cn, lane);
+  if (lane == 0 && marked) atomicAdd(&A.out[0], marked);
 }
 
 // ---------------------------------------------------------------------------
@@ -648,10 +685,10 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   M.cap = cap;
   M.hit = (unsigned*)ph;
   OW_CUDA(cudaMemsetAsync(ph, 0, 4 * (size_t)(n_leaves + (n_leaves & 1)) + 8, s));
-  OW_PROF_BEGIN(ctx, PROF_MARK, s);
   const int cg = ow_blocks((n_entries + 31) / 32, 128);
   if (f->dim == 3) k_chunk_boxes<3><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
   else k_chunk_boxes<2><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
+  OW_PROF_BEGIN(ctx, PROF_MARK, s);
   dim3 grd((unsigned)((n_leaves + MARK_WARPS - 1) / MARK_WARPS));
   const int gi = 8 * OW_SMS;
   if (f->dim == 3) {
@@ -684,7 +721,7 @@ extern "C" int ow_mark_near_wall(ow_ctx* ctx, ow_forest* f, const int32_t* d_lea
                                  int64_t* out_tests, int64_t* out_evaluated, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   unsigned long long* out = (unsigned long long*)(ctx->d_small + 16);
-  OW_CUDA(cudaMemsetAsync(out, 0, 3 * 8, s));
+  OW_CUDA(cudaMemsetAsync(out, 0, 5 * 8, s));
   OW_TRY(ow_mark_launch(ctx, f, d_leaves, n_leaves, d_coords, n_faces, geom_key, grid, d_bin_ids, d_bin_counts,
                         d_bin_offsets, n_bin_entries, d_spec, reach, out, s));
   int64_t h[3];

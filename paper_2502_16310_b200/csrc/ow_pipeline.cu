@@ -104,9 +104,9 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
   int64_t E = 0;
   const int passes = p->n_levels - 1;
   void *stats, *drv;
-  OW_TRY(ow_slot(ctx, SLOT_DRV_STATS, 24 * (size_t)passes, s, &stats));
+  OW_TRY(ow_slot(ctx, SLOT_DRV_STATS, 40 * (size_t)passes, s, &stats));
   OW_TRY(ow_slot(ctx, SLOT_DRV_STATE, 8 * 72 * (size_t)passes, s, &drv));
-  OW_CUDA(cudaMemsetAsync(stats, 0, 24 * (size_t)passes, s));
+  OW_CUDA(cudaMemsetAsync(stats, 0, 40 * (size_t)passes, s));
   for (int level = 0; level < passes; ++level) {
     // ---- bin_setup
     OW_TRY(record(se, level, 0, s));
@@ -146,7 +146,7 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
     OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(n_host + 1), s, &pl));
     int64_t* dn = (int64_t*)drv + 72 * level;  // [0] leaves at level, [8..72) refine state
     int64_t* rs = dn + 8;
-    unsigned long long* dst = (unsigned long long*)stats + 3 * level;
+    unsigned long long* dst = (unsigned long long*)stats + 5 * level;
     if (p->world > 1) {
       // sharded marking: each rank marks a contiguous slice, then the exchange
       // callback all-gathers the marks (the slice needs the leaf count on the host)
@@ -225,12 +225,14 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
     out->n_passes = level + 1;
   }
   if (passes > 0) {
-    int64_t h[3 * OW_MAX_PASSES];
-    OW_TRY(ow_readback(ctx, (const int64_t*)stats, 3 * passes, h, s));
+    int64_t h[5 * OW_MAX_PASSES];
+    OW_TRY(ow_readback(ctx, (const int64_t*)stats, 5 * passes, h, s));
     for (int level = 0; level < out->n_passes; ++level) {
-      out->marked_detected[level] = h[3 * level];
-      out->tests[level] = h[3 * level + 1];
-      out->evaluated[level] = h[3 * level + 2];
+      out->marked_detected[level] = h[5 * level];
+      out->tests[level] = h[5 * level + 1];
+      out->evaluated[level] = h[5 * level + 2];
+      out->sphere_tests[level] = h[5 * level + 3];
+      out->box_culls[level] = h[5 * level + 4];
     }
   }
   if (!ctx->defer_stage_times) return ow_stage_times(ctx, out);

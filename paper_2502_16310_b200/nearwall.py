@@ -167,6 +167,8 @@ class NearWallResult:
     grid: BinGrid | None = None
     cell_face_tests: list = field(default_factory=list)  # T per marking pass
     pairs_evaluated: list = field(default_factory=list)
+    sphere_tests: list = field(default_factory=list)  # bounding-sphere prefilter tests per pass
+    box_culls: list = field(default_factory=list)  # FP64 block-box culls per pass
 
     @property
     def total_marked(self):
@@ -267,6 +269,8 @@ def _driver_result(forest, params, st, out) -> NearWallResult:
     result.marked_refined = list(out.marked_refined[:n])
     result.cell_face_tests = list(out.tests[:n])
     result.pairs_evaluated = list(out.evaluated[:n])
+    result.sphere_tests = list(out.sphere_tests[:n])
+    result.box_culls = list(out.box_culls[:n])
     if binned:
         e = int(out.bin_entries)
         ids, counts, offsets = st["bins_t"]
