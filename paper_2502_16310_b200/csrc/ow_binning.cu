@@ -339,6 +339,10 @@ __global__ void k_emit_slow(GridC g, const float* __restrict__ c, int64_t n, con
   }
 }
 
+__global__ void k_small_init(int64_t* small) {
+  if (threadIdx.x < 8) small[threadIdx.x] = (threadIdx.x == 1 || threadIdx.x == 3) ? -1 : 0;
+}
+
 template <int D>
 int fill_count(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, int32_t* counts, int64_t n_bins,
                int64_t* out_entries, int64_t* out_outside, cudaStream_t s) {
@@ -349,18 +353,22 @@ int fill_count(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, 
   OW_TRY(ow_slot(ctx, SLOT_BIN_SLOW, 4 * (size_t)n, s, &psl));
   int64_t* small = ctx->d_small;
   OW_CUDA(cudaMemsetAsync(counts, 0, 4 * (size_t)n_bins, s));
-  OW_CUDA(cudaMemsetAsync(small, 0, 8 * 8, s));
-  OW_CUDA(cudaMemsetAsync(small + 1, 0xff, 8, s));
-  OW_CUDA(cudaMemsetAsync(small + 3, 0xff, 8, s));
+  k_small_init<<<1, 32, 0, s>>>(small);  // [1], [3] = -1 (none), rest 0
+  OW_LAUNCHED(ctx);
   k_count_fast<D><<<ow_blocks(n, 256), 256, 0, s>>>(g, c, n, h, (unsigned long long*)pm, (int32_t*)pnb, counts,
                                                    (int32_t*)psl, small);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
-  int64_t hs[1];
-  OW_TRY(ow_readback(ctx, small, 1, hs, s));
-  int64_t n_slow = hs[0];
+  // face offsets over the fast path's counts, read back with the slow-face
+  // count in one round trip; faces with too many bins for the bitmask path
+  // (rare: large faces) add a second pass and a re-scan
+  OW_TRY(scan(ctx, ow::LoadArr<int32_t>{(const int32_t*)pnb}, ow::StoreExcl<int32_t>{(int32_t*)pfo}, n, small + 5, s));
+  int64_t r[6];
+  OW_TRY(ow_readback(ctx, small, 6, r, s));
+  int64_t n_slow = r[0];
   ctx->bins_slow = n_slow;
   if (n_slow > 0) {
+    int64_t hs[1];
     void* po;
     OW_TRY(ow_slot(ctx, SLOT_BIN_SLOWOFF, 8 * (size_t)n_slow, s, &po));
     OW_TRY(scan(ctx, SlowVolLoad<D>{g, c, n, (const int32_t*)psl}, ow::StoreExcl<int64_t>{(int64_t*)po}, n_slow,
@@ -372,10 +380,10 @@ int fill_count(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, 
                                                      (unsigned*)pb, (int32_t*)pnb, counts, small);
     OW_LAUNCHED(ctx);
     OW_CHECK_LAUNCH();
+    OW_TRY(scan(ctx, ow::LoadArr<int32_t>{(const int32_t*)pnb}, ow::StoreExcl<int32_t>{(int32_t*)pfo}, n, small + 5,
+                s));
+    OW_TRY(ow_readback(ctx, small, 6, r, s));
   }
-  OW_TRY(scan(ctx, ow::LoadArr<int32_t>{(const int32_t*)pnb}, ow::StoreExcl<int32_t>{(int32_t*)pfo}, n, small + 5, s));
-  int64_t r[6];
-  OW_TRY(ow_readback(ctx, small, 6, r, s));
   if (r[2]) {
     ow_set_error("fill_bins: a face sample escaped its padded bin range (internal)");
     return OW_ERR_INTERNAL;

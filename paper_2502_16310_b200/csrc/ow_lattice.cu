@@ -36,6 +36,8 @@ constexpr int QMAX = 27;
 constexpr int MT_THREADS = 256;
 constexpr int MT_ITEMS = 2;
 constexpr int MT_TILE = MT_THREADS * MT_ITEMS;
+constexpr int RU_ROW_BITS = 28;  // rows per pass < 2^28, units < 2^36
+constexpr unsigned long long RU_ROW_MASK = (1ull << RU_ROW_BITS) - 1;
 
 // row record: x = leaf position, y = face,
 // z = dir | (i0_a | (ext_a-1) << 2) << (5 + 4a), w = units of the row
@@ -61,8 +63,7 @@ struct LatArgs {
   int64_t* rowoff;          // [R] units per row -> exclusive unit offsets
   int32_t* tile_row;        // [n_tiles] row of the first unit of each MT tile
   int64_t row_cap, unit_cap;
-  unsigned long long* n_rows_d;   // device row counter (may exceed row_cap: overflow)
-  const int64_t* n_units_d;       // device unit total
+  unsigned long long* ru_d;       // device (units << RU_ROW_BITS | rows) counter (may exceed the caps)
   int32_t* cand_rank;       // [n_leaves]
   int32_t* cand_blocks;     // [n_cb]
   int64_t n_cb;
@@ -237,18 +238,35 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
         if (nrow) A.has_pair[pos] = 1;
       }
     }
-    int incl = nrow;
+    // units of this lane's rows
+    unsigned long long nunit = 0;
+    for (unsigned vv = valid; vv; vv &= vv - 1) {
+      int units = 1, cc = __ffs(vv) - 1;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        units *= (int)((R[a] >> (4 * (cc % 3) + 2)) & 3u) + 1;
+        cc /= 3;
+      }
+      nunit += units;
+    }
+    // one 64-bit atomic reserves both the rows and their units (rows in the low
+    // RU_ROW_BITS bits): row order and unit order agree, so the unit offsets are
+    // monotone in the row index without a scan
+    const unsigned long long mine = (nunit << RU_ROW_BITS) | (unsigned long long)nrow;
+    unsigned long long incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
     }
-    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    const unsigned long long tot = __shfl_sync(0xffffffffu, incl, 31);
     if (!tot) continue;
     unsigned long long base = 0;
-    if (lane == 31) base = atomicAdd(A.n_rows_d, (unsigned long long)tot);
+    if (lane == 31) base = atomicAdd(A.ru_d, tot);
     base = __shfl_sync(0xffffffffu, base, 31);
-    int64_t k = (int64_t)base + incl - nrow;
+    const unsigned long long start = base + incl - mine;
+    int64_t k = (int64_t)(start & RU_ROW_MASK);
+    int64_t u = (int64_t)(start >> RU_ROW_BITS);
     while (valid) {
       const int ci = __ffs(valid) - 1;
       valid &= valid - 1;
@@ -261,11 +279,13 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
         w |= ra << (5 + 4 * a);
         units *= (int)(ra >> 2) + 1;
       }
-      if (k < A.row_cap) {
+      if (k < A.row_cap && u + units <= A.unit_cap) {
         A.rows[k] = make_int4(pos, (int)f, (int)w, units);
-        A.rowoff[k] = units;
+        A.rowoff[k] = u;
+        for (int64_t t = (u + MT_TILE - 1) / MT_TILE; t * MT_TILE < u + units; ++t) A.tile_row[t] = (int32_t)k;
       }
       ++k;
+      u += units;
     }
   }
 }
@@ -286,26 +306,6 @@ struct CandStore {
 
 // scans bounded by a device-side count (rows / candidate blocks are counted
 // on the device; the launch covers the host-known capacity)
-struct RowUnitsLoad {
-  const int64_t* units;
-  const unsigned long long* n;
-  int64_t cap;
-  __device__ int64_t operator()(int64_t i) const { return i < min((int64_t)*n, cap) ? units[i] : 0; }
-};
-// rowoff[i] = exclusive unit offset (in place over the unit counts); the row
-// holding the first unit of each MT tile is recorded on the fly
-struct RowCntStore {
-  int64_t* off;
-  int32_t* tile_row;
-  const unsigned long long* n;
-  int64_t row_cap, unit_cap;
-  __device__ void operator()(int64_t i, int64_t e, int64_t v) const {
-    if (i >= min((int64_t)*n, row_cap)) return;
-    off[i] = e;
-    for (int64_t t = (e + MT_TILE - 1) / MT_TILE; t * MT_TILE < e + v && t * MT_TILE < unit_cap; ++t)
-      tile_row[t] = (int32_t)i;
-  }
-};
 struct BcountLoad {
   const int32_t* c;
   const int64_t* n;
@@ -354,8 +354,9 @@ __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
   __shared__ int s_nh;
   for (int i = threadIdx.x; i < QMAX * 3; i += MT_THREADS) s_dv[i / 3][i % 3] = A.dv[i / 3][i % 3];
   if (threadIdx.x == 0) s_nh = 0;
-  const int64_t U = *A.n_units_d;
-  const int64_t R = (int64_t)*A.n_rows_d;
+  const unsigned long long ru = *A.ru_d;
+  const int64_t U = (int64_t)(ru >> RU_ROW_BITS);
+  const int64_t R = (int64_t)(ru & RU_ROW_MASK);
   if (R > A.row_cap || U > A.unit_cap) return;  // overflow: the host re-runs with room
   const int64_t n_tiles = (U + MT_TILE - 1) / MT_TILE;
   const int lane = threadIdx.x & 31;
@@ -520,8 +521,9 @@ __global__ void k_lat_emit(LatArgs A) {
 template <int D>
 __global__ void k_lat_hits(LatArgs A) {
   constexpr int C = D == 3 ? 64 : 16;
-  const int64_t U = *A.n_units_d;
-  if ((int64_t)*A.n_rows_d > A.row_cap || U > A.unit_cap) return;
+  const unsigned long long ru = *A.ru_d;
+  const int64_t U = (int64_t)(ru >> RU_ROW_BITS);
+  if ((int64_t)(ru & RU_ROW_MASK) > A.row_cap || U > A.unit_cap) return;
   const int64_t n_tiles = (U + MT_TILE - 1) / MT_TILE;
   const int lane = threadIdx.x & 31;
   for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_tiles;
@@ -585,8 +587,7 @@ LatArgs make_args(ow_ctx* ctx) {
   A.tile_row = (int32_t*)ctx->slot_ptr[SLOT_LAT_TILEROW];
   A.row_cap = ctx->lat_row_cap;
   A.unit_cap = ctx->lat_unit_cap;
-  A.n_rows_d = (unsigned long long*)(ctx->d_small + 48);
-  A.n_units_d = ctx->d_small + 49;
+  A.ru_d = (unsigned long long*)(ctx->d_small + 48);
   A.cand_rank = (int32_t*)ctx->slot_ptr[SLOT_LAT_RANK];
   A.cand_blocks = (int32_t*)ctx->slot_ptr[SLOT_LAT_LEAVES];
   A.n_cb = ctx->lat_ncb;
@@ -675,8 +676,6 @@ extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, int32_t l
   ctx->launches += 2;
   OW_CHECK_LAUNCH();
   OW_TRY(scan(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s));
-  OW_TRY(scan(ctx, RowUnitsLoad{A.rowoff, A.n_rows_d, rcap}, RowCntStore{A.rowoff, A.tile_row, A.n_rows_d, rcap, ucap},
-              rcap, ctx->d_small + 49, s));
   OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
   const int64_t tiles_max = ucap / MT_TILE + 1;
   if (D == 3) k_lat_mt<3><<<ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s>>>(A);
@@ -691,7 +690,12 @@ extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, int32_t l
   // single readback: candidate blocks, (scan scratch), boundary cells, rows, units
   int64_t h[17];
   OW_TRY(ow_readback(ctx, ctx->d_small + 33, 17, h, s));
-  const int64_t n_cb = h[0], nb = h[2], n_rows = h[15], n_units = h[16];
+  const int64_t n_cb = h[0], nb = h[2];
+  const int64_t n_rows = (int64_t)((uint64_t)h[15] & RU_ROW_MASK), n_units = (int64_t)((uint64_t)h[15] >> RU_ROW_BITS);
+  if (n_rows >= (int64_t(1) << RU_ROW_BITS) - (int64_t(1) << 20)) {
+    ow_set_error("lattice: %lld (block, face, direction) rows exceed one pass", (long long)n_rows);
+    return OW_ERR_CAPACITY;
+  }
   if (n_rows > rcap || n_units > ucap) {
     ctx->lat_row_cap = n_rows + n_rows / 4 + 1024;
     ctx->lat_unit_cap = n_units + n_units / 4 + 4096;

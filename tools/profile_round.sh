@@ -15,7 +15,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
 python tools/launch_summary.py $OUT/${TAG}_launches.csv > $OUT/${TAG}_launches.txt 2>&1
 # one full capture of each hot kernel of the last warm step (bench --steps 1 --warmup 1)
 ncu --set full --clock-control none --import-source on \
-    -k "regex:k_lat_mt|k_lat_faces|k_lat_emit|k_mark|k_chunk_boxes|k_count_fast|k_radix_scatter|k_radix_hist|k_emit_fast|k_stl_to_soa|k_prop_gather|k_scan" \
+    -k "regex:k_lat_mt|k_lat_faces|k_lat_emit|k_lat_hits|k_mark_blocks|k_mark_items|k_chunk_boxes|k_count_fast|k_radix_scatter|k_radix_hist|k_emit_fast|k_stl_to_soa|k_prop_gather_dev|k_split_ring|k_violators_dev" \
     --launch-skip 0 --launch-count 40 -f -o $OUT/${TAG}_full \
     python bench.py --config $CFG --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $OUT/${TAG}_ncu.log 2>&1
 ncu -i $OUT/${TAG}_full.ncu-rep --page raw --csv \
