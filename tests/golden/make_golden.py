@@ -180,6 +180,7 @@ GEOMS = {
     "cube_inset": lambda: tris_geometry(cube_triangles(0.2, 0.8)),
     "icosphere5": lambda: stl_geometry(shapes.icosphere_triangles(5)),
     "icosphere3": lambda: stl_geometry(shapes.icosphere_triangles(3)),
+    "bumpy70k": lambda: stl_geometry(shapes.bumpy_sphere_triangles()),
 }
 
 _geom_cache = {}
@@ -344,6 +345,45 @@ def gen_pipelines():
               f"refined {res.marked_refined} ({dt:.1f}s)")
 
 
+BIG_PIPE_CASES = [
+    # C3 of BASELINE.json at full size: bunny-scale bumpy lat-lon sphere (69 936 triangles) as
+    # binary STL, 16^3 root, d = 0.05, 4 levels, B = 8.  Arrays are too large to commit, so the
+    # fixture holds SHA-256 digests of the forest arrays and the bin CSR plus the counts.
+    ("bumpy70k", 16, 0.05, 4, "binned", 8),
+]
+
+
+def gen_bigpipes():
+    for gname, root, d, levels, strategy, b in BIG_PIPE_CASES:
+        g = geom(gname)
+        dom = domain_for(g.dim)
+        f = ow.init_root_grid(dom, (root,) * g.dim)
+        params = ow.NearWallParams(d_spec=d, n_levels=levels, strategy=strategy, bins_per_axis=b,
+                                   backend="parallel")
+        t0 = time.perf_counter()
+        res = ow.refine_near_wall(f, g, params)
+        dt = time.perf_counter() - t0
+        n = f.n_blocks
+        tag = f"bigpipe_{gname}_r{root}_d{d}_L{levels}_{strategy}_B{b}"
+        save(tag, geom_name=np.array(gname), geom_sha=np.array(sha(g.coords)), root=np.int64(root),
+             d_spec=np.float64(d), n_levels=np.int64(levels), strategy=np.array(strategy),
+             bins_per_axis=np.int64(b), n_blocks=np.int64(n),
+             marked_detected=np.asarray(res.marked_detected, np.int64),
+             marked_refined=np.asarray(res.marked_refined, np.int64),
+             blocks_per_level=np.asarray(f.blocks_per_level(), np.int64),
+             leaves_per_level=np.asarray(f.leaves_per_level(), np.int64),
+             sha_level=np.array(sha(f._level[:n].astype(np.int16))),
+             sha_coords=np.array(sha(f._coords[:n].astype(np.int64))),
+             sha_parent=np.array(sha(f._parent[:n].astype(np.int32))),
+             sha_first_child=np.array(sha(f._first_child[:n].astype(np.int32))),
+             sha_marks=np.array(sha(f.marks[:n].astype(np.int8))),
+             sha_bin_ids=np.array(sha(res.bins.ids.astype(np.int32))),
+             sha_bin_counts=np.array(sha(res.bins.counts.astype(np.int32))),
+             n_bin_entries=np.int64(res.bins.ids.size))
+        print(f"{tag}: blocks {f.blocks_per_level()} detect {res.marked_detected} "
+              f"refined {res.marked_refined} E={res.bins.ids.size} ({dt:.1f}s)")
+
+
 def gen_forest_units():
     """Propagation / refinement known answers beyond the reference's own asserts."""
     out = {}
@@ -428,6 +468,7 @@ GROUPS = {
     "pipelines": gen_pipelines,
     "forest": gen_forest_units,
     "links": gen_links,
+    "bigpipes": gen_bigpipes,
 }
 
 
