@@ -155,7 +155,7 @@ def gpu_arm(args, cfg, rank, world, local_rank):
             geom = ow.index_to_coords(ig) if text else ow.geometry.stl_records_to_coords(records, n_faces)
             forest = ow.init_root_grid(dom, (cfg["root"],) * dim, capacity=32 * cfg["root"] ** dim)
             res = ow.refine_near_wall(forest, geom, params, shard=shard)
-            ll = ow.build_lattice_links(forest, geom, None, cfg["lattice"])
+            ll = ow.build_lattice_links(forest, geom, None, cfg["lattice"], shard=shard)
             return res, forest, ll
         # fused native pass: STL records in HBM -> grid -> lattice links (ow_geometry_to_grid)
         gp = plan.run(records, n_faces)
@@ -305,7 +305,8 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         "config": {"workload": cfg["workload"], "faces": n_faces, "cell_face_tests_per_step": T_step,
                    "pairs_evaluated_per_step": evaluated, "blocks_per_level": blocks,
                    "boundary_cells": n_boundary, "l2": "flushed (256 MB write) before every step",
-                   "parallelism": f"octree-block shards x{world}, NCCL all-gather of marks"},
+                   "parallelism": f"octree-block shards x{world}: marking and lattice links per rank slice, NCCL "
+                                  f"all-gather of marks and of boundary links; bins/forest replicated"},
         "roofline": roofline,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

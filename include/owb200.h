@@ -274,6 +274,13 @@ int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const
                            int64_t n_leaves, const float* d_coords, int64_t n_faces, int64_t geom_key,
                            const ow_grid* grid, const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags,
                            int64_t* out_boundary, void* stream);
+/* Same, for the leaf positions [pos_lo, pos_hi) only (multi-GPU slice): the
+ * flags of other positions stay 0 and only this slice's boundary rows are
+ * emitted; ranks all-gather the slices (parallel.Shard). */
+int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_leaves,
+                                 int64_t n_leaves, int64_t pos_lo, int64_t pos_hi, const float* d_coords,
+                                 int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int8_t* h_dirs,
+                                 int32_t n_dirs, uint32_t* d_flags, int64_t* out_boundary, void* stream);
 int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, void* stream);
 /* Work counters of the last ow_lattice_links_count: [0] candidate blocks,
  * [1] (block, face, direction) rows, [2] Moller-Trumbore / segment tests. */

@@ -175,6 +175,8 @@ _SIGS = {
                                  I64, PI64, PI64, P],
     "ow_cell_face_links_emit": [P, P, P, P, P, P],
     "ow_lattice_links_count": [P, C.POINTER(ForestView), I32, P, I64, P, I64, I64, C.POINTER(Grid), P, I32, P, PI64, P],
+    "ow_lattice_links_count_range": [P, C.POINTER(ForestView), I32, P, I64, I64, I64, P, I64, I64, C.POINTER(Grid), P,
+                                     I32, P, PI64, P],
     "ow_lattice_links_emit": [P, P, P, P],
     "ow_lattice_stats": [P, PI64, P],
     "ow_near_pairs": [P, I32, P, P, P, I64, P, P],

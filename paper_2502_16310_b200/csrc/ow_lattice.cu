@@ -55,6 +55,7 @@ struct LatArgs {
   const int32_t* leaves;
   int64_t n_leaves;
   int32_t* pos_of;          // [n_blocks]
+  int64_t pos_lo, pos_hi;   // leaf positions this call owns (multi-GPU slice)
   float* cen;               // [n_leaves][D][4] cell-centre coordinates
   uint8_t* has_pair;        // [n_leaves]
   float4* rec;              // [n_faces * 3] (v0, e1, e2) / (a, s)
@@ -224,7 +225,9 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
       }
       int depth;
       const int node = locate(A.F, L, nc, &depth);
-      if (depth == L && A.F.first_child[node] < 0) {
+      // (leaves outside this call's position slice belong to another rank; no
+      // early `continue` here: the whole warp must reach the row-reservation scan)
+      if (depth == L && A.F.first_child[node] < 0 && A.pos_of[node] >= A.pos_lo && A.pos_of[node] < A.pos_hi) {
         pos = A.pos_of[node];
 #pragma unroll
         for (int a = 0; a < D; ++a)
@@ -578,6 +581,8 @@ LatArgs make_args(ow_ctx* ctx) {
   A.n_faces = ctx->lat_faces;
   A.leaves = ctx->lat_leaves_ptr;
   A.n_leaves = ctx->lat_leaves;
+  A.pos_lo = ctx->lat_pos_lo;
+  A.pos_hi = ctx->lat_pos_hi;
   A.pos_of = (int32_t*)ctx->slot_ptr[SLOT_LAT_POS];
   A.cen = (float*)ctx->slot_ptr[SLOT_LAT_CEN];
   A.has_pair = (uint8_t*)ctx->slot_ptr[SLOT_LAT_HAS];
@@ -608,7 +613,23 @@ extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, int32_t l
                                       int64_t n_leaves, const float* d_coords, int64_t n_faces, int64_t geom_key,
                                       const ow_grid* grid, const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags,
                                       int64_t* out_boundary, void* stream) {
+  return ow_lattice_links_count_range(ctx, f, level, d_leaves, n_leaves, 0, n_leaves, d_coords, n_faces, geom_key,
+                                      grid, h_dirs, n_dirs, d_flags, out_boundary, stream);
+}
+
+extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_leaves,
+                                            int64_t n_leaves, int64_t pos_lo, int64_t pos_hi, const float* d_coords,
+                                            int64_t n_faces, int64_t geom_key, const ow_grid* grid,
+                                            const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags,
+                                            int64_t* out_boundary, void* stream) {
   (void)geom_key;
+  if (pos_lo < 0 || pos_hi > n_leaves || pos_lo > pos_hi) {
+    ow_set_error("lattice: leaf range [%lld, %lld) outside [0, %lld)", (long long)pos_lo, (long long)pos_hi,
+                 (long long)n_leaves);
+    return OW_ERR_INVALID;
+  }
+  ctx->lat_pos_lo = pos_lo;
+  ctx->lat_pos_hi = pos_hi;
   cudaStream_t s = (cudaStream_t)stream;
   if (n_dirs < 2 || n_dirs > QMAX || (grid && grid->dim != f->dim) || level < 0 || level >= 28) {
     ow_set_error("lattice: bad direction set, grid or level");
@@ -703,8 +724,8 @@ extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, int32_t l
       ow_set_error("lattice: %lld link-face tests exceed one pass (2^31)", (long long)n_units);
       return OW_ERR_CAPACITY;
     }
-    return ow_lattice_links_count(ctx, f, level, d_leaves, n_leaves, d_coords, n_faces, geom_key, grid, h_dirs,
-                                  n_dirs, d_flags, out_boundary, stream);
+    return ow_lattice_links_count_range(ctx, f, level, d_leaves, n_leaves, pos_lo, pos_hi, d_coords, n_faces,
+                                        geom_key, grid, h_dirs, n_dirs, d_flags, out_boundary, stream);
   }
   ctx->lat_ncb = n_cb;
   ctx->lat_rows = n_rows;

@@ -71,7 +71,7 @@ class LatticeLinks:
 
 
 def build_lattice_links(forest: Forest, geom: CoordListGeometry, grid: BinGrid | None = None,
-                        lattice="D3Q19") -> LatticeLinks:
+                        lattice="D3Q19", shard=None) -> LatticeLinks:
     """Boundary links of the finest level.
 
     Candidate faces come from the forest itself (each face visits the finest
@@ -94,7 +94,13 @@ def build_lattice_links(forest: Forest, geom: CoordListGeometry, grid: BinGrid |
     nb = C.c_int64(0)
     hd = np.ascontiguousarray(dirs.reshape(-1))
     ctx, st = _lib.ctx(), _lib.stream()
-    _lib.call("ow_lattice_links_count", ctx, C.byref(forest.view()), level, _lib.ptr(leaves), n_leaves,
+    lo, hi = 0, n_leaves
+    sharded = shard is not None and shard.world > 1
+    if sharded:  # this rank's contiguous slice of the finest leaves (parallel.partition)
+        from .parallel import partition
+
+        lo, hi = partition(n_leaves, shard.rank, shard.world)
+    _lib.call("ow_lattice_links_count_range", ctx, C.byref(forest.view()), level, _lib.ptr(leaves), n_leaves, lo, hi,
               _lib.ptr(geom.coords), geom.n_faces, geom.key, None,
               hd.ctypes.data_as(C.c_void_p), len(dirs),
               _lib.ptr(flags), C.byref(nb), st)
@@ -102,4 +108,6 @@ def build_lattice_links(forest: Forest, geom: CoordListGeometry, grid: BinGrid |
     cells = torch.empty(n_b, dtype=torch.int64, device=dev)
     q = torch.empty((n_b, len(dirs)), dtype=torch.float32, device=dev)
     _lib.call("ow_lattice_links_emit", ctx, _lib.ptr(cells), _lib.ptr(q), st)
+    if sharded:
+        flags, cells, q = shard.gather_links(flags, cells, q, lo, hi, ncell, n_leaves)
     return LatticeLinks(lattice=lattice, level=level, leaves=leaves.to(torch.int64), flags=flags, cells=cells, q=q)

@@ -49,7 +49,7 @@ def gather_slices(local, n, world, group=None):
     slices are staged through host memory."""
     if local.is_cuda and dist.get_backend(group) == "gloo":
         return gather_slices(local.cpu(), n, world, group).to(local.device)
-    per = (n + world - 1) // world if world > 1 else n
+    per = 0 if n is None else ((n + world - 1) // world if world > 1 else n)
     dev = local.device
     counts = torch.tensor([local.numel()], dtype=torch.int64, device=dev)
     all_counts = [torch.zeros_like(counts) for _ in range(world)]
@@ -62,7 +62,7 @@ def gather_slices(local, n, world, group=None):
     dist.all_gather_into_tensor(out, buf, group=group)
     parts = [out[r * m: r * m + sizes[r]] for r in range(world)]
     res = torch.cat(parts)
-    assert res.numel() == n, (res.numel(), n)
+    assert n is None or res.numel() == n, (res.numel(), n)
     return res
 
 
@@ -73,6 +73,16 @@ class Shard:
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+
+    def gather_links(self, flags, cells, q, lo, hi, ncell, n_leaves):
+        """All-gather the lattice results of every rank's leaf slice: flag words
+        of leaves [lo, hi) and the slice's boundary rows (ascending, so the
+        rank-order concatenation is the single-GPU order)."""
+        nq = q.shape[1] if q.dim() == 2 else 0
+        allf = gather_slices(flags[lo * ncell: hi * ncell].contiguous(), n_leaves * ncell, self.world, self.group)
+        allc = gather_slices(cells, None, self.world, self.group)
+        allq = gather_slices(q.reshape(-1), None, self.world, self.group).view(-1, nq)
+        return allf, allc, allq
 
     def exchange_callback(self, forest):
         """ow_exchange_fn for the native driver: all-gather the marks of the

@@ -374,9 +374,11 @@ def _shard_worker(rank, world, port, q):
         coords = np.ascontiguousarray(np.transpose(shapes.icosphere_triangles(3).astype(np.float32), (1, 2, 0)))
         geom = ow.CoordListGeometry(3, coords)
         f = ow.init_root_grid(ow.Aabb(np.zeros(3), np.ones(3)), (8, 8, 8))
-        res = ow.refine_near_wall(f, geom, ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8),
-                                  shard=parallel.Shard())
-        q.put((rank, f._coords, f._first_child, res.marked_detected, res.cell_face_tests))
+        sh = parallel.Shard()
+        res = ow.refine_near_wall(f, geom, ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8), shard=sh)
+        ll = ow.build_lattice_links(f, geom, None, "D3Q19", shard=sh)
+        q.put((rank, f._coords, f._first_child, res.marked_detected, res.cell_face_tests,
+               ll.flags.cpu().numpy(), ll.cells.cpu().numpy(), ll.q.cpu().numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -395,6 +397,7 @@ def test_sharded_native_driver_matches_single_rank(ow):
     geom = ow.CoordListGeometry(3, coords)
     f = ow.init_root_grid(ow.Aabb(np.zeros(3), np.ones(3)), (8, 8, 8))
     ref = ow.refine_near_wall(f, geom, ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8))
+    lref = ow.build_lattice_links(f, geom, None, "D3Q19")
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
@@ -408,10 +411,13 @@ def test_sharded_native_driver_matches_single_rank(ow):
     for p in procs:
         p.join(60)
     assert all(p.exitcode == 0 for p in procs)
-    for _, co, fc, md, t in outs:
+    for _, co, fc, md, t, fl, ce, qq in outs:
         np.testing.assert_array_equal(co, f._coords)
         np.testing.assert_array_equal(fc, f._first_child)
         assert md == ref.marked_detected and t == ref.cell_face_tests
+        np.testing.assert_array_equal(fl, lref.flags.cpu().numpy())
+        np.testing.assert_array_equal(ce, lref.cells.cpu().numpy())
+        np.testing.assert_array_equal(qq, lref.q.cpu().numpy())
 
 
 def test_marking_dense_soup_single_root(ow):
