@@ -286,6 +286,11 @@ int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, void* strea
  * [1] (block, face, direction) rows, [2] Moller-Trumbore / segment tests. */
 int ow_lattice_stats(ow_ctx* ctx, int64_t* out3, void* stream);
 
+/* ---- output ------------------------------------------------------------------ */
+/* Legacy ASCII VTK of the leaf blocks, byte-identical to export_vtk
+ * (vtk_io.py:17-69): quads / hexahedra, `level` and `marked` scalars. */
+int ow_export_vtk(ow_ctx* ctx, const ow_forest* f, const char* path, const char* title, void* stream);
+
 /* ---- predicate probe (parity tests) ---------------------------------------- */
 /* out[i] = near(point i, face i, d[i]) for n independent pairs; points (n, D),
  * faces (D, D, n) SoA, d float32 (n).  The device predicate used by marking. */

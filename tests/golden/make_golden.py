@@ -384,6 +384,34 @@ def gen_bigpipes():
               f"refined {res.marked_refined} E={res.bins.ids.size} ({dt:.1f}s)")
 
 
+VTK_CASES = [
+    # (geometry, root, d, levels, B): forests refined by the reference, exported by its export_vtk
+    ("circle256", 8, 0.1, 3, 8),
+    ("icosphere3", 4, 0.08, 3, 4),
+]
+
+
+def gen_vtk():
+    from octowall.vtk_io import export_vtk
+
+    out = {}
+    for i, (gname, root, d, levels, b) in enumerate(VTK_CASES):
+        g = geom(gname)
+        f = ow.init_root_grid(domain_for(g.dim), (root,) * g.dim)
+        ow.refine_near_wall(f, g, ow.NearWallParams(d_spec=d, n_levels=levels, bins_per_axis=b, backend="parallel"))
+        with tempfile.TemporaryDirectory() as td:
+            path = os.path.join(td, "f.vtk")
+            export_vtk(f, path, title=f"case {gname}")
+            data = open(path, "rb").read()
+        out[f"case{i}_name"] = np.array(gname)
+        out[f"case{i}_params"] = np.array([root, d, levels, b], np.float64)
+        out[f"case{i}_sha"] = np.array(hashlib.sha256(data).hexdigest())
+        out[f"case{i}_bytes"] = np.int64(len(data))
+        out[f"case{i}_head"] = np.frombuffer(data[:2000], np.uint8)
+        print(f"vtk {gname}: {len(data)} bytes")
+    save("vtk_cases", **out)
+
+
 def gen_forest_units():
     """Propagation / refinement known answers beyond the reference's own asserts."""
     out = {}
@@ -469,6 +497,7 @@ GROUPS = {
     "forest": gen_forest_units,
     "links": gen_links,
     "bigpipes": gen_bigpipes,
+    "vtk": gen_vtk,
 }
 
 

@@ -2,6 +2,8 @@
 golden fixtures and the CPU oracle, bit-exact for every integer / boolean
 output (bins, marks, forest arrays, links, flags) and float32-exact for q."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -522,3 +524,50 @@ def test_native_driver_capacity_fallbacks(ow):
     assert rg.marked_refined == ro["marked_refined"]
     np.testing.assert_array_equal(fg._coords, fo.coords)
     np.testing.assert_array_equal(fg._first_child, fo.first_child)
+
+
+# --------------------------------------------------------------------------- VTK export
+def test_export_vtk_byte_identical(ow, tmp_path):
+    """export_vtk of GPU-refined forests is byte-identical to the reference's
+    export_vtk of the reference's forests (vtk_io.py:17-69)."""
+    import hashlib
+
+    from golden_util import GOLDEN, load
+    from paper_2502_16310_b200 import shapes
+
+    g = load(os.path.join(GOLDEN, "vtk_cases.npz"))
+    geoms = {
+        "circle256": lambda: ow.index_to_coords(ow.generate_circle((0.5, 0.5), 0.25, 256)),
+        "icosphere3": lambda: ow.import_stl_bytes(shapes.binary_stl_bytes(shapes.icosphere_triangles(3))),
+    }
+    for i in range(2):
+        name = str(g[f"case{i}_name"])
+        root, d, levels, b = g[f"case{i}_params"]
+        geom = geoms[name]()
+        f = ow.init_root_grid(domain(ow, geom.dim), (int(root),) * geom.dim)
+        ow.refine_near_wall(f, geom, ow.NearWallParams(d_spec=float(d), n_levels=int(levels), bins_per_axis=int(b)))
+        path = tmp_path / f"{name}.vtk"
+        ow.export_vtk(f, str(path), title=f"case {name}")
+        data = path.read_bytes()
+        head = bytes(g[f"case{i}_head"])
+        assert data[: len(head)] == head, name
+        assert len(data) == int(g[f"case{i}_bytes"]), name
+        assert hashlib.sha256(data).hexdigest() == str(g[f"case{i}_sha"]), name
+
+
+def test_bin_density_sweep_csv(ow, tmp_path):
+    """sweep() runs one pipeline per B (B=1 naive) and writes the reference's
+    CSV schema; blocks_marked / blocks_final match separate runs."""
+    from paper_2502_16310_b200 import report
+
+    geom = ow.index_to_coords(ow.generate_circle((0.5, 0.5), 0.25, 400))
+    dom = ow.Aabb((0, 0), (1, 1))
+    rows = report.sweep(geom, dom, (16, 16), 0.1, 3, [1, 2, 4, 8], out_csv=str(tmp_path / "s.csv"), verbose=False)
+    lines = (tmp_path / "s.csv").read_text().splitlines()
+    assert lines[0] == report.SWEEP_CSV_HEADER and len(lines) == 5
+    for r in rows:
+        f = ow.init_root_grid(dom, (16, 16))
+        res = ow.refine_near_wall(f, geom, ow.NearWallParams(d_spec=0.1, n_levels=3, bins_per_axis=r.bins_per_axis,
+                                                             strategy="naive" if r.bins_per_axis == 1 else "binned"))
+        assert r.blocks_marked == res.total_marked and r.blocks_final == sum(f.leaves_per_level())
+        assert r.bin_setup_ms >= 0 and r.face_detect_ms > 0 and r.total_ms > 0
