@@ -229,6 +229,20 @@ typedef struct {
   void* alloc_user;
   void* out_buf[4];         /* optional caller buffers per OW_OUT_*: used when */
   int64_t out_cap[4];       /* out_cap (bytes) covers the need, else alloc() */
+  /* optional pinned host destinations of the results: the forest arrays are
+   * copied on a side stream while the lattice work runs, the boundary rows
+   * (cells, q) after it; the call's stream waits for both copies, so a
+   * synchronisation of `stream` makes them visible.  A destination whose
+   * capacity is too small is skipped (ow_g2g_result.host_copied says which). */
+  void* host_level;         /* int16[host_block_cap] */
+  void* host_coord[3];      /* int32[host_block_cap] per axis */
+  void* host_parent;        /* int32[host_block_cap] */
+  void* host_first_child;   /* int32[host_block_cap] */
+  void* host_marks;         /* int8[host_block_cap] */
+  int64_t host_block_cap;
+  void* host_cells;         /* int64[host_row_cap] */
+  void* host_q;             /* float32[host_row_cap * lattice_q] */
+  int64_t host_row_cap;
 } ow_g2g_params;
 typedef struct {
   ow_face_summary faces;
@@ -238,6 +252,8 @@ typedef struct {
   int64_t n_finest_leaves;
   int64_t n_boundary;
   int64_t lattice_stats[3];
+  int32_t host_copied;      /* bit 0: forest arrays, bit 1: boundary rows */
+  int32_t _pad2;
 } ow_g2g_result;
 /* Binary STL records (or, with d_records NULL, coords already in d_coords) ->
  * validated SoA geometry -> root grid in `f` (capacity preallocated, grown

@@ -125,6 +125,15 @@ class G2GParamsC(C.Structure):  # ow_g2g_params
         ("alloc_user", C.c_void_p),
         ("out_buf", C.c_void_p * 4),
         ("out_cap", C.c_int64 * 4),
+        ("host_level", C.c_void_p),
+        ("host_coord", C.c_void_p * 3),
+        ("host_parent", C.c_void_p),
+        ("host_first_child", C.c_void_p),
+        ("host_marks", C.c_void_p),
+        ("host_block_cap", C.c_int64),
+        ("host_cells", C.c_void_p),
+        ("host_q", C.c_void_p),
+        ("host_row_cap", C.c_int64),
     ]
 
 
@@ -137,6 +146,8 @@ class G2GResultC(C.Structure):  # ow_g2g_result
         ("n_finest_leaves", C.c_int64),
         ("n_boundary", C.c_int64),
         ("lattice_stats", C.c_int64 * 3),
+        ("host_copied", C.c_int32),
+        ("_pad2", C.c_int32),
     ]
 
 

@@ -134,6 +134,8 @@ struct ow_ctx {
   uint32_t* lat_flags;
   ow_forest lat_forest;
   void* stage_events;  // native driver CUDA events
+  cudaStream_t copy_stream;       // side stream for result copies (lazily created)
+  cudaEvent_t copy_ev[2];         // [0] forest final, [1] copies done
   bool defer_stage_times;
 };
 

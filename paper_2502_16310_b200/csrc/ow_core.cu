@@ -49,6 +49,9 @@ extern "C" int ow_ctx_destroy(ow_ctx* c) {
   cudaDeviceSynchronize();
   for (int i = 0; i < SLOT_COUNT; ++i)
     if (c->slot_ptr[i]) cudaFree(c->slot_ptr[i]);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (int i = 0; i < 2; ++i)
+    if (c->copy_ev[i]) cudaEventDestroy(c->copy_ev[i]);
   if (c->stage_events) {
     cudaEvent_t* ev = (cudaEvent_t*)c->stage_events;  // StageEvents starts with its event table
     for (int i = 0; i < OW_MAX_PASSES * 5; ++i)

@@ -323,7 +323,33 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
   for (int l = 0; l < out->nw.n_passes; ++l)
     if (out->nw.n_split[l] > 0) finest = l + 1;
   out->finest_level = finest;
-  if (p->lattice_q < 2 || !p->alloc) return ow_stage_times(ctx, &out->nw);
+  // the forest is final: stream its arrays to the host on the side stream
+  // while the lattice work runs on `s`
+  const int64_t nbk = f->n_blocks;
+  bool side = false;
+  if (p->host_level && p->host_block_cap >= nbk) {
+    if (!ctx->copy_stream) {
+      OW_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+      OW_CUDA(cudaEventCreateWithFlags(&ctx->copy_ev[0], cudaEventDisableTiming));
+      OW_CUDA(cudaEventCreateWithFlags(&ctx->copy_ev[1], cudaEventDisableTiming));
+    }
+    cudaStream_t cs = ctx->copy_stream;
+    OW_CUDA(cudaEventRecord(ctx->copy_ev[0], s));
+    OW_CUDA(cudaStreamWaitEvent(cs, ctx->copy_ev[0], 0));
+    OW_CUDA(cudaMemcpyAsync(p->host_level, f->d_level, 2 * (size_t)nbk, cudaMemcpyDeviceToHost, cs));
+    for (int a = 0; a < D; ++a)
+      OW_CUDA(cudaMemcpyAsync(p->host_coord[a], f->d_coord[a], 4 * (size_t)nbk, cudaMemcpyDeviceToHost, cs));
+    OW_CUDA(cudaMemcpyAsync(p->host_parent, f->d_parent, 4 * (size_t)nbk, cudaMemcpyDeviceToHost, cs));
+    OW_CUDA(cudaMemcpyAsync(p->host_first_child, f->d_first_child, 4 * (size_t)nbk, cudaMemcpyDeviceToHost, cs));
+    OW_CUDA(cudaMemcpyAsync(p->host_marks, f->d_marks, (size_t)nbk, cudaMemcpyDeviceToHost, cs));
+    OW_CUDA(cudaEventRecord(ctx->copy_ev[1], cs));
+    out->host_copied |= 1;
+    side = true;
+  }
+  if (p->lattice_q < 2 || !p->alloc) {
+    if (side) OW_CUDA(cudaStreamWaitEvent(s, ctx->copy_ev[1], 0));
+    return ow_stage_times(ctx, &out->nw);
+  }
   void* pl;
   OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(f->n_blocks + 1), s, &pl));
   int64_t nl = 0;
@@ -350,6 +376,12 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
     return OW_ERR_INTERNAL;
   }
   OW_TRY(ow_lattice_links_emit(ctx, (int64_t*)cells, (float*)q, stream));
+  if (p->host_cells && p->host_q && p->host_row_cap >= nb && nb > 0) {
+    OW_CUDA(cudaMemcpyAsync(p->host_cells, cells, 8 * (size_t)nb, cudaMemcpyDeviceToHost, s));
+    OW_CUDA(cudaMemcpyAsync(p->host_q, q, 4 * (size_t)nb * p->lattice_q, cudaMemcpyDeviceToHost, s));
+    out->host_copied |= 2;
+  }
+  if (side) OW_CUDA(cudaStreamWaitEvent(s, ctx->copy_ev[1], 0));  // results complete on `s`
   OW_TRY(ow_lattice_stats(ctx, out->lattice_stats, stream));
   return ow_stage_times(ctx, &out->nw);  // host work overlapping the emit kernels
 }

@@ -41,6 +41,7 @@ class GridPass:
     forest: Forest
     result: NearWallResult
     links: LatticeLinks | None
+    host: dict | None = None  # pinned host copies of the results (run(host=True))
 
 
 class GridPlan:
@@ -64,7 +65,10 @@ class GridPlan:
             if self.dirs.shape[1] != self.dim:
                 raise InvalidParameterError(f"lattice {lattice} does not match a {self.dim}D domain")
         self._est = [0, 0, 0, 0]  # output bytes of the last pass (preallocation estimate)
+        self._est_blocks = 0      # forest blocks / boundary rows of the last pass (host buffers)
+        self._est_rows = 0
         self._outs = {}
+        self._hbuf = None
 
         def alloc(_user, what, nbytes, out_p):
             try:
@@ -82,11 +86,19 @@ class GridPlan:
         self._outs[what] = t
         return t
 
+    def _pinned(self, dtype, n):
+        return torch.empty(max(int(n), 1), dtype=dtype, pin_memory=True)
+
     def run(self, records: torch.Tensor | None = None, n_faces: int | None = None,
-            geometry: CoordListGeometry | None = None) -> GridPass:
+            geometry: CoordListGeometry | None = None, host: bool = False) -> GridPass:
         """Binary STL records (device uint8, 50 bytes per face, after the
         84-byte header) — or an existing ``geometry`` — to a refined forest and
-        its finest-level lattice links."""
+        its finest-level lattice links.
+
+        ``host=True`` also returns pinned host copies of the results
+        (``GridPass.host``: forest arrays, boundary cells, q): the forest
+        arrays stream to the host on a side stream while the lattice work
+        runs.  Flags are not copied: bit i of a boundary cell is q[:, i] >= 0."""
         if geometry is None and records is None:
             raise InvalidParameterError("geometry_to_grid needs STL records or a geometry")
         dim = self.dim
@@ -115,6 +127,28 @@ class GridPlan:
                     t = self._new_out(what, self._est[what] + self._est[what] // 8 + 64)
                     gp.out_buf[what] = t.data_ptr()
                     gp.out_cap[what] = t.numel() * t.element_size()
+        hbuf = None
+        if host:
+            # pinned host buffers owned by the plan and reused by every pass (a
+            # pass's host results stay valid until the next host=True pass)
+            nbk = max(self._est_blocks + self._est_blocks // 4 + 1024, 1024)
+            nrow = max(self._est_rows + self._est_rows // 4 + 1024, 1024)
+            nq = len(self.dirs) if self.dirs is not None else 1
+            hb = self._hbuf
+            if hb is None or hb["level"].numel() < nbk or hb["cells"].numel() < nrow:
+                hb = dict(level=self._pinned(torch.int16, nbk), parent=self._pinned(torch.int32, nbk),
+                          first_child=self._pinned(torch.int32, nbk), marks=self._pinned(torch.int8, nbk),
+                          coords=[self._pinned(torch.int32, nbk) for _ in range(dim)],
+                          cells=self._pinned(torch.int64, nrow), q=self._pinned(torch.float32, nrow * nq))
+                self._hbuf = hb
+            hbuf = dict(hb)
+            nbk, nrow = hb["level"].numel(), hb["cells"].numel()
+            gp.host_level, gp.host_parent = hbuf["level"].data_ptr(), hbuf["parent"].data_ptr()
+            gp.host_first_child, gp.host_marks = hbuf["first_child"].data_ptr(), hbuf["marks"].data_ptr()
+            for a in range(dim):
+                gp.host_coord[a] = hbuf["coords"][a].data_ptr()
+            gp.host_block_cap = nbk
+            gp.host_cells, gp.host_q, gp.host_row_cap = hbuf["cells"].data_ptr(), hbuf["q"].data_ptr(), nrow
         out = _lib.G2GResultC()
         g, bins_t = st["g"], st["bins_t"]
         v = forest.view()
@@ -141,10 +175,38 @@ class GridPlan:
             ncell = 4 ** dim
             need = (8 * nl, 4 * nl * ncell, 8 * nb, 4 * nb * nq)
             self._est = list(need)
+            self._est_rows = nb
             o = self._outs
             links = LatticeLinks(lattice=self.lattice, level=int(out.finest_level), leaves=o[0][:nl],
                                  flags=o[1][: nl * ncell], cells=o[2][:nb], q=o[3][: nb * nq].view(nb, nq))
-        return GridPass(geom, forest, result, links)
+        self._est_blocks = forest.n_blocks
+        hres = None
+        if host:
+            hres = self._host_results(hbuf, int(out.host_copied), forest, links)
+        return GridPass(geom, forest, result, links, hres)
+
+    def _host_results(self, hbuf, copied, forest, links):
+        """Pinned host copies (the C side streamed whatever fit; the rest is
+        copied here).  Valid once the current stream is synchronised."""
+        n = forest.n_blocks
+        if not copied & 1:
+            for name, t in (("level", forest._level_t), ("parent", forest._parent_t),
+                            ("first_child", forest._first_child_t), ("marks", forest._marks)):
+                hbuf[name] = self._pinned(t.dtype, n)
+                hbuf[name][:n].copy_(t[:n], non_blocking=True)
+            hbuf["coords"] = [self._pinned(torch.int32, n) for _ in range(self.dim)]
+            for a in range(self.dim):
+                hbuf["coords"][a][:n].copy_(forest._coord[a][:n], non_blocking=True)
+        res = dict(level=hbuf["level"][:n], parent=hbuf["parent"][:n], first_child=hbuf["first_child"][:n],
+                   marks=hbuf["marks"][:n], coords=[c[:n] for c in hbuf["coords"]])
+        if links is not None:
+            nb, nq = links.n_boundary, links.q.shape[1]
+            if not copied & 2:
+                hbuf["cells"], hbuf["q"] = self._pinned(torch.int64, nb), self._pinned(torch.float32, nb * nq)
+                hbuf["cells"][:nb].copy_(links.cells, non_blocking=True)
+                hbuf["q"][: nb * nq].copy_(links.q.reshape(-1), non_blocking=True)
+            res["cells"], res["q"] = hbuf["cells"][:nb], hbuf["q"][: nb * nq].view(nb, nq)
+        return res
 
 
 def geometry_to_grid(records: torch.Tensor | None, n_faces: int | None, domain: Aabb, root_dims,

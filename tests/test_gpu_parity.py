@@ -571,3 +571,29 @@ def test_bin_density_sweep_csv(ow, tmp_path):
                                                              strategy="naive" if r.bins_per_axis == 1 else "binned"))
         assert r.blocks_marked == res.total_marked and r.blocks_final == sum(f.leaves_per_level())
         assert r.bin_setup_ms >= 0 and r.face_detect_ms > 0 and r.total_ms > 0
+
+
+def test_geometry_to_grid_host_results(ow):
+    """run(host=True): the side-stream / tail copies into the plan's pinned
+    buffers equal the device results (forest arrays, boundary cells, q), also
+    on a first pass whose buffer estimate is too small (host fallback copy)."""
+    import torch
+
+    from paper_2502_16310_b200 import pipeline, shapes
+
+    data = shapes.binary_stl_bytes(shapes.icosphere_triangles(3))
+    n = int.from_bytes(data[80:84], "little")
+    rec = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda()
+    plan = pipeline.GridPlan(ow.Aabb(np.zeros(3), np.ones(3)), (8, 8, 8),
+                             ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8), "D3Q19")
+    for _ in range(2):
+        gp = plan.run(rec, n, host=True)
+        torch.cuda.current_stream().synchronize()
+        h, f = gp.host, gp.forest
+        np.testing.assert_array_equal(h["level"].numpy(), f._level)
+        np.testing.assert_array_equal(np.stack([c.numpy() for c in h["coords"]], 1), f._coords)
+        np.testing.assert_array_equal(h["parent"].numpy(), f._parent)
+        np.testing.assert_array_equal(h["first_child"].numpy(), f._first_child)
+        np.testing.assert_array_equal(h["marks"].numpy(), f.marks.cpu().numpy())
+        np.testing.assert_array_equal(h["cells"].numpy(), gp.links.cells.cpu().numpy())
+        np.testing.assert_array_equal(h["q"].numpy(), gp.links.q.cpu().numpy())
