@@ -60,6 +60,7 @@ struct LatArgs {
   uint8_t* has_pair;        // [n_leaves]
   float4* rec;              // [n_faces * 3] (v0, e1, e2) / (a, s)
   double q[3];              // finest block size per axis
+  double inv_q[3];          // 1 / q
   int4* rows;               // [R]
   int64_t* rowoff;          // [R] units per row -> exclusive unit offsets
   int32_t* tile_row;        // [n_tiles] row of the first unit of each MT tile
@@ -142,6 +143,41 @@ __device__ __forceinline__ unsigned row_word(const unsigned* R, const int8_t* c,
   return w;
 }
 
+// Row r of a warp's flattened row list (see k_lat_faces): the owning lane j
+// (excl_j <= r < excl_j + popc(valid_j)) is found by a 5-step shuffle search,
+// the row is its (r - excl_j)-th set combination.  All lanes must call it
+// (shuffles).  Returns (leaf position, -, row word, units); w = 0 past the end.
+template <int D>
+__device__ __forceinline__ int4 row_of(int r, int lane, int excl, unsigned valid, const unsigned* R, int pos,
+                                       const LatArgs& A) {
+  int j = 0;  // last lane with excl <= r
+#pragma unroll
+  for (int step = 16; step > 0; step >>= 1) {
+    const int e = __shfl_sync(0xffffffffu, excl, j + step);
+    if (e <= r) j += step;
+  }
+  const unsigned vj = __shfl_sync(0xffffffffu, valid, j);
+  const unsigned Rj0 = __shfl_sync(0xffffffffu, R[0], j);
+  const unsigned Rj1 = __shfl_sync(0xffffffffu, R[1], j);
+  const unsigned Rj2 = __shfl_sync(0xffffffffu, D == 3 ? R[2] : 0u, j);
+  const int pj = __shfl_sync(0xffffffffu, pos, j);
+  const int ej = __shfl_sync(0xffffffffu, excl, j);
+  const int nth = r - ej;
+  if (nth < 0 || nth >= __popc(vj)) return make_int4(0, 0, 0, 0);
+  const int ci = __fns(vj, 0, nth + 1);  // position of the (nth+1)-th set bit
+  const unsigned Rj[3] = {Rj0, Rj1, Rj2};
+  unsigned w = (unsigned)A.combo_dir[ci];
+  int units = 1, cc = ci;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const unsigned ra = (Rj[a] >> (4 * (cc % 3))) & 0xFu;
+    cc /= 3;
+    w |= ra << (5 + 4 * a);
+    units *= (int)(ra >> 2) + 1;
+  }
+  return make_int4(pj, 0, (int)w, units);
+}
+
 // Warp per face: lane 0 packs the face record; lanes test the directions'
 // determinants (a link parallel to the face plane never hits: Moller-Trumbore
 // and the segment test reject det == 0), then walk the finest-level lattice
@@ -203,8 +239,9 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   for (int a = 0; a < D; ++a) {
     const double q = A.q[a];
     const int64_t nmax = ((int64_t)A.F.root[a] << L) - 1;
-    int64_t a0 = (int64_t)ceil(((double)lo[a] - A.F.dmin[a]) / q - 1.135);
-    int64_t a1 = (int64_t)floor(((double)hi[a] - A.F.dmin[a]) / q + 0.135);
+    (void)q;  // the 0.01-block margin also absorbs the reciprocal's rounding
+    int64_t a0 = (int64_t)ceil(((double)lo[a] - A.F.dmin[a]) * A.inv_q[a] - 1.135);
+    int64_t a1 = (int64_t)floor(((double)hi[a] - A.F.dmin[a]) * A.inv_q[a] + 0.135);
     if (a0 < 0) a0 = 0;
     if (a1 > nmax) a1 = nmax;
     k0[a] = (int)a0;
@@ -241,54 +278,55 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
         if (nrow) A.has_pair[pos] = 1;
       }
     }
-    // units of this lane's rows
-    unsigned long long nunit = 0;
-    for (unsigned vv = valid; vv; vv &= vv - 1) {
-      int units = 1, cc = __ffs(vv) - 1;
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        units *= (int)((R[a] >> (4 * (cc % 3) + 2)) & 3u) + 1;
-        cc /= 3;
-      }
-      nunit += units;
-    }
-    // one 64-bit atomic reserves both the rows and their units (rows in the low
-    // RU_ROW_BITS bits): row order and unit order agree, so the unit offsets are
-    // monotone in the row index without a scan
-    const unsigned long long mine = (nunit << RU_ROW_BITS) | (unsigned long long)nrow;
-    unsigned long long incl = mine;
+    // rows of all lanes, flattened: lane j owns rows [excl_j, excl_j + nrow_j);
+    // the warp walks them 32 at a time (each lane decodes one row), so the cost
+    // follows the warp's row total instead of its busiest lane
+    int incl = nrow;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
     }
-    const unsigned long long tot = __shfl_sync(0xffffffffu, incl, 31);
-    if (!tot) continue;
-    unsigned long long base = 0;
-    if (lane == 31) base = atomicAdd(A.ru_d, tot);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    const unsigned long long start = base + incl - mine;
-    int64_t k = (int64_t)(start & RU_ROW_MASK);
-    int64_t u = (int64_t)(start >> RU_ROW_BITS);
-    while (valid) {
-      const int ci = __ffs(valid) - 1;
-      valid &= valid - 1;
-      unsigned w = (unsigned)A.combo_dir[ci];
-      int units = 1, cc = ci;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (!total) continue;
+    const int excl = incl - nrow;
+    // pass 1: units of every row -> one 64-bit atomic reserves rows and units
+    // together (rows in the low RU_ROW_BITS bits), so unit offsets are monotone
+    // in the row index without a scan
+    unsigned long long units_w = 0;
+    for (int r0 = 0; r0 < total; r0 += 32) {
+      const int r = r0 + lane;
+      if (r < total) units_w += (unsigned long long)row_of<D>(r, lane, excl, valid, R, pos, A).w;
+      else row_of<D>(r, lane, excl, valid, R, pos, A);
+    }
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        const unsigned ra = (R[a] >> (4 * (cc % 3))) & 0xFu;
-        cc /= 3;
-        w |= ra << (5 + 4 * a);
-        units *= (int)(ra >> 2) + 1;
+    for (int o = 16; o > 0; o >>= 1) units_w += __shfl_xor_sync(0xffffffffu, units_w, o);
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(A.ru_d, (units_w << RU_ROW_BITS) | (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    int64_t k0r = (int64_t)(base & RU_ROW_MASK);
+    int64_t u0r = (int64_t)(base >> RU_ROW_BITS);
+    // pass 2: write the rows; unit offsets by a warp scan per chunk of 32 rows
+    for (int r0 = 0; r0 < total; r0 += 32) {
+      const int r = r0 + lane;
+      const int4 row = row_of<D>(r, lane, excl, valid, R, pos, A);
+      const int units = r < total ? row.w : 0;
+      int ui = units;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, ui, o);
+        if (lane >= o) ui += y;
       }
-      if (k < A.row_cap && u + units <= A.unit_cap) {
-        A.rows[k] = make_int4(pos, (int)f, (int)w, units);
-        A.rowoff[k] = u;
-        for (int64_t t = (u + MT_TILE - 1) / MT_TILE; t * MT_TILE < u + units; ++t) A.tile_row[t] = (int32_t)k;
+      if (r < total) {
+        const int64_t k = k0r + r;
+        const int64_t u = u0r + ui - units;
+        if (k < A.row_cap && u + units <= A.unit_cap) {
+          A.rows[k] = make_int4(row.x, (int)f, row.z, units);
+          A.rowoff[k] = u;
+          for (int64_t t = (u + MT_TILE - 1) / MT_TILE; t * MT_TILE < u + units; ++t) A.tile_row[t] = (int32_t)k;
+        }
       }
-      ++k;
-      u += units;
+      u0r += __shfl_sync(0xffffffffu, ui, 31);
     }
   }
 }
@@ -554,6 +592,7 @@ LatArgs make_args(ow_ctx* ctx) {
   for (int a = 0; a < 3; ++a) {
     // float32 of the FP64 cell size, as the device's block_len / 4 (IEEE division both sides)
     A.q[a] = a < f->dim ? f->dext[a] / (double)((int64_t)f->root[a] << A.level) : 1.0;
+    A.inv_q[a] = 1.0 / A.q[a];
     A.h[a] = a < f->dim ? (float)(A.q[a] / 4.0) : 0.0f;
   }
   for (int i = 0; i < A.nq; ++i) {
