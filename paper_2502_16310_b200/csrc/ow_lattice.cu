@@ -49,6 +49,7 @@ struct LatArgs {
   int8_t dc[QMAX][3];       // lattice directions c_d
   uint8_t dir_combo[32];    // combination index sum_a (c_a + 1) 3^a of direction d
   uint8_t combo_dir[27];    // direction of each combination (lattice subset)
+  unsigned dirmask;         // combinations of the lattice's moving directions
   unsigned spread[3][8];    // per-axis non-empty-c mask -> mask over combinations
   const float* coords;
   int64_t n_faces;
@@ -146,9 +147,10 @@ __device__ __forceinline__ unsigned row_word(const unsigned* R, const int8_t* c,
 // Row r of a warp's flattened row list (see k_lat_faces): the owning lane j
 // (excl_j <= r < excl_j + popc(valid_j)) is found by a 5-step shuffle search,
 // the row is its (r - excl_j)-th set combination.  All lanes must call it
-// (shuffles).  Returns (leaf position, -, row word, units); w = 0 past the end.
+// (shuffles).  Returns (leaf position, face, row word, units); units = 0 past
+// the end.
 template <int D>
-__device__ __forceinline__ int4 row_of(int r, int lane, int excl, unsigned valid, const unsigned* R, int pos,
+__device__ __forceinline__ int4 row_of(int r, int excl, unsigned valid, const unsigned* R, int pos, int face,
                                        const LatArgs& A) {
   int j = 0;  // last lane with excl <= r
 #pragma unroll
@@ -161,6 +163,7 @@ __device__ __forceinline__ int4 row_of(int r, int lane, int excl, unsigned valid
   const unsigned Rj1 = __shfl_sync(0xffffffffu, R[1], j);
   const unsigned Rj2 = __shfl_sync(0xffffffffu, D == 3 ? R[2] : 0u, j);
   const int pj = __shfl_sync(0xffffffffu, pos, j);
+  const int fj = __shfl_sync(0xffffffffu, face, j);
   const int ej = __shfl_sync(0xffffffffu, excl, j);
   const int nth = r - ej;
   if (nth < 0 || nth >= __popc(vj)) return make_int4(0, 0, 0, 0);
@@ -175,28 +178,37 @@ __device__ __forceinline__ int4 row_of(int r, int lane, int excl, unsigned valid
     w |= ra << (5 + 4 * a);
     units *= (int)(ra >> 2) + 1;
   }
-  return make_int4(pj, 0, (int)w, units);
+  return make_int4(pj, fj, (int)w, units);
 }
 
-// Warp per face: lane 0 packs the face record; lanes test the directions'
-// determinants (a link parallel to the face plane never hits: Moller-Trumbore
-// and the segment test reject det == 0), then walk the finest-level lattice
-// blocks the face box can reach (root-lattice descent, no bins).  Link boxes of
-// block k span [o_k - q/8, o_k + 9q/8]; a 0.01-block margin absorbs float
-// rounding and the exact per-axis range test filters.  Rows are appended in
-// one pass (warp-aggregated counter): their order is irrelevant, every hit is
-// combined with atomicOr / atomicMin.  Rows past `row_cap` are counted but not
-// written (the host re-runs with room for them).
+// FACES_PER_WARP faces per warp, SLOT_LANES lanes per face: each lane group
+// walks the finest-level lattice blocks its face box can reach (root-lattice
+// descent, no bins; link boxes of block k span [o_k - q/8, o_k + 9q/8] and a
+// 0.01-block margin absorbs float rounding), computes the per-axis cell ranges
+// of each existing finest leaf (the exact filter) and the directions whose
+// cell box is non-empty on every axis.  The warp then walks its flattened row
+// list 32 rows at a time, reserves rows and units with one packed atomic (row
+// order and unit order agree, so unit offsets are monotone without a scan)
+// and writes them; rows past the capacities are counted, not written (the
+// host re-runs with room).  Links parallel to the face (det == 0) are rejected
+// by k_lat_mt.
+constexpr int FACES_PER_WARP = 4;
+constexpr int SLOT_LANES = 32 / FACES_PER_WARP;
+
 template <int D>
 __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   const int lane = threadIdx.x & 31;
-  const int64_t f = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (f >= A.n_faces) return;
-  float v[3][3], lo[3], hi[3], e1[3], e2[3];
+  const int sl = lane % SLOT_LANES;
+  const int64_t f = ((int64_t)blockIdx.x * 4 + (threadIdx.x >> 5)) * FACES_PER_WARP + lane / SLOT_LANES;
+  if (f - lane / SLOT_LANES >= A.n_faces) return;  // whole warp past the end
+  const bool live = f < A.n_faces;
+  float v[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  if (live) {
 #pragma unroll
-  for (int j = 0; j < D; ++j)
+    for (int j = 0; j < D; ++j)
 #pragma unroll
-    for (int a = 0; a < D; ++a) v[j][a] = A.coords[((int64_t)j * D + a) * A.n_faces + f];
+      for (int a = 0; a < D; ++a) v[j][a] = A.coords[((int64_t)j * D + a) * A.n_faces + f];
+  }
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     lo[a] = v[0][a];
@@ -206,40 +218,22 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
       lo[a] = fminf(lo[a], v[j][a]);
       hi[a] = fmaxf(hi[a], v[j][a]);
     }
-    e1[a] = FSUB(v[1][a], v[0][a]);  // e1 = v1 - v0 (3D) / s = b - a (2D), oracle/lattice.py
-    e2[a] = D == 3 ? FSUB(v[2][a], v[0][a]) : 0.0f;
   }
-  if (lane == 0) {
+  if (live && sl == 0) {  // e1 = v1 - v0, e2 = v2 - v0 (3D) / s = b - a (2D), oracle/lattice.py
     if (D == 3) {
       A.rec[3 * f + 0] = make_float4(v[0][0], v[0][1], v[0][2], 0.0f);
-      A.rec[3 * f + 1] = make_float4(e1[0], e1[1], e1[2], 0.0f);
-      A.rec[3 * f + 2] = make_float4(e2[0], e2[1], e2[2], 0.0f);
+      A.rec[3 * f + 1] = make_float4(FSUB(v[1][0], v[0][0]), FSUB(v[1][1], v[0][1]), FSUB(v[1][2], v[0][2]), 0.0f);
+      A.rec[3 * f + 2] = make_float4(FSUB(v[2][0], v[0][0]), FSUB(v[2][1], v[0][1]), FSUB(v[2][2], v[0][2]), 0.0f);
     } else {
-      A.rec[3 * f + 0] = make_float4(v[0][0], v[0][1], e1[0], e1[1]);
+      A.rec[3 * f + 0] = make_float4(v[0][0], v[0][1], FSUB(v[1][0], v[0][0]), FSUB(v[1][1], v[0][1]));
     }
   }
-  bool dok = false;  // lane d: determinant of direction d is non-zero
-  if (lane >= 1 && lane < A.nq) {
-    const float* dv = A.dv[lane];
-    if (D == 3) {
-      const float px = FSUB(FMUL(dv[1], e2[2]), FMUL(dv[2], e2[1]));
-      const float py = FSUB(FMUL(dv[2], e2[0]), FMUL(dv[0], e2[2]));
-      const float pz = FSUB(FMUL(dv[0], e2[1]), FMUL(dv[1], e2[0]));
-      dok = dot3f(e1[0], e1[1], e1[2], px, py, pz) != 0.0f;
-    } else {
-      dok = FSUB(FMUL(dv[0], e1[1]), FMUL(dv[1], e1[0])) != 0.0f;
-    }
-  }
-  // lattice directions with a non-zero determinant, over the 3^D combinations
-  const unsigned detmask = __reduce_or_sync(0xffffffffu, dok ? 1u << A.dir_combo[lane] : 0u);
   const int L = A.level;
   int k0[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
-  int64_t nslots = detmask ? 1 : 0;
+  int nslots = live ? 1 : 0;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    const double q = A.q[a];
     const int64_t nmax = ((int64_t)A.F.root[a] << L) - 1;
-    (void)q;  // the 0.01-block margin also absorbs the reciprocal's rounding
     int64_t a0 = (int64_t)ceil(((double)lo[a] - A.F.dmin[a]) * A.inv_q[a] - 1.135);
     int64_t a1 = (int64_t)floor(((double)hi[a] - A.F.dmin[a]) * A.inv_q[a] + 0.135);
     if (a0 < 0) a0 = 0;
@@ -248,39 +242,40 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
     ext[a] = a1 >= a0 ? (int)(a1 - a0 + 1) : 0;
     nslots *= ext[a];
   }
-  for (int64_t s0 = 0; s0 < nslots; s0 += 32) {
-    const int64_t slot = s0 + lane;
+  const int max_slots = __reduce_max_sync(0xffffffffu, nslots);
+  for (int s0 = 0; s0 < max_slots; s0 += SLOT_LANES) {
+    const int slot = s0 + sl;
     int nrow = 0, pos = 0;
     unsigned R[3] = {0u, 0u, 0u}, valid = 0u;
     if (slot < nslots) {
       int32_t nc[3] = {0, 0, 0};
-      int64_t rem = slot;
+      int rem = slot;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        nc[a] = k0[a] + (int)(rem % ext[a]);
+        nc[a] = k0[a] + rem % ext[a];
         rem /= ext[a];
       }
       int depth;
       const int node = locate(A.F, L, nc, &depth);
       // (leaves outside this call's position slice belong to another rank; no
-      // early `continue` here: the whole warp must reach the row-reservation scan)
-      if (depth == L && A.F.first_child[node] < 0 && A.pos_of[node] >= A.pos_lo && A.pos_of[node] < A.pos_hi) {
-        pos = A.pos_of[node];
+      // early `continue` here: the whole warp must reach the shuffles below)
+      if (depth == L && A.F.first_child[node] < 0) {
+        const int pn = A.pos_of[node];
+        if (pn >= A.pos_lo && pn < A.pos_hi) {
+          pos = pn;
 #pragma unroll
-        for (int a = 0; a < D; ++a)
-          R[a] = axis_ranges(reinterpret_cast<const float4*>(A.cen)[(int64_t)pos * D + a], A.h[a], lo[a], hi[a]);
-        // directions with a non-empty cell box on every axis, as a mask over the
-        // 3^D combinations c = (c_x, c_y[, c_z]) (outer product of per-axis masks)
-        valid = detmask;
+          for (int a = 0; a < D; ++a)
+            R[a] = axis_ranges(reinterpret_cast<const float4*>(A.cen)[(int64_t)pos * D + a], A.h[a], lo[a], hi[a]);
+          // directions with a non-empty cell box on every axis, as a mask over
+          // the 3^D combinations (outer product of the per-axis masks)
+          valid = A.dirmask;
 #pragma unroll
-        for (int a = 0; a < D; ++a) valid &= A.spread[a][(~R[a] >> 12) & 7u];
-        nrow = __popc(valid);
-        if (nrow) A.has_pair[pos] = 1;
+          for (int a = 0; a < D; ++a) valid &= A.spread[a][(~R[a] >> 12) & 7u];
+          nrow = __popc(valid);
+          if (nrow) A.has_pair[pos] = 1;
+        }
       }
     }
-    // rows of all lanes, flattened: lane j owns rows [excl_j, excl_j + nrow_j);
-    // the warp walks them 32 at a time (each lane decodes one row), so the cost
-    // follows the warp's row total instead of its busiest lane
     int incl = nrow;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -290,27 +285,23 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     if (!total) continue;
     const int excl = incl - nrow;
-    // pass 1: units of every row -> one 64-bit atomic reserves rows and units
-    // together (rows in the low RU_ROW_BITS bits), so unit offsets are monotone
-    // in the row index without a scan
+    const int fi = (int)f;
+    // pass 1: units of every row, then one reservation
     unsigned long long units_w = 0;
-    for (int r0 = 0; r0 < total; r0 += 32) {
-      const int r = r0 + lane;
-      if (r < total) units_w += (unsigned long long)row_of<D>(r, lane, excl, valid, R, pos, A).w;
-      else row_of<D>(r, lane, excl, valid, R, pos, A);
-    }
+    for (int r0 = 0; r0 < total; r0 += 32)
+      units_w += (unsigned long long)row_of<D>(r0 + lane, excl, valid, R, pos, fi, A).w;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) units_w += __shfl_xor_sync(0xffffffffu, units_w, o);
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(A.ru_d, (units_w << RU_ROW_BITS) | (unsigned long long)total);
     base = __shfl_sync(0xffffffffu, base, 0);
-    int64_t k0r = (int64_t)(base & RU_ROW_MASK);
+    const int64_t k0r = (int64_t)(base & RU_ROW_MASK);
     int64_t u0r = (int64_t)(base >> RU_ROW_BITS);
     // pass 2: write the rows; unit offsets by a warp scan per chunk of 32 rows
     for (int r0 = 0; r0 < total; r0 += 32) {
       const int r = r0 + lane;
-      const int4 row = row_of<D>(r, lane, excl, valid, R, pos, A);
-      const int units = r < total ? row.w : 0;
+      const int4 row = row_of<D>(r, excl, valid, R, pos, fi, A);
+      const int units = row.w;
       int ui = units;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -321,7 +312,7 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
         const int64_t k = k0r + r;
         const int64_t u = u0r + ui - units;
         if (k < A.row_cap && u + units <= A.unit_cap) {
-          A.rows[k] = make_int4(row.x, (int)f, row.z, units);
+          A.rows[k] = row;
           A.rowoff[k] = u;
           for (int64_t t = (u + MT_TILE - 1) / MT_TILE; t * MT_TILE < u + units; ++t) A.tile_row[t] = (int32_t)k;
         }
@@ -477,7 +468,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
           const float qz = FSUB(FMUL(tx, E1.y), FMUL(ty, E1.x));
           const float vn = dot3f(dv[0], dv[1], dv[2], qx, qy, qz);
           const float tn = dot3f(E2.x, E2.y, E2.z, qx, qy, qz);
-          if (quot_nonneg(un, det) & quot_nonneg(vn, det) & quot_nonneg(tn, det)) {
+          if ((det != 0.0f) & quot_nonneg(un, det) & quot_nonneg(vn, det) & quot_nonneg(tn, det)) {
             const float uu = FDIV(un, det), vv = FDIV(vn, det);
             t = FDIV(tn, det);
             hit = (FADD(uu, vv) <= 1.0f) & (t <= 1.0f);
@@ -489,7 +480,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
           const float qx = FSUB(V.x, x[0]), qy = FSUB(V.y, x[1]);
           const float tn = FSUB(FMUL(qx, S.y), FMUL(qy, S.x));
           const float sn = FSUB(FMUL(qx, dv[1]), FMUL(qy, dv[0]));
-          if (quot_nonneg(tn, den) && quot_nonneg(sn, den)) {
+          if ((den != 0.0f) && quot_nonneg(tn, den) && quot_nonneg(sn, den)) {
             t = FDIV(tn, den);
             const float ss = FDIV(sn, den);
             hit = t <= 1.0f && ss <= 1.0f;
@@ -607,6 +598,7 @@ LatArgs make_args(ow_ctx* ctx) {
     }
     A.dir_combo[i] = (uint8_t)ci;
     A.combo_dir[ci] = (uint8_t)i;
+    if (i > 0) A.dirmask |= 1u << ci;
   }
   for (int a = 0; a < 3; ++a)
     for (int m = 0; m < 8; ++m) {
@@ -728,10 +720,10 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   LatArgs A = make_args(ctx);
   if (D == 3) {
     k_lat_pos<3><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
-    k_lat_faces<3><<<ow_blocks(n_faces, 4), 128, 0, s>>>(A);
+    k_lat_faces<3><<<ow_blocks(n_faces, 4 * FACES_PER_WARP), 128, 0, s>>>(A);
   } else {
     k_lat_pos<2><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
-    k_lat_faces<2><<<ow_blocks(n_faces, 4), 128, 0, s>>>(A);
+    k_lat_faces<2><<<ow_blocks(n_faces, 4 * FACES_PER_WARP), 128, 0, s>>>(A);
   }
   ctx->launches += 2;
   OW_CHECK_LAUNCH();

@@ -180,6 +180,9 @@ class GridPlan:
             links = LatticeLinks(lattice=self.lattice, level=int(out.finest_level), leaves=o[0][:nl],
                                  flags=o[1][: nl * ncell], cells=o[2][:nb], q=o[3][: nb * nq].view(nb, nq))
         self._est_blocks = forest.n_blocks
+        # size the next pass's forest from this one: device refinement then never
+        # overflows into the host fallback (which grows the arrays with syncs)
+        self.capacity = max(self.capacity, forest.n_blocks + forest.n_blocks // 4)
         hres = None
         if host:
             hres = self._host_results(hbuf, int(out.host_copied), forest, links)
