@@ -313,6 +313,12 @@ int ow_export_vtk(ow_ctx* ctx, const ow_forest* f, const char* path, const char*
 int ow_near_pairs(ow_ctx* ctx, int32_t dim, const float* d_points, const float* d_faces, const float* d_d,
                   int64_t n, uint8_t* d_out, void* stream);
 
+/* Predicate-vs-referee sampling (validate.py:98-141): out_mask[i] = FP32
+ * near(point i, face i, f32(d[i])); out_exact[i] = FP64 exact distance of the
+ * point to the closed face (distance.py:260-345, same double op order). */
+int ow_referee_pairs(ow_ctx* ctx, int32_t dim, const float* d_points, const float* d_faces, const double* d_d,
+                     int64_t n, double* d_exact, uint8_t* d_mask, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

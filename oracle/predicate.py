@@ -12,6 +12,8 @@ broadcast against each other (faces on the last axis).
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 F32 = np.float32
@@ -91,3 +93,64 @@ def near(points, faces, d):
     if faces.shape[0] == 2:
         return near_edge(p[..., 0], p[..., 1], faces, d)
     return near_triangle(p[..., 0], p[..., 1], p[..., 2], faces, d)
+
+
+def exact_point_triangle_distance(p, a, b, c):
+    """FP64 referee, restated from distance.py:275-345 (Python floats: IEEE
+    double, no FMA, correctly rounded sqrt); degeneracy check omitted."""
+    px, py, pz = (float(x) for x in p)
+    ax, ay, az = (float(x) for x in a)
+    bx, by, bz = (float(x) for x in b)
+    cx, cy, cz = (float(x) for x in c)
+    abx, aby, abz = bx - ax, by - ay, bz - az
+    acx, acy, acz = cx - ax, cy - ay, cz - az
+    bcx, bcy, bcz = cx - bx, cy - by, cz - bz
+    apx, apy, apz = px - ax, py - ay, pz - az
+    d1 = abx * apx + aby * apy + abz * apz
+    d2 = acx * apx + acy * apy + acz * apz
+    if d1 <= 0.0 and d2 <= 0.0:
+        return math.sqrt(apx * apx + apy * apy + apz * apz)
+    bpx, bpy, bpz = px - bx, py - by, pz - bz
+    d3 = abx * bpx + aby * bpy + abz * bpz
+    d4 = acx * bpx + acy * bpy + acz * bpz
+    if d3 >= 0.0 and d4 <= d3:
+        return math.sqrt(bpx * bpx + bpy * bpy + bpz * bpz)
+    vc = d1 * d4 - d3 * d2
+    if vc <= 0.0 and d1 >= 0.0 and d3 <= 0.0:
+        t = d1 / (d1 - d3)
+        qx, qy, qz = apx - t * abx, apy - t * aby, apz - t * abz
+        return math.sqrt(qx * qx + qy * qy + qz * qz)
+    cpx, cpy, cpz = px - cx, py - cy, pz - cz
+    d5 = abx * cpx + aby * cpy + abz * cpz
+    d6 = acx * cpx + acy * cpy + acz * cpz
+    if d6 >= 0.0 and d5 <= d6:
+        return math.sqrt(cpx * cpx + cpy * cpy + cpz * cpz)
+    vb = d5 * d2 - d1 * d6
+    if vb <= 0.0 and d2 >= 0.0 and d6 <= 0.0:
+        t = d2 / (d2 - d6)
+        qx, qy, qz = apx - t * acx, apy - t * acy, apz - t * acz
+        return math.sqrt(qx * qx + qy * qy + qz * qz)
+    va = d3 * d6 - d5 * d4
+    if va <= 0.0 and (d4 - d3) >= 0.0 and (d5 - d6) >= 0.0:
+        t = (d4 - d3) / ((d4 - d3) + (d5 - d6))
+        qx, qy, qz = bpx - t * bcx, bpy - t * bcy, bpz - t * bcz
+        return math.sqrt(qx * qx + qy * qy + qz * qz)
+    denom = 1.0 / (va + vb + vc)
+    v = vb * denom
+    w = vc * denom
+    qx = apx - (v * abx + w * acx)
+    qy = apy - (v * aby + w * acy)
+    qz = apz - (v * abz + w * acz)
+    return math.sqrt(qx * qx + qy * qy + qz * qz)
+
+
+def point_segment_distance(p, a, b):
+    """sqrt of point_segment_distance_sq, distance.py:260-272 (FP64)."""
+    px, py = float(p[0]), float(p[1])
+    ax, ay, bx, by = float(a[0]), float(a[1]), float(b[0]), float(b[1])
+    ex, ey = bx - ax, by - ay
+    el2 = ex * ex + ey * ey
+    t = ((px - ax) * ex + (py - ay) * ey) / el2
+    t = min(1.0, max(0.0, t))
+    qx, qy = px - (ax + t * ex), py - (ay + t * ey)
+    return math.sqrt(qx * qx + qy * qy)

@@ -597,3 +597,24 @@ def test_geometry_to_grid_host_results(ow):
         np.testing.assert_array_equal(h["marks"].numpy(), f.marks.cpu().numpy())
         np.testing.assert_array_equal(h["cells"].numpy(), gp.links.cells.cpu().numpy())
         np.testing.assert_array_equal(h["q"].numpy(), gp.links.q.cpu().numpy())
+
+
+# --------------------------------------------------------------------------- predicate vs referee sampler
+def test_gpu_referee_sampler_matches_reference_run(ow):
+    """GPU predicate-vs-referee sampling reproduces the reference's recorded
+    acceptance numbers (test_output.txt:11,14: 1e5 samples, 0 disagreements
+    outside the band, 918 / 968 in band) and its FP64 exact distances equal the
+    oracle's restatement of the referee bit for bit."""
+    from oracle import predicate as op
+    from paper_2502_16310_b200 import validate
+
+    assert validate.check_triangle_predicate_oracle(2024, 100000) == (0, 918, 0)
+    assert validate.check_edge_predicate_oracle(2025, 100000) == (0, 968, 0)
+    tri, pts, d = validate.sample_triangle_cases(7, 3000)
+    _, exact = validate.referee_pairs(tri, pts, d)
+    ref = [op.exact_point_triangle_distance(pts[i], tri[i, 0], tri[i, 1], tri[i, 2]) for i in range(3000)]
+    np.testing.assert_array_equal(exact, np.asarray(ref))
+    seg, pts2, d2 = validate.sample_edge_cases(8, 3000)
+    _, exact2 = validate.referee_pairs(seg, pts2, d2)
+    ref2 = [op.point_segment_distance(pts2[i], seg[i, 0], seg[i, 1]) for i in range(3000)]
+    np.testing.assert_array_equal(exact2, np.asarray(ref2))
