@@ -313,6 +313,14 @@ int ow_export_vtk(ow_ctx* ctx, const ow_forest* f, const char* path, const char*
 int ow_near_pairs(ow_ctx* ctx, int32_t dim, const float* d_points, const float* d_faces, const float* d_d,
                   int64_t n, uint8_t* d_out, void* stream);
 
+/* ASCII STL fast path (host, _parse_ascii_stl geometry.py:349-412): parses
+ * pure-ASCII STL text into tris[n][3][3] float32 (float() then one float32
+ * rounding).  OW_ERR_PARSE (no message) for anything it does not accept —
+ * non-ASCII bytes or any syntax error — so the caller's reference-faithful
+ * parser reports the exact error; OW_ERR_CAPACITY when more than `cap`
+ * facets. */
+int ow_parse_ascii_stl(const char* data, int64_t len, float* tris, int64_t cap, int64_t* out_n);
+
 /* Predicate-vs-referee sampling (validate.py:98-141): out_mask[i] = FP32
  * near(point i, face i, f32(d[i])); out_exact[i] = FP64 exact distance of the
  * point to the closed face (distance.py:260-345, same double op order). */

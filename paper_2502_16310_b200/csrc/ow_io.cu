@@ -5,6 +5,7 @@
 // byte the reference's: corners "%.9g %.9g %.9g", quads (2D) / hexahedra (3D)
 // with unwelded corner points, `level` and `marked` cell scalars.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -144,5 +145,200 @@ extern "C" int ow_export_vtk(ow_ctx* ctx, const ow_forest* f, const char* path, 
     ow_set_error("write to %s failed", path);
     return OW_ERR_INTERNAL;
   }
+  return OW_OK;
+}
+
+// ---------------------------------------------------------------------------
+// ASCII STL (geometry.py:349-412), native fast path.  Exact on the inputs it
+// accepts: pure-ASCII text whose grammar parses; every number token is
+// validated against Python's float() grammar (sign, digits with single
+// underscores between digits, optional fraction and exponent, inf / infinity
+// / nan) before a correctly rounded strtod, then rounded once to float32 like
+// np.asarray(..., float32).  Anything else — non-ASCII bytes, any syntax error —
+// returns OW_ERR_PARSE without a message so the caller's reference-faithful
+// parser produces the exact GeometryParseError (with its line number).
+// ---------------------------------------------------------------------------
+namespace {
+
+inline bool py_space(unsigned char c) { return c == ' ' || (c >= 9 && c <= 13) || (c >= 0x1c && c <= 0x1f); }
+
+inline bool ieq(const char* t, int n, const char* kw) {
+  int i = 0;
+  for (; i < n && kw[i]; ++i) {
+    char c = t[i];
+    if (c >= 'A' && c <= 'Z') c = (char)(c - 'A' + 'a');
+    if (c != kw[i]) return false;
+  }
+  return i == n && kw[i] == 0;
+}
+
+// Python float() grammar on an ASCII token; writes the underscore-free text
+bool py_float(const char* t, int n, double* out) {
+  char buf[128];
+  if (n <= 0 || n >= (int)sizeof(buf)) return false;
+  int i = 0, o = 0;
+  if (t[i] == '+' || t[i] == '-') buf[o++] = t[i++];
+  const char* r = t + i;
+  const int rn = n - i;
+  if (ieq(r, rn, "inf") || ieq(r, rn, "infinity")) {
+    *out = (o && buf[0] == '-') ? -INFINITY : INFINITY;
+    return true;
+  }
+  if (ieq(r, rn, "nan")) {
+    *out = NAN;
+    return true;
+  }
+  auto digitpart = [&](void) -> bool {  // digit (['_'] digit)*
+    if (i >= n || t[i] < '0' || t[i] > '9') return false;
+    buf[o++] = t[i++];
+    while (i < n) {
+      if (t[i] >= '0' && t[i] <= '9') {
+        buf[o++] = t[i++];
+      } else if (t[i] == '_' && i + 1 < n && t[i + 1] >= '0' && t[i + 1] <= '9') {
+        ++i;
+      } else {
+        break;
+      }
+    }
+    return true;
+  };
+  bool mant = false;
+  if (i < n && t[i] >= '0' && t[i] <= '9') {
+    digitpart();
+    mant = true;
+  }
+  if (i < n && t[i] == '.') {
+    buf[o++] = t[i++];
+    if (i < n && t[i] >= '0' && t[i] <= '9') {
+      digitpart();
+      mant = true;
+    }
+  }
+  if (!mant) return false;
+  if (i < n && (t[i] == 'e' || t[i] == 'E')) {
+    buf[o++] = t[i++];
+    if (i < n && (t[i] == '+' || t[i] == '-')) buf[o++] = t[i++];
+    if (!digitpart()) return false;
+  }
+  if (i != n) return false;
+  buf[o] = 0;
+  char* end = nullptr;
+  *out = strtod(buf, &end);
+  return end == buf + o;
+}
+
+struct Tok {
+  const char* p;
+  const char* end;
+  const char* t;
+  int n;
+  bool next() {
+    while (p < end && py_space((unsigned char)*p)) ++p;
+    if (p >= end) return false;
+    t = p;
+    while (p < end && !py_space((unsigned char)*p)) ++p;
+    n = (int)(p - t);
+    return true;
+  }
+};
+
+}  // namespace
+
+extern "C" int ow_parse_ascii_stl(const char* data, int64_t len, float* tris, int64_t cap, int64_t* out_n) {
+  *out_n = 0;
+  // 1. tokenize in parallel chunks (boundaries moved to whitespace); any
+  //    non-ASCII byte sends the file to the reference-faithful parser
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt == 0) nt = 4;
+  if (nt > 32) nt = 32;
+  if (len < (int64_t(1) << 20)) nt = 1;
+  std::vector<int64_t> cut(nt + 1);
+  cut[0] = 0;
+  cut[nt] = len;
+  for (unsigned t = 1; t < nt; ++t) {
+    int64_t c = len * t / nt;
+    if (c < cut[t - 1]) c = cut[t - 1];
+    while (c < len && !py_space((unsigned char)data[c])) ++c;
+    cut[t] = c;
+  }
+  std::vector<std::vector<std::pair<int64_t, int>>> part(nt);
+  std::vector<int> bad(nt, 0);
+  {
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+      th.emplace_back([&, t]() {
+        for (int64_t i = cut[t]; i < cut[t + 1]; ++i)
+          if ((unsigned char)data[i] >= 0x80) {
+            bad[t] = 1;
+            return;
+          }
+        auto& v = part[t];
+        v.reserve((size_t)((cut[t + 1] - cut[t]) / 6 + 16));
+        Tok k{data + cut[t], data + cut[t + 1], nullptr, 0};
+        while (k.next()) v.emplace_back((int64_t)(k.t - data), k.n);
+      });
+    for (auto& x : th) x.join();
+  }
+  for (unsigned t = 0; t < nt; ++t)
+    if (bad[t]) return OW_ERR_PARSE;
+  size_t ntok = 0;
+  for (auto& v : part) ntok += v.size();
+  std::vector<std::pair<int64_t, int>> tok;
+  tok.reserve(ntok);
+  for (auto& v : part) tok.insert(tok.end(), v.begin(), v.end());
+  auto T = [&](size_t i) { return data + tok[i].first; };
+  auto N = [&](size_t i) { return tok[i].second; };
+  // 2. grammar walk (sequential); number tokens are only located here
+  size_t i = 0;
+  if (ntok == 0 || !ieq(T(0), N(0), "solid")) return OW_ERR_PARSE;
+  ++i;
+  while (i < ntok && !ieq(T(i), N(i), "facet") && !ieq(T(i), N(i), "endsolid")) ++i;
+  std::vector<size_t> facet_at;  // token index of each facet's "facet"
+  while (true) {
+    if (i >= ntok) return OW_ERR_PARSE;  // unexpected end of file
+    if (ieq(T(i), N(i), "endsolid")) break;
+    // facet normal n n n outer loop (vertex x y z) x3 endloop endfacet: 21 tokens
+    if (i + 21 > ntok) return OW_ERR_PARSE;
+    if (!ieq(T(i), N(i), "facet") || !ieq(T(i + 1), N(i + 1), "normal") || !ieq(T(i + 5), N(i + 5), "outer") ||
+        !ieq(T(i + 6), N(i + 6), "loop") || !ieq(T(i + 7), N(i + 7), "vertex") ||
+        !ieq(T(i + 11), N(i + 11), "vertex") || !ieq(T(i + 15), N(i + 15), "vertex") ||
+        !ieq(T(i + 19), N(i + 19), "endloop") || !ieq(T(i + 20), N(i + 20), "endfacet"))
+      return OW_ERR_PARSE;
+    facet_at.push_back(i);
+    i += 21;
+  }
+  // trailing solid-name tokens are allowed, other keywords are not
+  for (size_t j = i + 1; j < ntok; ++j)
+    if (ieq(T(j), N(j), "facet") || ieq(T(j), N(j), "solid") || ieq(T(j), N(j), "vertex") ||
+        ieq(T(j), N(j), "endsolid"))
+      return OW_ERR_PARSE;
+  const int64_t nf = (int64_t)facet_at.size();
+  if (nf > cap) return OW_ERR_CAPACITY;
+  // 3. numbers in parallel: normals are validated, vertices converted
+  std::vector<int> nbad(nt, 0);
+  {
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+      th.emplace_back([&, t]() {
+        const int64_t a = nf * t / nt, b = nf * (t + 1) / nt;
+        static const int num_at[12] = {2, 3, 4, 8, 9, 10, 12, 13, 14, 16, 17, 18};
+        for (int64_t fct = a; fct < b; ++fct) {
+          const size_t base = facet_at[(size_t)fct];
+          for (int q = 0; q < 12; ++q) {
+            double v;
+            const size_t k = base + num_at[q];
+            if (!py_float(T(k), N(k), &v)) {
+              nbad[t] = 1;
+              return;
+            }
+            if (q >= 3) tris[fct * 9 + (q - 3)] = (float)v;  // one rounding, as np.asarray(..., float32)
+          }
+        }
+      });
+    for (auto& x : th) x.join();
+  }
+  for (unsigned t = 0; t < nt; ++t)
+    if (nbad[t]) return OW_ERR_PARSE;
+  *out_n = nf;
   return OW_OK;
 }

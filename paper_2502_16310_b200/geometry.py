@@ -343,6 +343,18 @@ def _parse_binary(data, path):
 
 
 def _parse_ascii(data, path):
+    """Native fast path first (ow_parse_ascii_stl); on anything it does not
+    accept, the reference-faithful parser below reports the exact error."""
+    cap = len(data) // 64 + 1  # a facet takes > 64 bytes of ASCII text
+    tris = np.empty((cap, 3, 3), np.float32)
+    n = C.c_int64(0)
+    if _lib.lib().ow_parse_ascii_stl(bytes(data), len(data), tris.ctypes.data_as(C.c_void_p), cap, C.byref(n)) == 0:
+        coords = np.ascontiguousarray(np.transpose(tris[: n.value], (1, 2, 0)))
+        return CoordListGeometry(3, coords)
+    return _parse_ascii_py(data, path)
+
+
+def _parse_ascii_py(data, path):
     try:
         text = data.decode("utf-8", errors="strict")
     except UnicodeDecodeError:

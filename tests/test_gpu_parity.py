@@ -618,3 +618,39 @@ def test_gpu_referee_sampler_matches_reference_run(ow):
     _, exact2 = validate.referee_pairs(seg, pts2, d2)
     ref2 = [op.point_segment_distance(pts2[i], seg[i, 0], seg[i, 1]) for i in range(3000)]
     np.testing.assert_array_equal(exact2, np.asarray(ref2))
+
+
+def test_ascii_stl_native_fast_path(ow, tmp_path):
+    """The native ASCII parser gives the reference parser's float32 vertices
+    (float() then one rounding) on valid text, including Python-only float
+    spellings (underscores, inf/nan, '5.', '.5'), and defers every error to
+    the reference-faithful parser (same messages and line numbers)."""
+    import ctypes as C
+
+    from paper_2502_16310_b200 import _lib, geometry
+    from paper_2502_16310_b200 import shapes
+
+    tris = shapes.icosphere_triangles(2).astype(np.float32)
+    lines = ["solid s"]
+    for t in tris:
+        lines += [" facet normal 0 0 1", "  outer loop"]
+        lines += ["   vertex %r %r %r" % (float(v[0]), float(v[1]), float(v[2])) for v in t]
+        lines += ["  endloop", " endfacet"]
+    lines.append("endsolid s")
+    data = ("\n".join(lines) + "\n").encode()
+    g = ow.import_stl_bytes(data)
+    np.testing.assert_array_equal(g.coords_numpy(), np.ascontiguousarray(np.transpose(tris, (1, 2, 0))))
+    odd = (b"solid x facet normal 1_0 0 .5e-1_0 outer loop vertex 1_0.2_5 0.25 1e-4_0 vertex +.5 5. 1e-3 "
+           b"vertex 1 2 3 endloop endfacet endsolid x")
+    out = np.empty((2, 3, 3), np.float32)
+    n = C.c_int64(0)
+    assert _lib.lib().ow_parse_ascii_stl(odd, len(odd), out.ctypes.data_as(C.c_void_p), 2, C.byref(n)) == 0
+    ref = np.asarray([[float("1_0.2_5"), 0.25, float("1e-4_0")], [0.5, 5.0, 1e-3], [1, 2, 3]], np.float64)
+    np.testing.assert_array_equal(out[0], ref.astype(np.float32))
+    for bad, msg in ((b"solid x\nfacet normal 0 0 0\nouter loop\nvertex 0x1p3 2 3\n", "expected a number"),
+                     (b"solid x\nfacet normal 0 0 0\nouter lop\n", "expected 'loop'"),
+                     (b"solid x\nfacet normal 0 0 0\n", "unexpected end of file")):
+        with pytest.raises(ow.GeometryParseError, match=msg):
+            geometry._parse_ascii(bad, "f.stl")
+        with pytest.raises(ow.GeometryParseError, match=msg):
+            geometry._parse_ascii_py(bad, "f.stl")
