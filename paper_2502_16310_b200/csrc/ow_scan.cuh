@@ -71,24 +71,42 @@ k_scan(Load load, Store store, int64_t n, int64_t n_tiles, unsigned long long* s
   const int64_t agg = s_warp[SCAN_THREADS / 32 - 1];
   const int64_t thread_excl = (warp ? s_warp[warp - 1] : 0) + x - sum;
   const unsigned long long tag = epoch << ST_EPOCH_SHIFT;
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
+    // decoupled look-back, one warp: publish the aggregate, then inspect a
+    // window of 32 predecessors per step (lane k reads tile p - k) until an
+    // inclusive prefix appears; each step costs one round of parallel loads
     int64_t prefix = 0;
     if (tile == 0) {
-      st_status(&status[0], ST_INC | tag | (unsigned long long)agg);
+      if (lane == 0) st_status(&status[0], ST_INC | tag | (unsigned long long)agg);
     } else {
-      st_status(&status[tile], ST_AGG | tag | (unsigned long long)agg);
-      int64_t p = tile - 1;
+      if (lane == 0) st_status(&status[tile], ST_AGG | tag | (unsigned long long)agg);
+      int64_t p = tile - 1;  // newest predecessor of the current window
       while (true) {
-        unsigned long long st = ld_status(&status[p]);
-        if ((st & ~(3ull << 62)) >> ST_EPOCH_SHIFT != epoch) continue;  // not yet published this scan
-        prefix += (int64_t)(st & ST_VAL);
-        if ((st >> 62) == 2) break;
-        --p;
+        const int64_t q = p - lane;
+        unsigned long long st = 0;
+        bool ready = true;
+        if (q >= 0) {
+          st = ld_status(&status[q]);
+          ready = ((st & ~(3ull << 62)) >> ST_EPOCH_SHIFT) == epoch;
+        }
+        if (!__all_sync(0xffffffffu, ready)) continue;  // some predecessor not yet published
+        const bool inc = q >= 0 && (st >> 62) == 2;
+        const unsigned im = __ballot_sync(0xffffffffu, inc);
+        // lanes up to (and including) the nearest inclusive one contribute
+        const int stop = im ? __ffs(im) - 1 : 31;
+        int64_t val = (q >= 0 && lane <= stop) ? (int64_t)(st & ST_VAL) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        prefix += val;
+        if (im || p - 31 < 0) break;
+        p -= 32;
       }
-      st_status(&status[tile], ST_INC | tag | (unsigned long long)(prefix + agg));
+      if (lane == 0) st_status(&status[tile], ST_INC | tag | (unsigned long long)(prefix + agg));
     }
-    s_prefix = prefix;
-    if (tile == n_tiles - 1 && total_out) *total_out = prefix + agg;
+    if (lane == 0) {
+      s_prefix = prefix;
+      if (tile == n_tiles - 1 && total_out) *total_out = prefix + agg;
+    }
   }
   __syncthreads();
   int64_t run = s_prefix + thread_excl;
