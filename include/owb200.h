@@ -253,7 +253,8 @@ typedef struct {
   int64_t n_boundary;
   int64_t lattice_stats[3];
   int32_t host_copied;      /* bit 0: forest arrays, bit 1: boundary rows */
-  int32_t _pad2;
+  int32_t reran;            /* 1: the device-resident level loop outgrew the forest capacity
+                               and the pass reran with a host round trip per level */
 } ow_g2g_result;
 /* Binary STL records (or, with d_records NULL, coords already in d_coords) ->
  * validated SoA geometry -> root grid in `f` (capacity preallocated, grown

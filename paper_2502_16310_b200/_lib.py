@@ -147,7 +147,7 @@ class G2GResultC(C.Structure):  # ow_g2g_result
         ("n_boundary", C.c_int64),
         ("lattice_stats", C.c_int64 * 3),
         ("host_copied", C.c_int32),
-        ("_pad2", C.c_int32),
+        ("reran", C.c_int32),
     ]
 
 

@@ -9,7 +9,7 @@
 #include "../../include/owb200.h"
 
 #define OW_SMS 148  // B200 SM count: persistent grids are sized in multiples of it
-#define OW_PINNED_WORDS 256
+#define OW_PINNED_WORDS 512
 
 // ---------------------------------------------------------------------------
 // errors
@@ -137,6 +137,7 @@ struct ow_ctx {
   cudaStream_t copy_stream;       // side stream for result copies (lazily created)
   cudaEvent_t copy_ev[2];         // [0] forest final, [1] copies done
   bool defer_stage_times;
+  int64_t drv_spec_nl;  // leaves of the deepest level compacted by the device-resident driver (-1: none)
 };
 
 // one marking pass without a host round trip: stats accumulate in d_out[0..2]
@@ -148,12 +149,17 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
 
 int ow_stage_times(ow_ctx* ctx, ow_nearwall_result* out);
 
+// device-driven forest steps of the native driver (ow_forest.cu); refine
+// ring state per pass (int64 words, see ow_refine_dev)
+enum { RS_INTER = 0, RS_OVER, RS_MARKED, RS_SPLITS, RS_RESUME, RS_OVER_FIRST, RS_NR = 8, RS_CR = 36, RS_WORDS = 64 };
+constexpr int RS_MAX_ITERS = 26;
 // device-driven forest steps of the native driver (ow_forest.cu)
 int ow_forest_leaves_dev(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t* d_out, int64_t* d_count,
-                         cudaStream_t s);
+                         cudaStream_t s, const int64_t* d_nb = nullptr);
 int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, const int64_t* d_n, int64_t n_bound,
                      int32_t rounds, cudaStream_t s);
-int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64_t* d_st, cudaStream_t s);
+int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64_t* d_st, cudaStream_t s,
+                  int64_t* d_nb = nullptr);
 int ow_rebalance_host(ow_ctx* ctx, ow_forest* f, int64_t f0, int64_t* n_split, cudaStream_t s);
 
 // refine_marked returning the MARKED-leaf count of the split pass as well

@@ -56,6 +56,13 @@ struct LeafLoad {
   int L;
   __device__ int64_t operator()(int64_t i) const { return level[i] == L && fc[i] < 0; }
 };
+struct LeafLoadDev {  // blocks [0, *nb), the block count on the device
+  const int16_t* level;
+  const int32_t* fc;
+  const int64_t* nb;
+  int L;
+  __device__ int64_t operator()(int64_t i) const { return i < *nb && level[i] == L && fc[i] < 0; }
+};
 struct CompactStore {
   int32_t* out;
   __device__ void operator()(int64_t i, int64_t e, int64_t v) const {
@@ -79,8 +86,9 @@ struct SplitLoad {
   ForestC F;
   int L;
   int64_t* inter_flag;
+  const int64_t* nb;  // device block count (nullptr: the scan length)
   __device__ int64_t operator()(int64_t i) const {
-    if (F.level[i] != L) return 0;
+    if ((nb && i >= *nb) || F.level[i] != L) return 0;
     int8_t m = F.marks[i];
     if (m == OW_INTERMEDIATE) atomicExch((unsigned long long*)inter_flag, 1ull);
     return F.first_child[i] < 0 && m == OW_MARKED;
@@ -337,10 +345,10 @@ namespace {
 // [1] capacity overflow, [2] MARKED leaves split, [3] blocks split in total,
 // [4] frontier start to resume from on the host, [5] MARKED list did not fit,
 // [RS_NR + k] block count before split k, [RS_CR + k] length of split list k
-enum { RS_INTER = 0, RS_OVER, RS_MARKED, RS_SPLITS, RS_RESUME, RS_OVER_FIRST, RS_NR = 8, RS_CR = 36, RS_WORDS = 64 };
-constexpr int RS_MAX_ITERS = 26;
+// (layout constants RS_* in ow_common.cuh)
 
-__global__ void k_rs_init(int64_t* st, int64_t n) {
+__global__ void k_rs_init(int64_t* st, int64_t n, const int64_t* nd) {
+  if (nd) n = *nd;
   for (int i = threadIdx.x; i < RS_WORDS; i += blockDim.x) st[i] = 0;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -353,7 +361,8 @@ __global__ void k_rs_init(int64_t* st, int64_t n) {
 // n[k] + 2^D r + ci; one thread publishes n[k+1].  A list that does not fit
 // the capacity is dropped (n[k+1] = n[k]) and the frontier to resume from is
 // recorded; the MARKED list (k = 0) is not split beyond max_level.
-__global__ void k_split_ring(ow_forest f, const int32_t* __restrict__ list, int64_t* st, int k, int beyond_max) {
+__global__ void k_split_ring(ow_forest f, const int32_t* __restrict__ list, int64_t* st, int k, int beyond_max,
+                             int64_t* nb_out) {
   const int nc = 1 << f.dim;
   const int64_t base = st[RS_NR + k];
   int64_t m = st[RS_CR + k];
@@ -373,6 +382,7 @@ __global__ void k_split_ring(ow_forest f, const int32_t* __restrict__ list, int6
       st[RS_SPLITS] += m;
       st[RS_RESUME] = base;  // frontier of the newest children
     }
+    if (nb_out) *nb_out = st[RS_NR + k + 1];
   }
   if (over) return;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m * nc; t += (int64_t)gridDim.x * blockDim.x) {
@@ -455,8 +465,12 @@ __global__ void k_prop_promote_dev(int8_t* marks, const int32_t* __restrict__ le
 }  // namespace
 
 // leaves at `level` into d_out, count into *d_count (device; no readback)
+// (d_nb: the block count lives on the device; the scan then covers the capacity)
 int ow_forest_leaves_dev(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t* d_out, int64_t* d_count,
-                         cudaStream_t s) {
+                         cudaStream_t s, const int64_t* d_nb) {
+  if (d_nb)
+    return scan(ctx, LeafLoadDev{f->d_level, f->d_first_child, d_nb, level}, CompactStore{d_out}, f->capacity,
+                d_count, s);
   return scan(ctx, LeafLoad{f->d_level, f->d_first_child, level}, CompactStore{d_out}, f->n_blocks, d_count, s);
 }
 
@@ -482,7 +496,12 @@ int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, c
 // overflow or violators left after the last sweep are finished by
 // ow_rebalance_host from st[RS_RESUME] (or by a synchronous refine when the
 // MARKED list itself did not fit).
-int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64_t* d_st, cudaStream_t s) {
+//
+// d_nb (device-resident level loop): the block count is read from and the
+// final count written back to *d_nb, so f->n_blocks is stale until the caller
+// reads it.
+int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64_t* d_st, cudaStream_t s,
+                  int64_t* d_nb) {
   if (iters > RS_MAX_ITERS) iters = RS_MAX_ITERS;
   const int nc = 1 << f->dim;
   const int64_t n = f->n_blocks, cap = f->capacity;
@@ -490,12 +509,14 @@ int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64
   OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(cap + 1), s, &pl));
   OW_TRY(ow_slot(ctx, SLOT_FOREST_FLAG, (size_t)cap + 8, s, &pf));
   OW_PROF_BEGIN(ctx, PROF_REFINE, s);
-  k_rs_init<<<1, 64, 0, s>>>(d_st, n);
+  k_rs_init<<<1, 64, 0, s>>>(d_st, n, d_nb);
   OW_CUDA(cudaMemsetAsync(pf, 0, (size_t)cap, s));
-  OW_TRY(scan(ctx, SplitLoad{make_forestc(f), level, d_st + RS_INTER}, CompactStore{(int32_t*)pl}, n, d_st + RS_CR, s));
+  OW_TRY(scan(ctx, SplitLoad{make_forestc(f), level, d_st + RS_INTER, d_nb}, CompactStore{(int32_t*)pl},
+              d_nb ? cap : n, d_st + RS_CR, s));
   const ow_forest fv = *f;
   const int sg = ow_blocks(cap * nc, 256, 8 * OW_SMS);
-  k_split_ring<<<sg, 256, 0, s>>>(fv, (const int32_t*)pl, d_st, 0, level >= f->max_level);
+  k_split_ring<<<sg, 256, 0, s>>>(fv, (const int32_t*)pl, d_st, 0, level >= f->max_level,
+                                   iters == 0 ? d_nb : nullptr);
   ctx->launches += 2;
   ForestC F = make_forestc(f);
   F.n = cap;
@@ -503,7 +524,7 @@ int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64
     k_violators_dev<<<ow_blocks(cap * 2 * f->dim, 256, 8 * OW_SMS), 256, 0, s>>>(F, d_st, k, (uint8_t*)pf);
     OW_TRY(scan(ctx, FlagLoadDev{(const uint8_t*)pf, d_st + RS_NR + k}, FlagCompactClear{(int32_t*)pl, (uint8_t*)pf},
                 cap, d_st + RS_CR + k, s));
-    k_split_ring<<<sg, 256, 0, s>>>(fv, (const int32_t*)pl, d_st, k, 0);
+    k_split_ring<<<sg, 256, 0, s>>>(fv, (const int32_t*)pl, d_st, k, 0, k == iters ? d_nb : nullptr);
     ctx->launches += 2;
   }
   OW_PROF_END(ctx, PROF_REFINE, s);

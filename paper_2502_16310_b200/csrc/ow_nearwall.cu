@@ -266,7 +266,6 @@ __device__ __forceinline__ bool sweep_chunks(const MarkArgs& A, MarkSmem<D>& S, 
                                              int64_t off, int64_t cnt, const double* blo, const double* bhi,
                                              double reach2, float r2, const float (*p)[3], const bool* act,
                                              MarkCounts& cn) {
-  constexpr int PW = D == 3 ? PAY3 : PAY2;
   constexpr int CPL = D == 3 ? 2 : 1;
   int fv[CG];
   bool fok[CG];
@@ -337,12 +336,23 @@ __device__ __forceinline__ void flush_counts(const MarkArgs& A, MarkCounts& cn, 
 }
 
 template <int D, bool BINNED>
+__device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M, MarkSmem<D>& S, int64_t pos,
+                                           int lane, int wid);
+
+// persistent over the level's leaves (the count may live on the device)
+template <int D, bool BINNED>
 __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_blocks(MarkArgs A, MarkItems M) {
-  constexpr int CPL = D == 3 ? 2 : 1;
   __shared__ MarkSmem<D> S;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t pos = (int64_t)blockIdx.x * MARK_WARPS + wid;
-  if (pos >= (A.d_n ? *A.d_n : A.n_leaves)) return;
+  const int64_t n = A.d_n ? *A.d_n : A.n_leaves;
+  for (int64_t pos = (int64_t)blockIdx.x * MARK_WARPS + wid; pos < n; pos += (int64_t)gridDim.x * MARK_WARPS)
+    mark_block<D, BINNED>(A, M, S, pos, lane, wid);
+}
+
+template <int D, bool BINNED>
+__device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M, MarkSmem<D>& S, int64_t pos,
+                                           int lane, int wid) {
+  constexpr int CPL = D == 3 ? 2 : 1;
   const int id = A.leaves[pos];
   double blo[3], bhi[3];
   float p[CPL][3];
@@ -689,7 +699,9 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   if (f->dim == 3) k_chunk_boxes<3><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
   else k_chunk_boxes<2><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
   OW_PROF_BEGIN(ctx, PROF_MARK, s);
-  dim3 grd((unsigned)((n_leaves + MARK_WARPS - 1) / MARK_WARPS));
+  // persistent past 4 waves (k_mark_blocks strides over the device leaf count)
+  const int64_t nblk = (n_leaves + MARK_WARPS - 1) / MARK_WARPS;
+  dim3 grd((unsigned)(nblk < 24 * OW_SMS ? nblk : 24 * OW_SMS));
   const int gi = 8 * OW_SMS;
   if (f->dim == 3) {
     if (binned) {

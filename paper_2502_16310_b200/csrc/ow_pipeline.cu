@@ -56,6 +56,25 @@ int64_t overflow_total(const int32_t* h_counts, int64_t n_bins, int64_t bin_frac
   return acc;
 }
 
+__global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
+
+// Device-resident level loop: per pass, the words the host needs from the
+// refine ring state and the marking stats, gathered for one readback.
+constexpr int SUM_W = 13;  // [0..6) RS_INTER..RS_OVER_FIRST, [6] final blocks, [7] last sweep's list, [8..13) stats
+constexpr int DRV_RETRY = 1000;  // internal: rerun the pass with per-level host sync
+
+__global__ void k_drv_summary(const int64_t* drv, const unsigned long long* stats, int passes, int64_t* sum) {
+  for (int p = threadIdx.x; p < passes; p += blockDim.x) {
+    const int64_t* rs = drv + 72 * p + 8;
+    const int it = p + 2 < RS_MAX_ITERS ? p + 2 : RS_MAX_ITERS;
+    int64_t* o = sum + SUM_W * p;
+    for (int k = 0; k < 6; ++k) o[k] = rs[k];
+    o[6] = rs[RS_NR + it + 1];
+    o[7] = rs[RS_CR + it];
+    for (int k = 0; k < 5; ++k) o[8 + k] = (int64_t)stats[5 * p + k];
+  }
+}
+
 }  // namespace
 
 extern "C" int ow_forest_init_root(ow_ctx* ctx, ow_forest* f, void* stream) {
@@ -74,11 +93,21 @@ extern "C" int ow_forest_init_root(ow_ctx* ctx, ow_forest* f, void* stream) {
   return OW_OK;
 }
 
-extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_faces, int64_t geom_key,
-                                   const ow_grid* grid, const ow_nearwall_params* p, int32_t* d_bin_ids,
-                                   int64_t bin_ids_capacity, int32_t* d_bin_counts, int32_t* d_bin_offsets,
-                                   ow_nearwall_result* out, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
+namespace {
+// The level loop.  dev = false: the block count returns to the host after each
+// refinement (exact launch sizes; capacity overflows and deep 2:1 cascades are
+// finished on the host path, which grows the forest).  dev = true (fused pass
+// from a fresh root grid, one rank): every launch is sized by the forest
+// capacity and reads the live block count from the device, so the whole loop
+// runs without a host round trip; one readback at the end checks it, and an
+// overflow or cascade returns DRV_RETRY (the caller re-initialises the root
+// grid and reruns with dev = false).  In dev mode the leaves of the deepest
+// level are compacted too (ctx->drv_spec_nl; -1 when not available).
+int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_faces, int64_t geom_key,
+                  const ow_grid* grid, const ow_nearwall_params* p, int32_t* d_bin_ids, int64_t bin_ids_capacity,
+                  int32_t* d_bin_counts, int32_t* d_bin_offsets, ow_nearwall_result* out, cudaStream_t s, bool dev) {
+  ctx->drv_spec_nl = -1;
+  if (p->world > 1) dev = false;
   memset(out, 0, sizeof(*out));
   if (p->n_levels < 1 || p->n_levels - 1 > OW_MAX_PASSES) {
     ow_set_error("n_levels must be in [1, %d], got %d", OW_MAX_PASSES + 1, p->n_levels);
@@ -105,8 +134,15 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
   const int passes = p->n_levels - 1;
   void *stats, *drv;
   OW_TRY(ow_slot(ctx, SLOT_DRV_STATS, 40 * (size_t)passes, s, &stats));
-  OW_TRY(ow_slot(ctx, SLOT_DRV_STATE, 8 * 72 * (size_t)passes, s, &drv));
+  // [72 * pass] ring state | [72 * passes] device block count | summary
+  OW_TRY(ow_slot(ctx, SLOT_DRV_STATE, 8 * (72 * (size_t)passes + 16 + SUM_W * (size_t)passes), s, &drv));
   OW_CUDA(cudaMemsetAsync(stats, 0, 40 * (size_t)passes, s));
+  int64_t* d_nb = dev ? (int64_t*)drv + 72 * passes : nullptr;
+  int64_t* d_sum = (int64_t*)drv + 72 * passes + 8;
+  if (dev) {
+    k_set_i64<<<1, 1, 0, s>>>(d_nb, f->n_blocks);
+    OW_LAUNCHED(ctx);
+  }
   for (int level = 0; level < passes; ++level) {
     // ---- bin_setup
     OW_TRY(record(se, level, 0, s));
@@ -141,7 +177,7 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
     }
     // ---- face_detection
     OW_TRY(record(se, level, 1, s));
-    const int64_t n_host = f->n_blocks;
+    const int64_t n_host = dev ? f->capacity : f->n_blocks;  // bound on this level's leaves
     void* pl;
     OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(n_host + 1), s, &pl));
     int64_t* dn = (int64_t*)drv + 72 * level;  // [0] leaves at level, [8..72) refine state
@@ -176,7 +212,7 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
     } else {
       // leaf count stays on the device: marking is launched for n_host blocks
       // (an upper bound) and every warp checks the exact count
-      OW_TRY(ow_forest_leaves_dev(ctx, f, level, (int32_t*)pl, dn, s));
+      OW_TRY(ow_forest_leaves_dev(ctx, f, level, (int32_t*)pl, dn, s, d_nb));
       OW_TRY(ow_mark_launch(ctx, f, (const int32_t*)pl, n_host, d_coords, n_faces, geom_key,
                             p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
                             p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
@@ -197,9 +233,14 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
     OW_TRY(record(se, level, 3, s));
     // splits that would not fit the current capacity are detected on the device
     // and finished below on the host path, which grows the forest
-    const int iters = level + 2;  // a cascade of splits descends at least one level per sweep
-    OW_TRY(ow_refine_dev(ctx, f, level, iters, rs, s));
+    // a cascade of splits descends at least one level per sweep
+    const int iters = level + 2 < RS_MAX_ITERS ? level + 2 : RS_MAX_ITERS;
+    OW_TRY(ow_refine_dev(ctx, f, level, iters, rs, s, d_nb));
     OW_TRY(record(se, level, 4, s));
+    if (dev) {
+      out->n_passes = level + 1;
+      continue;
+    }
     int64_t h[64];
     OW_TRY(ow_readback(ctx, rs, 64, h, s));
     if (h[0]) {
@@ -224,7 +265,37 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
     out->n_split[level] = n_split;
     out->n_passes = level + 1;
   }
-  if (passes > 0) {
+  if (dev && passes > 0) {
+    // leaves of the deepest level (the lattice level whenever the last pass split)
+    void* pl;
+    OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(f->capacity + 1), s, &pl));
+    OW_TRY(ow_forest_leaves_dev(ctx, f, passes, (int32_t*)pl, d_sum + SUM_W * passes, s, d_nb));
+    k_drv_summary<<<1, 32, 0, s>>>((const int64_t*)drv, (const unsigned long long*)stats, passes, d_sum);
+    OW_LAUNCHED(ctx);
+    int64_t h[SUM_W * OW_MAX_PASSES + 1];
+    OW_TRY(ow_readback(ctx, d_sum, SUM_W * passes + 1, h, s));
+    for (int level = 0; level < passes; ++level) {
+      const int64_t* w = h + SUM_W * level;
+      if (w[RS_INTER]) {
+        ow_set_error("level %d still carries intermediate marks; finish propagation first", level);
+        return OW_ERR_INVALID;
+      }
+      if (w[RS_MARKED] > 0 && level >= f->max_level) {
+        ow_set_error("refinement beyond max level %d", f->max_level);
+        return OW_ERR_INVALID;
+      }
+      if (w[RS_OVER] || w[7] > 0) return DRV_RETRY;
+      f->n_blocks = w[6];
+      out->marked_refined[level] = w[RS_MARKED];
+      out->n_split[level] = w[RS_SPLITS];
+      out->marked_detected[level] = w[8];
+      out->tests[level] = w[9];
+      out->evaluated[level] = w[10];
+      out->sphere_tests[level] = w[11];
+      out->box_culls[level] = w[12];
+    }
+    ctx->drv_spec_nl = h[SUM_W * passes];
+  } else if (passes > 0) {
     int64_t h[5 * OW_MAX_PASSES];
     OW_TRY(ow_readback(ctx, (const int64_t*)stats, 5 * passes, h, s));
     for (int level = 0; level < out->n_passes; ++level) {
@@ -237,6 +308,15 @@ extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coo
   }
   if (!ctx->defer_stage_times) return ow_stage_times(ctx, out);
   return OW_OK;
+}
+}  // namespace
+
+extern "C" int ow_refine_near_wall(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_faces, int64_t geom_key,
+                                   const ow_grid* grid, const ow_nearwall_params* p, int32_t* d_bin_ids,
+                                   int64_t bin_ids_capacity, int32_t* d_bin_counts, int32_t* d_bin_offsets,
+                                   ow_nearwall_result* out, void* stream) {
+  return refine_driver(ctx, f, d_coords, n_faces, geom_key, grid, p, d_bin_ids, bin_ids_capacity, d_bin_counts,
+                       d_bin_offsets, out, (cudaStream_t)stream, false);
 }
 
 // stage times of the last driver pass from its CUDA events (all recorded
@@ -315,8 +395,14 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
   ow_nearwall_params nw = p->nw;
   if (!(nw.reach > 0.0)) nw.reach = nw.d_spec64 + 1e-3 * fmax(1.0, fmax(scale, nw.d_spec64));  // nearwall.py:38-40
   ctx->defer_stage_times = true;  // read the stage events after the lattice work is queued
-  const int st = ow_refine_near_wall(ctx, f, d_coords, n_faces, geom_key, grid, &nw, d_bin_ids, bin_ids_capacity,
-                                     d_bin_counts, d_bin_offsets, &out->nw, stream);
+  int st = refine_driver(ctx, f, d_coords, n_faces, geom_key, grid, &nw, d_bin_ids, bin_ids_capacity, d_bin_counts,
+                         d_bin_offsets, &out->nw, s, true);
+  if (st == DRV_RETRY) {  // the forest outgrew its capacity (or a deep cascade): per-level host path
+    out->reran = 1;
+    OW_TRY(ow_forest_init_root(ctx, f, stream));
+    st = refine_driver(ctx, f, d_coords, n_faces, geom_key, grid, &nw, d_bin_ids, bin_ids_capacity, d_bin_counts,
+                       d_bin_offsets, &out->nw, s, false);
+  }
   ctx->defer_stage_times = false;
   OW_TRY(st);
   int finest = 0;
@@ -352,8 +438,8 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
   }
   void* pl;
   OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(f->n_blocks + 1), s, &pl));
-  int64_t nl = 0;
-  OW_TRY(ow_forest_leaves(ctx, f, finest, (int32_t*)pl, &nl, stream));
+  int64_t nl = ctx->drv_spec_nl;  // compacted by the device-resident loop
+  if (nl < 0 || finest != out->nw.n_passes) OW_TRY(ow_forest_leaves(ctx, f, finest, (int32_t*)pl, &nl, stream));
   out->n_finest_leaves = nl;
   const int C = D == 3 ? 64 : 16;
   void *leaves64, *flags;

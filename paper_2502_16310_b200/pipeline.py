@@ -42,6 +42,7 @@ class GridPass:
     result: NearWallResult
     links: LatticeLinks | None
     host: dict | None = None  # pinned host copies of the results (run(host=True))
+    reran: bool = False  # the device-resident level loop outgrew the capacity; rerun with host sync
 
 
 class GridPlan:
@@ -186,7 +187,7 @@ class GridPlan:
         hres = None
         if host:
             hres = self._host_results(hbuf, int(out.host_copied), forest, links)
-        return GridPass(geom, forest, result, links, hres)
+        return GridPass(geom, forest, result, links, hres, bool(out.reran))
 
     def _host_results(self, hbuf, copied, forest, links):
         """Pinned host copies (the C side streamed whatever fit; the rest is

@@ -450,10 +450,13 @@ def test_marking_dense_soup_single_root(ow):
 
 
 # --------------------------------------------------------------------------- fused native pass
-def test_geometry_to_grid_matches_per_function_path(ow):
+@pytest.mark.parametrize("capacity", [None, 600])
+def test_geometry_to_grid_matches_per_function_path(ow, capacity):
     """ow_geometry_to_grid (one native call from STL records) equals the
     reference call sequence import_stl -> init_root_grid -> refine_near_wall
-    -> build_lattice_links, array for array."""
+    -> build_lattice_links, array for array.  capacity=600 (512 roots): the
+    device-resident level loop overflows and the pass reruns on the per-level
+    host path, which grows the forest."""
     import torch
 
     from paper_2502_16310_b200 import pipeline, shapes
@@ -464,9 +467,11 @@ def test_geometry_to_grid_matches_per_function_path(ow):
     rec = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda()
     dom = ow.Aabb(np.zeros(3), np.ones(3))
     params = ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8)
-    plan = pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q27")
-    plan.run(rec, n)
-    gp = plan.run(rec, n)  # second pass: preallocated outputs sized from the first
+    plan = pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q27", capacity=capacity)
+    g1 = plan.run(rec, n)
+    assert g1.reran == (capacity is not None)
+    gp = plan.run(rec, n)  # second pass: outputs and capacity sized from the first
+    assert not gp.reran
     geom = ow.import_stl_bytes(data)
     f = ow.init_root_grid(dom, (8, 8, 8))
     res = ow.refine_near_wall(f, geom, params)
@@ -474,6 +479,11 @@ def test_geometry_to_grid_matches_per_function_path(ow):
     assert torch.equal(gp.geometry.coords, geom.coords)
     assert gp.result.marked_detected == res.marked_detected and gp.result.cell_face_tests == res.cell_face_tests
     assert gp.result.marked_refined == res.marked_refined
+    for g in (g1, gp):
+        assert g.result.marked_detected == res.marked_detected
+        np.testing.assert_array_equal(g.forest._coords, f._coords)
+        np.testing.assert_array_equal(g.forest._parent, f._parent)
+        np.testing.assert_array_equal(g.forest.marks.cpu().numpy(), f.marks.cpu().numpy())
     np.testing.assert_array_equal(gp.forest._coords, f._coords)
     np.testing.assert_array_equal(gp.forest._first_child, f._first_child)
     assert gp.forest.blocks_per_level() == f.blocks_per_level()
