@@ -145,7 +145,7 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
                    int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int32_t* d_bin_ids,
                    const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,
                    double reach, unsigned long long* d_out, cudaStream_t s,
-                   const int64_t* d_n_leaves = nullptr);
+                   const int64_t* d_n_leaves = nullptr, bool chunk_boxes_ready = false);
 
 int ow_stage_times(ow_ctx* ctx, ow_nearwall_result* out);
 

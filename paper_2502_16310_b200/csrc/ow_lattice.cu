@@ -49,6 +49,7 @@ struct LatArgs {
   int8_t dc[QMAX][3];       // lattice directions c_d
   uint8_t dir_combo[32];    // combination index sum_a (c_a + 1) 3^a of direction d
   uint8_t combo_dir[27];    // direction of each combination (lattice subset)
+  unsigned combo_info[27];  // direction | (4 (c_a + 1)) << (8 + 8a): range-field shifts of a combination
   unsigned dirmask;         // combinations of the lattice's moving directions
   unsigned spread[3][8];    // per-axis non-empty-c mask -> mask over combinations
   const float* coords;
@@ -111,20 +112,39 @@ __global__ void k_lat_pos(ForestC F, int level, const int32_t* __restrict__ leav
 // on the same float32 centres.  Packed in one register: bits [4 ci, 4 ci + 4)
 // hold i0 | (ext-1) << 2 of c = ci - 1, bit 12 + ci marks an empty range.
 __device__ __forceinline__ unsigned axis_ranges(const float4 x4, float h, float lo, float hi) {
+  // e_i = fl(x_i + c h) is >= x_i for c = +1 and <= x_i for c = -1 (h > 0), so
+  // the box is [x_i, e_i] / [e_i, x_i] / {x_i} and the two comparisons with x_i
+  // are shared by the three directions
   const float x[4] = {x4.x, x4.y, x4.z, x4.w};
+  unsigned mm = 0, m0 = 0, mp = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool a = lo <= x[i], b = hi >= x[i];
+    mm |= (unsigned)(a && hi >= FADD(x[i], -h)) << i;
+    m0 |= (unsigned)(a && b) << i;
+    mp |= (unsigned)(lo <= FADD(x[i], h) && b) << i;
+  }
+  const unsigned m[3] = {mm, m0, mp};
   unsigned r = 0;
 #pragma unroll
-  for (int ci = 0; ci < 3; ++ci) {
-    const float dv = FMUL((float)(ci - 1), h);
-    unsigned m = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float en = FADD(x[i], dv);
-      m |= (unsigned)(lo <= fmaxf(x[i], en) && hi >= fminf(x[i], en)) << i;
-    }
-    r |= m == 0 ? (1u << (12 + ci)) : (((unsigned)(__ffs(m) - 1) | ((unsigned)(__popc(m) - 1) << 2)) << (4 * ci));
-  }
+  for (int ci = 0; ci < 3; ++ci)
+    r |= m[ci] == 0 ? (1u << (12 + ci))
+                    : (((unsigned)(__ffs(m[ci]) - 1) | ((unsigned)(__popc(m[ci]) - 1) << 2)) << (4 * ci));
   return r;  // contiguous by monotonicity
+}
+
+// position of the (n+1)-th set bit of v (n < popc(v)): popc bisection
+__device__ __forceinline__ int nth_set_bit(unsigned v, int n) {
+  int pos = 0, c;
+  c = __popc(v & 0xFFFFu);
+  if (n >= c) n -= c, v >>= 16, pos += 16;
+  c = __popc(v & 0xFFu);
+  if (n >= c) n -= c, v >>= 8, pos += 8;
+  c = __popc(v & 0xFu);
+  if (n >= c) n -= c, v >>= 4, pos += 4;
+  c = __popc(v & 0x3u);
+  if (n >= c) n -= c, v >>= 2, pos += 2;
+  return pos + (n >= (int)(v & 1u));
 }
 
 // row word of direction d from the packed axis ranges (0 when some axis is empty)
@@ -167,14 +187,13 @@ __device__ __forceinline__ int4 row_of(int r, int excl, unsigned valid, const un
   const int ej = __shfl_sync(0xffffffffu, excl, j);
   const int nth = r - ej;
   if (nth < 0 || nth >= __popc(vj)) return make_int4(0, 0, 0, 0);
-  const int ci = __fns(vj, 0, nth + 1);  // position of the (nth+1)-th set bit
+  const unsigned info = A.combo_info[nth_set_bit(vj, nth)];
   const unsigned Rj[3] = {Rj0, Rj1, Rj2};
-  unsigned w = (unsigned)A.combo_dir[ci];
-  int units = 1, cc = ci;
+  unsigned w = info & 0xFFu;
+  int units = 1;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    const unsigned ra = (Rj[a] >> (4 * (cc % 3))) & 0xFu;
-    cc /= 3;
+    const unsigned ra = (Rj[a] >> ((info >> (8 + 8 * a)) & 0xFFu)) & 0xFu;
     w |= ra << (5 + 4 * a);
     units *= (int)(ra >> 2) + 1;
   }
@@ -230,6 +249,7 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   }
   const int L = A.level;
   int k0[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
+  float rext[3] = {1.0f, 1.0f, 1.0f};
   int nslots = live ? 1 : 0;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
@@ -240,6 +260,7 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
     if (a1 > nmax) a1 = nmax;
     k0[a] = (int)a0;
     ext[a] = a1 >= a0 ? (int)(a1 - a0 + 1) : 0;
+    rext[a] = ext[a] ? __frcp_rn((float)ext[a]) : 0.0f;
     nslots *= ext[a];
   }
   const int max_slots = __reduce_max_sync(0xffffffffu, nslots);
@@ -251,9 +272,13 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
       int32_t nc[3] = {0, 0, 0};
       int rem = slot;
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        nc[a] = k0[a] + rem % ext[a];
-        rem /= ext[a];
+      for (int a = 0; a < D; ++a) {  // rem / ext by a float reciprocal, corrected to exact
+        int qd = (int)(__fmul_rz((float)rem, rext[a]));
+        int rr = rem - qd * ext[a];
+        while (rr < 0) rr += ext[a], --qd;
+        while (rr >= ext[a]) rr -= ext[a], ++qd;
+        nc[a] = k0[a] + rr;
+        rem = qd;
       }
       int depth;
       const int node = locate(A.F, L, nc, &depth);
@@ -598,6 +623,8 @@ LatArgs make_args(ow_ctx* ctx) {
     }
     A.dir_combo[i] = (uint8_t)ci;
     A.combo_dir[ci] = (uint8_t)i;
+    A.combo_info[ci] = (unsigned)i;
+    for (int a = 0, cc = ci; a < f->dim; ++a, cc /= 3) A.combo_info[ci] |= (unsigned)(4 * (cc % 3)) << (8 + 8 * a);
     if (i > 0) A.dirmask |= 1u << ci;
   }
   for (int a = 0; a < 3; ++a)

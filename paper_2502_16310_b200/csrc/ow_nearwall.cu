@@ -134,18 +134,32 @@ struct MarkArgs {
 template <int D>
 __global__ void k_chunk_boxes(const int32_t* __restrict__ ids, int64_t n_entries, const float4* __restrict__ box,
                               float4* cbox) {
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g * 32 >= n_entries) return;
-  float4 lo = make_float4(INFINITY, INFINITY, INFINITY, 0.0f), hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.0f);
-  const int64_t e1 = min(n_entries, g * 32 + 32);
-  for (int64_t e = g * 32; e < e1; ++e) {
-    const int64_t f = ids ? ids[e] : e;
-    const float4 l = box[2 * f], h = box[2 * f + 1];
-    lo.x = fminf(lo.x, l.x), lo.y = fminf(lo.y, l.y), lo.z = fminf(lo.z, l.z);
-    hi.x = fmaxf(hi.x, h.x), hi.y = fmaxf(hi.y, h.y), hi.z = fmaxf(hi.z, h.z);
+  // warp per chunk: independent loads, min / max (exact, order-free) by shuffles
+  const int lane = threadIdx.x & 31;
+  const int64_t n_chunks = (n_entries + 31) / 32;
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < n_chunks;
+       g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t e = g * 32 + lane;
+    float4 lo = make_float4(INFINITY, INFINITY, INFINITY, 0.0f), hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.0f);
+    if (e < n_entries) {
+      const int64_t f = ids ? ids[e] : e;
+      lo = box[2 * f];
+      hi = box[2 * f + 1];
+      lo.w = hi.w = 0.0f;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lo.x = fminf(lo.x, __shfl_xor_sync(0xffffffffu, lo.x, o));
+      lo.y = fminf(lo.y, __shfl_xor_sync(0xffffffffu, lo.y, o));
+      lo.z = fminf(lo.z, __shfl_xor_sync(0xffffffffu, lo.z, o));
+      hi.x = fmaxf(hi.x, __shfl_xor_sync(0xffffffffu, hi.x, o));
+      hi.y = fmaxf(hi.y, __shfl_xor_sync(0xffffffffu, hi.y, o));
+      hi.z = fmaxf(hi.z, __shfl_xor_sync(0xffffffffu, hi.z, o));
+    }
+    if (lane == 0) {
+      cbox[2 * g] = lo;
+      cbox[2 * g + 1] = hi;
+    }
   }
-  cbox[2 * g] = lo;
-  cbox[2 * g + 1] = hi;
 }
 
 // Marking, two flat passes so no block's work is one long serial chain:
@@ -646,7 +660,8 @@ __global__ void k_near_pairs(int dim, const float* __restrict__ pts, const float
 int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves, const float* d_coords,
                    int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int32_t* d_bin_ids,
                    const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,
-                   double reach, unsigned long long* out, cudaStream_t s, const int64_t* d_n_leaves) {
+                   double reach, unsigned long long* out, cudaStream_t s, const int64_t* d_n_leaves,
+                   bool chunk_boxes_ready) {
   if (!(d_spec > 0.0f)) {
     ow_set_error("near-wall distance must be positive, got %g", (double)d_spec);
     return OW_ERR_INVALID;
@@ -695,9 +710,11 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   M.cap = cap;
   M.hit = (unsigned*)ph;
   OW_CUDA(cudaMemsetAsync(ph, 0, 4 * (size_t)(n_leaves + (n_leaves & 1)) + 8, s));
-  const int cg = ow_blocks((n_entries + 31) / 32, 128);
-  if (f->dim == 3) k_chunk_boxes<3><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
-  else k_chunk_boxes<2><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
+  if (!chunk_boxes_ready) {  // the driver reuses them while the bins and face boxes are unchanged
+    const int cg = ow_blocks((n_entries + 31) / 32, 4, 16 * OW_SMS);
+    if (f->dim == 3) k_chunk_boxes<3><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
+    else k_chunk_boxes<2><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
+  }
   OW_PROF_BEGIN(ctx, PROF_MARK, s);
   // persistent past 4 waves (k_mark_blocks strides over the device leaf count)
   const int64_t nblk = (n_leaves + MARK_WARPS - 1) / MARK_WARPS;

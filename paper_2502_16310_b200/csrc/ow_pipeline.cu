@@ -146,7 +146,9 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
   for (int level = 0; level < passes; ++level) {
     // ---- bin_setup
     OW_TRY(record(se, level, 0, s));
+    bool fresh_bins = level == 0;  // chunk boxes of the bins (marking) need a rebuild
     if (p->binned && (!have_bins || !p->reuse_bins)) {
+      fresh_bins = true;
       int64_t outside = -1;
       OW_TRY(ow_fill_bins_count(ctx, grid, d_coords, n_faces, p->spacing, d_bin_counts, &E, &outside, s));
       if (outside >= 0) {
@@ -195,7 +197,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
       OW_TRY(ow_mark_launch(ctx, f, (const int32_t*)pl + lo, hi - lo, d_coords, n_faces, geom_key,
                             p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
                             p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
-                            p->binned ? E : 0, p->d_spec, p->reach, dst, s));
+                            p->binned ? E : 0, p->d_spec, p->reach, dst, s, nullptr, !fresh_bins));
       if (!p->exchange) {
         ow_set_error("refine_near_wall: world > 1 needs an exchange callback");
         return OW_ERR_INVALID;
@@ -216,7 +218,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
       OW_TRY(ow_mark_launch(ctx, f, (const int32_t*)pl, n_host, d_coords, n_faces, geom_key,
                             p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
                             p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
-                            p->binned ? E : 0, p->d_spec, p->reach, dst, s, dn));
+                            p->binned ? E : 0, p->d_spec, p->reach, dst, s, dn, !fresh_bins));
     }
     // ---- propagation (binned only): 1 + floor(d / min block length)
     OW_TRY(record(se, level, 2, s));

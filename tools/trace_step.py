@@ -61,5 +61,13 @@ for a, b in zip(ks, ks[1:]):
         gaps.append((g, a["name"][:50], b["name"][:50], b["ts"]))
 print(f"idle between GPU ops: {sum(g for g, *_ in gaps):.1f} us in {len(gaps)} gaps > 5 us; first op at +{ks[0]['ts'] - t0:.1f} us")
 cpu = [e for e in ev if e.get("ph") == "X" and e.get("cat") in ("cpu_op", "user_annotation", "python_function")]
-for g, a, b, ts in sorted(gaps, reverse=True)[:25]:
+for g, a, b, ts in sorted(gaps, reverse=True)[:8]:
     print(f"{g:8.1f} us  after {a:50s} before {b}")
+agg = {}
+for k in ks:
+    nm = k["name"].replace("(anonymous namespace)::", "").split("(")[0][:60]
+    c, t = agg.get(nm, (0, 0.0))
+    agg[nm] = (c + 1, t + k["dur"])
+print("per kernel (last step):")
+for nm, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:30]:
+    print(f"{t:9.1f} us {c:4d}x  {nm}")
