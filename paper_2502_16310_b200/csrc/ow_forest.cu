@@ -14,6 +14,7 @@
 namespace {
 
 using ow::scan;
+using ow::scan01;
 
 __global__ void k_cell_centers(ForestC F, const int32_t* __restrict__ ids, int64_t n, float* out) {
   const int C = F.dim == 2 ? 16 : 64;
@@ -54,14 +55,7 @@ struct LeafLoad {
   const int16_t* level;
   const int32_t* fc;
   int L;
-  __device__ int64_t operator()(int64_t i) const { return level[i] == L && fc[i] < 0; }
-};
-struct LeafLoadDev {  // blocks [0, *nb), the block count on the device
-  const int16_t* level;
-  const int32_t* fc;
-  const int64_t* nb;
-  int L;
-  __device__ int64_t operator()(int64_t i) const { return i < *nb && level[i] == L && fc[i] < 0; }
+  __device__ int64_t operator()(int64_t i) const { return (level[i] == L) & (fc[i] < 0); }
 };
 struct CompactStore {
   int32_t* out;
@@ -86,12 +80,14 @@ struct SplitLoad {
   ForestC F;
   int L;
   int64_t* inter_flag;
-  const int64_t* nb;  // device block count (nullptr: the scan length)
   __device__ int64_t operator()(int64_t i) const {
-    if ((nb && i >= *nb) || F.level[i] != L) return 0;
-    int8_t m = F.marks[i];
+    // unconditional loads (issued together)
+    const int lv = F.level[i];
+    const int8_t m = F.marks[i];
+    const int32_t fc = F.first_child[i];
+    if (lv != L) return 0;
     if (m == OW_INTERMEDIATE) atomicExch((unsigned long long*)inter_flag, 1ull);
-    return F.first_child[i] < 0 && m == OW_MARKED;
+    return fc < 0 && m == OW_MARKED;
   }
 };
 
@@ -214,7 +210,7 @@ int split_list(ow_ctx* ctx, ow_forest* f, const int32_t* list, int64_t m, cudaSt
 extern "C" int ow_forest_leaves(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t* d_out, int64_t* out_n,
                                 void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  OW_TRY(scan(ctx, LeafLoad{f->d_level, f->d_first_child, level}, CompactStore{d_out}, f->n_blocks,
+  OW_TRY(scan01(ctx, LeafLoad{f->d_level, f->d_first_child, level}, CompactStore{d_out}, f->n_blocks,
               ctx->d_small + 8, s));
   return ow_readback(ctx, ctx->d_small + 8, 1, out_n, s);
 }
@@ -241,7 +237,7 @@ extern "C" int ow_forest_level_counts(ow_ctx* ctx, const ow_forest* f, int64_t* 
 extern "C" int ow_forest_count_marks(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t leaf_only,
                                      int32_t mark, int64_t* out_n, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  OW_TRY(scan(ctx, MarkCountLoad{make_forestc(f), level, leaf_only, mark}, NullStore{}, f->n_blocks,
+  OW_TRY(scan01(ctx, MarkCountLoad{make_forestc(f), level, leaf_only, mark}, NullStore{}, f->n_blocks,
               ctx->d_small + 8, s));
   return ow_readback(ctx, ctx->d_small + 8, 1, out_n, s);
 }
@@ -295,7 +291,7 @@ static int refine_marked_impl(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t*
   void* pl;
   OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(f->n_blocks + 1), s, &pl));
   OW_CUDA(cudaMemsetAsync(small + 9, 0, 8, s));
-  OW_TRY(scan(ctx, SplitLoad{make_forestc(f), level, small + 9}, CompactStore{(int32_t*)pl}, f->n_blocks, small + 8, s));
+  OW_TRY(scan01(ctx, SplitLoad{make_forestc(f), level, small + 9}, CompactStore{(int32_t*)pl}, f->n_blocks, small + 8, s));
   int64_t h[2];
   OW_TRY(ow_readback(ctx, small + 8, 2, h, s));
   if (h[1]) {
@@ -322,7 +318,7 @@ static int refine_marked_impl(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t*
     OW_LAUNCHED(ctx);
     OW_CHECK_LAUNCH();
     OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(f1 + 1), s, &pl));
-    OW_TRY(scan(ctx, FlagLoad{(const uint8_t*)pf}, CompactStore{(int32_t*)pl}, f1, small + 8, s));
+    OW_TRY(scan01(ctx, FlagLoad{(const uint8_t*)pf}, CompactStore{(int32_t*)pl}, f1, small + 8, s));
     OW_TRY(ow_readback(ctx, small + 8, 1, h, s));
     int64_t v = h[0];
     if (v == 0) break;
@@ -420,11 +416,6 @@ __global__ void k_violators_dev(ForestC F, const int64_t* st, int k, uint8_t* fl
   }
 }
 
-struct FlagLoadDev {  // violator flags of blocks [0, n), n on the device
-  const uint8_t* flag;
-  const int64_t* n;
-  __device__ int64_t operator()(int64_t i) const { return i < *n && flag[i] != 0; }
-};
 struct FlagCompactClear {  // compaction that also clears the flags it consumed
   int32_t* out;
   uint8_t* flag;
@@ -469,9 +460,9 @@ __global__ void k_prop_promote_dev(int8_t* marks, const int32_t* __restrict__ le
 int ow_forest_leaves_dev(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t* d_out, int64_t* d_count,
                          cudaStream_t s, const int64_t* d_nb) {
   if (d_nb)
-    return scan(ctx, LeafLoadDev{f->d_level, f->d_first_child, d_nb, level}, CompactStore{d_out}, f->capacity,
-                d_count, s);
-  return scan(ctx, LeafLoad{f->d_level, f->d_first_child, level}, CompactStore{d_out}, f->n_blocks, d_count, s);
+    return scan01(ctx, LeafLoad{f->d_level, f->d_first_child, level}, CompactStore{d_out}, f->capacity, d_count, s,
+                  d_nb);
+  return scan01(ctx, LeafLoad{f->d_level, f->d_first_child, level}, CompactStore{d_out}, f->n_blocks, d_count, s);
 }
 
 int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, const int64_t* d_n, int64_t n_bound,
@@ -511,8 +502,8 @@ int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64
   OW_PROF_BEGIN(ctx, PROF_REFINE, s);
   k_rs_init<<<1, 64, 0, s>>>(d_st, n, d_nb);
   OW_CUDA(cudaMemsetAsync(pf, 0, (size_t)cap, s));
-  OW_TRY(scan(ctx, SplitLoad{make_forestc(f), level, d_st + RS_INTER, d_nb}, CompactStore{(int32_t*)pl},
-              d_nb ? cap : n, d_st + RS_CR, s));
+  OW_TRY(scan01(ctx, SplitLoad{make_forestc(f), level, d_st + RS_INTER}, CompactStore{(int32_t*)pl},
+                d_nb ? cap : n, d_st + RS_CR, s, d_nb));
   const ow_forest fv = *f;
   const int sg = ow_blocks(cap * nc, 256, 8 * OW_SMS);
   k_split_ring<<<sg, 256, 0, s>>>(fv, (const int32_t*)pl, d_st, 0, level >= f->max_level,
@@ -522,8 +513,9 @@ int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64
   F.n = cap;
   for (int k = 1; k <= iters; ++k) {
     k_violators_dev<<<ow_blocks(cap * 2 * f->dim, 256, 8 * OW_SMS), 256, 0, s>>>(F, d_st, k, (uint8_t*)pf);
-    OW_TRY(scan(ctx, FlagLoadDev{(const uint8_t*)pf, d_st + RS_NR + k}, FlagCompactClear{(int32_t*)pl, (uint8_t*)pf},
-                cap, d_st + RS_CR + k, s));
+    // violator flags of blocks [0, n[k]), n[k] on the device
+    OW_TRY(scan01(ctx, FlagLoad{(const uint8_t*)pf}, FlagCompactClear{(int32_t*)pl, (uint8_t*)pf}, cap,
+                  d_st + RS_CR + k, s, d_st + RS_NR + k));
     k_split_ring<<<sg, 256, 0, s>>>(fv, (const int32_t*)pl, d_st, k, 0, k == iters ? d_nb : nullptr);
     ctx->launches += 2;
   }
@@ -547,7 +539,7 @@ int ow_rebalance_host(ow_ctx* ctx, ow_forest* f, int64_t f0, int64_t* n_split, c
     OW_LAUNCHED(ctx);
     OW_CHECK_LAUNCH();
     OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(f1 + 1), s, &pl));
-    OW_TRY(scan(ctx, FlagLoad{(const uint8_t*)pf}, CompactStore{(int32_t*)pl}, f1, small + 8, s));
+    OW_TRY(scan01(ctx, FlagLoad{(const uint8_t*)pf}, CompactStore{(int32_t*)pl}, f1, small + 8, s));
     OW_TRY(ow_readback(ctx, small + 8, 1, h, s));
     if (h[0] == 0) break;
     *n_split += h[0];

@@ -754,7 +754,7 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   }
   ctx->launches += 2;
   OW_CHECK_LAUNCH();
-  OW_TRY(scan(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s));
+  OW_TRY(ow::scan01(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s));
   OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
   const int64_t tiles_max = ucap / MT_TILE + 1;
   if (D == 3) k_lat_mt<3><<<ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s>>>(A);

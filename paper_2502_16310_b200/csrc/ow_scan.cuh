@@ -10,10 +10,11 @@ namespace ow {
 constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+constexpr int64_t SCAN_MAX_CHUNKS = 8 * OW_SMS;  // one wave of 256-thread CTAs
 // Status words carry an epoch so the array never needs clearing between
 // scans: [63:62] flag (1 aggregate, 2 inclusive prefix), [61:46] epoch,
-// [45:0] value (sums < 2^46).  The tile-ticket counter is reset by the last
-// tile to finish.
+// [45:0] value (sums < 2^46).  Tiles are blockIdx order: CTAs dispatch in
+// index order, so every predecessor a tile waits on is already running.
 constexpr unsigned long long ST_AGG = 1ull << 62;
 constexpr unsigned long long ST_INC = 2ull << 62;
 constexpr unsigned long long ST_VAL = (1ull << 46) - 1;
@@ -28,101 +29,151 @@ __device__ __forceinline__ unsigned long long ld_status(const unsigned long long
   return v;
 }
 
-// Load: int64_t operator()(int64_t i) const      (non-negative values)
+// Load: int64_t operator()(int64_t i) const      (non-negative values; may be
+//       called twice per index, so it must be free of non-idempotent effects)
 // Store: void operator()(int64_t i, int64_t exclusive_prefix, int64_t value) const
+//
+// Decoupled look-back by one warp (all lanes call it; agg is warp-uniform):
+// publish this tile's aggregate, then inspect 128 predecessors per step (lane
+// k, window j reads tile p - k - 32 j) until an inclusive prefix appears;
+// publish the inclusive prefix and return the exclusive one.
+__device__ __forceinline__ int64_t lookback(unsigned long long* status, int64_t tile, int64_t agg,
+                                            unsigned long long epoch, int lane) {
+  const unsigned long long tag = epoch << ST_EPOCH_SHIFT;
+  int64_t prefix = 0;
+  if (tile == 0) {
+    if (lane == 0) st_status(&status[0], ST_INC | tag | (unsigned long long)agg);
+    return 0;
+  }
+  if (lane == 0) st_status(&status[tile], ST_AGG | tag | (unsigned long long)agg);
+  int64_t p = tile - 1;  // newest predecessor of the current window
+  while (true) {
+    unsigned long long st[4];
+    bool ready = true;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = p - lane - 32 * j;
+      st[j] = q >= 0 ? ld_status(&status[q]) : 0ull;
+      ready &= q < 0 || ((st[j] & ~(3ull << 62)) >> ST_EPOCH_SHIFT) == epoch;
+    }
+    if (!__all_sync(0xffffffffu, ready)) {  // some predecessor not yet published
+      __nanosleep(64);
+      continue;
+    }
+    int jstop = 4, lstop = 31;
+#pragma unroll
+    for (int j = 3; j >= 0; --j) {
+      const unsigned im = __ballot_sync(0xffffffffu, p - lane - 32 * j >= 0 && (st[j] >> 62) == 2);
+      if (im) jstop = j, lstop = __ffs(im) - 1;
+    }
+    int64_t val = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (p - lane - 32 * j >= 0 && (j < jstop || (j == jstop && lane <= lstop))) val += (int64_t)(st[j] & ST_VAL);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+    prefix += val;
+    if (jstop < 4 || p - 127 < 0) break;
+    p -= 128;
+  }
+  if (lane == 0) st_status(&status[tile], ST_INC | tag | (unsigned long long)(prefix + agg));
+  return prefix;
+}
+
+// Chunked reduce-then-scan: each CTA takes a contiguous chunk of whole tiles
+// (chunks in ticket order) and each of its warps a contiguous slice of the
+// chunk.  Pass 1 sums the slices with coalesced loads (SCAN_ITEMS in flight
+// per thread); the chunk aggregate is published and one warp looks back over
+// 128 predecessors per step; pass 2 rescans every slice independently (warp
+// scans only, no CTA barrier; the re-read hits L2) and stores.  One tile per
+// CTA would make the look-back chain grow with n / SCAN_TILE and dominate:
+// when tiles are cheap every tile looks back at once.
 template <class Load, class Store>
 __global__ void __launch_bounds__(SCAN_THREADS)
-k_scan(Load load, Store store, int64_t n, int64_t n_tiles, unsigned long long* status, unsigned int* tile_ctr,
+k_scan(Load load, Store store, int64_t n, int64_t n_chunks, int64_t chunk, unsigned long long* status,
        int64_t* total_out, unsigned long long epoch) {
-  __shared__ int s_tile;
-  __shared__ int64_t s_warp[SCAN_THREADS / 32];
-  __shared__ int64_t s_prefix;
-  if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_ctr, 1u);
-  __syncthreads();
-  const int64_t tile = s_tile;
-  const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+  constexpr int W = SCAN_THREADS / 32;
+  __shared__ int64_t s_warp[W];
+  const int64_t tile = blockIdx.x;  // chunk index (CTAs dispatch in index order)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wch = chunk / W;  // slice length (a multiple of 32 * SCAN_ITEMS)
+  const int64_t w0 = min(n, tile * chunk + warp * wch), w1 = min(n, w0 + wch);
+  const bool one = w1 - w0 <= 32 * SCAN_ITEMS;  // single-step slice: keep the values
   int64_t v[SCAN_ITEMS];
   int64_t sum = 0;
+  if (one) {
+    const int64_t base = w0 + lane * SCAN_ITEMS;
 #pragma unroll
-  for (int k = 0; k < SCAN_ITEMS; ++k) {
-    int64_t i = base + k;
-    v[k] = (i < n) ? load(i) : 0;
-    sum += v[k];
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int64_t x = sum;
+    for (int k = 0; k < SCAN_ITEMS; ++k) v[k] = base + k < w1 ? load(base + k) : 0;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+    for (int k = 0; k < SCAN_ITEMS; ++k) sum += v[k];
+  } else {
+    for (int64_t i0 = w0 + lane; i0 < w1; i0 += 32 * SCAN_ITEMS) {
+#pragma unroll
+      for (int k = 0; k < SCAN_ITEMS; ++k) v[k] = i0 + k * 32 < w1 ? load(i0 + k * 32) : 0;
+#pragma unroll
+      for (int k = 0; k < SCAN_ITEMS; ++k) sum += v[k];
+    }
   }
-  if (lane == 31) s_warp[warp] = x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) s_warp[warp] = sum;
   __syncthreads();
   if (warp == 0) {
-    int64_t w = (lane < SCAN_THREADS / 32) ? s_warp[lane] : 0;
+    int64_t x = lane < W ? s_warp[lane] : 0;  // exclusive scan of the slice sums
 #pragma unroll
-    for (int o = 1; o < SCAN_THREADS / 32; o <<= 1) {
-      int64_t y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
+    for (int o = 1; o < W; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    if (lane < SCAN_THREADS / 32) s_warp[lane] = w;
+    const int64_t agg = __shfl_sync(0xffffffffu, x, W - 1);
+    const int64_t wex = x - (lane < W ? s_warp[lane] : 0);
+    const int64_t prefix = lookback(status, tile, agg, epoch, lane);
+    if (lane < W) s_warp[lane] = prefix + wex;  // start of every slice
+    if (lane == 0 && tile == n_chunks - 1 && total_out) *total_out = prefix + agg;
   }
   __syncthreads();
-  const int64_t agg = s_warp[SCAN_THREADS / 32 - 1];
-  const int64_t thread_excl = (warp ? s_warp[warp - 1] : 0) + x - sum;
-  const unsigned long long tag = epoch << ST_EPOCH_SHIFT;
-  if (warp == 0) {
-    // decoupled look-back, one warp: publish the aggregate, then inspect a
-    // window of 32 predecessors per step (lane k reads tile p - k) until an
-    // inclusive prefix appears; each step costs one round of parallel loads
-    int64_t prefix = 0;
-    if (tile == 0) {
-      if (lane == 0) st_status(&status[0], ST_INC | tag | (unsigned long long)agg);
-    } else {
-      if (lane == 0) st_status(&status[tile], ST_AGG | tag | (unsigned long long)agg);
-      int64_t p = tile - 1;  // newest predecessor of the current window
-      while (true) {
-        const int64_t q = p - lane;
-        unsigned long long st = 0;
-        bool ready = true;
-        if (q >= 0) {
-          st = ld_status(&status[q]);
-          ready = ((st & ~(3ull << 62)) >> ST_EPOCH_SHIFT) == epoch;
-        }
-        if (!__all_sync(0xffffffffu, ready)) continue;  // some predecessor not yet published
-        const bool inc = q >= 0 && (st >> 62) == 2;
-        const unsigned im = __ballot_sync(0xffffffffu, inc);
-        // lanes up to (and including) the nearest inclusive one contribute
-        const int stop = im ? __ffs(im) - 1 : 31;
-        int64_t val = (q >= 0 && lane <= stop) ? (int64_t)(st & ST_VAL) : 0;
+  int64_t run0 = s_warp[warp];
+  for (int64_t t0 = w0; t0 < w1; t0 += 32 * SCAN_ITEMS) {
+    const int64_t base = t0 + lane * SCAN_ITEMS;
+    if (!one) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-        prefix += val;
-        if (im || p - 31 < 0) break;
-        p -= 32;
-      }
-      if (lane == 0) st_status(&status[tile], ST_INC | tag | (unsigned long long)(prefix + agg));
+      for (int k = 0; k < SCAN_ITEMS; ++k) v[k] = base + k < w1 ? load(base + k) : 0;
     }
-    if (lane == 0) {
-      s_prefix = prefix;
-      if (tile == n_tiles - 1 && total_out) *total_out = prefix + agg;
-    }
-  }
-  __syncthreads();
-  int64_t run = s_prefix + thread_excl;
+    int64_t ts = 0;
 #pragma unroll
-  for (int k = 0; k < SCAN_ITEMS; ++k) {
-    int64_t i = base + k;
-    if (i < n) store(i, run, v[k]);
-    run += v[k];
-  }
-  if (threadIdx.x == 0) {  // last tile out resets the ticket counters for the next scan
-    __threadfence();
-    if (atomicAdd(tile_ctr + 1, 1u) == (unsigned)(n_tiles - 1)) {
-      tile_ctr[0] = 0;
-      tile_ctr[1] = 0;
+    for (int k = 0; k < SCAN_ITEMS; ++k) ts += v[k];
+    int64_t x = ts;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
+    int64_t run = run0 + x - ts;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+      if (base + k < w1) store(base + k, run, v[k]);
+      run += v[k];
+    }
+    run0 += __shfl_sync(0xffffffffu, x, 31);
   }
+}
+
+// status words for `tiles` tiles (+ the ticket counters) and this scan's epoch
+inline int scan_status(ow_ctx* ctx, int64_t tiles, cudaStream_t s, unsigned long long** status,
+                       unsigned long long* epoch) {
+  void* old = ctx->slot_ptr[SLOT_SCAN_STATUS];
+  const size_t old_bytes = ctx->slot_bytes[SLOT_SCAN_STATUS];
+  void* p;
+  OW_TRY(ow_slot(ctx, SLOT_SCAN_STATUS, 8 * (size_t)(tiles + 1), s, &p));
+  if (p != old || ctx->slot_bytes[SLOT_SCAN_STATUS] != old_bytes || ctx->scan_epoch >= 65535) {
+    // fresh (or wrapped) status array: clear once, epochs restart at 1
+    OW_CUDA(cudaMemsetAsync(p, 0, ctx->slot_bytes[SLOT_SCAN_STATUS], s));
+    ctx->scan_epoch = 0;
+  }
+  *epoch = (unsigned long long)(++ctx->scan_epoch);
+  *status = (unsigned long long*)p + 1;  // (word 0 spare)
+  return OW_OK;
 }
 
 // Exclusive scan of load(0..n-1); *d_total (device) receives the sum.
@@ -132,20 +183,101 @@ int scan(ow_ctx* ctx, Load load, Store store, int64_t n, int64_t* d_total, cudaS
     if (d_total) OW_CUDA(cudaMemsetAsync(d_total, 0, sizeof(int64_t), s));
     return OW_OK;
   }
-  int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-  const size_t need = 8 * (size_t)(tiles + 1);
-  void* old = ctx->slot_ptr[SLOT_SCAN_STATUS];
-  const size_t old_bytes = ctx->slot_bytes[SLOT_SCAN_STATUS];
-  void* p;
-  OW_TRY(ow_slot(ctx, SLOT_SCAN_STATUS, need, s, &p));
-  if (p != old || ctx->slot_bytes[SLOT_SCAN_STATUS] != old_bytes || ctx->scan_epoch >= 65535) {
-    // fresh (or wrapped) status array: clear once, epochs restart at 1
-    OW_CUDA(cudaMemsetAsync(p, 0, ctx->slot_bytes[SLOT_SCAN_STATUS], s));
-    ctx->scan_epoch = 0;
+  // chunks of whole tiles, at most SCAN_MAX_CHUNKS of them
+  const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  const int64_t per = (tiles + SCAN_MAX_CHUNKS - 1) / SCAN_MAX_CHUNKS;
+  const int64_t chunk = per * SCAN_TILE;
+  const int64_t n_chunks = (n + chunk - 1) / chunk;
+  unsigned long long* status;
+  unsigned long long epoch;
+  OW_TRY(scan_status(ctx, n_chunks, s, &status, &epoch));
+  k_scan<<<(unsigned)n_chunks, SCAN_THREADS, 0, s>>>(load, store, n, n_chunks, chunk, status, d_total, epoch);
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  return OW_OK;
+}
+
+// ---- 0/1 scans (compactions) -----------------------------------------------
+// Load returns 0 or 1.  One tile of C01_TILE elements per CTA, element i =
+// base + k * 256 + threadIdx.x (coalesced), all C01_ITEMS predicates in flight
+// per thread; ranks come from ballots, so values never leave registers.
+constexpr int C01_ITEMS = 16;
+constexpr int C01_TILE = SCAN_THREADS * C01_ITEMS;
+
+template <class Load, class Store>
+__global__ void __launch_bounds__(SCAN_THREADS, 6)
+k_scan01(Load load, Store store, int64_t n, const int64_t* d_n, unsigned long long* status, int64_t* total_out,
+         unsigned long long epoch) {
+  constexpr int W = SCAN_THREADS / 32;
+  static_assert(C01_ITEMS * W == 128, "warp 0 holds 4 counts per lane");
+  __shared__ int s_cnt[C01_ITEMS * W];  // per (item k, warp) in element order -> exclusive ranks
+  __shared__ int64_t s_pre;
+  const int64_t tile = blockIdx.x;
+  if (d_n) {  // live length on the device: tiles past it do nothing
+    const int64_t dn = *d_n;
+    n = dn < n ? dn : n;
+    if (tile > 0 && tile * C01_TILE >= n) return;
   }
-  const unsigned long long epoch = (unsigned long long)(++ctx->scan_epoch);
-  unsigned long long* status = (unsigned long long*)p + 1;  // word 0: ticket counters
-  k_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(load, store, n, tiles, status, (unsigned int*)p, d_total, epoch);
+  const int64_t last = n > 0 ? (n - 1) / C01_TILE : 0;  // writes the total
+  const int64_t base = tile * C01_TILE + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // only the ballot masks are kept (few registers: many CTAs per SM hide the latency)
+  bool v[C01_ITEMS];
+#pragma unroll
+  for (int k = 0; k < C01_ITEMS; ++k) v[k] = base + k * SCAN_THREADS < n && load(base + k * SCAN_THREADS) != 0;
+  unsigned m[C01_ITEMS];
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < C01_ITEMS; ++k) {
+    m[k] = __ballot_sync(0xffffffffu, v[k]);
+    if (lane == k) c = __popc(m[k]);
+  }
+  if (lane < C01_ITEMS) s_cnt[lane * W + warp] = c;
+  __syncthreads();
+  if (warp == 0) {
+    const int a0 = s_cnt[4 * lane], a1 = s_cnt[4 * lane + 1], a2 = s_cnt[4 * lane + 2], a3 = s_cnt[4 * lane + 3];
+    const int s4 = a0 + a1 + a2 + a3;
+    int x = s4;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    const int ex = x - s4;
+    s_cnt[4 * lane] = ex;
+    s_cnt[4 * lane + 1] = ex + a0;
+    s_cnt[4 * lane + 2] = ex + a0 + a1;
+    s_cnt[4 * lane + 3] = ex + a0 + a1 + a2;
+    const int64_t agg = __shfl_sync(0xffffffffu, x, 31);
+    const int64_t prefix = lookback(status, tile, agg, epoch, lane);
+    if (lane == 0) {
+      s_pre = prefix;
+      if (tile == last && total_out) *total_out = prefix + agg;
+    }
+  }
+  __syncthreads();
+  const int64_t pre = s_pre;
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int k = 0; k < C01_ITEMS; ++k) {
+    const int64_t i = base + k * SCAN_THREADS;
+    if (i < n) store(i, pre + s_cnt[k * W + warp] + __popc(m[k] & lt), (int64_t)((m[k] >> lane) & 1u));
+  }
+}
+
+// d_n (optional): the live length is min(n, *d_n), read on the device.
+template <class Load, class Store>
+int scan01(ow_ctx* ctx, Load load, Store store, int64_t n, int64_t* d_total, cudaStream_t s,
+           const int64_t* d_n = nullptr) {
+  if (n <= 0) {
+    if (d_total) OW_CUDA(cudaMemsetAsync(d_total, 0, sizeof(int64_t), s));
+    return OW_OK;
+  }
+  const int64_t tiles = (n + C01_TILE - 1) / C01_TILE;
+  unsigned long long* status;
+  unsigned long long epoch;
+  OW_TRY(scan_status(ctx, tiles, s, &status, &epoch));
+  k_scan01<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(load, store, n, d_n, status, d_total, epoch);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;

@@ -12,7 +12,7 @@ kern = sys.argv[2] if len(sys.argv) > 2 else None
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
 cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--launch-count", "1"]
 if kern:
-    cmd += ["--kernel-name", "regex:" + kern]
+    cmd += ["--kernel-name-base", "demangled", "--kernel-name", "regex:" + kern]
 out = subprocess.run(cmd, capture_output=True, text=True).stdout
 lines = out.splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
