@@ -148,7 +148,8 @@ def gpu_arm(args, cfg, rank, world, local_rank):
 
     from paper_2502_16310_b200 import pipeline
 
-    plan = pipeline.GridPlan(dom, (cfg["root"],) * dim, params, cfg["lattice"]) if not text else None
+    plan = (pipeline.GridPlan(dom, (cfg["root"],) * dim, params, cfg["lattice"], reuse_outputs=True)
+            if not text else None)
 
     def step(records):
         if text or shard is not None:  # per-function path (reference call sequence, cli.py:87-113)
@@ -288,10 +289,12 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     sw_ms, sw_n = prof["lattice_sweep"]
     n_cb, n_rows, mt = lat_stats
     per_mt = 45 if dim == 3 else 13
-    lattice = entry("k_lat_mt (boundary-link intersection sweep)", sw_ms, sw_n, per_mt * mt * args.steps,
+    lattice = entry("k_lat_faces + k_lat_mt (boundary-link intersection sweep)", sw_ms, sw_n,
+                    per_mt * mt * args.steps,
                     f"per step: {mt} {'Moller-Trumbore' if dim == 3 else 'segment-segment'} link-face tests x "
                     f"{per_mt} FP32 ops ({n_rows} (block, face, direction) rows over {n_cb} candidate blocks; "
-                    f"every test is a link whose AABB meets the face AABB)", "lattice")
+                    f"every test is a link whose AABB meets the face AABB; rows of <= 16 cells are tested "
+                    f"inside k_lat_faces, larger ones by k_lat_mt)", "lattice")
     dominant = lattice if sw_ms >= mark_ms else mark
     roofline = dict(dominant)
     roofline["secondary"] = mark if dominant is lattice else lattice

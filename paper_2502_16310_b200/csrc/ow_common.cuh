@@ -71,6 +71,8 @@ enum ow_slot {
   SLOT_LAT_HITS,       // hit list (flat cell, t bits)
   SLOT_LAT_HITDIR,     // hit list directions
   SLOT_LAT_TILEHITS,   // hits per intersection tile
+  SLOT_LAT_IHITS,      // hit list of the rows swept inline by k_lat_faces (flat cell, t bits)
+  SLOT_LAT_IHITDIR,    // ... and their directions
   SLOT_LAT_BMASK,      // boundary-cell mask per candidate block
   SLOT_MARK_CBOX,      // union boxes of 32-entry bin chunks (marking cull)
   SLOT_MARK_ITEMS,     // (block, chunk, bin) marking items
@@ -125,7 +127,7 @@ struct ow_ctx {
   ow_grid link_grid;
   // lattice phase state
   int64_t lat_leaves, lat_boundary, lat_faces, lat_ncb, lat_rows, lat_units;
-  int64_t lat_row_cap, lat_unit_cap;
+  int64_t lat_row_cap, lat_unit_cap, lat_ihit_cap;
   int64_t lat_pos_lo, lat_pos_hi;  // leaf-position slice of the last count call  // capacities of the single-pass row / unit lists
   int32_t lat_dirs, lat_level;
   int8_t lat_dir[27 * 3];

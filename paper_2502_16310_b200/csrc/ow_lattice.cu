@@ -76,6 +76,11 @@ struct LatArgs {
   uint2* hits;              // [<= n_units] (flat cell, t bits)
   uint8_t* hit_dir;         // [<= n_units] direction of each hit
   int32_t* tile_hits;       // [n_tiles] hits of each MT tile
+  uint2* ihits;             // [ihit_cap] hits of the rows swept inline by k_lat_faces
+  uint8_t* ihit_dir;
+  int64_t ihit_cap;
+  unsigned long long* ihit_d;  // device inline-hit counter (may exceed the capacity)
+  unsigned long long* iru_d;   // inline (units << RU_ROW_BITS | rows), statistics
   int32_t* bcount;          // [n_cb] boundary cells per candidate block
   unsigned long long* bmask;  // [n_cb] boundary-cell mask
   const int64_t* boff;      // [n_cb]
@@ -200,6 +205,89 @@ __device__ __forceinline__ int4 row_of(int r, int excl, unsigned valid, const un
   return make_int4(pj, fj, (int)w, units);
 }
 
+// q = fl(a / det) >= 0 is decided before dividing: it holds iff a is zero, a
+// and det agree in sign, or the negative quotient underflows to -0
+// (|a / det| <= 2^-150; |a| 2^150 is formed by two exact power-of-two scalings,
+// overflow to +inf meaning "not tiny").  A miss never pays for a division and a
+// hit gets the quotient bits the oracle computes.
+__device__ __forceinline__ bool quot_nonneg(float a, float det) {
+  // branch-free: evaluated for every unit of the sweep
+  return (a == 0.0f) | ((a > 0.0f) == (det > 0.0f)) | (FMUL(FMUL(fabsf(a), 0x1p75f), 0x1p75f) <= fabsf(det));
+}
+
+// x / ext for 0 <= x < 64, ext in 1..4 (multiply-shift, exact in that range)
+__device__ __forceinline__ int div_small(int x, int ext) {
+  const int m = ext == 1 ? 256 : ext == 2 ? 128 : ext == 3 ? 86 : 64;
+  return (x * m) >> 8;
+}
+
+// One link-face test, oracle/lattice.py:mt_hits (3D) / seg_hits (2D), fixed
+// float32 op order.  3D: V = (v0, det), E1 = (e1, p.x), E2 = (e2, p.y), pz
+// with p = d x e2, det = e1 . p (mt_prep3); 2D: V = (a.xy, den), S = (s.xy)
+// with den = d x s (mt_prep2).  Divisions only for hits.
+__device__ __forceinline__ void mt_prep3(const float* dv, float4 a, float4 b, float4 c, float4& V, float4& E1,
+                                         float4& E2, float& pz) {
+  const float px = FSUB(FMUL(dv[1], c.z), FMUL(dv[2], c.y));
+  const float py = FSUB(FMUL(dv[2], c.x), FMUL(dv[0], c.z));
+  pz = FSUB(FMUL(dv[0], c.y), FMUL(dv[1], c.x));
+  V = make_float4(a.x, a.y, a.z, dot3f(b.x, b.y, b.z, px, py, pz));
+  E1 = make_float4(b.x, b.y, b.z, px);
+  E2 = make_float4(c.x, c.y, c.z, py);
+}
+__device__ __forceinline__ bool mt_test3(const float* x, const float* dv, float4 V, float4 E1, float4 E2, float pz,
+                                         float& t) {
+  const float det = V.w, px = E1.w, py = E2.w;
+  const float tx = FSUB(x[0], V.x), ty = FSUB(x[1], V.y), tz = FSUB(x[2], V.z);
+  const float un = dot3f(tx, ty, tz, px, py, pz);
+  const float qx = FSUB(FMUL(ty, E1.z), FMUL(tz, E1.y));
+  const float qy = FSUB(FMUL(tz, E1.x), FMUL(tx, E1.z));
+  const float qz = FSUB(FMUL(tx, E1.y), FMUL(ty, E1.x));
+  const float vn = dot3f(dv[0], dv[1], dv[2], qx, qy, qz);
+  const float tn = dot3f(E2.x, E2.y, E2.z, qx, qy, qz);
+  bool hit = false;
+  if ((det != 0.0f) & quot_nonneg(un, det) & quot_nonneg(vn, det) & quot_nonneg(tn, det)) {
+    const float uu = FDIV(un, det), vv = FDIV(vn, det);
+    t = FDIV(tn, det);
+    hit = (FADD(uu, vv) <= 1.0f) & (t <= 1.0f);
+  }
+  return hit;
+}
+__device__ __forceinline__ float4 mt_prep2(const float* dv, float4 a) {
+  return make_float4(a.x, a.y, FSUB(FMUL(dv[0], a.w), FMUL(dv[1], a.z)), 0.0f);
+}
+__device__ __forceinline__ bool mt_test2(const float* x, const float* dv, float4 V, float4 S, float& t) {
+  // segment-segment (oracle/lattice.py:seg_hits), s = b - a pre-formed
+  const float den = V.z;
+  const float qx = FSUB(V.x, x[0]), qy = FSUB(V.y, x[1]);
+  const float tn = FSUB(FMUL(qx, S.y), FMUL(qy, S.x));
+  const float sn = FSUB(FMUL(qx, dv[1]), FMUL(qy, dv[0]));
+  bool hit = false;
+  if ((den != 0.0f) && quot_nonneg(tn, den) && quot_nonneg(sn, den)) {
+    t = FDIV(tn, den);
+    const float ss = FDIV(sn, den);
+    hit = t <= 1.0f && ss <= 1.0f;
+  }
+  return hit;
+}
+
+// cell index (flat, within the block) and centre of unit `rem` of a row
+// word w (cells in x-fastest order over the per-axis ranges)
+template <int D>
+__device__ __forceinline__ int row_cell(unsigned w, int rem, const float* cen_pos, float* x) {
+  int cell = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const unsigned ra = (w >> (5 + 4 * a)) & 0xFu;
+    const int ext = (int)(ra >> 2) + 1;
+    const int qd = div_small(rem, ext);
+    const int i = (int)(ra & 3u) + (rem - qd * ext);
+    rem = qd;
+    cell |= i << (2 * a);
+    x[a] = __ldg(cen_pos + a * 4 + i);
+  }
+  return cell;
+}
+
 // FACES_PER_WARP faces per warp, SLOT_LANES lanes per face: each lane group
 // walks the finest-level lattice blocks its face box can reach (root-lattice
 // descent, no bins; link boxes of block k span [o_k - q/8, o_k + 9q/8] and a
@@ -213,12 +301,39 @@ __device__ __forceinline__ int4 row_of(int r, int excl, unsigned valid, const un
 // by k_lat_mt.
 constexpr int FACES_PER_WARP = 4;
 constexpr int SLOT_LANES = 32 / FACES_PER_WARP;
+constexpr int INLINE_UNITS = 16;  // rows of at most this many cells are tested inside k_lat_faces
+constexpr int HITBUF = 64;        // per-warp hit buffer (flushed with one atomic)
+
+// a warp's buffered hits -> the inline hit list (one reservation); returns 0
+__device__ __forceinline__ int flush_hits(const LatArgs& A, const uint2* hb, const uint8_t* hd, int nh, int lane) {
+  __syncwarp();
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(A.ihit_d, (unsigned long long)nh);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (int j = lane; j < nh; j += 32)
+    if ((int64_t)base + j < A.ihit_cap) {  // past the capacity: counted only (the host re-runs)
+      A.ihits[base + j] = hb[j];
+      A.ihit_dir[base + j] = hd[j];
+    }
+  __syncwarp();
+  return 0;
+}
 
 template <int D>
 __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
-  const int lane = threadIdx.x & 31;
+  constexpr int C = D == 3 ? 64 : 16;
+  __shared__ float4 s_face[4][FACES_PER_WARP][3];  // per warp: (v0, e1, e2) / (a, s) of its faces
+  __shared__ uint2 s_hit[4][HITBUF];
+  __shared__ uint8_t s_hdir[4][HITBUF];
+  __shared__ float s_dv[QMAX][3];
+  for (int i = threadIdx.x; i < QMAX * 3; i += blockDim.x) s_dv[i / 3][i % 3] = A.dv[i / 3][i % 3];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sl = lane % SLOT_LANES;
-  const int64_t f = ((int64_t)blockIdx.x * 4 + (threadIdx.x >> 5)) * FACES_PER_WARP + lane / SLOT_LANES;
+  const int64_t fbase = ((int64_t)blockIdx.x * 4 + wid) * FACES_PER_WARP;
+  const int64_t f = fbase + lane / SLOT_LANES;
+  int nh = 0;  // hits buffered by this warp
+  unsigned long long iru = 0;  // inline units / rows of this warp (statistics)
   if (f - lane / SLOT_LANES >= A.n_faces) return;  // whole warp past the end
   const bool live = f < A.n_faces;
   float v[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
@@ -239,14 +354,25 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
     }
   }
   if (live && sl == 0) {  // e1 = v1 - v0, e2 = v2 - v0 (3D) / s = b - a (2D), oracle/lattice.py
+    float4 r0, r1 = make_float4(0.0f, 0.0f, 0.0f, 0.0f), r2 = r1;
     if (D == 3) {
-      A.rec[3 * f + 0] = make_float4(v[0][0], v[0][1], v[0][2], 0.0f);
-      A.rec[3 * f + 1] = make_float4(FSUB(v[1][0], v[0][0]), FSUB(v[1][1], v[0][1]), FSUB(v[1][2], v[0][2]), 0.0f);
-      A.rec[3 * f + 2] = make_float4(FSUB(v[2][0], v[0][0]), FSUB(v[2][1], v[0][1]), FSUB(v[2][2], v[0][2]), 0.0f);
+      r0 = make_float4(v[0][0], v[0][1], v[0][2], 0.0f);
+      r1 = make_float4(FSUB(v[1][0], v[0][0]), FSUB(v[1][1], v[0][1]), FSUB(v[1][2], v[0][2]), 0.0f);
+      r2 = make_float4(FSUB(v[2][0], v[0][0]), FSUB(v[2][1], v[0][1]), FSUB(v[2][2], v[0][2]), 0.0f);
     } else {
-      A.rec[3 * f + 0] = make_float4(v[0][0], v[0][1], FSUB(v[1][0], v[0][0]), FSUB(v[1][1], v[0][1]));
+      r0 = make_float4(v[0][0], v[0][1], FSUB(v[1][0], v[0][0]), FSUB(v[1][1], v[0][1]));
     }
+    A.rec[3 * f + 0] = r0;
+    if (D == 3) {
+      A.rec[3 * f + 1] = r1;
+      A.rec[3 * f + 2] = r2;
+    }
+    float4* sf = s_face[wid][lane / SLOT_LANES];
+    sf[0] = r0;
+    sf[1] = r1;
+    sf[2] = r2;
   }
+  __syncwarp();
   const int L = A.level;
   int k0[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
   float rext[3] = {1.0f, 1.0f, 1.0f};
@@ -311,40 +437,95 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
     if (!total) continue;
     const int excl = incl - nrow;
     const int fi = (int)f;
-    // pass 1: units of every row, then one reservation
-    unsigned long long units_w = 0;
-    for (int r0 = 0; r0 < total; r0 += 32)
-      units_w += (unsigned long long)row_of<D>(r0 + lane, excl, valid, R, pos, fi, A).w;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) units_w += __shfl_xor_sync(0xffffffffu, units_w, o);
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(A.ru_d, (units_w << RU_ROW_BITS) | (unsigned long long)total);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    const int64_t k0r = (int64_t)(base & RU_ROW_MASK);
-    int64_t u0r = (int64_t)(base >> RU_ROW_BITS);
-    // pass 2: write the rows; unit offsets by a warp scan per chunk of 32 rows
     for (int r0 = 0; r0 < total; r0 += 32) {
       const int r = r0 + lane;
-      const int4 row = row_of<D>(r, excl, valid, R, pos, fi, A);
+      const int4 row = row_of<D>(r, excl, valid, R, pos, fi, A);  // units 0 past the end
       const int units = row.w;
-      int ui = units;
+      // rows of more than INLINE_UNITS cells go to k_lat_mt (load-balanced over
+      // units): one packed reservation of rows and units per chunk, so row
+      // order and unit order agree and unit offsets stay monotone
+      const bool big = units > INLINE_UNITS;
+      const unsigned bm = __ballot_sync(0xffffffffu, big);
+      if (bm) {
+        const int ub = big ? units : 0;
+        int ui = ub;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, ui, o);
-        if (lane >= o) ui += y;
-      }
-      if (r < total) {
-        const int64_t k = k0r + r;
-        const int64_t u = u0r + ui - units;
-        if (k < A.row_cap && u + units <= A.unit_cap) {
-          A.rows[k] = row;
-          A.rowoff[k] = u;
-          for (int64_t t = (u + MT_TILE - 1) / MT_TILE; t * MT_TILE < u + units; ++t) A.tile_row[t] = (int32_t)k;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, ui, o);
+          if (lane >= o) ui += y;
+        }
+        const unsigned long long tu = (unsigned long long)__shfl_sync(0xffffffffu, ui, 31);
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(A.ru_d, (tu << RU_ROW_BITS) | (unsigned long long)__popc(bm));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (big) {
+          const int64_t k = (int64_t)(base & RU_ROW_MASK) + __popc(bm & lanemask_lt());
+          const int64_t u = (int64_t)(base >> RU_ROW_BITS) + ui - ub;
+          if (k < A.row_cap && u + ub <= A.unit_cap) {
+            A.rows[k] = row;
+            A.rowoff[k] = u;
+            for (int64_t t = (u + MT_TILE - 1) / MT_TILE; t * MT_TILE < u + ub; ++t) A.tile_row[t] = (int32_t)k;
+          }
         }
       }
-      u0r += __shfl_sync(0xffffffffu, ui, 31);
+      // the other rows: their units flattened over the warp and tested here
+      const int us = big ? 0 : units;
+      int si = us;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, si, o);
+        if (lane >= o) si += y;
+      }
+      const int S = __shfl_sync(0xffffffffu, si, 31);
+      const int se = si - us;
+      iru += ((unsigned long long)S << RU_ROW_BITS) + (unsigned long long)__popc(__ballot_sync(0xffffffffu, us > 0));
+      for (int u0 = 0; u0 < S; u0 += 32) {
+        const int u = u0 + lane;
+        int j = 0;  // owning lane: the first with si > u
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1)
+          if (__shfl_sync(0xffffffffu, si, j + step - 1) <= u) j += step;
+        const int ej = __shfl_sync(0xffffffffu, se, j);
+        const int pj = __shfl_sync(0xffffffffu, row.x, j);
+        const int fj = __shfl_sync(0xffffffffu, row.y, j);
+        const unsigned wj = (unsigned)__shfl_sync(0xffffffffu, row.z, j);
+        bool hit = false;
+        float t = 0.0f;
+        unsigned cellg = 0;
+        const int d = (int)(wj & 31u);
+        if (u < S) {
+          float x[3];
+          const int cell = row_cell<D>(wj, u - ej, A.cen + (int64_t)pj * D * 4, x);
+          cellg = (unsigned)pj * (unsigned)C + (unsigned)cell;
+          const float4* F4 = s_face[wid][fj - fbase];
+          const float* dv = s_dv[d];
+          if (D == 3) {
+            float4 V, E1, E2;
+            float pz;
+            mt_prep3(dv, F4[0], F4[1], F4[2], V, E1, E2, pz);
+            hit = mt_test3(x, dv, V, E1, E2, pz, t);
+          } else {
+            const float4 a = F4[0];
+            hit = mt_test2(x, dv, mt_prep2(dv, a), make_float4(a.z, a.w, 0.0f, 0.0f), t);
+          }
+        }
+        const unsigned hm = __ballot_sync(0xffffffffu, hit);
+        if (hm) {
+          if (nh + __popc(hm) > HITBUF) nh = flush_hits(A, s_hit[wid], s_hdir[wid], nh, lane);
+          if (hit) {
+            atomicOr(&A.flags[cellg], 1u << d);
+            const int k = nh + __popc(hm & lanemask_lt());
+            s_hit[wid][k] = make_uint2(cellg, __float_as_uint(FADD(t, 0.0f)));  // -0 -> +0
+            s_hdir[wid][k] = (uint8_t)d;
+          }
+          nh += __popc(hm);
+          __syncwarp();
+        }
+      }
     }
   }
+  if (nh) flush_hits(A, s_hit[wid], s_hdir[wid], nh, lane);
+  if (iru && lane == 0) atomicAdd(A.iru_d, iru);
 }
 
 // ranks of candidate blocks (leaves with at least one row)
@@ -375,22 +556,6 @@ struct BoffStore {
     if (i < *n) off[i] = e;
   }
 };
-
-// q = fl(a / det) >= 0 is decided before dividing: it holds iff a is zero, a
-// and det agree in sign, or the negative quotient underflows to -0
-// (|a / det| <= 2^-150; |a| 2^150 is formed by two exact power-of-two scalings,
-// overflow to +inf meaning "not tiny").  A miss never pays for a division and a
-// hit gets the quotient bits the oracle computes.
-__device__ __forceinline__ bool quot_nonneg(float a, float det) {
-  // branch-free: evaluated for every unit of the sweep
-  return (a == 0.0f) | ((a > 0.0f) == (det > 0.0f)) | (FMUL(FMUL(fabsf(a), 0x1p75f), 0x1p75f) <= fabsf(det));
-}
-
-// x / ext for 0 <= x < 64, ext in 1..4 (multiply-shift, exact in that range)
-__device__ __forceinline__ int div_small(int x, int ext) {
-  const int m = ext == 1 ? 256 : ext == 2 ? 128 : ext == 3 ? 86 : 64;
-  return (x * m) >> 8;
-}
 
 // Persistent, load-balanced over units: a tile of MT_TILE consecutive units
 // covers at most MT_TILE + 1 rows (the first one recorded by the unit scan).
@@ -430,17 +595,16 @@ __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
       const float* dv = s_dv[m.z & 31];
       const float4* Rf = A.rec + 3 * (int64_t)m.y;
       if (D == 3) {
-        const float4 a = Rf[0], b = Rf[1], c = Rf[2];
-        const float px = FSUB(FMUL(dv[1], c.z), FMUL(dv[2], c.y));
-        const float py = FSUB(FMUL(dv[2], c.x), FMUL(dv[0], c.z));
-        const float pz = FSUB(FMUL(dv[0], c.y), FMUL(dv[1], c.x));
-        s_v0[i] = make_float4(a.x, a.y, a.z, dot3f(b.x, b.y, b.z, px, py, pz));
-        s_e1[i] = make_float4(b.x, b.y, b.z, px);
-        s_e2[i] = make_float4(c.x, c.y, c.z, py);
+        float4 V, E1, E2;
+        float pz;
+        mt_prep3(dv, Rf[0], Rf[1], Rf[2], V, E1, E2, pz);
+        s_v0[i] = V;
+        s_e1[i] = E1;
+        s_e2[i] = E2;
         s_pz[i] = pz;
       } else {
         const float4 a = Rf[0];
-        s_v0[i] = make_float4(a.x, a.y, FSUB(FMUL(dv[0], a.w), FMUL(dv[1], a.z)), 0.0f);
+        s_v0[i] = mt_prep2(dv, a);
         s_e1[i] = make_float4(a.z, a.w, 0.0f, 0.0f);
       }
     }
@@ -468,49 +632,12 @@ __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
         const int4 m = s_meta[row];
         const unsigned w = (unsigned)m.z;
         d = (int)(w & 31u);
-        int rem = u - s_off[row];
-        int cell = 0;
         float x[3];
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          const unsigned ra = (w >> (5 + 4 * a)) & 0xFu;
-          const int ext = (int)(ra >> 2) + 1;
-          const int qd = div_small(rem, ext);
-          const int i = (int)(ra & 3u) + (rem - qd * ext);
-          rem = qd;
-          cell |= i << (2 * a);
-          x[a] = __ldg(A.cen + ((int64_t)m.x * D + a) * 4 + i);
-        }
+        const int cell = row_cell<D>(w, u - s_off[row], A.cen + (int64_t)m.x * D * 4, x);
         cellg = m.x * C + cell;
         const float* dv = s_dv[d];
-        if (D == 3) {
-          const float4 V = s_v0[row], E1 = s_e1[row], E2 = s_e2[row];
-          const float det = V.w, px = E1.w, py = E2.w, pz = s_pz[row];
-          const float tx = FSUB(x[0], V.x), ty = FSUB(x[1], V.y), tz = FSUB(x[2], V.z);
-          const float un = dot3f(tx, ty, tz, px, py, pz);
-          const float qx = FSUB(FMUL(ty, E1.z), FMUL(tz, E1.y));
-          const float qy = FSUB(FMUL(tz, E1.x), FMUL(tx, E1.z));
-          const float qz = FSUB(FMUL(tx, E1.y), FMUL(ty, E1.x));
-          const float vn = dot3f(dv[0], dv[1], dv[2], qx, qy, qz);
-          const float tn = dot3f(E2.x, E2.y, E2.z, qx, qy, qz);
-          if ((det != 0.0f) & quot_nonneg(un, det) & quot_nonneg(vn, det) & quot_nonneg(tn, det)) {
-            const float uu = FDIV(un, det), vv = FDIV(vn, det);
-            t = FDIV(tn, det);
-            hit = (FADD(uu, vv) <= 1.0f) & (t <= 1.0f);
-          }
-        } else {
-          // segment-segment (oracle/lattice.py:seg_hits), s = b - a pre-formed
-          const float4 V = s_v0[row], S = s_e1[row];
-          const float den = V.z;
-          const float qx = FSUB(V.x, x[0]), qy = FSUB(V.y, x[1]);
-          const float tn = FSUB(FMUL(qx, S.y), FMUL(qy, S.x));
-          const float sn = FSUB(FMUL(qx, dv[1]), FMUL(qy, dv[0]));
-          if ((den != 0.0f) && quot_nonneg(tn, den) && quot_nonneg(sn, den)) {
-            t = FDIV(tn, den);
-            const float ss = FDIV(sn, den);
-            hit = t <= 1.0f && ss <= 1.0f;
-          }
-        }
+        if (D == 3) hit = mt_test3(x, dv, s_v0[row], s_e1[row], s_e2[row], s_pz[row], t);
+        else hit = mt_test2(x, dv, s_v0[row], s_e1[row], t);
       }
       // hits of this tile go to its own slots [u0, u0 + n) of the hit list
       // (a tile has at most MT_TILE hits): shared-memory append, no global counter
@@ -596,6 +723,15 @@ __global__ void k_lat_hits(LatArgs A) {
       atomicMin(reinterpret_cast<unsigned*>(A.q_out) + row * A.nq + A.hit_dir[i], h.y);
     }
   }
+  const int64_t ni = (int64_t)*A.ihit_d;  // hits of the rows swept inline (<= capacity here)
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint2 h = A.ihits[i];
+    const int64_t pos = h.x / C;
+    const int c = (int)(h.x % C);
+    const int r = A.cand_rank[pos];
+    const int64_t row = A.boff[r] + __popcll(A.bmask[r] & ((1ull << c) - 1ull));
+    atomicMin(reinterpret_cast<unsigned*>(A.q_out) + row * A.nq + A.ihit_dir[i], h.y);
+  }
 }
 
 LatArgs make_args(ow_ctx* ctx) {
@@ -659,6 +795,11 @@ LatArgs make_args(ow_ctx* ctx) {
   A.hits = (uint2*)ctx->slot_ptr[SLOT_LAT_HITS];
   A.hit_dir = (uint8_t*)ctx->slot_ptr[SLOT_LAT_HITDIR];
   A.tile_hits = (int32_t*)ctx->slot_ptr[SLOT_LAT_TILEHITS];
+  A.ihits = (uint2*)ctx->slot_ptr[SLOT_LAT_IHITS];
+  A.ihit_dir = (uint8_t*)ctx->slot_ptr[SLOT_LAT_IHITDIR];
+  A.ihit_cap = ctx->lat_ihit_cap;
+  A.ihit_d = (unsigned long long*)(ctx->d_small + 49);
+  A.iru_d = (unsigned long long*)(ctx->d_small + 50);
   A.bcount = (int32_t*)ctx->slot_ptr[SLOT_LAT_BCOUNT];
   A.bmask = (unsigned long long*)ctx->slot_ptr[SLOT_LAT_BMASK];
   A.boff = (const int64_t*)ctx->slot_ptr[SLOT_LAT_BOFFS];
@@ -723,7 +864,8 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   // an overflow is detected at the single readback and the pass re-runs
   if (ctx->lat_row_cap < 64 * n_faces + 1024) ctx->lat_row_cap = 64 * n_faces + 1024;
   if (ctx->lat_unit_cap < 8 * ctx->lat_row_cap) ctx->lat_unit_cap = 8 * ctx->lat_row_cap;
-  const int64_t rcap = ctx->lat_row_cap, ucap = ctx->lat_unit_cap;
+  if (ctx->lat_ihit_cap < 8 * n_faces + 65536) ctx->lat_ihit_cap = 8 * n_faces + 65536;
+  const int64_t rcap = ctx->lat_row_cap, ucap = ctx->lat_unit_cap, icap = ctx->lat_ihit_cap;
   void* p;
   const int64_t nl = n_leaves;
   OW_TRY(ow_slot(ctx, SLOT_LAT_POS, 4 * (size_t)f->n_blocks, s, &p));
@@ -738,24 +880,24 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   OW_TRY(ow_slot(ctx, SLOT_LAT_HITS, 8 * (size_t)ucap, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_HITDIR, (size_t)ucap, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_TILEHITS, 4 * (size_t)(ucap / MT_TILE + 2), s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_IHITS, 8 * (size_t)icap, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_IHITDIR, (size_t)icap, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_BCOUNT, 4 * (size_t)nl, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_BMASK, 8 * (size_t)nl, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_BOFFS, 8 * (size_t)nl, s, &p));
-  OW_CUDA(cudaMemsetAsync(ctx->d_small + 48, 0, 2 * 8, s));
+  OW_CUDA(cudaMemsetAsync(ctx->d_small + 48, 0, 3 * 8, s));
   OW_CUDA(cudaMemsetAsync(d_flags, 0, 4 * (size_t)n_leaves * C, s));
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
   LatArgs A = make_args(ctx);
-  if (D == 3) {
-    k_lat_pos<3><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
-    k_lat_faces<3><<<ow_blocks(n_faces, 4 * FACES_PER_WARP), 128, 0, s>>>(A);
-  } else {
-    k_lat_pos<2><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
-    k_lat_faces<2><<<ow_blocks(n_faces, 4 * FACES_PER_WARP), 128, 0, s>>>(A);
-  }
+  if (D == 3) k_lat_pos<3><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
+  else k_lat_pos<2><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
+  // the sweep: k_lat_faces (rows; small rows tested inline) + k_lat_mt (large rows)
+  OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
+  if (D == 3) k_lat_faces<3><<<ow_blocks(n_faces, 4 * FACES_PER_WARP), 128, 0, s>>>(A);
+  else k_lat_faces<2><<<ow_blocks(n_faces, 4 * FACES_PER_WARP), 128, 0, s>>>(A);
   ctx->launches += 2;
   OW_CHECK_LAUNCH();
   OW_TRY(ow::scan01(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s));
-  OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
   const int64_t tiles_max = ucap / MT_TILE + 1;
   if (D == 3) k_lat_mt<3><<<ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s>>>(A);
   else k_lat_mt<2><<<ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s>>>(A);
@@ -767,17 +909,19 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   OW_TRY(scan(ctx, BcountLoad{A.bcount, A.n_cb_d}, BoffStore{(int64_t*)A.boff, A.n_cb_d}, nl, ctx->d_small + 35, s));
   OW_PROF_END(ctx, PROF_LATTICE, s);
   // single readback: candidate blocks, (scan scratch), boundary cells, rows, units
-  int64_t h[17];
-  OW_TRY(ow_readback(ctx, ctx->d_small + 33, 17, h, s));
+  int64_t h[18];
+  OW_TRY(ow_readback(ctx, ctx->d_small + 33, 18, h, s));
   const int64_t n_cb = h[0], nb = h[2];
   const int64_t n_rows = (int64_t)((uint64_t)h[15] & RU_ROW_MASK), n_units = (int64_t)((uint64_t)h[15] >> RU_ROW_BITS);
+  const int64_t n_ihits = h[16];
   if (n_rows >= (int64_t(1) << RU_ROW_BITS) - (int64_t(1) << 20)) {
     ow_set_error("lattice: %lld (block, face, direction) rows exceed one pass", (long long)n_rows);
     return OW_ERR_CAPACITY;
   }
-  if (n_rows > rcap || n_units > ucap) {
+  if (n_rows > rcap || n_units > ucap || n_ihits > icap) {
     ctx->lat_row_cap = n_rows + n_rows / 4 + 1024;
     ctx->lat_unit_cap = n_units + n_units / 4 + 4096;
+    if (n_ihits > icap) ctx->lat_ihit_cap = n_ihits + n_ihits / 4 + 65536;
     if (ctx->lat_unit_cap >= (int64_t(1) << 31)) {
       ow_set_error("lattice: %lld link-face tests exceed one pass (2^31)", (long long)n_units);
       return OW_ERR_CAPACITY;
@@ -786,8 +930,9 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
                                         geom_key, grid, h_dirs, n_dirs, d_flags, out_boundary, stream);
   }
   ctx->lat_ncb = n_cb;
-  ctx->lat_rows = n_rows;
-  ctx->lat_units = n_units;
+  // statistics over both sweeps (rows of k_lat_mt + rows tested inline)
+  ctx->lat_rows = n_rows + (int64_t)((uint64_t)h[17] & RU_ROW_MASK);
+  ctx->lat_units = n_units + (int64_t)((uint64_t)h[17] >> RU_ROW_BITS);
   ctx->lat_boundary = nb;
   *out_boundary = nb;
   return OW_OK;

@@ -158,6 +158,13 @@ class Forest:
         self._fill_view(self._view_struct)
         return self._view_struct
 
+    def _reset_for_pass(self):
+        """Empty forest over the same storage (ow_geometry_to_grid writes the roots)."""
+        self._n = 0
+        self._n_levels = 1
+        self._version += 1
+        self._leaf_cache.clear()
+
     def _sync_from_view(self):
         self._n = int(self._view_struct.n_blocks)
 

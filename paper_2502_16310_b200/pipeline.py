@@ -50,7 +50,11 @@ class GridPlan:
     NearWallParams, lattice)."""
 
     def __init__(self, domain: Aabb, root_dims, params: NearWallParams, lattice: str | None = "D3Q19",
-                 capacity=None, max_level=DEFAULT_MAX_LEVEL):
+                 capacity=None, max_level=DEFAULT_MAX_LEVEL, reuse_outputs=False):
+        """``reuse_outputs=True``: every pass writes into the same device
+        arrays (forest, bins, links), so a pass's results are valid until the
+        next ``run`` — for loops that consume each pass before the next
+        (benchmarks, time series); all work is still recomputed."""
         self.domain = domain if isinstance(domain, Aabb) else Aabb(*domain)
         self.dim = self.domain.dim
         self.root_dims = tuple(int(v) for v in np.asarray(root_dims).reshape(-1))
@@ -70,8 +74,16 @@ class GridPlan:
         self._est_rows = 0
         self._outs = {}
         self._hbuf = None
+        self.reuse = bool(reuse_outputs)
+        self._forest = None
+        self._setup = None  # (n_faces, _driver_setup result): the parts that depend on n_faces only
+        self._gp0 = _lib.G2GParamsC()  # static fields of the call's parameter struct
+        if self.dirs is not None:
+            self._gp0.lattice_q = len(self.dirs)
+            for i, v in enumerate(self.dirs.reshape(-1)):
+                self._gp0.lattice_dirs[i] = int(v)
 
-        def alloc(_user, what, nbytes, out_p):
+        def alloc(_user, what, nbytes, out_p):  # noqa: ARG001
             try:
                 t = self._new_out(int(what), int(nbytes))
                 out_p[0] = t.data_ptr() if t.numel() else None
@@ -80,6 +92,8 @@ class GridPlan:
                 return 1
 
         self._alloc_cb = _lib.ALLOC_FN(alloc)
+        if self.dirs is not None:
+            self._gp0.alloc = self._alloc_cb
 
     def _new_out(self, what, nbytes):
         dt = _OUT_DTYPES[what]
@@ -112,20 +126,31 @@ class GridPlan:
                 raise InvalidParameterError("binary STL records are 3D")
             coords = torch.empty((3, 3, int(n_faces)), dtype=torch.float32, device=self.dev)
         nf = int(coords.shape[2])
-        forest = Forest(self.domain, self.root_dims, max_level=self.max_level, capacity=self.capacity,
-                        _init_root=False)
-        st = _driver_setup(forest, nf, self.params, True, None)
-        gp = _lib.G2GParamsC()
+        forest = self._forest
+        if forest is not None and forest.capacity >= self.capacity:
+            forest._reset_for_pass()
+        else:
+            forest = Forest(self.domain, self.root_dims, max_level=self.max_level, capacity=self.capacity,
+                            _init_root=False)
+            if self.reuse:
+                self._forest = forest
+        if self._setup is None or self._setup[0] != nf:
+            self._setup = (nf, _driver_setup(forest, nf, self.params, True, None))
+        st = self._setup[1]
+        if not self.reuse and st["bins_t"] is not None:  # fresh bin buffers for this pass's result
+            st = dict(st)
+            st["bins_t"] = tuple(torch.empty_like(t) for t in st["bins_t"])
+        gp = _lib.G2GParamsC.from_buffer_copy(self._gp0)
         gp.nw = st["p"]
-        self._outs = {}
+        if not self.reuse:
+            self._outs = {}
         if self.dirs is not None:
-            gp.lattice_q = len(self.dirs)
-            for i, v in enumerate(self.dirs.reshape(-1)):
-                gp.lattice_dirs[i] = int(v)
-            gp.alloc = self._alloc_cb
-            for what in range(4):  # fresh tensors sized from the last pass: no callback in steady state
+            for what in range(4):  # tensors sized from the last pass: no callback in steady state
                 if self._est[what]:
-                    t = self._new_out(what, self._est[what] + self._est[what] // 8 + 64)
+                    want = self._est[what] + self._est[what] // 8 + 64
+                    t = self._outs.get(what)
+                    if t is None or t.numel() * t.element_size() < self._est[what]:
+                        t = self._new_out(what, want)
                     gp.out_buf[what] = t.data_ptr()
                     gp.out_cap[what] = t.numel() * t.element_size()
         hbuf = None

@@ -492,6 +492,31 @@ def test_geometry_to_grid_matches_per_function_path(ow, capacity):
         assert torch.equal(getattr(gp.links, name), getattr(ll, name)), name
 
 
+def test_grid_plan_reuse_outputs(ow):
+    """reuse_outputs=True: passes write into the plan's arrays; each pass
+    (consumed before the next) equals a fresh plan's pass."""
+    import torch
+
+    from paper_2502_16310_b200 import pipeline, shapes
+
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8)
+    plan = pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19", reuse_outputs=True)
+    for sub in (3, 2, 3):  # geometry changes between passes
+        tris = shapes.icosphere_triangles(sub)
+        data = shapes.binary_stl_bytes(tris)
+        n = int.from_bytes(data[80:84], "little")
+        rec = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda()
+        ref = pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19").run(rec, n)
+        gp = plan.run(rec, n)
+        assert gp.result.marked_refined == ref.result.marked_refined
+        np.testing.assert_array_equal(gp.forest._coords, ref.forest._coords)
+        np.testing.assert_array_equal(gp.forest._parent, ref.forest._parent)
+        assert torch.equal(gp.result.bins.ids, ref.result.bins.ids)
+        for name in ("leaves", "flags", "cells", "q"):
+            assert torch.equal(getattr(gp.links, name), getattr(ref.links, name)), name
+
+
 def test_geometry_to_grid_errors(ow):
     import torch
 

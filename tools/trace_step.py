@@ -29,7 +29,7 @@ params = ow.NearWallParams(d_spec=cfg["d"], n_levels=cfg["levels"], bins_per_axi
 from paper_2502_16310_b200 import pipeline  # noqa: E402
 
 
-plan = pipeline.GridPlan(dom, (cfg["root"],) * dim, params, cfg["lattice"])
+plan = pipeline.GridPlan(dom, (cfg["root"],) * dim, params, cfg["lattice"], reuse_outputs=True)
 
 
 def step():
