@@ -299,6 +299,11 @@ int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int32_t level,
                                  int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int8_t* h_dirs,
                                  int32_t n_dirs, uint32_t* d_flags, int64_t* out_boundary, void* stream);
 int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, void* stream);
+/* Tuning / testing knob of the lattice sweep: rows of more than `units` cells
+ * are tested by the unit-balanced k_lat_mt pass, the others inside the
+ * face pass (default 64: all rows inline); units < 0 restores the default. */
+int ow_lattice_set_inline_units(ow_ctx* ctx, int32_t units);
+
 /* Work counters of the last ow_lattice_links_count: [0] candidate blocks,
  * [1] (block, face, direction) rows, [2] Moller-Trumbore / segment tests. */
 int ow_lattice_stats(ow_ctx* ctx, int64_t* out3, void* stream);

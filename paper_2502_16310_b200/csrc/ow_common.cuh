@@ -128,6 +128,8 @@ struct ow_ctx {
   // lattice phase state
   int64_t lat_leaves, lat_boundary, lat_faces, lat_ncb, lat_rows, lat_units;
   int64_t lat_row_cap, lat_unit_cap, lat_ihit_cap;
+  int32_t lat_inline_units;
+  bool lat_inline_set;
   int64_t lat_pos_lo, lat_pos_hi;  // leaf-position slice of the last count call  // capacities of the single-pass row / unit lists
   int32_t lat_dirs, lat_level;
   int8_t lat_dir[27 * 3];

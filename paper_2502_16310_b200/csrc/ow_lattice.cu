@@ -26,6 +26,7 @@
 //   k_lat_bcount + scan : boundary rows in (block, cell) order.
 //   k_lat_emit + k_lat_hits : cells, q rows (-1 / min t via atomicMin).
 #include "ow_scan.cuh"
+#include <stdlib.h>
 #include <string.h>
 
 namespace {
@@ -81,6 +82,7 @@ struct LatArgs {
   int64_t ihit_cap;
   unsigned long long* ihit_d;  // device inline-hit counter (may exceed the capacity)
   unsigned long long* iru_d;   // inline (units << RU_ROW_BITS | rows), statistics
+  int inline_units;            // rows of more cells go to k_lat_mt (OW_INLINE_UNITS overrides; tuning)
   int32_t* bcount;          // [n_cb] boundary cells per candidate block
   unsigned long long* bmask;  // [n_cb] boundary-cell mask
   const int64_t* boff;      // [n_cb]
@@ -301,7 +303,11 @@ __device__ __forceinline__ int row_cell(unsigned w, int rem, const float* cen_po
 // by k_lat_mt.
 constexpr int FACES_PER_WARP = 4;
 constexpr int SLOT_LANES = 32 / FACES_PER_WARP;
-constexpr int INLINE_UNITS = 16;  // rows of at most this many cells are tested inside k_lat_faces
+// Rows of at most this many cells are tested inside k_lat_faces; larger ones
+// by k_lat_mt.  Measured on C2/C3/C5 (OW_INLINE_UNITS sweep, profiles/): the
+// inline sweep wins at every row size, so by default every row is inline
+// (64 = 4^3 cells) and k_lat_mt only runs for a lower override.
+constexpr int INLINE_UNITS = 64;
 constexpr int HITBUF = 64;        // per-warp hit buffer (flushed with one atomic)
 
 // a warp's buffered hits -> the inline hit list (one reservation); returns 0
@@ -444,7 +450,7 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
       // rows of more than INLINE_UNITS cells go to k_lat_mt (load-balanced over
       // units): one packed reservation of rows and units per chunk, so row
       // order and unit order agree and unit offsets stay monotone
-      const bool big = units > INLINE_UNITS;
+      const bool big = units > A.inline_units;
       const unsigned bm = __ballot_sync(0xffffffffu, big);
       if (bm) {
         const int ub = big ? units : 0;
@@ -734,6 +740,15 @@ __global__ void k_lat_hits(LatArgs A) {
   }
 }
 
+int inline_units_setting(const ow_ctx* ctx) {
+  if (ctx->lat_inline_set) return ctx->lat_inline_units;
+  static const int v = [] {
+    const char* e = getenv("OW_INLINE_UNITS");
+    return e ? atoi(e) : INLINE_UNITS;
+  }();
+  return v;
+}
+
 LatArgs make_args(ow_ctx* ctx) {
   LatArgs A;
   memset(&A, 0, sizeof(A));
@@ -800,6 +815,7 @@ LatArgs make_args(ow_ctx* ctx) {
   A.ihit_cap = ctx->lat_ihit_cap;
   A.ihit_d = (unsigned long long*)(ctx->d_small + 49);
   A.iru_d = (unsigned long long*)(ctx->d_small + 50);
+  A.inline_units = inline_units_setting(ctx);
   A.bcount = (int32_t*)ctx->slot_ptr[SLOT_LAT_BCOUNT];
   A.bmask = (unsigned long long*)ctx->slot_ptr[SLOT_LAT_BMASK];
   A.boff = (const int64_t*)ctx->slot_ptr[SLOT_LAT_BOFFS];
@@ -862,7 +878,9 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   if (n_leaves <= 0) return OW_OK;
   // row / unit capacities: last pass's sizes + 25 % (first pass: per-face guess);
   // an overflow is detected at the single readback and the pass re-runs
-  if (ctx->lat_row_cap < 64 * n_faces + 1024) ctx->lat_row_cap = 64 * n_faces + 1024;
+  const int inline_all = inline_units_setting(ctx) >= C;  // no rows for k_lat_mt
+  const int64_t rows0 = inline_all ? 1024 : 64 * n_faces + 1024;
+  if (ctx->lat_row_cap < rows0) ctx->lat_row_cap = rows0;
   if (ctx->lat_unit_cap < 8 * ctx->lat_row_cap) ctx->lat_unit_cap = 8 * ctx->lat_row_cap;
   if (ctx->lat_ihit_cap < 8 * n_faces + 65536) ctx->lat_ihit_cap = 8 * n_faces + 65536;
   const int64_t rcap = ctx->lat_row_cap, ucap = ctx->lat_unit_cap, icap = ctx->lat_ihit_cap;
@@ -960,6 +978,14 @@ extern "C" int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, 
   OW_PROF_END(ctx, PROF_LATTICE, s);
   ctx->launches += 2;
   OW_CHECK_LAUNCH();
+  return OW_OK;
+}
+
+// Rows of more than `units` cells are tested by k_lat_mt, the others inside
+// k_lat_faces; units < 0 restores the default (tuning / testing knob)
+extern "C" int ow_lattice_set_inline_units(ow_ctx* ctx, int32_t units) {
+  ctx->lat_inline_set = units >= 0;
+  ctx->lat_inline_units = units;
   return OW_OK;
 }
 
