@@ -112,7 +112,8 @@ typedef struct {
   float bbox_min[3];
   float bbox_max[3];
   float abs_max;
-  float _pad;
+  float mean_extent;        /* mean largest bounding-box side per face (approximate:
+                               unordered float sum; shapes work, never results) */
 } ow_face_summary;
 int ow_face_check(ow_ctx* ctx, int32_t dim, const float* d_coords, int64_t n_faces,
                   ow_face_summary* out, void* stream);
@@ -299,10 +300,12 @@ int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int32_t level,
                                  int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int8_t* h_dirs,
                                  int32_t n_dirs, uint32_t* d_flags, int64_t* out_boundary, void* stream);
 int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, void* stream);
-/* Tuning / testing knob of the lattice sweep: rows of more than `units` cells
- * are tested by the unit-balanced k_lat_mt pass, the others inside the
- * face pass (default 64: all rows inline); units < 0 restores the default. */
-int ow_lattice_set_inline_units(ow_ctx* ctx, int32_t units);
+/* Tuning / testing knobs of the lattice sweep (results never depend on them):
+ * rows of more than `inline_units` cells are tested by the unit-balanced
+ * k_lat_mt pass, the others inside the face pass (default 64: all inline);
+ * faces_per_warp (4 or 8) fixes the face pass's lane groups (default: chosen
+ * from the mean face size against the finest block).  Negative = default. */
+int ow_lattice_tune(ow_ctx* ctx, int32_t inline_units, int32_t faces_per_warp);
 
 /* Work counters of the last ow_lattice_links_count: [0] candidate blocks,
  * [1] (block, face, direction) rows, [2] Moller-Trumbore / segment tests. */

@@ -70,7 +70,7 @@ class FaceSummary(C.Structure):  # ow_face_summary
         ("bbox_min", C.c_float * 3),
         ("bbox_max", C.c_float * 3),
         ("abs_max", C.c_float),
-        ("_pad", C.c_float),
+        ("mean_extent", C.c_float),
     ]
 
 
@@ -190,7 +190,7 @@ _SIGS = {
                                      I32, P, PI64, P],
     "ow_lattice_links_emit": [P, P, P, P],
     "ow_lattice_stats": [P, PI64, P],
-    "ow_lattice_set_inline_units": [P, C.c_int32],
+    "ow_lattice_tune": [P, C.c_int32, C.c_int32],
     "ow_near_pairs": [P, I32, P, P, P, I64, P, P],
     "ow_export_vtk": [P, C.POINTER(ForestView), C.c_char_p, C.c_char_p, P],
     "ow_referee_pairs": [P, I32, P, P, P, I64, P, P, P],

@@ -130,6 +130,8 @@ struct ow_ctx {
   int64_t lat_row_cap, lat_unit_cap, lat_ihit_cap;
   int32_t lat_inline_units;
   bool lat_inline_set;
+  float lat_mean_extent;
+  int32_t lat_fpw;  // faces per warp of the face pass (0: chosen per call)  // mean largest face side when known (geometry_to_grid), else 0
   int64_t lat_pos_lo, lat_pos_hi;  // leaf-position slice of the last count call  // capacities of the single-pass row / unit lists
   int32_t lat_dirs, lat_level;
   int8_t lat_dir[27 * 3];

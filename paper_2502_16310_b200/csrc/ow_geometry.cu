@@ -51,6 +51,7 @@ __device__ __forceinline__ void atomic_max_f(float* a, float v) {
 // then floats: min[3], max[3], absmax at ((float*)(small+2))[0..6]
 __global__ void __launch_bounds__(256) k_face_check(int dim, const float* __restrict__ c, int64_t n, int64_t* small) {
   float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY}, am = 0.0f;
+  float ext_sum = 0.0f;  // sum of per-face largest bounding-box sides (a work-shape estimate)
   unsigned long long bad_deg = ~0ull, bad_fin = ~0ull;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     float v[3][3];
@@ -68,6 +69,13 @@ __global__ void __launch_bounds__(256) k_face_check(int dim, const float* __rest
       bad_fin = min(bad_fin, (unsigned long long)k);
       continue;
     }
+    float side = 0.0f;
+    for (int a = 0; a < dim; ++a) {
+      float lo = v[0][a], hi = v[0][a];
+      for (int j = 1; j < dim; ++j) lo = fminf(lo, v[j][a]), hi = fmaxf(hi, v[j][a]);
+      side = fmaxf(side, hi - lo);
+    }
+    ext_sum += side;
     bool deg;
     if (dim == 2) {  // geometry.py:281-285
       double dx = DSUB((double)v[1][0], (double)v[0][0]), dy = DSUB((double)v[1][1], (double)v[0][1]);
@@ -98,6 +106,7 @@ __global__ void __launch_bounds__(256) k_face_check(int dim, const float* __rest
       mx[a] = fmaxf(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
     }
     am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+    ext_sum += __shfl_xor_sync(0xffffffffu, ext_sum, o);
     bad_deg = min(bad_deg, __shfl_xor_sync(0xffffffffu, bad_deg, o));
     bad_fin = min(bad_fin, __shfl_xor_sync(0xffffffffu, bad_fin, o));
   }
@@ -108,6 +117,7 @@ __global__ void __launch_bounds__(256) k_face_check(int dim, const float* __rest
       atomic_max_f(&fs[3 + a], mx[a]);
     }
     atomic_max_f(&fs[6], am);
+    atomicAdd(&fs[7], ext_sum);
     if (bad_deg != ~0ull) atomicMin((unsigned long long*)&small[0], bad_deg);
     if (bad_fin != ~0ull) atomicMin((unsigned long long*)&small[1], bad_fin);
   }
@@ -185,6 +195,6 @@ extern "C" int ow_face_check(ow_ctx* ctx, int32_t dim, const float* d_coords, in
     out->bbox_max[a] = fs[3 + a];
   }
   out->abs_max = fs[6];
-  out->_pad = 0.0f;
+  out->mean_extent = n > 0 ? fs[7] / (float)n : 0.0f;
   return OW_OK;
 }

@@ -301,8 +301,8 @@ __device__ __forceinline__ int row_cell(unsigned w, int rem, const float* cen_po
 // and writes them; rows past the capacities are counted, not written (the
 // host re-runs with room).  Links parallel to the face (det == 0) are rejected
 // by k_lat_mt.
-constexpr int FACES_PER_WARP = 4;
-constexpr int SLOT_LANES = 32 / FACES_PER_WARP;
+// (FPW faces per warp is a template parameter: 4 for faces spanning several
+// finest blocks, 8 when most faces reach only one or two, see faces_per_warp)
 // Rows of at most this many cells are tested inside k_lat_faces; larger ones
 // by k_lat_mt.  Measured on C2/C3/C5 (OW_INLINE_UNITS sweep, profiles/): the
 // inline sweep wins at every row size, so by default every row is inline
@@ -325,9 +325,10 @@ __device__ __forceinline__ int flush_hits(const LatArgs& A, const uint2* hb, con
   return 0;
 }
 
-template <int D>
+template <int D, int FPW>
 __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   constexpr int C = D == 3 ? 64 : 16;
+  constexpr int FACES_PER_WARP = FPW, SLOT_LANES = 32 / FPW;
   __shared__ float4 s_face[4][FACES_PER_WARP][3];  // per warp: (v0, e1, e2) / (a, s) of its faces
   __shared__ uint2 s_hit[4][HITBUF];
   __shared__ uint8_t s_hdir[4][HITBUF];
@@ -740,6 +741,25 @@ __global__ void k_lat_hits(LatArgs A) {
   }
 }
 
+// Faces per warp of k_lat_faces: 8 lane groups of 4 when faces are small next
+// to the finest blocks (most reach one or two blocks per axis), else 4 of 8.
+// OW_FACES_PER_WARP overrides (tuning).
+int faces_per_warp(const ow_ctx* ctx, int D, int64_t n_faces, int64_t n_leaves) {
+  static const int env = [] {
+    const char* e = getenv("OW_FACES_PER_WARP");
+    return e ? atoi(e) : 0;
+  }();
+  if (ctx->lat_fpw) return ctx->lat_fpw;
+  if (env == 4 || env == 8) return env;
+  if (ctx->lat_mean_extent > 0.0f) {  // measured (C2-C5 sweep): 8 wins at 0.17 and 0.28 blocks, 4 at 0.69 and 0.94
+    const ow_forest* f = &ctx->lat_forest;
+    double q = INFINITY;
+    for (int a = 0; a < D; ++a) q = fmin(q, f->dext[a] / (double)((int64_t)f->root[a] << ctx->lat_level));
+    return (double)ctx->lat_mean_extent < 0.5 * q ? 8 : 4;
+  }
+  return n_faces > 4 * n_leaves ? 8 : 4;
+}
+
 int inline_units_setting(const ow_ctx* ctx) {
   if (ctx->lat_inline_set) return ctx->lat_inline_units;
   static const int v = [] {
@@ -911,8 +931,14 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   else k_lat_pos<2><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
   // the sweep: k_lat_faces (rows; small rows tested inline) + k_lat_mt (large rows)
   OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
-  if (D == 3) k_lat_faces<3><<<ow_blocks(n_faces, 4 * FACES_PER_WARP), 128, 0, s>>>(A);
-  else k_lat_faces<2><<<ow_blocks(n_faces, 4 * FACES_PER_WARP), 128, 0, s>>>(A);
+  const int fpw = faces_per_warp(ctx, D, n_faces, nl);
+  if (D == 3) {
+    if (fpw == 8) k_lat_faces<3, 8><<<ow_blocks(n_faces, 4 * 8), 128, 0, s>>>(A);
+    else k_lat_faces<3, 4><<<ow_blocks(n_faces, 4 * 4), 128, 0, s>>>(A);
+  } else {
+    if (fpw == 8) k_lat_faces<2, 8><<<ow_blocks(n_faces, 4 * 8), 128, 0, s>>>(A);
+    else k_lat_faces<2, 4><<<ow_blocks(n_faces, 4 * 4), 128, 0, s>>>(A);
+  }
   ctx->launches += 2;
   OW_CHECK_LAUNCH();
   OW_TRY(ow::scan01(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s));
@@ -981,11 +1007,17 @@ extern "C" int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, 
   return OW_OK;
 }
 
-// Rows of more than `units` cells are tested by k_lat_mt, the others inside
-// k_lat_faces; units < 0 restores the default (tuning / testing knob)
-extern "C" int ow_lattice_set_inline_units(ow_ctx* ctx, int32_t units) {
-  ctx->lat_inline_set = units >= 0;
-  ctx->lat_inline_units = units;
+// Tuning / testing knobs: rows of more than `inline_units` cells are tested by
+// k_lat_mt, the others inside k_lat_faces; faces_per_warp 4 or 8 fixes the
+// face-pass shape.  Negative values restore the defaults.
+extern "C" int ow_lattice_tune(ow_ctx* ctx, int32_t inline_units, int32_t faces_per_warp) {
+  if (faces_per_warp >= 0 && faces_per_warp != 4 && faces_per_warp != 8) {
+    ow_set_error("lattice: faces_per_warp must be 4 or 8, got %d", faces_per_warp);
+    return OW_ERR_INVALID;
+  }
+  ctx->lat_inline_set = inline_units >= 0;
+  ctx->lat_inline_units = inline_units;
+  ctx->lat_fpw = faces_per_warp > 0 ? faces_per_warp : 0;
   return OW_OK;
 }
 

@@ -455,8 +455,11 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
     OW_CHECK_LAUNCH();
   }
   int64_t nb = 0;
-  OW_TRY(ow_lattice_links_count(ctx, f, finest, (const int32_t*)pl, nl, d_coords, n_faces, geom_key, grid,
-                                p->lattice_dirs, p->lattice_q, (uint32_t*)flags, &nb, stream));
+  ctx->lat_mean_extent = out->faces.mean_extent;  // shapes the face pass
+  const int lst = ow_lattice_links_count(ctx, f, finest, (const int32_t*)pl, nl, d_coords, n_faces, geom_key, grid,
+                                         p->lattice_dirs, p->lattice_q, (uint32_t*)flags, &nb, stream);
+  ctx->lat_mean_extent = 0.0f;
+  OW_TRY(lst);
   out->n_boundary = nb;
   void *cells, *q;
   if (out_buffer(p, OW_OUT_CELLS, 8 * nb, &cells) || out_buffer(p, OW_OUT_Q, 4 * nb * p->lattice_q, &q)) {

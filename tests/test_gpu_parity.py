@@ -287,16 +287,16 @@ def test_pipeline_random_soups_vs_oracle(ow, dim, seed, n_faces, root, d, B):
 
 
 # --------------------------------------------------------------------------- lattice links vs oracle
-@pytest.fixture(params=[None, 0, 6], ids=["inline-all", "mt-all", "split6"])
+@pytest.fixture(params=[(-1, 4), (-1, 8), (0, 4), (6, 8)], ids=["inline-fpw4", "inline-fpw8", "mt-all", "split6"])
 def inline_units(request):
-    """Row routing of the lattice sweep: default (every row tested inside the
-    face pass), every row through k_lat_mt, rows of > 6 cells through k_lat_mt."""
+    """Shapes of the lattice sweep (results must not depend on them): every
+    row tested inside the face pass with 4 or 8 faces per warp, every row
+    through k_lat_mt, rows of > 6 cells through k_lat_mt."""
     from paper_2502_16310_b200 import _lib
 
-    if request.param is not None:
-        _lib.call("ow_lattice_set_inline_units", _lib.ctx(), request.param)
+    _lib.call("ow_lattice_tune", _lib.ctx(), *request.param)
     yield request.param
-    _lib.call("ow_lattice_set_inline_units", _lib.ctx(), -1)
+    _lib.call("ow_lattice_tune", _lib.ctx(), -1, -1)
 
 
 @pytest.mark.parametrize("case", ["circle", "icosphere", "soup3d", "soup2d"])
