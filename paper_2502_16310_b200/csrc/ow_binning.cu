@@ -153,14 +153,12 @@ __device__ __forceinline__ int64_t local_to_bin(const GridC& g, const Range& r, 
 
 // small: [0] slow count, [1] first outside face (u64 min), [2] escape flag,
 // [3] too-many-samples face
+// (bin, face) pairs of one face by its samples (MaskVisit walk); faces whose
+// padded range or sample count is too large go to the slow list
 template <int D>
-__global__ void __launch_bounds__(256)
-k_count_fast(GridC g, const float* __restrict__ c, int64_t n, float h, unsigned long long* masks, int32_t* nb,
-             int32_t* counts, int32_t* slow, int64_t* small) {
-  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= n) return;
-  float v[3][3];
-  load_face<D>(c, n, f, v);
+__device__ __forceinline__ void count_walk(const GridC& g, const float v[3][3], int64_t f, float h,
+                                           unsigned long long* masks, int32_t* nb, int32_t* counts, int32_t* slow,
+                                           int64_t* small) {
   Range r = face_range<D>(g, v, 1);
   bool go_slow = r.vol > 64 || estimate_samples<D>(v, h) > FAST_MAX_SAMPLES;
   if (!go_slow) {
@@ -188,6 +186,70 @@ k_count_fast(GridC g, const float* __restrict__ c, int64_t n, float h, unsigned 
   nb[f] = 0;
   int idx = atomicAdd((unsigned long long*)&small[0], 1ull);
   slow[idx] = (int32_t)f;
+}
+
+// Pass 1 over all faces.  Single-bin faces (most faces of a fine mesh): every
+// sample lies within 2^-16 max|x| of the vertex hull (a few roundings of hull
+// coordinates), and bin_axis is monotone, so a hull widened by that much
+// inside one bin and inside the domain puts every sample in that bin: no walk
+// needed (then bin(min) = bin(max) = b and the padded range is [b - 1, b + 1]
+// clipped).  The other faces are listed for k_count_walk, so the walks run on
+// full warps instead of stalling warps of single-bin faces.
+template <int D>
+__global__ void __launch_bounds__(256)
+k_count_fast(GridC g, const float* __restrict__ c, int64_t n, unsigned long long* masks, int32_t* nb,
+             int32_t* counts, int32_t* mid, int64_t* small) {
+  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool one = true;
+  if (f < n) {
+    float v[3][3];
+    load_face<D>(c, n, f, v);
+    int loc = 0, mul = 1;
+    int64_t lin = 0, lmul = 1;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      float mn = v[0][a], mx = v[0][a];
+#pragma unroll
+      for (int j = 1; j < D; ++j) mn = fminf(mn, v[j][a]), mx = fmaxf(mx, v[j][a]);
+      const float del = fmaxf(fabsf(mn), fabsf(mx)) * 0x1p-16f + 0x1p-100f;
+      const float lo = FSUB(mn, del), hi = FADD(mx, del);
+      const int b = bin_axis(lo, g.min32[a], g.len32[a], g.B);
+      one &= b == bin_axis(hi, g.min32[a], g.len32[a], g.B) && (double)lo >= g.lo_tol[a] && (double)hi <= g.hi_tol[a];
+      const int rlo = max(b - 1, 0), rhi = min(b + 1, g.B - 1);
+      loc += (b - rlo) * mul;
+      mul *= rhi - rlo + 1;
+      lin += (int64_t)b * lmul;
+      lmul *= g.B;
+    }
+    if (one) {
+      masks[f] = 1ull << loc;
+      nb[f] = 1;
+      atomicAdd(&counts[lin], 1);
+    }
+  }
+  const bool walk = f < n && !one;
+  const unsigned wm = __ballot_sync(0xffffffffu, walk);
+  if (wm) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd((unsigned long long*)&small[6], (unsigned long long)__popc(wm));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (walk) mid[base + __popc(wm & lanemask_lt())] = (int32_t)f;
+  }
+}
+
+// Pass 2: the listed faces, by their samples (count on the device)
+template <int D>
+__global__ void __launch_bounds__(256)
+k_count_walk(GridC g, const float* __restrict__ c, int64_t n, float h, const int32_t* __restrict__ mid,
+             unsigned long long* masks, int32_t* nb, int32_t* counts, int32_t* slow, int64_t* small) {
+  const int64_t m = small[6];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = mid[i];
+    float v[3][3];
+    load_face<D>(c, n, f, v);
+    count_walk<D>(g, v, f, h, masks, nb, counts, slow, small);
+  }
 }
 
 struct BitVisitCtx {
@@ -355,9 +417,14 @@ int fill_count(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, 
   OW_CUDA(cudaMemsetAsync(counts, 0, 4 * (size_t)n_bins, s));
   k_small_init<<<1, 32, 0, s>>>(small);  // [1], [3] = -1 (none), rest 0
   OW_LAUNCHED(ctx);
-  k_count_fast<D><<<ow_blocks(n, 256), 256, 0, s>>>(g, c, n, h, (unsigned long long*)pm, (int32_t*)pnb, counts,
-                                                   (int32_t*)psl, small);
-  OW_LAUNCHED(ctx);
+  void* pmid;
+  OW_TRY(ow_slot(ctx, SLOT_BIN_MID, 4 * (size_t)n, s, &pmid));
+  k_count_fast<D><<<ow_blocks(n, 256), 256, 0, s>>>(g, c, n, (unsigned long long*)pm, (int32_t*)pnb, counts,
+                                                   (int32_t*)pmid, small);
+  k_count_walk<D><<<ow_blocks(n, 256, 8 * OW_SMS), 256, 0, s>>>(g, c, n, h, (const int32_t*)pmid,
+                                                                (unsigned long long*)pm, (int32_t*)pnb, counts,
+                                                                (int32_t*)psl, small);
+  ctx->launches += 2;
   OW_CHECK_LAUNCH();
   // face offsets over the fast path's counts, read back with the slow-face
   // count in one round trip; faces with too many bins for the bitmask path

@@ -71,6 +71,7 @@ enum ow_slot {
   SLOT_LAT_HITS,       // hit list (flat cell, t bits)
   SLOT_LAT_HITDIR,     // hit list directions
   SLOT_LAT_TILEHITS,   // hits per intersection tile
+  SLOT_BIN_MID,        // faces whose bins need the sample walk
   SLOT_LAT_IHITS,      // hit list of the rows swept inline by k_lat_faces (flat cell, t bits)
   SLOT_LAT_IHITDIR,    // ... and their directions
   SLOT_LAT_BMASK,      // boundary-cell mask per candidate block

@@ -12,11 +12,19 @@ constexpr int STL_TILE = 256;  // faces per CTA
 // shared memory with coalesced 16-bit loads, then emit 9 coalesced float planes.
 __global__ void __launch_bounds__(STL_TILE)
 k_stl_to_soa(const uint16_t* rec16, int64_t n, float* coords) {
-  __shared__ uint16_t s[STL_TILE * 25];
+  __shared__ __align__(16) uint16_t s[STL_TILE * 25];
   const int64_t f0 = (int64_t)blockIdx.x * STL_TILE;
   const int64_t nf = min((int64_t)STL_TILE, n - f0);
   const uint16_t* src = rec16 + f0 * 25;
-  for (int i = threadIdx.x; i < nf * 25; i += STL_TILE) s[i] = src[i];
+  int i0 = 0;  // 16-byte loads when the tile is 16-byte aligned (the common case), 2-byte for the rest
+  if ((((uintptr_t)src) & 15) == 0) {
+    const int nv = (int)(nf * 50 / 16);
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(s);
+    for (int i = threadIdx.x; i < nv; i += STL_TILE) d4[i] = s4[i];
+    i0 = nv * 8;
+  }
+  for (int i = i0 + threadIdx.x; i < nf * 25; i += STL_TILE) s[i] = src[i];
   __syncthreads();
   if (threadIdx.x < nf) {
     const uint16_t* r = s + threadIdx.x * 25 + 6;  // skip the 12-byte normal
@@ -110,7 +118,27 @@ __global__ void __launch_bounds__(256) k_face_check(int dim, const float* __rest
     bad_deg = min(bad_deg, __shfl_xor_sync(0xffffffffu, bad_deg, o));
     bad_fin = min(bad_fin, __shfl_xor_sync(0xffffffffu, bad_fin, o));
   }
-  if ((threadIdx.x & 31) == 0) {
+  // CTA reduce (warp 0), then one atomic per quantity per CTA
+  __shared__ float s_f[8][8];
+  __shared__ unsigned long long s_b[8][2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    for (int a = 0; a < 3; ++a) s_f[w][a] = mn[a], s_f[w][3 + a] = mx[a];
+    s_f[w][6] = am;
+    s_f[w][7] = ext_sum;
+    s_b[w][0] = bad_deg;
+    s_b[w][1] = bad_fin;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+    for (int k = 1; k < nw; ++k) {
+      for (int a = 0; a < 3; ++a) mn[a] = fminf(mn[a], s_f[k][a]), mx[a] = fmaxf(mx[a], s_f[k][3 + a]);
+      am = fmaxf(am, s_f[k][6]);
+      ext_sum += s_f[k][7];
+      bad_deg = min(bad_deg, s_b[k][0]);
+      bad_fin = min(bad_fin, s_b[k][1]);
+    }
     float* fs = (float*)(small + 2);
     for (int a = 0; a < dim; ++a) {
       atomic_min_f(&fs[a], mn[a]);
@@ -181,7 +209,7 @@ extern "C" int ow_face_check(ow_ctx* ctx, int32_t dim, const float* d_coords, in
   k_face_check_init<<<1, 1, 0, s>>>(ctx->d_small);
   OW_LAUNCHED(ctx);
   if (n > 0) {
-    k_face_check<<<ow_blocks(n, 256, 4 * OW_SMS), 256, 0, s>>>(dim, d_coords, n, ctx->d_small);
+    k_face_check<<<ow_blocks(n, 256, 16 * OW_SMS), 256, 0, s>>>(dim, d_coords, n, ctx->d_small);
     OW_LAUNCHED(ctx);
   }
   OW_CHECK_LAUNCH();

@@ -691,20 +691,30 @@ __global__ void k_lat_bcount(LatArgs A) {
 }
 
 // boundary rows in (block, cell) order: cells and q rows (-1 where the link
-// misses; flagged entries start at +big and receive min t from k_lat_hits)
+// misses; flagged entries start at +big and receive min t from k_lat_hits).
+// CTA per candidate block: the block's q rows are one contiguous run, written
+// linearly (coalesced) from the flags staged in shared memory.
 template <int D>
 __global__ void k_lat_emit(LatArgs A) {
   constexpr int C = D == 3 ? 64 : 16;
+  __shared__ unsigned s_fl[C];
   const int64_t r = blockIdx.x;
   const unsigned long long m = A.bmask[r];
   const int c = threadIdx.x;
-  if (!((m >> c) & 1ull)) return;
   const int64_t pos = A.cand_blocks[r];
-  const unsigned fl = A.flags[pos * C + c];
-  const int64_t row = A.boff[r] + __popcll(m & ((1ull << c) - 1ull));
-  A.cells_out[row] = pos * C + c;
-  float* q = A.q_out + row * A.nq;
-  for (int i = 0; i < A.nq; ++i) q[i] = ((fl >> i) & 1) ? __uint_as_float(0x7f7f7f7fu) : -1.0f;
+  const int64_t row0 = A.boff[r];
+  if ((m >> c) & 1ull) {
+    const int k = __popcll(m & ((1ull << c) - 1ull));
+    s_fl[k] = A.flags[pos * C + c];
+    A.cells_out[row0 + k] = pos * C + c;
+  }
+  __syncthreads();
+  const int nrow = __popcll(m), nq = A.nq;
+  float* q = A.q_out + row0 * nq;
+  for (int i = c; i < nrow * nq; i += C) {
+    const int k = i / nq, d = i - k * nq;
+    q[i] = ((s_fl[k] >> d) & 1u) ? __uint_as_float(0x7f7f7f7fu) : -1.0f;
+  }
 }
 
 // min t per (boundary row, direction): t >= 0, so float order = uint order.
@@ -730,14 +740,29 @@ __global__ void k_lat_hits(LatArgs A) {
       atomicMin(reinterpret_cast<unsigned*>(A.q_out) + row * A.nq + A.hit_dir[i], h.y);
     }
   }
-  const int64_t ni = (int64_t)*A.ihit_d;  // hits of the rows swept inline (<= capacity here)
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint2 h = A.ihits[i];
-    const int64_t pos = h.x / C;
-    const int c = (int)(h.x % C);
-    const int r = A.cand_rank[pos];
-    const int64_t row = A.boff[r] + __popcll(A.bmask[r] & ((1ull << c) - 1ull));
-    atomicMin(reinterpret_cast<unsigned*>(A.q_out) + row * A.nq + A.ihit_dir[i], h.y);
+  // hits of the rows swept inline (<= capacity here): HU independent chains
+  // (hit -> rank -> row offset / mask -> atomic) in flight per thread
+  constexpr int HU = 4;
+  const int64_t ni = (int64_t)*A.ihit_d;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < ni; i0 += HU * stride) {
+    uint2 h[HU];
+    int dir[HU], r[HU];
+#pragma unroll
+    for (int k = 0; k < HU; ++k) {
+      const int64_t i = i0 + k * stride;
+      h[k] = i < ni ? A.ihits[i] : make_uint2(0u, 0u);
+      dir[k] = i < ni ? A.ihit_dir[i] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < HU; ++k) r[k] = i0 + k * stride < ni ? A.cand_rank[h[k].x / C] : 0;
+#pragma unroll
+    for (int k = 0; k < HU; ++k) {
+      if (i0 + k * stride >= ni) continue;
+      const int c = (int)(h[k].x % C);
+      const int64_t row = A.boff[r[k]] + __popcll(A.bmask[r[k]] & ((1ull << c) - 1ull));
+      atomicMin(reinterpret_cast<unsigned*>(A.q_out) + row * A.nq + dir[k], h[k].y);
+    }
   }
 }
 
@@ -996,10 +1021,10 @@ extern "C" int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, 
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
   if (ctx->lat_forest.dim == 3) {
     k_lat_emit<3><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
-    k_lat_hits<3><<<2 * OW_SMS, 256, 0, s>>>(A);
+    k_lat_hits<3><<<8 * OW_SMS, 256, 0, s>>>(A);
   } else {
     k_lat_emit<2><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
-    k_lat_hits<2><<<2 * OW_SMS, 256, 0, s>>>(A);
+    k_lat_hits<2><<<8 * OW_SMS, 256, 0, s>>>(A);
   }
   OW_PROF_END(ctx, PROF_LATTICE, s);
   ctx->launches += 2;

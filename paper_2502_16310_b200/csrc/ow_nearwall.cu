@@ -23,36 +23,50 @@ using ow::scan;
 
 constexpr int MARK_THREADS = 128;
 
+constexpr int PREP_THREADS = 128;
+
+// Per-face terms of marking: FP32 box, bounding sphere and predicate payload.
+// Records are assembled in shared memory and leave as contiguous float4 runs
+// (a thread's own 192-byte payload record would be a 16-byte scatter per lane).
 template <int D>
-__global__ void k_face_prep(const float* __restrict__ c, int64_t n, float d, double reach, float4* box,
-                            float4* sph, float4* pay) {
-  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= n) return;
-  float lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-  for (int a = 0; a < D; ++a) {
-    float mn = c[(int64_t)a * n + f], mx = mn;
-    for (int j = 1; j < D; ++j) {
-      float x = c[((int64_t)j * D + a) * n + f];
-      mn = fminf(mn, x);
-      mx = fmaxf(mx, x);
+__global__ void __launch_bounds__(PREP_THREADS) k_face_prep(const float* __restrict__ c, int64_t n, float d,
+                                                            double reach, float4* box, float4* sph, float4* pay) {
+  constexpr int PW = D == 3 ? PAY3 : PAY2;
+  __shared__ float4 s_pay[PREP_THREADS * PW];
+  __shared__ float4 s_box[PREP_THREADS * 2];
+  const int64_t f0 = (int64_t)blockIdx.x * PREP_THREADS;
+  const int64_t f = f0 + threadIdx.x;
+  const int nv = (int)min((int64_t)PREP_THREADS, n - f0);
+  if (f < n) {
+    float lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) {
+      float mn = c[(int64_t)a * n + f], mx = mn;
+      for (int j = 1; j < D; ++j) {
+        float x = c[((int64_t)j * D + a) * n + f];
+        mn = fminf(mn, x);
+        mx = fmaxf(mx, x);
+      }
+      lo[a] = mn;
+      hi[a] = mx;
     }
-    lo[a] = mn;
-    hi[a] = mx;
+    s_box[2 * threadIdx.x] = make_float4(lo[0], lo[1], lo[2], 0.0f);
+    s_box[2 * threadIdx.x + 1] = make_float4(hi[0], hi[1], hi[2], 0.0f);
+    // bounding sphere: centre f32(0.5 (lo+hi)), radius^2 f32((|0.5 (hi-lo)| + reach)^2)
+    double ctr[3] = {0, 0, 0}, ss = 0.0;
+    for (int a = 0; a < D; ++a) {
+      double l = lo[a], h = hi[a];
+      ctr[a] = DMUL(0.5, DADD(l, h));
+      double hh = DMUL(0.5, DSUB(h, l));
+      ss = a ? DADD(ss, DMUL(hh, hh)) : DMUL(hh, hh);
+    }
+    double r = DADD(__dsqrt_rn(ss), reach);
+    sph[f] = make_float4(__double2float_rn(ctr[0]), __double2float_rn(ctr[1]), __double2float_rn(ctr[2]),
+                         __double2float_rn(DMUL(r, r)));
+    face_prep_one<D>(c, n, f, d, s_pay + threadIdx.x * PW);
   }
-  box[2 * f] = make_float4(lo[0], lo[1], lo[2], 0.0f);
-  box[2 * f + 1] = make_float4(hi[0], hi[1], hi[2], 0.0f);
-  // bounding sphere: centre f32(0.5 (lo+hi)), radius^2 f32((|0.5 (hi-lo)| + reach)^2)
-  double ctr[3] = {0, 0, 0}, ss = 0.0;
-  for (int a = 0; a < D; ++a) {
-    double l = lo[a], h = hi[a];
-    ctr[a] = DMUL(0.5, DADD(l, h));
-    double hh = DMUL(0.5, DSUB(h, l));
-    ss = a ? DADD(ss, DMUL(hh, hh)) : DMUL(hh, hh);
-  }
-  double r = DADD(__dsqrt_rn(ss), reach);
-  sph[f] = make_float4(__double2float_rn(ctr[0]), __double2float_rn(ctr[1]), __double2float_rn(ctr[2]),
-                       __double2float_rn(DMUL(r, r)));
-  face_prep_one<D>(c, n, f, d, pay + f * (D == 3 ? PAY3 : PAY2));
+  __syncthreads();
+  for (int i = threadIdx.x; i < nv * PW; i += PREP_THREADS) pay[f0 * PW + i] = s_pay[i];
+  for (int i = threadIdx.x; i < nv * 2; i += PREP_THREADS) box[f0 * 2 + i] = s_box[i];
 }
 
 int prepare_faces(ow_ctx* ctx, int dim, const float* c, int64_t n, int64_t key, float d, double reach,
@@ -69,9 +83,11 @@ int prepare_faces(ow_ctx* ctx, int dim, const float* c, int64_t n, int64_t key, 
   OW_TRY(ow_slot(ctx, SLOT_FACE_SPHERE, 16 * (size_t)n, s, &ps));
   OW_TRY(ow_slot(ctx, SLOT_FACE_PREP, need_pay, s, &pp));
   if (dim == 3)
-    k_face_prep<3><<<ow_blocks(n, 128), 128, 0, s>>>(c, n, d, reach, (float4*)pb, (float4*)ps, (float4*)pp);
+    k_face_prep<3><<<ow_blocks(n, PREP_THREADS), PREP_THREADS, 0, s>>>(c, n, d, reach, (float4*)pb, (float4*)ps,
+                                                                        (float4*)pp);
   else
-    k_face_prep<2><<<ow_blocks(n, 128), 128, 0, s>>>(c, n, d, reach, (float4*)pb, (float4*)ps, (float4*)pp);
+    k_face_prep<2><<<ow_blocks(n, PREP_THREADS), PREP_THREADS, 0, s>>>(c, n, d, reach, (float4*)pb, (float4*)ps,
+                                                                        (float4*)pp);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   ctx->prep_key = key;

@@ -296,35 +296,39 @@ struct StoreExcl {  // out[i] = exclusive prefix
 };
 
 // ---- stable LSD radix sort of (key, value) ----------------------------------
+// BITS-bit digits (8..10): keys of up to 10 bits sort in one pass, up to 20 in
+// two (bin ids of every grid here).
 constexpr int RS_THREADS = 256;
 constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
-constexpr int RS_BITS = 8;
-constexpr int RS_DIGITS = 1 << RS_BITS;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_WARP_ITEMS = RS_TILE / RS_WARPS;  // 512 contiguous items per warp
 
-static __global__ void __launch_bounds__(RS_THREADS)
+template <int BITS>
+__global__ void __launch_bounds__(RS_THREADS)
 k_radix_hist(const uint32_t* keys, int64_t n, int shift, int64_t n_tiles, int32_t* hist) {
-  __shared__ int h[RS_DIGITS];
-  for (int d = threadIdx.x; d < RS_DIGITS; d += RS_THREADS) h[d] = 0;
+  constexpr int DIG = 1 << BITS;
+  __shared__ int h[DIG];
+  for (int d = threadIdx.x; d < DIG; d += RS_THREADS) h[d] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * RS_TILE;
 #pragma unroll 4
   for (int k = 0; k < RS_ITEMS; ++k) {
     int64_t i = base + (int64_t)k * RS_THREADS + threadIdx.x;
-    if (i < n) atomicAdd(&h[(keys[i] >> shift) & (RS_DIGITS - 1)], 1);
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & (DIG - 1)], 1);
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < RS_DIGITS; d += RS_THREADS) hist[(int64_t)d * n_tiles + blockIdx.x] = h[d];
+  for (int d = threadIdx.x; d < DIG; d += RS_THREADS) hist[(int64_t)d * n_tiles + blockIdx.x] = h[d];
 }
 
-static __global__ void __launch_bounds__(RS_THREADS)
+template <int BITS>
+__global__ void __launch_bounds__(RS_THREADS)
 k_radix_scatter(const uint32_t* keys, const int32_t* vals, int64_t n, int shift, int64_t n_tiles,
                 const int32_t* hist_excl, uint32_t* keys_out, int32_t* vals_out) {
-  __shared__ int cnt[RS_WARPS][RS_DIGITS];
+  constexpr int DIG = 1 << BITS;
+  __shared__ int cnt[RS_WARPS][DIG];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int d = lane; d < RS_DIGITS; d += 32) cnt[warp][d] = 0;
+  for (int d = lane; d < DIG; d += 32) cnt[warp][d] = 0;
   __syncwarp();
   const int64_t base = (int64_t)blockIdx.x * RS_TILE + (int64_t)warp * RS_WARP_ITEMS;
   uint32_t kk[RS_ITEMS];
@@ -335,13 +339,13 @@ k_radix_scatter(const uint32_t* keys, const int32_t* vals, int64_t n, int shift,
     bool ok = i < n;
     kk[r] = ok ? keys[i] : 0u;
     vv[r] = ok ? vals[i] : 0;
-    int d = ok ? (int)((kk[r] >> shift) & (RS_DIGITS - 1)) : RS_DIGITS;
+    int d = ok ? (int)((kk[r] >> shift) & (DIG - 1)) : DIG;
     unsigned peers = __match_any_sync(0xffffffffu, d);
     if (ok && lane == __ffs(peers) - 1) cnt[warp][d] += __popc(peers);
     __syncwarp();
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < RS_DIGITS; d += RS_THREADS) {
+  for (int d = threadIdx.x; d < DIG; d += RS_THREADS) {
     int run = hist_excl[(int64_t)d * n_tiles + blockIdx.x];
 #pragma unroll
     for (int w = 0; w < RS_WARPS; ++w) {
@@ -355,7 +359,7 @@ k_radix_scatter(const uint32_t* keys, const int32_t* vals, int64_t n, int shift,
   for (int r = 0; r < RS_ITEMS; ++r) {
     int64_t i = base + r * 32 + lane;
     bool ok = i < n;
-    int d = ok ? (int)((kk[r] >> shift) & (RS_DIGITS - 1)) : RS_DIGITS;
+    int d = ok ? (int)((kk[r] >> shift) & (DIG - 1)) : DIG;
     unsigned peers = __match_any_sync(0xffffffffu, d);
     if (ok) {
       int pos = cnt[warp][d] + __popc(peers & lanemask_lt());
@@ -368,6 +372,19 @@ k_radix_scatter(const uint32_t* keys, const int32_t* vals, int64_t n, int shift,
   }
 }
 
+template <int BITS>
+inline int radix_pass(ow_ctx* ctx, const uint32_t* ki, const int32_t* vi, uint32_t* ko, int32_t* vo, int64_t n,
+                      int shift, int64_t tiles, int32_t* hist, cudaStream_t s) {
+  k_radix_hist<BITS><<<(unsigned)tiles, RS_THREADS, 0, s>>>(ki, n, shift, tiles, hist);
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  OW_TRY(scan(ctx, LoadArr<int32_t>{hist}, StoreExcl<int32_t>{hist}, (int64_t)(1 << BITS) * tiles, nullptr, s));
+  k_radix_scatter<BITS><<<(unsigned)tiles, RS_THREADS, 0, s>>>(ki, vi, n, shift, tiles, hist, ko, vo);
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  return OW_OK;
+}
+
 // Sort n pairs by the low `key_bits` bits of key, stably.  Input in (k0, v0);
 // the sorted result pointer pair is returned through (*rk, *rv), which is
 // either (k0, v0) or (k1, v1).
@@ -376,20 +393,20 @@ inline int radix_sort_pairs(ow_ctx* ctx, uint32_t* k0, int32_t* v0, uint32_t* k1
   *rk = k0;
   *rv = v0;
   if (n <= 1 || key_bits <= 0) return OW_OK;
+  // fewest passes of 8..10-bit digits
+  const int passes = (key_bits + 9) / 10;
+  int bits = (key_bits + passes - 1) / passes;
+  if (bits < 8) bits = 8;
   int64_t tiles = (n + RS_TILE - 1) / RS_TILE;
   void* hp;
-  OW_TRY(ow_slot(ctx, SLOT_RADIX_HIST, sizeof(int32_t) * RS_DIGITS * (size_t)tiles, s, &hp));
+  OW_TRY(ow_slot(ctx, SLOT_RADIX_HIST, sizeof(int32_t) * ((size_t)1 << bits) * (size_t)tiles, s, &hp));
   int32_t* hist = (int32_t*)hp;
   uint32_t *ki = k0, *ko = k1;
   int32_t *vi = v0, *vo = v1;
-  for (int shift = 0; shift < key_bits; shift += RS_BITS) {
-    k_radix_hist<<<(unsigned)tiles, RS_THREADS, 0, s>>>(ki, n, shift, tiles, hist);
-    OW_LAUNCHED(ctx);
-    OW_CHECK_LAUNCH();
-    OW_TRY(scan(ctx, LoadArr<int32_t>{hist}, StoreExcl<int32_t>{hist}, RS_DIGITS * tiles, nullptr, s));
-    k_radix_scatter<<<(unsigned)tiles, RS_THREADS, 0, s>>>(ki, vi, n, shift, tiles, hist, ko, vo);
-    OW_LAUNCHED(ctx);
-    OW_CHECK_LAUNCH();
+  for (int shift = 0; shift < key_bits; shift += bits) {
+    if (bits == 8) OW_TRY(radix_pass<8>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s));
+    else if (bits == 9) OW_TRY(radix_pass<9>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s));
+    else OW_TRY(radix_pass<10>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s));
     uint32_t* tk = ki; ki = ko; ko = tk;
     int32_t* tv = vi; vi = vo; vo = tv;
   }
