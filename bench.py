@@ -259,8 +259,10 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         ms2 = float(t2.item()) / args.steps
         e2e = {"value": T_step / (ms2 / 1e3), "unit": "cell-face tests/s", "ms_per_step": ms2,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "result": "forest arrays (level, coords, parent, first_child, marks) + boundary cells and q; "
-                         "link flags are implied by q >= 0"}
+               "result": ("forest arrays (level, coords, parent, first_child, marks) + boundary cells and q"
+                          if text else
+                          "forest arrays (level, coords, parent, first_child, marks) + boundary rows packed: cell "
+                          "ids, flag words and the q of the set bits (GridPass.host_q() expands to the dense rows)")}
 
     # ---- roofline of the dominant kernel family
     peaks = {}

@@ -242,8 +242,16 @@ typedef struct {
   void* host_marks;         /* int8[host_block_cap] */
   int64_t host_block_cap;
   void* host_cells;         /* int64[host_row_cap] */
-  void* host_q;             /* float32[host_row_cap * lattice_q] */
+  void* host_q;             /* float32[host_row_cap * lattice_q] (dense rows; unused when the
+                               packed destinations below are given and fit) */
   int64_t host_row_cap;
+  /* packed boundary rows (preferred over host_q when both fit): the flag word
+   * of every boundary row and the q of its set bits only, rows in order and
+   * directions ascending within a row — the dense q row is -1 where a bit is
+   * clear, so the pair is the whole result at (4 + 4 popc) bytes per row */
+  void* host_row_flags;     /* uint32[host_row_cap] */
+  void* host_q_packed;      /* float32[host_link_cap] */
+  int64_t host_link_cap;
 } ow_g2g_params;
 typedef struct {
   ow_face_summary faces;
@@ -253,9 +261,11 @@ typedef struct {
   int64_t n_finest_leaves;
   int64_t n_boundary;
   int64_t lattice_stats[3];
-  int32_t host_copied;      /* bit 0: forest arrays, bit 1: boundary rows */
+  int32_t host_copied;      /* bit 0: forest arrays, bit 1: boundary rows (cells + dense q),
+                               bit 2: boundary rows packed (cells + row flags + packed q) */
   int32_t reran;            /* 1: the device-resident level loop outgrew the forest capacity
                                and the pass reran with a host round trip per level */
+  int64_t n_links;          /* boundary links = set flag bits = packed-q length */
 } ow_g2g_result;
 /* Binary STL records (or, with d_records NULL, coords already in d_coords) ->
  * validated SoA geometry -> root grid in `f` (capacity preallocated, grown
@@ -300,6 +310,13 @@ int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int32_t level,
                                  int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int8_t* h_dirs,
                                  int32_t n_dirs, uint32_t* d_flags, int64_t* out_boundary, void* stream);
 int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, void* stream);
+/* Emit plus the packed form: d_row_flags[n_boundary] = flag word per boundary
+ * row, d_q_packed[n_links] = q of the set bits (rows in order, directions
+ * ascending).  Both null = ow_lattice_links_emit. */
+int ow_lattice_links_emit_packed(ow_ctx* ctx, int64_t* d_cells, float* d_q, uint32_t* d_row_flags,
+                                 float* d_q_packed, void* stream);
+/* Boundary links (set flag bits over the boundary rows) of the last count. */
+int ow_lattice_links_n_links(ow_ctx* ctx, int64_t* out);
 /* Tuning / testing knobs of the lattice sweep (results never depend on them):
  * rows of more than `inline_units` cells are tested by the unit-balanced
  * k_lat_mt pass, the others inside the face pass (default 64: all inline);

@@ -134,6 +134,9 @@ class G2GParamsC(C.Structure):  # ow_g2g_params
         ("host_cells", C.c_void_p),
         ("host_q", C.c_void_p),
         ("host_row_cap", C.c_int64),
+        ("host_row_flags", C.c_void_p),
+        ("host_q_packed", C.c_void_p),
+        ("host_link_cap", C.c_int64),
     ]
 
 
@@ -148,6 +151,7 @@ class G2GResultC(C.Structure):  # ow_g2g_result
         ("lattice_stats", C.c_int64 * 3),
         ("host_copied", C.c_int32),
         ("reran", C.c_int32),
+        ("n_links", C.c_int64),
     ]
 
 
@@ -189,6 +193,8 @@ _SIGS = {
     "ow_lattice_links_count_range": [P, C.POINTER(ForestView), I32, P, I64, I64, I64, P, I64, I64, C.POINTER(Grid), P,
                                      I32, P, PI64, P],
     "ow_lattice_links_emit": [P, P, P, P],
+    "ow_lattice_links_emit_packed": [P, P, P, P, P, P],
+    "ow_lattice_links_n_links": [P, PI64],
     "ow_lattice_stats": [P, PI64, P],
     "ow_lattice_tune": [P, C.c_int32, C.c_int32],
     "ow_near_pairs": [P, I32, P, P, P, I64, P, P],
@@ -286,3 +292,44 @@ def profile_read():
         call("ow_profile_read", ctx(), i, C.byref(ms), C.byref(n))
         out[name] = (float(ms.value), int(n.value))
     return out
+
+
+def device_numa_node(index=None):
+    """NUMA node of the GPU's PCIe root (sysfs), or None when unknown."""
+    index = torch.cuda.current_device() if index is None else index
+    p = torch.cuda.get_device_properties(index)
+    bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+    try:
+        node = int(open(f"/sys/bus/pci/devices/{bus}/numa_node").read().strip())
+    except (OSError, ValueError):
+        return None
+    return node if node >= 0 else None
+
+
+def _cpulist(text):
+    cpus = set()
+    for part in text.strip().split(","):
+        if part:
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+    return cpus
+
+
+def bind_host_numa(index=None):
+    """Pin this process's host threads to the CPUs of the GPU's NUMA node, so
+    pinned staging buffers allocated afterwards are first-touched there and
+    H2D / D2H copies do not cross the socket interconnect.  Call it before
+    allocating pinned memory (once per rank, with the rank's device).  Returns
+    the node, or None when the topology is unknown (nothing is changed)."""
+    node = device_numa_node(index)
+    if node is None:
+        return None
+    try:
+        cpus = _cpulist(open(f"/sys/devices/system/node/node{node}/cpulist").read())
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return node
+    except (OSError, AttributeError):
+        pass
+    return None

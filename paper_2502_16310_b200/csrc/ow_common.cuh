@@ -81,6 +81,10 @@ enum ow_slot {
   SLOT_DRV_LEAVES,     // native driver: leaves of the current level
   SLOT_DRV_STATS,      // native driver: per-pass marking statistics
   SLOT_DRV_STATE,      // native driver: per-pass leaf count + refine state
+  SLOT_LAT_HCOUNT,     // boundary links (set flag bits) per candidate block
+  SLOT_LAT_HOFFS,      // packed-q offsets per candidate block
+  SLOT_LAT_RFLAGS,     // flag word per boundary row (packed host output)
+  SLOT_LAT_QPACK,      // q of the set flag bits, row-major (packed host output)
   SLOT_MISC,
   SLOT_COUNT
 };
@@ -127,7 +131,7 @@ struct ow_ctx {
   ow_forest link_forest;
   ow_grid link_grid;
   // lattice phase state
-  int64_t lat_leaves, lat_boundary, lat_faces, lat_ncb, lat_rows, lat_units;
+  int64_t lat_leaves, lat_boundary, lat_faces, lat_ncb, lat_rows, lat_units, lat_links;
   int64_t lat_row_cap, lat_unit_cap, lat_ihit_cap;
   int32_t lat_inline_units;
   bool lat_inline_set;

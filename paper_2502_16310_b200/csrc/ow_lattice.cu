@@ -84,6 +84,11 @@ struct LatArgs {
   unsigned long long* iru_d;   // inline (units << RU_ROW_BITS | rows), statistics
   int inline_units;            // rows of more cells go to k_lat_mt (OW_INLINE_UNITS overrides; tuning)
   int32_t* bcount;          // [n_cb] boundary cells per candidate block
+  int32_t* hcount;          // [n_cb] boundary links (set flag bits) per candidate block
+  int64_t* hoff;            // [n_cb] packed-q offsets
+  unsigned long long* links_d;  // device boundary-link counter (set flag bits)
+  uint32_t* rflags_out;     // [n_boundary] flag word per boundary row (packed output), or null
+  float* qp_out;            // [n_links] q of the set bits, row-major (packed output)
   unsigned long long* bmask;  // [n_cb] boundary-cell mask
   const int64_t* boff;      // [n_cb]
   int64_t* cells_out;
@@ -678,15 +683,21 @@ __global__ void k_lat_bcount(LatArgs A) {
   if (r >= *A.n_cb_d) return;
   const int64_t pos = A.cand_blocks[r];
   unsigned long long m = 0;
+  int links = 0;
 #pragma unroll
   for (int k = 0; k < (C + 31) / 32; ++k) {
     const int c = lane + 32 * k;
-    const unsigned b = __ballot_sync(0xffffffffu, c < C && A.flags[pos * C + c] != 0);
+    const unsigned fl = c < C ? A.flags[pos * C + c] : 0u;
+    const unsigned b = __ballot_sync(0xffffffffu, fl != 0);
     m |= (unsigned long long)b << (32 * k);
+    links += __popc(fl);
   }
+  links = __reduce_add_sync(0xffffffffu, links);
   if (lane == 0) {
     A.bcount[r] = __popcll(m);
+    A.hcount[r] = links;
     A.bmask[r] = m;
+    if (links) atomicAdd(A.links_d, (unsigned long long)links);
   }
 }
 
@@ -707,6 +718,7 @@ __global__ void k_lat_emit(LatArgs A) {
     const int k = __popcll(m & ((1ull << c) - 1ull));
     s_fl[k] = A.flags[pos * C + c];
     A.cells_out[row0 + k] = pos * C + c;
+    if (A.rflags_out) A.rflags_out[row0 + k] = s_fl[k];
   }
   __syncthreads();
   const int nrow = __popcll(m), nq = A.nq;
@@ -764,6 +776,37 @@ __global__ void k_lat_hits(LatArgs A) {
       atomicMin(reinterpret_cast<unsigned*>(A.q_out) + row * A.nq + dir[k], h[k].y);
     }
   }
+}
+
+// Packed q (host output): per candidate block (CTA, thread per cell) the q of
+// every set flag bit, rows in (block, cell) order and directions ascending
+// within a row — q[row][d] for the bits of rflags[row], concatenated.  With the
+// flag words it is the whole result (q = -1 where the bit is clear).
+template <int D>
+__global__ void k_lat_pack(LatArgs A) {
+  constexpr int C = D == 3 ? 64 : 16;
+  __shared__ int s_n[2];
+  const int64_t r = blockIdx.x;
+  const unsigned long long m = A.bmask[r];
+  const int c = threadIdx.x, lane = c & 31, w = c >> 5;
+  const int k = __popcll(m & ((1ull << c) - 1ull));  // row of cell c within the block
+  const int64_t row = A.boff[r] + k;
+  const unsigned fl = ((m >> c) & 1ull) ? A.rflags_out[row] : 0u;
+  constexpr unsigned FULL = C >= 32 ? 0xffffffffu : (1u << C) - 1u;  // 2D: a 16-thread CTA
+  int incl = __popc(fl);
+#pragma unroll
+  for (int o = 1; o < (C < 32 ? C : 32); o <<= 1) {
+    const int y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (C > 32) {
+    if (lane == 31) s_n[w] = incl;
+    __syncthreads();
+    if (w == 1) incl += s_n[0];
+  }
+  int64_t o = A.hoff[r] + incl - __popc(fl);
+  const float* q = A.q_out + row * A.nq;
+  for (unsigned b = fl; b; b &= b - 1u) A.qp_out[o++] = q[__ffs(b) - 1];
 }
 
 // Faces per warp of k_lat_faces: 8 lane groups of 4 when faces are small next
@@ -864,6 +907,9 @@ LatArgs make_args(ow_ctx* ctx) {
   A.bcount = (int32_t*)ctx->slot_ptr[SLOT_LAT_BCOUNT];
   A.bmask = (unsigned long long*)ctx->slot_ptr[SLOT_LAT_BMASK];
   A.boff = (const int64_t*)ctx->slot_ptr[SLOT_LAT_BOFFS];
+  A.hcount = (int32_t*)ctx->slot_ptr[SLOT_LAT_HCOUNT];
+  A.hoff = (int64_t*)ctx->slot_ptr[SLOT_LAT_HOFFS];
+  A.links_d = (unsigned long long*)(ctx->d_small + 51);
   return A;
 }
 
@@ -910,6 +956,7 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   ctx->lat_level = level;
   ctx->lat_leaves = n_leaves;
   ctx->lat_boundary = 0;
+  ctx->lat_links = 0;
   ctx->lat_ncb = 0;
   ctx->lat_rows = 0;
   ctx->lat_units = 0;
@@ -948,7 +995,9 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   OW_TRY(ow_slot(ctx, SLOT_LAT_BCOUNT, 4 * (size_t)nl, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_BMASK, 8 * (size_t)nl, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_BOFFS, 8 * (size_t)nl, s, &p));
-  OW_CUDA(cudaMemsetAsync(ctx->d_small + 48, 0, 3 * 8, s));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_HCOUNT, 4 * (size_t)nl, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_HOFFS, 8 * (size_t)nl, s, &p));
+  OW_CUDA(cudaMemsetAsync(ctx->d_small + 48, 0, 4 * 8, s));
   OW_CUDA(cudaMemsetAsync(d_flags, 0, 4 * (size_t)n_leaves * C, s));
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
   LatArgs A = make_args(ctx);
@@ -977,10 +1026,10 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   OW_CHECK_LAUNCH();
   OW_TRY(scan(ctx, BcountLoad{A.bcount, A.n_cb_d}, BoffStore{(int64_t*)A.boff, A.n_cb_d}, nl, ctx->d_small + 35, s));
   OW_PROF_END(ctx, PROF_LATTICE, s);
-  // single readback: candidate blocks, (scan scratch), boundary cells, rows, units
-  int64_t h[18];
-  OW_TRY(ow_readback(ctx, ctx->d_small + 33, 18, h, s));
-  const int64_t n_cb = h[0], nb = h[2];
+  // single readback: candidate blocks, (scan scratch), boundary cells, rows, units, links
+  int64_t h[19];
+  OW_TRY(ow_readback(ctx, ctx->d_small + 33, 19, h, s));
+  const int64_t n_cb = h[0], nb = h[2], n_links = h[18];
   const int64_t n_rows = (int64_t)((uint64_t)h[15] & RU_ROW_MASK), n_units = (int64_t)((uint64_t)h[15] >> RU_ROW_BITS);
   const int64_t n_ihits = h[16];
   if (n_rows >= (int64_t(1) << RU_ROW_BITS) - (int64_t(1) << 20)) {
@@ -1003,12 +1052,22 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   ctx->lat_rows = n_rows + (int64_t)((uint64_t)h[17] & RU_ROW_MASK);
   ctx->lat_units = n_units + (int64_t)((uint64_t)h[17] >> RU_ROW_BITS);
   ctx->lat_boundary = nb;
+  ctx->lat_links = n_links;
   *out_boundary = nb;
   return OW_OK;
 }
 
 extern "C" int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, void* stream) {
+  return ow_lattice_links_emit_packed(ctx, d_cells, d_q, nullptr, nullptr, stream);
+}
+
+extern "C" int ow_lattice_links_emit_packed(ow_ctx* ctx, int64_t* d_cells, float* d_q, uint32_t* d_row_flags,
+                                            float* d_q_packed, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
+  if ((d_row_flags == nullptr) != (d_q_packed == nullptr)) {
+    ow_set_error("ow_lattice_links_emit_packed: row flags and packed q go together");
+    return OW_ERR_INVALID;
+  }
   if (ctx->lat_dirs < 2) {
     ow_set_error("ow_lattice_links_emit without ow_lattice_links_count");
     return OW_ERR_INVALID;
@@ -1017,17 +1076,24 @@ extern "C" int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, 
   LatArgs A = make_args(ctx);
   A.cells_out = d_cells;
   A.q_out = d_q;
+  A.rflags_out = d_row_flags;
+  A.qp_out = d_q_packed;
   const int C = ctx->lat_forest.dim == 3 ? 64 : 16;
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
+  if (d_q_packed)  // packed-q offsets per candidate block (host-known count: no device bound)
+    OW_TRY(scan(ctx, ow::LoadArr<int32_t>{A.hcount}, ow::StoreExcl<int64_t>{A.hoff}, ctx->lat_ncb,
+                ctx->d_small + 36, s));
   if (ctx->lat_forest.dim == 3) {
     k_lat_emit<3><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
     k_lat_hits<3><<<8 * OW_SMS, 256, 0, s>>>(A);
+    if (d_q_packed) k_lat_pack<3><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
   } else {
     k_lat_emit<2><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
     k_lat_hits<2><<<8 * OW_SMS, 256, 0, s>>>(A);
+    if (d_q_packed) k_lat_pack<2><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
   }
   OW_PROF_END(ctx, PROF_LATTICE, s);
-  ctx->launches += 2;
+  ctx->launches += d_q_packed ? 3 : 2;
   OW_CHECK_LAUNCH();
   return OW_OK;
 }
@@ -1043,6 +1109,12 @@ extern "C" int ow_lattice_tune(ow_ctx* ctx, int32_t inline_units, int32_t faces_
   ctx->lat_inline_set = inline_units >= 0;
   ctx->lat_inline_units = inline_units;
   ctx->lat_fpw = faces_per_warp > 0 ? faces_per_warp : 0;
+  return OW_OK;
+}
+
+// boundary links (set flag bits) of the last count pass = packed-q length
+extern "C" int ow_lattice_links_n_links(ow_ctx* ctx, int64_t* out) {
+  *out = ctx->lat_links;
   return OW_OK;
 }
 

@@ -44,6 +44,21 @@ class GridPass:
     host: dict | None = None  # pinned host copies of the results (run(host=True))
     reran: bool = False  # the device-resident level loop outgrew the capacity; rerun with host sync
 
+    def host_q(self) -> np.ndarray:
+        """Dense (boundary rows, Q) float32 q from the packed host copy (-1 where
+        the link misses); valid once the stream is synchronised."""
+        h = self.host
+        return unpack_q(h["flags"].numpy().view(np.uint32), h["q_packed"].numpy(), self.links.q.shape[1])
+
+
+def unpack_q(row_flags: np.ndarray, q_packed: np.ndarray, nq: int) -> np.ndarray:
+    """Packed boundary rows -> dense q: row r's set bits of ``row_flags[r]``, in
+    ascending direction order, take the next entries of ``q_packed``."""
+    bits = ((row_flags[:, None] >> np.arange(nq, dtype=np.uint32)) & 1).astype(bool)
+    q = np.full(bits.shape, -1.0, np.float32)
+    q[bits] = q_packed[: int(bits.sum())]
+    return q
+
 
 class GridPlan:
     """Reusable setup of ``geometry_to_grid`` for one (domain, root grid,
@@ -72,6 +87,7 @@ class GridPlan:
         self._est = [0, 0, 0, 0]  # output bytes of the last pass (preallocation estimate)
         self._est_blocks = 0      # forest blocks / boundary rows of the last pass (host buffers)
         self._est_rows = 0
+        self._est_links = 0
         self._outs = {}
         self._hbuf = None
         self.reuse = bool(reuse_outputs)
@@ -111,9 +127,11 @@ class GridPlan:
         its finest-level lattice links.
 
         ``host=True`` also returns pinned host copies of the results
-        (``GridPass.host``: forest arrays, boundary cells, q): the forest
-        arrays stream to the host on a side stream while the lattice work
-        runs.  Flags are not copied: bit i of a boundary cell is q[:, i] >= 0."""
+        (``GridPass.host``: forest arrays, boundary cells, their flag words
+        and the packed q of the set bits): the forest arrays stream to the
+        host on a side stream while the lattice work runs; the boundary rows
+        travel packed ((4 + 4 popc) bytes per row instead of 4 Q) and
+        ``GridPass.host_q()`` expands them to the dense (rows, Q) array."""
         if geometry is None and records is None:
             raise InvalidParameterError("geometry_to_grid needs STL records or a geometry")
         dim = self.dim
@@ -159,13 +177,15 @@ class GridPlan:
             # pass's host results stay valid until the next host=True pass)
             nbk = max(self._est_blocks + self._est_blocks // 4 + 1024, 1024)
             nrow = max(self._est_rows + self._est_rows // 4 + 1024, 1024)
-            nq = len(self.dirs) if self.dirs is not None else 1
+            nlink = max(self._est_links + self._est_links // 4 + 4096, 4096)
             hb = self._hbuf
-            if hb is None or hb["level"].numel() < nbk or hb["cells"].numel() < nrow:
+            if (hb is None or hb["level"].numel() < nbk or hb["cells"].numel() < nrow
+                    or hb["q_packed"].numel() < nlink):
                 hb = dict(level=self._pinned(torch.int16, nbk), parent=self._pinned(torch.int32, nbk),
                           first_child=self._pinned(torch.int32, nbk), marks=self._pinned(torch.int8, nbk),
                           coords=[self._pinned(torch.int32, nbk) for _ in range(dim)],
-                          cells=self._pinned(torch.int64, nrow), q=self._pinned(torch.float32, nrow * nq))
+                          cells=self._pinned(torch.int64, nrow), flags=self._pinned(torch.int32, nrow),
+                          q_packed=self._pinned(torch.float32, nlink))
                 self._hbuf = hb
             hbuf = dict(hb)
             nbk, nrow = hb["level"].numel(), hb["cells"].numel()
@@ -174,7 +194,9 @@ class GridPlan:
             for a in range(dim):
                 gp.host_coord[a] = hbuf["coords"][a].data_ptr()
             gp.host_block_cap = nbk
-            gp.host_cells, gp.host_q, gp.host_row_cap = hbuf["cells"].data_ptr(), hbuf["q"].data_ptr(), nrow
+            gp.host_cells, gp.host_row_cap = hbuf["cells"].data_ptr(), nrow
+            gp.host_row_flags, gp.host_q_packed = hbuf["flags"].data_ptr(), hbuf["q_packed"].data_ptr()
+            gp.host_link_cap = hb["q_packed"].numel()
         out = _lib.G2GResultC()
         g, bins_t = st["g"], st["bins_t"]
         v = forest.view()
@@ -202,6 +224,7 @@ class GridPlan:
             need = (8 * nl, 4 * nl * ncell, 8 * nb, 4 * nb * nq)
             self._est = list(need)
             self._est_rows = nb
+            self._est_links = int(out.n_links)
             o = self._outs
             links = LatticeLinks(lattice=self.lattice, level=int(out.finest_level), leaves=o[0][:nl],
                                  flags=o[1][: nl * ncell], cells=o[2][:nb], q=o[3][: nb * nq].view(nb, nq))
@@ -211,10 +234,10 @@ class GridPlan:
         self.capacity = max(self.capacity, forest.n_blocks + forest.n_blocks // 4)
         hres = None
         if host:
-            hres = self._host_results(hbuf, int(out.host_copied), forest, links)
+            hres = self._host_results(hbuf, int(out.host_copied), forest, links, int(out.n_links))
         return GridPass(geom, forest, result, links, hres, bool(out.reran))
 
-    def _host_results(self, hbuf, copied, forest, links):
+    def _host_results(self, hbuf, copied, forest, links, n_links):
         """Pinned host copies (the C side streamed whatever fit; the rest is
         copied here).  Valid once the current stream is synchronised."""
         n = forest.n_blocks
@@ -230,11 +253,16 @@ class GridPlan:
                    marks=hbuf["marks"][:n], coords=[c[:n] for c in hbuf["coords"]])
         if links is not None:
             nb, nq = links.n_boundary, links.q.shape[1]
-            if not copied & 2:
-                hbuf["cells"], hbuf["q"] = self._pinned(torch.int64, nb), self._pinned(torch.float32, nb * nq)
+            if not copied & 4:  # the buffers did not fit (first pass of a plan): pack with torch
+                hit = links.q >= 0
+                rflags = (hit.to(torch.int64) << torch.arange(nq, device=hit.device)).sum(1).to(torch.int32)
+                hbuf["cells"], hbuf["flags"] = self._pinned(torch.int64, nb), self._pinned(torch.int32, nb)
+                hbuf["q_packed"] = self._pinned(torch.float32, n_links)
                 hbuf["cells"][:nb].copy_(links.cells, non_blocking=True)
-                hbuf["q"][: nb * nq].copy_(links.q.reshape(-1), non_blocking=True)
-            res["cells"], res["q"] = hbuf["cells"][:nb], hbuf["q"][: nb * nq].view(nb, nq)
+                hbuf["flags"][:nb].copy_(rflags, non_blocking=True)
+                hbuf["q_packed"][:n_links].copy_(links.q[hit], non_blocking=True)
+            res["cells"], res["flags"] = hbuf["cells"][:nb], hbuf["flags"][:nb]
+            res["q_packed"] = hbuf["q_packed"][:n_links]
         return res
 
 

@@ -643,7 +643,35 @@ def test_geometry_to_grid_host_results(ow):
         np.testing.assert_array_equal(h["first_child"].numpy(), f._first_child)
         np.testing.assert_array_equal(h["marks"].numpy(), f.marks.cpu().numpy())
         np.testing.assert_array_equal(h["cells"].numpy(), gp.links.cells.cpu().numpy())
-        np.testing.assert_array_equal(h["q"].numpy(), gp.links.q.cpu().numpy())
+        _check_packed_rows(gp)
+
+
+def _check_packed_rows(gp):
+    """Packed host rows (flag word + q of the set bits) == the device links."""
+    h, ll = gp.host, gp.links
+    cells = ll.cells.cpu().numpy()
+    flags = ll.flags.cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(h["flags"].numpy().view(np.uint32), flags[cells])
+    q = ll.q.cpu().numpy()
+    assert h["q_packed"].numel() == int((q >= 0).sum())
+    np.testing.assert_array_equal(gp.host_q(), q)
+
+
+def test_geometry_to_grid_packed_rows_2d(ow):
+    """The packed host rows of a 2D pass (16-cell blocks, D2Q9), native and
+    first-pass fallback packing."""
+    import torch
+
+    from paper_2502_16310_b200 import pipeline
+
+    geom = ow.index_to_coords(ow.generate_circle((0.5, 0.5), 0.25, 256))
+    plan = pipeline.GridPlan(ow.Aabb((0, 0), (1, 1)), (8, 8),
+                             ow.NearWallParams(d_spec=0.1, n_levels=3, bins_per_axis=8), "D2Q9")
+    for _ in range(2):
+        gp = plan.run(geometry=geom, host=True)
+        torch.cuda.current_stream().synchronize()
+        assert gp.links.n_boundary > 0
+        _check_packed_rows(gp)
 
 
 # --------------------------------------------------------------------------- predicate vs referee sampler

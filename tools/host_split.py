@@ -1,7 +1,9 @@
 """Host-side split of one GridPlan.run (GPU box helper): Python before the
 native call, the native call (which ends at its last readback), Python after.
 
-    python tools/host_split.py [C2] [steps]
+    python tools/host_split.py [C2] [steps] [host]
+
+``host``: run(host=True) from pinned STL bytes (the bench's e2e step).
 """
 
 import cProfile
@@ -41,14 +43,28 @@ def timed_call(name, *a):
 
 
 _lib.call = timed_call
+HOST = len(sys.argv) > 3 and sys.argv[3] == "host"
+rec_host = rec.cpu().pin_memory()
+_run = plan.run
+
+
+def run_step(r, nf):
+    if HOST:
+        _run(rec_host.to("cuda", non_blocking=True), nf, host=True)
+        torch.cuda.current_stream().synchronize()
+    else:
+        _run(r, nf)
+
+
+plan_run = run_step
 for _ in range(5):
-    plan.run(rec, n)
+    plan_run(rec, n)
 torch.cuda.synchronize()
 tot = pre = nat = post = 0.0
 for _ in range(steps):
     marks.clear()
     t0 = time.perf_counter()
-    plan.run(rec, n)
+    plan_run(rec, n)
     t1 = time.perf_counter()
     g = [m for m in marks if m[0] == "ow_geometry_to_grid"][0]
     tot += t1 - t0
@@ -61,7 +77,7 @@ print(f"{name}: run {1e6 * tot / steps:.1f} us = python before {1e6 * pre / step
 pr = cProfile.Profile()
 pr.enable()
 for _ in range(steps):
-    plan.run(rec, n)
+    plan_run(rec, n)
 pr.disable()
 torch.cuda.synchronize()
 pstats.Stats(pr).sort_stats("tottime").print_stats(18)

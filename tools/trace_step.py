@@ -1,7 +1,10 @@
 """GPU timeline of bench steps with torch.profiler (CUPTI): kernel gaps and the
 host call that was running during each gap (GPU box helper).
 
-    python tools/trace_step.py [C2] [steps]
+    python tools/trace_step.py [C2] [steps] [e2e]
+
+``e2e``: the bench's e2e step (pinned STL bytes in, run(host=True), results
+out, stream synchronised) instead of the HBM-resident step.
 """
 
 import json
@@ -20,7 +23,9 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 cfg = bench.CONFIGS[name]
 data = bench.make_input(cfg)
 n = int.from_bytes(data[80:84], "little")
-rec = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda()
+e2e = len(sys.argv) > 3 and sys.argv[3] == "e2e"
+rec_host = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).pin_memory()
+rec = rec_host.cuda()
 dim = cfg["dim"]
 dom = ow.Aabb(np.zeros(dim), np.ones(dim))
 params = ow.NearWallParams(d_spec=cfg["d"], n_levels=cfg["levels"], bins_per_axis=cfg["B"])
@@ -33,13 +38,18 @@ plan = pipeline.GridPlan(dom, (cfg["root"],) * dim, params, cfg["lattice"], reus
 
 
 def step():
-    plan.run(rec, n)
+    if e2e:
+        rd = rec_host.to("cuda", non_blocking=True)
+        plan.run(rd, n, host=True)
+        torch.cuda.current_stream().synchronize()
+    else:
+        plan.run(rec, n)
 
 
 for _ in range(3):
     step()
 torch.cuda.synchronize()
-out = os.path.join("gpurun_out", f"trace_{name}.json")
+out = os.path.join("gpurun_out", f"trace_{name}{'_e2e' if e2e else ''}.json")
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CPU, torch.profiler.ProfilerActivity.CUDA]) as prof:
     for _ in range(steps):
         with torch.profiler.record_function("step"):
@@ -71,3 +81,9 @@ for k in ks:
 print("per kernel (last step):")
 for nm, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:30]:
     print(f"{t:9.1f} us {c:4d}x  {nm}")
+print("copies (last step, offset from step start):")
+for k in ks:
+    if k.get("cat") in ("gpu_memcpy", "gpu_memset"):
+        b = k.get("args", {}).get("bytes", 0)
+        print(f"  +{k['ts'] - t0:8.1f} us {k['dur']:7.1f} us {b:>10} B  {k['name'][:40]}")
+print(f"last GPU op ends at +{max(k['ts'] + k['dur'] for k in ks) - t0:.1f} us of a {s['dur']:.1f} us step")
