@@ -87,6 +87,7 @@ struct LatArgs {
   int32_t* hcount;          // [n_cb] boundary links (set flag bits) per candidate block
   int64_t* hoff;            // [n_cb] packed-q offsets
   unsigned long long* links_d;  // device boundary-link counter (set flag bits)
+  unsigned long long* face_next;  // k_lat_faces: next face group (dynamic schedule)
   uint32_t* rflags_out;     // [n_boundary] flag word per boundary row (packed output), or null
   float* qp_out;            // [n_links] q of the set bits, row-major (packed output)
   unsigned long long* bmask;  // [n_cb] boundary-cell mask
@@ -330,6 +331,7 @@ __device__ __forceinline__ int flush_hits(const LatArgs& A, const uint2* hb, con
   return 0;
 }
 
+
 template <int D, int FPW>
 __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   constexpr int C = D == 3 ? 64 : 16;
@@ -342,11 +344,19 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sl = lane % SLOT_LANES;
-  const int64_t fbase = ((int64_t)blockIdx.x * 4 + wid) * FACES_PER_WARP;
-  const int64_t f = fbase + lane / SLOT_LANES;
   int nh = 0;  // hits buffered by this warp
   unsigned long long iru = 0;  // inline units / rows of this warp (statistics)
-  if (f - lane / SLOT_LANES >= A.n_faces) return;  // whole warp past the end
+  // persistent warps take face groups from a global counter: the cost of a
+  // face (blocks in reach x rows x cells) varies by orders of magnitude, so
+  // dynamic assignment replaces the static one-group-per-warp grid (whose
+  // single wave ended in a long tail of a few heavy warps)
+  for (;;) {
+  unsigned long long grp = 0;
+  if (lane == 0) grp = atomicAdd(A.face_next, 1ull);
+  grp = __shfl_sync(0xffffffffu, grp, 0);
+  const int64_t fbase = (int64_t)grp * FACES_PER_WARP;
+  if (fbase >= A.n_faces) break;  // whole warp past the end
+  const int64_t f = fbase + lane / SLOT_LANES;
   const bool live = f < A.n_faces;
   float v[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
   if (live) {
@@ -535,6 +545,8 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
         }
       }
     }
+  }
+  __syncwarp();  // s_face is rewritten by the next group
   }
   if (nh) flush_hits(A, s_hit[wid], s_hdir[wid], nh, lane);
   if (iru && lane == 0) atomicAdd(A.iru_d, iru);
@@ -828,6 +840,18 @@ int faces_per_warp(const ow_ctx* ctx, int D, int64_t n_faces, int64_t n_leaves) 
   return n_faces > 4 * n_leaves ? 8 : 4;
 }
 
+// persistent face pass: resident CTAs only (9 per SM at 56 registers x 128
+// threads), fewer when the faces do not fill them
+unsigned lat_face_grid(int64_t n_faces, int fpw) {
+  static const int per_sm = [] {
+    const char* e = getenv("OW_LAT_CTAS_PER_SM");
+    return e && atoi(e) > 0 ? atoi(e) : 9;
+  }();
+  const int64_t need = (n_faces + 4 * fpw - 1) / (4 * fpw);
+  const int64_t cap = (int64_t)per_sm * OW_SMS;
+  return (unsigned)(need < cap ? need : cap);
+}
+
 int inline_units_setting(const ow_ctx* ctx) {
   if (ctx->lat_inline_set) return ctx->lat_inline_units;
   static const int v = [] {
@@ -910,6 +934,7 @@ LatArgs make_args(ow_ctx* ctx) {
   A.hcount = (int32_t*)ctx->slot_ptr[SLOT_LAT_HCOUNT];
   A.hoff = (int64_t*)ctx->slot_ptr[SLOT_LAT_HOFFS];
   A.links_d = (unsigned long long*)(ctx->d_small + 51);
+  A.face_next = (unsigned long long*)(ctx->d_small + 52);
   return A;
 }
 
@@ -997,7 +1022,7 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   OW_TRY(ow_slot(ctx, SLOT_LAT_BOFFS, 8 * (size_t)nl, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_HCOUNT, 4 * (size_t)nl, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_HOFFS, 8 * (size_t)nl, s, &p));
-  OW_CUDA(cudaMemsetAsync(ctx->d_small + 48, 0, 4 * 8, s));
+  OW_CUDA(cudaMemsetAsync(ctx->d_small + 48, 0, 5 * 8, s));
   OW_CUDA(cudaMemsetAsync(d_flags, 0, 4 * (size_t)n_leaves * C, s));
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
   LatArgs A = make_args(ctx);
@@ -1007,11 +1032,11 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
   const int fpw = faces_per_warp(ctx, D, n_faces, nl);
   if (D == 3) {
-    if (fpw == 8) k_lat_faces<3, 8><<<ow_blocks(n_faces, 4 * 8), 128, 0, s>>>(A);
-    else k_lat_faces<3, 4><<<ow_blocks(n_faces, 4 * 4), 128, 0, s>>>(A);
+    if (fpw == 8) k_lat_faces<3, 8><<<lat_face_grid(n_faces, 8), 128, 0, s>>>(A);
+    else k_lat_faces<3, 4><<<lat_face_grid(n_faces, 4), 128, 0, s>>>(A);
   } else {
-    if (fpw == 8) k_lat_faces<2, 8><<<ow_blocks(n_faces, 4 * 8), 128, 0, s>>>(A);
-    else k_lat_faces<2, 4><<<ow_blocks(n_faces, 4 * 4), 128, 0, s>>>(A);
+    if (fpw == 8) k_lat_faces<2, 8><<<lat_face_grid(n_faces, 8), 128, 0, s>>>(A);
+    else k_lat_faces<2, 4><<<lat_face_grid(n_faces, 4), 128, 0, s>>>(A);
   }
   ctx->launches += 2;
   OW_CHECK_LAUNCH();
