@@ -17,6 +17,7 @@ timed region.  ``ms_per_step`` is the geometry-to-grid time.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -181,6 +182,8 @@ def gpu_arm(args, cfg, rank, world, local_rank):
 
     # ---- value: inputs resident in HBM
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed regions (re-enabled after e2e)
     launches0 = _lib.launches()
     with ClockSampler(local_rank) as clk:
         barrier()
@@ -263,6 +266,8 @@ def gpu_arm(args, cfg, rank, world, local_rank):
                           if text else
                           "forest arrays (level, coords, parent, first_child, marks) + boundary rows packed: cell "
                           "ids, flag words and the q of the set bits (GridPass.host_q() expands to the dense rows)")}
+
+    gc.enable()
 
     # ---- roofline of the dominant kernel family
     peaks = {}

@@ -199,6 +199,7 @@ template <int D>
 __global__ void __launch_bounds__(256)
 k_count_fast(GridC g, const float* __restrict__ c, int64_t n, unsigned long long* masks, int32_t* nb,
              int32_t* counts, int32_t* mid, int64_t* small) {
+  ow_pdl_wait();
   int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool one = true;
   if (f < n) {
@@ -243,6 +244,7 @@ template <int D>
 __global__ void __launch_bounds__(256)
 k_count_walk(GridC g, const float* __restrict__ c, int64_t n, float h, const int32_t* __restrict__ mid,
              unsigned long long* masks, int32_t* nb, int32_t* counts, int32_t* slow, int64_t* small) {
+  ow_pdl_wait();
   const int64_t m = small[6];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t f = mid[i];
@@ -288,6 +290,7 @@ template <int D>
 __global__ void __launch_bounds__(256)
 k_count_slow(GridC g, const float* __restrict__ c, int64_t n, float h, const int32_t* slow,
              const int64_t* bitoff, unsigned* bitmap, int32_t* nb, int32_t* counts, int64_t* small) {
+  ow_pdl_wait();
   const int64_t f = slow[blockIdx.x];
   float v[3][3];
   load_face<D>(c, n, f, v);
@@ -345,6 +348,7 @@ struct SlowVolLoad {
 template <int D>
 __global__ void k_emit_fast(GridC g, const float* __restrict__ c, int64_t n, const unsigned long long* masks,
                             const int32_t* foff, uint32_t* keys, int32_t* vals) {
+  ow_pdl_wait();
   int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= n) return;
   unsigned long long m = masks[f];
@@ -367,6 +371,7 @@ template <int D>
 __global__ void k_emit_slow(GridC g, const float* __restrict__ c, int64_t n, const int32_t* slow,
                             const int64_t* bitoff, const unsigned* bitmap, const int32_t* foff, uint32_t* keys,
                             int32_t* vals) {
+  ow_pdl_wait();
   const int64_t f = slow[blockIdx.x];
   const int lane = threadIdx.x;
   float v[3][3];
@@ -402,6 +407,7 @@ __global__ void k_emit_slow(GridC g, const float* __restrict__ c, int64_t n, con
 }
 
 __global__ void k_small_init(int64_t* small) {
+  ow_pdl_wait();
   if (threadIdx.x < 8) small[threadIdx.x] = (threadIdx.x == 1 || threadIdx.x == 3) ? -1 : 0;
 }
 
@@ -415,13 +421,13 @@ int fill_count(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, 
   OW_TRY(ow_slot(ctx, SLOT_BIN_SLOW, 4 * (size_t)n, s, &psl));
   int64_t* small = ctx->d_small;
   OW_CUDA(cudaMemsetAsync(counts, 0, 4 * (size_t)n_bins, s));
-  k_small_init<<<1, 32, 0, s>>>(small);  // [1], [3] = -1 (none), rest 0
+  ow_launch(k_small_init, 1, 32, 0, s, small);  // [1], [3] = -1 (none), rest 0
   OW_LAUNCHED(ctx);
   void* pmid;
   OW_TRY(ow_slot(ctx, SLOT_BIN_MID, 4 * (size_t)n, s, &pmid));
-  k_count_fast<D><<<ow_blocks(n, 256), 256, 0, s>>>(g, c, n, (unsigned long long*)pm, (int32_t*)pnb, counts,
+  ow_launch(k_count_fast<D>, ow_blocks(n, 256), 256, 0, s, g, c, n, (unsigned long long*)pm, (int32_t*)pnb, counts,
                                                    (int32_t*)pmid, small);
-  k_count_walk<D><<<ow_blocks(n, 256, 8 * OW_SMS), 256, 0, s>>>(g, c, n, h, (const int32_t*)pmid,
+  ow_launch(k_count_walk<D>, ow_blocks(n, 256, 8 * OW_SMS), 256, 0, s, g, c, n, h, (const int32_t*)pmid,
                                                                 (unsigned long long*)pm, (int32_t*)pnb, counts,
                                                                 (int32_t*)psl, small);
   ctx->launches += 2;
@@ -443,7 +449,7 @@ int fill_count(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, 
     OW_TRY(ow_readback(ctx, small + 4, 1, hs, s));
     void* pb;
     OW_TRY(ow_slot(ctx, SLOT_BIN_BITMAP, 4 * (size_t)(hs[0] + 1), s, &pb));
-    k_count_slow<D><<<(unsigned)n_slow, 256, 0, s>>>(g, c, n, h, (const int32_t*)psl, (const int64_t*)po,
+    ow_launch(k_count_slow<D>, (unsigned)n_slow, 256, 0, s, g, c, n, h, (const int32_t*)psl, (const int64_t*)po,
                                                      (unsigned*)pb, (int32_t*)pnb, counts, small);
     OW_LAUNCHED(ctx);
     OW_CHECK_LAUNCH();
@@ -470,11 +476,11 @@ int fill_emit(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, int32_t* i
   OW_TRY(ow_slot(ctx, SLOT_PAIR_KEY1, 4 * (size_t)E, s, &pk1));
   OW_TRY(ow_slot(ctx, SLOT_PAIR_VAL1, 4 * (size_t)E, s, &pv1));
   const int32_t* foff = (const int32_t*)ctx->slot_ptr[SLOT_BIN_FOFF];
-  k_emit_fast<D><<<ow_blocks(n, 256), 256, 0, s>>>(g, c, n, (const unsigned long long*)ctx->slot_ptr[SLOT_BIN_MASK],
+  ow_launch(k_emit_fast<D>, ow_blocks(n, 256), 256, 0, s, g, c, n, (const unsigned long long*)ctx->slot_ptr[SLOT_BIN_MASK],
                                                   foff, (uint32_t*)pk0, (int32_t*)pv0);
   OW_LAUNCHED(ctx);
   if (ctx->bins_slow > 0) {
-    k_emit_slow<D><<<(unsigned)ctx->bins_slow, 32, 0, s>>>(
+    ow_launch(k_emit_slow<D>, (unsigned)ctx->bins_slow, 32, 0, s, 
         g, c, n, (const int32_t*)ctx->slot_ptr[SLOT_BIN_SLOW], (const int64_t*)ctx->slot_ptr[SLOT_BIN_SLOWOFF],
         (const unsigned*)ctx->slot_ptr[SLOT_BIN_BITMAP], foff, (uint32_t*)pk0, (int32_t*)pv0);
     OW_LAUNCHED(ctx);

@@ -1,4 +1,5 @@
 // Context, error state, scratch slots and readback for libowb200.
+#include <stdlib.h>
 #include <stdarg.h>
 #include <string.h>
 
@@ -128,4 +129,12 @@ int ow_readback(ow_ctx* ctx, const int64_t* d_src, int n, int64_t* h_dst, cudaSt
   OW_CUDA(cudaStreamSynchronize(s));
   memcpy(h_dst, ctx->h_pinned, n * sizeof(int64_t));
   return OW_OK;
+}
+
+bool ow_pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("OW_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }

@@ -17,6 +17,7 @@ using ow::scan;
 using ow::scan01;
 
 __global__ void k_cell_centers(ForestC F, const int32_t* __restrict__ ids, int64_t n, float* out) {
+  ow_pdl_wait();
   const int C = F.dim == 2 ? 16 : 64;
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n * C) return;
@@ -34,6 +35,7 @@ __global__ void k_cell_centers(ForestC F, const int32_t* __restrict__ ids, int64
 }
 
 __global__ void k_level_counts(ForestC F, int max_levels, unsigned long long* blocks, unsigned long long* leaves) {
+  ow_pdl_wait();
   __shared__ unsigned long long sb[64], sl[64];
   for (int i = threadIdx.x; i < 64; i += blockDim.x) sb[i] = sl[i] = 0;
   __syncthreads();
@@ -99,6 +101,7 @@ struct FlagLoad {
 // Split list[0..m) (ascending ids): children ids base + 2^D * r + ci with
 // coords 2c + bits(ci); parent mark reset (forest.py:300-329).
 __global__ void k_split(ow_forest f, const int32_t* __restrict__ list, int64_t m, int64_t base) {
+  ow_pdl_wait();
   const int nc = 1 << f.dim;
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= m * nc) return;
@@ -120,6 +123,7 @@ __global__ void k_split(ow_forest f, const int32_t* __restrict__ list, int64_t m
 // 2:1 violators among the face-adjacent leaves of frontier blocks
 // [f0, f1): a coarser leaf more than one level above (forest.py:351-370).
 __global__ void k_violators(ForestC F, int64_t f0, int64_t f1, uint8_t* flag) {
+  ow_pdl_wait();
   const int sides = 2 * F.dim;
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (f1 - f0) * sides) return;
@@ -158,6 +162,7 @@ __device__ bool side_has_marked(const ForestC& F, int L, const int32_t* nc, int 
 }
 
 __global__ void k_prop_gather(ForestC F, const int32_t* __restrict__ leaves, int64_t n) {
+  ow_pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int id = leaves[i];
@@ -175,6 +180,7 @@ __global__ void k_prop_gather(ForestC F, const int32_t* __restrict__ leaves, int
 }
 
 __global__ void k_prop_promote(int8_t* marks, const int32_t* __restrict__ leaves, int64_t n) {
+  ow_pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int id = leaves[i];
@@ -198,7 +204,7 @@ int split_list(ow_ctx* ctx, ow_forest* f, const int32_t* list, int64_t m, cudaSt
       return OW_ERR_INTERNAL;
     }
   }
-  k_split<<<ow_blocks(m * nc, 256), 256, 0, s>>>(*f, list, m, f->n_blocks);
+  ow_launch(k_split, ow_blocks(m * nc, 256), 256, 0, s, *f, list, m, f->n_blocks);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   f->n_blocks = need;
@@ -221,7 +227,7 @@ extern "C" int ow_forest_level_counts(ow_ctx* ctx, const ow_forest* f, int64_t* 
   if (max_levels > 28) max_levels = 28;
   OW_CUDA(cudaMemsetAsync(ctx->d_small, 0, 64 * 8, s));
   ForestC F = make_forestc(f);
-  k_level_counts<<<ow_blocks(F.n, 256, 2 * OW_SMS), 256, 0, s>>>(F, max_levels, (unsigned long long*)ctx->d_small,
+  ow_launch(k_level_counts, ow_blocks(F.n, 256, 2 * OW_SMS), 256, 0, s, F, max_levels, (unsigned long long*)ctx->d_small,
                                                                  (unsigned long long*)ctx->d_small + 32);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
@@ -247,7 +253,7 @@ extern "C" int ow_forest_cell_centers(ow_ctx* ctx, const ow_forest* f, const int
   cudaStream_t s = (cudaStream_t)stream;
   if (n <= 0) return OW_OK;
   const int C = f->dim == 2 ? 16 : 64;
-  k_cell_centers<<<ow_blocks(n * C, 256), 256, 0, s>>>(make_forestc(f), d_ids, n, d_out);
+  ow_launch(k_cell_centers, ow_blocks(n * C, 256), 256, 0, s, make_forestc(f), d_ids, n, d_out);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;
@@ -260,8 +266,8 @@ extern "C" int ow_propagate_marks(ow_ctx* ctx, const ow_forest* f, const int32_t
   ForestC F = make_forestc(f);
   OW_PROF_BEGIN(ctx, PROF_PROP, s);
   for (int r = 0; r < rounds; ++r) {
-    k_prop_gather<<<ow_blocks(n_leaves, 128), 128, 0, s>>>(F, d_leaves, n_leaves);
-    k_prop_promote<<<ow_blocks(n_leaves, 256), 256, 0, s>>>(F.marks, d_leaves, n_leaves);
+    ow_launch(k_prop_gather, ow_blocks(n_leaves, 128), 128, 0, s, F, d_leaves, n_leaves);
+    ow_launch(k_prop_promote, ow_blocks(n_leaves, 256), 256, 0, s, F.marks, d_leaves, n_leaves);
     ctx->launches += 2;
   }
   OW_PROF_END(ctx, PROF_PROP, s);
@@ -314,7 +320,7 @@ static int refine_marked_impl(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t*
     OW_TRY(ow_slot(ctx, SLOT_FOREST_FLAG, (size_t)f->capacity, s, &pf));
     OW_CUDA(cudaMemsetAsync(pf, 0, (size_t)f1, s));
     ForestC F = make_forestc(f);
-    k_violators<<<ow_blocks((f1 - f0) * 2 * f->dim, 256), 256, 0, s>>>(F, f0, f1, (uint8_t*)pf);
+    ow_launch(k_violators, ow_blocks((f1 - f0) * 2 * f->dim, 256), 256, 0, s, F, f0, f1, (uint8_t*)pf);
     OW_LAUNCHED(ctx);
     OW_CHECK_LAUNCH();
     OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(f1 + 1), s, &pl));
@@ -344,6 +350,7 @@ namespace {
 // (layout constants RS_* in ow_common.cuh)
 
 __global__ void k_rs_init(int64_t* st, int64_t n, const int64_t* nd) {
+  ow_pdl_wait();
   if (nd) n = *nd;
   for (int i = threadIdx.x; i < RS_WORDS; i += blockDim.x) st[i] = 0;
   __syncthreads();
@@ -359,6 +366,7 @@ __global__ void k_rs_init(int64_t* st, int64_t n, const int64_t* nd) {
 // recorded; the MARKED list (k = 0) is not split beyond max_level.
 __global__ void k_split_ring(ow_forest f, const int32_t* __restrict__ list, int64_t* st, int k, int beyond_max,
                              int64_t* nb_out) {
+  ow_pdl_wait();
   const int nc = 1 << f.dim;
   const int64_t base = st[RS_NR + k];
   int64_t m = st[RS_CR + k];
@@ -400,6 +408,7 @@ __global__ void k_split_ring(ow_forest f, const int32_t* __restrict__ list, int6
 
 // 2:1 violators around the frontier [n[k-1], n[k]) read on the device (grid-stride)
 __global__ void k_violators_dev(ForestC F, const int64_t* st, int k, uint8_t* flag) {
+  ow_pdl_wait();
   const int sides = 2 * F.dim;
   const int64_t f0 = st[RS_NR + k - 1], f1 = st[RS_NR + k];
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (f1 - f0) * sides;
@@ -428,6 +437,7 @@ struct FlagCompactClear {  // compaction that also clears the flags it consumed
 };
 
 __global__ void k_prop_gather_dev(ForestC F, const int32_t* __restrict__ leaves, const int64_t* n) {
+  ow_pdl_wait();
   const int64_t nn = *n;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
     const int id = leaves[i];
@@ -446,6 +456,7 @@ __global__ void k_prop_gather_dev(ForestC F, const int32_t* __restrict__ leaves,
 }
 
 __global__ void k_prop_promote_dev(int8_t* marks, const int32_t* __restrict__ leaves, const int64_t* n) {
+  ow_pdl_wait();
   const int64_t nn = *n;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
     const int id = leaves[i];
@@ -471,8 +482,8 @@ int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, c
   ForestC F = make_forestc(f);
   OW_PROF_BEGIN(ctx, PROF_PROP, s);
   for (int r = 0; r < rounds; ++r) {
-    k_prop_gather_dev<<<ow_blocks(n_bound, 128, 16 * OW_SMS), 128, 0, s>>>(F, d_leaves, d_n);
-    k_prop_promote_dev<<<ow_blocks(n_bound, 256, 8 * OW_SMS), 256, 0, s>>>(F.marks, d_leaves, d_n);
+    ow_launch(k_prop_gather_dev, ow_blocks(n_bound, 128, 16 * OW_SMS), 128, 0, s, F, d_leaves, d_n);
+    ow_launch(k_prop_promote_dev, ow_blocks(n_bound, 256, 8 * OW_SMS), 256, 0, s, F.marks, d_leaves, d_n);
     ctx->launches += 2;
   }
   OW_PROF_END(ctx, PROF_PROP, s);
@@ -500,23 +511,23 @@ int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64
   OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(cap + 1), s, &pl));
   OW_TRY(ow_slot(ctx, SLOT_FOREST_FLAG, (size_t)cap + 8, s, &pf));
   OW_PROF_BEGIN(ctx, PROF_REFINE, s);
-  k_rs_init<<<1, 64, 0, s>>>(d_st, n, d_nb);
+  ow_launch(k_rs_init, 1, 64, 0, s, d_st, n, d_nb);
   OW_CUDA(cudaMemsetAsync(pf, 0, (size_t)cap, s));
   OW_TRY(scan01(ctx, SplitLoad{make_forestc(f), level, d_st + RS_INTER}, CompactStore{(int32_t*)pl},
                 d_nb ? cap : n, d_st + RS_CR, s, d_nb));
   const ow_forest fv = *f;
   const int sg = ow_blocks(cap * nc, 256, 8 * OW_SMS);
-  k_split_ring<<<sg, 256, 0, s>>>(fv, (const int32_t*)pl, d_st, 0, level >= f->max_level,
+  ow_launch(k_split_ring, sg, 256, 0, s, fv, (const int32_t*)pl, d_st, 0, level >= f->max_level,
                                    iters == 0 ? d_nb : nullptr);
   ctx->launches += 2;
   ForestC F = make_forestc(f);
   F.n = cap;
   for (int k = 1; k <= iters; ++k) {
-    k_violators_dev<<<ow_blocks(cap * 2 * f->dim, 256, 8 * OW_SMS), 256, 0, s>>>(F, d_st, k, (uint8_t*)pf);
+    ow_launch(k_violators_dev, ow_blocks(cap * 2 * f->dim, 256, 8 * OW_SMS), 256, 0, s, F, d_st, k, (uint8_t*)pf);
     // violator flags of blocks [0, n[k]), n[k] on the device
     OW_TRY(scan01(ctx, FlagLoad{(const uint8_t*)pf}, FlagCompactClear{(int32_t*)pl, (uint8_t*)pf}, cap,
                   d_st + RS_CR + k, s, d_st + RS_NR + k));
-    k_split_ring<<<sg, 256, 0, s>>>(fv, (const int32_t*)pl, d_st, k, 0, k == iters ? d_nb : nullptr);
+    ow_launch(k_split_ring, sg, 256, 0, s, fv, (const int32_t*)pl, d_st, k, 0, k == iters ? d_nb : nullptr);
     ctx->launches += 2;
   }
   OW_PROF_END(ctx, PROF_REFINE, s);
@@ -535,7 +546,7 @@ int ow_rebalance_host(ow_ctx* ctx, ow_forest* f, int64_t f0, int64_t* n_split, c
     OW_TRY(ow_slot(ctx, SLOT_FOREST_FLAG, (size_t)f->capacity + 8, s, &pf));
     OW_CUDA(cudaMemsetAsync(pf, 0, (size_t)f1, s));
     ForestC F = make_forestc(f);
-    k_violators<<<ow_blocks((f1 - f0) * 2 * f->dim, 256), 256, 0, s>>>(F, f0, f1, (uint8_t*)pf);
+    ow_launch(k_violators, ow_blocks((f1 - f0) * 2 * f->dim, 256), 256, 0, s, F, f0, f1, (uint8_t*)pf);
     OW_LAUNCHED(ctx);
     OW_CHECK_LAUNCH();
     OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(f1 + 1), s, &pl));

@@ -12,6 +12,7 @@ constexpr int STL_TILE = 256;  // faces per CTA
 // shared memory with coalesced 16-bit loads, then emit 9 coalesced float planes.
 __global__ void __launch_bounds__(STL_TILE)
 k_stl_to_soa(const uint16_t* rec16, int64_t n, float* coords) {
+  ow_pdl_wait();
   __shared__ __align__(16) uint16_t s[STL_TILE * 25];
   const int64_t f0 = (int64_t)blockIdx.x * STL_TILE;
   const int64_t nf = min((int64_t)STL_TILE, n - f0);
@@ -38,6 +39,7 @@ k_stl_to_soa(const uint16_t* rec16, int64_t n, float* coords) {
 
 __global__ void k_index_to_coords(int dim, const float* __restrict__ verts, const int32_t* __restrict__ faces,
                                   int64_t n, float* coords) {
+  ow_pdl_wait();
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   for (int j = 0; j < dim; ++j) {
@@ -58,6 +60,7 @@ __device__ __forceinline__ void atomic_max_f(float* a, float v) {
 // small[0] first degenerate (u64 min), small[1] first non-finite (u64 min),
 // then floats: min[3], max[3], absmax at ((float*)(small+2))[0..6]
 __global__ void __launch_bounds__(256) k_face_check(int dim, const float* __restrict__ c, int64_t n, int64_t* small) {
+  ow_pdl_wait();
   float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY}, am = 0.0f;
   float ext_sum = 0.0f;  // sum of per-face largest bounding-box sides (a work-shape estimate)
   unsigned long long bad_deg = ~0ull, bad_fin = ~0ull;
@@ -152,6 +155,7 @@ __global__ void __launch_bounds__(256) k_face_check(int dim, const float* __rest
 }
 
 __global__ void k_face_check_init(int64_t* small) {
+  ow_pdl_wait();
   small[0] = -1;  // 0xfff.. as unsigned = "none"
   small[1] = -1;
   float* fs = (float*)(small + 2);
@@ -178,7 +182,7 @@ extern "C" int ow_stl_binary_to_soa(ow_ctx* ctx, const uint8_t* d_records, int64
   }
   if (n == 0) return OW_OK;
   OW_PROF_BEGIN(ctx, PROF_STL, s);
-  k_stl_to_soa<<<ow_blocks(n, STL_TILE), STL_TILE, 0, s>>>((const uint16_t*)d_records, n, d_coords);
+  ow_launch(k_stl_to_soa, ow_blocks(n, STL_TILE), STL_TILE, 0, s, (const uint16_t*)d_records, n, d_coords);
   OW_PROF_END(ctx, PROF_STL, s);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
@@ -193,7 +197,7 @@ extern "C" int ow_index_to_coords(ow_ctx* ctx, int32_t dim, const float* d_verti
     return OW_ERR_INVALID;
   }
   if (n == 0) return OW_OK;
-  k_index_to_coords<<<ow_blocks(n, 256), 256, 0, s>>>(dim, d_vertices, d_faces, n, d_coords);
+  ow_launch(k_index_to_coords, ow_blocks(n, 256), 256, 0, s, dim, d_vertices, d_faces, n, d_coords);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;
@@ -206,10 +210,10 @@ extern "C" int ow_face_check(ow_ctx* ctx, int32_t dim, const float* d_coords, in
     ow_set_error("dim must be 2 or 3, got %d", dim);
     return OW_ERR_INVALID;
   }
-  k_face_check_init<<<1, 1, 0, s>>>(ctx->d_small);
+  ow_launch(k_face_check_init, 1, 1, 0, s, ctx->d_small);
   OW_LAUNCHED(ctx);
   if (n > 0) {
-    k_face_check<<<ow_blocks(n, 256, 16 * OW_SMS), 256, 0, s>>>(dim, d_coords, n, ctx->d_small);
+    ow_launch(k_face_check, ow_blocks(n, 256, 16 * OW_SMS), 256, 0, s, dim, d_coords, n, ctx->d_small);
     OW_LAUNCHED(ctx);
   }
   OW_CHECK_LAUNCH();

@@ -99,6 +99,7 @@ struct LatArgs {
 template <int D>
 __global__ void k_lat_pos(ForestC F, int level, const int32_t* __restrict__ leaves, int64_t n, int32_t* pos_of,
                           uint8_t* has_pair, float* cen) {
+  ow_pdl_wait();
   double q[3];
 #pragma unroll
   for (int a = 0; a < D; ++a) q[a] = block_len(F, a, level);
@@ -334,6 +335,7 @@ __device__ __forceinline__ int flush_hits(const LatArgs& A, const uint2* hb, con
 
 template <int D, int FPW>
 __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
+  ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
   constexpr int FACES_PER_WARP = FPW, SLOT_LANES = 32 / FPW;
   __shared__ float4 s_face[4][FACES_PER_WARP][3];  // per warp: (v0, e1, e2) / (a, s) of its faces
@@ -589,6 +591,7 @@ struct BoffStore {
 // its first unit and walks forward.
 template <int D>
 __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
+  ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
   __shared__ int s_off[MT_TILE + 1];
   __shared__ int4 s_meta[MT_TILE + 1];    // pos, face, w, units
@@ -689,6 +692,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
 // boundary cells per candidate block (warp per block): count + cell mask
 template <int D>
 __global__ void k_lat_bcount(LatArgs A) {
+  ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -719,6 +723,7 @@ __global__ void k_lat_bcount(LatArgs A) {
 // linearly (coalesced) from the flags staged in shared memory.
 template <int D>
 __global__ void k_lat_emit(LatArgs A) {
+  ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
   __shared__ unsigned s_fl[C];
   const int64_t r = blockIdx.x;
@@ -745,6 +750,7 @@ __global__ void k_lat_emit(LatArgs A) {
 // Warp per MT tile over that tile's hit slots.
 template <int D>
 __global__ void k_lat_hits(LatArgs A) {
+  ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
   const unsigned long long ru = *A.ru_d;
   const int64_t U = (int64_t)(ru >> RU_ROW_BITS);
@@ -796,6 +802,7 @@ __global__ void k_lat_hits(LatArgs A) {
 // flag words it is the whole result (q = -1 where the bit is clear).
 template <int D>
 __global__ void k_lat_pack(LatArgs A) {
+  ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
   __shared__ int s_n[2];
   const int64_t r = blockIdx.x;
@@ -1026,27 +1033,27 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   OW_CUDA(cudaMemsetAsync(d_flags, 0, 4 * (size_t)n_leaves * C, s));
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
   LatArgs A = make_args(ctx);
-  if (D == 3) k_lat_pos<3><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
-  else k_lat_pos<2><<<ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s>>>(A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
+  if (D == 3) ow_launch(k_lat_pos<3>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
+  else ow_launch(k_lat_pos<2>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
   // the sweep: k_lat_faces (rows; small rows tested inline) + k_lat_mt (large rows)
   OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
   const int fpw = faces_per_warp(ctx, D, n_faces, nl);
   if (D == 3) {
-    if (fpw == 8) k_lat_faces<3, 8><<<lat_face_grid(n_faces, 8), 128, 0, s>>>(A);
-    else k_lat_faces<3, 4><<<lat_face_grid(n_faces, 4), 128, 0, s>>>(A);
+    if (fpw == 8) ow_launch(k_lat_faces<3, 8>, lat_face_grid(n_faces, 8), 128, 0, s, A);
+    else ow_launch(k_lat_faces<3, 4>, lat_face_grid(n_faces, 4), 128, 0, s, A);
   } else {
-    if (fpw == 8) k_lat_faces<2, 8><<<lat_face_grid(n_faces, 8), 128, 0, s>>>(A);
-    else k_lat_faces<2, 4><<<lat_face_grid(n_faces, 4), 128, 0, s>>>(A);
+    if (fpw == 8) ow_launch(k_lat_faces<2, 8>, lat_face_grid(n_faces, 8), 128, 0, s, A);
+    else ow_launch(k_lat_faces<2, 4>, lat_face_grid(n_faces, 4), 128, 0, s, A);
   }
   ctx->launches += 2;
   OW_CHECK_LAUNCH();
   OW_TRY(ow::scan01(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s));
   const int64_t tiles_max = ucap / MT_TILE + 1;
-  if (D == 3) k_lat_mt<3><<<ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s>>>(A);
-  else k_lat_mt<2><<<ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s>>>(A);
+  if (D == 3) ow_launch(k_lat_mt<3>, ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s, A);
+  else ow_launch(k_lat_mt<2>, ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s, A);
   OW_PROF_END(ctx, PROF_LAT_SWEEP, s);
-  if (D == 3) k_lat_bcount<3><<<ow_blocks(nl, 8), 256, 0, s>>>(A);
-  else k_lat_bcount<2><<<ow_blocks(nl, 8), 256, 0, s>>>(A);
+  if (D == 3) ow_launch(k_lat_bcount<3>, ow_blocks(nl, 8), 256, 0, s, A);
+  else ow_launch(k_lat_bcount<2>, ow_blocks(nl, 8), 256, 0, s, A);
   ctx->launches += 2;
   OW_CHECK_LAUNCH();
   OW_TRY(scan(ctx, BcountLoad{A.bcount, A.n_cb_d}, BoffStore{(int64_t*)A.boff, A.n_cb_d}, nl, ctx->d_small + 35, s));
@@ -1109,13 +1116,13 @@ extern "C" int ow_lattice_links_emit_packed(ow_ctx* ctx, int64_t* d_cells, float
     OW_TRY(scan(ctx, ow::LoadArr<int32_t>{A.hcount}, ow::StoreExcl<int64_t>{A.hoff}, ctx->lat_ncb,
                 ctx->d_small + 36, s));
   if (ctx->lat_forest.dim == 3) {
-    k_lat_emit<3><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
-    k_lat_hits<3><<<8 * OW_SMS, 256, 0, s>>>(A);
-    if (d_q_packed) k_lat_pack<3><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
+    ow_launch(k_lat_emit<3>, (unsigned)ctx->lat_ncb, C, 0, s, A);
+    ow_launch(k_lat_hits<3>, 8 * OW_SMS, 256, 0, s, A);
+    if (d_q_packed) ow_launch(k_lat_pack<3>, (unsigned)ctx->lat_ncb, C, 0, s, A);
   } else {
-    k_lat_emit<2><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
-    k_lat_hits<2><<<8 * OW_SMS, 256, 0, s>>>(A);
-    if (d_q_packed) k_lat_pack<2><<<(unsigned)ctx->lat_ncb, C, 0, s>>>(A);
+    ow_launch(k_lat_emit<2>, (unsigned)ctx->lat_ncb, C, 0, s, A);
+    ow_launch(k_lat_hits<2>, 8 * OW_SMS, 256, 0, s, A);
+    if (d_q_packed) ow_launch(k_lat_pack<2>, (unsigned)ctx->lat_ncb, C, 0, s, A);
   }
   OW_PROF_END(ctx, PROF_LATTICE, s);
   ctx->launches += d_q_packed ? 3 : 2;

@@ -31,6 +31,7 @@ constexpr int PREP_THREADS = 128;
 template <int D>
 __global__ void __launch_bounds__(PREP_THREADS) k_face_prep(const float* __restrict__ c, int64_t n, float d,
                                                             double reach, float4* box, float4* sph, float4* pay) {
+  ow_pdl_wait();
   constexpr int PW = D == 3 ? PAY3 : PAY2;
   __shared__ float4 s_pay[PREP_THREADS * PW];
   __shared__ float4 s_box[PREP_THREADS * 2];
@@ -83,10 +84,10 @@ int prepare_faces(ow_ctx* ctx, int dim, const float* c, int64_t n, int64_t key, 
   OW_TRY(ow_slot(ctx, SLOT_FACE_SPHERE, 16 * (size_t)n, s, &ps));
   OW_TRY(ow_slot(ctx, SLOT_FACE_PREP, need_pay, s, &pp));
   if (dim == 3)
-    k_face_prep<3><<<ow_blocks(n, PREP_THREADS), PREP_THREADS, 0, s>>>(c, n, d, reach, (float4*)pb, (float4*)ps,
+    ow_launch(k_face_prep<3>, ow_blocks(n, PREP_THREADS), PREP_THREADS, 0, s, c, n, d, reach, (float4*)pb, (float4*)ps,
                                                                         (float4*)pp);
   else
-    k_face_prep<2><<<ow_blocks(n, PREP_THREADS), PREP_THREADS, 0, s>>>(c, n, d, reach, (float4*)pb, (float4*)ps,
+    ow_launch(k_face_prep<2>, ow_blocks(n, PREP_THREADS), PREP_THREADS, 0, s, c, n, d, reach, (float4*)pb, (float4*)ps,
                                                                         (float4*)pp);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
@@ -150,6 +151,7 @@ struct MarkArgs {
 template <int D>
 __global__ void k_chunk_boxes(const int32_t* __restrict__ ids, int64_t n_entries, const float4* __restrict__ box,
                               float4* cbox) {
+  ow_pdl_wait();
   // warp per chunk: independent loads, min / max (exact, order-free) by shuffles
   const int lane = threadIdx.x & 31;
   const int64_t n_chunks = (n_entries + 31) / 32;
@@ -372,6 +374,7 @@ __device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M
 // persistent over the level's leaves (the count may live on the device)
 template <int D, bool BINNED>
 __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_blocks(MarkArgs A, MarkItems M) {
+  ow_pdl_wait();
   __shared__ MarkSmem<D> S;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t n = A.d_n ? *A.d_n : A.n_leaves;
@@ -482,6 +485,7 @@ __device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M
 
 template <int D, bool BINNED>
 __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_items(MarkArgs A, MarkItems M) {
+  ow_pdl_wait();
   constexpr int CPL = D == 3 ? 2 : 1;
   __shared__ MarkSmem<D> S;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -547,6 +551,7 @@ struct LinkArgs {
 
 template <int D, bool EMIT>
 __global__ void __launch_bounds__(MARK_THREADS) k_links(LinkArgs A) {
+  ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
   constexpr int PW = D == 3 ? PAY3 : PAY2;
   __shared__ float s_cen[C][D];
@@ -651,6 +656,7 @@ struct LinkedStore {
 
 __global__ void k_near_pairs(int dim, const float* __restrict__ pts, const float* __restrict__ faces,
                              const float* __restrict__ dd, int64_t n, uint8_t* out) {
+  ow_pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float4 pay[PAY3];
@@ -728,8 +734,8 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   OW_CUDA(cudaMemsetAsync(ph, 0, 4 * (size_t)(n_leaves + (n_leaves & 1)) + 8, s));
   if (!chunk_boxes_ready) {  // the driver reuses them while the bins and face boxes are unchanged
     const int cg = ow_blocks((n_entries + 31) / 32, 4, 16 * OW_SMS);
-    if (f->dim == 3) k_chunk_boxes<3><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
-    else k_chunk_boxes<2><<<cg, 128, 0, s>>>(d_bin_ids, n_entries, A.box, (float4*)pc);
+    if (f->dim == 3) ow_launch(k_chunk_boxes<3>, cg, 128, 0, s, d_bin_ids, n_entries, A.box, (float4*)pc);
+    else ow_launch(k_chunk_boxes<2>, cg, 128, 0, s, d_bin_ids, n_entries, A.box, (float4*)pc);
   }
   OW_PROF_BEGIN(ctx, PROF_MARK, s);
   // persistent past 4 waves (k_mark_blocks strides over the device leaf count)
@@ -738,19 +744,19 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   const int gi = 8 * OW_SMS;
   if (f->dim == 3) {
     if (binned) {
-      k_mark_blocks<3, true><<<grd, MARK_THREADS, 0, s>>>(A, M);
-      k_mark_items<3, true><<<gi, MARK_THREADS, 0, s>>>(A, M);
+      ow_launch(k_mark_blocks<3, true>, grd, MARK_THREADS, 0, s, A, M);
+      ow_launch(k_mark_items<3, true>, gi, MARK_THREADS, 0, s, A, M);
     } else {
-      k_mark_blocks<3, false><<<grd, MARK_THREADS, 0, s>>>(A, M);
-      k_mark_items<3, false><<<gi, MARK_THREADS, 0, s>>>(A, M);
+      ow_launch(k_mark_blocks<3, false>, grd, MARK_THREADS, 0, s, A, M);
+      ow_launch(k_mark_items<3, false>, gi, MARK_THREADS, 0, s, A, M);
     }
   } else {
     if (binned) {
-      k_mark_blocks<2, true><<<grd, MARK_THREADS, 0, s>>>(A, M);
-      k_mark_items<2, true><<<gi, MARK_THREADS, 0, s>>>(A, M);
+      ow_launch(k_mark_blocks<2, true>, grd, MARK_THREADS, 0, s, A, M);
+      ow_launch(k_mark_items<2, true>, gi, MARK_THREADS, 0, s, A, M);
     } else {
-      k_mark_blocks<2, false><<<grd, MARK_THREADS, 0, s>>>(A, M);
-      k_mark_items<2, false><<<gi, MARK_THREADS, 0, s>>>(A, M);
+      ow_launch(k_mark_blocks<2, false>, grd, MARK_THREADS, 0, s, A, M);
+      ow_launch(k_mark_items<2, false>, gi, MARK_THREADS, 0, s, A, M);
     }
   }
   ctx->launches += 3;
@@ -811,8 +817,8 @@ extern "C" int ow_cell_face_links_count(ow_ctx* ctx, const ow_forest* f, const i
   A.cell_cnt = (int32_t*)pc;
   A.over = over;
   if (n_leaves > 0) {
-    if (f->dim == 3) k_links<3, false><<<(unsigned)n_leaves, MARK_THREADS, 0, s>>>(A);
-    else k_links<2, false><<<(unsigned)n_leaves, MARK_THREADS, 0, s>>>(A);
+    if (f->dim == 3) ow_launch(k_links<3, false>, (unsigned)n_leaves, MARK_THREADS, 0, s, A);
+    else ow_launch(k_links<2, false>, (unsigned)n_leaves, MARK_THREADS, 0, s, A);
     OW_LAUNCHED(ctx);
     OW_CHECK_LAUNCH();
   }
@@ -884,8 +890,8 @@ extern "C" int ow_cell_face_links_emit(ow_ctx* ctx, int64_t* d_block_ids, int64_
   A.cell_off = off;
   A.face_ids = d_face_ids;
   if (ctx->link_leaves > 0) {
-    if (ctx->link_dim == 3) k_links<3, true><<<(unsigned)ctx->link_leaves, MARK_THREADS, 0, s>>>(A);
-    else k_links<2, true><<<(unsigned)ctx->link_leaves, MARK_THREADS, 0, s>>>(A);
+    if (ctx->link_dim == 3) ow_launch(k_links<3, true>, (unsigned)ctx->link_leaves, MARK_THREADS, 0, s, A);
+    else ow_launch(k_links<2, true>, (unsigned)ctx->link_leaves, MARK_THREADS, 0, s, A);
     OW_LAUNCHED(ctx);
     OW_CHECK_LAUNCH();
   }
@@ -901,7 +907,7 @@ extern "C" int ow_near_pairs(ow_ctx* ctx, int32_t dim, const float* d_points, co
     return OW_ERR_INVALID;
   }
   if (n <= 0) return OW_OK;
-  k_near_pairs<<<ow_blocks(n, 128), 128, 0, s>>>(dim, d_points, d_faces, d_d, n, d_out);
+  ow_launch(k_near_pairs, ow_blocks(n, 128), 128, 0, s, dim, d_points, d_faces, d_d, n, d_out);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;

@@ -16,6 +16,7 @@
 namespace {
 
 __global__ void k_root_init(ow_forest f, int64_t r) {
+  ow_pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= r) return;
   int64_t rem = i;
@@ -56,7 +57,8 @@ int64_t overflow_total(const int32_t* h_counts, int64_t n_bins, int64_t bin_frac
   return acc;
 }
 
-__global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
+__global__ void k_set_i64(int64_t* p, int64_t v) {
+  ow_pdl_wait(); *p = v; }
 
 // Device-resident level loop: per pass, the words the host needs from the
 // refine ring state and the marking stats, gathered for one readback.
@@ -64,6 +66,7 @@ constexpr int SUM_W = 13;  // [0..6) RS_INTER..RS_OVER_FIRST, [6] final blocks, 
 constexpr int DRV_RETRY = 1000;  // internal: rerun the pass with per-level host sync
 
 __global__ void k_drv_summary(const int64_t* drv, const unsigned long long* stats, int passes, int64_t* sum) {
+  ow_pdl_wait();
   for (int p = threadIdx.x; p < passes; p += blockDim.x) {
     const int64_t* rs = drv + 72 * p + 8;
     const int it = p + 2 < RS_MAX_ITERS ? p + 2 : RS_MAX_ITERS;
@@ -86,7 +89,7 @@ extern "C" int ow_forest_init_root(ow_ctx* ctx, ow_forest* f, void* stream) {
                  (long long)f->capacity);
     return OW_ERR_INVALID;
   }
-  k_root_init<<<ow_blocks(r, 256), 256, 0, s>>>(*f, r);
+  ow_launch(k_root_init, ow_blocks(r, 256), 256, 0, s, *f, r);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   f->n_blocks = r;
@@ -140,7 +143,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
   int64_t* d_nb = dev ? (int64_t*)drv + 72 * passes : nullptr;
   int64_t* d_sum = (int64_t*)drv + 72 * passes + 8;
   if (dev) {
-    k_set_i64<<<1, 1, 0, s>>>(d_nb, f->n_blocks);
+    ow_launch(k_set_i64, 1, 1, 0, s, d_nb, f->n_blocks);
     OW_LAUNCHED(ctx);
   }
   for (int level = 0; level < passes; ++level) {
@@ -272,7 +275,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
     void* pl;
     OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(f->capacity + 1), s, &pl));
     OW_TRY(ow_forest_leaves_dev(ctx, f, passes, (int32_t*)pl, d_sum + SUM_W * passes, s, d_nb));
-    k_drv_summary<<<1, 32, 0, s>>>((const int64_t*)drv, (const unsigned long long*)stats, passes, d_sum);
+    ow_launch(k_drv_summary, 1, 32, 0, s, (const int64_t*)drv, (const unsigned long long*)stats, passes, d_sum);
     OW_LAUNCHED(ctx);
     int64_t h[SUM_W * OW_MAX_PASSES + 1];
     OW_TRY(ow_readback(ctx, d_sum, SUM_W * passes + 1, h, s));
@@ -353,6 +356,7 @@ int out_buffer(const ow_g2g_params* p, int what, int64_t bytes, void** out) {
 }
 
 __global__ void k_widen(const int32_t* __restrict__ in, int64_t n, int64_t* out) {
+  ow_pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = in[i];
 }
@@ -450,7 +454,7 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
     return OW_ERR_INTERNAL;
   }
   if (nl > 0) {
-    k_widen<<<ow_blocks(nl, 256), 256, 0, s>>>((const int32_t*)pl, nl, (int64_t*)leaves64);
+    ow_launch(k_widen, ow_blocks(nl, 256), 256, 0, s, (const int32_t*)pl, nl, (int64_t*)leaves64);
     OW_LAUNCHED(ctx);
     OW_CHECK_LAUNCH();
   }

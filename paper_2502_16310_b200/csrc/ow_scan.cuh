@@ -92,6 +92,7 @@ template <class Load, class Store>
 __global__ void __launch_bounds__(SCAN_THREADS)
 k_scan(Load load, Store store, int64_t n, int64_t n_chunks, int64_t chunk, unsigned long long* status,
        int64_t* total_out, unsigned long long epoch) {
+  ow_pdl_wait();
   constexpr int W = SCAN_THREADS / 32;
   __shared__ int64_t s_warp[W];
   const int64_t tile = blockIdx.x;  // chunk index (CTAs dispatch in index order)
@@ -191,7 +192,7 @@ int scan(ow_ctx* ctx, Load load, Store store, int64_t n, int64_t* d_total, cudaS
   unsigned long long* status;
   unsigned long long epoch;
   OW_TRY(scan_status(ctx, n_chunks, s, &status, &epoch));
-  k_scan<<<(unsigned)n_chunks, SCAN_THREADS, 0, s>>>(load, store, n, n_chunks, chunk, status, d_total, epoch);
+  ow_launch(k_scan<Load, Store>, (unsigned)n_chunks, SCAN_THREADS, 0, s, load, store, n, n_chunks, chunk, status, d_total, epoch);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;
@@ -208,6 +209,7 @@ template <class Load, class Store>
 __global__ void __launch_bounds__(SCAN_THREADS, 6)
 k_scan01(Load load, Store store, int64_t n, const int64_t* d_n, unsigned long long* status, int64_t* total_out,
          unsigned long long epoch) {
+  ow_pdl_wait();
   constexpr int W = SCAN_THREADS / 32;
   static_assert(C01_ITEMS * W == 128, "warp 0 holds 4 counts per lane");
   __shared__ int s_cnt[C01_ITEMS * W];  // per (item k, warp) in element order -> exclusive ranks
@@ -277,7 +279,7 @@ int scan01(ow_ctx* ctx, Load load, Store store, int64_t n, int64_t* d_total, cud
   unsigned long long* status;
   unsigned long long epoch;
   OW_TRY(scan_status(ctx, tiles, s, &status, &epoch));
-  k_scan01<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(load, store, n, d_n, status, d_total, epoch);
+  ow_launch(k_scan01<Load, Store>, (unsigned)tiles, SCAN_THREADS, 0, s, load, store, n, d_n, status, d_total, epoch);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;
@@ -307,6 +309,7 @@ constexpr int RS_WARP_ITEMS = RS_TILE / RS_WARPS;  // 512 contiguous items per w
 template <int BITS>
 __global__ void __launch_bounds__(RS_THREADS)
 k_radix_hist(const uint32_t* keys, int64_t n, int shift, int64_t n_tiles, int32_t* hist) {
+  ow_pdl_wait();
   constexpr int DIG = 1 << BITS;
   __shared__ int h[DIG];
   for (int d = threadIdx.x; d < DIG; d += RS_THREADS) h[d] = 0;
@@ -325,6 +328,7 @@ template <int BITS>
 __global__ void __launch_bounds__(RS_THREADS)
 k_radix_scatter(const uint32_t* keys, const int32_t* vals, int64_t n, int shift, int64_t n_tiles,
                 const int32_t* hist_excl, uint32_t* keys_out, int32_t* vals_out) {
+  ow_pdl_wait();
   constexpr int DIG = 1 << BITS;
   __shared__ int cnt[RS_WARPS][DIG];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -375,11 +379,11 @@ k_radix_scatter(const uint32_t* keys, const int32_t* vals, int64_t n, int shift,
 template <int BITS>
 inline int radix_pass(ow_ctx* ctx, const uint32_t* ki, const int32_t* vi, uint32_t* ko, int32_t* vo, int64_t n,
                       int shift, int64_t tiles, int32_t* hist, cudaStream_t s) {
-  k_radix_hist<BITS><<<(unsigned)tiles, RS_THREADS, 0, s>>>(ki, n, shift, tiles, hist);
+  ow_launch(k_radix_hist<BITS>, (unsigned)tiles, RS_THREADS, 0, s, ki, n, shift, tiles, hist);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   OW_TRY(scan(ctx, LoadArr<int32_t>{hist}, StoreExcl<int32_t>{hist}, (int64_t)(1 << BITS) * tiles, nullptr, s));
-  k_radix_scatter<BITS><<<(unsigned)tiles, RS_THREADS, 0, s>>>(ki, vi, n, shift, tiles, hist, ko, vo);
+  ow_launch(k_radix_scatter<BITS>, (unsigned)tiles, RS_THREADS, 0, s, ki, vi, n, shift, tiles, hist, ko, vo);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;

@@ -62,6 +62,7 @@ __device__ double seg_dist_sq(const double* p, const double* a, const double* b)
 
 __global__ void k_referee(int dim, const float* __restrict__ pts, const float* __restrict__ faces,
                           const double* __restrict__ dd, int64_t n, double* exact, uint8_t* mask) {
+  ow_pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float4 pay[PAY3];
@@ -95,7 +96,7 @@ extern "C" int ow_referee_pairs(ow_ctx* ctx, int32_t dim, const float* d_points,
     return OW_ERR_INVALID;
   }
   if (n <= 0) return OW_OK;
-  k_referee<<<ow_blocks(n, 128), 128, 0, s>>>(dim, d_points, d_faces, d_d, n, d_exact, d_mask);
+  ow_launch(k_referee, ow_blocks(n, 128), 128, 0, s, dim, d_points, d_faces, d_d, n, d_exact, d_mask);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;
