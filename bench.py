@@ -221,6 +221,7 @@ def gpu_arm(args, cfg, rank, world, local_rank):
                for _ in range(args.steps)]
         h2d = d2h = 0
         pinned = []
+        slow_path = []  # steps that reran the level loop or copied results from Python
         barrier()
         for k in range(-1, args.steps):  # k = -1: untimed, sizes the pinned result buffers
             l2_flush()
@@ -249,6 +250,8 @@ def gpu_arm(args, cfg, rank, world, local_rank):
                 gp = plan.run(rd, n_faces, host=True)
                 res, forest, ll = gp.result, gp.forest, gp.links
                 hres = gp.host
+                if k >= 0 and (gp.reran or gp.host_copied & 5 != 5):
+                    slow_path.append(k)
                 d2h = sum(t.numel() * t.element_size() for k2, t in hres.items() if k2 != "coords")
                 d2h += sum(t.numel() * t.element_size() for t in hres["coords"])
             torch.cuda.current_stream().synchronize()
@@ -260,12 +263,16 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         if world > 1:
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
         ms2 = float(t2.item()) / args.steps
+        per = sorted(a.elapsed_time(b) for a, b in ev2)
         e2e = {"value": T_step / (ms2 / 1e3), "unit": "cell-face tests/s", "ms_per_step": ms2,
+               "ms_step_median": per[len(per) // 2], "ms_step_max": per[-1],
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "result": ("forest arrays (level, coords, parent, first_child, marks) + boundary cells and q"
                           if text else
                           "forest arrays (level, coords, parent, first_child, marks) + boundary rows packed: cell "
                           "ids, flag words and the q of the set bits (GridPass.host_q() expands to the dense rows)")}
+        if not text:
+            e2e["slow_path_steps"] = slow_path
 
     gc.enable()
 

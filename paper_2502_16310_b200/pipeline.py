@@ -43,6 +43,7 @@ class GridPass:
     links: LatticeLinks | None
     host: dict | None = None  # pinned host copies of the results (run(host=True))
     reran: bool = False  # the device-resident level loop outgrew the capacity; rerun with host sync
+    host_copied: int = 0  # native host copies made (bit 0 forest, bit 2 packed rows); else Python copied
 
     def host_q(self) -> np.ndarray:
         """Dense (boundary rows, Q) float32 q from the packed host copy (-1 where
@@ -235,7 +236,7 @@ class GridPlan:
         hres = None
         if host:
             hres = self._host_results(hbuf, int(out.host_copied), forest, links, int(out.n_links))
-        return GridPass(geom, forest, result, links, hres, bool(out.reran))
+        return GridPass(geom, forest, result, links, hres, bool(out.reran), int(out.host_copied))
 
     def _host_results(self, hbuf, copied, forest, links, n_links):
         """Pinned host copies (the C side streamed whatever fit; the rest is
