@@ -225,8 +225,10 @@ __device__ __forceinline__ bool quot_nonneg(float a, float det) {
 }
 
 // x / ext for 0 <= x < 64, ext in 1..4 (multiply-shift, exact in that range)
+// (multipliers 256, 128, 86, 64 as packed bytes minus one: one shift and mask
+// instead of a compare / select chain)
 __device__ __forceinline__ int div_small(int x, int ext) {
-  const int m = ext == 1 ? 256 : ext == 2 ? 128 : ext == 3 ? 86 : 64;
+  const int m = (int)((0x3F557FFFu >> (8 * (ext - 1))) & 0xFFu) + 1;
   return (x * m) >> 8;
 }
 
@@ -287,10 +289,15 @@ __device__ __forceinline__ int row_cell(unsigned w, int rem, const float* cen_po
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     const unsigned ra = (w >> (5 + 4 * a)) & 0xFu;
-    const int ext = (int)(ra >> 2) + 1;
-    const int qd = div_small(rem, ext);
-    const int i = (int)(ra & 3u) + (rem - qd * ext);
-    rem = qd;
+    int i;
+    if (a + 1 < D) {
+      const int ext = (int)(ra >> 2) + 1;
+      const int qd = div_small(rem, ext);
+      i = (int)(ra & 3u) + (rem - qd * ext);
+      rem = qd;
+    } else {
+      i = (int)(ra & 3u) + rem;  // the last axis takes the quotient as is (rem < ext)
+    }
     cell |= i << (2 * a);
     x[a] = __ldg(cen_pos + a * 4 + i);
   }
@@ -386,10 +393,12 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
     } else {
       r0 = make_float4(v[0][0], v[0][1], FSUB(v[1][0], v[0][0]), FSUB(v[1][1], v[0][1]));
     }
-    A.rec[3 * f + 0] = r0;
-    if (D == 3) {
-      A.rec[3 * f + 1] = r1;
-      A.rec[3 * f + 2] = r2;
+    if (A.inline_units < C) {  // records for k_lat_mt (no large rows when every row is inline)
+      A.rec[3 * f + 0] = r0;
+      if (D == 3) {
+        A.rec[3 * f + 1] = r1;
+        A.rec[3 * f + 2] = r2;
+      }
     }
     float4* sf = s_face[wid][lane / SLOT_LANES];
     sf[0] = r0;
@@ -410,7 +419,7 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
     if (a1 > nmax) a1 = nmax;
     k0[a] = (int)a0;
     ext[a] = a1 >= a0 ? (int)(a1 - a0 + 1) : 0;
-    rext[a] = ext[a] ? __frcp_rn((float)ext[a]) : 0.0f;
+    if (a + 1 < D) rext[a] = ext[a] ? __frcp_rn((float)ext[a]) : 0.0f;  // (unused for the last axis)
     nslots *= ext[a];
   }
   const int max_slots = __reduce_max_sync(0xffffffffu, nslots);
@@ -423,6 +432,10 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
       int rem = slot;
 #pragma unroll
       for (int a = 0; a < D; ++a) {  // rem / ext by a float reciprocal, corrected to exact
+        if (a + 1 == D) {  // last axis: rem < ext
+          nc[a] = k0[a] + rem;
+          break;
+        }
         int qd = (int)(__fmul_rz((float)rem, rext[a]));
         int rr = rem - qd * ext[a];
         while (rr < 0) rr += ext[a], --qd;
