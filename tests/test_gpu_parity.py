@@ -729,3 +729,42 @@ def test_ascii_stl_native_fast_path(ow, tmp_path):
             geometry._parse_ascii(bad, "f.stl")
         with pytest.raises(ow.GeometryParseError, match=msg):
             geometry._parse_ascii_py(bad, "f.stl")
+
+
+_PDL_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[2])
+import paper_2502_16310_b200 as ow
+from paper_2502_16310_b200 import pipeline, shapes
+data = shapes.binary_stl_bytes(shapes.icosphere_triangles(4))
+n = int.from_bytes(data[80:84], "little")
+rec = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda()
+plan = pipeline.GridPlan(ow.Aabb(np.zeros(3), np.ones(3)), (8, 8, 8),
+                         ow.NearWallParams(d_spec=0.05, n_levels=3, bins_per_axis=8), "D3Q19")
+gp = plan.run(rec, n)
+f, ll = gp.forest, gp.links
+np.savez(sys.argv[1], level=f._level, coords=f._coords, parent=f._parent, marks=f.marks.cpu().numpy(),
+         flags=ll.flags.cpu().numpy(), cells=ll.cells.cpu().numpy(), q=ll.q.cpu().numpy())
+"""
+
+
+def test_pdl_off_matches_pdl_on(ow, tmp_path):
+    """Every kernel is launched with programmatic dependent launch (kernels
+    wait on griddepcontrol.wait before touching memory); the same fused pass
+    launched without it (OW_PDL=0, fresh process) is identical array for array."""
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for pdl in ("1", "0"):
+        path = str(tmp_path / f"pdl{pdl}.npz")
+        env = dict(os.environ, OW_PDL=pdl)
+        r = subprocess.run([sys.executable, "-c", _PDL_SCRIPT, path, repo], env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[pdl] = np.load(path)
+    for k in out["1"].files:
+        np.testing.assert_array_equal(out["1"][k], out["0"][k], err_msg=k)
+    assert len(out["1"]["cells"]) > 0

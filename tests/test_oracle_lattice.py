@@ -97,3 +97,26 @@ def test_square_2d():
     # corner cell (0,0) centre (0.125, 0.125): diagonal (1,1) reaches (0.375, 0.375) through the corner region
     c0 = list(out["boundary"]).index(0)
     assert abs(out["q"][c0, 5] - F32(0.7)) < 1e-6
+
+
+def test_packed_rows_round_trip_the_oracle_output():
+    """The packed host form (flag word per boundary row + q of the set bits,
+    rows in order, directions ascending) that GridPlan.run(host=True)
+    transfers is lossless: pipeline.unpack_q restores the oracle's dense rows,
+    and the set bits are exactly the q >= 0 entries."""
+    from paper_2502_16310_b200.pipeline import unpack_q
+
+    f = of.Forest((0, 0, 0), (1, 1, 1), (2, 2, 2))
+    rng = np.random.default_rng(5)
+    v0 = rng.uniform(0.1, 0.9, (40, 3)).astype(F32)
+    tri = np.stack([v0, v0 + rng.uniform(-0.2, 0.2, (40, 3)).astype(F32),
+                    v0 + rng.uniform(-0.2, 0.2, (40, 3)).astype(F32)], 1)
+    coords = np.ascontiguousarray(np.transpose(tri, (1, 2, 0)))
+    out = ol.lattice_links(f, coords, "D3Q27")
+    q, cells = out["q"], out["boundary"]
+    assert len(cells) > 0
+    row_flags = out["flags"][cells].astype(np.uint32)
+    bits = ((row_flags[:, None] >> np.arange(27, dtype=np.uint32)) & 1).astype(bool)
+    np.testing.assert_array_equal(bits, q >= 0)
+    q_packed = q[bits]  # row-major: rows in order, directions ascending
+    np.testing.assert_array_equal(unpack_q(row_flags, q_packed, 27), q)
