@@ -227,9 +227,15 @@ def gpu_arm(args, cfg, rank, world, local_rank):
             l2_flush()
             if k >= 0:
                 ev2[k][0].record()
-            if text:
-                res, forest, ll = step(None)
+            if text or shard is not None:
+                # per-function path (text primitives; sharded ranks): STL records
+                # in from pinned memory, every result array out through torch copies
+                rd = None
                 h2d = 0
+                if not text:
+                    rd = rec_host.to(dev, non_blocking=True)
+                    h2d = rec_host.numel()
+                res, forest, ll = step(rd)
                 outs = [forest.level_tensor, forest.coords_tensor, forest._parent_t[: forest.n_blocks],
                         forest._first_child_t[: forest.n_blocks], forest.marks, ll.cells, ll.q]
                 d2h = 0
@@ -268,10 +274,10 @@ def gpu_arm(args, cfg, rank, world, local_rank):
                "ms_step_median": per[len(per) // 2], "ms_step_max": per[-1],
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "result": ("forest arrays (level, coords, parent, first_child, marks) + boundary cells and q"
-                          if text else
+                          if text or shard is not None else
                           "forest arrays (level, coords, parent, first_child, marks) + boundary rows packed: cell "
                           "ids, flag words and the q of the set bits (GridPass.host_q() expands to the dense rows)")}
-        if not text:
+        if not text and shard is None:
             e2e["slow_path_steps"] = slow_path
 
     gc.enable()
@@ -442,8 +448,15 @@ def main():
         import torch
         import torch.distributed as dist
 
+        # one rank per GPU over NCCL; OW_BENCH_BACKEND=gloo with more ranks than
+        # GPUs (ranks share devices) only exercises the N>1 code path on a small box
+        backend = os.environ.get("OW_BENCH_BACKEND", "nccl")
+        local_rank %= max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     from paper_2502_16310_b200 import _build
 
     if rank == 0:

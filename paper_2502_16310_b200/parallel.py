@@ -42,28 +42,37 @@ def partition(n, rank, world, weights=None):
     return int(idx[rank]), int(idx[rank + 1])
 
 
-def gather_slices(local, n, world, group=None):
+def gather_slices(local, n, world, group=None, sizes=None):
     """All-gather variable-length contiguous slices (padded to the largest);
-    returns the concatenation in rank order, length n.  NCCL gathers device
-    memory directly; under gloo (CPU tests, several ranks on one device) the
-    slices are staged through host memory."""
+    returns the concatenation in rank order, length n.  ``sizes`` (every
+    rank's slice length, when the caller knows them) skips the length
+    exchange; otherwise the lengths travel in one all-gather and one host
+    read.  NCCL gathers device memory directly; under gloo (CPU tests,
+    several ranks on one device) the slices are staged through host memory."""
     if local.is_cuda and dist.get_backend(group) == "gloo":
-        return gather_slices(local.cpu(), n, world, group).to(local.device)
-    per = 0 if n is None else ((n + world - 1) // world if world > 1 else n)
+        res, sizes = gather_slices(local.cpu(), n, world, group, sizes)
+        return res.to(local.device), sizes
     dev = local.device
-    counts = torch.tensor([local.numel()], dtype=torch.int64, device=dev)
-    all_counts = [torch.zeros_like(counts) for _ in range(world)]
-    dist.all_gather(all_counts, counts, group=group)
-    sizes = [int(c.item()) for c in all_counts]
-    m = max(max(sizes), per, 1)
-    buf = torch.zeros(m, dtype=local.dtype, device=dev)
-    buf[: local.numel()] = local
+    if sizes is None:
+        counts = torch.tensor([local.numel()], dtype=torch.int64, device=dev)
+        all_counts = torch.empty(world, dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(all_counts, counts, group=group)
+        sizes = all_counts.tolist()  # the one host read of the exchange
+    assert sizes[dist.get_rank(group) if world > 1 else 0] == local.numel()
+    m = max(max(sizes), 1)
+    if local.numel() == m:
+        buf = local.contiguous()
+    else:
+        buf = torch.zeros(m, dtype=local.dtype, device=dev)
+        buf[: local.numel()] = local
     out = torch.empty(world * m, dtype=local.dtype, device=dev)
     dist.all_gather_into_tensor(out, buf, group=group)
-    parts = [out[r * m: r * m + sizes[r]] for r in range(world)]
-    res = torch.cat(parts)
+    if all(sz == m for sz in sizes):
+        res = out
+    else:
+        res = torch.cat([out[r * m: r * m + sizes[r]] for r in range(world)])
     assert n is None or res.numel() == n, (res.numel(), n)
-    return res
+    return res, sizes
 
 
 class Shard:
@@ -79,10 +88,12 @@ class Shard:
         of leaves [lo, hi) and the slice's boundary rows (ascending, so the
         rank-order concatenation is the single-GPU order)."""
         nq = q.shape[1] if q.dim() == 2 else 0
-        allf = gather_slices(flags[lo * ncell: hi * ncell].contiguous(), n_leaves * ncell, self.world, self.group)
-        allc = gather_slices(cells, None, self.world, self.group)
-        allq = gather_slices(q.reshape(-1), None, self.world, self.group).view(-1, nq)
-        return allf, allc, allq
+        fsz = [(b - a) * ncell for a, b in (partition(n_leaves, r, self.world) for r in range(self.world))]
+        allf, _ = gather_slices(flags[lo * ncell: hi * ncell].contiguous(), n_leaves * ncell, self.world,
+                                self.group, sizes=fsz)
+        allc, csz = gather_slices(cells, None, self.world, self.group)  # one length exchange for both
+        allq, _ = gather_slices(q.reshape(-1), None, self.world, self.group, sizes=[c * nq for c in csz])
+        return allf, allc, allq.view(-1, nq)
 
     def exchange_callback(self, forest):
         """ow_exchange_fn for the native driver: all-gather the marks of the
@@ -94,7 +105,9 @@ class Shard:
                 leaves = _wrap_int32(ptr, n, forest.device)
                 idx = leaves.to(torch.int64)
                 mine = forest._marks.index_select(0, idx[lo:hi])
-                allm = gather_slices(mine, n, self.world, self.group)
+                per = (n + self.world - 1) // self.world  # the driver's slices (refine_driver)
+                msz = [max(0, min(n, per * (r + 1)) - min(n, per * r)) for r in range(self.world)]
+                allm, _ = gather_slices(mine, n, self.world, self.group, sizes=msz)
                 forest._marks.index_copy_(0, idx, allm)
                 sdev = "cpu" if dist.get_backend(self.group) == "gloo" else forest.device
                 tot = torch.tensor([stats3[0], stats3[1], stats3[2]], dtype=torch.int64, device=sdev)
@@ -119,7 +132,8 @@ class Shard:
         st = mark_fn(forest, level, geom, d_spec, bins, grid, leaves=leaves[lo:hi].contiguous())
         if self.world > 1:
             mine = forest.marks.index_select(0, leaves[lo:hi].to(torch.int64))
-            allm = gather_slices(mine, n, self.world, self.group)
+            msz = [b - a for a, b in (partition(n, r, self.world) for r in range(self.world))]
+            allm, _ = gather_slices(mine, n, self.world, self.group, sizes=msz)
             forest.marks.index_copy_(0, leaves.to(torch.int64), allm)
             tot = torch.tensor([st.marked, st.tests, st.evaluated], dtype=torch.int64, device=allm.device)
             dist.all_reduce(tot, group=self.group)

@@ -52,7 +52,7 @@ def _worker(rank, world, port, q):
             on.mark(sub, level, coords, 0.1, bins, grid)
             sub.first_child[others] = saved
             mine = torch.from_numpy(sub.marks[leaves[lo:hi]].copy())
-            allm = parallel.gather_slices(mine, len(leaves), world)
+            allm, _ = parallel.gather_slices(mine, len(leaves), world)
             f.marks[leaves] = allm.numpy()
             on.propagate(f, level, 0.1)
             f.refine_marked(level)
