@@ -223,7 +223,8 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         pinned = []
         slow_path = []  # steps that reran the level loop or copied results from Python
         barrier()
-        for k in range(-1, args.steps):  # k = -1: untimed, sizes the pinned result buffers
+        # k < 0: untimed warm-up (the first sizes the pinned result buffers)
+        for k in range(-max(args.warmup, 1), args.steps):
             l2_flush()
             if k >= 0:
                 ev2[k][0].record()
@@ -269,7 +270,9 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         if world > 1:
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
         ms2 = float(t2.item()) / args.steps
-        per = sorted(a.elapsed_time(b) for a, b in ev2)
+        per = [a.elapsed_time(b) for a, b in ev2]
+        log("e2e steps ms", " ".join(f"{x:.3f}" for x in per))
+        per = sorted(per)
         e2e = {"value": T_step / (ms2 / 1e3), "unit": "cell-face tests/s", "ms_per_step": ms2,
                "ms_step_median": per[len(per) // 2], "ms_step_max": per[-1],
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

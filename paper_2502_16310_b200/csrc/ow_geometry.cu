@@ -203,22 +203,8 @@ extern "C" int ow_index_to_coords(ow_ctx* ctx, int32_t dim, const float* d_verti
   return OW_OK;
 }
 
-extern "C" int ow_face_check(ow_ctx* ctx, int32_t dim, const float* d_coords, int64_t n,
-                             ow_face_summary* out, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
-  if (dim != 2 && dim != 3) {
-    ow_set_error("dim must be 2 or 3, got %d", dim);
-    return OW_ERR_INVALID;
-  }
-  ow_launch(k_face_check_init, 1, 1, 0, s, ctx->d_small);
-  OW_LAUNCHED(ctx);
-  if (n > 0) {
-    ow_launch(k_face_check, ow_blocks(n, 256, 16 * OW_SMS), 256, 0, s, dim, d_coords, n, ctx->d_small);
-    OW_LAUNCHED(ctx);
-  }
-  OW_CHECK_LAUNCH();
-  int64_t h[6];
-  OW_TRY(ow_readback(ctx, ctx->d_small, 6, h, s));
+// face summary words [0, 6) from a readback -> ow_face_summary
+void ow_face_summary_from(const int64_t* h, int64_t n, ow_face_summary* out) {
   out->first_degenerate = h[0];
   out->first_nonfinite = h[1];
   const float* fs = (const float*)(h + 2);
@@ -228,5 +214,30 @@ extern "C" int ow_face_check(ow_ctx* ctx, int32_t dim, const float* d_coords, in
   }
   out->abs_max = fs[6];
   out->mean_extent = n > 0 ? fs[7] / (float)n : 0.0f;
+}
+
+// launch the face check into d_small[dst, dst + 6) without reading it back
+int ow_face_check_launch(ow_ctx* ctx, int32_t dim, const float* d_coords, int64_t n, int64_t* dst, cudaStream_t s) {
+  if (dim != 2 && dim != 3) {
+    ow_set_error("dim must be 2 or 3, got %d", dim);
+    return OW_ERR_INVALID;
+  }
+  ow_launch(k_face_check_init, 1, 1, 0, s, dst);
+  OW_LAUNCHED(ctx);
+  if (n > 0) {
+    ow_launch(k_face_check, ow_blocks(n, 256, 16 * OW_SMS), 256, 0, s, dim, d_coords, n, dst);
+    OW_LAUNCHED(ctx);
+  }
+  OW_CHECK_LAUNCH();
+  return OW_OK;
+}
+
+extern "C" int ow_face_check(ow_ctx* ctx, int32_t dim, const float* d_coords, int64_t n,
+                             ow_face_summary* out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  OW_TRY(ow_face_check_launch(ctx, dim, d_coords, n, ctx->d_small, s));
+  int64_t h[6];
+  OW_TRY(ow_readback(ctx, ctx->d_small, 6, h, s));
+  ow_face_summary_from(h, n, out);
   return OW_OK;
 }

@@ -1062,8 +1062,12 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   OW_CHECK_LAUNCH();
   OW_TRY(ow::scan01(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s));
   const int64_t tiles_max = ucap / MT_TILE + 1;
-  if (D == 3) ow_launch(k_lat_mt<3>, ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s, A);
-  else ow_launch(k_lat_mt<2>, ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s, A);
+  if (!inline_all) {  // (every row inline: no k_lat_mt rows, and k_lat_hits sees zero units)
+    if (D == 3) ow_launch(k_lat_mt<3>, ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s, A);
+    else ow_launch(k_lat_mt<2>, ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s, A);
+  } else {
+    ctx->launches -= 1;
+  }
   OW_PROF_END(ctx, PROF_LAT_SWEEP, s);
   if (D == 3) ow_launch(k_lat_bcount<3>, ow_blocks(nl, 8), 256, 0, s, A);
   else ow_launch(k_lat_bcount<2>, ow_blocks(nl, 8), 256, 0, s, A);
