@@ -137,12 +137,16 @@ class Forest:
             return 1
 
     def _fill_view(self, v):
-        v.dim = self.dim
+        if not getattr(v, "_static_done", False):  # domain / root grid: once per (owned) struct
+            v.dim = self.dim
+            v.max_level = self.max_level
+            for a in range(3):
+                v.root[a] = self.root_dims[a] if a < self.dim else 1
+                v.dmin[a] = float(self.domain.min[a]) if a < self.dim else 0.0
+                v.dext[a] = float(self.domain.extent[a]) if a < self.dim else 1.0
+            v._static_done = True
         v.max_level = self.max_level
         for a in range(3):
-            v.root[a] = self.root_dims[a] if a < self.dim else 1
-            v.dmin[a] = float(self.domain.min[a]) if a < self.dim else 0.0
-            v.dext[a] = float(self.domain.extent[a]) if a < self.dim else 1.0
             v.d_coord[a] = self._coord[a].data_ptr() if a < self.dim else 0
         v.n_blocks = self._n
         v.capacity = self._cap

@@ -91,6 +91,9 @@ class GridPlan:
         self._est_links = 0
         self._outs = {}
         self._hbuf = None
+        self._coords = None
+        self._gp = None  # the call's parameter struct, reused while nothing static changes
+        self._gp_key = None
         self.reuse = bool(reuse_outputs)
         self._forest = None
         self._setup = None  # (n_faces, _driver_setup result): the parts that depend on n_faces only
@@ -143,7 +146,12 @@ class GridPlan:
         else:
             if dim != 3:
                 raise InvalidParameterError("binary STL records are 3D")
-            coords = torch.empty((3, 3, int(n_faces)), dtype=torch.float32, device=self.dev)
+            c = self._coords if self.reuse else None  # (reuse_outputs: one geometry buffer per plan)
+            if c is None or c.shape[2] != int(n_faces):
+                c = torch.empty((3, 3, int(n_faces)), dtype=torch.float32, device=self.dev)
+                if self.reuse:
+                    self._coords = c
+            coords = c
         nf = int(coords.shape[2])
         forest = self._forest
         if forest is not None and forest.capacity >= self.capacity:
@@ -159,20 +167,27 @@ class GridPlan:
         if not self.reuse and st["bins_t"] is not None:  # fresh bin buffers for this pass's result
             st = dict(st)
             st["bins_t"] = tuple(torch.empty_like(t) for t in st["bins_t"])
-        gp = _lib.G2GParamsC.from_buffer_copy(self._gp0)
-        gp.nw = st["p"]
+        if self.reuse and self._gp is not None and self._gp_key is st:
+            gp = self._gp  # steady state: same setup struct, output buffers checked below
+        else:
+            gp = _lib.G2GParamsC.from_buffer_copy(self._gp0)
+            gp.nw = st["p"]
+            if self.reuse:
+                self._gp, self._gp_key = gp, st
         if not self.reuse:
             self._outs = {}
         if self.dirs is not None:
             for what in range(4):  # tensors sized from the last pass: no callback in steady state
                 if self._est[what]:
-                    want = self._est[what] + self._est[what] // 8 + 64
                     t = self._outs.get(what)
                     if t is None or t.numel() * t.element_size() < self._est[what]:
-                        t = self._new_out(what, want)
+                        t = self._new_out(what, self._est[what] + self._est[what] // 8 + 64)
                     gp.out_buf[what] = t.data_ptr()
                     gp.out_cap[what] = t.numel() * t.element_size()
         hbuf = None
+        if not host and gp.host_level:  # a reused struct from a host=True pass: no host copies now
+            gp.host_level = gp.host_cells = gp.host_q = gp.host_row_flags = gp.host_q_packed = None
+            gp.host_block_cap = gp.host_row_cap = gp.host_link_cap = 0
         if host:
             # pinned host buffers owned by the plan and reused by every pass (a
             # pass's host results stay valid until the next host=True pass)
