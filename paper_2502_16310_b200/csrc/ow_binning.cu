@@ -15,6 +15,7 @@
 //   sort  : stable LSD radix sort by bin (8-bit digits) => ascending face per bin.
 //   scan  : offsets = exclusive scan of counts.
 #include "ow_scan.cuh"
+#include <string.h>
 
 namespace {
 
@@ -437,7 +438,18 @@ int fill_count(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, 
   // (rare: large faces) add a second pass and a re-scan
   OW_TRY(scan(ctx, ow::LoadArr<int32_t>{(const int32_t*)pnb}, ow::StoreExcl<int32_t>{(int32_t*)pfo}, n, small + 5, s));
   int64_t r[6];
-  OW_TRY(ow_readback(ctx, small, 6, r, s));
+  if (ctx->faces_pending) {
+    // fused pass: the face summary travels with this readback and is checked
+    // before anything depends on valid faces (the slow path sizes bitmaps by
+    // face extent); the count kernels above do bounded work on any input
+    int64_t hf[6];
+    OW_CUDA(cudaMemcpyAsync(ctx->h_pinned + 64, ctx->faces_pending, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    OW_TRY(ow_readback(ctx, small, 6, r, s));
+    memcpy(hf, ctx->h_pinned + 64, sizeof(hf));
+    OW_TRY(ow_faces_settle(ctx, hf, s));
+  } else {
+    OW_TRY(ow_readback(ctx, small, 6, r, s));
+  }
   int64_t n_slow = r[0];
   ctx->bins_slow = n_slow;
   if (n_slow > 0) {

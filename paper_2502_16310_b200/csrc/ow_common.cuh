@@ -150,6 +150,10 @@ struct ow_ctx {
   cudaStream_t copy_stream;       // side stream for result copies (lazily created)
   cudaEvent_t copy_ev[2];         // [0] forest final, [1] copies done
   bool defer_stage_times;
+  // fused pass: the face check's summary words on the device, not yet read
+  // (ow_faces_settle reads them with the next readback and validates)
+  const int64_t* faces_pending;
+  void* faces_state;  // the fused call's (result, forest, parameters) for ow_faces_settle
   int64_t drv_spec_nl;  // leaves of the deepest level compacted by the device-resident driver (-1: none)
 };
 
@@ -185,6 +189,12 @@ int ow_slot(ow_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out);
 
 // Copy n int64 device values to host and synchronise.
 int ow_readback(ow_ctx* ctx, const int64_t* d_src, int n, int64_t* h_dst, cudaStream_t s);
+// the pending face summary (ctx->faces_pending): validate it (errors of the
+// reference's import order) and derive the near-wall reach.  h6 = the words
+// if they were already read with another readback, else null (reads them).
+int ow_faces_settle(ow_ctx* ctx, const int64_t* h6, cudaStream_t s);
+void ow_face_summary_from(const int64_t* h, int64_t n, ow_face_summary* out);
+int ow_face_check_launch(ow_ctx* ctx, int32_t dim, const float* d_coords, int64_t n, int64_t* dst, cudaStream_t s);
 
 // bracket device work of kernel family `id` with events when profiling is on
 void ow_prof_mark(ow_ctx* ctx, int id, int end, cudaStream_t s);

@@ -181,6 +181,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
       out->bins_built += 1;
     }
     // ---- face_detection
+    if (ctx->faces_pending) OW_TRY(ow_faces_settle(ctx, nullptr, s));  // (naive strategy: no bin readback)
     OW_TRY(record(se, level, 1, s));
     const int64_t n_host = dev ? f->capacity : f->n_blocks;  // bound on this level's leaves
     void* pl;
@@ -362,20 +363,27 @@ __global__ void k_widen(const int32_t* __restrict__ in, int64_t n, int64_t* out)
 }
 }  // namespace
 
-extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces,
-                                   int64_t geom_key, ow_forest* f, const ow_grid* grid, const ow_g2g_params* p,
-                                   int32_t* d_bin_ids, int64_t bin_ids_capacity, int32_t* d_bin_counts,
-                                   int32_t* d_bin_offsets, ow_g2g_result* out, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
-  memset(out, 0, sizeof(*out));
-  out->faces.first_degenerate = out->faces.first_nonfinite = -1;
-  const int D = f->dim;
-  if (n_faces <= 0) {
-    ow_set_error("cannot refine around empty geometry");
-    return OW_ERR_INVALID;
+struct FacesState {
+  ow_g2g_result* out;
+  const ow_forest* f;
+  ow_nearwall_params* nw;
+  int64_t n_faces;
+};
+
+int ow_faces_settle(ow_ctx* ctx, const int64_t* h6, cudaStream_t s) {
+  if (!ctx->faces_pending) return OW_OK;
+  int64_t h[6];
+  if (h6) {
+    memcpy(h, h6, sizeof(h));
+  } else {
+    OW_TRY(ow_readback(ctx, ctx->faces_pending, 6, h, s));
   }
-  if (d_records) OW_TRY(ow_stl_binary_to_soa(ctx, d_records, n_faces, d_coords, stream));
-  OW_TRY(ow_face_check(ctx, D, d_coords, n_faces, &out->faces, stream));
+  ctx->faces_pending = nullptr;
+  FacesState* fs = (FacesState*)ctx->faces_state;
+  ow_g2g_result* out = fs->out;
+  const ow_forest* f = fs->f;
+  const int D = f->dim;
+  ow_face_summary_from(h, fs->n_faces, &out->faces);
   if (out->faces.first_nonfinite >= 0) {
     ow_set_error("geometry has non-finite coordinates");
     return OW_ERR_INVALID;
@@ -397,12 +405,42 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
     scale = fmax(scale, fmax(fabs(lo), fabs(hi)));
   }
   scale = fmax(scale, (double)out->faces.abs_max);
+  ow_nearwall_params* nw = fs->nw;
+  if (!(nw->reach > 0.0)) nw->reach = nw->d_spec64 + 1e-3 * fmax(1.0, fmax(scale, nw->d_spec64));  // nearwall.py:38-40
+  return OW_OK;
+}
+
+extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces,
+                                   int64_t geom_key, ow_forest* f, const ow_grid* grid, const ow_g2g_params* p,
+                                   int32_t* d_bin_ids, int64_t bin_ids_capacity, int32_t* d_bin_counts,
+                                   int32_t* d_bin_offsets, ow_g2g_result* out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  memset(out, 0, sizeof(*out));
+  out->faces.first_degenerate = out->faces.first_nonfinite = -1;
+  const int D = f->dim;
+  if (n_faces <= 0) {
+    ow_set_error("cannot refine around empty geometry");
+    return OW_ERR_INVALID;
+  }
+  if (d_records) OW_TRY(ow_stl_binary_to_soa(ctx, d_records, n_faces, d_coords, stream));
+  // the face check's summary is read with the first bin-count readback (one
+  // host round trip less) and validated there, before anything depends on it
+  OW_TRY(ow_face_check_launch(ctx, D, d_coords, n_faces, ctx->d_small + 56, s));
   OW_TRY(ow_forest_init_root(ctx, f, stream));
   ow_nearwall_params nw = p->nw;
-  if (!(nw.reach > 0.0)) nw.reach = nw.d_spec64 + 1e-3 * fmax(1.0, fmax(scale, nw.d_spec64));  // nearwall.py:38-40
+  FacesState fs_state{out, f, &nw, n_faces};
+  ctx->faces_state = &fs_state;
+  ctx->faces_pending = ctx->d_small + 56;
   ctx->defer_stage_times = true;  // read the stage events after the lattice work is queued
   int st = refine_driver(ctx, f, d_coords, n_faces, geom_key, grid, &nw, d_bin_ids, bin_ids_capacity, d_bin_counts,
                          d_bin_offsets, &out->nw, s, true);
+  if (st == OW_OK && ctx->faces_pending) st = ow_faces_settle(ctx, nullptr, s);  // (no pass read it)
+  ctx->faces_pending = nullptr;
+  ctx->faces_state = nullptr;
+  if (out->faces.first_nonfinite >= 0 || out->faces.first_degenerate >= 0 || out->outside_domain) {
+    ctx->defer_stage_times = false;
+    return OW_ERR_INVALID;  // (the message was set by ow_faces_settle)
+  }
   if (st == DRV_RETRY) {  // the forest outgrew its capacity (or a deep cascade): per-level host path
     out->reran = 1;
     OW_TRY(ow_forest_init_root(ctx, f, stream));

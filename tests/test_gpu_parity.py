@@ -550,6 +550,45 @@ def test_geometry_to_grid_errors(ow):
     out = tris + np.float32(0.9)
     with pytest.raises(ow.InvalidParameterError, match="outside the forest domain"):
         run(out)
+    # the face summary is read with the first bin-count readback: binning runs
+    # on these faces first and must stay bounded (inf / NaN / huge faces)
+    for val, msg in ((np.inf, "non-finite"), (np.nan, "non-finite")):
+        bad = tris.copy()
+        bad[7, 2, 1] = val
+        with pytest.raises(ow.InvalidParameterError, match=msg):
+            run(bad)
+    bad = tris.copy()
+    bad[7] *= np.float32(1e6)  # a valid but enormous face (its sample walk would be ~1e16 samples)
+    with pytest.raises(ow.InvalidParameterError, match="outside the forest domain"):
+        run(bad)
+    # degenerate beats outside (the reference validates faces first)
+    bad = tris + np.float32(0.9)
+    bad[3, 1] = bad[3, 0]
+    with pytest.raises(ow.InvalidParameterError, match="degenerate triangle .* at face 3"):
+        run(bad)
+    # the plan is usable after errors
+    f = run(tris).forest
+    assert f.n_blocks > 64
+
+
+def test_geometry_to_grid_naive_strategy(ow):
+    """Fused pass with the naive strategy (no bins, so the face summary is
+    settled before the first marking pass) equals the per-function path."""
+    import torch
+
+    from paper_2502_16310_b200 import pipeline, shapes
+
+    tris = shapes.icosphere_triangles(2).astype(np.float32)
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.06, n_levels=3, strategy="naive")
+    data = shapes.binary_stl_bytes(tris)
+    rec = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda()
+    gp = pipeline.geometry_to_grid(rec, len(tris), dom, (4, 4, 4), params, "D3Q19")
+    f2 = ow.init_root_grid(dom, (4, 4, 4))
+    res = ow.refine_near_wall(f2, gp.geometry, params)
+    np.testing.assert_array_equal(gp.forest._coords, f2._coords)
+    np.testing.assert_array_equal(gp.forest._level, f2._level)
+    assert gp.result.marked_detected == res.marked_detected
 
 
 def test_native_driver_capacity_fallbacks(ow):
