@@ -860,14 +860,22 @@ int faces_per_warp(const ow_ctx* ctx, int D, int64_t n_faces, int64_t n_leaves) 
   return n_faces > 4 * n_leaves ? 8 : 4;
 }
 
-// persistent face pass: resident CTAs only (9 per SM at 56 registers x 128
-// threads), fewer when the faces do not fill them
-unsigned lat_face_grid(int64_t n_faces, int fpw) {
+// persistent face pass: resident CTAs only (occupancy of the instantiation,
+// queried once: 10 per SM at 48 registers x 128 threads), fewer when the faces
+// do not fill them; OW_LAT_CTAS_PER_SM overrides (tuning)
+template <int D, int FPW>
+unsigned lat_face_grid(int64_t n_faces) {
   static const int per_sm = [] {
     const char* e = getenv("OW_LAT_CTAS_PER_SM");
-    return e && atoi(e) > 0 ? atoi(e) : 9;
+    if (e && atoi(e) > 0) return atoi(e);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_lat_faces<D, FPW>, 128, 0) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 8;
+    }
+    return n;
   }();
-  const int64_t need = (n_faces + 4 * fpw - 1) / (4 * fpw);
+  const int64_t need = (n_faces + 4 * FPW - 1) / (4 * FPW);
   const int64_t cap = (int64_t)per_sm * OW_SMS;
   return (unsigned)(need < cap ? need : cap);
 }
@@ -1052,11 +1060,11 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
   const int fpw = faces_per_warp(ctx, D, n_faces, nl);
   if (D == 3) {
-    if (fpw == 8) ow_launch(k_lat_faces<3, 8>, lat_face_grid(n_faces, 8), 128, 0, s, A);
-    else ow_launch(k_lat_faces<3, 4>, lat_face_grid(n_faces, 4), 128, 0, s, A);
+    if (fpw == 8) ow_launch(k_lat_faces<3, 8>, lat_face_grid<3, 8>(n_faces), 128, 0, s, A);
+    else ow_launch(k_lat_faces<3, 4>, lat_face_grid<3, 4>(n_faces), 128, 0, s, A);
   } else {
-    if (fpw == 8) ow_launch(k_lat_faces<2, 8>, lat_face_grid(n_faces, 8), 128, 0, s, A);
-    else ow_launch(k_lat_faces<2, 4>, lat_face_grid(n_faces, 4), 128, 0, s, A);
+    if (fpw == 8) ow_launch(k_lat_faces<2, 8>, lat_face_grid<2, 8>(n_faces), 128, 0, s, A);
+    else ow_launch(k_lat_faces<2, 4>, lat_face_grid<2, 4>(n_faces), 128, 0, s, A);
   }
   ctx->launches += 2;
   OW_CHECK_LAUNCH();
