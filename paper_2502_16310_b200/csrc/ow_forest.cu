@@ -407,10 +407,13 @@ __global__ void k_split_ring(ow_forest f, const int32_t* __restrict__ list, int6
 }
 
 // 2:1 violators around the frontier [n[k-1], n[k]) read on the device (grid-stride)
-__global__ void k_violators_dev(ForestC F, const int64_t* st, int k, uint8_t* flag) {
+// (scan_n: the length the following flag compaction scans, 0 when the
+// previous sweep split nothing — then no block can be flagged)
+__global__ void k_violators_dev(ForestC F, const int64_t* st, int k, uint8_t* flag, int64_t* scan_n) {
   ow_pdl_wait();
   const int sides = 2 * F.dim;
   const int64_t f0 = st[RS_NR + k - 1], f1 = st[RS_NR + k];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *scan_n = f1 > f0 ? f1 : 0;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (f1 - f0) * sides;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t id = f0 + t / sides;
@@ -523,10 +526,12 @@ int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64
   ForestC F = make_forestc(f);
   F.n = cap;
   for (int k = 1; k <= iters; ++k) {
-    ow_launch(k_violators_dev, ow_blocks(cap * 2 * f->dim, 256, 8 * OW_SMS), 256, 0, s, F, d_st, k, (uint8_t*)pf);
-    // violator flags of blocks [0, n[k]), n[k] on the device
+    int64_t* scan_n = ctx->d_small + 53;
+    ow_launch(k_violators_dev, ow_blocks(cap * 2 * f->dim, 256, 8 * OW_SMS), 256, 0, s, F, d_st, k, (uint8_t*)pf,
+              scan_n);
+    // violator flags of blocks [0, n[k]) (n[k] on the device; 0 after a sweep without splits)
     OW_TRY(scan01(ctx, FlagLoad{(const uint8_t*)pf}, FlagCompactClear{(int32_t*)pl, (uint8_t*)pf}, cap,
-                  d_st + RS_CR + k, s, d_st + RS_NR + k));
+                  d_st + RS_CR + k, s, scan_n));
     ow_launch(k_split_ring, sg, 256, 0, s, fv, (const int32_t*)pl, d_st, k, 0, k == iters ? d_nb : nullptr);
     ctx->launches += 2;
   }
