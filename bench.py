@@ -132,6 +132,7 @@ def gpu_arm(args, cfg, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    numa = _lib.bind_host_numa(local_rank)  # pinned staging buffers on the GPU's socket (no-op on one node)
     shard = parallel.Shard() if world > 1 else None
     data = make_input(cfg)
     dim = cfg["dim"]
@@ -350,6 +351,7 @@ def gpu_arm(args, cfg, rank, world, local_rank):
                                   f"all-gather of marks and of boundary links; bins/forest replicated"},
         "roofline": roofline,
         "gpu_launches": int(launches),
+        "host_numa_node": numa,
         "clocks": clk.summary(),
     }
     if e2e:

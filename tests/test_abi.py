@@ -113,3 +113,12 @@ def test_struct_layouts_match_header(tmp_path):
             C.sizeof(_lib.NearWallParamsC), C.sizeof(_lib.NearWallResultC), C.sizeof(_lib.G2GParamsC),
             C.sizeof(_lib.G2GResultC), _lib.G2GResultC.nw.offset]
     assert got == want
+
+
+def test_cpulist_parser():
+    """sysfs cpulist syntax used by bind_host_numa (pinned buffers on the GPU's node)."""
+    from paper_2502_16310_b200 import _lib
+
+    assert _lib._cpulist("0-3,8,10-11\n") == {0, 1, 2, 3, 8, 10, 11}
+    assert _lib._cpulist("5") == {5}
+    assert _lib._cpulist("") == set()
