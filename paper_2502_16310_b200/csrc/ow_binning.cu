@@ -487,6 +487,14 @@ int fill_emit(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, int32_t* i
   OW_TRY(ow_slot(ctx, SLOT_PAIR_VAL0, 4 * (size_t)E, s, &pv0));
   OW_TRY(ow_slot(ctx, SLOT_PAIR_KEY1, 4 * (size_t)E, s, &pk1));
   OW_TRY(ow_slot(ctx, SLOT_PAIR_VAL1, 4 * (size_t)E, s, &pv1));
+  int bits = 0;
+  while ((int64_t(1) << bits) < n_bins) ++bits;
+  // the sort's last pass writes the face ids straight into `ids` (no copy):
+  // an odd number of digit passes ends in the second buffer, an even one
+  // (including none) in the first
+  const int passes = (E <= 1 || bits <= 0) ? 0 : ow::radix_passes(bits);
+  if (passes & 1) pv1 = ids;
+  else pv0 = ids;
   const int32_t* foff = (const int32_t*)ctx->slot_ptr[SLOT_BIN_FOFF];
   ow_launch(k_emit_fast<D>, ow_blocks(n, 256), 256, 0, s, g, c, n, (const unsigned long long*)ctx->slot_ptr[SLOT_BIN_MASK],
                                                   foff, (uint32_t*)pk0, (int32_t*)pv0);
@@ -498,12 +506,10 @@ int fill_emit(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, int32_t* i
     OW_LAUNCHED(ctx);
   }
   OW_CHECK_LAUNCH();
-  int bits = 0;
-  while ((int64_t(1) << bits) < n_bins) ++bits;
   uint32_t* rk;
   int32_t* rv;
   OW_TRY(ow::radix_sort_pairs(ctx, (uint32_t*)pk0, (int32_t*)pv0, (uint32_t*)pk1, (int32_t*)pv1, E, bits, &rk, &rv, s));
-  if (E > 0) OW_CUDA(cudaMemcpyAsync(ids, rv, 4 * (size_t)E, cudaMemcpyDeviceToDevice, s));
+  if (E > 0 && rv != ids) OW_CUDA(cudaMemcpyAsync(ids, rv, 4 * (size_t)E, cudaMemcpyDeviceToDevice, s));
   OW_TRY(scan(ctx, ow::LoadArr<int32_t>{counts}, ow::StoreExcl<int32_t>{offsets}, n_bins, nullptr, s));
   return OW_OK;
 }

@@ -392,13 +392,16 @@ inline int radix_pass(ow_ctx* ctx, const uint32_t* ki, const int32_t* vi, uint32
 // Sort n pairs by the low `key_bits` bits of key, stably.  Input in (k0, v0);
 // the sorted result pointer pair is returned through (*rk, *rv), which is
 // either (k0, v0) or (k1, v1).
+// digit passes of a key_bits-bit sort (radix_sort_pairs)
+inline int radix_passes(int key_bits) { return key_bits <= 0 ? 0 : (key_bits + 9) / 10; }
+
 inline int radix_sort_pairs(ow_ctx* ctx, uint32_t* k0, int32_t* v0, uint32_t* k1, int32_t* v1, int64_t n,
                             int key_bits, uint32_t** rk, int32_t** rv, cudaStream_t s) {
   *rk = k0;
   *rv = v0;
   if (n <= 1 || key_bits <= 0) return OW_OK;
   // fewest passes of 8..10-bit digits
-  const int passes = (key_bits + 9) / 10;
+  const int passes = radix_passes(key_bits);
   int bits = (key_bits + passes - 1) / passes;
   if (bits < 8) bits = 8;
   int64_t tiles = (n + RS_TILE - 1) / RS_TILE;
