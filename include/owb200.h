@@ -245,11 +245,12 @@ typedef struct {
   void* host_q;             /* float32[host_row_cap * lattice_q] (dense rows; unused when the
                                packed destinations below are given and fit) */
   int64_t host_row_cap;
-  /* packed boundary rows (preferred over host_q when both fit): the flag word
-   * of every boundary row and the q of its set bits only, rows in order and
+  /* packed boundary rows (preferred over host_cells / host_q when they fit):
+   * per boundary row its flat cell id (uint32: finest cells < 2^32 is checked)
+   * and flag word, and the q of the set bits only, rows in order and
    * directions ascending within a row — the dense q row is -1 where a bit is
-   * clear, so the pair is the whole result at (4 + 4 popc) bytes per row */
-  void* host_row_flags;     /* uint32[host_row_cap] */
+   * clear, so the pair is the whole result at (8 + 4 popc) bytes per row */
+  void* host_rows;          /* uint32[2 * host_row_cap]: (cell id, flag word) per row */
   void* host_q_packed;      /* float32[host_link_cap] */
   int64_t host_link_cap;
 } ow_g2g_params;
@@ -262,7 +263,7 @@ typedef struct {
   int64_t n_boundary;
   int64_t lattice_stats[3];
   int32_t host_copied;      /* bit 0: forest arrays, bit 1: boundary rows (cells + dense q),
-                               bit 2: boundary rows packed (cells + row flags + packed q) */
+                               bit 2: boundary rows packed (rows + packed q) */
   int32_t reran;            /* 1: the device-resident level loop outgrew the forest capacity
                                and the pass reran with a host round trip per level */
   int64_t n_links;          /* boundary links = set flag bits = packed-q length */
@@ -310,10 +311,10 @@ int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int32_t level,
                                  int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int8_t* h_dirs,
                                  int32_t n_dirs, uint32_t* d_flags, int64_t* out_boundary, void* stream);
 int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, void* stream);
-/* Emit plus the packed form: d_row_flags[n_boundary] = flag word per boundary
- * row, d_q_packed[n_links] = q of the set bits (rows in order, directions
- * ascending).  Both null = ow_lattice_links_emit. */
-int ow_lattice_links_emit_packed(ow_ctx* ctx, int64_t* d_cells, float* d_q, uint32_t* d_row_flags,
+/* Emit plus the packed form: d_rows[2 * n_boundary] = (cell id as uint32, flag
+ * word) per boundary row, d_q_packed[n_links] = q of the set bits (rows in
+ * order, directions ascending).  Both null = ow_lattice_links_emit. */
+int ow_lattice_links_emit_packed(ow_ctx* ctx, int64_t* d_cells, float* d_q, uint32_t* d_rows,
                                  float* d_q_packed, void* stream);
 /* Boundary links (set flag bits over the boundary rows) of the last count. */
 int ow_lattice_links_n_links(ow_ctx* ctx, int64_t* out);

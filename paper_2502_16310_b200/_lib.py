@@ -134,7 +134,7 @@ class G2GParamsC(C.Structure):  # ow_g2g_params
         ("host_cells", C.c_void_p),
         ("host_q", C.c_void_p),
         ("host_row_cap", C.c_int64),
-        ("host_row_flags", C.c_void_p),
+        ("host_rows", C.c_void_p),
         ("host_q_packed", C.c_void_p),
         ("host_link_cap", C.c_int64),
     ]

@@ -85,7 +85,7 @@ enum ow_slot {
   SLOT_DRV_STATE,      // native driver: per-pass leaf count + refine state
   SLOT_LAT_HCOUNT,     // boundary links (set flag bits) per candidate block
   SLOT_LAT_HOFFS,      // packed-q offsets per candidate block
-  SLOT_LAT_RFLAGS,     // flag word per boundary row (packed host output)
+  SLOT_LAT_RFLAGS,     // (cell id, flag word) per boundary row (packed host output)
   SLOT_LAT_QPACK,      // q of the set flag bits, row-major (packed host output)
   SLOT_MISC,
   SLOT_COUNT

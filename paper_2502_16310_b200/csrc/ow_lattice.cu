@@ -88,7 +88,7 @@ struct LatArgs {
   int64_t* hoff;            // [n_cb] packed-q offsets
   unsigned long long* links_d;  // device boundary-link counter (set flag bits)
   unsigned long long* face_next;  // k_lat_faces: next face group (dynamic schedule)
-  uint32_t* rflags_out;     // [n_boundary] flag word per boundary row (packed output), or null
+  uint2* rows_out;          // [n_boundary] (cell id, flag word) per boundary row (packed output), or null
   float* qp_out;            // [n_links] q of the set bits, row-major (packed output)
   unsigned long long* bmask;  // [n_cb] boundary-cell mask
   const int64_t* boff;      // [n_cb]
@@ -748,7 +748,7 @@ __global__ void k_lat_emit(LatArgs A) {
     const int k = __popcll(m & ((1ull << c) - 1ull));
     s_fl[k] = A.flags[pos * C + c];
     A.cells_out[row0 + k] = pos * C + c;
-    if (A.rflags_out) A.rflags_out[row0 + k] = s_fl[k];
+    if (A.rows_out) A.rows_out[row0 + k] = make_uint2((unsigned)(pos * C + c), s_fl[k]);
   }
   __syncthreads();
   const int nrow = __popcll(m), nq = A.nq;
@@ -811,7 +811,7 @@ __global__ void k_lat_hits(LatArgs A) {
 
 // Packed q (host output): per candidate block (CTA, thread per cell) the q of
 // every set flag bit, rows in (block, cell) order and directions ascending
-// within a row — q[row][d] for the bits of rflags[row], concatenated.  With the
+// within a row — q[row][d] for the bits of rows[row].y, concatenated.  With the
 // flag words it is the whole result (q = -1 where the bit is clear).
 template <int D>
 __global__ void k_lat_pack(LatArgs A) {
@@ -823,7 +823,7 @@ __global__ void k_lat_pack(LatArgs A) {
   const int c = threadIdx.x, lane = c & 31, w = c >> 5;
   const int k = __popcll(m & ((1ull << c) - 1ull));  // row of cell c within the block
   const int64_t row = A.boff[r] + k;
-  const unsigned fl = ((m >> c) & 1ull) ? A.rflags_out[row] : 0u;
+  const unsigned fl = ((m >> c) & 1ull) ? A.rows_out[row].y : 0u;
   constexpr unsigned FULL = C >= 32 ? 0xffffffffu : (1u << C) - 1u;  // 2D: a 16-thread CTA
   int incl = __popc(fl);
 #pragma unroll
@@ -1118,11 +1118,11 @@ extern "C" int ow_lattice_links_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, 
   return ow_lattice_links_emit_packed(ctx, d_cells, d_q, nullptr, nullptr, stream);
 }
 
-extern "C" int ow_lattice_links_emit_packed(ow_ctx* ctx, int64_t* d_cells, float* d_q, uint32_t* d_row_flags,
+extern "C" int ow_lattice_links_emit_packed(ow_ctx* ctx, int64_t* d_cells, float* d_q, uint32_t* d_rows,
                                             float* d_q_packed, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  if ((d_row_flags == nullptr) != (d_q_packed == nullptr)) {
-    ow_set_error("ow_lattice_links_emit_packed: row flags and packed q go together");
+  if ((d_rows == nullptr) != (d_q_packed == nullptr)) {
+    ow_set_error("ow_lattice_links_emit_packed: packed rows and packed q go together");
     return OW_ERR_INVALID;
   }
   if (ctx->lat_dirs < 2) {
@@ -1133,7 +1133,7 @@ extern "C" int ow_lattice_links_emit_packed(ow_ctx* ctx, int64_t* d_cells, float
   LatArgs A = make_args(ctx);
   A.cells_out = d_cells;
   A.q_out = d_q;
-  A.rflags_out = d_row_flags;
+  A.rows_out = reinterpret_cast<uint2*>(d_rows);
   A.qp_out = d_q_packed;
   const int C = ctx->lat_forest.dim == 3 ? 64 : 16;
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);

@@ -511,21 +511,20 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
   int64_t n_links = 0;
   OW_TRY(ow_lattice_links_n_links(ctx, &n_links));
   out->n_links = n_links;
-  const bool packed = p->host_cells && p->host_row_flags && p->host_q_packed && p->host_row_cap >= nb &&
-                      p->host_link_cap >= n_links && nb > 0;
-  uint32_t* d_rflags = nullptr;
+  const bool packed = p->host_rows && p->host_q_packed && p->host_row_cap >= nb && p->host_link_cap >= n_links &&
+                      nb > 0;
+  uint32_t* d_rows = nullptr;
   float* d_qp = nullptr;
   if (packed) {
     void *pr, *pq;
-    OW_TRY(ow_slot(ctx, SLOT_LAT_RFLAGS, 4 * (size_t)nb, s, &pr));
+    OW_TRY(ow_slot(ctx, SLOT_LAT_RFLAGS, 8 * (size_t)nb, s, &pr));
     OW_TRY(ow_slot(ctx, SLOT_LAT_QPACK, 4 * (size_t)n_links, s, &pq));
-    d_rflags = (uint32_t*)pr;
+    d_rows = (uint32_t*)pr;
     d_qp = (float*)pq;
   }
-  OW_TRY(ow_lattice_links_emit_packed(ctx, (int64_t*)cells, (float*)q, d_rflags, d_qp, stream));
-  if (packed) {  // (4 + 4 popc) bytes per row instead of 4 Q: the host tail is the transfer
-    OW_CUDA(cudaMemcpyAsync(p->host_cells, cells, 8 * (size_t)nb, cudaMemcpyDeviceToHost, s));
-    OW_CUDA(cudaMemcpyAsync(p->host_row_flags, d_rflags, 4 * (size_t)nb, cudaMemcpyDeviceToHost, s));
+  OW_TRY(ow_lattice_links_emit_packed(ctx, (int64_t*)cells, (float*)q, d_rows, d_qp, stream));
+  if (packed) {  // (8 + 4 popc) bytes per row instead of 8 + 4 Q: the host tail is the transfer
+    OW_CUDA(cudaMemcpyAsync(p->host_rows, d_rows, 8 * (size_t)nb, cudaMemcpyDeviceToHost, s));
     OW_CUDA(cudaMemcpyAsync(p->host_q_packed, d_qp, 4 * (size_t)n_links, cudaMemcpyDeviceToHost, s));
     out->host_copied |= 4;
   } else if (p->host_cells && p->host_q && p->host_row_cap >= nb && nb > 0) {

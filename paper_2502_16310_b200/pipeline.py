@@ -131,11 +131,12 @@ class GridPlan:
         its finest-level lattice links.
 
         ``host=True`` also returns pinned host copies of the results
-        (``GridPass.host``: forest arrays, boundary cells, their flag words
-        and the packed q of the set bits): the forest arrays stream to the
-        host on a side stream while the lattice work runs; the boundary rows
-        travel packed ((4 + 4 popc) bytes per row instead of 4 Q) and
-        ``GridPass.host_q()`` expands them to the dense (rows, Q) array."""
+        (``GridPass.host``: forest arrays, boundary cells (uint32 ids as int32
+        views), their flag words and the packed q of the set bits): the forest
+        arrays stream to the host on a side stream while the lattice work
+        runs; the boundary rows travel packed ((8 + 4 popc) bytes per row
+        instead of 8 + 4 Q) and ``GridPass.host_q()`` expands them to the
+        dense (rows, Q) array."""
         if geometry is None and records is None:
             raise InvalidParameterError("geometry_to_grid needs STL records or a geometry")
         dim = self.dim
@@ -186,7 +187,7 @@ class GridPlan:
                     gp.out_cap[what] = t.numel() * t.element_size()
         hbuf = None
         if not host and gp.host_level:  # a reused struct from a host=True pass: no host copies now
-            gp.host_level = gp.host_cells = gp.host_q = gp.host_row_flags = gp.host_q_packed = None
+            gp.host_level = gp.host_cells = gp.host_q = gp.host_rows = gp.host_q_packed = None
             gp.host_block_cap = gp.host_row_cap = gp.host_link_cap = 0
         if host:
             # pinned host buffers owned by the plan and reused by every pass (a
@@ -195,23 +196,22 @@ class GridPlan:
             nrow = max(self._est_rows + self._est_rows // 4 + 1024, 1024)
             nlink = max(self._est_links + self._est_links // 4 + 4096, 4096)
             hb = self._hbuf
-            if (hb is None or hb["level"].numel() < nbk or hb["cells"].numel() < nrow
+            if (hb is None or hb["level"].numel() < nbk or hb["rows"].numel() < 2 * nrow
                     or hb["q_packed"].numel() < nlink):
                 hb = dict(level=self._pinned(torch.int16, nbk), parent=self._pinned(torch.int32, nbk),
                           first_child=self._pinned(torch.int32, nbk), marks=self._pinned(torch.int8, nbk),
                           coords=[self._pinned(torch.int32, nbk) for _ in range(dim)],
-                          cells=self._pinned(torch.int64, nrow), flags=self._pinned(torch.int32, nrow),
-                          q_packed=self._pinned(torch.float32, nlink))
+                          rows=self._pinned(torch.int32, 2 * nrow), q_packed=self._pinned(torch.float32, nlink))
                 self._hbuf = hb
             hbuf = dict(hb)
-            nbk, nrow = hb["level"].numel(), hb["cells"].numel()
+            nbk, nrow = hb["level"].numel(), hb["rows"].numel() // 2
             gp.host_level, gp.host_parent = hbuf["level"].data_ptr(), hbuf["parent"].data_ptr()
             gp.host_first_child, gp.host_marks = hbuf["first_child"].data_ptr(), hbuf["marks"].data_ptr()
             for a in range(dim):
                 gp.host_coord[a] = hbuf["coords"][a].data_ptr()
             gp.host_block_cap = nbk
-            gp.host_cells, gp.host_row_cap = hbuf["cells"].data_ptr(), nrow
-            gp.host_row_flags, gp.host_q_packed = hbuf["flags"].data_ptr(), hbuf["q_packed"].data_ptr()
+            gp.host_row_cap = nrow
+            gp.host_rows, gp.host_q_packed = hbuf["rows"].data_ptr(), hbuf["q_packed"].data_ptr()
             gp.host_link_cap = hb["q_packed"].numel()
         out = _lib.G2GResultC()
         g, bins_t = st["g"], st["bins_t"]
@@ -272,12 +272,12 @@ class GridPlan:
             if not copied & 4:  # the buffers did not fit (first pass of a plan): pack with torch
                 hit = links.q >= 0
                 rflags = (hit.to(torch.int64) << torch.arange(nq, device=hit.device)).sum(1).to(torch.int32)
-                hbuf["cells"], hbuf["flags"] = self._pinned(torch.int64, nb), self._pinned(torch.int32, nb)
-                hbuf["q_packed"] = self._pinned(torch.float32, n_links)
-                hbuf["cells"][:nb].copy_(links.cells, non_blocking=True)
-                hbuf["flags"][:nb].copy_(rflags, non_blocking=True)
+                rows = torch.stack([links.cells.to(torch.int32), rflags], 1).reshape(-1)
+                hbuf["rows"], hbuf["q_packed"] = self._pinned(torch.int32, 2 * nb), self._pinned(torch.float32, n_links)
+                hbuf["rows"][: 2 * nb].copy_(rows, non_blocking=True)
                 hbuf["q_packed"][:n_links].copy_(links.q[hit], non_blocking=True)
-            res["cells"], res["flags"] = hbuf["cells"][:nb], hbuf["flags"][:nb]
+            rows = hbuf["rows"][: 2 * nb].view(nb, 2)  # (cell id as uint32, flag word) per row
+            res["cells"], res["flags"] = rows[:, 0], rows[:, 1]
             res["q_packed"] = hbuf["q_packed"][:n_links]
         return res
 

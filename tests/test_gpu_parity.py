@@ -681,7 +681,7 @@ def test_geometry_to_grid_host_results(ow):
         np.testing.assert_array_equal(h["parent"].numpy(), f._parent)
         np.testing.assert_array_equal(h["first_child"].numpy(), f._first_child)
         np.testing.assert_array_equal(h["marks"].numpy(), f.marks.cpu().numpy())
-        np.testing.assert_array_equal(h["cells"].numpy(), gp.links.cells.cpu().numpy())
+        np.testing.assert_array_equal(h["cells"].numpy().view(np.uint32).astype(np.int64), gp.links.cells.cpu().numpy())
         _check_packed_rows(gp)
 
 
@@ -689,6 +689,7 @@ def _check_packed_rows(gp):
     """Packed host rows (flag word + q of the set bits) == the device links."""
     h, ll = gp.host, gp.links
     cells = ll.cells.cpu().numpy()
+    np.testing.assert_array_equal(h["cells"].numpy().view(np.uint32).astype(np.int64), cells)
     flags = ll.flags.cpu().numpy().view(np.uint32)
     np.testing.assert_array_equal(h["flags"].numpy().view(np.uint32), flags[cells])
     q = ll.q.cpu().numpy()
