@@ -263,6 +263,38 @@ __device__ __forceinline__ bool mt_test3(const float* x, const float* dv, float4
   }
   return hit;
 }
+// mt_test3 split for deferred division: the candidate test (signs of u, v, t
+// and det != 0, as mt_test3, plus a conservative magnitude bound that only
+// rejects pairs mt_test3 rejects: with |det| in the normal range the float
+// sums and products below are within 2^-23 relative of the exact ones, so
+// fl(|un| + |vn|) > fl(1.00001 |det|) implies (|un| + |vn|) / |det| > 1 + 2^-21
+// and then fl(fl(un/det) + fl(vn/det)) > 1; likewise for t) and the numerators.
+__device__ __forceinline__ bool mt_cand3(const float* x, const float* dv, float4 V, float4 E1, float4 E2, float pz,
+                                         float4& num) {
+  const float det = V.w, px = E1.w, py = E2.w;
+  const float tx = FSUB(x[0], V.x), ty = FSUB(x[1], V.y), tz = FSUB(x[2], V.z);
+  const float un = dot3f(tx, ty, tz, px, py, pz);
+  const float qx = FSUB(FMUL(ty, E1.z), FMUL(tz, E1.y));
+  const float qy = FSUB(FMUL(tz, E1.x), FMUL(tx, E1.z));
+  const float qz = FSUB(FMUL(tx, E1.y), FMUL(ty, E1.x));
+  const float vn = dot3f(dv[0], dv[1], dv[2], qx, qy, qz);
+  const float tn = dot3f(E2.x, E2.y, E2.z, qx, qy, qz);
+  bool c = (det != 0.0f) & quot_nonneg(un, det) & quot_nonneg(vn, det) & quot_nonneg(tn, det);
+  const float ad = fabsf(det);
+  if (ad >= 0x1p-100f) {
+    const float lim = FMUL(ad, 1.00001f);
+    c = c & (FADD(fabsf(un), fabsf(vn)) <= lim) & (fabsf(tn) <= lim);
+  }
+  num = make_float4(un, vn, tn, det);
+  return c;
+}
+// the rest of mt_test3 for a candidate: the three IEEE divisions and bounds
+__device__ __forceinline__ bool mt_finish3(float4 num, float& t) {
+  const float uu = FDIV(num.x, num.w), vv = FDIV(num.y, num.w);
+  t = FDIV(num.z, num.w);
+  return (FADD(uu, vv) <= 1.0f) & (t <= 1.0f);
+}
+
 __device__ __forceinline__ float4 mt_prep2(const float* dv, float4 a) {
   return make_float4(a.x, a.y, FSUB(FMUL(dv[0], a.w), FMUL(dv[1], a.z)), 0.0f);
 }
@@ -323,6 +355,7 @@ __device__ __forceinline__ int row_cell(unsigned w, int rem, const float* cen_po
 // (64 = 4^3 cells) and k_lat_mt only runs for a lower override.
 constexpr int INLINE_UNITS = 64;
 constexpr int HITBUF = 64;        // per-warp hit buffer (flushed with one atomic)
+constexpr int CANDBUF = 64;       // per-warp candidate buffer (3D: divisions run on full warps)
 
 // a warp's buffered hits -> the inline hit list (one reservation); returns 0
 __device__ __forceinline__ int flush_hits(const LatArgs& A, const uint2* hb, const uint8_t* hd, int nh, int lane) {
@@ -340,6 +373,38 @@ __device__ __forceinline__ int flush_hits(const LatArgs& A, const uint2* hb, con
 }
 
 
+// record the hits of one warp-wide step (hit / cellg / d per lane)
+__device__ __forceinline__ int record_hits(const LatArgs& A, uint2* hb, uint8_t* hd, int nh, bool hit,
+                                           unsigned cellg, int d, float t, int lane) {
+  const unsigned hm = __ballot_sync(0xffffffffu, hit);
+  if (hm) {
+    if (nh + __popc(hm) > HITBUF) nh = flush_hits(A, hb, hd, nh, lane);
+    if (hit) {
+      atomicOr(&A.flags[cellg], 1u << d);
+      const int k = nh + __popc(hm & lanemask_lt());
+      hb[k] = make_uint2(cellg, __float_as_uint(FADD(t, 0.0f)));  // -0 -> +0
+      hd[k] = (uint8_t)d;
+    }
+    nh += __popc(hm);
+    __syncwarp();
+  }
+  return nh;
+}
+
+// divide the top n (<= 32) buffered candidates of a warp, one per lane
+__device__ __forceinline__ int drain_cands(const LatArgs& A, const float4* cnum, const uint2* cmeta, int nc, int n,
+                                           uint2* hb, uint8_t* hd, int nh, int lane) {
+  bool hit = false;
+  float t = 0.0f;
+  uint2 m = make_uint2(0u, 0u);
+  if (lane < n) {
+    m = cmeta[nc - n + lane];
+    hit = mt_finish3(cnum[nc - n + lane], t);
+  }
+  __syncwarp();  // the drained slots are reused by the next pushes
+  return record_hits(A, hb, hd, nh, hit, m.x, (int)m.y, t, lane);
+}
+
 template <int D, int FPW>
 __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   ow_pdl_wait();
@@ -349,6 +414,10 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   __shared__ uint2 s_hit[4][HITBUF];
   __shared__ uint8_t s_hdir[4][HITBUF];
   __shared__ float s_dv[QMAX][3];
+  // 3D: candidate hits (numerators, det) + (flat cell, direction), divided 32 at a time
+  __shared__ float4 s_cnum[4][D == 3 ? CANDBUF : 1];
+  __shared__ uint2 s_cmeta[4][D == 3 ? CANDBUF : 1];
+  int nc = 0;  // candidates buffered by this warp
   for (int i = threadIdx.x; i < QMAX * 3; i += blockDim.x) s_dv[i / 3][i % 3] = A.dv[i / 3][i % 3];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -530,39 +599,52 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
         float t = 0.0f;
         unsigned cellg = 0;
         const int d = (int)(wj & 31u);
-        if (u < S) {
-          float x[3];
-          const int cell = row_cell<D>(wj, u - ej, A.cen + (int64_t)pj * D * 4, x);
-          cellg = (unsigned)pj * (unsigned)C + (unsigned)cell;
-          const float4* F4 = s_face[wid][fj - fbase];
-          const float* dv = s_dv[d];
-          if (D == 3) {
+        if (D == 3) {
+          bool cand = false;
+          float4 num = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          if (u < S) {
+            float x[3];
+            const int cell = row_cell<D>(wj, u - ej, A.cen + (int64_t)pj * D * 4, x);
+            cellg = (unsigned)pj * (unsigned)C + (unsigned)cell;
+            const float4* F4 = s_face[wid][fj - fbase];
+            const float* dv = s_dv[d];
             float4 V, E1, E2;
             float pz;
             mt_prep3(dv, F4[0], F4[1], F4[2], V, E1, E2, pz);
-            hit = mt_test3(x, dv, V, E1, E2, pz, t);
-          } else {
+            cand = mt_cand3(x, dv, V, E1, E2, pz, num);
+          }
+          const unsigned cm = __ballot_sync(0xffffffffu, cand);
+          if (cm) {
+            if (cand) {
+              const int k = nc + __popc(cm & lanemask_lt());
+              s_cnum[wid][k] = num;
+              s_cmeta[wid][k] = make_uint2(cellg, (unsigned)d);
+            }
+            nc += __popc(cm);
+            __syncwarp();
+            if (nc >= 32) {  // a full warp of divisions
+              nh = drain_cands(A, s_cnum[wid], s_cmeta[wid], nc, 32, s_hit[wid], s_hdir[wid], nh, lane);
+              nc -= 32;
+            }
+          }
+        } else {
+          if (u < S) {
+            float x[3];
+            const int cell = row_cell<D>(wj, u - ej, A.cen + (int64_t)pj * D * 4, x);
+            cellg = (unsigned)pj * (unsigned)C + (unsigned)cell;
+            const float4* F4 = s_face[wid][fj - fbase];
+            const float* dv = s_dv[d];
             const float4 a = F4[0];
             hit = mt_test2(x, dv, mt_prep2(dv, a), make_float4(a.z, a.w, 0.0f, 0.0f), t);
           }
-        }
-        const unsigned hm = __ballot_sync(0xffffffffu, hit);
-        if (hm) {
-          if (nh + __popc(hm) > HITBUF) nh = flush_hits(A, s_hit[wid], s_hdir[wid], nh, lane);
-          if (hit) {
-            atomicOr(&A.flags[cellg], 1u << d);
-            const int k = nh + __popc(hm & lanemask_lt());
-            s_hit[wid][k] = make_uint2(cellg, __float_as_uint(FADD(t, 0.0f)));  // -0 -> +0
-            s_hdir[wid][k] = (uint8_t)d;
-          }
-          nh += __popc(hm);
-          __syncwarp();
+          nh = record_hits(A, s_hit[wid], s_hdir[wid], nh, hit, cellg, d, t, lane);
         }
       }
     }
   }
   __syncwarp();  // s_face is rewritten by the next group
   }
+  if (D == 3 && nc > 0) nh = drain_cands(A, s_cnum[wid], s_cmeta[wid], nc, nc, s_hit[wid], s_hdir[wid], nh, lane);
   if (nh) flush_hits(A, s_hit[wid], s_hdir[wid], nh, lane);
   if (iru && lane == 0) atomicAdd(A.iru_d, iru);
 }
