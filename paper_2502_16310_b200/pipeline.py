@@ -92,6 +92,8 @@ class GridPlan:
         self._outs = {}
         self._hbuf = None
         self._coords = None
+        self._links = self._links_key = None
+        self._ctx = _lib.ctx()
         self._gp = None  # the call's parameter struct, reused while nothing static changes
         self._gp_key = None
         self.reuse = bool(reuse_outputs)
@@ -217,7 +219,7 @@ class GridPlan:
         g, bins_t = st["g"], st["bins_t"]
         v = forest.view()
         try:
-            _lib.call("ow_geometry_to_grid", _lib.ctx(), _lib.ptr(records) if geometry is None else None,
+            _lib.call("ow_geometry_to_grid", self._ctx, _lib.ptr(records) if geometry is None else None,
                       _lib.ptr(coords), nf, next(_geom_keys), C.byref(v), C.byref(g) if g is not None else None,
                       C.byref(gp), _lib.ptr(bins_t[0]) if bins_t else None, st["cap"],
                       _lib.ptr(bins_t[1]) if bins_t else None, _lib.ptr(bins_t[2]) if bins_t else None,
@@ -242,8 +244,16 @@ class GridPlan:
             self._est_rows = nb
             self._est_links = int(out.n_links)
             o = self._outs
-            links = LatticeLinks(lattice=self.lattice, level=int(out.finest_level), leaves=o[0][:nl],
-                                 flags=o[1][: nl * ncell], cells=o[2][:nb], q=o[3][: nb * nq].view(nb, nq))
+            key = (o[0], o[1], o[2], o[3], nl, nb, int(out.finest_level))
+            lk = self._links_key
+            if self.reuse and lk is not None and all(a is b if isinstance(a, torch.Tensor) else a == b
+                                                     for a, b in zip(key, lk)):
+                links = self._links  # same storage and sizes as the last pass: the same views
+            else:
+                links = LatticeLinks(lattice=self.lattice, level=int(out.finest_level), leaves=o[0][:nl],
+                                     flags=o[1][: nl * ncell], cells=o[2][:nb], q=o[3][: nb * nq].view(nb, nq))
+                if self.reuse:
+                    self._links, self._links_key = links, key
         self._est_blocks = forest.n_blocks
         # size the next pass's forest from this one: device refinement then never
         # overflows into the host fallback (which grows the arrays with syncs)
