@@ -8,15 +8,33 @@ reference where it has them: finest-level leaves in ascending block id and
 x-fastest cell index (nearwall.py:537-553), FP32 arithmetic with a fixed
 operation order (distance.py:9-14).
 
-Definition (DESIGN.md §Lattice links):
+Definition ("Lattice links"):
   * link i of a cell with centre x (float32) and finest cell size h (per
     axis, float32 of the FP64 value) is the segment x -> x + c_i*h;
   * candidate faces: every face whose float32 AABB overlaps the link's
     float32 AABB [min(x, x+c_i*h), max(x, x+c_i*h)] (closed intervals);
-  * 3D test: Moller-Trumbore, accept det != 0, u >= 0, v >= 0, u+v <= 1,
-    0 <= t <= 1; 2D test: segment-segment, 0 <= t <= 1 and 0 <= s <= 1;
+  * the segment-face test is WATERTIGHT (Woop, Benthin & Wald, "Watertight
+    Ray/Triangle Intersection", JCGT 2(1), 2013, restated for segments):
+    per direction a fixed frame (kz = first axis of max |dv|, kx, ky the
+    next two cyclically, swapped when dv[kz] < 0; shear Sx = dv[kx]/dv[kz],
+    Sy = dv[ky]/dv[kz], Sz = 1/dv[kz] in float32), vertices translated to
+    the link origin and sheared (A = v - x; Ax = A[kx] - Sx A[kz], ...),
+    edge functions U = Cx By - Cy Bx, V = Ax Cy - Ay Cx, W = Bx Ay - By Ax
+    (float32; recomputed in float64 from the same sheared float32 values
+    when any of them is zero), miss when they have mixed signs or when
+    det = (U + V) + W is zero; T = (U Az + V Bz) + W Cz with Az = Sz A[kz]
+    ...; t = T / det; hit iff 0 <= t <= 1.  An edge function depends only on
+    the edge's two (translated, sheared) vertices, so faces that share an
+    edge or a vertex evaluate it identically (up to sign): a link crossing a
+    closed surface cannot slip between two faces (tests/test_oracle_lattice.py
+    checks it on a closed icosphere against an exact FP64 inside/outside
+    referee).  2D is the same with one transverse axis: the edge's endpoints
+    have transverse coordinates Ax, Bx; U = Bx, V = -Ax (no products);
   * q_i = min t over hits (float32), -1 when link i hits nothing;
   * flags bit i set iff link i hits.
+Opposite directions d, -d share the frame up to exact negations (the swap
+exchanges the edge functions' sign, Sz changes sign), so t(-d) = -t(d)
+bitwise; the CUDA kernel tests each lattice line once for both directions.
 """
 
 from __future__ import annotations
@@ -49,10 +67,75 @@ def directions(name):
     return np.asarray(LATTICES[name], np.int64)
 
 
-def mt_hits(x, dvec, tri):
-    """Moller-Trumbore on pairs. x, dvec: (n, 3) f32; tri (3, 3, n) f32.
+def ray_frame(dv):
+    """(kz, kx, ky, Sx, Sy, Sz) of a direction vector dv (float32, nonzero)."""
+    dv = np.asarray(dv, F32)
+    dim = dv.size
+    a = np.abs(dv)
+    kz = int(np.flatnonzero(a == a.max())[0])  # first axis of max |dv|
+    if dim == 2:
+        kx = 1 - kz
+        return kz, kx, None, F32(dv[kx] / dv[kz]), None, F32(F32(1.0) / dv[kz])
+    kx, ky = (kz + 1) % 3, (kz + 2) % 3
+    if dv[kz] < 0:
+        kx, ky = ky, kx
+    return kz, kx, ky, F32(dv[kx] / dv[kz]), F32(dv[ky] / dv[kz]), F32(F32(1.0) / dv[kz])
+
+
+def wt_hits(x, dv, tri):
+    """Watertight segment-triangle test of pairs. x (n, 3) f32 origins, dv (3,)
+    f32 direction shared by the pairs, tri (3, 3, n) f32 [vertex, axis, pair].
 
     Returns (hit bool (n,), t f32 (n,))."""
+    kz, kx, ky, sx, sy, sz = ray_frame(dv)
+    x = np.asarray(x, F32)
+    P = []
+    for j in range(3):  # translated, sheared vertices (float32, fixed order)
+        a = [tri[j][k] - x[:, k] for k in range(3)]
+        P.append((a[kx] - sx * a[kz], a[ky] - sy * a[kz], sz * a[kz]))
+    (ax, ay, az), (bx, by, bz), (cx, cy, cz) = P
+    u = cx * by - cy * bx
+    v = ax * cy - ay * cx
+    w = bx * ay - by * ax
+    z = (u == 0) | (v == 0) | (w == 0)
+    if z.any():  # exact signs: float products are exact in float64
+        def d(a):
+            return a[z].astype(np.float64)
+
+        u[z] = (d(cx) * d(by) - d(cy) * d(bx)).astype(F32)
+        v[z] = (d(ax) * d(cy) - d(ay) * d(cx)).astype(F32)
+        w[z] = (d(bx) * d(ay) - d(by) * d(ax)).astype(F32)
+    mixed = ((u < 0) | (v < 0) | (w < 0)) & ((u > 0) | (v > 0) | (w > 0))
+    det = (u + v) + w
+    T = (u * az + v * bz) + w * cz
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t = T / det
+    hit = ~mixed & (det != 0) & (t >= 0) & (t <= 1)
+    return hit, t
+
+
+def wt_hits2(x, dv, seg):
+    """2D watertight segment-segment test of pairs. x (n, 2) f32, dv (2,) f32,
+    seg (2, 2, n) f32 [endpoint, axis, pair]."""
+    kz, kx, _, sx, _, sz = ray_frame(dv)
+    x = np.asarray(x, F32)
+    a = [seg[0][k] - x[:, k] for k in range(2)]
+    b = [seg[1][k] - x[:, k] for k in range(2)]
+    ax, az = a[kx] - sx * a[kz], sz * a[kz]
+    bx, bz = b[kx] - sx * b[kz], sz * b[kz]
+    u, v = bx, -ax
+    mixed = ((u < 0) | (v < 0)) & ((u > 0) | (v > 0))
+    det = u + v
+    T = u * az + v * bz
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t = T / det
+    hit = ~mixed & (det != 0) & (t >= 0) & (t <= 1)
+    return hit, t
+
+
+def mt_hits(x, dvec, tri):
+    """Round-1 definition (Moller-Trumbore, not watertight), kept only so the
+    tests can count the links it loses at shared edges. x, dvec: (n, 3) f32."""
     v0, v1, v2 = tri[0], tri[1], tri[2]
     e1 = v1 - v0
     e2 = v2 - v0
@@ -69,22 +152,14 @@ def mt_hits(x, dvec, tri):
         u = ((tx * px + ty * py) + tz * pz) / det
         v = ((dx * qx + dy * qy) + dz * qz) / det
         t = ((e2[0] * qx + e2[1] * qy) + e2[2] * qz) / det
-    hit = (det != 0) & (u >= 0) & (v >= 0) & ((u + v) <= 1) & (t >= 0) & (t <= 1)
+    with np.errstate(invalid="ignore"):
+        hit = (det != 0) & (u >= 0) & (v >= 0) & ((u + v) <= 1) & (t >= 0) & (t <= 1)
     return hit, t
 
 
-def seg_hits(x, dvec, seg):
-    """2D segment-segment on pairs. x, dvec (n, 2) f32; seg (2, 2, n) f32."""
-    ax, ay = seg[0, 0], seg[0, 1]
-    sx, sy = seg[1, 0] - ax, seg[1, 1] - ay
-    rx, ry = dvec[:, 0], dvec[:, 1]
-    den = rx * sy - ry * sx
-    qx, qy = ax - x[:, 0], ay - x[:, 1]
-    with np.errstate(divide="ignore", invalid="ignore"):
-        t = (qx * sy - qy * sx) / den
-        s = (qx * ry - qy * rx) / den
-    hit = (den != 0) & (t >= 0) & (t <= 1) & (s >= 0) & (s <= 1)
-    return hit, t
+def link_hits(x, dv, faces):
+    """The definition's test for one direction: 3D triangles or 2D segments."""
+    return wt_hits(x, dv, faces) if faces.shape[0] == 3 else wt_hits2(x, dv, faces)
 
 
 def lattice_links(forest, coords, lattice="D3Q19"):
@@ -127,11 +202,7 @@ def lattice_links(forest, coords, lattice="D3Q19"):
             cell, fac = cell0[ov], fac0[ov]
             if cell.size == 0:
                 continue
-            dvec = np.broadcast_to(dvs[i], (cell.size, dim))
-            if dim == 3:
-                hit, t = mt_hits(cen[cell], dvec, coords[:, :, fac])
-            else:
-                hit, t = seg_hits(cen[cell], dvec, coords[:, :, fac])
+            hit, t = link_hits(cen[cell], dvs[i], coords[:, :, fac])
             cell, t = cell[hit], t[hit] + F32(0.0)  # -0 -> +0
             if cell.size == 0:
                 continue

@@ -8,7 +8,9 @@ default IEEE ``-prec-div=true -prec-sqrt=true -ftz=false``; never
 
 from __future__ import annotations
 
+import concurrent.futures
 import glob
+import hashlib
 import os
 import shutil
 import subprocess
@@ -17,6 +19,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libowb200.so")
+STAMP = LIB + ".sha256"  # fingerprint of the build inputs (travels with the .so)
 REPO = os.path.dirname(HERE)
 
 NVCC_FLAGS = [
@@ -24,7 +27,6 @@ NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
     "-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
     "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
-    "-shared",
 ]
 
 
@@ -43,26 +45,57 @@ def deps():
     return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(REPO, "include", "owb200.h")]
 
 
-def up_to_date():
-    if not os.path.exists(LIB):
+def fingerprint(extra=()):
+    """sha256 over the sources, headers, nvcc flags and this script: the
+    library is rebuilt whenever any of them changes (mtimes are not trusted:
+    copies to the GPU box keep them, and the flags carry correctness)."""
+    h = hashlib.sha256()
+    for p in deps() + [os.path.abspath(__file__)]:
+        h.update(os.path.relpath(p, REPO).encode())
+        with open(p, "rb") as fh:
+            h.update(fh.read())
+    h.update("\0".join([*NVCC_FLAGS, *extra]).encode())
+    return h.hexdigest()
+
+
+def up_to_date(extra=()):
+    if not (os.path.exists(LIB) and os.path.exists(STAMP)):
         return False
-    t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(p) <= t for p in deps())
+    with open(STAMP) as fh:
+        return fh.read().strip() == fingerprint(extra)
 
 
-def build(force=False, verbose=False, extra=()):
-    if not force and up_to_date():
-        return LIB
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-o", tmp, *sources()]
+def _compile(src, obj, extra, verbose):
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(REPO, "include"), "-c", "-o", obj, src]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     r = subprocess.run(cmd, capture_output=True, text=True)
+    return r.returncode, r.stdout + r.stderr
+
+
+def build(force=False, verbose=False, extra=()):
+    if not force and up_to_date(extra):
+        return LIB
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    srcs = sources()
+    objs = [os.path.join(objdir, os.path.basename(p)[:-3] + ".o") for p in srcs]
+    # one nvcc per translation unit, in parallel (no device code crosses units)
+    with concurrent.futures.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(lambda so: _compile(so[0], so[1], extra, verbose), zip(srcs, objs)))
+    for (rc, log), src in zip(results, srcs):
+        if rc != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n{log}")
+        if verbose and log.strip():
+            print(log, file=sys.stderr)
+    tmp = LIB + ".tmp"
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
+    r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
-    if verbose and (r.stdout or r.stderr):
-        print(r.stdout + r.stderr, file=sys.stderr)
+        raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as fh:
+        fh.write(fingerprint(extra) + "\n")
     return LIB
 
 

@@ -205,7 +205,8 @@ _SIGS = {
 _RESTYPE = {"ow_last_error": C.c_char_p, "ow_version": C.c_int, "ow_launch_count": C.c_int64}
 
 _lib = None
-_ctx = {}
+_tls = threading.local()  # per host thread: {device index: ow_ctx}
+_all_ctx = []             # every context made by this process (launch accounting)
 _lock = threading.Lock()
 
 
@@ -234,14 +235,26 @@ def device():
 
 
 def ctx():
-    """Per-device ow_ctx (created lazily)."""
+    """The calling thread's ow_ctx on the current device (created lazily).
+
+    A context carries two-phase state between calls (fill_bins count -> emit,
+    lattice count -> emit, the pinned readback buffer, the copy stream), so
+    it is never shared between host threads: one per (thread, device), which
+    makes the entry points safe to call concurrently from several threads as
+    the reference's pure functions are."""
     dev = device()
     key = dev.index
-    if key not in _ctx:
-        p = P()
-        check(lib().ow_ctx_create(key, C.byref(p)))
-        _ctx[key] = p
-    return _ctx[key]
+    per = getattr(_tls, "ctx", None)
+    if per is None:
+        per = _tls.ctx = {}
+    c = per.get(key)
+    if c is None:
+        c = P()
+        check(lib().ow_ctx_create(key, C.byref(c)))
+        per[key] = c
+        with _lock:
+            _all_ctx.append(c)
+    return c
 
 
 def stream():
@@ -266,7 +279,9 @@ def ptr(t):
 
 def launches():
     """Kernels launched by this process's contexts so far (bench instrumentation)."""
-    return sum(int(lib().ow_launch_count(c)) for c in _ctx.values())
+    with _lock:
+        cs = list(_all_ctx)
+    return sum(int(lib().ow_launch_count(c)) for c in cs)
 
 
 PROF_IDS = {"mark": 0, "lattice": 1, "fill_bins": 2, "refine": 3, "propagate": 4, "links": 5, "stl": 6, "prep": 7,

@@ -18,11 +18,14 @@
 //                  box and a non-zero determinant (count pass, then EMIT).
 //   scans        : row/unit offsets per face, candidate-block ranks, unit
 //                  offsets per row (+ the first row of every MT tile).
-//   k_lat_mt     : one thread per (row, cell) unit, load-balanced over rows
-//                  staged in shared memory with their per-row Moller-Trumbore
-//                  terms (p = d x e2, det); per unit the FP32 test with a fixed
-//                  op order (divisions only for hits); atomicOr flag bits and
-//                  a compact hit list (cell, direction, t).
+//                  Rows are tested inline (warp-flattened (row, cell) units):
+//                  the watertight segment-face test (Woop et al. 2013,
+//                  oracle/lattice.py:wt_hits) with the oracle's float32 op
+//                  order, one division per candidate crossing, deferred to a
+//                  per-warp buffer; atomicOr flag bits and a compact hit list.
+//   k_lat_mt     : (rows above a tunable size only; not launched by default)
+//                  one thread per (row, cell) unit, load-balanced over rows
+//                  staged in shared memory, the same test.
 //   k_lat_bcount + scan : boundary rows in (block, cell) order.
 //   k_lat_emit + k_lat_hits : cells, q rows (-1 / min t via atomicMin).
 #include "ow_scan.cuh"
@@ -47,6 +50,8 @@ struct LatArgs {
   int nq, level;
   float h[3];               // finest cell size per axis (float32 of the FP64 value)
   float dv[QMAX][3];        // link vectors c_d * h (exact)
+  unsigned frame[QMAX];     // watertight frame of direction d: kx | ky << 2 | kz << 4
+  float4 shear[QMAX];       // (Sx, Sy, Sz, -) of direction d (float32 divisions, oracle/lattice.py:ray_frame)
   int8_t dc[QMAX][3];       // lattice directions c_d
   uint8_t dir_combo[32];    // combination index sum_a (c_a + 1) 3^a of direction d
   uint8_t combo_dir[27];    // direction of each combination (lattice subset)
@@ -232,83 +237,78 @@ __device__ __forceinline__ int div_small(int x, int ext) {
   return (x * m) >> 8;
 }
 
-// One link-face test, oracle/lattice.py:mt_hits (3D) / seg_hits (2D), fixed
-// float32 op order.  3D: V = (v0, det), E1 = (e1, p.x), E2 = (e2, p.y), pz
-// with p = d x e2, det = e1 . p (mt_prep3); 2D: V = (a.xy, den), S = (s.xy)
-// with den = d x s (mt_prep2).  Divisions only for hits.
-__device__ __forceinline__ void mt_prep3(const float* dv, float4 a, float4 b, float4 c, float4& V, float4& E1,
-                                         float4& E2, float& pz) {
-  const float px = FSUB(FMUL(dv[1], c.z), FMUL(dv[2], c.y));
-  const float py = FSUB(FMUL(dv[2], c.x), FMUL(dv[0], c.z));
-  pz = FSUB(FMUL(dv[0], c.y), FMUL(dv[1], c.x));
-  V = make_float4(a.x, a.y, a.z, dot3f(b.x, b.y, b.z, px, py, pz));
-  E1 = make_float4(b.x, b.y, b.z, px);
-  E2 = make_float4(c.x, c.y, c.z, py);
+// One link-face test, oracle/lattice.py:wt_hits (3D) / wt_hits2 (2D): the
+// watertight segment test of Woop, Benthin & Wald (JCGT 2013) with the
+// definition's fixed float32 op order.  Per direction a frame (LatArgs.frame:
+// kx | ky << 2 | kz << 4, shear Sx, Sy, Sz), the face's vertices translated to
+// the link origin (exact: nearby float32 values, Sterbenz) and sheared; the
+// three edge functions decide the crossing (recomputed in float64 from the
+// same sheared values when one is zero) and only candidate crossings form
+// t = T / det.  Face vertices come from shared memory, indexed by the frame's
+// axes (no register permutation); the centre by two selects per axis.
+struct WtNum {
+  float T, det;
+};
+__device__ __forceinline__ float sel3(float a0, float a1, float a2, unsigned k) {
+  return k == 0 ? a0 : (k == 1 ? a1 : a2);
 }
-__device__ __forceinline__ bool mt_test3(const float* x, const float* dv, float4 V, float4 E1, float4 E2, float pz,
-                                         float& t) {
-  const float det = V.w, px = E1.w, py = E2.w;
-  const float tx = FSUB(x[0], V.x), ty = FSUB(x[1], V.y), tz = FSUB(x[2], V.z);
-  const float un = dot3f(tx, ty, tz, px, py, pz);
-  const float qx = FSUB(FMUL(ty, E1.z), FMUL(tz, E1.y));
-  const float qy = FSUB(FMUL(tz, E1.x), FMUL(tx, E1.z));
-  const float qz = FSUB(FMUL(tx, E1.y), FMUL(ty, E1.x));
-  const float vn = dot3f(dv[0], dv[1], dv[2], qx, qy, qz);
-  const float tn = dot3f(E2.x, E2.y, E2.z, qx, qy, qz);
-  bool hit = false;
-  if ((det != 0.0f) & quot_nonneg(un, det) & quot_nonneg(vn, det) & quot_nonneg(tn, det)) {
-    const float uu = FDIV(un, det), vv = FDIV(vn, det);
-    t = FDIV(tn, det);
-    hit = (FADD(uu, vv) <= 1.0f) & (t <= 1.0f);
+// v: 3 vertices x 4 floats (x, y, z, -) in shared memory
+__device__ __forceinline__ bool wt_cand3(const float* x, const float* v, unsigned fr, float4 S, WtNum& num) {
+  const unsigned kx = fr & 3u, ky = (fr >> 2) & 3u, kz = (fr >> 4) & 3u;
+  const float xx = sel3(x[0], x[1], x[2], kx), xy = sel3(x[0], x[1], x[2], ky), xz = sel3(x[0], x[1], x[2], kz);
+  float X[3], Y[3], Z[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float az = FSUB(v[4 * j + kz], xz);
+    X[j] = FSUB(FSUB(v[4 * j + kx], xx), FMUL(S.x, az));
+    Y[j] = FSUB(FSUB(v[4 * j + ky], xy), FMUL(S.y, az));
+    Z[j] = az;
   }
-  return hit;
-}
-// mt_test3 split for deferred division: the candidate test (signs of u, v, t
-// and det != 0, as mt_test3, plus a conservative magnitude bound that only
-// rejects pairs mt_test3 rejects: with |det| in the normal range the float
-// sums and products below are within 2^-23 relative of the exact ones, so
-// fl(|un| + |vn|) > fl(1.00001 |det|) implies (|un| + |vn|) / |det| > 1 + 2^-21
-// and then fl(fl(un/det) + fl(vn/det)) > 1; likewise for t) and the numerators.
-__device__ __forceinline__ bool mt_cand3(const float* x, const float* dv, float4 V, float4 E1, float4 E2, float pz,
-                                         float4& num) {
-  const float det = V.w, px = E1.w, py = E2.w;
-  const float tx = FSUB(x[0], V.x), ty = FSUB(x[1], V.y), tz = FSUB(x[2], V.z);
-  const float un = dot3f(tx, ty, tz, px, py, pz);
-  const float qx = FSUB(FMUL(ty, E1.z), FMUL(tz, E1.y));
-  const float qy = FSUB(FMUL(tz, E1.x), FMUL(tx, E1.z));
-  const float qz = FSUB(FMUL(tx, E1.y), FMUL(ty, E1.x));
-  const float vn = dot3f(dv[0], dv[1], dv[2], qx, qy, qz);
-  const float tn = dot3f(E2.x, E2.y, E2.z, qx, qy, qz);
-  bool c = (det != 0.0f) & quot_nonneg(un, det) & quot_nonneg(vn, det) & quot_nonneg(tn, det);
+  float U = FSUB(FMUL(X[2], Y[1]), FMUL(Y[2], X[1]));
+  float V = FSUB(FMUL(X[0], Y[2]), FMUL(Y[0], X[2]));
+  float W = FSUB(FMUL(X[1], Y[0]), FMUL(Y[1], X[0]));
+  if ((U == 0.0f) | (V == 0.0f) | (W == 0.0f)) {  // exact signs: float products are exact in float64
+    U = __double2float_rn(DSUB(DMUL((double)X[2], (double)Y[1]), DMUL((double)Y[2], (double)X[1])));
+    V = __double2float_rn(DSUB(DMUL((double)X[0], (double)Y[2]), DMUL((double)Y[0], (double)X[2])));
+    W = __double2float_rn(DSUB(DMUL((double)X[1], (double)Y[0]), DMUL((double)Y[1], (double)X[0])));
+  }
+  const bool mixed = ((U < 0.0f) | (V < 0.0f) | (W < 0.0f)) & ((U > 0.0f) | (V > 0.0f) | (W > 0.0f));
+  const float det = FADD(FADD(U, V), W);
+  const float T = FADD(FADD(FMUL(U, FMUL(S.z, Z[0])), FMUL(V, FMUL(S.z, Z[1]))), FMUL(W, FMUL(S.z, Z[2])));
+  bool c = !mixed & (det != 0.0f) & quot_nonneg(T, det);
+  // conservative t <= 1 bound (normal |det|): fl(|T|) > fl(1.00001 |det|)
+  // implies |T| / |det| > 1 + 2^-21, hence fl(T / det) > 1
   const float ad = fabsf(det);
-  if (ad >= 0x1p-100f) {
-    const float lim = FMUL(ad, 1.00001f);
-    c = c & (FADD(fabsf(un), fabsf(vn)) <= lim) & (fabsf(tn) <= lim);
-  }
-  num = make_float4(un, vn, tn, det);
+  if (ad >= 0x1p-100f) c = c & (fabsf(T) <= FMUL(ad, 1.00001f));
+  num.T = T;
+  num.det = det;
   return c;
 }
-// the rest of mt_test3 for a candidate: the three IEEE divisions and bounds
-__device__ __forceinline__ bool mt_finish3(float4 num, float& t) {
-  const float uu = FDIV(num.x, num.w), vv = FDIV(num.y, num.w);
-  t = FDIV(num.z, num.w);
-  return (FADD(uu, vv) <= 1.0f) & (t <= 1.0f);
+__device__ __forceinline__ bool wt_finish(WtNum n, float& t) {
+  t = FDIV(n.T, n.det);
+  return t <= 1.0f;
 }
-
-__device__ __forceinline__ float4 mt_prep2(const float* dv, float4 a) {
-  return make_float4(a.x, a.y, FSUB(FMUL(dv[0], a.w), FMUL(dv[1], a.z)), 0.0f);
+__device__ __forceinline__ bool wt_test3(const float* x, const float* v, unsigned fr, float4 S, float& t) {
+  WtNum n;
+  return wt_cand3(x, v, fr, S, n) && wt_finish(n, t);
 }
-__device__ __forceinline__ bool mt_test2(const float* x, const float* dv, float4 V, float4 S, float& t) {
-  // segment-segment (oracle/lattice.py:seg_hits), s = b - a pre-formed
-  const float den = V.z;
-  const float qx = FSUB(V.x, x[0]), qy = FSUB(V.y, x[1]);
-  const float tn = FSUB(FMUL(qx, S.y), FMUL(qy, S.x));
-  const float sn = FSUB(FMUL(qx, dv[1]), FMUL(qy, dv[0]));
+// 2D: v = (a.x, a.y, b.x, b.y); frame kx | kz << 4, S = (Sx, -, Sz)
+__device__ __forceinline__ bool wt_test2(const float* x, const float* v, unsigned fr, float4 S, float& t) {
+  const unsigned kx = fr & 3u, kz = (fr >> 4) & 3u;
+  const float xx = kx ? x[1] : x[0], xz = kz ? x[1] : x[0];
+  const float aaz = FSUB(v[kz], xz), baz = FSUB(v[2 + kz], xz);
+  const float ax = FSUB(FSUB(v[kx], xx), FMUL(S.x, aaz));
+  const float bx = FSUB(FSUB(v[2 + kx], xx), FMUL(S.x, baz));
+  const float U = bx, V = -ax;
+  const bool mixed = ((U < 0.0f) | (V < 0.0f)) & ((U > 0.0f) | (V > 0.0f));
+  const float det = FADD(U, V);
   bool hit = false;
-  if ((den != 0.0f) && quot_nonneg(tn, den) && quot_nonneg(sn, den)) {
-    t = FDIV(tn, den);
-    const float ss = FDIV(sn, den);
-    hit = t <= 1.0f && ss <= 1.0f;
+  if (!mixed && det != 0.0f) {
+    const float T = FADD(FMUL(U, FMUL(S.z, aaz)), FMUL(V, FMUL(S.z, baz)));
+    if (quot_nonneg(T, det)) {
+      t = FDIV(T, det);
+      hit = t <= 1.0f;
+    }
   }
   return hit;
 }
@@ -392,14 +392,14 @@ __device__ __forceinline__ int record_hits(const LatArgs& A, uint2* hb, uint8_t*
 }
 
 // divide the top n (<= 32) buffered candidates of a warp, one per lane
-__device__ __forceinline__ int drain_cands(const LatArgs& A, const float4* cnum, const uint2* cmeta, int nc, int n,
+__device__ __forceinline__ int drain_cands(const LatArgs& A, const WtNum* cnum, const uint2* cmeta, int nc, int n,
                                            uint2* hb, uint8_t* hd, int nh, int lane) {
   bool hit = false;
   float t = 0.0f;
   uint2 m = make_uint2(0u, 0u);
   if (lane < n) {
     m = cmeta[nc - n + lane];
-    hit = mt_finish3(cnum[nc - n + lane], t);
+    hit = wt_finish(cnum[nc - n + lane], t);
   }
   __syncwarp();  // the drained slots are reused by the next pushes
   return record_hits(A, hb, hd, nh, hit, m.x, (int)m.y, t, lane);
@@ -410,15 +410,19 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
   constexpr int FACES_PER_WARP = FPW, SLOT_LANES = 32 / FPW;
-  __shared__ float4 s_face[4][FACES_PER_WARP][3];  // per warp: (v0, e1, e2) / (a, s) of its faces
+  __shared__ float4 s_face[4][FACES_PER_WARP][3];  // per warp: vertices (v0, v1, v2) / (a.xy, b.xy) of its faces
   __shared__ uint2 s_hit[4][HITBUF];
   __shared__ uint8_t s_hdir[4][HITBUF];
-  __shared__ float s_dv[QMAX][3];
-  // 3D: candidate hits (numerators, det) + (flat cell, direction), divided 32 at a time
-  __shared__ float4 s_cnum[4][D == 3 ? CANDBUF : 1];
+  __shared__ unsigned s_frame[QMAX];
+  __shared__ float4 s_shear[QMAX];
+  // 3D: candidate hits (T, det) + (flat cell, direction), divided 32 at a time
+  __shared__ WtNum s_cnum[4][D == 3 ? CANDBUF : 1];
   __shared__ uint2 s_cmeta[4][D == 3 ? CANDBUF : 1];
   int nc = 0;  // candidates buffered by this warp
-  for (int i = threadIdx.x; i < QMAX * 3; i += blockDim.x) s_dv[i / 3][i % 3] = A.dv[i / 3][i % 3];
+  for (int i = threadIdx.x; i < QMAX; i += blockDim.x) {
+    s_frame[i] = A.frame[i];
+    s_shear[i] = A.shear[i];
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sl = lane % SLOT_LANES;
@@ -453,14 +457,14 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
       hi[a] = fmaxf(hi[a], v[j][a]);
     }
   }
-  if (live && sl == 0) {  // e1 = v1 - v0, e2 = v2 - v0 (3D) / s = b - a (2D), oracle/lattice.py
+  if (live && sl == 0) {  // the face's vertices (the watertight test translates them per link)
     float4 r0, r1 = make_float4(0.0f, 0.0f, 0.0f, 0.0f), r2 = r1;
     if (D == 3) {
       r0 = make_float4(v[0][0], v[0][1], v[0][2], 0.0f);
-      r1 = make_float4(FSUB(v[1][0], v[0][0]), FSUB(v[1][1], v[0][1]), FSUB(v[1][2], v[0][2]), 0.0f);
-      r2 = make_float4(FSUB(v[2][0], v[0][0]), FSUB(v[2][1], v[0][1]), FSUB(v[2][2], v[0][2]), 0.0f);
+      r1 = make_float4(v[1][0], v[1][1], v[1][2], 0.0f);
+      r2 = make_float4(v[2][0], v[2][1], v[2][2], 0.0f);
     } else {
-      r0 = make_float4(v[0][0], v[0][1], FSUB(v[1][0], v[0][0]), FSUB(v[1][1], v[0][1]));
+      r0 = make_float4(v[0][0], v[0][1], v[1][0], v[1][1]);
     }
     if (A.inline_units < C) {  // records for k_lat_mt (no large rows when every row is inline)
       A.rec[3 * f + 0] = r0;
@@ -601,17 +605,12 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
         const int d = (int)(wj & 31u);
         if (D == 3) {
           bool cand = false;
-          float4 num = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          WtNum num{0.0f, 0.0f};
           if (u < S) {
             float x[3];
             const int cell = row_cell<D>(wj, u - ej, A.cen + (int64_t)pj * D * 4, x);
             cellg = (unsigned)pj * (unsigned)C + (unsigned)cell;
-            const float4* F4 = s_face[wid][fj - fbase];
-            const float* dv = s_dv[d];
-            float4 V, E1, E2;
-            float pz;
-            mt_prep3(dv, F4[0], F4[1], F4[2], V, E1, E2, pz);
-            cand = mt_cand3(x, dv, V, E1, E2, pz, num);
+            cand = wt_cand3(x, reinterpret_cast<const float*>(s_face[wid][fj - fbase]), s_frame[d], s_shear[d], num);
           }
           const unsigned cm = __ballot_sync(0xffffffffu, cand);
           if (cm) {
@@ -632,10 +631,7 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
             float x[3];
             const int cell = row_cell<D>(wj, u - ej, A.cen + (int64_t)pj * D * 4, x);
             cellg = (unsigned)pj * (unsigned)C + (unsigned)cell;
-            const float4* F4 = s_face[wid][fj - fbase];
-            const float* dv = s_dv[d];
-            const float4 a = F4[0];
-            hit = mt_test2(x, dv, mt_prep2(dv, a), make_float4(a.z, a.w, 0.0f, 0.0f), t);
+            hit = wt_test2(x, reinterpret_cast<const float*>(s_face[wid][fj - fbase]), s_frame[d], s_shear[d], t);
           }
           nh = record_hits(A, s_hit[wid], s_hdir[wid], nh, hit, cellg, d, t, lane);
         }
@@ -680,23 +676,23 @@ struct BoffStore {
 
 // Persistent, load-balanced over units: a tile of MT_TILE consecutive units
 // covers at most MT_TILE + 1 rows (the first one recorded by the unit scan).
-// The tile's rows are staged in shared memory with their per-row terms of
-// Moller-Trumbore (oracle/lattice.py:mt_hits, same float32 ops): p = d x e2,
-// det = e1 . p (3D) / den = d x s (2D).  Each thread binary-searches the row of
-// its first unit and walks forward.
+// The tile's rows are staged in shared memory with their face vertices; each
+// unit runs the watertight test (oracle/lattice.py:wt_hits / wt_hits2).  Each
+// thread binary-searches the row of its first unit and walks forward.
 template <int D>
 __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
   ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
   __shared__ int s_off[MT_TILE + 1];
   __shared__ int4 s_meta[MT_TILE + 1];    // pos, face, w, units
-  __shared__ float4 s_v0[MT_TILE + 1];    // v0.xyz, det     (2D: a.xy, den, -)
-  __shared__ float4 s_e1[MT_TILE + 1];    // e1.xyz, p.x     (2D: s.xy, -, -)
-  __shared__ float4 s_e2[MT_TILE + 1];    // e2.xyz, p.y
-  __shared__ float s_pz[MT_TILE + 1];     // p.z
-  __shared__ float s_dv[QMAX][3];
+  __shared__ float4 s_tri[MT_TILE + 1][3];  // the row's face vertices (2D: (a.xy, b.xy))
+  __shared__ unsigned s_frame[QMAX];
+  __shared__ float4 s_shear[QMAX];
   __shared__ int s_nh;
-  for (int i = threadIdx.x; i < QMAX * 3; i += MT_THREADS) s_dv[i / 3][i % 3] = A.dv[i / 3][i % 3];
+  for (int i = threadIdx.x; i < QMAX; i += MT_THREADS) {
+    s_frame[i] = A.frame[i];
+    s_shear[i] = A.shear[i];
+  }
   if (threadIdx.x == 0) s_nh = 0;
   const unsigned long long ru = *A.ru_d;
   const int64_t U = (int64_t)(ru >> RU_ROW_BITS);
@@ -709,25 +705,16 @@ __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
     const int64_t u1 = min(U, u0 + MT_TILE);
     const int64_t r0 = A.tile_row[tile];
     const int nr = (int)((tile + 1 < n_tiles ? (int64_t)A.tile_row[tile + 1] : R - 1) - r0 + 1);
-    __syncthreads();  // previous tile done with the staging buffers (and s_dv written)
+    __syncthreads();  // previous tile done with the staging buffers (and the frames written)
     for (int i = threadIdx.x; i < nr; i += MT_THREADS) {
       const int4 m = A.rows[r0 + i];
       s_off[i] = (int)(A.rowoff[r0 + i] - u0);  // >= -63 for the first row
       s_meta[i] = m;
-      const float* dv = s_dv[m.z & 31];
       const float4* Rf = A.rec + 3 * (int64_t)m.y;
+      s_tri[i][0] = Rf[0];
       if (D == 3) {
-        float4 V, E1, E2;
-        float pz;
-        mt_prep3(dv, Rf[0], Rf[1], Rf[2], V, E1, E2, pz);
-        s_v0[i] = V;
-        s_e1[i] = E1;
-        s_e2[i] = E2;
-        s_pz[i] = pz;
-      } else {
-        const float4 a = Rf[0];
-        s_v0[i] = mt_prep2(dv, a);
-        s_e1[i] = make_float4(a.z, a.w, 0.0f, 0.0f);
+        s_tri[i][1] = Rf[1];
+        s_tri[i][2] = Rf[2];
       }
     }
     __syncthreads();
@@ -757,9 +744,9 @@ __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
         float x[3];
         const int cell = row_cell<D>(w, u - s_off[row], A.cen + (int64_t)m.x * D * 4, x);
         cellg = m.x * C + cell;
-        const float* dv = s_dv[d];
-        if (D == 3) hit = mt_test3(x, dv, s_v0[row], s_e1[row], s_e2[row], s_pz[row], t);
-        else hit = mt_test2(x, dv, s_v0[row], s_e1[row], t);
+        const float* tv = reinterpret_cast<const float*>(s_tri[row]);
+        if (D == 3) hit = wt_test3(x, tv, s_frame[d], s_shear[d], t);
+        else hit = wt_test2(x, tv, s_frame[d], s_shear[d], t);
       }
       // hits of this tile go to its own slots [u0, u0 + n) of the hit list
       // (a tile has at most MT_TILE hits): shared-memory append, no global counter
@@ -992,6 +979,31 @@ LatArgs make_args(ow_ctx* ctx) {
       if (a < f->dim) {
         ci += (ctx->lat_dir[i * 3 + a] + 1) * mul;
         mul *= 3;
+      }
+    }
+    {  // watertight frame (oracle/lattice.py:ray_frame): kz = first axis of max |dv|
+      const int D = f->dim;
+      int kz = 0;
+      for (int a = 1; a < D; ++a)
+        if (fabsf(A.dv[i][a]) > fabsf(A.dv[i][kz])) kz = a;
+      int kx, ky = 0;
+      if (D == 2) {
+        kx = 1 - kz;
+      } else {
+        kx = (kz + 1) % 3;
+        ky = (kz + 2) % 3;
+        if (A.dv[i][kz] < 0.0f) {
+          const int t = kx;
+          kx = ky;
+          ky = t;
+        }
+      }
+      A.frame[i] = (unsigned)kx | (unsigned)ky << 2 | (unsigned)kz << 4;
+      volatile float dz = A.dv[i][kz];  // (IEEE float32 divisions, as the oracle's)
+      if (i > 0) {
+        A.shear[i].x = A.dv[i][kx] / dz;
+        A.shear[i].y = D == 3 ? A.dv[i][ky] / dz : 0.0f;
+        A.shear[i].z = 1.0f / dz;
       }
     }
     A.dir_combo[i] = (uint8_t)ci;

@@ -497,7 +497,12 @@ __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_items(MarkArgs A, Mark
   for (int64_t it = (int64_t)blockIdx.x * MARK_WARPS + wid; it < n; it += (int64_t)gridDim.x * MARK_WARPS) {
     const int4 item = M.items[it];
     const int pos = item.x;
-    if (*(volatile unsigned*)&M.hit[pos]) continue;  // block already marked
+    // block already marked: lane 0 reads the flag (other warps atomicOr it at
+    // any time) and broadcasts it, so the skip is warp-uniform before the
+    // full-mask collectives below
+    unsigned done = 0u;
+    if (lane == 0) done = *(volatile unsigned*)&M.hit[pos];
+    if (__shfl_sync(0xffffffffu, done, 0)) continue;
     const int id = A.leaves[pos];
     const int b = item.z;
     double blo[3], bhi[3];

@@ -476,10 +476,18 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
     out->host_copied |= 1;
     side = true;
   }
-  if (p->lattice_q < 2 || !p->alloc) {
-    if (side) OW_CUDA(cudaStreamWaitEvent(s, ctx->copy_ev[1], 0));
-    return ow_stage_times(ctx, &out->nw);
-  }
+  // from here on every return path (errors included) joins the side stream
+  // into `s`: the caller may reuse the forest storage on `s` as soon as the
+  // call returns, and the copies still read it
+  struct JoinCopies {
+    ow_ctx* ctx;
+    cudaStream_t s;
+    bool on;
+    ~JoinCopies() {
+      if (on) cudaStreamWaitEvent(s, ctx->copy_ev[1], 0);
+    }
+  } join{ctx, s, side};
+  if (p->lattice_q < 2 || !p->alloc) return ow_stage_times(ctx, &out->nw);
   void* pl;
   OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(f->n_blocks + 1), s, &pl));
   int64_t nl = ctx->drv_spec_nl;  // compacted by the device-resident loop
@@ -532,7 +540,10 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
     OW_CUDA(cudaMemcpyAsync(p->host_q, q, 4 * (size_t)nb * p->lattice_q, cudaMemcpyDeviceToHost, s));
     out->host_copied |= 2;
   }
-  if (side) OW_CUDA(cudaStreamWaitEvent(s, ctx->copy_ev[1], 0));  // results complete on `s`
+  if (side) {  // results complete on `s`
+    join.on = false;
+    OW_CUDA(cudaStreamWaitEvent(s, ctx->copy_ev[1], 0));
+  }
   OW_TRY(ow_lattice_stats(ctx, out->lattice_stats, stream));
   return ow_stage_times(ctx, &out->nw);  // host work overlapping the emit kernels
 }

@@ -93,7 +93,6 @@ class GridPlan:
         self._hbuf = None
         self._coords = None
         self._links = self._links_key = None
-        self._ctx = _lib.ctx()
         self._gp = None  # the call's parameter struct, reused while nothing static changes
         self._gp_key = None
         self.reuse = bool(reuse_outputs)
@@ -219,7 +218,7 @@ class GridPlan:
         g, bins_t = st["g"], st["bins_t"]
         v = forest.view()
         try:
-            _lib.call("ow_geometry_to_grid", self._ctx, _lib.ptr(records) if geometry is None else None,
+            _lib.call("ow_geometry_to_grid", _lib.ctx(), _lib.ptr(records) if geometry is None else None,
                       _lib.ptr(coords), nf, next(_geom_keys), C.byref(v), C.byref(g) if g is not None else None,
                       C.byref(gp), _lib.ptr(bins_t[0]) if bins_t else None, st["cap"],
                       _lib.ptr(bins_t[1]) if bins_t else None, _lib.ptr(bins_t[2]) if bins_t else None,

@@ -252,3 +252,42 @@ def test_primitives_and_stl_roundtrip():
     assert v.shape == (16, 2) and fcs.shape == (16, 2)
     v, fcs = og.parse_primitives("sphere 0.5 0.5 0.5 0.3 15 18")
     assert fcs.shape[0] == 2 * 18 + 2 * 13 * 18
+
+
+def test_forest_invariant_checker_on_oracle_forests():
+    """The full-size invariant checker (tests/forest_invariants.py) accepts
+    the oracle's own refined forests (2D and 3D) and rejects a forest with a
+    2:1 violation and one with a broken child link."""
+    import pytest
+
+    from forest_invariants import check_forest_invariants
+    from oracle import forest as of
+    from oracle import nearwall as on
+    from paper_2502_16310_b200 import shapes
+
+    tri = shapes.icosphere_triangles(2).astype(np.float32)
+    coords = np.ascontiguousarray(np.transpose(tri, (1, 2, 0)))
+    for dim, (dmin, dmax, root, geo, d) in {
+        3: ((0, 0, 0), (1, 1, 1), (4, 4, 4), coords, 0.08),
+        2: ((0, 0), (1, 1), (8, 8), None, 0.1),
+    }.items():
+        if geo is None:
+            from oracle import geometry as og
+
+            v, fcs = og.circle(0.5, 0.5, 0.25, 256)
+            geo = og.index_to_coords(v, fcs)
+        f = of.Forest(dmin, dmax, root)
+        on.refine_near_wall(f, geo, d, n_levels=3, bins_per_axis=4)
+        args = (f.level.astype(np.int64), f.coords.astype(np.int64), f.parent.astype(np.int64),
+                f.first_child.astype(np.int64), np.asarray(root, np.int64))
+        check_forest_invariants(*args)
+    # a leaf at level 2 next to a level-0 leaf: split one child of a root block twice
+    f = of.Forest((0, 0), (1, 1), (4, 4))
+    f.marks[5] = 1
+    f.refine_marked(0)
+    kid = int(f.first_child[5])
+    f.marks[kid] = 1
+    f._append_children(np.array([kid]))
+    with pytest.raises(AssertionError):
+        check_forest_invariants(f.level.astype(np.int64), f.coords.astype(np.int64), f.parent.astype(np.int64),
+                                f.first_child.astype(np.int64), np.asarray((4, 4), np.int64))
