@@ -327,7 +327,7 @@ def test_marks_every_level_sampled_full_size(ow, cfg):
         leaves = f.leaf_blocks_at(L).cpu().numpy()
         mk = leaves[marks[leaves] == 1]
         pick = np.unique(np.concatenate([rng.choice(mk, min(mk.size, 500), replace=False),
-                                         rng.choice(leaves, min(leaves.size, 700), replace=False)]))
+                                         rng.choice(leaves, min(leaves.size, 1000), replace=False)]))
         fo = _oracle_forest_of(f)
         hide = np.ones(fo.n, bool)
         hide[pick] = False

@@ -529,6 +529,81 @@ def test_grid_plan_reuse_outputs(ow):
             assert torch.equal(getattr(gp.links, name), getattr(ref.links, name)), name
 
 
+def test_grid_plan_reuse_equal_sizes(ow):
+    """reuse_outputs=True with equal output sizes between passes (the same
+    geometry twice, then its cyclic coordinate permutation: same leaf and
+    boundary counts, different faces and links).  The plan hands back the
+    same LatticeLinks views (documented aliasing: a pass's results live
+    until the next run) and every pass equals a fresh plan's."""
+    import torch
+
+    from paper_2502_16310_b200 import pipeline, shapes
+
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8)
+    plan = pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19", reuse_outputs=True)
+    tris = shapes.icosphere_triangles(3)
+    prev = None
+    for k, t in enumerate((tris, tris, tris[:, :, [1, 2, 0]])):
+        data = shapes.binary_stl_bytes(t)
+        n = int.from_bytes(data[80:84], "little")
+        rec = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda()
+        gp = plan.run(rec, n)
+        ref = pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19").run(rec, n)
+        assert gp.forest.blocks_per_level() == ref.forest.blocks_per_level()
+        np.testing.assert_array_equal(gp.forest._coords, ref.forest._coords)
+        for name in ("leaves", "flags", "cells", "q"):
+            assert torch.equal(getattr(gp.links, name), getattr(ref.links, name)), (k, name)
+        if prev is not None and prev[0] == (gp.links.n_boundary, gp.links.leaves.numel()):
+            assert gp.links is prev[1]  # same storage, same sizes: the cached views
+        prev = ((gp.links.n_boundary, gp.links.leaves.numel()), gp.links)
+
+
+def test_two_host_threads_concurrently(ow):
+    """The entry points are safe to call from several host threads at once
+    (SPEC.md:133, 218): each thread gets its own context, so two threads
+    binning and linking different geometries on their own streams, many
+    times over, reproduce the single-threaded results exactly."""
+    import threading
+
+    import torch
+
+    from paper_2502_16310_b200 import shapes
+
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    geoms = [ow.CoordListGeometry(3, np.ascontiguousarray(np.transpose(
+        shapes.icosphere_triangles(s, radius=r).astype(np.float32), (1, 2, 0)))) for s, r in ((3, 0.3), (4, 0.25))]
+    grids = [ow.BinGrid(dom, 8), ow.BinGrid(dom, 6)]
+
+    def work(k):
+        bins = ow.fill_bins(geoms[k], grids[k])
+        f = ow.init_root_grid(dom, (8, 8, 8))
+        ll = ow.build_lattice_links(f, geoms[k], None, "D3Q19")
+        return [t.cpu() for t in (bins.ids, bins.counts, bins.offsets, ll.flags, ll.cells, ll.q)]
+
+    ref = [work(0), work(1)]
+    errors = []
+
+    def thread(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(6):
+                    got = work(k)
+                    for a, b in zip(got, ref[k]):
+                        if not torch.equal(a, b):
+                            errors.append(k)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=thread, args=(k,)) for k in (0, 1)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+
+
 def test_geometry_to_grid_errors(ow):
     import torch
 
