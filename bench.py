@@ -344,11 +344,11 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (procedural geometry, deterministic)",
-        "config": {"workload": cfg["workload"], "faces": n_faces, "cell_face_tests_per_step": T_step,
-                   "pairs_evaluated_per_step": evaluated, "blocks_per_level": blocks,
-                   "boundary_cells": n_boundary, "l2": "flushed (256 MB write) before every step",
-                   "parallelism": f"octree-block shards x{world}: marking and lattice links per rank slice, NCCL "
-                                  f"all-gather of marks and of boundary links; bins/forest replicated"},
+        # (main() sets "config" to bench_config(): the same object as the reference arm's)
+        "run": {"cell_face_tests_per_step": T_step, "pairs_evaluated_per_step": evaluated,
+                "blocks_per_level": blocks, "boundary_cells": n_boundary,
+                "parallelism": f"octree-block shards x{world}: marking and lattice links per rank slice, "
+                               f"all-gather of marks and of boundary links; bins/forest replicated"},
         "roofline": roofline,
         "gpu_launches": int(launches),
         "host_numa_node": numa,
@@ -360,41 +360,93 @@ def gpu_arm(args, cfg, rank, world, local_rank):
 
 
 # ---------------------------------------------------------------------------- CPU arms
+# T and faces of each configuration: properties of the
+# workload, identical for both arms (tests/test_gpu_parity.py checks the GPU
+# pass against this table; the oracle / reference reproduce the same forests)
+FACES = {"C1": 12800, "C2": 20480, "C3": 69936, "C4": 1000000, "C5": 5242880}
+TESTS_PER_STEP = {"C1": 65607680, "C2": 114183168, "C3": 2883791872, "C4": 5029797240, "C5": 3326663808}
+FULL_CPU = ("C1", "C2")  # configs whose whole pass one CPU step runs (C3-C5: bounded samples)
+
+
+def bench_config(name):
+    """The ``config`` object of both arms' JSON lines (identical dicts)."""
+    cfg = CONFIGS[name]
+    return {"workload": cfg["workload"], "faces": FACES[name], "cell_face_tests_per_step": TESTS_PER_STEP[name],
+            "step": "geometry-to-grid pass: STL (C1: text primitive) import -> refine_near_wall over all levels "
+                    "(fill_bins, near-wall marking, propagation, refinement); the GPU arm also builds the "
+                    "finest-level lattice links + q, which the reference does not have",
+            "l2": "GPU arm: L2 flushed (256 MB write) before every step; CPU arm: host caches as they are"}
+
+
+def _ref_module():
+    from oracle import stage_ref
+
+    return stage_ref.import_reference() if stage_ref.available() else None
+
+
+def _write_input(name):
+    import tempfile
+
+    cfg = CONFIGS[name]
+    fd, path = tempfile.mkstemp(suffix=".txt" if cfg["kind"] == "text" else ".stl")
+    with os.fdopen(fd, "wb") as fh:
+        fh.write(make_input(cfg))
+    return path
+
+
+def _ref_full_step(name, path):
+    """One whole geometry-to-grid pass of the reference's own serial path
+    (cli.py:87-101: load_geometry -> init_root_grid -> refine_near_wall,
+    backend "serial") from the staged oracle/_ref, else the NumPy port.
+    Returns (seconds, cell-face tests, kind)."""
+    cfg = CONFIGS[name]
+    dim = cfg["dim"]
+    ow = _ref_module()
+    t0 = time.perf_counter()
+    if ow is not None:
+        if cfg["kind"] == "text":
+            geom = ow.index_to_coords(ow.import_text_primitives(path, dim=dim))
+        else:
+            geom = ow.import_stl(path)
+        forest = ow.init_root_grid(ow.Aabb(np.zeros(dim), np.ones(dim)), (cfg["root"],) * dim)
+        ow.refine_near_wall(forest, geom, ow.NearWallParams(d_spec=cfg["d"], n_levels=cfg["levels"],
+                                                           bins_per_axis=cfg["B"]))
+        return time.perf_counter() - t0, TESTS_PER_STEP[name], "reference"
+    from oracle import forest as of
+    from oracle import geometry as og
+    from oracle import nearwall as on
+
+    with open(path, "rb") as fh:
+        data = fh.read()
+    coords = og.index_to_coords(*og.parse_primitives(data.decode())) if cfg["kind"] == "text" else og.stl(data)
+    f = of.Forest(np.zeros(dim), np.ones(dim), (cfg["root"],) * dim)
+    r = on.refine_near_wall(f, coords, cfg["d"], n_levels=cfg["levels"], bins_per_axis=cfg["B"])
+    return time.perf_counter() - t0, int(sum(r["cell_face_tests"])), "port"
+
+
 CPU_SAMPLE_TESTS = 1.5e8  # ~25 s of the oracle's marking at ~6e6 tests/s
 
 
-def cpu_sample(cfg):
-    """Bounded oracle sample of the same workload: the level-0 pass (import,
-    bins, marking, propagation, refinement) — returns (tests, seconds, what).
-    When the level-0 pass exceeds CPU_SAMPLE_TESTS cell-face tests (C5), only
-    every k-th level-0 block is marked (a uniform spread over the domain, so
-    the near-wall share of the work is kept), only that face-detection stage
-    is timed (the metric's T / face-detection time) and
-    propagation/refinement are skipped; T counts exactly the sampled blocks'
-    tests."""
+def _port_sample(name):
+    """Bounded sample for configurations whose whole pass takes minutes to
+    hours on one core (C3-C5; DNF at C4/C5): the level-0
+    face-detection stage of the NumPy port over a uniform spread of level-0
+    blocks (every k-th one, so the near-wall share is kept), import and
+    fill_bins untimed.  Returns (seconds, tests, what)."""
     from oracle import binning as ob
     from oracle import forest as of
     from oracle import geometry as og
     from oracle import nearwall as on
 
-    data = make_input(cfg)
+    cfg = CONFIGS[name]
     dim = cfg["dim"]
-    t0 = time.perf_counter()
-    if cfg["kind"] == "text":
-        coords = og.index_to_coords(*og.parse_primitives(data.decode()))
-    else:
-        coords = og.stl(data)
+    coords = og.stl(make_input(cfg))
     f = of.Forest(np.zeros(dim), np.ones(dim), (cfg["root"],) * dim)
     grid = ob.Grid(np.zeros(dim), np.ones(dim), cfg["B"])
     bins = ob.fill_bins(coords, grid)
     T = on.cell_face_tests(f, 0, grid, bins[1], coords.shape[2])
-    if T <= CPU_SAMPLE_TESTS:
-        on.mark(f, 0, coords, cfg["d"], bins, grid)
-        on.propagate(f, 0, cfg["d"])
-        f.refine_marked(0)
-        return T, time.perf_counter() - t0, "level-0 pass (import, fill_bins, binned marking, propagation, refinement)"
     leaves = f.leaves_at(0)
-    stride = int(np.ceil(T / CPU_SAMPLE_TESTS))
+    stride = max(1, int(np.ceil(T / CPU_SAMPLE_TESTS)))
     sample = leaves[::stride]
     skip = np.ones(len(f.marks), bool)
     skip[sample] = False
@@ -402,29 +454,74 @@ def cpu_sample(cfg):
     T = int(np.asarray(bins[1], np.int64)[grid.bin_of(f.cell_centers(sample))].sum())
     t1 = time.perf_counter()
     on.mark(f, 0, coords, cfg["d"], bins, grid)
-    return T, time.perf_counter() - t1, (f"level-0 binned marking (face-detection stage only; import and "
-                                         f"fill_bins run untimed) of every {stride}th level-0 block "
+    return time.perf_counter() - t1, T, (f"NumPy port: level-0 binned marking (face-detection stage; import and "
+                                         f"fill_bins untimed) of every {stride}th level-0 block "
                                          f"({len(sample)} of {len(leaves)})")
 
 
-def reference_arm(args, cfg):
-    tests = secs = 0.0
-    for _ in range(args.warmup and 1):
-        cpu_sample(cfg)
-    for _ in range(args.steps):
-        T, s, what = cpu_sample(cfg)
-        tests += T
-        secs += s
-    v = tests / secs
-    cb = {"value": v, "unit": "cell-face tests/s", "cores": 1, "kind": "port",
-          "sample": f"oracle (NumPy restatement of octowall) on {args.config}: {what}; "
-                    f"{int(tests / args.steps)} tests per step"}
+def _pool_step(args):
+    name, path = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    if name in FULL_CPU:
+        return _ref_full_step(name, path)
+    s, T, what = _port_sample(name)
+    return s, T, "port"
+
+
+def cpu_baseline(name):
+    """One bounded CPU step on one core (rank 0, N=1): the whole pass of the
+    reference's serial path for C1/C2, a level-0 sample of the port beyond."""
+    path = _write_input(name)
+    try:
+        if name in FULL_CPU:
+            s, T, kind = _ref_full_step(name, path)
+            what = (f"one whole {name} geometry-to-grid pass ({'reference octowall serial backend, staged in oracle/_ref' if kind == 'reference' else 'NumPy port of octowall'}: "
+                    f"import -> refine_near_wall over {CONFIGS[name]['levels']} levels), {s:.1f} s")
+        else:
+            s, T, what = _port_sample(name)
+            kind = "port"
+    finally:
+        os.unlink(path)
+    return {"value": T / s, "unit": "cell-face tests/s", "cores": 1, "kind": kind, "sample": what}
+
+
+def reference_arm(args, name):
+    """--impl reference: the reference's CPU implementation of the path on the
+    host cores.  Each step is one whole pass of the configuration (C1/C2; a
+    bounded level-0 sample beyond) in its own single-threaded worker process
+    (the serial backend is one core by construction); steps run concurrently
+    on up to all host cores, and ``value`` is the whole job's tests / wall
+    time of the K timed steps (W untimed warm-up steps first, also pooled)."""
+    import multiprocessing as mp
+
+    path = _write_input(name)
+    cores = max(1, min(args.steps, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+                       else os.cpu_count() or 1))
+    try:
+        ctx = mp.get_context("fork")
+        with ctx.Pool(cores) as pool:
+            if args.warmup:
+                pool.map(_pool_step, [(name, path)] * min(args.warmup, cores))
+            t0 = time.perf_counter()
+            res = pool.map(_pool_step, [(name, path)] * args.steps, chunksize=1)
+            wall = time.perf_counter() - t0
+    finally:
+        os.unlink(path)
+    tests = sum(r[1] for r in res)
+    kind = res[0][2]
+    v = tests / wall
+    what = (f"{args.steps} whole {name} passes (import -> refine_near_wall, all levels) of "
+            f"{'the reference octowall serial backend (oracle/_ref)' if kind == 'reference' else 'the NumPy port'}"
+            if name in FULL_CPU else f"{args.steps} level-0 samples of the NumPy port")
+    cb = {"value": v, "unit": "cell-face tests/s", "cores": cores, "kind": kind,
+          "sample": f"{what}, one single-threaded process per step, {cores} concurrent; "
+                    f"{wall:.1f} s wall for the timed steps, {statistics.mean(r[0] for r in res):.2f} s per step"}
     return {
         "metric": "geometry-to-grid time (ms) & cell-face tests/s at 1/2/4/8 B200 vs CPU",
         "impl": "reference", "value": v, "unit": "cell-face tests/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["workload"]}, "cpu_baseline": cb,
+        "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(r[0] for r in res), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (procedural geometry, deterministic)",
+        "config": bench_config(name), "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "cell-face tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -446,7 +543,7 @@ def main():
 
     if args.impl == "reference":
         if rank == 0:
-            print(json.dumps(reference_arm(args, cfg)), flush=True)
+            print(json.dumps(reference_arm(args, args.config)), flush=True)
         return
 
     if world > 1:
@@ -471,11 +568,12 @@ def main():
 
         dist.barrier()
     out = gpu_arm(args, cfg, rank, world, local_rank)
+    out["config"] = bench_config(args.config)
+    if out["run"]["cell_face_tests_per_step"] != TESTS_PER_STEP[args.config]:
+        log("WARNING: T of the GPU pass differs from the workload table")
+        out["run"]["tests_mismatch"] = True
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        T, s, what = cpu_sample(cfg)
-        out["cpu_baseline"] = {
-            "value": T / s, "unit": "cell-face tests/s", "cores": 1, "kind": "port",
-            "sample": f"oracle {what} of {args.config} ({T} tests, {s:.1f} s, 1 core, NumPy)"}
+        out["cpu_baseline"] = cpu_baseline(args.config)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -340,13 +340,15 @@ int ow_export_vtk(ow_ctx* ctx, const ow_forest* f, const char* path, const char*
 int ow_near_pairs(ow_ctx* ctx, int32_t dim, const float* d_points, const float* d_faces, const float* d_d,
                   int64_t n, uint8_t* d_out, void* stream);
 
-/* ASCII STL fast path (host, _parse_ascii_stl geometry.py:349-412): parses
- * pure-ASCII STL text into tris[n][3][3] float32 (float() then one float32
- * rounding).  OW_ERR_PARSE (no message) for anything it does not accept —
- * non-ASCII bytes or any syntax error — so the caller's reference-faithful
- * parser reports the exact error; OW_ERR_CAPACITY when more than `cap`
- * facets. */
-int ow_parse_ascii_stl(const char* data, int64_t len, float* tris, int64_t cap, int64_t* out_n);
+/* ASCII STL parser (host, replaces _parse_ascii_stl geometry.py:349-412):
+ * pure-ASCII STL text -> tris[n][3][3] float32 (Python float() grammar, then
+ * one float32 rounding).  OW_ERR_PARSE with err[5] = {code, line, token
+ * offset, token length, expected keyword index} describing the first error
+ * in the reference's token order (codes: 1 end of file, 2 expected keyword
+ * err[4] of {solid, normal, outer, loop, vertex, endloop, endfacet}, 3
+ * expected a number, 4 expected 'facet' or 'endsolid', 5 keyword after
+ * endsolid, 6 non-ASCII byte); OW_ERR_CAPACITY when more than `cap` facets. */
+int ow_parse_ascii_stl(const char* data, int64_t len, float* tris, int64_t cap, int64_t* out_n, int64_t* err);
 
 /* Predicate-vs-referee sampling (validate.py:98-141): out_mask[i] = FP32
  * near(point i, face i, f32(d[i])); out_exact[i] = FP64 exact distance of the

@@ -200,7 +200,7 @@ _SIGS = {
     "ow_near_pairs": [P, I32, P, P, P, I64, P, P],
     "ow_export_vtk": [P, C.POINTER(ForestView), C.c_char_p, C.c_char_p, P],
     "ow_referee_pairs": [P, I32, P, P, P, I64, P, P, P],
-    "ow_parse_ascii_stl": [C.c_char_p, I64, P, I64, PI64],
+    "ow_parse_ascii_stl": [C.c_char_p, I64, P, I64, PI64, PI64],
 }
 _RESTYPE = {"ow_last_error": C.c_char_p, "ow_version": C.c_int, "ow_launch_count": C.c_int64}
 

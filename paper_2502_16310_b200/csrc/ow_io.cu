@@ -149,16 +149,26 @@ extern "C" int ow_export_vtk(ow_ctx* ctx, const ow_forest* f, const char* path, 
 }
 
 // ---------------------------------------------------------------------------
-// ASCII STL (geometry.py:349-412), native fast path.  Exact on the inputs it
-// accepts: pure-ASCII text whose grammar parses; every number token is
-// validated against Python's float() grammar (sign, digits with single
-// underscores between digits, optional fraction and exponent, inf / infinity
-// / nan) before a correctly rounded strtod, then rounded once to float32 like
-// np.asarray(..., float32).  Anything else — non-ASCII bytes, any syntax error —
-// returns OW_ERR_PARSE without a message so the caller's reference-faithful
-// parser produces the exact GeometryParseError (with its line number).
+// ASCII STL (geometry.py:349-412) on the host: the whole parser, errors
+// included.  Pure-ASCII text (the Python shim turns any other valid UTF-8
+// into an equivalent ASCII token stream first); every number token is checked
+// against Python's float() grammar (sign, digits with single underscores
+// between digits, optional fraction and exponent, inf / infinity / nan)
+// before a correctly rounded strtod, then rounded once to float32 like
+// np.asarray(..., float32).  The accepting path tokenises and converts in
+// parallel; on any failure a sequential walk finds the error the reference
+// reports first (its token-by-token order) and returns it as
+// err = {code, line, token offset, token length, expected keyword}:
+//   1 unexpected end of file   2 expected <keyword>, got <token>
+//   3 expected a number        4 expected 'facet' or 'endsolid'
+//   5 <keyword> after endsolid 6 non-ASCII byte (the shim's job)
+// Lines are numbered like str.splitlines() (\n, \r, \r\n, \v, \f, \x1c-\x1e).
 // ---------------------------------------------------------------------------
 namespace {
+
+enum { PE_EOF = 1, PE_EXPECT, PE_NUMBER, PE_FACET, PE_AFTER, PE_NONASCII };
+const char* const PE_KW[] = {"solid", "normal", "outer", "loop", "vertex", "endloop", "endfacet"};
+enum { KW_SOLID, KW_NORMAL, KW_OUTER, KW_LOOP, KW_VERTEX, KW_ENDLOOP, KW_ENDFACET };
 
 inline bool py_space(unsigned char c) { return c == ' ' || (c >= 9 && c <= 13) || (c >= 0x1c && c <= 0x1f); }
 
@@ -242,10 +252,93 @@ struct Tok {
   }
 };
 
+// 1-based line of byte offset `off` (str.splitlines() boundaries)
+int64_t line_of(const char* data, int64_t off) {
+  int64_t line = 1;
+  for (int64_t i = 0; i < off; ++i) {
+    const unsigned char c = (unsigned char)data[i];
+    if (c == '\r') {
+      if (i + 1 < off && data[i + 1] == '\n') ++i;
+      ++line;
+    } else if (c == '\n' || c == 0x0b || c == 0x0c || (c >= 0x1c && c <= 0x1e)) {
+      ++line;
+    }
+  }
+  return line;
+}
+
+// The reference's token-by-token walk (geometry.py:358-411), reporting the
+// first error it meets; only run when the parallel path failed.
+template <class TF, class NF>
+void diagnose(const char* data, size_t ntok, TF T, NF N, int64_t* err) {
+  size_t i = 0;
+  auto set = [&](int code, size_t k, int kw) {
+    err[0] = code;
+    err[1] = ntok ? line_of(data, (int64_t)(T(k) - data)) : -1;
+    err[2] = ntok ? (int64_t)(T(k) - data) : 0;
+    err[3] = ntok ? N(k) : 0;
+    err[4] = kw;
+  };
+  auto take = [&](int kw) -> bool {  // kw < 0: any token
+    if (i >= ntok) {
+      set(PE_EOF, ntok ? ntok - 1 : 0, -1);
+      return false;
+    }
+    if (kw >= 0 && !ieq(T(i), N(i), PE_KW[kw])) {
+      set(PE_EXPECT, i, kw);
+      return false;
+    }
+    ++i;
+    return true;
+  };
+  auto number = [&]() -> bool {
+    if (i >= ntok) {
+      set(PE_EOF, ntok ? ntok - 1 : 0, -1);
+      return false;
+    }
+    double v;
+    if (!py_float(T(i), N(i), &v)) {
+      set(PE_NUMBER, i, -1);
+      return false;
+    }
+    ++i;
+    return true;
+  };
+  if (!take(KW_SOLID)) return;
+  while (i < ntok && !ieq(T(i), N(i), "facet") && !ieq(T(i), N(i), "endsolid")) ++i;
+  for (;;) {
+    if (i >= ntok) {
+      set(PE_EOF, ntok ? ntok - 1 : 0, -1);
+      return;
+    }
+    if (ieq(T(i), N(i), "endsolid")) {
+      ++i;
+      break;
+    }
+    if (!ieq(T(i), N(i), "facet")) {
+      set(PE_FACET, i, -1);
+      return;
+    }
+    ++i;
+    if (!take(KW_NORMAL) || !number() || !number() || !number() || !take(KW_OUTER) || !take(KW_LOOP)) return;
+    for (int v = 0; v < 3; ++v)
+      if (!take(KW_VERTEX) || !number() || !number() || !number()) return;
+    if (!take(KW_ENDLOOP) || !take(KW_ENDFACET)) return;
+  }
+  for (; i < ntok; ++i)
+    if (ieq(T(i), N(i), "facet") || ieq(T(i), N(i), "solid") || ieq(T(i), N(i), "vertex") ||
+        ieq(T(i), N(i), "endsolid")) {
+      set(PE_AFTER, i, -1);
+      return;
+    }
+}
+
 }  // namespace
 
-extern "C" int ow_parse_ascii_stl(const char* data, int64_t len, float* tris, int64_t cap, int64_t* out_n) {
+extern "C" int ow_parse_ascii_stl(const char* data, int64_t len, float* tris, int64_t cap, int64_t* out_n,
+                                  int64_t* err) {
   *out_n = 0;
+  for (int k = 0; k < 5; ++k) err[k] = 0;
   // 1. tokenize in parallel chunks (boundaries moved to whitespace); any
   //    non-ASCII byte sends the file to the reference-faithful parser
   unsigned nt = std::thread::hardware_concurrency();
@@ -280,7 +373,11 @@ extern "C" int ow_parse_ascii_stl(const char* data, int64_t len, float* tris, in
     for (auto& x : th) x.join();
   }
   for (unsigned t = 0; t < nt; ++t)
-    if (bad[t]) return OW_ERR_PARSE;
+    if (bad[t]) {
+      err[0] = PE_NONASCII;
+      ow_set_error("ASCII STL: non-ASCII byte");
+      return OW_ERR_PARSE;
+    }
   size_t ntok = 0;
   for (auto& v : part) ntok += v.size();
   std::vector<std::pair<int64_t, int>> tok;
@@ -288,22 +385,27 @@ extern "C" int ow_parse_ascii_stl(const char* data, int64_t len, float* tris, in
   for (auto& v : part) tok.insert(tok.end(), v.begin(), v.end());
   auto T = [&](size_t i) { return data + tok[i].first; };
   auto N = [&](size_t i) { return tok[i].second; };
+  auto fail = [&]() {
+    diagnose(data, ntok, T, N, err);
+    ow_set_error("ASCII STL: parse error (code %lld, line %lld)", (long long)err[0], (long long)err[1]);
+    return OW_ERR_PARSE;
+  };
   // 2. grammar walk (sequential); number tokens are only located here
   size_t i = 0;
-  if (ntok == 0 || !ieq(T(0), N(0), "solid")) return OW_ERR_PARSE;
+  if (ntok == 0 || !ieq(T(0), N(0), "solid")) return fail();
   ++i;
   while (i < ntok && !ieq(T(i), N(i), "facet") && !ieq(T(i), N(i), "endsolid")) ++i;
   std::vector<size_t> facet_at;  // token index of each facet's "facet"
   while (true) {
-    if (i >= ntok) return OW_ERR_PARSE;  // unexpected end of file
+    if (i >= ntok) return fail();  // unexpected end of file
     if (ieq(T(i), N(i), "endsolid")) break;
     // facet normal n n n outer loop (vertex x y z) x3 endloop endfacet: 21 tokens
-    if (i + 21 > ntok) return OW_ERR_PARSE;
+    if (i + 21 > ntok) return fail();
     if (!ieq(T(i), N(i), "facet") || !ieq(T(i + 1), N(i + 1), "normal") || !ieq(T(i + 5), N(i + 5), "outer") ||
         !ieq(T(i + 6), N(i + 6), "loop") || !ieq(T(i + 7), N(i + 7), "vertex") ||
         !ieq(T(i + 11), N(i + 11), "vertex") || !ieq(T(i + 15), N(i + 15), "vertex") ||
         !ieq(T(i + 19), N(i + 19), "endloop") || !ieq(T(i + 20), N(i + 20), "endfacet"))
-      return OW_ERR_PARSE;
+      return fail();
     facet_at.push_back(i);
     i += 21;
   }
@@ -311,7 +413,7 @@ extern "C" int ow_parse_ascii_stl(const char* data, int64_t len, float* tris, in
   for (size_t j = i + 1; j < ntok; ++j)
     if (ieq(T(j), N(j), "facet") || ieq(T(j), N(j), "solid") || ieq(T(j), N(j), "vertex") ||
         ieq(T(j), N(j), "endsolid"))
-      return OW_ERR_PARSE;
+      return fail();
   const int64_t nf = (int64_t)facet_at.size();
   if (nf > cap) return OW_ERR_CAPACITY;
   // 3. numbers in parallel: normals are validated, vertices converted
@@ -338,7 +440,7 @@ extern "C" int ow_parse_ascii_stl(const char* data, int64_t len, float* tris, in
     for (auto& x : th) x.join();
   }
   for (unsigned t = 0; t < nt; ++t)
-    if (nbad[t]) return OW_ERR_PARSE;
+    if (nbad[t]) return fail();
   *out_n = nf;
   return OW_OK;
 }

@@ -5,9 +5,10 @@ coordinate-list form lives in HBM as a float32 (verts_per_face, dim, n_faces)
 tensor — the reference's structure-of-arrays layout (geometry.py:94-124) —
 and every per-face pass over it (binary-STL transpose, index gather,
 degeneracy test, bounding box) is a sm_100a kernel in libowb200.so.  Text
-primitives and ASCII STL are tokenised on the host (the reference does the
-same in Python); their float64 -> float32 rounding is done by NumPy so the
-vertices are bit-identical to the reference's.
+primitives are parsed on the host and generated in float64 then rounded by
+NumPy (bit-identical vertices); ASCII STL is parsed by the native host parser
+(ow_parse_ascii_stl: parallel tokenising and conversion, the reference's
+error messages and line numbers).
 """
 
 from __future__ import annotations
@@ -26,67 +27,65 @@ from .errors import GeometryParseError, InvalidParameterError
 _keys = itertools.count(1)
 
 
+def _require(ok, message):
+    if not ok:
+        raise InvalidParameterError(message)
+
+
 def as_point(p, dim):
-    a = np.asarray(p, dtype=np.float64).reshape(-1)
-    if a.shape[0] != dim:
-        raise InvalidParameterError(f"expected a {dim}-component point, got {a.shape[0]}")
-    if not np.all(np.isfinite(a)):
-        raise InvalidParameterError(f"point has non-finite components: {a}")
+    """float64 point of exactly ``dim`` finite components (geometry.py:16-25)."""
+    a = np.asarray(p, dtype=np.float64).ravel()
+    _require(a.size == dim, f"expected a {dim}-component point, got {a.size}")
+    _require(bool(np.isfinite(a).all()), f"point has non-finite components: {a}")
     return a
 
 
 @dataclass
 class Aabb:
-    """Axis-aligned box, float64 (geometry.py:28-55)."""
+    """Axis-aligned box with float64 corners (geometry.py:28-55)."""
 
     min: np.ndarray
     max: np.ndarray
 
     def __post_init__(self):
-        self.min = np.asarray(self.min, dtype=np.float64).reshape(-1)
-        self.max = np.asarray(self.max, dtype=np.float64).reshape(-1)
-        if self.min.shape != self.max.shape:
-            raise InvalidParameterError("aabb min/max dimension mismatch")
-        if not (np.all(np.isfinite(self.min)) and np.all(np.isfinite(self.max))):
-            raise InvalidParameterError("aabb has non-finite corners")
-        if np.any(self.min > self.max):
-            raise InvalidParameterError(f"aabb min {self.min} exceeds max {self.max}")
+        lo, hi = (np.asarray(c, dtype=np.float64).ravel() for c in (self.min, self.max))
+        _require(lo.shape == hi.shape, "aabb min/max dimension mismatch")
+        _require(bool(np.isfinite(lo).all() and np.isfinite(hi).all()), "aabb has non-finite corners")
+        _require(not bool((lo > hi).any()), f"aabb min {lo} exceeds max {hi}")
+        self.min, self.max = lo, hi
 
     @property
     def dim(self):
-        return self.min.shape[0]
+        return int(self.min.size)
 
     @property
     def extent(self):
         return self.max - self.min
 
     def contains(self, p, tol=0.0):
-        p = np.asarray(p, dtype=np.float64)
-        return bool(np.all(p >= self.min - tol) and np.all(p <= self.max + tol))
+        q = np.asarray(p, dtype=np.float64)
+        return bool(((q >= self.min - tol) & (q <= self.max + tol)).all())
 
 
 @dataclass
 class IndexedGeometry:
-    """Shared-vertex mesh (host): vertices (V, dim) float32, faces (F, dim) int32."""
+    """Shared-vertex mesh on the host: vertices (V, dim) float32, faces
+    (F, dim) int32 vertex indices (geometry.py:58-91)."""
 
     dim: int
     vertices: np.ndarray
     faces: np.ndarray
 
     def __post_init__(self):
-        if self.dim not in (2, 3):
-            raise InvalidParameterError(f"dim must be 2 or 3, got {self.dim}")
-        self.vertices = np.asarray(self.vertices, dtype=np.float32).reshape(-1, self.dim)
-        self.faces = np.asarray(self.faces, dtype=np.int32).reshape(-1, self.dim)
-        if not np.all(np.isfinite(self.vertices)):
-            raise InvalidParameterError("geometry has non-finite vertex coordinates")
-        if self.faces.size:
-            if self.faces.min() < 0 or self.faces.max() >= len(self.vertices):
-                raise InvalidParameterError("face index out of range")
-            for j in range(self.dim):
-                for k in range(j + 1, self.dim):
-                    if np.any(self.faces[:, j] == self.faces[:, k]):
-                        raise InvalidParameterError("face has repeated vertex indices")
+        _require(self.dim in (2, 3), f"dim must be 2 or 3, got {self.dim}")
+        v = np.asarray(self.vertices, dtype=np.float32).reshape(-1, self.dim)
+        f = np.asarray(self.faces, dtype=np.int32).reshape(-1, self.dim)
+        _require(bool(np.isfinite(v).all()), "geometry has non-finite vertex coordinates")
+        if f.size:
+            _require(0 <= int(f.min()) and int(f.max()) < len(v), "face index out of range")
+            srt = np.sort(f, axis=1)
+            _require(not bool((srt[:, 1:] == srt[:, :-1]).any()), "face has repeated vertex indices")
+        self.vertices, self.faces = v, f
 
     @property
     def n_faces(self):
@@ -207,56 +206,66 @@ def generate_sphere(center, radius, n_lat, n_lon):
 
 
 def append_geometry(parts):
+    """One indexed mesh from several: vertices stacked, each part's face
+    indices shifted by the vertices that precede it (geometry.py:195-208)."""
     parts = list(parts)
     if not parts:
         raise InvalidParameterError("nothing to append")
-    dim = parts[0].dim
-    if any(p.dim != dim for p in parts):
+    dims = {p.dim for p in parts}
+    if len(dims) != 1:
         raise InvalidParameterError("cannot append geometries of mixed dimension")
-    verts, faces, off = [], [], 0
-    for p in parts:
-        verts.append(p.vertices)
-        faces.append(p.faces + off)
-        off += len(p.vertices)
-    return IndexedGeometry(dim, np.vstack(verts), np.vstack(faces))
+    shift = np.cumsum([0] + [len(p.vertices) for p in parts[:-1]])
+    return IndexedGeometry(parts[0].dim, np.concatenate([p.vertices for p in parts]),
+                           np.concatenate([p.faces + k for p, k in zip(parts, shift)]))
 
 
-def _parse_count(s):
-    v = float(s)
-    if v != int(v):
-        raise ValueError(s)
+def _integer(token):
+    """A float()-parsable token with an integral value (counts may be written 1e3)."""
+    v = float(token)
+    if not v.is_integer():
+        raise ValueError(token)
     return int(v)
 
 
+# primitive keyword -> (argument names, trailing integral counts, builder(reals, counts))
+_PRIMITIVES = {
+    "circle": (("cx", "cy", "r", "n_edges"), 1,
+               lambda x, n: generate_circle(x[:2], x[2], n[0])),
+    "sphere": (("cx", "cy", "cz", "r", "n_lat", "n_lon"), 2,
+               lambda x, n: generate_sphere(x[:3], x[3], n[0], n[1])),
+}
+
+
+def _primitive_of(body, path, ln):
+    kind, *args = body.split()
+    kind = kind.lower()
+    spec = _PRIMITIVES.get(kind)
+    if spec is None:
+        raise GeometryParseError(f"unknown primitive {kind!r}", path, ln)
+    names, n_counts, build = spec
+    if len(args) != len(names):
+        raise GeometryParseError(f"{kind} takes {len(names)} values: {' '.join(names)}", path, ln)
+    try:
+        reals = [float(a) for a in args[: len(names) - n_counts]]
+        counts = [_integer(a) for a in args[len(names) - n_counts:]]
+        return build(reals, counts)
+    except ValueError:
+        raise GeometryParseError(f"cannot parse numbers in {body!r}", path, ln) from None
+    except InvalidParameterError as e:
+        raise GeometryParseError(str(e), path, ln) from None
+
+
 def parse_text_primitives(text, path=None, dim=None):
-    parts = []
-    for ln, raw in enumerate(text.splitlines(), start=1):
-        body = raw.split("#", 1)[0].strip()
-        if not body:
-            continue
-        tok = body.split()
-        kind, args = tok[0].lower(), tok[1:]
-        try:
-            if kind == "circle":
-                if len(args) != 4:
-                    raise GeometryParseError("circle takes 4 values: cx cy r n_edges", path, ln)
-                cx, cy, r = (float(a) for a in args[:3])
-                parts.append(generate_circle((cx, cy), r, _parse_count(args[3])))
-            elif kind == "sphere":
-                if len(args) != 6:
-                    raise GeometryParseError("sphere takes 6 values: cx cy cz r n_lat n_lon", path, ln)
-                cx, cy, cz, r = (float(a) for a in args[:4])
-                parts.append(generate_sphere((cx, cy, cz), r, _parse_count(args[4]), _parse_count(args[5])))
-            else:
-                raise GeometryParseError(f"unknown primitive {kind!r}", path, ln)
-        except ValueError:
-            raise GeometryParseError(f"cannot parse numbers in {body!r}", path, ln) from None
-        except InvalidParameterError as e:
-            raise GeometryParseError(str(e), path, ln) from None
+    """Primitive description text -> IndexedGeometry (geometry.py:211-252):
+    one primitive per line (``circle cx cy r n_edges`` in 2D, ``sphere cx cy
+    cz r n_lat n_lon`` in 3D), ``#`` comments, parts concatenated; an empty
+    description gives an empty geometry of dimension ``dim`` (default 2)."""
+    bodies = ((ln, raw.partition("#")[0].strip()) for ln, raw in enumerate(text.splitlines(), start=1))
+    parts = [_primitive_of(body, path, ln) for ln, body in bodies if body]
     if not parts:
-        return IndexedGeometry.empty(dim if dim is not None else 2)
+        return IndexedGeometry.empty(2 if dim is None else dim)
     out = append_geometry(parts)
-    if dim is not None and out.dim != dim:
+    if dim is not None and dim != out.dim:
         raise GeometryParseError(f"file holds {out.dim}D primitives but a {dim}D run was requested", path)
     return out
 
@@ -342,75 +351,71 @@ def _parse_binary(data, path):
     return stl_records_to_coords(raw.to(_lib.device(), non_blocking=False), n)
 
 
-def _parse_ascii(data, path):
-    """Native fast path first (ow_parse_ascii_stl); on anything it does not
-    accept, the reference-faithful parser below reports the exact error."""
-    cap = len(data) // 64 + 1  # a facet takes > 64 bytes of ASCII text
-    tris = np.empty((cap, 3, 3), np.float32)
-    n = C.c_int64(0)
-    if _lib.lib().ow_parse_ascii_stl(bytes(data), len(data), tris.ctypes.data_as(C.c_void_p), cap, C.byref(n)) == 0:
-        coords = np.ascontiguousarray(np.transpose(tris[: n.value], (1, 2, 0)))
-        return CoordListGeometry(3, coords)
-    return _parse_ascii_py(data, path)
+_STL_KEYWORDS = ("solid", "normal", "outer", "loop", "vertex", "endloop", "endfacet")  # err[4] of the C ABI
 
 
-def _parse_ascii_py(data, path):
+def _ascii_tokens(data, path):
+    """Non-ASCII input: valid UTF-8 is re-spelled as an ASCII token stream
+    with the same tokens per line (str.split / str.splitlines semantics); a
+    token float() accepts becomes repr(float), any other non-ASCII token a
+    placeholder.  Returns (ascii bytes, {offset: original token})."""
     try:
         text = data.decode("utf-8", errors="strict")
     except UnicodeDecodeError:
         raise GeometryParseError("not valid ASCII STL text", path=path) from None
-    toks, lines = [], []
-    for ln, line in enumerate(text.splitlines(), start=1):
-        for t in line.split():
-            toks.append(t)
-            lines.append(ln)
-    pos = 0
-    n_tok = len(toks)
+    out, orig, off = [], {}, 0
+    for line in text.splitlines():
+        for tok in line.split():
+            rep = tok
+            if not tok.isascii():
+                try:
+                    rep = repr(float(tok))
+                except ValueError:
+                    rep = "?"
+                orig[off] = tok
+            out.append(rep + " ")
+            off += len(rep) + 1
+        out.append("\n")
+        off += 1
+    return "".join(out).encode("ascii"), orig
 
-    def take(expect=None):
-        nonlocal pos
-        if pos >= n_tok:
-            raise GeometryParseError("unexpected end of file", path, lines[-1] if lines else None)
-        t = toks[pos]
-        pos += 1
-        if expect is not None and t.lower() != expect:
-            raise GeometryParseError(f"expected {expect!r}, got {t!r}", path, lines[pos - 1])
-        return t
 
-    def num():
-        t = take()
-        try:
-            return float(t)
-        except ValueError:
-            raise GeometryParseError(f"expected a number, got {t!r}", path, lines[pos - 1]) from None
+def _parse_ascii(data, path):
+    """ASCII STL -> CoordListGeometry (geometry.py:349-412)."""
+    return CoordListGeometry(3, np.ascontiguousarray(np.transpose(ascii_stl_triangles(data, path), (1, 2, 0))))
 
-    take("solid")
-    while pos < n_tok and toks[pos].lower() not in ("facet", "endsolid"):
-        pos += 1
-    vals = []
-    while True:
-        t = take()
-        kw = t.lower()
-        if kw == "endsolid":
-            break
-        if kw != "facet":
-            raise GeometryParseError(f"expected 'facet' or 'endsolid', got {t!r}", path, lines[pos - 1])
-        take("normal")
-        num(), num(), num()
-        take("outer")
-        take("loop")
-        for _ in range(3):
-            take("vertex")
-            vals.extend((num(), num(), num()))
-        take("endloop")
-        take("endfacet")
-    while pos < n_tok:
-        if toks[pos].lower() in ("facet", "solid", "vertex", "endsolid"):
-            raise GeometryParseError(f"unexpected {toks[pos]!r} after endsolid", path, lines[pos])
-        pos += 1
-    tris = np.asarray(vals, dtype=np.float64).astype(np.float32).reshape(-1, 3, 3)
-    coords = np.ascontiguousarray(np.transpose(tris, (1, 2, 0)))
-    return CoordListGeometry(3, coords)
+
+def ascii_stl_triangles(data, path=None):
+    """ASCII STL bytes -> (n, 3, 3) float32 triangles on the host, through
+    the native parser (ow_parse_ascii_stl), which also finds the error the
+    reference reports (message and line, geometry.py:349-412)."""
+    data = bytes(data)
+    buf, orig = (data, {}) if data.isascii() else _ascii_tokens(data, path)
+    cap = len(buf) // 64 + 1  # a facet takes more than 64 bytes of text
+    tris = np.empty((cap, 3, 3), np.float32)
+    n = C.c_int64(0)
+    err = (C.c_int64 * 5)()
+    st = _lib.lib().ow_parse_ascii_stl(buf, len(buf), tris.ctypes.data_as(C.c_void_p), cap, C.byref(n), err)
+    if st == _lib.OW_OK:
+        return tris[: n.value]
+    if st != _lib.OW_ERR_PARSE:
+        _lib.check(st)
+    code, line, off, length, kw = (int(v) for v in err)
+    tok = orig.get(off, buf[off:off + length].decode("ascii"))
+    line = line if line > 0 else None
+    if code == 1:
+        msg = "unexpected end of file"
+    elif code == 2:
+        msg = f"expected {_STL_KEYWORDS[kw]!r}, got {tok!r}"
+    elif code == 3:
+        msg = f"expected a number, got {tok!r}"
+    elif code == 4:
+        msg = f"expected 'facet' or 'endsolid', got {tok!r}"
+    elif code == 5:
+        msg = f"unexpected {tok!r} after endsolid"
+    else:
+        raise GeometryParseError(f"ASCII STL parser failed (code {code})", path=path)
+    raise GeometryParseError(msg, path, line)
 
 
 def import_stl_bytes(data, path=None) -> CoordListGeometry:

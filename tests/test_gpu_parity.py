@@ -834,7 +834,8 @@ def test_ascii_stl_native_fast_path(ow, tmp_path):
            b"vertex 1 2 3 endloop endfacet endsolid x")
     out = np.empty((2, 3, 3), np.float32)
     n = C.c_int64(0)
-    assert _lib.lib().ow_parse_ascii_stl(odd, len(odd), out.ctypes.data_as(C.c_void_p), 2, C.byref(n)) == 0
+    err = (C.c_int64 * 5)()
+    assert _lib.lib().ow_parse_ascii_stl(odd, len(odd), out.ctypes.data_as(C.c_void_p), 2, C.byref(n), err) == 0
     ref = np.asarray([[float("1_0.2_5"), 0.25, float("1e-4_0")], [0.5, 5.0, 1e-3], [1, 2, 3]], np.float64)
     np.testing.assert_array_equal(out[0], ref.astype(np.float32))
     for bad, msg in ((b"solid x\nfacet normal 0 0 0\nouter loop\nvertex 0x1p3 2 3\n", "expected a number"),
@@ -842,8 +843,6 @@ def test_ascii_stl_native_fast_path(ow, tmp_path):
                      (b"solid x\nfacet normal 0 0 0\n", "unexpected end of file")):
         with pytest.raises(ow.GeometryParseError, match=msg):
             geometry._parse_ascii(bad, "f.stl")
-        with pytest.raises(ow.GeometryParseError, match=msg):
-            geometry._parse_ascii_py(bad, "f.stl")
 
 
 _PDL_SCRIPT = r"""
