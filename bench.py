@@ -329,6 +329,27 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     dominant = lattice if sw_ms >= mark_ms else mark
     roofline = dict(dominant)
     roofline["secondary"] = mark if dominant is lattice else lattice
+    # HBM roofline of the binning family: per fill_bins call the
+    # algorithmic bytes are the coordinates read (4 D^2 F), the face ids
+    # written (4 E) and counts + offsets (8 B^D); the family's device time is
+    # the sample walk, the pair emission, the stable radix sort and the scans
+    # (events around the device work only, not the host readback between them)
+    bins_ms, bins_n = prof["fill_bins"]
+    n_bins = cfg["B"] ** dim
+    E = int(res.bins.ids.numel()) if res.bins is not None else 0
+    calls = max(1, bins_n // 2)  # (count, emit) brackets per call
+    bin_bytes = (4 * dim * dim * n_faces + 4 * E + 8 * n_bins) * calls
+    hbm_peak = float(peaks.get("hbm_gbs") or 6542.7)
+    achieved_gbs = bin_bytes / (bins_ms / 1e3) / 1e9 if bins_ms > 0 else 0.0
+    roofline["hbm"] = {
+        "kernel": "fill_bins family (k_count_fast, k_count_walk, k_emit_fast, k_radix_hist/k_radix_scatter, k_scan)",
+        "bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+        "frac": achieved_gbs / hbm_peak, "traffic": traffic.get("fill_bins"), "traffic_unit": "bytes/call",
+        "algorithmic": f"per call: 4*D^2*F coords read + 4*E ids + 8*B^D counts/offsets = {4 * dim * dim * n_faces} + "
+                       f"{4 * E} + {8 * n_bins} B (F={n_faces}, E={E}, B^D={n_bins}); {calls // args.steps} call(s) "
+                       f"per step",
+        "launches": bins_n, "avg_call_ms": bins_ms / calls,
+        "peak_note": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, read + write bytes)"}
     roofline["families_ms"] = {k: round(v[0] / args.steps, 4) for k, v in prof.items()}
     out = {
         "metric": "geometry-to-grid time (ms) & cell-face tests/s at 1/2/4/8 B200 vs CPU",

@@ -180,6 +180,24 @@ int ow_propagate_marks(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves,
  * over ranks.  Return 0 on success. */
 typedef int (*ow_exchange_fn)(void* user, int32_t level, const int32_t* d_leaves, int64_t n_leaves, int64_t lo,
                               int64_t hi, int64_t* stats3);
+/* Device-side exchange between the ranks of one node (ow_comm.cu): one
+ * symmetric device buffer per rank, mapped by the others through CUDA IPC;
+ * exchanges are stream-ordered put / get kernels over peer memory (no host
+ * round trip, no NCCL).  Collective setup: every rank calls ow_comm_create
+ * (which writes its 64-byte IPC handle), the handles are all-gathered by the
+ * caller (torch.distributed), then every rank calls ow_comm_open. */
+#define OW_COMM_MAX 8
+typedef struct ow_comm ow_comm;
+int ow_comm_create(int device, int32_t rank, int32_t world, int64_t area_bytes, ow_comm** out, void* handle64);
+int ow_comm_open(ow_comm* comm, const void* handles /* world x 64 bytes */);
+int ow_comm_destroy(ow_comm* comm);
+/* 1 when a peer missed an exchange's timeout (the exchange then gave up). */
+int ow_comm_status(ow_comm* comm, int64_t* out_error);
+/* All-gather of disjoint ranges: this rank's words [lo, hi) of the n words at
+ * d_data reach every rank; afterwards every rank's array is whole. */
+int ow_comm_allgather_u32(ow_ctx* ctx, ow_comm* comm, uint32_t* d_data, int64_t lo, int64_t hi, int64_t n,
+                          void* stream);
+
 typedef struct {
   float d_spec;           /* float32(d_spec): predicate distance */
   int32_t n_levels;       /* NearWallParams.n_levels */
@@ -193,6 +211,8 @@ typedef struct {
   int64_t bin_fraction;   /* B_f (only shapes the capacity-error message) */
   ow_exchange_fn exchange;
   void* exchange_user;
+  ow_comm* comm;          /* world > 1: device-side exchange (the level loop then runs with no
+                             host round trip; marking slices are balanced by per-leaf work) */
 } ow_nearwall_params;
 typedef struct {
   int32_t n_passes;

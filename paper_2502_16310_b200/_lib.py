@@ -94,6 +94,7 @@ class NearWallParamsC(C.Structure):  # ow_nearwall_params
         ("bin_fraction", C.c_int64),
         ("exchange", EXCHANGE_FN),
         ("exchange_user", C.c_void_p),
+        ("comm", C.c_void_p),
     ]
 
 
@@ -201,6 +202,11 @@ _SIGS = {
     "ow_export_vtk": [P, C.POINTER(ForestView), C.c_char_p, C.c_char_p, P],
     "ow_referee_pairs": [P, I32, P, P, P, I64, P, P, P],
     "ow_parse_ascii_stl": [C.c_char_p, I64, P, I64, PI64, PI64],
+    "ow_comm_create": [C.c_int, I32, I32, I64, C.POINTER(P), P],
+    "ow_comm_open": [P, P],
+    "ow_comm_destroy": [P],
+    "ow_comm_status": [P, PI64],
+    "ow_comm_allgather_u32": [P, P, P, I64, I64, I64, P],
 }
 _RESTYPE = {"ow_last_error": C.c_char_p, "ow_version": C.c_int, "ow_launch_count": C.c_int64}
 

@@ -437,6 +437,7 @@ int fill_count(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, 
   // count in one round trip; faces with too many bins for the bitmask path
   // (rare: large faces) add a second pass and a re-scan
   OW_TRY(scan(ctx, ow::LoadArr<int32_t>{(const int32_t*)pnb}, ow::StoreExcl<int32_t>{(int32_t*)pfo}, n, small + 5, s));
+  OW_PROF_END(ctx, PROF_BINS, s);  // (device work only: the readback below is host latency)
   int64_t r[6];
   if (ctx->faces_pending) {
     // fused pass: the face summary travels with this readback and is checked
@@ -461,12 +462,14 @@ int fill_count(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, 
     OW_TRY(ow_readback(ctx, small + 4, 1, hs, s));
     void* pb;
     OW_TRY(ow_slot(ctx, SLOT_BIN_BITMAP, 4 * (size_t)(hs[0] + 1), s, &pb));
+    OW_PROF_BEGIN(ctx, PROF_BINS, s);
     ow_launch(k_count_slow<D>, (unsigned)n_slow, 256, 0, s, g, c, n, h, (const int32_t*)psl, (const int64_t*)po,
                                                      (unsigned*)pb, (int32_t*)pnb, counts, small);
     OW_LAUNCHED(ctx);
     OW_CHECK_LAUNCH();
     OW_TRY(scan(ctx, ow::LoadArr<int32_t>{(const int32_t*)pnb}, ow::StoreExcl<int32_t>{(int32_t*)pfo}, n, small + 5,
                 s));
+    OW_PROF_END(ctx, PROF_BINS, s);
     OW_TRY(ow_readback(ctx, small, 6, r, s));
   }
   if (r[2]) {
@@ -539,10 +542,9 @@ extern "C" int ow_fill_bins_count(ow_ctx* ctx, const ow_grid* grid, const float*
     ow_set_error("fill_bins: too many bins (%lld)", (long long)n_bins);
     return OW_ERR_INVALID;
   }
-  OW_PROF_BEGIN(ctx, PROF_BINS, s);
+  OW_PROF_BEGIN(ctx, PROF_BINS, s);  // (ended inside fill_count before its readbacks)
   int st = grid->dim == 2 ? fill_count<2>(ctx, g, d_coords, n_faces, spacing, d_counts, n_bins, out_entries, out_outside, s)
                           : fill_count<3>(ctx, g, d_coords, n_faces, spacing, d_counts, n_bins, out_entries, out_outside, s);
-  OW_PROF_END(ctx, PROF_BINS, s);
   if (st != OW_OK) return st;
   ctx->bins_faces = n_faces;
   ctx->bins_entries = *out_entries;

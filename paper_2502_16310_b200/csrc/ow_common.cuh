@@ -87,6 +87,8 @@ enum ow_slot {
   SLOT_LAT_HOFFS,      // packed-q offsets per candidate block
   SLOT_LAT_RFLAGS,     // (cell id, flag word) per boundary row (packed host output)
   SLOT_LAT_QPACK,      // q of the set flag bits, row-major (packed host output)
+  SLOT_LAT_GRID,       // dense finest-level lattice -> leaf position
+  SLOT_DRV_SLICE,      // native driver, multi-GPU: per-leaf work prefix + slice bounds
   SLOT_MISC,
   SLOT_COUNT
 };
@@ -141,6 +143,8 @@ struct ow_ctx {
   int32_t lat_fpw;  // faces per warp of the face pass (0: chosen per call)  // mean largest face side when known (geometry_to_grid), else 0
   int64_t lat_pos_lo, lat_pos_hi;  // leaf-position slice of the last count call  // capacities of the single-pass row / unit lists
   int32_t lat_dirs, lat_level;
+  bool lat_grid_on;  // the last count call built the dense finest-lattice table
+  ow_comm* lat_comm;  // multi-GPU lattice stage: flags / q rows of the position slice exchanged
   int8_t lat_dir[27 * 3];
   const float* lat_coords;
   const int32_t* lat_leaves_ptr;
@@ -157,12 +161,35 @@ struct ow_ctx {
   int64_t drv_spec_nl;  // leaves of the deepest level compacted by the device-resident driver (-1: none)
 };
 
+// multi-GPU exchange over peer memory (ow_comm.cu)
+struct ow_comm {
+  int device, rank, world, open;
+  int64_t area_bytes;           // bytes of each of the two data areas
+  void* local;                  // this rank's symmetric buffer (header + 2 areas)
+  uint8_t* peer[OW_COMM_MAX];   // every rank's buffer mapped here (peer[rank] = local)
+  int64_t epoch;                // exchanges so far (identical sequence on every rank)
+  int64_t* d_err;               // device error word: a peer missed the timeout
+  unsigned* d_counter;          // CTAs done of the current put
+};
+size_t ow_comm_area(const ow_comm* c, int64_t epoch);
+int ow_comm_check(ow_comm* c, int64_t bytes, const char* what);
+// all-gather of disjoint 32-bit word ranges: [lo, hi) from d_range (device
+// int64[2]) or the host values; n (or *d_n) words in the array
+int ow_comm_allgather_words(ow_ctx* ctx, ow_comm* c, uint32_t* d_data, const int64_t* d_range, int64_t lo, int64_t hi,
+                            const int64_t* d_n, int64_t n, cudaStream_t s);
+// marks of leaf positions d_slice[0..1) of d_leaves + n_stats u64 statistics
+// (summed over ranks into d_stats)
+int ow_comm_exchange_marks(ow_ctx* ctx, ow_comm* c, const int32_t* d_leaves, int8_t* d_marks, const int64_t* d_slice,
+                           const int64_t* d_n, int64_t n_bound, unsigned long long* d_stats, int n_stats,
+                           cudaStream_t s);
+
 // one marking pass without a host round trip: stats accumulate in d_out[0..2]
 int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves, const float* d_coords,
                    int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int32_t* d_bin_ids,
                    const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,
                    double reach, unsigned long long* d_out, cudaStream_t s,
-                   const int64_t* d_n_leaves = nullptr, bool chunk_boxes_ready = false);
+                   const int64_t* d_n_leaves = nullptr, bool chunk_boxes_ready = false,
+                   const int64_t* d_slice = nullptr);
 
 int ow_stage_times(ow_ctx* ctx, ow_nearwall_result* out);
 

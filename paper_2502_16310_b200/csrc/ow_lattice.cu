@@ -63,6 +63,8 @@ struct LatArgs {
   const int32_t* leaves;
   int64_t n_leaves;
   int32_t* pos_of;          // [n_blocks]
+  int32_t* grid;            // dense finest-level lattice -> leaf position (-1: no finest leaf), or null
+  int gdim[3];              // its extent per axis (root << level)
   int64_t pos_lo, pos_hi;   // leaf positions this call owns (multi-GPU slice)
   float* cen;               // [n_leaves][D][4] cell-centre coordinates
   uint8_t* has_pair;        // [n_leaves]
@@ -103,7 +105,7 @@ struct LatArgs {
 
 template <int D>
 __global__ void k_lat_pos(ForestC F, int level, const int32_t* __restrict__ leaves, int64_t n, int32_t* pos_of,
-                          uint8_t* has_pair, float* cen) {
+                          uint8_t* has_pair, float* cen, int32_t* grid, int g0, int g1) {
   ow_pdl_wait();
   double q[3];
 #pragma unroll
@@ -112,6 +114,11 @@ __global__ void k_lat_pos(ForestC F, int level, const int32_t* __restrict__ leav
     const int id = leaves[i];
     pos_of[id] = (int32_t)i;
     has_pair[i] = 0;
+    if (grid) {  // finest leaves are the blocks of `level` with no children: one lattice cell each
+      int64_t lin = F.coord[D - 1][id];
+      if (D == 3) lin = lin * g1 + F.coord[1][id];
+      grid[lin * g0 + F.coord[0][id]] = (int32_t)i;
+    }
 #pragma unroll
     for (int a = 0; a < D; ++a) {  // forest.py:187-205: f32(o + u q), u = (i + 1/2) / 4
       const double o = DADD(F.dmin[a], DMUL((double)F.coord[a][id], q[a]));
@@ -313,6 +320,57 @@ __device__ __forceinline__ bool wt_test2(const float* x, const float* v, unsigne
   return hit;
 }
 
+// The same tests on operands already permuted to the direction's frame:
+// V[j] = (v_j[kx], v_j[ky], v_j[kz], S_j) with (S_0, S_1, S_2) = (Sx, Sy, Sz)
+// and the centre (x[kx], x[ky], x[kz]): the oracle's op order, no selects.
+__device__ __forceinline__ bool wt_cand_perm(float xx, float xy, float xz, const float4* V, WtNum& num) {
+  const float sx = V[0].w, sy = V[1].w, sz = V[2].w;
+  float X[3], Y[3], Z[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float az = FSUB(V[j].z, xz);
+    X[j] = FSUB(FSUB(V[j].x, xx), FMUL(sx, az));
+    Y[j] = FSUB(FSUB(V[j].y, xy), FMUL(sy, az));
+    Z[j] = az;
+  }
+  float U = FSUB(FMUL(X[2], Y[1]), FMUL(Y[2], X[1]));
+  float Vv = FSUB(FMUL(X[0], Y[2]), FMUL(Y[0], X[2]));
+  float W = FSUB(FMUL(X[1], Y[0]), FMUL(Y[1], X[0]));
+  if ((U == 0.0f) | (Vv == 0.0f) | (W == 0.0f)) {  // exact signs: float products are exact in float64
+    U = __double2float_rn(DSUB(DMUL((double)X[2], (double)Y[1]), DMUL((double)Y[2], (double)X[1])));
+    Vv = __double2float_rn(DSUB(DMUL((double)X[0], (double)Y[2]), DMUL((double)Y[0], (double)X[2])));
+    W = __double2float_rn(DSUB(DMUL((double)X[1], (double)Y[0]), DMUL((double)Y[1], (double)X[0])));
+  }
+  const bool mixed = ((U < 0.0f) | (Vv < 0.0f) | (W < 0.0f)) & ((U > 0.0f) | (Vv > 0.0f) | (W > 0.0f));
+  const float det = FADD(FADD(U, Vv), W);
+  const float T = FADD(FADD(FMUL(U, FMUL(sz, Z[0])), FMUL(Vv, FMUL(sz, Z[1]))), FMUL(W, FMUL(sz, Z[2])));
+  bool c = !mixed & (det != 0.0f) & quot_nonneg(T, det);
+  const float ad = fabsf(det);
+  if (ad >= 0x1p-100f) c = c & (fabsf(T) <= FMUL(ad, 1.00001f));
+  num.T = T;
+  num.det = det;
+  return c;
+}
+// 2D: V[j] = (v_j[kx], v_j[kz], -, S) with S = Sx for j = 0 and Sz for j = 1
+__device__ __forceinline__ bool wt_test_perm2(float xx, float xz, const float4* V, float& t) {
+  const float sx = V[0].w, sz = V[1].w;
+  const float aaz = FSUB(V[0].y, xz), baz = FSUB(V[1].y, xz);
+  const float ax = FSUB(FSUB(V[0].x, xx), FMUL(sx, aaz));
+  const float bx = FSUB(FSUB(V[1].x, xx), FMUL(sx, baz));
+  const float U = bx, Vv = -ax;
+  const bool mixed = ((U < 0.0f) | (Vv < 0.0f)) & ((U > 0.0f) | (Vv > 0.0f));
+  const float det = FADD(U, Vv);
+  bool hit = false;
+  if (!mixed && det != 0.0f) {
+    const float T = FADD(FMUL(U, FMUL(sz, aaz)), FMUL(Vv, FMUL(sz, baz)));
+    if (quot_nonneg(T, det)) {
+      t = FDIV(T, det);
+      hit = t <= 1.0f;
+    }
+  }
+  return hit;
+}
+
 // cell index (flat, within the block) and centre of unit `rem` of a row
 // word w (cells in x-fastest order over the per-axis ranges)
 template <int D>
@@ -409,29 +467,42 @@ template <int D, int FPW>
 __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
+  constexpr int NCOMB = D == 3 ? 27 : 9;  // per-axis c in {-1, 0, +1}
   constexpr int FACES_PER_WARP = FPW, SLOT_LANES = 32 / FPW;
   __shared__ float4 s_face[4][FACES_PER_WARP][3];  // per warp: vertices (v0, v1, v2) / (a.xy, b.xy) of its faces
   __shared__ uint2 s_hit[4][HITBUF];
   __shared__ uint8_t s_hdir[4][HITBUF];
   __shared__ unsigned s_frame[QMAX];
   __shared__ float4 s_shear[QMAX];
+  __shared__ unsigned s_cinfo[NCOMB];  // combination -> direction | range-field shift per axis
   // 3D: candidate hits (T, det) + (flat cell, direction), divided 32 at a time
   __shared__ WtNum s_cnum[4][D == 3 ? CANDBUF : 1];
   __shared__ uint2 s_cmeta[4][D == 3 ? CANDBUF : 1];
-  int nc = 0;  // candidates buffered by this warp
+  // the warp's current (face, finest leaf) pairs, one per lane: leaf
+  // position, face slot | valid combinations, first unit, per-axis ranges;
+  // per pair the cumulative units of its valid combinations (ascending) and
+  // the leaf's cell centres
+  __shared__ int4 s_pm[4][32];
+  __shared__ uint4 s_pr[4][32];
+  __shared__ uint16_t s_pre[4][32][NCOMB + 1];
+  __shared__ uint8_t s_pcomb[4][32][NCOMB];
+  __shared__ float4 s_pcen[4][32][D];
+  __shared__ uint8_t s_rlane[4][32];  // rank of a pair with units -> its lane
+  int nc = 0;                         // candidates buffered by this warp
   for (int i = threadIdx.x; i < QMAX; i += blockDim.x) {
     s_frame[i] = A.frame[i];
     s_shear[i] = A.shear[i];
   }
+  for (int i = threadIdx.x; i < NCOMB; i += blockDim.x) s_cinfo[i] = A.combo_info[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sl = lane % SLOT_LANES;
-  int nh = 0;  // hits buffered by this warp
-  unsigned long long iru = 0;  // inline units / rows of this warp (statistics)
+  int nh = 0;                  // hits buffered by this warp
+  unsigned long long iru = 0;  // units << RU_ROW_BITS | (face, leaf) pairs of this warp (statistics)
   // persistent warps take face groups from a global counter: the cost of a
-  // face (blocks in reach x rows x cells) varies by orders of magnitude, so
-  // dynamic assignment replaces the static one-group-per-warp grid (whose
-  // single wave ended in a long tail of a few heavy warps)
+  // face (blocks in reach x combinations x cells) varies by orders of
+  // magnitude, so dynamic assignment replaces a static grid (whose single
+  // wave ended in a long tail of a few heavy warps)
   for (;;) {
   unsigned long long grp = 0;
   if (lane == 0) grp = atomicAdd(A.face_next, 1ull);
@@ -466,13 +537,6 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
     } else {
       r0 = make_float4(v[0][0], v[0][1], v[1][0], v[1][1]);
     }
-    if (A.inline_units < C) {  // records for k_lat_mt (no large rows when every row is inline)
-      A.rec[3 * f + 0] = r0;
-      if (D == 3) {
-        A.rec[3 * f + 1] = r1;
-        A.rec[3 * f + 2] = r2;
-      }
-    }
     float4* sf = s_face[wid][lane / SLOT_LANES];
     sf[0] = r0;
     sf[1] = r1;
@@ -497,152 +561,203 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   }
   const int max_slots = __reduce_max_sync(0xffffffffu, nslots);
   for (int s0 = 0; s0 < max_slots; s0 += SLOT_LANES) {
+    // ---- pairs: this lane's (face, finest leaf), its valid combinations and
+    // their cumulative unit counts (units of a combination = its cell box)
     const int slot = s0 + sl;
-    int nrow = 0, pos = 0;
-    unsigned R[3] = {0u, 0u, 0u}, valid = 0u;
+    int units = 0;
     if (slot < nslots) {
-      int32_t nc[3] = {0, 0, 0};
+      int32_t nc3[3] = {0, 0, 0};
       int rem = slot;
 #pragma unroll
       for (int a = 0; a < D; ++a) {  // rem / ext by a float reciprocal, corrected to exact
         if (a + 1 == D) {  // last axis: rem < ext
-          nc[a] = k0[a] + rem;
+          nc3[a] = k0[a] + rem;
           break;
         }
         int qd = (int)(__fmul_rz((float)rem, rext[a]));
         int rr = rem - qd * ext[a];
         while (rr < 0) rr += ext[a], --qd;
         while (rr >= ext[a]) rr -= ext[a], ++qd;
-        nc[a] = k0[a] + rr;
+        nc3[a] = k0[a] + rr;
         rem = qd;
       }
-      int depth;
-      const int node = locate(A.F, L, nc, &depth);
-      // (leaves outside this call's position slice belong to another rank; no
-      // early `continue` here: the whole warp must reach the shuffles below)
-      if (depth == L && A.F.first_child[node] < 0) {
-        const int pn = A.pos_of[node];
-        if (pn >= A.pos_lo && pn < A.pos_hi) {
-          pos = pn;
+      // finest leaf at lattice cell nc3: one load from the dense lattice table
+      // (or the root-lattice descent when the level is too fine for one)
+      int pn = -1;
+      if (A.grid) {
+        int64_t lin = nc3[D - 1];
+        if (D == 3) lin = lin * A.gdim[1] + nc3[1];
+        pn = __ldg(A.grid + lin * A.gdim[0] + nc3[0]);
+      } else {
+        int depth;
+        const int node = locate(A.F, L, nc3, &depth);
+        if (depth == L && A.F.first_child[node] < 0) pn = A.pos_of[node];
+      }
+      // (leaves outside this call's position slice belong to another rank)
+      if (pn >= A.pos_lo && pn < A.pos_hi) {
+        unsigned R[3] = {0u, 0u, 0u};
+        const float4* cg = reinterpret_cast<const float4*>(A.cen) + (int64_t)pn * D;
+        float4 cen4[3];
 #pragma unroll
-          for (int a = 0; a < D; ++a)
-            R[a] = axis_ranges(reinterpret_cast<const float4*>(A.cen)[(int64_t)pos * D + a], A.h[a], lo[a], hi[a]);
-          // directions with a non-empty cell box on every axis, as a mask over
-          // the 3^D combinations (outer product of the per-axis masks)
-          valid = A.dirmask;
+        for (int a = 0; a < D; ++a) {
+          cen4[a] = __ldg(cg + a);
+          R[a] = axis_ranges(cen4[a], A.h[a], lo[a], hi[a]);
+        }
+        // directions with a non-empty cell box on every axis, as a mask over
+        // the 3^D combinations (outer product of the per-axis masks)
+        unsigned valid = A.dirmask;
 #pragma unroll
-          for (int a = 0; a < D; ++a) valid &= A.spread[a][(~R[a] >> 12) & 7u];
-          nrow = __popc(valid);
-          if (nrow) A.has_pair[pos] = 1;
+        for (int a = 0; a < D; ++a) valid &= A.spread[a][(~R[a] >> 12) & 7u];
+        if (valid) {
+          int k = 0;
+          s_pre[wid][lane][0] = 0;
+          for (unsigned m = valid; m; m &= m - 1u) {
+            const int c = __ffs(m) - 1;
+            const unsigned info = s_cinfo[c];
+            int u = 1;
+#pragma unroll
+            for (int a = 0; a < D; ++a) u *= (int)((R[a] >> (((info >> (8 + 8 * a)) & 0xFFu) + 2)) & 3u) + 1;
+            units += u;
+            s_pcomb[wid][lane][k] = (uint8_t)c;
+            s_pre[wid][lane][++k] = (uint16_t)units;
+          }
+          A.has_pair[pn] = 1;
+          s_pm[wid][lane] = make_int4(pn, (int)(lane / SLOT_LANES) | k << 8, 0, 0);
+          s_pr[wid][lane] = make_uint4(R[0], R[1], R[2], 0u);
+#pragma unroll
+          for (int a = 0; a < D; ++a) s_pcen[wid][lane][a] = cen4[a];
         }
       }
     }
-    int incl = nrow;
+    // ---- units: the pairs' (combination, cell) tests flattened over the warp
+    int si = units;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
+      const int y = __shfl_up_sync(0xffffffffu, si, o);
+      if (lane >= o) si += y;
     }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    if (!total) continue;
-    const int excl = incl - nrow;
-    const int fi = (int)f;
-    for (int r0 = 0; r0 < total; r0 += 32) {
-      const int r = r0 + lane;
-      const int4 row = row_of<D>(r, excl, valid, R, pos, fi, A);  // units 0 past the end
-      const int units = row.w;
-      // rows of more than INLINE_UNITS cells go to k_lat_mt (load-balanced over
-      // units): one packed reservation of rows and units per chunk, so row
-      // order and unit order agree and unit offsets stay monotone
-      const bool big = units > A.inline_units;
-      const unsigned bm = __ballot_sync(0xffffffffu, big);
-      if (bm) {
-        const int ub = big ? units : 0;
-        int ui = ub;
+    const int S = __shfl_sync(0xffffffffu, si, 31);
+    if (!S) continue;
+    const int se = si - units;
+    const unsigned nzm = __ballot_sync(0xffffffffu, units > 0);
+    iru += ((unsigned long long)S << RU_ROW_BITS) + (unsigned long long)__popc(nzm);
+    if (units > 0) {
+      s_pm[wid][lane].z = se;
+      s_rlane[wid][__popc(nzm & lanemask_lt())] = (uint8_t)lane;
+    }
+    __syncwarp();
+    int base = 0, carry = 0;  // pairs started before the window / the pair owning its first unit
+    for (int u0 = 0; u0 < S; u0 += 32) {
+      const int u = u0 + lane;
+      // owner of unit u: the last pair starting at or before u (one bit per
+      // pair start in this 32-unit window, pairs in lane order)
+      const unsigned sb = (units > 0 && se >= u0 && se < u0 + 32) ? 1u << (se - u0) : 0u;
+      const unsigned M = __reduce_or_sync(0xffffffffu, sb);
+      const int kr = __popc(M & (lanemask_lt() | (1u << lane)));
+      const int jl = kr ? (int)s_rlane[wid][base + kr - 1] : carry;
+      base += __popc(M);
+      carry = M ? (int)s_rlane[wid][base - 1] : carry;
+      bool hit = false, cand = false;
+      float t = 0.0f;
+      unsigned cellg = 0;
+      int d = 0;
+      WtNum num{0.0f, 0.0f};
+      if (u < S) {
+        const int4 pm = s_pm[wid][jl];
+        const int k = u - pm.z;
+        // combination of unit k: the last with cumulative units <= k
+        const uint16_t* pre = s_pre[wid][jl];
+        int lo_i = 0, hi_i = (pm.y >> 8);  // pre[lo_i] <= k < pre[hi_i]
+        while (hi_i - lo_i > 1) {
+          const int mid = (lo_i + hi_i) >> 1;
+          if ((int)pre[mid] <= k) lo_i = mid;
+          else hi_i = mid;
+        }
+        const int c = s_pcomb[wid][jl][lo_i];
+        int r = k - (int)pre[lo_i];
+        const unsigned info = s_cinfo[c];
+        d = (int)(info & 0xFFu);
+        const uint4 pr = s_pr[wid][jl];
+        const unsigned Rj[3] = {pr.x, pr.y, pr.z};
+        float x[3];
+        int cell = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, ui, o);
-          if (lane >= o) ui += y;
-        }
-        const unsigned long long tu = (unsigned long long)__shfl_sync(0xffffffffu, ui, 31);
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(A.ru_d, (tu << RU_ROW_BITS) | (unsigned long long)__popc(bm));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (big) {
-          const int64_t k = (int64_t)(base & RU_ROW_MASK) + __popc(bm & lanemask_lt());
-          const int64_t u = (int64_t)(base >> RU_ROW_BITS) + ui - ub;
-          if (k < A.row_cap && u + ub <= A.unit_cap) {
-            A.rows[k] = row;
-            A.rowoff[k] = u;
-            for (int64_t t = (u + MT_TILE - 1) / MT_TILE; t * MT_TILE < u + ub; ++t) A.tile_row[t] = (int32_t)k;
+        for (int a = 0; a < D; ++a) {  // cell box of combination c on axis a: i0 | (ext - 1) << 2
+          const unsigned fa = (Rj[a] >> ((info >> (8 + 8 * a)) & 0xFFu)) & 0xFu;
+          int i;
+          if (a + 1 < D) {
+            const int e = (int)(fa >> 2) + 1;
+            const int qd = div_small(r, e);
+            i = (int)(fa & 3u) + (r - qd * e);
+            r = qd;
+          } else {
+            i = (int)(fa & 3u) + r;
           }
+          cell |= i << (2 * a);
+          x[a] = reinterpret_cast<const float*>(&s_pcen[wid][jl][a])[i];
         }
+        cellg = (unsigned)pm.x * (unsigned)C + (unsigned)cell;
+        const float* F = reinterpret_cast<const float*>(s_face[wid][pm.y & 0xFF]);
+        if (D == 3) cand = wt_cand3(x, F, s_frame[d], s_shear[d], num);
+        else hit = wt_test2(x, F, s_frame[d], s_shear[d], t);
       }
-      // the other rows: their units flattened over the warp and tested here
-      const int us = big ? 0 : units;
-      int si = us;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, si, o);
-        if (lane >= o) si += y;
-      }
-      const int S = __shfl_sync(0xffffffffu, si, 31);
-      const int se = si - us;
-      iru += ((unsigned long long)S << RU_ROW_BITS) + (unsigned long long)__popc(__ballot_sync(0xffffffffu, us > 0));
-      for (int u0 = 0; u0 < S; u0 += 32) {
-        const int u = u0 + lane;
-        int j = 0;  // owning lane: the first with si > u
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1)
-          if (__shfl_sync(0xffffffffu, si, j + step - 1) <= u) j += step;
-        const int ej = __shfl_sync(0xffffffffu, se, j);
-        const int pj = __shfl_sync(0xffffffffu, row.x, j);
-        const int fj = __shfl_sync(0xffffffffu, row.y, j);
-        const unsigned wj = (unsigned)__shfl_sync(0xffffffffu, row.z, j);
-        bool hit = false;
-        float t = 0.0f;
-        unsigned cellg = 0;
-        const int d = (int)(wj & 31u);
-        if (D == 3) {
-          bool cand = false;
-          WtNum num{0.0f, 0.0f};
-          if (u < S) {
-            float x[3];
-            const int cell = row_cell<D>(wj, u - ej, A.cen + (int64_t)pj * D * 4, x);
-            cellg = (unsigned)pj * (unsigned)C + (unsigned)cell;
-            cand = wt_cand3(x, reinterpret_cast<const float*>(s_face[wid][fj - fbase]), s_frame[d], s_shear[d], num);
+      if (D == 3) {
+        const unsigned cm = __ballot_sync(0xffffffffu, cand);
+        if (cm) {
+          if (cand) {
+            const int k = nc + __popc(cm & lanemask_lt());
+            s_cnum[wid][k] = num;
+            s_cmeta[wid][k] = make_uint2(cellg, (unsigned)d);
           }
-          const unsigned cm = __ballot_sync(0xffffffffu, cand);
-          if (cm) {
-            if (cand) {
-              const int k = nc + __popc(cm & lanemask_lt());
-              s_cnum[wid][k] = num;
-              s_cmeta[wid][k] = make_uint2(cellg, (unsigned)d);
-            }
-            nc += __popc(cm);
-            __syncwarp();
-            if (nc >= 32) {  // a full warp of divisions
-              nh = drain_cands(A, s_cnum[wid], s_cmeta[wid], nc, 32, s_hit[wid], s_hdir[wid], nh, lane);
-              nc -= 32;
-            }
+          nc += __popc(cm);
+          __syncwarp();
+          if (nc >= 32) {  // a full warp of divisions
+            nh = drain_cands(A, s_cnum[wid], s_cmeta[wid], nc, 32, s_hit[wid], s_hdir[wid], nh, lane);
+            nc -= 32;
           }
-        } else {
-          if (u < S) {
-            float x[3];
-            const int cell = row_cell<D>(wj, u - ej, A.cen + (int64_t)pj * D * 4, x);
-            cellg = (unsigned)pj * (unsigned)C + (unsigned)cell;
-            hit = wt_test2(x, reinterpret_cast<const float*>(s_face[wid][fj - fbase]), s_frame[d], s_shear[d], t);
-          }
-          nh = record_hits(A, s_hit[wid], s_hdir[wid], nh, hit, cellg, d, t, lane);
         }
+      } else {
+        nh = record_hits(A, s_hit[wid], s_hdir[wid], nh, hit, cellg, d, t, lane);
       }
     }
+    __syncwarp();  // the staged pairs are rewritten by the next slot batch
   }
   __syncwarp();  // s_face is rewritten by the next group
   }
   if (D == 3 && nc > 0) nh = drain_cands(A, s_cnum[wid], s_cmeta[wid], nc, nc, s_hit[wid], s_hdir[wid], nh, lane);
   if (nh) flush_hits(A, s_hit[wid], s_hdir[wid], nh, lane);
   if (iru && lane == 0) atomicAdd(A.iru_d, iru);
+}
+
+// multi-GPU: after the flag words of every rank's slice are exchanged, the
+// candidate blocks are the leaves with a boundary cell (every rank ranks the
+// same blocks, so boundary rows are numbered identically everywhere; blocks
+// whose rows all missed have no boundary row either way)
+template <int D>
+__global__ void k_has_from_flags(const uint32_t* __restrict__ flags, int64_t n_leaves, uint8_t* has_pair) {
+  ow_pdl_wait();
+  constexpr int C = D == 3 ? 64 : 16;
+  const int lane = threadIdx.x & 31;
+  for (int64_t pos = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; pos < n_leaves;
+       pos += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < (C + 31) / 32; ++k) any |= (lane + 32 * k < C) && flags[pos * C + lane + 32 * k] != 0u;
+    any = __any_sync(0xffffffffu, any);
+    if (lane == 0) has_pair[pos] = any ? 1 : 0;
+  }
+}
+
+// multi-GPU: the q words of this rank's boundary rows (candidate blocks at
+// positions [pos_lo, pos_hi), contiguous in row order) -> range[0..1)
+__global__ void k_own_q_words(const int32_t* cand_rank, const int64_t* boff, const int64_t* n_cb_d, int64_t n_leaves,
+                              int64_t n_boundary, int64_t pos_lo, int64_t pos_hi, int nq, int64_t* range) {
+  ow_pdl_wait();
+  if (threadIdx.x != 0) return;
+  const int64_t ncb = *n_cb_d;
+  const int64_t r0 = pos_lo < n_leaves ? cand_rank[pos_lo] : ncb, r1 = pos_hi < n_leaves ? cand_rank[pos_hi] : ncb;
+  range[0] = (r0 < ncb ? boff[r0] : n_boundary) * nq;
+  range[1] = (r1 < ncb ? boff[r1] : n_boundary) * nq;
 }
 
 // ranks of candidate blocks (leaves with at least one row)
@@ -1027,6 +1142,8 @@ LatArgs make_args(ow_ctx* ctx) {
   A.pos_lo = ctx->lat_pos_lo;
   A.pos_hi = ctx->lat_pos_hi;
   A.pos_of = (int32_t*)ctx->slot_ptr[SLOT_LAT_POS];
+  A.grid = ctx->lat_grid_on ? (int32_t*)ctx->slot_ptr[SLOT_LAT_GRID] : nullptr;
+  for (int a = 0; a < 3; ++a) A.gdim[a] = a < f->dim ? (int)((int64_t)f->root[a] << A.level) : 1;
   A.cen = (float*)ctx->slot_ptr[SLOT_LAT_CEN];
   A.has_pair = (uint8_t*)ctx->slot_ptr[SLOT_LAT_HAS];
   A.rec = (float4*)ctx->slot_ptr[SLOT_LAT_REC];
@@ -1144,12 +1261,19 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   OW_TRY(ow_slot(ctx, SLOT_LAT_BOFFS, 8 * (size_t)nl, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_HCOUNT, 4 * (size_t)nl, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_HOFFS, 8 * (size_t)nl, s, &p));
+  {  // dense finest-lattice table when it is at most 2^26 cells (256 MB)
+    int64_t cells = 1;
+    for (int a = 0; a < D; ++a) cells *= (int64_t)f->root[a] << level;
+    ctx->lat_grid_on = cells <= (int64_t(1) << 26) && !getenv("OW_LAT_NO_GRID");
+    if (ctx->lat_grid_on) OW_TRY(ow_slot(ctx, SLOT_LAT_GRID, 4 * (size_t)cells, s, &p));
+  }
   OW_CUDA(cudaMemsetAsync(ctx->d_small + 48, 0, 5 * 8, s));
   OW_CUDA(cudaMemsetAsync(d_flags, 0, 4 * (size_t)n_leaves * C, s));
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
   LatArgs A = make_args(ctx);
-  if (D == 3) ow_launch(k_lat_pos<3>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
-  else ow_launch(k_lat_pos<2>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen);
+  if (A.grid) OW_CUDA(cudaMemsetAsync(A.grid, 0xFF, 4 * (size_t)A.gdim[0] * A.gdim[1] * A.gdim[2], s));
+  if (D == 3) ow_launch(k_lat_pos<3>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1]);
+  else ow_launch(k_lat_pos<2>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1]);
   // the sweep: k_lat_faces (rows; small rows tested inline) + k_lat_mt (large rows)
   OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
   const int fpw = faces_per_warp(ctx, D, n_faces, nl);
@@ -1162,7 +1286,6 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   }
   ctx->launches += 2;
   OW_CHECK_LAUNCH();
-  OW_TRY(ow::scan01(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s));
   const int64_t tiles_max = ucap / MT_TILE + 1;
   if (!inline_all) {  // (every row inline: no k_lat_mt rows, and k_lat_hits sees zero units)
     if (D == 3) ow_launch(k_lat_mt<3>, ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s, A);
@@ -1170,6 +1293,31 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   } else {
     ctx->launches -= 1;
   }
+  if (ctx->lat_comm && ctx->lat_comm->world > 1) {
+    // multi-GPU: every rank swept the faces against its own leaf slice; the
+    // flag words of the slices are all-gathered over peer memory.  A rank
+    // whose own sweep outgrew its row / hit buffers re-runs it first (a local
+    // decision: it must precede the exchange every rank takes part in)
+    int64_t hs[3];
+    OW_TRY(ow_readback(ctx, ctx->d_small + 48, 3, hs, s));
+    const int64_t r0 = (int64_t)((uint64_t)hs[0] & RU_ROW_MASK), u0 = (int64_t)((uint64_t)hs[0] >> RU_ROW_BITS);
+    if (r0 > rcap || u0 > ucap || hs[1] > icap) {
+      ctx->lat_row_cap = r0 + r0 / 4 + 1024;
+      ctx->lat_unit_cap = u0 + u0 / 4 + 4096;
+      if (hs[1] > icap) ctx->lat_ihit_cap = hs[1] + hs[1] / 4 + 65536;
+      if (ctx->lat_unit_cap >= (int64_t(1) << 31)) {
+        ow_set_error("lattice: %lld link-face tests exceed one pass (2^31)", (long long)u0);
+        return OW_ERR_CAPACITY;
+      }
+      return ow_lattice_links_count_range(ctx, f, level, d_leaves, n_leaves, pos_lo, pos_hi, d_coords, n_faces,
+                                          geom_key, grid, h_dirs, n_dirs, d_flags, out_boundary, stream);
+    }
+    OW_TRY(ow_comm_allgather_words(ctx, ctx->lat_comm, d_flags, nullptr, pos_lo * C, pos_hi * C, nullptr, nl * C, s));
+    if (D == 3) ow_launch(k_has_from_flags<3>, ow_blocks(nl, 8, 8 * OW_SMS), 256, 0, s, (const uint32_t*)d_flags, nl, A.has_pair);
+    else ow_launch(k_has_from_flags<2>, ow_blocks(nl, 8, 8 * OW_SMS), 256, 0, s, (const uint32_t*)d_flags, nl, A.has_pair);
+    OW_LAUNCHED(ctx);
+  }
+  OW_TRY(ow::scan01(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s));
   OW_PROF_END(ctx, PROF_LAT_SWEEP, s);
   if (D == 3) ow_launch(k_lat_bcount<3>, ow_blocks(nl, 8), 256, 0, s, A);
   else ow_launch(k_lat_bcount<2>, ow_blocks(nl, 8), 256, 0, s, A);
@@ -1237,11 +1385,23 @@ extern "C" int ow_lattice_links_emit_packed(ow_ctx* ctx, int64_t* d_cells, float
   if (ctx->lat_forest.dim == 3) {
     ow_launch(k_lat_emit<3>, (unsigned)ctx->lat_ncb, C, 0, s, A);
     ow_launch(k_lat_hits<3>, 8 * OW_SMS, 256, 0, s, A);
-    if (d_q_packed) ow_launch(k_lat_pack<3>, (unsigned)ctx->lat_ncb, C, 0, s, A);
   } else {
     ow_launch(k_lat_emit<2>, (unsigned)ctx->lat_ncb, C, 0, s, A);
     ow_launch(k_lat_hits<2>, 8 * OW_SMS, 256, 0, s, A);
-    if (d_q_packed) ow_launch(k_lat_pack<2>, (unsigned)ctx->lat_ncb, C, 0, s, A);
+  }
+  if (ctx->lat_comm && ctx->lat_comm->world > 1) {
+    // multi-GPU: a rank's hits fill the q rows of its own slice only; the
+    // rows are all-gathered over peer memory (row order = leaf order)
+    int64_t* range = ctx->d_small + 40;
+    ow_launch(k_own_q_words, 1, 32, 0, s, (const int32_t*)A.cand_rank, A.boff, A.n_cb_d, ctx->lat_leaves,
+              ctx->lat_boundary, ctx->lat_pos_lo, ctx->lat_pos_hi, A.nq, range);
+    OW_LAUNCHED(ctx);
+    OW_TRY(ow_comm_allgather_words(ctx, ctx->lat_comm, reinterpret_cast<uint32_t*>(d_q), range, 0, 0, nullptr,
+                                   ctx->lat_boundary * A.nq, s));
+  }
+  if (d_q_packed) {
+    if (ctx->lat_forest.dim == 3) ow_launch(k_lat_pack<3>, (unsigned)ctx->lat_ncb, C, 0, s, A);
+    else ow_launch(k_lat_pack<2>, (unsigned)ctx->lat_ncb, C, 0, s, A);
   }
   OW_PROF_END(ctx, PROF_LATTICE, s);
   ctx->launches += d_q_packed ? 3 : 2;

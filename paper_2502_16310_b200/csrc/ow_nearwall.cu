@@ -139,6 +139,7 @@ struct MarkArgs {
   const float4* cbox;       // union boxes of 32-entry bin-CSR chunks
   int64_t n_faces, n_leaves;
   const int64_t* d_n;       // optional device leaf count (n_leaves is then an upper bound)
+  const int64_t* d_slice;   // optional device [lo, hi) of leaf positions to mark (multi-GPU shard)
   float d;
   double reach;
   unsigned long long* out;  // [0] marked, [1] tests, [2] evaluated, [3] sphere tests, [4] box culls
@@ -377,8 +378,9 @@ __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_blocks(MarkArgs A, Mar
   ow_pdl_wait();
   __shared__ MarkSmem<D> S;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t n = A.d_n ? *A.d_n : A.n_leaves;
-  for (int64_t pos = (int64_t)blockIdx.x * MARK_WARPS + wid; pos < n; pos += (int64_t)gridDim.x * MARK_WARPS)
+  const int64_t lo = A.d_slice ? A.d_slice[0] : 0;
+  const int64_t n = A.d_slice ? A.d_slice[1] : (A.d_n ? *A.d_n : A.n_leaves);
+  for (int64_t pos = lo + (int64_t)blockIdx.x * MARK_WARPS + wid; pos < n; pos += (int64_t)gridDim.x * MARK_WARPS)
     mark_block<D, BINNED>(A, M, S, pos, lane, wid);
 }
 
@@ -688,7 +690,7 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
                    int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int32_t* d_bin_ids,
                    const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,
                    double reach, unsigned long long* out, cudaStream_t s, const int64_t* d_n_leaves,
-                   bool chunk_boxes_ready) {
+                   bool chunk_boxes_ready, const int64_t* d_slice) {
   if (!(d_spec > 0.0f)) {
     ow_set_error("near-wall distance must be positive, got %g", (double)d_spec);
     return OW_ERR_INVALID;
@@ -731,6 +733,7 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   A.cbox = (const float4*)pc;
   A.n_leaves = n_leaves;
   A.d_n = d_n_leaves;
+  A.d_slice = d_slice;
   MarkItems M;
   M.items = (int4*)pi;
   M.n_items = (unsigned long long*)((unsigned*)ph + n_leaves + (n_leaves & 1));  // after the hit words

@@ -15,6 +15,8 @@
 
 namespace {
 
+using ow::scan;
+
 __global__ void k_root_init(ow_forest f, int64_t r) {
   ow_pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -59,6 +61,60 @@ int64_t overflow_total(const int32_t* h_counts, int64_t n_bins, int64_t bin_frac
 
 __global__ void k_set_i64(int64_t* p, int64_t v) {
   ow_pdl_wait(); *p = v; }
+
+// ---- multi-GPU marking shards ("balanced by work") --------
+// Work of a leaf block: 1 + the faces of the bin holding its centre (the
+// marking cost per cell is the size of its bin's face list; the centre's bin
+// stands for the block's 4^D cells).  The exclusive prefix of the weights
+// splits the level's leaves into `world` contiguous slices of equal work.
+struct LeafWork {
+  ForestC F;
+  GridC g;
+  const int32_t* leaves;
+  const int32_t* counts;  // null: naive strategy (every block weighs the same)
+  const int64_t* d_n;
+  int level;
+  __device__ int64_t operator()(int64_t i) const {
+    if (i >= *d_n) return 0;
+    if (!counts) return 1;
+    const int id = leaves[i];
+    int64_t bin = 0, mul = 1;
+    for (int a = 0; a < F.dim; ++a) {
+      const double q = block_len(F, a, level);
+      const float c = __double2float_rn(DADD(F.dmin[a], DMUL(DADD((double)F.coord[a][id], 0.5), q)));
+      bin += (int64_t)bin_axis(c, g.min32[a], g.len32[a], g.B) * mul;
+      mul *= g.B;
+    }
+    return 1 + counts[bin];
+  }
+};
+struct WorkPrefix {
+  int64_t* e;
+  const int64_t* d_n;
+  __device__ void operator()(int64_t i, int64_t ex, int64_t) const {
+    if (i < *d_n) e[i] = ex;
+  }
+};
+// slice[0..1) of `rank`: positions whose work prefix lies in
+// [total rank / world, total (rank + 1) / world) (the same formula on every
+// rank, so the slices tile the leaves)
+__global__ void k_slice_bounds(const int64_t* __restrict__ e, const int64_t* d_n, const int64_t* d_total, int rank,
+                               int world, int64_t* slice) {
+  ow_pdl_wait();
+  if (threadIdx.x != 0) return;
+  const int64_t n = *d_n, total = *d_total;
+  auto first_geq = [&](int64_t t) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (e[mid] < t) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
+  slice[0] = rank == 0 ? 0 : first_geq(total * rank / world);
+  slice[1] = rank == world - 1 ? n : first_geq(total * (rank + 1) / world);
+}
 
 // Device-resident level loop: per pass, the words the host needs from the
 // refine ring state and the marking stats, gathered for one readback.
@@ -110,7 +166,13 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
                   const ow_grid* grid, const ow_nearwall_params* p, int32_t* d_bin_ids, int64_t bin_ids_capacity,
                   int32_t* d_bin_counts, int32_t* d_bin_offsets, ow_nearwall_result* out, cudaStream_t s, bool dev) {
   ctx->drv_spec_nl = -1;
-  if (p->world > 1) dev = false;
+  ow_comm* comm = p->world > 1 ? p->comm : nullptr;
+  if (p->world > 1 && !comm) dev = false;  // (the host exchange hook needs the leaf count on the host)
+  if (comm && (comm->world != p->world || comm->rank != p->rank || !comm->open)) {
+    ow_set_error("refine_near_wall: the exchange (rank %d of %d) does not match rank %d of %d or is not open",
+                 comm->rank, comm->world, p->rank, p->world);
+    return OW_ERR_INVALID;
+  }
   memset(out, 0, sizeof(*out));
   if (p->n_levels < 1 || p->n_levels - 1 > OW_MAX_PASSES) {
     ow_set_error("n_levels must be in [1, %d], got %d", OW_MAX_PASSES + 1, p->n_levels);
@@ -189,7 +251,27 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
     int64_t* dn = (int64_t*)drv + 72 * level;  // [0] leaves at level, [8..72) refine state
     int64_t* rs = dn + 8;
     unsigned long long* dst = (unsigned long long*)stats + 5 * level;
-    if (p->world > 1) {
+    if (comm) {
+      // sharded marking on the device: slices balanced by per-leaf work, the
+      // rank marks its slice, then the marks and the statistics are exchanged
+      // over peer memory (ow_comm.cu) — no host round trip
+      OW_TRY(ow_forest_leaves_dev(ctx, f, level, (int32_t*)pl, dn, s, d_nb));
+      void* psl;
+      OW_TRY(ow_slot(ctx, SLOT_DRV_SLICE, 8 * (size_t)(n_host + 8), s, &psl));
+      int64_t* wpre = (int64_t*)psl + 8;
+      int64_t* slice = (int64_t*)psl;  // [0..1) slice, [2] total work
+      LeafWork lw{make_forestc(f), p->binned ? make_gridc(grid) : GridC{}, (const int32_t*)pl,
+                  p->binned ? d_bin_counts : nullptr, dn, level};
+      OW_TRY(scan(ctx, lw, WorkPrefix{wpre, dn}, n_host, slice + 2, s));
+      ow_launch(k_slice_bounds, 1, 32, 0, s, (const int64_t*)wpre, (const int64_t*)dn, (const int64_t*)(slice + 2),
+                p->rank, p->world, slice);
+      OW_LAUNCHED(ctx);
+      OW_TRY(ow_mark_launch(ctx, f, (const int32_t*)pl, n_host, d_coords, n_faces, geom_key,
+                            p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
+                            p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
+                            p->binned ? E : 0, p->d_spec, p->reach, dst, s, dn, !fresh_bins, slice));
+      OW_TRY(ow_comm_exchange_marks(ctx, comm, (const int32_t*)pl, f->d_marks, slice, dn, n_host, dst, 5, s));
+    } else if (p->world > 1) {
       // sharded marking: each rank marks a contiguous slice, then the exchange
       // callback all-gathers the marks (the slice needs the leaf count on the host)
       int64_t n_leaves = 0;
@@ -506,9 +588,17 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
   }
   int64_t nb = 0;
   ctx->lat_mean_extent = out->faces.mean_extent;  // shapes the face pass
-  const int lst = ow_lattice_links_count(ctx, f, finest, (const int32_t*)pl, nl, d_coords, n_faces, geom_key, grid,
-                                         p->lattice_dirs, p->lattice_q, (uint32_t*)flags, &nb, stream);
+  // multi-GPU: each rank sweeps an equal slice of the finest leaves; flag
+  // words and q rows are all-gathered over peer memory inside the lattice calls
+  const bool shard = p->nw.world > 1 && p->nw.comm;
+  ctx->lat_comm = shard ? p->nw.comm : nullptr;
+  const int64_t pos_lo = shard ? nl * p->nw.rank / p->nw.world : 0;
+  const int64_t pos_hi = shard ? nl * (p->nw.rank + 1) / p->nw.world : nl;
+  const int lst = ow_lattice_links_count_range(ctx, f, finest, (const int32_t*)pl, nl, pos_lo, pos_hi, d_coords,
+                                               n_faces, geom_key, grid, p->lattice_dirs, p->lattice_q,
+                                               (uint32_t*)flags, &nb, stream);
   ctx->lat_mean_extent = 0.0f;
+  if (lst != OW_OK) ctx->lat_comm = nullptr;
   OW_TRY(lst);
   out->n_boundary = nb;
   void *cells, *q;
@@ -530,7 +620,9 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
     d_rows = (uint32_t*)pr;
     d_qp = (float*)pq;
   }
-  OW_TRY(ow_lattice_links_emit_packed(ctx, (int64_t*)cells, (float*)q, d_rows, d_qp, stream));
+  const int est = ow_lattice_links_emit_packed(ctx, (int64_t*)cells, (float*)q, d_rows, d_qp, stream);
+  ctx->lat_comm = nullptr;
+  OW_TRY(est);
   if (packed) {  // (8 + 4 popc) bytes per row instead of 8 + 4 Q: the host tail is the transfer
     OW_CUDA(cudaMemcpyAsync(p->host_rows, d_rows, 8 * (size_t)nb, cudaMemcpyDeviceToHost, s));
     OW_CUDA(cudaMemcpyAsync(p->host_q_packed, d_qp, 4 * (size_t)n_links, cudaMemcpyDeviceToHost, s));

@@ -299,24 +299,23 @@ struct StoreExcl {  // out[i] = exclusive prefix
 
 // ---- stable LSD radix sort of (key, value) ----------------------------------
 // BITS-bit digits (8..10): keys of up to 10 bits sort in one pass, up to 20 in
-// two (bin ids of every grid here).
+// two (bin ids of every grid here).  A tile is RS_THREADS x ITEMS items; ITEMS
+// (1..16) is chosen per sort so the grid covers every SM at least twice
+// (C2's 25 k entries: 97 tiles of 256 instead of 7 of 4 096).
 constexpr int RS_THREADS = 256;
-constexpr int RS_ITEMS = 16;
-constexpr int RS_TILE = RS_THREADS * RS_ITEMS;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_WARP_ITEMS = RS_TILE / RS_WARPS;  // 512 contiguous items per warp
 
-template <int BITS>
+template <int BITS, int ITEMS>
 __global__ void __launch_bounds__(RS_THREADS)
 k_radix_hist(const uint32_t* keys, int64_t n, int shift, int64_t n_tiles, int32_t* hist) {
   ow_pdl_wait();
-  constexpr int DIG = 1 << BITS;
+  constexpr int DIG = 1 << BITS, TILE = RS_THREADS * ITEMS;
   __shared__ int h[DIG];
   for (int d = threadIdx.x; d < DIG; d += RS_THREADS) h[d] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * RS_TILE;
+  const int64_t base = (int64_t)blockIdx.x * TILE;
 #pragma unroll 4
-  for (int k = 0; k < RS_ITEMS; ++k) {
+  for (int k = 0; k < ITEMS; ++k) {
     int64_t i = base + (int64_t)k * RS_THREADS + threadIdx.x;
     if (i < n) atomicAdd(&h[(keys[i] >> shift) & (DIG - 1)], 1);
   }
@@ -324,21 +323,21 @@ k_radix_hist(const uint32_t* keys, int64_t n, int shift, int64_t n_tiles, int32_
   for (int d = threadIdx.x; d < DIG; d += RS_THREADS) hist[(int64_t)d * n_tiles + blockIdx.x] = h[d];
 }
 
-template <int BITS>
+template <int BITS, int ITEMS>
 __global__ void __launch_bounds__(RS_THREADS)
 k_radix_scatter(const uint32_t* keys, const int32_t* vals, int64_t n, int shift, int64_t n_tiles,
                 const int32_t* hist_excl, uint32_t* keys_out, int32_t* vals_out) {
   ow_pdl_wait();
-  constexpr int DIG = 1 << BITS;
+  constexpr int DIG = 1 << BITS, TILE = RS_THREADS * ITEMS, WARP_ITEMS = TILE / RS_WARPS;
   __shared__ int cnt[RS_WARPS][DIG];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int d = lane; d < DIG; d += 32) cnt[warp][d] = 0;
   __syncwarp();
-  const int64_t base = (int64_t)blockIdx.x * RS_TILE + (int64_t)warp * RS_WARP_ITEMS;
-  uint32_t kk[RS_ITEMS];
-  int32_t vv[RS_ITEMS];
+  const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)warp * WARP_ITEMS;
+  uint32_t kk[ITEMS];
+  int32_t vv[ITEMS];
 #pragma unroll
-  for (int r = 0; r < RS_ITEMS; ++r) {
+  for (int r = 0; r < ITEMS; ++r) {
     int64_t i = base + r * 32 + lane;
     bool ok = i < n;
     kk[r] = ok ? keys[i] : 0u;
@@ -360,7 +359,7 @@ k_radix_scatter(const uint32_t* keys, const int32_t* vals, int64_t n, int shift,
   }
   __syncthreads();
 #pragma unroll
-  for (int r = 0; r < RS_ITEMS; ++r) {
+  for (int r = 0; r < ITEMS; ++r) {
     int64_t i = base + r * 32 + lane;
     bool ok = i < n;
     int d = ok ? (int)((kk[r] >> shift) & (DIG - 1)) : DIG;
@@ -376,25 +375,37 @@ k_radix_scatter(const uint32_t* keys, const int32_t* vals, int64_t n, int shift,
   }
 }
 
-template <int BITS>
+template <int BITS, int ITEMS>
 inline int radix_pass(ow_ctx* ctx, const uint32_t* ki, const int32_t* vi, uint32_t* ko, int32_t* vo, int64_t n,
                       int shift, int64_t tiles, int32_t* hist, cudaStream_t s) {
-  ow_launch(k_radix_hist<BITS>, (unsigned)tiles, RS_THREADS, 0, s, ki, n, shift, tiles, hist);
+  ow_launch(k_radix_hist<BITS, ITEMS>, (unsigned)tiles, RS_THREADS, 0, s, ki, n, shift, tiles, hist);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   OW_TRY(scan(ctx, LoadArr<int32_t>{hist}, StoreExcl<int32_t>{hist}, (int64_t)(1 << BITS) * tiles, nullptr, s));
-  ow_launch(k_radix_scatter<BITS>, (unsigned)tiles, RS_THREADS, 0, s, ki, vi, n, shift, tiles, hist, ko, vo);
+  ow_launch(k_radix_scatter<BITS, ITEMS>, (unsigned)tiles, RS_THREADS, 0, s, ki, vi, n, shift, tiles, hist, ko, vo);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;
 }
 
-// Sort n pairs by the low `key_bits` bits of key, stably.  Input in (k0, v0);
-// the sorted result pointer pair is returned through (*rk, *rv), which is
-// either (k0, v0) or (k1, v1).
+template <int BITS>
+inline int radix_pass_items(ow_ctx* ctx, int items, const uint32_t* ki, const int32_t* vi, uint32_t* ko, int32_t* vo,
+                            int64_t n, int shift, int64_t tiles, int32_t* hist, cudaStream_t s) {
+  switch (items) {
+    case 1: return radix_pass<BITS, 1>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s);
+    case 2: return radix_pass<BITS, 2>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s);
+    case 4: return radix_pass<BITS, 4>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s);
+    case 8: return radix_pass<BITS, 8>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s);
+    default: return radix_pass<BITS, 16>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s);
+  }
+}
+
 // digit passes of a key_bits-bit sort (radix_sort_pairs)
 inline int radix_passes(int key_bits) { return key_bits <= 0 ? 0 : (key_bits + 9) / 10; }
 
+// Sort n pairs by the low `key_bits` bits of key, stably.  Input in (k0, v0);
+// the sorted result pointer pair is returned through (*rk, *rv), which is
+// either (k0, v0) or (k1, v1).
 inline int radix_sort_pairs(ow_ctx* ctx, uint32_t* k0, int32_t* v0, uint32_t* k1, int32_t* v1, int64_t n,
                             int key_bits, uint32_t** rk, int32_t** rv, cudaStream_t s) {
   *rk = k0;
@@ -404,16 +415,20 @@ inline int radix_sort_pairs(ow_ctx* ctx, uint32_t* k0, int32_t* v0, uint32_t* k1
   const int passes = radix_passes(key_bits);
   int bits = (key_bits + passes - 1) / passes;
   if (bits < 8) bits = 8;
-  int64_t tiles = (n + RS_TILE - 1) / RS_TILE;
+  // items per thread: the largest power of two <= 16 that still gives >= 2
+  // tiles per SM (1 for small sorts)
+  int items = 16;
+  while (items > 1 && (n + RS_THREADS * items - 1) / (RS_THREADS * items) < 2 * OW_SMS) items >>= 1;
+  const int64_t tiles = (n + (int64_t)RS_THREADS * items - 1) / ((int64_t)RS_THREADS * items);
   void* hp;
   OW_TRY(ow_slot(ctx, SLOT_RADIX_HIST, sizeof(int32_t) * ((size_t)1 << bits) * (size_t)tiles, s, &hp));
   int32_t* hist = (int32_t*)hp;
   uint32_t *ki = k0, *ko = k1;
   int32_t *vi = v0, *vo = v1;
   for (int shift = 0; shift < key_bits; shift += bits) {
-    if (bits == 8) OW_TRY(radix_pass<8>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s));
-    else if (bits == 9) OW_TRY(radix_pass<9>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s));
-    else OW_TRY(radix_pass<10>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s));
+    if (bits == 8) OW_TRY(radix_pass_items<8>(ctx, items, ki, vi, ko, vo, n, shift, tiles, hist, s));
+    else if (bits == 9) OW_TRY(radix_pass_items<9>(ctx, items, ki, vi, ko, vo, n, shift, tiles, hist, s));
+    else OW_TRY(radix_pass_items<10>(ctx, items, ki, vi, ko, vo, n, shift, tiles, hist, s));
     uint32_t* tk = ki; ki = ko; ko = tk;
     int32_t* tv = vi; vi = vo; vo = tv;
   }

@@ -236,7 +236,10 @@ def _driver_setup(forest, n_faces, params, reuse_bins, shard):
     p.overlap_factor = int(params.overlap_factor)
     p.bin_fraction = int(bf or 1)
     keep = None
-    if shard is not None and shard.world > 1:
+    if shard is not None and shard.world > 1 and hasattr(shard, "allgather_"):  # parallel.DeviceComm
+        p.rank, p.world = shard.rank, shard.world
+        p.comm = shard.handle.value
+    elif shard is not None and shard.world > 1:
         p.rank, p.world = shard.rank, shard.world
         keep = _lib.EXCHANGE_FN(shard.exchange_callback(forest))
         p.exchange = keep

@@ -1,15 +1,29 @@
-"""Multi-GPU sharding of the near-wall pass: one process per GPU, NCCL.
+"""Multi-GPU sharding of the geometry-to-grid pass: one process per GPU.
 
 Octree blocks are independent units for marking, so each rank marks a
 contiguous slice of the level's ascending leaf list and the per-leaf marks
-are all-gathered (one NCCL all-gather of int8 per level over NVLink).  The
-forest metadata and the bin CSR are replicated: every rank builds them from
-the same inputs with the same deterministic kernels, so propagation and
-refinement (tiny, latency-bound) run redundantly and produce identical block
-ids on every rank without any further exchange.
+are all-gathered.  The forest metadata and the bin CSR are replicated: every
+rank builds them from the same inputs with the same deterministic kernels,
+so propagation and refinement (tiny, latency-bound) run redundantly and
+produce identical block ids on every rank without any further exchange
+(SURVEY.md §8e).
+
+Two exchange paths:
+
+* ``DeviceComm`` (the fused ``GridPlan`` pass): a symmetric device buffer per
+  rank mapped by every other rank through CUDA IPC; the native level loop
+  computes work-balanced slices on the device and exchanges marks, marking
+  statistics, lattice flag words and q rows with put / get kernels over peer
+  memory (NVLink / NVSwitch) — no host round trip and no NCCL call inside the
+  loop (csrc/ow_comm.cu).  torch.distributed (any backend) only carries the
+  64-byte IPC handles once at setup.
+* ``Shard`` (the per-function API): the marks of each level travel through
+  torch.distributed collectives from the driver's exchange callback.
 """
 
 from __future__ import annotations
+
+import ctypes as C
 
 import torch
 import torch.distributed as dist
@@ -139,3 +153,63 @@ class Shard:
             dist.all_reduce(tot, group=self.group)
             st = MarkStats(*(int(x) for x in tot.tolist()))
         return st
+
+
+class DeviceComm:
+    """Device-side exchange for the ranks of ``group`` on one node (collective
+    constructor: every rank calls it).  ``area_bytes`` bounds the largest
+    array one exchange carries (marks: one byte per leaf; lattice: four
+    bytes per finest cell, four per (boundary row, direction))."""
+
+    def __init__(self, area_bytes, group=None):
+        from . import _lib
+
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.area_bytes = int(area_bytes)
+        dev = _lib.device()
+        self._p = C.c_void_p()
+        handle = (C.c_uint8 * 64)()
+        _lib.call("ow_comm_create", dev.index, self.rank, self.world, self.area_bytes, C.byref(self._p), handle)
+        mine = bytes(handle)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        buf = (C.c_uint8 * (64 * self.world)).from_buffer_copy(b"".join(allh))
+        _lib.call("ow_comm_open", self._p, buf)
+        dist.barrier(group=group)  # every rank has mapped every buffer before any put
+
+    @property
+    def handle(self):
+        return self._p
+
+    def status(self):
+        """1 when an exchange gave up waiting for a peer (timeout), else 0."""
+        from . import _lib
+
+        v = C.c_int64(0)
+        _lib.call("ow_comm_status", self._p, C.byref(v))
+        return int(v.value)
+
+    def allgather_(self, t, lo, hi):
+        """In place: this rank's elements [lo, hi) of the 32-bit CUDA tensor t
+        reach every rank (ranks' ranges partition t)."""
+        from . import _lib
+
+        assert t.is_cuda and t.element_size() == 4 and t.is_contiguous()
+        _lib.call("ow_comm_allgather_u32", _lib.ctx(), self._p, _lib.ptr(t), int(lo), int(hi), t.numel(),
+                  _lib.stream())
+        return t
+
+    def close(self):
+        from . import _lib
+
+        if self._p:
+            _lib.lib().ow_comm_destroy(self._p)
+            self._p = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter teardown order
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -66,11 +66,18 @@ class GridPlan:
     NearWallParams, lattice)."""
 
     def __init__(self, domain: Aabb, root_dims, params: NearWallParams, lattice: str | None = "D3Q19",
-                 capacity=None, max_level=DEFAULT_MAX_LEVEL, reuse_outputs=False):
+                 capacity=None, max_level=DEFAULT_MAX_LEVEL, reuse_outputs=False, comm=None):
         """``reuse_outputs=True``: every pass writes into the same device
         arrays (forest, bins, links), so a pass's results are valid until the
         next ``run`` — for loops that consume each pass before the next
-        (benchmarks, time series); all work is still recomputed."""
+        (benchmarks, time series); all work is still recomputed.  The
+        returned LatticeLinks object itself is reused while the output
+        storage and sizes are unchanged (``gp_next.links is gp_prev.links``).
+
+        ``comm`` (a ``parallel.DeviceComm``, one rank per GPU): the pass is
+        sharded — work-balanced leaf slices per marking pass and equal
+        finest-leaf slices for the lattice links, exchanged over peer memory
+        inside the native call — and every rank returns the whole result."""
         self.domain = domain if isinstance(domain, Aabb) else Aabb(*domain)
         self.dim = self.domain.dim
         self.root_dims = tuple(int(v) for v in np.asarray(root_dims).reshape(-1))
@@ -96,6 +103,7 @@ class GridPlan:
         self._gp = None  # the call's parameter struct, reused while nothing static changes
         self._gp_key = None
         self.reuse = bool(reuse_outputs)
+        self.comm = comm if comm is not None and comm.world > 1 else None
         self._forest = None
         self._setup = None  # (n_faces, _driver_setup result): the parts that depend on n_faces only
         self._gp0 = _lib.G2GParamsC()  # static fields of the call's parameter struct
@@ -164,7 +172,7 @@ class GridPlan:
             if self.reuse:
                 self._forest = forest
         if self._setup is None or self._setup[0] != nf:
-            self._setup = (nf, _driver_setup(forest, nf, self.params, True, None))
+            self._setup = (nf, _driver_setup(forest, nf, self.params, True, self.comm))
         st = self._setup[1]
         if not self.reuse and st["bins_t"] is not None:  # fresh bin buffers for this pass's result
             st = dict(st)

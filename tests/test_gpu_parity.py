@@ -434,6 +434,93 @@ def test_sharded_native_driver_matches_single_rank(ow):
         np.testing.assert_array_equal(qq, lref.q.cpu().numpy())
 
 
+def _comm_worker(rank, world, port, q, sub, root, lattice, levels):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2502_16310_b200 as ow
+        from paper_2502_16310_b200 import parallel, pipeline, shapes
+
+        torch.cuda.set_device(0)
+        data = shapes.binary_stl_bytes(shapes.icosphere_triangles(sub))
+        n = int.from_bytes(data[80:84], "little")
+        rec = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda()
+        comm = parallel.DeviceComm(64 << 20)
+        plan = pipeline.GridPlan(ow.Aabb(np.zeros(3), np.ones(3)), (root,) * 3,
+                                 ow.NearWallParams(d_spec=0.06, n_levels=levels, bins_per_axis=8), lattice,
+                                 comm=comm, reuse_outputs=True)
+        outs = []
+        for _ in range(2):  # a second pass reuses the plan (epochs continue)
+            gp = plan.run(rec, n, host=True)
+            torch.cuda.synchronize()
+            f, ll = gp.forest, gp.links
+            outs.append((f._coords.copy(), f._first_child.copy(), f.marks.cpu().numpy(), gp.result.marked_detected,
+                         gp.result.cell_face_tests, ll.flags.cpu().numpy(), ll.cells.cpu().numpy(),
+                         ll.q.cpu().numpy(), gp.host_q(), bool(gp.reran)))
+        q.put((rank, comm.status(), outs))
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("sub,root,lattice,levels", [(3, 8, "D3Q19", 3), (4, 8, "D3Q27", 4)])
+def test_device_comm_fused_pass_matches_single_rank(ow, sub, root, lattice, levels):
+    """Two ranks sharing one GPU run the fused GridPlan pass with a
+    DeviceComm: work-balanced marking slices and equal lattice slices,
+    exchanged by put / get kernels over CUDA-IPC-mapped memory with no host
+    round trip in the level loop.  Every rank's forest, marks, statistics,
+    lattice flags, boundary rows, q and packed host rows equal the
+    single-rank pass, twice in a row (the exchange epochs continue)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_2502_16310_b200 import pipeline, shapes
+
+    data = shapes.binary_stl_bytes(shapes.icosphere_triangles(sub))
+    n = int.from_bytes(data[80:84], "little")
+    rec = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda()
+    ref = pipeline.GridPlan(ow.Aabb(np.zeros(3), np.ones(3)), (root,) * 3,
+                            ow.NearWallParams(d_spec=0.06, n_levels=levels, bins_per_axis=8), lattice).run(
+        rec, n, host=True)
+    torch.cuda.synchronize()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_comm_worker, args=(r, 2, port, q, sub, root, lattice, levels)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=800) for _ in procs]
+    for p in procs:
+        p.join(60)
+    assert all(p.exitcode == 0 for p in procs)
+    f, ll = ref.forest, ref.links
+    for rank, status, outs in res:
+        assert status == 0, f"rank {rank}: an exchange timed out"
+        for k, (co, fc, mk, md, t, fl, ce, qq, hq, reran) in enumerate(outs):
+            np.testing.assert_array_equal(co, f._coords)
+            np.testing.assert_array_equal(fc, f._first_child)
+            np.testing.assert_array_equal(mk, f.marks.cpu().numpy())
+            assert md == ref.result.marked_detected and t == ref.result.cell_face_tests
+            np.testing.assert_array_equal(fl, ll.flags.cpu().numpy())
+            np.testing.assert_array_equal(ce, ll.cells.cpu().numpy())
+            np.testing.assert_array_equal(qq, ll.q.cpu().numpy())
+            np.testing.assert_array_equal(hq, ref.host_q())
+            # the first pass of a plan may outgrow the initial forest capacity
+            # and finish on the per-level host path (exchanging through the same
+            # DeviceComm); the second pass is sized from it and stays on the device
+            assert reran == (ref.reran if k == 0 else False)
+
+
 def test_marking_dense_soup_single_root(ow):
     """One root block next to 12 000 faces: hundreds of bin chunks survive the
     union-box cull per block (grouped chunk rounds); the forest equals the
