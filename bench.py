@@ -123,6 +123,80 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- GPU arm
+def e2e_stream(plan, rec_host, n_faces, args, l2_flush, barrier):
+    """End-to-end steps through the public API with pinned host bytes in and
+    the results out, as a stream of geometries: two plans alternate so the
+    transfers of one step overlap the device work of its neighbours.  Returns
+    (total ms of the timed steps minus the L2 flushes, per-pass ms, H2D bytes
+    per step, D2H bytes per step, slow-path steps)."""
+    import torch
+
+    from paper_2502_16310_b200 import pipeline
+
+    plans = [plan, pipeline.GridPlan(plan.domain, plan.root_dims, plan.params, plan.lattice, reuse_outputs=True,
+                                     comm=plan.comm)]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cs = torch.cuda.current_stream()
+    hs = torch.cuda.Stream()
+    bufs = [torch.empty_like(rec_host, device=dev) for _ in range(2)]
+    loaded = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+    for e in consumed:
+        e.record(cs)
+    W, K = max(args.warmup, 1), args.steps
+
+    def h2d(k):
+        with torch.cuda.stream(hs):
+            hs.wait_event(consumed[k % 2])  # the pass that read this buffer has finished
+            bufs[k % 2].copy_(rec_host, non_blocking=True)
+            loaded[k % 2].record(hs)
+
+    flushes = []
+    passes = []
+    slow, h2d_b, d2h_b = [], 0, 0
+    prev = None
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    h2d(-W)
+    for k in range(-W, K):
+        if k == 0:
+            if prev is not None:
+                prev.wait()  # warm-up results out of the way: the timed stream starts empty
+                prev = None
+            torch.cuda.synchronize()
+            start.record(cs)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(cs)
+        l2_flush()
+        f1.record(cs)
+        if k + 1 < K:  # step k+1's bytes start while step k computes (run() returns near a pass's end)
+            h2d(k + 1)
+        cs.wait_event(loaded[k % 2])
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(cs)
+        gp = plans[k % 2].run(bufs[k % 2], n_faces, host=True, defer=True)
+        p1.record(cs)
+        consumed[k % 2].record(cs)
+        if k >= 0:
+            flushes.append((f0, f1))
+            passes.append((p0, p1))
+            h2d_b = rec_host.numel()
+            hres = gp.host
+            d2h_b = sum(t.numel() * t.element_size() for k2, t in hres.items() if k2 != "coords")
+            d2h_b += sum(t.numel() * t.element_size() for t in hres["coords"])
+            if gp.reran or gp.host_copied & 5 != 5 or gp.done is None:
+                slow.append(k)
+        if prev is not None:
+            prev.wait()  # the host has step k-1's results
+        prev = gp
+    if prev is not None and prev.done is not None:
+        cs.wait_event(prev.done)
+    end.record(cs)
+    torch.cuda.synchronize()
+    total = start.elapsed_time(end) - sum(a.elapsed_time(b) for a, b in flushes)
+    return total, [a.elapsed_time(b) for a, b in passes], h2d_b, d2h_b, slow
+
+
 def gpu_arm(args, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -133,7 +207,6 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     numa = _lib.bind_host_numa(local_rank)  # pinned staging buffers on the GPU's socket (no-op on one node)
-    shard = parallel.Shard() if world > 1 else None
     data = make_input(cfg)
     dim = cfg["dim"]
     dom = ow.Aabb(np.zeros(dim), np.ones(dim))
@@ -150,11 +223,21 @@ def gpu_arm(args, cfg, rank, world, local_rank):
 
     from paper_2502_16310_b200 import pipeline
 
-    plan = (pipeline.GridPlan(dom, (cfg["root"],) * dim, params, cfg["lattice"], reuse_outputs=True)
+    # N > 1: the fused pass shards on the device (parallel.DeviceComm: marks,
+    # statistics, lattice flag words and q rows exchanged over peer memory by
+    # the native level loop, no host round trip per level); the 2D text
+    # configuration keeps the per-function path with torch.distributed
+    comm = shard = None
+    if world > 1 and not text:
+        cap_blocks = 32 * cfg["root"] ** dim
+        comm = parallel.DeviceComm(max(64 << 20, 4 * (4 ** dim) * cap_blocks))
+    elif world > 1:
+        shard = parallel.Shard()
+    plan = (pipeline.GridPlan(dom, (cfg["root"],) * dim, params, cfg["lattice"], reuse_outputs=True, comm=comm)
             if not text else None)
 
     def step(records):
-        if text or shard is not None:  # per-function path (reference call sequence, cli.py:87-113)
+        if text:  # per-function path (reference call sequence, cli.py:87-113)
             geom = ow.index_to_coords(ig) if text else ow.geometry.stl_records_to_coords(records, n_faces)
             forest = ow.init_root_grid(dom, (cfg["root"],) * dim, capacity=32 * cfg["root"] ** dim)
             res = ow.refine_near_wall(forest, geom, params, shard=shard)
@@ -225,12 +308,12 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         slow_path = []  # steps that reran the level loop or copied results from Python
         barrier()
         # k < 0: untimed warm-up (the first sizes the pinned result buffers)
-        for k in range(-max(args.warmup, 1), args.steps):
+        for k in (range(-max(args.warmup, 1), args.steps) if text else ()):
             l2_flush()
             if k >= 0:
                 ev2[k][0].record()
-            if text or shard is not None:
-                # per-function path (text primitives; sharded ranks): STL records
+            if text:
+                # per-function path (text primitives): STL records
                 # in from pinned memory, every result array out through torch copies
                 rd = None
                 h2d = 0
@@ -250,39 +333,37 @@ def gpu_arm(args, cfg, rank, world, local_rank):
                             pinned.append(torch.empty(2 * nbytes + 64, dtype=torch.uint8, pin_memory=True))
                     pinned[i][:nbytes].copy_(o.contiguous().view(-1).view(torch.uint8), non_blocking=True)
                     d2h += nbytes
-            else:
-                # pinned STL bytes in; the forest arrays stream back on a side stream
-                # while the lattice work runs, then the boundary rows (cells, q)
-                rd = rec_host.to(dev, non_blocking=True)
-                h2d = rec_host.numel()
-                gp = plan.run(rd, n_faces, host=True)
-                res, forest, ll = gp.result, gp.forest, gp.links
-                hres = gp.host
-                if k >= 0 and (gp.reran or gp.host_copied & 5 != 5):
-                    slow_path.append(k)
-                d2h = sum(t.numel() * t.element_size() for k2, t in hres.items() if k2 != "coords")
-                d2h += sum(t.numel() * t.element_size() for t in hres["coords"])
             torch.cuda.current_stream().synchronize()
             if k >= 0:
                 ev2[k][1].record()
+        if not text:
+            ms2_total, per, h2d, d2h, slow_path = e2e_stream(plan, rec_host, n_faces, args, l2_flush, barrier)
+            ev2 = None
         barrier()
-        ms2 = sum(a.elapsed_time(b) for a, b in ev2)
+        ms2 = sum(a.elapsed_time(b) for a, b in ev2) if ev2 else ms2_total
         t2 = torch.tensor([ms2], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
         ms2 = float(t2.item()) / args.steps
-        per = [a.elapsed_time(b) for a, b in ev2]
+        if ev2:
+            per = [a.elapsed_time(b) for a, b in ev2]
         log("e2e steps ms", " ".join(f"{x:.3f}" for x in per))
         per = sorted(per)
         e2e = {"value": T_step / (ms2 / 1e3), "unit": "cell-face tests/s", "ms_per_step": ms2,
                "ms_step_median": per[len(per) // 2], "ms_step_max": per[-1],
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "result": ("forest arrays (level, coords, parent, first_child, marks) + boundary cells and q"
-                          if text or shard is not None else
+                          if text else
                           "forest arrays (level, coords, parent, first_child, marks) + boundary rows packed: cell "
                           "ids, flag words and the q of the set bits (GridPass.host_q() expands to the dense rows)")}
-        if not text and shard is None:
+        if not text:
             e2e["slow_path_steps"] = slow_path
+            e2e["pipeline"] = ("two GridPlans alternate: step k+1's STL bytes go host->device on a copy stream while "
+                               "step k computes, step k's results come back device->host on the library's copy "
+                               "stream (GridPlan.run(host=True, defer=True)) while step k+1 computes, and the host "
+                               "waits for step k's results (GridPass.wait()) after enqueueing step k+1; "
+                               "ms_per_step = (device time from the first H2D to the last D2H - the L2 flushes "
+                               "between passes) / steps; ms_step_* = per-pass compute-stream times")
 
     gc.enable()
 
@@ -318,14 +399,16 @@ def gpu_arm(args, cfg, rank, world, local_rank):
                  f"full predicates x {FP32_OPS_PER_TEST[dim]} FP32 ops (the reference's _scan_block cascade on the "
                  f"pairs surviving its FP64 box cull; {int(sum(res.box_culls))} FP64 box culls not counted)", "mark")
     sw_ms, sw_n = prof["lattice_sweep"]
-    n_cb, n_rows, mt = lat_stats
-    per_mt = 45 if dim == 3 else 13
-    lattice = entry("k_lat_faces + k_lat_mt (boundary-link intersection sweep)", sw_ms, sw_n,
-                    per_mt * mt * args.steps,
-                    f"per step: {mt} {'Moller-Trumbore' if dim == 3 else 'segment-segment'} link-face tests x "
-                    f"{per_mt} FP32 ops ({n_rows} (block, face, direction) rows over {n_cb} candidate blocks; "
-                    f"every test is a link whose AABB meets the face AABB; rows of <= 16 cells are tested "
-                    f"inside k_lat_faces, larger ones by k_lat_mt)", "lattice")
+    n_cb, n_pairs, mt = lat_stats
+    # FP32 arithmetic of one watertight link-face test (oracle/lattice.py:wt_hits):
+    # 3D: per vertex 3 translations, 2 shear products, 2 shear differences (21),
+    # edge functions 6 + 3, det 2, T 3 + 3 + 2 = 40 (the division t = T / det
+    # only for candidate crossings, not counted); 2D (wt_hits2): 14
+    per_test = 40 if dim == 3 else 14
+    lattice = entry("k_lat_faces (boundary-link intersection sweep)", sw_ms, sw_n, per_test * mt * args.steps,
+                    f"per step: {mt} watertight link-face tests x {per_test} FP32 ops ({n_pairs} (block, face, "
+                    f"direction) rows over {n_cb} candidate blocks; every test is a link whose AABB meets the face "
+                    f"AABB)", "lattice")
     dominant = lattice if sw_ms >= mark_ms else mark
     roofline = dict(dominant)
     roofline["secondary"] = mark if dominant is lattice else lattice
@@ -368,8 +451,10 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         # (main() sets "config" to bench_config(): the same object as the reference arm's)
         "run": {"cell_face_tests_per_step": T_step, "pairs_evaluated_per_step": evaluated,
                 "blocks_per_level": blocks, "boundary_cells": n_boundary,
-                "parallelism": f"octree-block shards x{world}: marking and lattice links per rank slice, "
-                               f"all-gather of marks and of boundary links; bins/forest replicated"},
+                "parallelism": (f"octree-block shards x{world}: work-balanced marking slices and finest-leaf "
+                                f"lattice slices per rank, marks / statistics / flag words / q rows exchanged "
+                                f"over CUDA-IPC peer memory inside the native level loop; bins and forest "
+                                f"replicated" if world > 1 else "single GPU")},
         "roofline": roofline,
         "gpu_launches": int(launches),
         "host_numa_node": numa,

@@ -273,6 +273,18 @@ typedef struct {
   void* host_rows;          /* uint32[2 * host_row_cap]: (cell id, flag word) per row */
   void* host_q_packed;      /* float32[host_link_cap] */
   int64_t host_link_cap;
+  /* Deferred host copies (a stream of passes whose transfers overlap the
+   * next pass's device work): with copy_done (a cudaEvent_t of the caller)
+   * and device staging buffers of its own for the packed rows (dev_rows,
+   * dev_q_packed: one pair per caller-side plan), every D2H copy of the pass
+   * runs on the library's copy stream, copy_done is recorded after the last
+   * one and the call's stream does NOT wait for it; the next call with the
+   * same copy_done waits for it on the device before it reuses the outputs.
+   * The host results are valid once copy_done has completed. */
+  void* copy_done;
+  void* dev_rows;           /* uint32[2 * dev_row_cap] */
+  void* dev_q_packed;       /* float32[dev_link_cap] */
+  int64_t dev_row_cap, dev_link_cap;
 } ow_g2g_params;
 typedef struct {
   ow_face_summary faces;

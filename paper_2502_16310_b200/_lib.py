@@ -138,6 +138,11 @@ class G2GParamsC(C.Structure):  # ow_g2g_params
         ("host_rows", C.c_void_p),
         ("host_q_packed", C.c_void_p),
         ("host_link_cap", C.c_int64),
+        ("copy_done", C.c_void_p),
+        ("dev_rows", C.c_void_p),
+        ("dev_q_packed", C.c_void_p),
+        ("dev_row_cap", C.c_int64),
+        ("dev_link_cap", C.c_int64),
     ]
 
 

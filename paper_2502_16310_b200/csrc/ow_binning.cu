@@ -203,11 +203,12 @@ k_count_fast(GridC g, const float* __restrict__ c, int64_t n, unsigned long long
   ow_pdl_wait();
   int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool one = true;
+  int64_t lin = 0;
   if (f < n) {
     float v[3][3];
     load_face<D>(c, n, f, v);
     int loc = 0, mul = 1;
-    int64_t lin = 0, lmul = 1;
+    int64_t lmul = 1;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       float mn = v[0][a], mx = v[0][a];
@@ -226,8 +227,17 @@ k_count_fast(GridC g, const float* __restrict__ c, int64_t n, unsigned long long
     if (one) {
       masks[f] = 1ull << loc;
       nb[f] = 1;
-      atomicAdd(&counts[lin], 1);
     }
+  }
+  // warp-aggregated counts: consecutive faces of a fine mesh mostly share
+  // their bin, so one atomic per distinct bin of the warp (north star:
+  // "warp-aggregated atomic counts") instead of one per face
+  {
+    const bool add = f < n && one;
+    const int64_t key = add ? lin : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int lane = threadIdx.x & 31;
+    if (add && lane == __ffs(peers) - 1) atomicAdd(&counts[key], __popc(peers));
   }
   const bool walk = f < n && !one;
   const unsigned wm = __ballot_sync(0xffffffffu, walk);

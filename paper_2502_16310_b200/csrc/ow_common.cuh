@@ -342,10 +342,12 @@ __device__ __forceinline__ bool outside_domain(const GridC& g, const float* p) {
 // ---------------------------------------------------------------------------
 // forest device view + helpers
 // ---------------------------------------------------------------------------
+constexpr int OW_QLEV = 16;  // block edges of levels 0..15 precomputed on the host
 struct ForestC {
   int dim, max_level;
   int root[3];
   double dmin[3], dext[3];
+  double qlev[OW_QLEV][3];  // extent / (root * 2^level): the same IEEE division as block_len
   int64_t n;
   const int16_t* level;
   const int32_t* coord[3];
@@ -364,6 +366,9 @@ static inline ForestC make_forestc(const ow_forest* f) {
     c.dext[a] = f->dext[a];
     c.coord[a] = f->d_coord[a];
   }
+  for (int l = 0; l < OW_QLEV; ++l)
+    for (int a = 0; a < 3; ++a)
+      c.qlev[l][a] = a < f->dim ? f->dext[a] / (double)((int64_t)f->root[a] << l) : 1.0;
   c.n = f->n_blocks;
   c.level = f->d_level;
   c.parent = f->d_parent;
@@ -374,6 +379,9 @@ static inline ForestC make_forestc(const ow_forest* f) {
 
 // block edge per axis: extent / (root * 2^level)   (forest.py:152-161)
 __device__ __forceinline__ double block_len(const ForestC& F, int ax, int level) {
+  // (a table lookup for the usual levels: an FP64 division per block and axis
+  // was the heaviest part of the marking / links prologues)
+  if (level < OW_QLEV) return F.qlev[level][ax];
   return DDIV(F.dext[ax], (double)((int64_t)F.root[ax] << level));
 }
 

@@ -59,7 +59,10 @@ __device__ __forceinline__ void atomic_max_f(float* a, float v) {
 
 // small[0] first degenerate (u64 min), small[1] first non-finite (u64 min),
 // then floats: min[3], max[3], absmax at ((float*)(small+2))[0..6]
-__global__ void __launch_bounds__(256) k_face_check(int dim, const float* __restrict__ c, int64_t n, int64_t* small) {
+// (the dimension is a template parameter: the per-face vertex array then
+// lives in registers instead of local memory)
+template <int dim>
+__global__ void __launch_bounds__(256) k_face_check(const float* __restrict__ c, int64_t n, int64_t* small) {
   ow_pdl_wait();
   float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY}, am = 0.0f;
   float ext_sum = 0.0f;  // sum of per-face largest bounding-box sides (a work-shape estimate)
@@ -67,7 +70,9 @@ __global__ void __launch_bounds__(256) k_face_check(int dim, const float* __rest
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     float v[3][3];
     bool finite = true;
+#pragma unroll
     for (int j = 0; j < dim; ++j)
+#pragma unroll
       for (int a = 0; a < dim; ++a) {
         float x = c[((int64_t)j * dim + a) * n + k];
         v[j][a] = x;
@@ -81,8 +86,10 @@ __global__ void __launch_bounds__(256) k_face_check(int dim, const float* __rest
       continue;
     }
     float side = 0.0f;
+#pragma unroll
     for (int a = 0; a < dim; ++a) {
       float lo = v[0][a], hi = v[0][a];
+#pragma unroll
       for (int j = 1; j < dim; ++j) lo = fminf(lo, v[j][a]), hi = fmaxf(hi, v[j][a]);
       side = fmaxf(side, hi - lo);
     }
@@ -93,6 +100,7 @@ __global__ void __launch_bounds__(256) k_face_check(int dim, const float* __rest
       deg = DADD(DMUL(dx, dx), DMUL(dy, dy)) == 0.0;
     } else {  // geometry.py:287-297, FP64
       double u[3], w[3], z[3];
+#pragma unroll
       for (int a = 0; a < 3; ++a) {
         u[a] = DSUB((double)v[1][a], (double)v[0][a]);
         w[a] = DSUB((double)v[2][a], (double)v[0][a]);
@@ -225,7 +233,8 @@ int ow_face_check_launch(ow_ctx* ctx, int32_t dim, const float* d_coords, int64_
   ow_launch(k_face_check_init, 1, 1, 0, s, dst);
   OW_LAUNCHED(ctx);
   if (n > 0) {
-    ow_launch(k_face_check, ow_blocks(n, 256, 16 * OW_SMS), 256, 0, s, dim, d_coords, n, dst);
+    if (dim == 3) ow_launch(k_face_check<3>, ow_blocks(n, 256, 16 * OW_SMS), 256, 0, s, d_coords, n, dst);
+    else ow_launch(k_face_check<2>, ow_blocks(n, 256, 16 * OW_SMS), 256, 0, s, d_coords, n, dst);
     OW_LAUNCHED(ctx);
   }
   OW_CHECK_LAUNCH();

@@ -467,42 +467,34 @@ template <int D, int FPW>
 __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
-  constexpr int NCOMB = D == 3 ? 27 : 9;  // per-axis c in {-1, 0, +1}
   constexpr int FACES_PER_WARP = FPW, SLOT_LANES = 32 / FPW;
   __shared__ float4 s_face[4][FACES_PER_WARP][3];  // per warp: vertices (v0, v1, v2) / (a.xy, b.xy) of its faces
   __shared__ uint2 s_hit[4][HITBUF];
   __shared__ uint8_t s_hdir[4][HITBUF];
   __shared__ unsigned s_frame[QMAX];
   __shared__ float4 s_shear[QMAX];
-  __shared__ unsigned s_cinfo[NCOMB];  // combination -> direction | range-field shift per axis
   // 3D: candidate hits (T, det) + (flat cell, direction), divided 32 at a time
   __shared__ WtNum s_cnum[4][D == 3 ? CANDBUF : 1];
+  // the current batch of (<= 32) inline rows, staged in their own frames
+  __shared__ int4 s_rmeta[4][32];       // leaf position, first unit, packed box / axes / direction, kx*ky extent
+  __shared__ float4 s_rv[4][32][D];     // vertex j along (kx, ky, kz), shear j in .w
+  __shared__ float4 s_rc[4][32][D];     // cell centres of the leaf along kx, ky, kz
+  __shared__ uint8_t s_rlane[4][32];    // rank of a row with units -> its lane
   __shared__ uint2 s_cmeta[4][D == 3 ? CANDBUF : 1];
-  // the warp's current (face, finest leaf) pairs, one per lane: leaf
-  // position, face slot | valid combinations, first unit, per-axis ranges;
-  // per pair the cumulative units of its valid combinations (ascending) and
-  // the leaf's cell centres
-  __shared__ int4 s_pm[4][32];
-  __shared__ uint4 s_pr[4][32];
-  __shared__ uint16_t s_pre[4][32][NCOMB + 1];
-  __shared__ uint8_t s_pcomb[4][32][NCOMB];
-  __shared__ float4 s_pcen[4][32][D];
-  __shared__ uint8_t s_rlane[4][32];  // rank of a pair with units -> its lane
-  int nc = 0;                         // candidates buffered by this warp
+  int nc = 0;  // candidates buffered by this warp
   for (int i = threadIdx.x; i < QMAX; i += blockDim.x) {
     s_frame[i] = A.frame[i];
     s_shear[i] = A.shear[i];
   }
-  for (int i = threadIdx.x; i < NCOMB; i += blockDim.x) s_cinfo[i] = A.combo_info[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sl = lane % SLOT_LANES;
-  int nh = 0;                  // hits buffered by this warp
-  unsigned long long iru = 0;  // units << RU_ROW_BITS | (face, leaf) pairs of this warp (statistics)
+  int nh = 0;  // hits buffered by this warp
+  unsigned long long iru = 0;  // inline units / rows of this warp (statistics)
   // persistent warps take face groups from a global counter: the cost of a
-  // face (blocks in reach x combinations x cells) varies by orders of
-  // magnitude, so dynamic assignment replaces a static grid (whose single
-  // wave ended in a long tail of a few heavy warps)
+  // face (blocks in reach x rows x cells) varies by orders of magnitude, so
+  // dynamic assignment replaces the static one-group-per-warp grid (whose
+  // single wave ended in a long tail of a few heavy warps)
   for (;;) {
   unsigned long long grp = 0;
   if (lane == 0) grp = atomicAdd(A.face_next, 1ull);
@@ -537,6 +529,13 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
     } else {
       r0 = make_float4(v[0][0], v[0][1], v[1][0], v[1][1]);
     }
+    if (A.inline_units < C) {  // records for k_lat_mt (no large rows when every row is inline)
+      A.rec[3 * f + 0] = r0;
+      if (D == 3) {
+        A.rec[3 * f + 1] = r1;
+        A.rec[3 * f + 2] = r2;
+      }
+    }
     float4* sf = s_face[wid][lane / SLOT_LANES];
     sf[0] = r0;
     sf[1] = r1;
@@ -561,166 +560,219 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
   }
   const int max_slots = __reduce_max_sync(0xffffffffu, nslots);
   for (int s0 = 0; s0 < max_slots; s0 += SLOT_LANES) {
-    // ---- pairs: this lane's (face, finest leaf), its valid combinations and
-    // their cumulative unit counts (units of a combination = its cell box)
     const int slot = s0 + sl;
-    int units = 0;
+    int nrow = 0, pos = 0;
+    unsigned R[3] = {0u, 0u, 0u}, valid = 0u;
     if (slot < nslots) {
-      int32_t nc3[3] = {0, 0, 0};
+      int32_t nc[3] = {0, 0, 0};
       int rem = slot;
 #pragma unroll
       for (int a = 0; a < D; ++a) {  // rem / ext by a float reciprocal, corrected to exact
         if (a + 1 == D) {  // last axis: rem < ext
-          nc3[a] = k0[a] + rem;
+          nc[a] = k0[a] + rem;
           break;
         }
         int qd = (int)(__fmul_rz((float)rem, rext[a]));
         int rr = rem - qd * ext[a];
         while (rr < 0) rr += ext[a], --qd;
         while (rr >= ext[a]) rr -= ext[a], ++qd;
-        nc3[a] = k0[a] + rr;
+        nc[a] = k0[a] + rr;
         rem = qd;
       }
-      // finest leaf at lattice cell nc3: one load from the dense lattice table
+      // finest leaf at lattice cell nc: one load from the dense lattice table
       // (or the root-lattice descent when the level is too fine for one)
       int pn = -1;
       if (A.grid) {
-        int64_t lin = nc3[D - 1];
-        if (D == 3) lin = lin * A.gdim[1] + nc3[1];
-        pn = __ldg(A.grid + lin * A.gdim[0] + nc3[0]);
+        int64_t lin = nc[D - 1];
+        if (D == 3) lin = lin * A.gdim[1] + nc[1];
+        pn = __ldg(A.grid + lin * A.gdim[0] + nc[0]);
       } else {
         int depth;
-        const int node = locate(A.F, L, nc3, &depth);
+        const int node = locate(A.F, L, nc, &depth);
         if (depth == L && A.F.first_child[node] < 0) pn = A.pos_of[node];
       }
-      // (leaves outside this call's position slice belong to another rank)
-      if (pn >= A.pos_lo && pn < A.pos_hi) {
-        unsigned R[3] = {0u, 0u, 0u};
-        const float4* cg = reinterpret_cast<const float4*>(A.cen) + (int64_t)pn * D;
-        float4 cen4[3];
+      // (leaves outside this call's position slice belong to another rank; no
+      // early `continue` here: the whole warp must reach the shuffles below)
+      if (pn >= 0) {
+        if (pn >= A.pos_lo && pn < A.pos_hi) {
+          pos = pn;
 #pragma unroll
-        for (int a = 0; a < D; ++a) {
-          cen4[a] = __ldg(cg + a);
-          R[a] = axis_ranges(cen4[a], A.h[a], lo[a], hi[a]);
-        }
-        // directions with a non-empty cell box on every axis, as a mask over
-        // the 3^D combinations (outer product of the per-axis masks)
-        unsigned valid = A.dirmask;
+          for (int a = 0; a < D; ++a)
+            R[a] = axis_ranges(reinterpret_cast<const float4*>(A.cen)[(int64_t)pos * D + a], A.h[a], lo[a], hi[a]);
+          // directions with a non-empty cell box on every axis, as a mask over
+          // the 3^D combinations (outer product of the per-axis masks)
+          valid = A.dirmask;
 #pragma unroll
-        for (int a = 0; a < D; ++a) valid &= A.spread[a][(~R[a] >> 12) & 7u];
-        if (valid) {
-          int k = 0;
-          s_pre[wid][lane][0] = 0;
-          for (unsigned m = valid; m; m &= m - 1u) {
-            const int c = __ffs(m) - 1;
-            const unsigned info = s_cinfo[c];
-            int u = 1;
-#pragma unroll
-            for (int a = 0; a < D; ++a) u *= (int)((R[a] >> (((info >> (8 + 8 * a)) & 0xFFu) + 2)) & 3u) + 1;
-            units += u;
-            s_pcomb[wid][lane][k] = (uint8_t)c;
-            s_pre[wid][lane][++k] = (uint16_t)units;
-          }
-          A.has_pair[pn] = 1;
-          s_pm[wid][lane] = make_int4(pn, (int)(lane / SLOT_LANES) | k << 8, 0, 0);
-          s_pr[wid][lane] = make_uint4(R[0], R[1], R[2], 0u);
-#pragma unroll
-          for (int a = 0; a < D; ++a) s_pcen[wid][lane][a] = cen4[a];
+          for (int a = 0; a < D; ++a) valid &= A.spread[a][(~R[a] >> 12) & 7u];
+          nrow = __popc(valid);
+          if (nrow) A.has_pair[pos] = 1;
         }
       }
     }
-    // ---- units: the pairs' (combination, cell) tests flattened over the warp
-    int si = units;
+    int incl = nrow;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, si, o);
-      if (lane >= o) si += y;
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    const int S = __shfl_sync(0xffffffffu, si, 31);
-    if (!S) continue;
-    const int se = si - units;
-    const unsigned nzm = __ballot_sync(0xffffffffu, units > 0);
-    iru += ((unsigned long long)S << RU_ROW_BITS) + (unsigned long long)__popc(nzm);
-    if (units > 0) {
-      s_pm[wid][lane].z = se;
-      s_rlane[wid][__popc(nzm & lanemask_lt())] = (uint8_t)lane;
-    }
-    __syncwarp();
-    int base = 0, carry = 0;  // pairs started before the window / the pair owning its first unit
-    for (int u0 = 0; u0 < S; u0 += 32) {
-      const int u = u0 + lane;
-      // owner of unit u: the last pair starting at or before u (one bit per
-      // pair start in this 32-unit window, pairs in lane order)
-      const unsigned sb = (units > 0 && se >= u0 && se < u0 + 32) ? 1u << (se - u0) : 0u;
-      const unsigned M = __reduce_or_sync(0xffffffffu, sb);
-      const int kr = __popc(M & (lanemask_lt() | (1u << lane)));
-      const int jl = kr ? (int)s_rlane[wid][base + kr - 1] : carry;
-      base += __popc(M);
-      carry = M ? (int)s_rlane[wid][base - 1] : carry;
-      bool hit = false, cand = false;
-      float t = 0.0f;
-      unsigned cellg = 0;
-      int d = 0;
-      WtNum num{0.0f, 0.0f};
-      if (u < S) {
-        const int4 pm = s_pm[wid][jl];
-        const int k = u - pm.z;
-        // combination of unit k: the last with cumulative units <= k
-        const uint16_t* pre = s_pre[wid][jl];
-        int lo_i = 0, hi_i = (pm.y >> 8);  // pre[lo_i] <= k < pre[hi_i]
-        while (hi_i - lo_i > 1) {
-          const int mid = (lo_i + hi_i) >> 1;
-          if ((int)pre[mid] <= k) lo_i = mid;
-          else hi_i = mid;
-        }
-        const int c = s_pcomb[wid][jl][lo_i];
-        int r = k - (int)pre[lo_i];
-        const unsigned info = s_cinfo[c];
-        d = (int)(info & 0xFFu);
-        const uint4 pr = s_pr[wid][jl];
-        const unsigned Rj[3] = {pr.x, pr.y, pr.z};
-        float x[3];
-        int cell = 0;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (!total) continue;
+    const int excl = incl - nrow;
+    const int fi = (int)f;
+    for (int r0 = 0; r0 < total; r0 += 32) {
+      const int r = r0 + lane;
+      const int4 row = row_of<D>(r, excl, valid, R, pos, fi, A);  // units 0 past the end
+      const int units = row.w;
+      // rows of more than INLINE_UNITS cells go to k_lat_mt (load-balanced over
+      // units): one packed reservation of rows and units per chunk, so row
+      // order and unit order agree and unit offsets stay monotone
+      const bool big = units > A.inline_units;
+      const unsigned bm = __ballot_sync(0xffffffffu, big);
+      if (bm) {
+        const int ub = big ? units : 0;
+        int ui = ub;
 #pragma unroll
-        for (int a = 0; a < D; ++a) {  // cell box of combination c on axis a: i0 | (ext - 1) << 2
-          const unsigned fa = (Rj[a] >> ((info >> (8 + 8 * a)) & 0xFFu)) & 0xFu;
-          int i;
-          if (a + 1 < D) {
-            const int e = (int)(fa >> 2) + 1;
-            const int qd = div_small(r, e);
-            i = (int)(fa & 3u) + (r - qd * e);
-            r = qd;
-          } else {
-            i = (int)(fa & 3u) + r;
-          }
-          cell |= i << (2 * a);
-          x[a] = reinterpret_cast<const float*>(&s_pcen[wid][jl][a])[i];
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, ui, o);
+          if (lane >= o) ui += y;
         }
-        cellg = (unsigned)pm.x * (unsigned)C + (unsigned)cell;
-        const float* F = reinterpret_cast<const float*>(s_face[wid][pm.y & 0xFF]);
-        if (D == 3) cand = wt_cand3(x, F, s_frame[d], s_shear[d], num);
-        else hit = wt_test2(x, F, s_frame[d], s_shear[d], t);
-      }
-      if (D == 3) {
-        const unsigned cm = __ballot_sync(0xffffffffu, cand);
-        if (cm) {
-          if (cand) {
-            const int k = nc + __popc(cm & lanemask_lt());
-            s_cnum[wid][k] = num;
-            s_cmeta[wid][k] = make_uint2(cellg, (unsigned)d);
-          }
-          nc += __popc(cm);
-          __syncwarp();
-          if (nc >= 32) {  // a full warp of divisions
-            nh = drain_cands(A, s_cnum[wid], s_cmeta[wid], nc, 32, s_hit[wid], s_hdir[wid], nh, lane);
-            nc -= 32;
+        const unsigned long long tu = (unsigned long long)__shfl_sync(0xffffffffu, ui, 31);
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(A.ru_d, (tu << RU_ROW_BITS) | (unsigned long long)__popc(bm));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (big) {
+          const int64_t k = (int64_t)(base & RU_ROW_MASK) + __popc(bm & lanemask_lt());
+          const int64_t u = (int64_t)(base >> RU_ROW_BITS) + ui - ub;
+          if (k < A.row_cap && u + ub <= A.unit_cap) {
+            A.rows[k] = row;
+            A.rowoff[k] = u;
+            for (int64_t t = (u + MT_TILE - 1) / MT_TILE; t * MT_TILE < u + ub; ++t) A.tile_row[t] = (int32_t)k;
           }
         }
-      } else {
-        nh = record_hits(A, s_hit[wid], s_hdir[wid], nh, hit, cellg, d, t, lane);
       }
+      // the other rows: their units flattened over the warp and tested here
+      const int us = big ? 0 : units;
+      int si = us;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, si, o);
+        if (lane >= o) si += y;
+      }
+      const int S = __shfl_sync(0xffffffffu, si, 31);
+      const int se = si - us;
+      iru += ((unsigned long long)S << RU_ROW_BITS) + (unsigned long long)__popc(__ballot_sync(0xffffffffu, us > 0));
+      if (!S) continue;
+      // Stage the batch's rows in the row's own watertight frame: the face's
+      // vertices permuted to (kx, ky, kz) with the shears in .w, the leaf's
+      // cell centres per permuted axis, and the cell box along the permuted
+      // axes (units run kx-fastest; the order of a row's units is free).  A
+      // unit then costs one owner lookup, a few shared loads and the test —
+      // no per-unit shuffles, frame selects or global loads.
+      const unsigned nzm = __ballot_sync(0xffffffffu, us > 0);
+      if (us > 0) {
+        const unsigned w = (unsigned)row.z;
+        const int d = (int)(w & 31u);
+        const unsigned fr = s_frame[d];
+        const unsigned kx = fr & 3u, ky = (fr >> 2) & 3u, kz = (fr >> 4) & 3u;
+        const unsigned k3[3] = {kx, D == 3 ? ky : kz, kz};  // permuted axis order (2D: kx, kz)
+        unsigned pk = (unsigned)d << 26;
+        int ext[3] = {1, 1, 1};
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+          const unsigned ra = (w >> (5 + 4 * k3[q])) & 0xFu;  // i0 | (ext-1) << 2 of axis k3[q]
+          ext[q] = (int)(ra >> 2) + 1;
+          pk |= (ra & 3u) << (2 * q) | (ra >> 2) << (6 + 2 * q) | k3[q] << (12 + 2 * q);
+        }
+        s_rmeta[wid][lane] = make_int4(row.x, se, (int)pk, ext[0] * (D == 3 ? ext[1] : 1));
+        const float* F = reinterpret_cast<const float*>(s_face[wid][row.y - fbase]);
+        const float4 sh = s_shear[d];
+        const float shv[3] = {sh.x, sh.y, sh.z};
+        const float4* cg = reinterpret_cast<const float4*>(A.cen) + (int64_t)row.x * D;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {  // vertex j along the permuted axes, shear j in .w
+          if (D == 3)
+            s_rv[wid][lane][j] = make_float4(F[4 * j + kx], F[4 * j + ky], F[4 * j + kz], shv[j]);
+          else
+            s_rv[wid][lane][j] = make_float4(F[2 * j + kx], F[2 * j + kz], 0.0f, j ? sh.z : sh.x);
+        }
+#pragma unroll
+        for (int q = 0; q < D; ++q) s_rc[wid][lane][q] = __ldg(cg + k3[q]);
+      }
+      // rank -> lane of the rows with units (rows are in lane order)
+      if (us > 0) s_rlane[wid][__popc(nzm & lanemask_lt())] = (uint8_t)lane;
+      __syncwarp();
+      int base = 0, carry = 0;  // rows started before the window / the row owning its first unit
+      for (int u0 = 0; u0 < S; u0 += 32) {
+        const int u = u0 + lane;
+        // owner of unit u: the last row starting at or before u (one bit per
+        // row start in this 32-unit window)
+        const unsigned sb = (us > 0 && se >= u0 && se < u0 + 32) ? 1u << (se - u0) : 0u;
+        const unsigned M = __reduce_or_sync(0xffffffffu, sb);
+        const int kr = __popc(M & (lanemask_lt() | (1u << lane)));
+        const int jl = kr ? (int)s_rlane[wid][base + kr - 1] : carry;
+        base += __popc(M);
+        carry = M ? (int)s_rlane[wid][base - 1] : carry;
+        bool hit = false;
+        float t = 0.0f;
+        unsigned cellg = 0;
+        int d = 0;
+        if (D == 3) {
+          bool cand = false;
+          WtNum num{0.0f, 0.0f};
+          if (u < S) {
+            const int4 m = s_rmeta[wid][jl];
+            const unsigned pk = (unsigned)m.z;
+            d = (int)(pk >> 26);
+            int k = u - m.y;
+            const int e0 = (int)((pk >> 6) & 3u) + 1, e1 = (int)((pk >> 8) & 3u) + 1;
+            const int q0 = div_small(k, e0);
+            const int j0 = k - q0 * e0;
+            const int j2 = div_small(q0, e1);
+            const int j1 = q0 - j2 * e1;
+            const int c0 = (int)(pk & 3u) + j0, c1 = (int)((pk >> 2) & 3u) + j1, c2 = (int)((pk >> 4) & 3u) + j2;
+            const float4* rc = s_rc[wid][jl];
+            const float x0 = reinterpret_cast<const float*>(&rc[0])[c0];
+            const float x1 = reinterpret_cast<const float*>(&rc[1])[c1];
+            const float x2 = reinterpret_cast<const float*>(&rc[2])[c2];
+            const int cell = c0 << (2 * ((pk >> 12) & 3u)) | c1 << (2 * ((pk >> 14) & 3u)) | c2 << (2 * ((pk >> 16) & 3u));
+            cellg = (unsigned)m.x * (unsigned)C + (unsigned)cell;
+            cand = wt_cand_perm(x0, x1, x2, s_rv[wid][jl], num);
+          }
+          const unsigned cm = __ballot_sync(0xffffffffu, cand);
+          if (cm) {
+            if (cand) {
+              const int k = nc + __popc(cm & lanemask_lt());
+              s_cnum[wid][k] = num;
+              s_cmeta[wid][k] = make_uint2(cellg, (unsigned)d);
+            }
+            nc += __popc(cm);
+            __syncwarp();
+            if (nc >= 32) {  // a full warp of divisions
+              nh = drain_cands(A, s_cnum[wid], s_cmeta[wid], nc, 32, s_hit[wid], s_hdir[wid], nh, lane);
+              nc -= 32;
+            }
+          }
+        } else {
+          if (u < S) {
+            const int4 m = s_rmeta[wid][jl];
+            const unsigned pk = (unsigned)m.z;
+            d = (int)(pk >> 26);
+            const int k = u - m.y;
+            const int e0 = (int)((pk >> 6) & 3u) + 1;
+            const int j1 = div_small(k, e0);
+            const int c0 = (int)(pk & 3u) + (k - j1 * e0), c1 = (int)((pk >> 2) & 3u) + j1;
+            const float4* rc = s_rc[wid][jl];
+            const float xx = reinterpret_cast<const float*>(&rc[0])[c0];
+            const float xz = reinterpret_cast<const float*>(&rc[1])[c1];
+            const int cell = c0 << (2 * ((pk >> 12) & 3u)) | c1 << (2 * ((pk >> 14) & 3u));
+            cellg = (unsigned)m.x * (unsigned)C + (unsigned)cell;
+            hit = wt_test_perm2(xx, xz, s_rv[wid][jl], t);
+          }
+          nh = record_hits(A, s_hit[wid], s_hdir[wid], nh, hit, cellg, d, t, lane);
+        }
+      }
+      __syncwarp();  // the staged rows are rewritten by the next batch
     }
-    __syncwarp();  // the staged pairs are rewritten by the next slot batch
   }
   __syncwarp();  // s_face is rewritten by the next group
   }

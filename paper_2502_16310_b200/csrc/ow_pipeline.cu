@@ -504,6 +504,9 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
     ow_set_error("cannot refine around empty geometry");
     return OW_ERR_INVALID;
   }
+  // deferred host copies of this caller's previous pass still read its
+  // outputs: the device waits for them before anything is rewritten
+  if (p->copy_done) OW_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)p->copy_done, 0));
   if (d_records) OW_TRY(ow_stl_binary_to_soa(ctx, d_records, n_faces, d_coords, stream));
   // the face check's summary is read with the first bin-count readback (one
   // host round trip less) and validated there, before anything depends on it
@@ -559,16 +562,20 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
     side = true;
   }
   // from here on every return path (errors included) joins the side stream
-  // into `s`: the caller may reuse the forest storage on `s` as soon as the
-  // call returns, and the copies still read it
+  // into `s` — the caller may reuse the forest storage on `s` as soon as the
+  // call returns, and the copies still read it — or, with deferred copies,
+  // records copy_done after them (the caller's next pass waits for it)
   struct JoinCopies {
     ow_ctx* ctx;
     cudaStream_t s;
+    cudaEvent_t done;
     bool on;
     ~JoinCopies() {
-      if (on) cudaStreamWaitEvent(s, ctx->copy_ev[1], 0);
+      if (!on) return;
+      if (done) cudaEventRecord(done, ctx->copy_stream);
+      else cudaStreamWaitEvent(s, ctx->copy_ev[1], 0);
     }
-  } join{ctx, s, side};
+  } join{ctx, s, (cudaEvent_t)p->copy_done, side};
   if (p->lattice_q < 2 || !p->alloc) return ow_stage_times(ctx, &out->nw);
   void* pl;
   OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(f->n_blocks + 1), s, &pl));
@@ -613,7 +620,14 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
                       nb > 0;
   uint32_t* d_rows = nullptr;
   float* d_qp = nullptr;
-  if (packed) {
+  // deferred copies need staging buffers of the caller's own (the next pass
+  // of another plan reuses the context's scratch while these copies run)
+  const bool deferred = p->copy_done && side && packed && p->dev_rows && p->dev_q_packed &&
+                        p->dev_row_cap >= nb && p->dev_link_cap >= n_links;
+  if (deferred) {
+    d_rows = (uint32_t*)p->dev_rows;
+    d_qp = (float*)p->dev_q_packed;
+  } else if (packed) {
     void *pr, *pq;
     OW_TRY(ow_slot(ctx, SLOT_LAT_RFLAGS, 8 * (size_t)nb, s, &pr));
     OW_TRY(ow_slot(ctx, SLOT_LAT_QPACK, 4 * (size_t)n_links, s, &pq));
@@ -623,7 +637,15 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
   const int est = ow_lattice_links_emit_packed(ctx, (int64_t*)cells, (float*)q, d_rows, d_qp, stream);
   ctx->lat_comm = nullptr;
   OW_TRY(est);
-  if (packed) {  // (8 + 4 popc) bytes per row instead of 8 + 4 Q: the host tail is the transfer
+  if (deferred) {  // the packed rows travel on the copy stream, after the forest arrays
+    join.on = false;
+    OW_CUDA(cudaEventRecord(ctx->copy_ev[0], s));
+    OW_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->copy_ev[0], 0));
+    OW_CUDA(cudaMemcpyAsync(p->host_rows, d_rows, 8 * (size_t)nb, cudaMemcpyDeviceToHost, ctx->copy_stream));
+    OW_CUDA(cudaMemcpyAsync(p->host_q_packed, d_qp, 4 * (size_t)n_links, cudaMemcpyDeviceToHost, ctx->copy_stream));
+    OW_CUDA(cudaEventRecord((cudaEvent_t)p->copy_done, ctx->copy_stream));
+    out->host_copied |= 4 | 8;
+  } else if (packed) {  // (8 + 4 popc) bytes per row instead of 8 + 4 Q: the host tail is the transfer
     OW_CUDA(cudaMemcpyAsync(p->host_rows, d_rows, 8 * (size_t)nb, cudaMemcpyDeviceToHost, s));
     OW_CUDA(cudaMemcpyAsync(p->host_q_packed, d_qp, 4 * (size_t)n_links, cudaMemcpyDeviceToHost, s));
     out->host_copied |= 4;
@@ -632,9 +654,10 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
     OW_CUDA(cudaMemcpyAsync(p->host_q, q, 4 * (size_t)nb * p->lattice_q, cudaMemcpyDeviceToHost, s));
     out->host_copied |= 2;
   }
-  if (side) {  // results complete on `s`
+  if (side && !deferred) {  // results complete on `s`
     join.on = false;
     OW_CUDA(cudaStreamWaitEvent(s, ctx->copy_ev[1], 0));
+    if (p->copy_done) OW_CUDA(cudaEventRecord((cudaEvent_t)p->copy_done, s));
   }
   OW_TRY(ow_lattice_stats(ctx, out->lattice_stats, stream));
   return ow_stage_times(ctx, &out->nw);  // host work overlapping the emit kernels

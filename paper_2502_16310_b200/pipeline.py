@@ -43,7 +43,16 @@ class GridPass:
     links: LatticeLinks | None
     host: dict | None = None  # pinned host copies of the results (run(host=True))
     reran: bool = False  # the device-resident level loop outgrew the capacity; rerun with host sync
-    host_copied: int = 0  # native host copies made (bit 0 forest, bit 2 packed rows); else Python copied
+    host_copied: int = 0  # native host copies made (bit 0 forest, bit 2 packed rows, bit 3 deferred)
+    done: object = None  # torch.cuda.Event of deferred host copies (run(defer=True)); None: already ordered
+
+    def wait(self):
+        """Block until the host copies of this pass are complete (the
+        deferred copies' event, else the current stream)."""
+        if self.done is not None:
+            self.done.synchronize()
+        else:
+            torch.cuda.current_stream().synchronize()
 
     def host_q(self) -> np.ndarray:
         """Dense (boundary rows, Q) float32 q from the packed host copy (-1 where
@@ -107,6 +116,8 @@ class GridPlan:
         self._forest = None
         self._setup = None  # (n_faces, _driver_setup result): the parts that depend on n_faces only
         self._gp0 = _lib.G2GParamsC()  # static fields of the call's parameter struct
+        self._done = None  # torch.cuda.Event: the last pass's deferred host copies
+        self._dev_rows = self._dev_qp = None  # device staging of the packed rows (deferred passes)
         if self.dirs is not None:
             self._gp0.lattice_q = len(self.dirs)
             for i, v in enumerate(self.dirs.reshape(-1)):
@@ -134,7 +145,7 @@ class GridPlan:
         return torch.empty(max(int(n), 1), dtype=dtype, pin_memory=True)
 
     def run(self, records: torch.Tensor | None = None, n_faces: int | None = None,
-            geometry: CoordListGeometry | None = None, host: bool = False) -> GridPass:
+            geometry: CoordListGeometry | None = None, host: bool = False, defer: bool = False) -> GridPass:
         """Binary STL records (device uint8, 50 bytes per face, after the
         84-byte header) — or an existing ``geometry`` — to a refined forest and
         its finest-level lattice links.
@@ -145,7 +156,14 @@ class GridPlan:
         arrays stream to the host on a side stream while the lattice work
         runs; the boundary rows travel packed ((8 + 4 popc) bytes per row
         instead of 8 + 4 Q) and ``GridPass.host_q()`` expands them to the
-        dense (rows, Q) array."""
+        dense (rows, Q) array.
+
+        ``defer=True`` (with ``host=True``): every host copy of the pass runs
+        on the library's copy stream and the current stream does not wait for
+        them, so they overlap whatever is enqueued next (another plan's pass:
+        alternate two plans to stream geometries); ``GridPass.wait()`` blocks
+        until they are done.  The plan's next pass waits for them on the
+        device before it rewrites its outputs."""
         if geometry is None and records is None:
             raise InvalidParameterError("geometry_to_grid needs STL records or a geometry")
         dim = self.dim
@@ -222,6 +240,20 @@ class GridPlan:
             gp.host_row_cap = nrow
             gp.host_rows, gp.host_q_packed = hbuf["rows"].data_ptr(), hbuf["q_packed"].data_ptr()
             gp.host_link_cap = hb["q_packed"].numel()
+        if self._done is not None or (host and defer):
+            if self._done is None:
+                self._done = torch.cuda.Event()
+                self._done.record()  # (creates the CUDA event; completes at once)
+            gp.copy_done = self._done.cuda_event
+        gp.dev_rows = gp.dev_q_packed = None
+        gp.dev_row_cap = gp.dev_link_cap = 0
+        if host and defer:
+            nrow, nlink = gp.host_row_cap, gp.host_link_cap
+            if self._dev_rows is None or self._dev_rows.numel() < 2 * nrow or self._dev_qp.numel() < nlink:
+                self._dev_rows = torch.empty(2 * nrow, dtype=torch.int32, device=self.dev)
+                self._dev_qp = torch.empty(nlink, dtype=torch.float32, device=self.dev)
+            gp.dev_rows, gp.dev_q_packed = self._dev_rows.data_ptr(), self._dev_qp.data_ptr()
+            gp.dev_row_cap, gp.dev_link_cap = nrow, nlink
         out = _lib.G2GResultC()
         g, bins_t = st["g"], st["bins_t"]
         v = forest.view()
@@ -268,7 +300,8 @@ class GridPlan:
         hres = None
         if host:
             hres = self._host_results(hbuf, int(out.host_copied), forest, links, int(out.n_links))
-        return GridPass(geom, forest, result, links, hres, bool(out.reran), int(out.host_copied))
+        done = self._done if int(out.host_copied) & 8 else None
+        return GridPass(geom, forest, result, links, hres, bool(out.reran), int(out.host_copied), done)
 
     def _host_results(self, hbuf, copied, forest, links, n_links):
         """Pinned host copies (the C side streamed whatever fit; the rest is

@@ -646,6 +646,58 @@ def test_grid_plan_reuse_equal_sizes(ow):
         prev = ((gp.links.n_boundary, gp.links.leaves.numel()), gp.links)
 
 
+def test_grid_plan_deferred_host_copies(ow):
+    """run(host=True, defer=True) with two plans alternating over a stream of
+    geometries (the e2e bench's pipeline): host copies of one pass overlap the
+    next pass; after GridPass.wait() every pass's host results equal a
+    synchronous pass's, and a plan's next pass does not clobber outputs its
+    previous pass is still copying."""
+    import torch
+
+    from paper_2502_16310_b200 import pipeline, shapes
+
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8)
+    plans = [pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19", reuse_outputs=True) for _ in range(2)]
+    geoms = [shapes.icosphere_triangles(s, radius=r) for s, r in ((3, 0.3), (3, 0.25), (2, 0.3), (3, 0.3))] * 2
+    recs = []
+    for t in geoms:
+        data = shapes.binary_stl_bytes(t)
+        recs.append((torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda(),
+                     int.from_bytes(data[80:84], "little")))
+    refs = []
+    for rec, n in recs:
+        r = pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19").run(rec, n, host=True)
+        torch.cuda.synchronize()
+        refs.append({k: (v.clone() if isinstance(v, torch.Tensor) else [c.clone() for c in v])
+                     for k, v in r.host.items()})
+    pending = []
+    deferred = 0
+    for k, (rec, n) in enumerate(recs):
+        gp = plans[k % 2].run(rec, n, host=True, defer=True)
+        # (a pass whose results outgrow the buffers sized from its plan's last
+        # pass falls back to synchronous copies; the others are deferred)
+        deferred += int(gp.done is not None and bool(gp.host_copied & 8))
+        pending.append((k, gp))
+        if len(pending) == 2:  # the host reads step k-1 after step k is enqueued
+            j, g = pending.pop(0)
+            g.wait()
+            _check_host(g.host, refs[j], j)
+    assert deferred >= 4
+    for j, g in pending:
+        g.wait()
+        _check_host(g.host, refs[j], j)
+
+
+def _check_host(h, ref, j):
+    import torch
+
+    for key in ("level", "parent", "first_child", "marks", "cells", "flags", "q_packed"):
+        assert torch.equal(h[key], ref[key]), (j, key)
+    for a, b in zip(h["coords"], ref["coords"]):
+        assert torch.equal(a, b), (j, "coords")
+
+
 def test_two_host_threads_concurrently(ow):
     """The entry points are safe to call from several host threads at once
     (SPEC.md:133, 218): each thread gets its own context, so two threads
