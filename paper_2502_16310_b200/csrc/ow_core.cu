@@ -35,6 +35,9 @@ extern "C" int ow_ctx_create(int device, ow_ctx** out) {
   c->prep_key = -1;
   cudaError_t e = cudaMallocHost((void**)&c->h_pinned, OW_PINNED_WORDS * sizeof(int64_t));
   if (e == cudaSuccess) e = cudaMalloc((void**)&c->d_small, 64 * sizeof(int64_t));
+  // (the readbacks copy contiguous runs of these words, spare ones included:
+  // defined from the start, compute-sanitizer initcheck stays clean)
+  if (e == cudaSuccess) e = cudaMemset(c->d_small, 0, 64 * sizeof(int64_t));
   if (e != cudaSuccess) {
     ow_set_error("ow_ctx_create: %s", cudaGetErrorString(e));
     free(c);
