@@ -285,6 +285,8 @@ typedef struct {
   void* dev_rows;           /* uint32[2 * dev_row_cap] */
   void* dev_q_packed;       /* float32[dev_link_cap] */
   int64_t dev_row_cap, dev_link_cap;
+  int32_t no_stage_times;   /* 1: no stage-timing events in the level loop (an event between two
+                               kernels stops their programmatic overlap); stage_ms reads 0 */
 } ow_g2g_params;
 typedef struct {
   ow_face_summary faces;

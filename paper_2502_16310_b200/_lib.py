@@ -143,6 +143,7 @@ class G2GParamsC(C.Structure):  # ow_g2g_params
         ("dev_q_packed", C.c_void_p),
         ("dev_row_cap", C.c_int64),
         ("dev_link_cap", C.c_int64),
+        ("no_stage_times", C.c_int32),
     ]
 
 

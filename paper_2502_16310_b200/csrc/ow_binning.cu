@@ -431,7 +431,7 @@ int fill_count(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, 
   OW_TRY(ow_slot(ctx, SLOT_BIN_FOFF, 4 * (size_t)n, s, &pfo));
   OW_TRY(ow_slot(ctx, SLOT_BIN_SLOW, 4 * (size_t)n, s, &psl));
   int64_t* small = ctx->d_small;
-  OW_CUDA(cudaMemsetAsync(counts, 0, 4 * (size_t)n_bins, s));
+  OW_TRY(ow_fill_async(ctx, counts, 0, 4 * (size_t)n_bins, s));
   ow_launch(k_small_init, 1, 32, 0, s, small);  // [1], [3] = -1 (none), rest 0
   OW_LAUNCHED(ctx);
   void* pmid;

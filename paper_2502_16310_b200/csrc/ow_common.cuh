@@ -154,6 +154,7 @@ struct ow_ctx {
   cudaStream_t copy_stream;       // side stream for result copies (lazily created)
   cudaEvent_t copy_ev[2];         // [0] forest final, [1] copies done
   bool defer_stage_times;
+  bool no_stage_events;  // fused pass without stage-timing events (ow_g2g_params.no_stage_times)
   // fused pass: the face check's summary words on the device, not yet read
   // (ow_faces_settle reads them with the next readback and validates)
   const int64_t* faces_pending;
@@ -213,6 +214,9 @@ int ow_refine_marked_counted(ow_ctx* ctx, ow_forest* f, int32_t level, int64_t* 
 // Scratch slot of at least `bytes`; contents are preserved across calls unless
 // the slot grows (then it is reallocated, stream-ordered, uninitialised).
 int ow_slot(ow_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out);
+
+// cudaMemsetAsync semantics as a PDL kernel (hot paths)
+int ow_fill_async(ow_ctx* ctx, void* p, int value, size_t bytes, cudaStream_t s);
 
 // Copy n int64 device values to host and synchronise.
 int ow_readback(ow_ctx* ctx, const int64_t* d_src, int n, int64_t* h_dst, cudaStream_t s);

@@ -141,3 +141,33 @@ bool ow_pdl_enabled() {
   }();
   return on;
 }
+
+// ---------------------------------------------------------------------------
+// memset as a kernel: it joins the programmatic-dependent-launch chain of the
+// kernels around it (a cudaMemsetAsync node breaks the overlap and costs a
+// launch bubble in the level loop)
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void k_fill(uint32_t* __restrict__ w, int64_t n_words, uint8_t* __restrict__ tail, int n_tail, uint32_t v) {
+  ow_pdl_wait();
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t i = i0; i < n_words; i += (int64_t)gridDim.x * blockDim.x) w[i] = v;
+  if (i0 < n_tail) tail[i0] = (uint8_t)v;
+}
+}  // namespace
+
+int ow_fill_async(ow_ctx* ctx, void* p, int value, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return OW_OK;
+  if (((uintptr_t)p & 3u) != 0) {
+    OW_CUDA(cudaMemsetAsync(p, value, bytes, s));
+    return OW_OK;
+  }
+  const uint32_t b = (uint32_t)(value & 0xFF);
+  const int64_t n_words = (int64_t)(bytes >> 2);
+  const int n_tail = (int)(bytes & 3u);
+  ow_launch(k_fill, ow_blocks(n_words > 0 ? n_words : 1, 256, 4 * OW_SMS), 256, 0, s, (uint32_t*)p, n_words,
+            (uint8_t*)p + 4 * n_words, n_tail, b | b << 8 | b << 16 | b << 24);
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  return OW_OK;
+}

@@ -515,7 +515,7 @@ int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64
   OW_TRY(ow_slot(ctx, SLOT_FOREST_FLAG, (size_t)cap + 8, s, &pf));
   OW_PROF_BEGIN(ctx, PROF_REFINE, s);
   ow_launch(k_rs_init, 1, 64, 0, s, d_st, n, d_nb);
-  OW_CUDA(cudaMemsetAsync(pf, 0, (size_t)cap, s));
+  OW_TRY(ow_fill_async(ctx, pf, 0, (size_t)cap, s));
   OW_TRY(scan01(ctx, SplitLoad{make_forestc(f), level, d_st + RS_INTER}, CompactStore{(int32_t*)pl},
                 d_nb ? cap : n, d_st + RS_CR, s, d_nb));
   const ow_forest fv = *f;

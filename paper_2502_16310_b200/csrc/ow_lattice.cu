@@ -1319,11 +1319,11 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
     ctx->lat_grid_on = cells <= (int64_t(1) << 26) && !getenv("OW_LAT_NO_GRID");
     if (ctx->lat_grid_on) OW_TRY(ow_slot(ctx, SLOT_LAT_GRID, 4 * (size_t)cells, s, &p));
   }
-  OW_CUDA(cudaMemsetAsync(ctx->d_small + 48, 0, 5 * 8, s));
-  OW_CUDA(cudaMemsetAsync(d_flags, 0, 4 * (size_t)n_leaves * C, s));
+  OW_TRY(ow_fill_async(ctx, ctx->d_small + 48, 0, 5 * 8, s));
+  OW_TRY(ow_fill_async(ctx, d_flags, 0, 4 * (size_t)n_leaves * C, s));
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
   LatArgs A = make_args(ctx);
-  if (A.grid) OW_CUDA(cudaMemsetAsync(A.grid, 0xFF, 4 * (size_t)A.gdim[0] * A.gdim[1] * A.gdim[2], s));
+  if (A.grid) OW_TRY(ow_fill_async(ctx, A.grid, 0xFF, 4 * (size_t)A.gdim[0] * A.gdim[1] * A.gdim[2], s));
   if (D == 3) ow_launch(k_lat_pos<3>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1]);
   else ow_launch(k_lat_pos<2>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1]);
   // the sweep: k_lat_faces (rows; small rows tested inline) + k_lat_mt (large rows)

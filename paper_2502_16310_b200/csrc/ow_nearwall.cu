@@ -739,7 +739,7 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   M.n_items = (unsigned long long*)((unsigned*)ph + n_leaves + (n_leaves & 1));  // after the hit words
   M.cap = cap;
   M.hit = (unsigned*)ph;
-  OW_CUDA(cudaMemsetAsync(ph, 0, 4 * (size_t)(n_leaves + (n_leaves & 1)) + 8, s));
+  OW_TRY(ow_fill_async(ctx, ph, 0, 4 * (size_t)(n_leaves + (n_leaves & 1)) + 8, s));
   if (!chunk_boxes_ready) {  // the driver reuses them while the bins and face boxes are unchanged
     const int cg = ow_blocks((n_entries + 31) / 32, 4, 16 * OW_SMS);
     if (f->dim == 3) ow_launch(k_chunk_boxes<3>, cg, 128, 0, s, d_bin_ids, n_entries, A.box, (float4*)pc);

@@ -37,7 +37,8 @@ struct StageEvents {
   bool used[OW_MAX_PASSES][5];
 };
 
-int record(StageEvents* se, int lv, int k, cudaStream_t s) {
+int record(StageEvents* se, int lv, int k, cudaStream_t s, bool skip = false) {
+  if (skip) return OW_OK;
   if (!se->ev[lv][k]) OW_CUDA(cudaEventCreate(&se->ev[lv][k]));
   OW_CUDA(cudaEventRecord(se->ev[lv][k], s));
   se->used[lv][k] = true;
@@ -201,7 +202,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
   OW_TRY(ow_slot(ctx, SLOT_DRV_STATS, 40 * (size_t)passes, s, &stats));
   // [72 * pass] ring state | [72 * passes] device block count | summary
   OW_TRY(ow_slot(ctx, SLOT_DRV_STATE, 8 * (72 * (size_t)passes + 16 + SUM_W * (size_t)passes), s, &drv));
-  OW_CUDA(cudaMemsetAsync(stats, 0, 40 * (size_t)passes, s));
+  OW_TRY(ow_fill_async(ctx, stats, 0, 40 * (size_t)passes, s));
   int64_t* d_nb = dev ? (int64_t*)drv + 72 * passes : nullptr;
   int64_t* d_sum = (int64_t*)drv + 72 * passes + 8;
   if (dev) {
@@ -210,7 +211,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
   }
   for (int level = 0; level < passes; ++level) {
     // ---- bin_setup
-    OW_TRY(record(se, level, 0, s));
+    OW_TRY(record(se, level, 0, s, ctx->no_stage_events));
     bool fresh_bins = level == 0;  // chunk boxes of the bins (marking) need a rebuild
     if (p->binned && (!have_bins || !p->reuse_bins)) {
       fresh_bins = true;
@@ -244,7 +245,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
     }
     // ---- face_detection
     if (ctx->faces_pending) OW_TRY(ow_faces_settle(ctx, nullptr, s));  // (naive strategy: no bin readback)
-    OW_TRY(record(se, level, 1, s));
+    OW_TRY(record(se, level, 1, s, ctx->no_stage_events));
     const int64_t n_host = dev ? f->capacity : f->n_blocks;  // bound on this level's leaves
     void* pl;
     OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(n_host + 1), s, &pl));
@@ -307,7 +308,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
                             p->binned ? E : 0, p->d_spec, p->reach, dst, s, dn, !fresh_bins));
     }
     // ---- propagation (binned only): 1 + floor(d / min block length)
-    OW_TRY(record(se, level, 2, s));
+    OW_TRY(record(se, level, 2, s, ctx->no_stage_events));
     if (p->binned) {
       double bl = INFINITY;
       for (int a = 0; a < f->dim; ++a) {
@@ -318,13 +319,13 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
       OW_TRY(ow_propagate_dev(ctx, f, (const int32_t*)pl, dn, n_host, rounds, s));
     }
     // ---- refinement on the device; one readback of its state per level
-    OW_TRY(record(se, level, 3, s));
+    OW_TRY(record(se, level, 3, s, ctx->no_stage_events));
     // splits that would not fit the current capacity are detected on the device
     // and finished below on the host path, which grows the forest
     // a cascade of splits descends at least one level per sweep
     const int iters = level + 2 < RS_MAX_ITERS ? level + 2 : RS_MAX_ITERS;
     OW_TRY(ow_refine_dev(ctx, f, level, iters, rs, s, d_nb));
-    OW_TRY(record(se, level, 4, s));
+    OW_TRY(record(se, level, 4, s, ctx->no_stage_events));
     if (dev) {
       out->n_passes = level + 1;
       continue;
@@ -517,6 +518,7 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
   ctx->faces_state = &fs_state;
   ctx->faces_pending = ctx->d_small + 56;
   ctx->defer_stage_times = true;  // read the stage events after the lattice work is queued
+  ctx->no_stage_events = p->no_stage_times != 0;
   int st = refine_driver(ctx, f, d_coords, n_faces, geom_key, grid, &nw, d_bin_ids, bin_ids_capacity, d_bin_counts,
                          d_bin_offsets, &out->nw, s, true);
   if (st == OW_OK && ctx->faces_pending) st = ow_faces_settle(ctx, nullptr, s);  // (no pass read it)
@@ -524,6 +526,7 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
   ctx->faces_state = nullptr;
   if (out->faces.first_nonfinite >= 0 || out->faces.first_degenerate >= 0 || out->outside_domain) {
     ctx->defer_stage_times = false;
+    ctx->no_stage_events = false;
     return OW_ERR_INVALID;  // (the message was set by ow_faces_settle)
   }
   if (st == DRV_RETRY) {  // the forest outgrew its capacity (or a deep cascade): per-level host path
@@ -533,6 +536,7 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
                        d_bin_offsets, &out->nw, s, false);
   }
   ctx->defer_stage_times = false;
+  ctx->no_stage_events = false;
   OW_TRY(st);
   int finest = 0;
   for (int l = 0; l < out->nw.n_passes; ++l)

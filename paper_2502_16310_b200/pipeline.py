@@ -75,7 +75,7 @@ class GridPlan:
     NearWallParams, lattice)."""
 
     def __init__(self, domain: Aabb, root_dims, params: NearWallParams, lattice: str | None = "D3Q19",
-                 capacity=None, max_level=DEFAULT_MAX_LEVEL, reuse_outputs=False, comm=None):
+                 capacity=None, max_level=DEFAULT_MAX_LEVEL, reuse_outputs=False, comm=None, stage_times=True):
         """``reuse_outputs=True``: every pass writes into the same device
         arrays (forest, bins, links), so a pass's results are valid until the
         next ``run`` — for loops that consume each pass before the next
@@ -86,7 +86,11 @@ class GridPlan:
         ``comm`` (a ``parallel.DeviceComm``, one rank per GPU): the pass is
         sharded — work-balanced leaf slices per marking pass and equal
         finest-leaf slices for the lattice links, exchanged over peer memory
-        inside the native call — and every rank returns the whole result."""
+        inside the native call — and every rank returns the whole result.
+
+        ``stage_times=False``: no CUDA events between the level loop's stages
+        (an event between two kernels stops their programmatic overlap);
+        ``NearWallResult.timings`` then read 0 ms.  Settable per pass."""
         self.domain = domain if isinstance(domain, Aabb) else Aabb(*domain)
         self.dim = self.domain.dim
         self.root_dims = tuple(int(v) for v in np.asarray(root_dims).reshape(-1))
@@ -113,6 +117,7 @@ class GridPlan:
         self._gp_key = None
         self.reuse = bool(reuse_outputs)
         self.comm = comm if comm is not None and comm.world > 1 else None
+        self.stage_times = bool(stage_times)
         self._forest = None
         self._setup = None  # (n_faces, _driver_setup result): the parts that depend on n_faces only
         self._gp0 = _lib.G2GParamsC()  # static fields of the call's parameter struct
@@ -254,6 +259,7 @@ class GridPlan:
                 self._dev_qp = torch.empty(nlink, dtype=torch.float32, device=self.dev)
             gp.dev_rows, gp.dev_q_packed = self._dev_rows.data_ptr(), self._dev_qp.data_ptr()
             gp.dev_row_cap, gp.dev_link_cap = nrow, nlink
+        gp.no_stage_times = 0 if self.stage_times else 1
         out = _lib.G2GResultC()
         g, bins_t = st["g"], st["bins_t"]
         v = forest.view()
