@@ -213,9 +213,10 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     params = ow.NearWallParams(d_spec=cfg["d"], n_levels=cfg["levels"], bins_per_axis=cfg["B"])
     grid = ow.BinGrid(dom, cfg["B"])
     text = cfg["kind"] == "text"
-    if text:
+    if text:  # C1: the text primitive's geometry stays resident for `value`; e2e re-parses it every step
         ig = ow.geometry.parse_text_primitives(data.decode())
         n_faces = ig.n_faces
+        geom_dev = ow.index_to_coords(ig)
     else:
         n_faces = int.from_bytes(data[80:84], "little")
         rec_host = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).pin_memory()
@@ -225,28 +226,20 @@ def gpu_arm(args, cfg, rank, world, local_rank):
 
     # N > 1: the fused pass shards on the device (parallel.DeviceComm: marks,
     # statistics, lattice flag words and q rows exchanged over peer memory by
-    # the native level loop, no host round trip per level); the 2D text
-    # configuration keeps the per-function path with torch.distributed
-    comm = shard = None
-    if world > 1 and not text:
+    # the native level loop, no host round trip per level)
+    comm = None
+    if world > 1:
         cap_blocks = 32 * cfg["root"] ** dim
         comm = parallel.DeviceComm(max(64 << 20, 4 * (4 ** dim) * cap_blocks))
-    elif world > 1:
-        shard = parallel.Shard()
     # (stage-timing events off in the timed loops: an event between two kernels
     # stops their programmatic overlap; the profiled pass below records them)
-    plan = (pipeline.GridPlan(dom, (cfg["root"],) * dim, params, cfg["lattice"], reuse_outputs=True, comm=comm,
-                              stage_times=False) if not text else None)
+    plan = pipeline.GridPlan(dom, (cfg["root"],) * dim, params, cfg["lattice"], reuse_outputs=True, comm=comm,
+                             stage_times=False)
 
     def step(records):
-        if text:  # per-function path (reference call sequence, cli.py:87-113)
-            geom = ow.index_to_coords(ig) if text else ow.geometry.stl_records_to_coords(records, n_faces)
-            forest = ow.init_root_grid(dom, (cfg["root"],) * dim, capacity=32 * cfg["root"] ** dim)
-            res = ow.refine_near_wall(forest, geom, params, shard=shard)
-            ll = ow.build_lattice_links(forest, geom, None, cfg["lattice"], shard=shard)
-            return res, forest, ll
-        # fused native pass: STL records in HBM -> grid -> lattice links (ow_geometry_to_grid)
-        gp = plan.run(records, n_faces)
+        # fused native pass: STL records (C1: the resident text-primitive
+        # geometry) -> grid -> lattice links (ow_geometry_to_grid)
+        gp = plan.run(geometry=geom_dev) if text else plan.run(records, n_faces)
         return gp.result, gp.forest, gp.links
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
@@ -319,26 +312,16 @@ def gpu_arm(args, cfg, rank, world, local_rank):
             if k >= 0:
                 ev2[k][0].record()
             if text:
-                # per-function path (text primitives): STL records
-                # in from pinned memory, every result array out through torch copies
-                rd = None
-                h2d = 0
-                if not text:
-                    rd = rec_host.to(dev, non_blocking=True)
-                    h2d = rec_host.numel()
-                res, forest, ll = step(rd)
-                outs = [forest.level_tensor, forest.coords_tensor, forest._parent_t[: forest.n_blocks],
-                        forest._first_child_t[: forest.n_blocks], forest.marks, ll.cells, ll.q]
-                d2h = 0
-                for i, o in enumerate(outs):  # pinned host result buffers, reused across steps
-                    nbytes = o.numel() * o.element_size()
-                    if i >= len(pinned) or pinned[i].numel() < nbytes:
-                        if i < len(pinned):
-                            pinned[i] = torch.empty(2 * nbytes, dtype=torch.uint8, pin_memory=True)
-                        else:
-                            pinned.append(torch.empty(2 * nbytes + 64, dtype=torch.uint8, pin_memory=True))
-                    pinned[i][:nbytes].copy_(o.contiguous().view(-1).view(torch.uint8), non_blocking=True)
-                    d2h += nbytes
+                # the text primitive parsed on the host every step (the reference's
+                # import_text_primitives + index_to_coords: the vertices and faces go
+                # host -> device), the fused pass, every result back to pinned memory
+                igk = ow.geometry.parse_text_primitives(data.decode())
+                h2d = igk.vertices.nbytes + igk.faces.nbytes
+                gp = plan.run(geometry=ow.index_to_coords(igk), host=True)
+                res, forest, ll = gp.result, gp.forest, gp.links
+                hres = gp.host
+                d2h = sum(t.numel() * t.element_size() for k2, t in hres.items() if k2 != "coords")
+                d2h += sum(t.numel() * t.element_size() for t in hres["coords"])
             torch.cuda.current_stream().synchronize()
             if k >= 0:
                 ev2[k][1].record()
@@ -358,9 +341,7 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         e2e = {"value": T_step / (ms2 / 1e3), "unit": "cell-face tests/s", "ms_per_step": ms2,
                "ms_step_median": per[len(per) // 2], "ms_step_max": per[-1],
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "result": ("forest arrays (level, coords, parent, first_child, marks) + boundary cells and q"
-                          if text else
-                          "forest arrays (level, coords, parent, first_child, marks) + boundary rows packed: cell "
+               "result": ("forest arrays (level, coords, parent, first_child, marks) + boundary rows packed: cell "
                           "ids, flag words and the q of the set bits (GridPass.host_q() expands to the dense rows)")}
         if not text:
             e2e["slow_path_steps"] = slow_path

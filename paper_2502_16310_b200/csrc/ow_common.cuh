@@ -6,6 +6,7 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <functional>
 #include <utility>
 
 #include "../../include/owb200.h"
@@ -89,6 +90,7 @@ enum ow_slot {
   SLOT_LAT_QPACK,      // q of the set flag bits, row-major (packed host output)
   SLOT_LAT_GRID,       // dense finest-level lattice -> leaf position
   SLOT_DRV_SLICE,      // native driver, multi-GPU: per-leaf work prefix + slice bounds
+  SLOT_SCAN_STATUS_G,  // look-back status words of scans inside a CUDA graph (ow_graph.cu)
   SLOT_MISC,
   SLOT_COUNT
 };
@@ -103,6 +105,7 @@ struct ow_prof {
   cudaEvent_t ev[PROF_N][PROF_MAX][2];
 };
 
+struct GraphKey;
 struct ow_ctx {
   int device;
   ow_prof* prof;
@@ -160,7 +163,39 @@ struct ow_ctx {
   const int64_t* faces_pending;
   void* faces_state;  // the fused call's (result, forest, parameters) for ow_faces_settle
   int64_t drv_spec_nl;  // leaves of the deepest level compacted by the device-resident driver (-1: none)
+  // CUDA graph of the device-resident level loop (ow_graph.cu)
+  bool capturing;                      // stream capture in progress: scratch must not grow
+  bool capture_failed;
+  int graph_site;                      // scans recorded in the current capture
+  unsigned long long* d_graph_epoch;   // device epoch base of the scans inside the graph
+  // a few graphs per context (a stream of passes may alternate plans)
+  cudaGraphExec_t loop_exec[4];
+  GraphKey* loop_key[4];               // inputs of each captured loop
+  int64_t loop_launches[4];            // kernels per replay
+  GraphKey* eager_key[4];              // inputs of recent eager passes
+  int loop_next, eager_next;           // round-robin victims
+  cudaStream_t capture_stream;         // private stream the loop is recorded on (the caller's may be the
+                                       // legacy default stream, which cannot be captured)
 };
+
+// host-side inputs of the device-resident loop (a replay is valid only when
+// they are all unchanged)
+struct GraphKey {
+  ow_forest f;
+  ow_grid g;
+  ow_nearwall_params p;
+  const void* coords;
+  int64_t n_faces;
+  const void *ids, *counts, *offsets;
+  int64_t E;
+  const void *stats, *drv;
+  void* slot_ptr[SLOT_COUNT];
+  size_t slot_bytes[SLOT_COUNT];
+};
+void make_loop_key(GraphKey* k, const ow_ctx* ctx, const ow_forest* f, const float* d_coords, int64_t n_faces,
+                   const ow_grid* grid, const ow_nearwall_params* p, const int32_t* ids, const int32_t* counts,
+                   const int32_t* offsets, int64_t E, const void* stats, const void* drv);
+int ow_loop_graph(ow_ctx* ctx, bool ok, const GraphKey* key, cudaStream_t* ps, const std::function<int()>& body);
 
 // multi-GPU exchange over peer memory (ow_comm.cu)
 struct ow_comm {

@@ -54,6 +54,13 @@ extern "C" int ow_ctx_destroy(ow_ctx* c) {
   for (int i = 0; i < SLOT_COUNT; ++i)
     if (c->slot_ptr[i]) cudaFree(c->slot_ptr[i]);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (int i = 0; i < 4; ++i) {
+    if (c->loop_exec[i]) cudaGraphExecDestroy(c->loop_exec[i]);
+    free(c->loop_key[i]);
+    free(c->eager_key[i]);
+  }
+  if (c->capture_stream) cudaStreamDestroy(c->capture_stream);
+  if (c->d_graph_epoch) cudaFree(c->d_graph_epoch);
   for (int i = 0; i < 2; ++i)
     if (c->copy_ev[i]) cudaEventDestroy(c->copy_ev[i]);
   if (c->stage_events) {
@@ -77,6 +84,11 @@ extern "C" int ow_ctx_destroy(ow_ctx* c) {
 
 int ow_slot(ow_ctx* ctx, int slot, size_t bytes, cudaStream_t s, void** out) {
   if (bytes == 0) bytes = 16;
+  if (ctx->slot_bytes[slot] < bytes && ctx->capturing) {  // (a graph must not own scratch: run eagerly)
+    ctx->capture_failed = true;
+    ow_set_error("graph capture: scratch slot %d would grow", slot);
+    return OW_ERR_INTERNAL;
+  }
   if (ctx->slot_bytes[slot] < bytes) {
     size_t want = bytes + bytes / 4 + 256;
     if (ctx->slot_ptr[slot]) OW_CUDA(cudaFreeAsync(ctx->slot_ptr[slot], s));
@@ -150,8 +162,17 @@ bool ow_pdl_enabled() {
 namespace {
 __global__ void k_fill(uint32_t* __restrict__ w, int64_t n_words, uint8_t* __restrict__ tail, int n_tail, uint32_t v) {
   ow_pdl_wait();
-  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (int64_t i = i0; i < n_words; i += (int64_t)gridDim.x * blockDim.x) w[i] = v;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  // 16-byte stores for the aligned body (w is 4-byte aligned; the head up to
+  // 16-byte alignment and the remainder word by word)
+  const int64_t head = (int64_t)(((16 - ((uintptr_t)w & 15u)) & 15u) >> 2);
+  const int64_t h = head < n_words ? head : n_words;
+  const int64_t n4 = (n_words - h) >> 2;
+  uint4* w4 = reinterpret_cast<uint4*>(w + h);
+  const uint4 v4 = make_uint4(v, v, v, v);
+  for (int64_t i = i0; i < n4; i += stride) w4[i] = v4;
+  for (int64_t i = i0; i < h; i += stride) w[i] = v;
+  for (int64_t i = h + 4 * n4 + i0; i < n_words; i += stride) w[i] = v;
   if (i0 < n_tail) tail[i0] = (uint8_t)v;
 }
 }  // namespace
@@ -165,7 +186,7 @@ int ow_fill_async(ow_ctx* ctx, void* p, int value, size_t bytes, cudaStream_t s)
   const uint32_t b = (uint32_t)(value & 0xFF);
   const int64_t n_words = (int64_t)(bytes >> 2);
   const int n_tail = (int)(bytes & 3u);
-  ow_launch(k_fill, ow_blocks(n_words > 0 ? n_words : 1, 256, 4 * OW_SMS), 256, 0, s, (uint32_t*)p, n_words,
+  ow_launch(k_fill, ow_blocks(n_words > 0 ? (n_words + 3) / 4 : 1, 256, 8 * OW_SMS), 256, 0, s, (uint32_t*)p, n_words,
             (uint8_t*)p + 4 * n_words, n_tail, b | b << 8 | b << 16 | b << 24);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();

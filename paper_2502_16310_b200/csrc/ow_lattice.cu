@@ -944,8 +944,11 @@ __global__ void k_lat_bcount(LatArgs A) {
   ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
   const int lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (r >= *A.n_cb_d) return;
+  // persistent warps over the candidate blocks (their count is on the device;
+  // a grid over every leaf launched ~7x more CTAs than there is work at C5)
+  const int64_t ncb = *A.n_cb_d;
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < ncb;
+       r += (int64_t)gridDim.x * (blockDim.x >> 5)) {
   const int64_t pos = A.cand_blocks[r];
   unsigned long long m = 0;
   int links = 0;
@@ -963,6 +966,7 @@ __global__ void k_lat_bcount(LatArgs A) {
     A.hcount[r] = links;
     A.bmask[r] = m;
     if (links) atomicAdd(A.links_d, (unsigned long long)links);
+  }
   }
 }
 
@@ -1371,8 +1375,8 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   }
   OW_TRY(ow::scan01(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s));
   OW_PROF_END(ctx, PROF_LAT_SWEEP, s);
-  if (D == 3) ow_launch(k_lat_bcount<3>, ow_blocks(nl, 8), 256, 0, s, A);
-  else ow_launch(k_lat_bcount<2>, ow_blocks(nl, 8), 256, 0, s, A);
+  if (D == 3) ow_launch(k_lat_bcount<3>, ow_blocks(nl, 8, 8 * OW_SMS), 256, 0, s, A);
+  else ow_launch(k_lat_bcount<2>, ow_blocks(nl, 8, 8 * OW_SMS), 256, 0, s, A);
   ctx->launches += 2;
   OW_CHECK_LAUNCH();
   OW_TRY(scan(ctx, BcountLoad{A.bcount, A.n_cb_d}, BoffStore{(int64_t*)A.boff, A.n_cb_d}, nl, ctx->d_small + 35, s));

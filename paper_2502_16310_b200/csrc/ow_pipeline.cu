@@ -202,42 +202,64 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
   OW_TRY(ow_slot(ctx, SLOT_DRV_STATS, 40 * (size_t)passes, s, &stats));
   // [72 * pass] ring state | [72 * passes] device block count | summary
   OW_TRY(ow_slot(ctx, SLOT_DRV_STATE, 8 * (72 * (size_t)passes + 16 + SUM_W * (size_t)passes), s, &drv));
-  OW_TRY(ow_fill_async(ctx, stats, 0, 40 * (size_t)passes, s));
+  // the bin count of fill_bins with its host checks (one readback: the entry
+  // count sizes the emission); in the device-resident loop it runs before the
+  // loop so the loop itself has no host round trip
+  auto count_bins = [&]() -> int {
+    int64_t outside = -1;
+    OW_TRY(ow_fill_bins_count(ctx, grid, d_coords, n_faces, p->spacing, d_bin_counts, &E, &outside, s));
+    if (outside >= 0) {
+      ow_set_error("face sample outside binning domain (face %lld)", (long long)outside);
+      return OW_ERR_INVALID;
+    }
+    const int64_t capacity = p->overlap_factor * n_faces;
+    if (E > capacity || E > bin_ids_capacity) {
+      int32_t* h = (int32_t*)malloc(4 * (size_t)n_bins);
+      if (!h) {
+        ow_set_error("refine_near_wall: out of host memory");
+        return OW_ERR_INTERNAL;
+      }
+      cudaError_t e = cudaMemcpyAsync(h, d_bin_counts, 4 * (size_t)n_bins, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      const int64_t acc = e == cudaSuccess ? overflow_total(h, n_bins, p->bin_fraction, capacity) : E;
+      free(h);
+      OW_CUDA(e);
+      ow_set_error("bin assignment overflow: %lld face-bin entries exceed capacity %lld (= %lld x %lld faces); "
+                   "raise overlap_factor, or raise bin_fraction to shrink the per-batch indicator",
+                   (long long)acc, (long long)capacity, (long long)p->overlap_factor, (long long)n_faces);
+      return OW_ERR_CAPACITY;
+    }
+    return OW_OK;
+  };
   int64_t* d_nb = dev ? (int64_t*)drv + 72 * passes : nullptr;
   int64_t* d_sum = (int64_t*)drv + 72 * passes + 8;
+  // device-resident loop: its only host round trips (the bin count, the
+  // face summary) happen first, so everything below runs without one and can
+  // be replayed as a CUDA graph (ow_graph.cu)
+  bool pre_counted = false;
+  if (dev && p->binned && p->reuse_bins) {
+    OW_TRY(record(se, 0, 0, s, ctx->no_stage_events));
+    OW_TRY(count_bins());
+    pre_counted = true;
+  } else if (dev && ctx->faces_pending) {
+    OW_TRY(ow_faces_settle(ctx, nullptr, s));
+  }
+  auto device_part = [&]() -> int {
+  bool bins_counted = pre_counted;
+  have_bins = false;
+  OW_TRY(ow_fill_async(ctx, stats, 0, 40 * (size_t)passes, s));
   if (dev) {
     ow_launch(k_set_i64, 1, 1, 0, s, d_nb, f->n_blocks);
     OW_LAUNCHED(ctx);
   }
   for (int level = 0; level < passes; ++level) {
     // ---- bin_setup
-    OW_TRY(record(se, level, 0, s, ctx->no_stage_events));
+    if (!(pre_counted && level == 0)) OW_TRY(record(se, level, 0, s, ctx->no_stage_events));
     bool fresh_bins = level == 0;  // chunk boxes of the bins (marking) need a rebuild
     if (p->binned && (!have_bins || !p->reuse_bins)) {
       fresh_bins = true;
-      int64_t outside = -1;
-      OW_TRY(ow_fill_bins_count(ctx, grid, d_coords, n_faces, p->spacing, d_bin_counts, &E, &outside, s));
-      if (outside >= 0) {
-        ow_set_error("face sample outside binning domain (face %lld)", (long long)outside);
-        return OW_ERR_INVALID;
-      }
-      const int64_t capacity = p->overlap_factor * n_faces;
-      if (E > capacity || E > bin_ids_capacity) {
-        int32_t* h = (int32_t*)malloc(4 * (size_t)n_bins);
-        if (!h) {
-          ow_set_error("refine_near_wall: out of host memory");
-          return OW_ERR_INTERNAL;
-        }
-        cudaError_t e = cudaMemcpyAsync(h, d_bin_counts, 4 * (size_t)n_bins, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        const int64_t acc = e == cudaSuccess ? overflow_total(h, n_bins, p->bin_fraction, capacity) : E;
-        free(h);
-        OW_CUDA(e);
-        ow_set_error("bin assignment overflow: %lld face-bin entries exceed capacity %lld (= %lld x %lld faces); "
-                     "raise overlap_factor, or raise bin_fraction to shrink the per-batch indicator",
-                     (long long)acc, (long long)capacity, (long long)p->overlap_factor, (long long)n_faces);
-        return OW_ERR_CAPACITY;
-      }
+      if (!bins_counted) OW_TRY(count_bins());
+      bins_counted = false;
       OW_TRY(ow_fill_bins_emit(ctx, grid, d_bin_ids, d_bin_counts, d_bin_offsets, s));
       have_bins = true;
       out->bin_entries = E;
@@ -361,6 +383,29 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
     OW_TRY(ow_forest_leaves_dev(ctx, f, passes, (int32_t*)pl, d_sum + SUM_W * passes, s, d_nb));
     ow_launch(k_drv_summary, 1, 32, 0, s, (const int64_t*)drv, (const unsigned long long*)stats, passes, d_sum);
     OW_LAUNCHED(ctx);
+  }
+  return OW_OK;
+  };  // device_part
+  if (dev) {
+    // replay / capture / run of the device-resident loop (graph eligible only
+    // without host-side events, profiling or a multi-GPU exchange)
+    const bool graph_ok = p->binned && p->reuse_bins && ctx->no_stage_events && !comm &&
+                          !(ctx->prof && ctx->prof->enabled);
+    GraphKey key;
+    make_loop_key(&key, ctx, f, d_coords, n_faces, grid, p, d_bin_ids, d_bin_counts, d_bin_offsets, E, stats, drv);
+    const int gs = ow_loop_graph(ctx, graph_ok, &key, &s, device_part);
+    OW_TRY(gs < 0 ? OW_OK : gs);
+    if (gs < 0) {  // replayed: the host-side bookkeeping of the loop
+      out->n_passes = passes;
+      if (p->binned) {
+        out->bin_entries = E;
+        out->bins_built = 1;
+      }
+    }
+  } else {
+    OW_TRY(device_part());
+  }
+  if (dev && passes > 0) {
     int64_t h[SUM_W * OW_MAX_PASSES + 1];
     OW_TRY(ow_readback(ctx, d_sum, SUM_W * passes + 1, h, s));
     for (int level = 0; level < passes; ++level) {

@@ -19,6 +19,7 @@ constexpr unsigned long long ST_AGG = 1ull << 62;
 constexpr unsigned long long ST_INC = 2ull << 62;
 constexpr unsigned long long ST_VAL = (1ull << 46) - 1;
 constexpr int ST_EPOCH_SHIFT = 46;
+constexpr unsigned long long GRAPH_SITES = 64;  // scans per captured pass (ow_graph.cu: epoch = base * 64 + site)
 
 __device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -91,8 +92,9 @@ __device__ __forceinline__ int64_t lookback(unsigned long long* status, int64_t 
 template <class Load, class Store>
 __global__ void __launch_bounds__(SCAN_THREADS)
 k_scan(Load load, Store store, int64_t n, int64_t n_chunks, int64_t chunk, unsigned long long* status,
-       int64_t* total_out, unsigned long long epoch) {
+       int64_t* total_out, unsigned long long epoch, const unsigned long long* d_epoch_base) {
   ow_pdl_wait();
+  if (d_epoch_base) epoch += *d_epoch_base * GRAPH_SITES;  // inside a CUDA graph (ow_graph.cu)
   constexpr int W = SCAN_THREADS / 32;
   __shared__ int64_t s_warp[W];
   const int64_t tile = blockIdx.x;  // chunk index (CTAs dispatch in index order)
@@ -161,8 +163,20 @@ k_scan(Load load, Store store, int64_t n, int64_t n_chunks, int64_t chunk, unsig
 }
 
 // status words for `tiles` tiles (+ the ticket counters) and this scan's epoch
+// (inside a graph capture: the graph's own status array and the scan's site;
+// the kernel adds the device epoch base, see ow_graph.cu)
 inline int scan_status(ow_ctx* ctx, int64_t tiles, cudaStream_t s, unsigned long long** status,
                        unsigned long long* epoch) {
+  if (ctx->capturing) {
+    if (8 * (size_t)(tiles + 1) > ctx->slot_bytes[SLOT_SCAN_STATUS_G] || ctx->graph_site + 1 >= GRAPH_SITES) {
+      ctx->capture_failed = true;
+      ow_set_error("graph capture: scan status array too small or too many scans");
+      return OW_ERR_INTERNAL;
+    }
+    *epoch = (unsigned long long)(++ctx->graph_site);
+    *status = (unsigned long long*)ctx->slot_ptr[SLOT_SCAN_STATUS_G] + 1;
+    return OW_OK;
+  }
   void* old = ctx->slot_ptr[SLOT_SCAN_STATUS];
   const size_t old_bytes = ctx->slot_bytes[SLOT_SCAN_STATUS];
   void* p;
@@ -192,7 +206,8 @@ int scan(ow_ctx* ctx, Load load, Store store, int64_t n, int64_t* d_total, cudaS
   unsigned long long* status;
   unsigned long long epoch;
   OW_TRY(scan_status(ctx, n_chunks, s, &status, &epoch));
-  ow_launch(k_scan<Load, Store>, (unsigned)n_chunks, SCAN_THREADS, 0, s, load, store, n, n_chunks, chunk, status, d_total, epoch);
+  ow_launch(k_scan<Load, Store>, (unsigned)n_chunks, SCAN_THREADS, 0, s, load, store, n, n_chunks, chunk, status, d_total,
+            epoch, (const unsigned long long*)(ctx->capturing ? ctx->d_graph_epoch : nullptr));
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;
@@ -208,8 +223,9 @@ constexpr int C01_TILE = SCAN_THREADS * C01_ITEMS;
 template <class Load, class Store>
 __global__ void __launch_bounds__(SCAN_THREADS, 6)
 k_scan01(Load load, Store store, int64_t n, const int64_t* d_n, unsigned long long* status, int64_t* total_out,
-         unsigned long long epoch) {
+         unsigned long long epoch, const unsigned long long* d_epoch_base) {
   ow_pdl_wait();
+  if (d_epoch_base) epoch += *d_epoch_base * GRAPH_SITES;  // inside a CUDA graph (ow_graph.cu)
   constexpr int W = SCAN_THREADS / 32;
   static_assert(C01_ITEMS * W == 128, "warp 0 holds 4 counts per lane");
   __shared__ int s_cnt[C01_ITEMS * W];  // per (item k, warp) in element order -> exclusive ranks
@@ -279,7 +295,8 @@ int scan01(ow_ctx* ctx, Load load, Store store, int64_t n, int64_t* d_total, cud
   unsigned long long* status;
   unsigned long long epoch;
   OW_TRY(scan_status(ctx, tiles, s, &status, &epoch));
-  ow_launch(k_scan01<Load, Store>, (unsigned)tiles, SCAN_THREADS, 0, s, load, store, n, d_n, status, d_total, epoch);
+  ow_launch(k_scan01<Load, Store>, (unsigned)tiles, SCAN_THREADS, 0, s, load, store, n, d_n, status, d_total, epoch,
+            (const unsigned long long*)(ctx->capturing ? ctx->d_graph_epoch : nullptr));
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;

@@ -698,6 +698,44 @@ def _check_host(h, ref, j):
         assert torch.equal(a, b), (j, "coords")
 
 
+def test_grid_plan_graph_replay(ow):
+    """stage_times=False: the device-resident level loop is captured as a CUDA
+    graph on the second pass with unchanged inputs and replayed afterwards
+    (ow_graph.cu; scans take their look-back epochs from the device).  Every
+    pass — eager, capture, replays, a geometry change (eager again, then a new
+    capture) — equals a fresh plan's pass, and the launch accounting counts
+    the replayed kernels."""
+    import torch
+
+    from paper_2502_16310_b200 import _lib, pipeline, shapes
+
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.06, n_levels=4, bins_per_axis=8)
+    plan = pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19", reuse_outputs=True, stage_times=False)
+    seq = [(3, 0.3)] * 5 + [(3, 0.25)] * 4 + [(3, 0.3)] * 2
+    cache = {}
+    for k, (sub, r) in enumerate(seq):
+        data = shapes.binary_stl_bytes(shapes.icosphere_triangles(sub, radius=r))
+        n = int.from_bytes(data[80:84], "little")
+        rec = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda()
+        if (sub, r) not in cache:
+            ref = pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19").run(rec, n)
+            cache[(sub, r)] = (ref.forest._coords.copy(), ref.forest._first_child.copy(),
+                               ref.forest.marks.cpu().numpy(), ref.result.marked_detected, ref.result.cell_face_tests,
+                               [t.clone() for t in (ref.links.flags, ref.links.cells, ref.links.q)])
+        l0 = _lib.launches()
+        gp = plan.run(rec, n)
+        torch.cuda.synchronize()
+        co, fc, mk, md, t, lk = cache[(sub, r)]
+        np.testing.assert_array_equal(gp.forest._coords, co, err_msg=f"pass {k}")
+        np.testing.assert_array_equal(gp.forest._first_child, fc, err_msg=f"pass {k}")
+        np.testing.assert_array_equal(gp.forest.marks.cpu().numpy(), mk, err_msg=f"pass {k}")
+        assert gp.result.marked_detected == md and gp.result.cell_face_tests == t, k
+        for a, b in zip((gp.links.flags, gp.links.cells, gp.links.q), lk):
+            assert torch.equal(a, b), k
+        assert _lib.launches() - l0 > 40, k  # replays count their kernels
+
+
 def test_two_host_threads_concurrently(ow):
     """The entry points are safe to call from several host threads at once
     (SPEC.md:133, 218): each thread gets its own context, so two threads
