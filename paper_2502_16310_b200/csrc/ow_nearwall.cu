@@ -373,8 +373,8 @@ __device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M
                                            int lane, int wid);
 
 // persistent over the level's leaves (the count may live on the device)
-template <int D, bool BINNED>
-__global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_blocks(MarkArgs A, MarkItems M) {
+template <int D, bool BINNED, int MINB = 6>
+__global__ void __launch_bounds__(MARK_THREADS, MINB) k_mark_blocks(MarkArgs A, MarkItems M) {
   ow_pdl_wait();
   __shared__ MarkSmem<D> S;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -686,6 +686,16 @@ __global__ void k_near_pairs(int dim, const float* __restrict__ pts, const float
 // Launch one marking pass; statistics accumulate into d_out[0..2] (marked,
 // tests, evaluated) on the device (no host round trip: the native driver reads
 // them once at the end).
+// (OW_MARK_MINB: resident CTAs per SM the 3D binned block pass is compiled
+// for — 6: 80 registers (measured best of 4..8 at C2 / C4 / C5; 4 and 5 remove the
+// spills but lose occupancy)
+static int mark_minb() {
+  static const int v = [] {
+    const char* e = getenv("OW_MARK_MINB");
+    return e ? atoi(e) : 6;
+  }();
+  return v;
+}
 int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves, const float* d_coords,
                    int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int32_t* d_bin_ids,
                    const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,
@@ -752,7 +762,9 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   const int gi = 8 * OW_SMS;
   if (f->dim == 3) {
     if (binned) {
-      ow_launch(k_mark_blocks<3, true>, grd, MARK_THREADS, 0, s, A, M);
+      if (mark_minb() == 8) ow_launch(k_mark_blocks<3, true, 8>, grd, MARK_THREADS, 0, s, A, M);
+      else if (mark_minb() == 7) ow_launch(k_mark_blocks<3, true, 7>, grd, MARK_THREADS, 0, s, A, M);
+      else ow_launch(k_mark_blocks<3, true>, grd, MARK_THREADS, 0, s, A, M);
       ow_launch(k_mark_items<3, true>, gi, MARK_THREADS, 0, s, A, M);
     } else {
       ow_launch(k_mark_blocks<3, false>, grd, MARK_THREADS, 0, s, A, M);
