@@ -151,6 +151,8 @@ int ow_loop_graph(ow_ctx* ctx, bool ok, const GraphKey* key, cudaStream_t* ps, c
     ctx->launches = launches0;
     return body();
   }
+  cudaGraphUpload(exec, s);  // (device-side resources staged once: lower launch latency)
+  cudaGetLastError();
   ctx->loop_exec[v] = exec;
   *ctx->loop_key[v] = *key;
   ctx->loop_launches[v] = ctx->launches - launches0;
