@@ -83,8 +83,10 @@ class IndexedGeometry:
         _require(bool(np.isfinite(v).all()), "geometry has non-finite vertex coordinates")
         if f.size:
             _require(0 <= int(f.min()) and int(f.max()) < len(v), "face index out of range")
-            srt = np.sort(f, axis=1)
-            _require(not bool((srt[:, 1:] == srt[:, :-1]).any()), "face has repeated vertex indices")
+            rep = f[:, 0] == f[:, 1]
+            if self.dim == 3:
+                rep |= (f[:, 0] == f[:, 2]) | (f[:, 1] == f[:, 2])
+            _require(not bool(rep.any()), "face has repeated vertex indices")
         self.vertices, self.faces = v, f
 
     @property
@@ -214,6 +216,8 @@ def append_geometry(parts):
     dims = {p.dim for p in parts}
     if len(dims) != 1:
         raise InvalidParameterError("cannot append geometries of mixed dimension")
+    if len(parts) == 1:
+        return parts[0]
     shift = np.cumsum([0] + [len(p.vertices) for p in parts[:-1]])
     return IndexedGeometry(parts[0].dim, np.concatenate([p.vertices for p in parts]),
                            np.concatenate([p.faces + k for p, k in zip(parts, shift)]))
