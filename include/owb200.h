@@ -301,6 +301,9 @@ typedef struct {
   int32_t reran;            /* 1: the device-resident level loop outgrew the forest capacity
                                and the pass reran with a host round trip per level */
   int64_t n_links;          /* boundary links = set flag bits = packed-q length */
+  int32_t device_sized;     /* 1: one device-sized pass (a single readback at its end); 2: a
+                               device-sized attempt fell back to the synchronous pass; 0: synchronous */
+  int32_t reserved;
 } ow_g2g_result;
 /* Binary STL records (or, with d_records NULL, coords already in d_coords) ->
  * validated SoA geometry -> root grid in `f` (capacity preallocated, grown
@@ -311,6 +314,13 @@ int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, 
                         ow_forest* f, const ow_grid* grid, const ow_g2g_params* params, int32_t* d_bin_ids,
                         int64_t bin_ids_capacity, int32_t* d_bin_counts, int32_t* d_bin_offsets,
                         ow_g2g_result* out, void* stream);
+
+/* Device-sized fused passes (on by default once a pass has sized the caller's
+ * output buffers): enable = 0 keeps ow_geometry_to_grid on the synchronous
+ * path (a host round trip per size it needs).  Stats: [0] device-sized passes,
+ * [1] device-sized attempts that fell back to the synchronous path. */
+int ow_set_device_pass(ow_ctx* ctx, int32_t enable);
+int ow_device_pass_stats(ow_ctx* ctx, int64_t* out2);
 
 /* Cell-face links (build_cell_face_links, nearwall.py:522-594), two phases.
  * Count: per leaf cell the faces of its bin within d_link.  On overflow of

@@ -159,6 +159,8 @@ class G2GResultC(C.Structure):  # ow_g2g_result
         ("host_copied", C.c_int32),
         ("reran", C.c_int32),
         ("n_links", C.c_int64),
+        ("device_sized", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -204,6 +206,8 @@ _SIGS = {
     "ow_lattice_links_n_links": [P, PI64],
     "ow_lattice_stats": [P, PI64, P],
     "ow_lattice_tune": [P, C.c_int32, C.c_int32],
+    "ow_set_device_pass": [P, C.c_int32],
+    "ow_device_pass_stats": [P, PI64],
     "ow_near_pairs": [P, I32, P, P, P, I64, P, P],
     "ow_export_vtk": [P, C.POINTER(ForestView), C.c_char_p, C.c_char_p, P],
     "ow_referee_pairs": [P, I32, P, P, P, I64, P, P, P],
@@ -305,6 +309,20 @@ def lattice_stats():
     out = (C.c_int64 * 3)()
     call("ow_lattice_stats", ctx(), out, stream())
     return tuple(int(x) for x in out)
+
+
+def set_device_pass(enable=True):
+    """Device-sized fused passes on this thread's context (default on):
+    ``False`` keeps ``GridPlan.run`` on the synchronous path."""
+    call("ow_set_device_pass", ctx(), int(bool(enable)))
+
+
+def device_pass_stats():
+    """(device-sized passes, device-sized attempts that fell back) of this
+    thread's context."""
+    out = (C.c_int64 * 2)()
+    call("ow_device_pass_stats", ctx(), out)
+    return int(out[0]), int(out[1])
 
 
 def profile(enable=True):

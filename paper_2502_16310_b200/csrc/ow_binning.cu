@@ -358,7 +358,7 @@ struct SlowVolLoad {
 
 template <int D>
 __global__ void k_emit_fast(GridC g, const float* __restrict__ c, int64_t n, const unsigned long long* masks,
-                            const int32_t* foff, uint32_t* keys, int32_t* vals) {
+                            const int32_t* foff, uint32_t* keys, int32_t* vals, int64_t cap) {
   ow_pdl_wait();
   int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= n) return;
@@ -368,6 +368,9 @@ __global__ void k_emit_fast(GridC g, const float* __restrict__ c, int64_t n, con
   load_face<D>(c, n, f, v);
   Range r = face_range<D>(g, v, 1);
   int64_t pos = foff[f];
+  // cap: the pair buffers' length (device-sized pass: the entry count is only
+  // checked on the host after the pass; entries past the buffers are dropped)
+  if (pos + __popcll(m) > cap) return;
   while (m) {
     int loc = __ffsll(m) - 1;
     m &= m - 1;
@@ -510,7 +513,7 @@ int fill_emit(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, int32_t* i
   else pv0 = ids;
   const int32_t* foff = (const int32_t*)ctx->slot_ptr[SLOT_BIN_FOFF];
   ow_launch(k_emit_fast<D>, ow_blocks(n, 256), 256, 0, s, g, c, n, (const unsigned long long*)ctx->slot_ptr[SLOT_BIN_MASK],
-                                                  foff, (uint32_t*)pk0, (int32_t*)pv0);
+                                                  foff, (uint32_t*)pk0, (int32_t*)pv0, E);
   OW_LAUNCHED(ctx);
   if (ctx->bins_slow > 0) {
     ow_launch(k_emit_slow<D>, (unsigned)ctx->bins_slow, 32, 0, s, 
@@ -527,7 +530,79 @@ int fill_emit(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, int32_t* i
   return OW_OK;
 }
 
+// Device-sized fill_bins (fused pass, ow_pipeline.cu): count, face offsets,
+// emission and the stable sort with the entry count left on the device
+// (small[5]); e_cap bounds the pair buffers and sizes the sort's grid.  The
+// host checks small[0] (slow faces: this path does not bin them), small[1]
+// (a sample outside the domain), small[2] and small[5] <= e_cap after the
+// pass and re-runs it on the synchronous path when one fails.
+template <int D>
+int fill_dev(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, int32_t* counts, int32_t* ids,
+             int32_t* offsets, int64_t n_bins, int64_t e_cap, cudaStream_t s) {
+  void *pm, *pnb, *pfo, *psl, *pmid;
+  OW_TRY(ow_slot(ctx, SLOT_BIN_MASK, 8 * (size_t)n, s, &pm));
+  OW_TRY(ow_slot(ctx, SLOT_BIN_NB, 4 * (size_t)n, s, &pnb));
+  OW_TRY(ow_slot(ctx, SLOT_BIN_FOFF, 4 * (size_t)n, s, &pfo));
+  OW_TRY(ow_slot(ctx, SLOT_BIN_SLOW, 4 * (size_t)n, s, &psl));
+  OW_TRY(ow_slot(ctx, SLOT_BIN_MID, 4 * (size_t)n, s, &pmid));
+  int64_t* small = ctx->d_small;
+  OW_TRY(ow_fill_async(ctx, counts, 0, 4 * (size_t)n_bins, s));
+  ow_launch(k_small_init, 1, 32, 0, s, small);
+  ow_launch(k_count_fast<D>, ow_blocks(n, 256), 256, 0, s, g, c, n, (unsigned long long*)pm, (int32_t*)pnb, counts,
+            (int32_t*)pmid, small);
+  ow_launch(k_count_walk<D>, ow_blocks(n, 256, 8 * OW_SMS), 256, 0, s, g, c, n, h, (const int32_t*)pmid,
+            (unsigned long long*)pm, (int32_t*)pnb, counts, (int32_t*)psl, small);
+  ctx->launches += 3;
+  OW_CHECK_LAUNCH();
+  OW_TRY(scan(ctx, ow::LoadArr<int32_t>{(const int32_t*)pnb}, ow::StoreExcl<int32_t>{(int32_t*)pfo}, n, small + 5, s));
+  void *pk0, *pv0, *pk1, *pv1;
+  OW_TRY(ow_slot(ctx, SLOT_PAIR_KEY0, 4 * (size_t)e_cap, s, &pk0));
+  OW_TRY(ow_slot(ctx, SLOT_PAIR_VAL0, 4 * (size_t)e_cap, s, &pv0));
+  OW_TRY(ow_slot(ctx, SLOT_PAIR_KEY1, 4 * (size_t)e_cap, s, &pk1));
+  OW_TRY(ow_slot(ctx, SLOT_PAIR_VAL1, 4 * (size_t)e_cap, s, &pv1));
+  int bits = 0;
+  while ((int64_t(1) << bits) < n_bins) ++bits;
+  const int passes = bits <= 0 ? 0 : ow::radix_passes(bits);
+  if (passes & 1) pv1 = ids;
+  else pv0 = ids;
+  ow_launch(k_emit_fast<D>, ow_blocks(n, 256), 256, 0, s, g, c, n, (const unsigned long long*)pm,
+            (const int32_t*)pfo, (uint32_t*)pk0, (int32_t*)pv0, e_cap);
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  uint32_t* rk;
+  int32_t* rv;
+  OW_TRY(ow::radix_sort_pairs(ctx, (uint32_t*)pk0, (int32_t*)pv0, (uint32_t*)pk1, (int32_t*)pv1, e_cap, bits, &rk,
+                              &rv, s, small + 5));
+  if (rv != ids) {
+    ow_set_error("fill_bins: sort ended outside the id buffer (internal)");
+    return OW_ERR_INTERNAL;
+  }
+  OW_TRY(scan(ctx, ow::LoadArr<int32_t>{counts}, ow::StoreExcl<int32_t>{offsets}, n_bins, nullptr, s));
+  ctx->bins_faces = n;
+  ctx->bins_entries = -1;  // (on the device)
+  ctx->bins_slow = 0;
+  ctx->bins_dim = D;
+  ctx->bins_B = g.B;
+  ctx->bins_h = h;
+  ctx->bins_coords = c;
+  return OW_OK;
+}
+
 }  // namespace
+
+int ow_fill_bins_dev(ow_ctx* ctx, const ow_grid* grid, const float* d_coords, int64_t n_faces, float spacing,
+                     int32_t* d_counts, int32_t* d_ids, int32_t* d_offsets, int64_t e_cap, cudaStream_t s) {
+  GridC g = make_gridc(grid);
+  int64_t n_bins = 1;
+  for (int a = 0; a < grid->dim; ++a) n_bins *= grid->bins_per_axis;
+  OW_PROF_BEGIN(ctx, PROF_BINS, s);
+  const int st = grid->dim == 2 ? fill_dev<2>(ctx, g, d_coords, n_faces, spacing, d_counts, d_ids, d_offsets, n_bins,
+                                              e_cap, s)
+                                : fill_dev<3>(ctx, g, d_coords, n_faces, spacing, d_counts, d_ids, d_offsets, n_bins,
+                                              e_cap, s);
+  OW_PROF_END(ctx, PROF_BINS, s);
+  return st;
+}
 
 extern "C" int ow_fill_bins_count(ow_ctx* ctx, const ow_grid* grid, const float* d_coords, int64_t n_faces,
                                   float spacing, int32_t* d_counts, int64_t* out_entries, int64_t* out_outside,

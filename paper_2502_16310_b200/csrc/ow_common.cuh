@@ -112,6 +112,7 @@ struct ow_ctx {
   void* slot_ptr[SLOT_COUNT];
   size_t slot_bytes[SLOT_COUNT];
   int64_t* h_pinned;  // OW_PINNED_WORDS int64 of pinned host memory for readbacks
+  int64_t* h_pinned_dev;  // the same memory mapped into the device (lazily resolved)
   int64_t* d_small;   // 64 int64 of device scalars (counters, flags)
   int64_t launches;
   int64_t scan_epoch;  // epoch of the last scan (status words are epoch-tagged)
@@ -176,6 +177,14 @@ struct ow_ctx {
   int loop_next, eager_next;           // round-robin victims
   cudaStream_t capture_stream;         // private stream the loop is recorded on (the caller's may be the
                                        // legacy default stream, which cannot be captured)
+  // device-sized fused pass (ow_pipeline.cu: g2g_device): capacities learnt
+  // from earlier passes, one readback per pass
+  bool dev_pass;                       // refine_driver runs inside a device-sized pass
+  int dev_disabled;                    // ow_set_device_pass(ctx, 0): always the synchronous path
+  int64_t dev_e_cap;                   // bin entries (0: no estimate yet)
+  int64_t dev_ncb;                     // candidate blocks of the last pass (emit grid)
+  float dev_mean_extent;               // face summary of the last pass (face-pass shape)
+  int64_t dev_passes, dev_fallbacks;   // statistics
 };
 
 // host-side inputs of the device-resident loop (a replay is valid only when
@@ -189,6 +198,7 @@ struct GraphKey {
   const void *ids, *counts, *offsets;
   int64_t E;
   const void *stats, *drv;
+  int dev;  // captured inside a device-sized pass (bins counted on the device)
   void* slot_ptr[SLOT_COUNT];
   size_t slot_bytes[SLOT_COUNT];
 };
@@ -225,7 +235,18 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
                    const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,
                    double reach, unsigned long long* d_out, cudaStream_t s,
                    const int64_t* d_n_leaves = nullptr, bool chunk_boxes_ready = false,
-                   const int64_t* d_slice = nullptr);
+                   const int64_t* d_slice = nullptr, const int64_t* d_bin_entries = nullptr);
+
+// device-sized lattice stage of the fused pass (ow_lattice.cu)
+int ow_lattice_dev_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_leaves, const int64_t* d_nl,
+                         int64_t nl_cap, const float* d_coords, int64_t n_faces, const int8_t* h_dirs, int32_t n_dirs,
+                         uint32_t* d_flags, cudaStream_t s);
+int ow_lattice_dev_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, int64_t row_cap, uint32_t* d_rows,
+                        float* d_q_packed, int64_t link_cap, int64_t ncb_grid, cudaStream_t s);
+
+// fill_bins with the entry count left on the device (ow_binning.cu: fill_dev)
+int ow_fill_bins_dev(ow_ctx* ctx, const ow_grid* grid, const float* d_coords, int64_t n_faces, float spacing,
+                     int32_t* d_counts, int32_t* d_ids, int32_t* d_offsets, int64_t e_cap, cudaStream_t s);
 
 int ow_stage_times(ow_ctx* ctx, ow_nearwall_result* out);
 

@@ -54,6 +54,7 @@ void make_loop_key(GraphKey* k, const ow_ctx* ctx, const ow_forest* f, const flo
   k->E = E;
   k->stats = stats;
   k->drv = drv;
+  k->dev = ctx->dev_pass ? 1 : 0;
   for (int i = 0; i < SLOT_COUNT; ++i) {
     if (i == SLOT_SCAN_STATUS_G) continue;  // (allocated by the capture itself)
     k->slot_ptr[i] = ctx->slot_ptr[i];

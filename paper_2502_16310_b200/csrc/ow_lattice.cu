@@ -101,12 +101,23 @@ struct LatArgs {
   const int64_t* boff;      // [n_cb]
   int64_t* cells_out;
   float* q_out;
+  // device-sized pass (ow_lattice_dev_*): the candidate-block count is only on
+  // the device, so the emit kernels stride over it and every output write is
+  // bounded by the caller's buffers (rows: cells / q / packed rows; links:
+  // packed q); a pass that would overflow one is re-run by the host
+  int64_t out_row_cap, out_link_cap;
 };
 
 template <int D>
 __global__ void k_lat_pos(ForestC F, int level, const int32_t* __restrict__ leaves, int64_t n, int32_t* pos_of,
-                          uint8_t* has_pair, float* cen, int32_t* grid, int g0, int g1) {
+                          uint8_t* has_pair, float* cen, int32_t* grid, int g0, int g1, const int64_t* d_n,
+                          uint4* zero_flags) {
   ow_pdl_wait();
+  if (d_n && *d_n < n) n = *d_n;  // device-sized pass: the leaf count lives on the device
+  if (zero_flags)  // ... and the flag words of those leaves are cleared here (no separate fill)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * (D == 3 ? 16 : 4);
+         i += (int64_t)gridDim.x * blockDim.x)
+      zero_flags[i] = make_uint4(0u, 0u, 0u, 0u);
   double q[3];
 #pragma unroll
   for (int a = 0; a < D; ++a) q[a] = block_len(F, a, level);
@@ -979,11 +990,14 @@ __global__ void k_lat_emit(LatArgs A) {
   ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
   __shared__ unsigned s_fl[C];
-  const int64_t r = blockIdx.x;
+  const int64_t ncb = *A.n_cb_d;
+  for (int64_t r = blockIdx.x; r < ncb; r += gridDim.x) {
   const unsigned long long m = A.bmask[r];
   const int c = threadIdx.x;
   const int64_t pos = A.cand_blocks[r];
   const int64_t row0 = A.boff[r];
+  const int nrow = __popcll(m), nq = A.nq;
+  if (row0 + nrow > A.out_row_cap) continue;  // (uniform per CTA; the host re-runs with room)
   if ((m >> c) & 1ull) {
     const int k = __popcll(m & ((1ull << c) - 1ull));
     s_fl[k] = A.flags[pos * C + c];
@@ -991,11 +1005,12 @@ __global__ void k_lat_emit(LatArgs A) {
     if (A.rows_out) A.rows_out[row0 + k] = make_uint2((unsigned)(pos * C + c), s_fl[k]);
   }
   __syncthreads();
-  const int nrow = __popcll(m), nq = A.nq;
   float* q = A.q_out + row0 * nq;
   for (int i = c; i < nrow * nq; i += C) {
     const int k = i / nq, d = i - k * nq;
     q[i] = ((s_fl[k] >> d) & 1u) ? __uint_as_float(0x7f7f7f7fu) : -1.0f;
+  }
+  __syncthreads();  // s_fl is rewritten by the next block
   }
 }
 
@@ -1020,7 +1035,7 @@ __global__ void k_lat_hits(LatArgs A) {
       const int c = (int)(h.x % C);
       const int r = A.cand_rank[pos];
       const int64_t row = A.boff[r] + __popcll(A.bmask[r] & ((1ull << c) - 1ull));
-      atomicMin(reinterpret_cast<unsigned*>(A.q_out) + row * A.nq + A.hit_dir[i], h.y);
+      if (row < A.out_row_cap) atomicMin(reinterpret_cast<unsigned*>(A.q_out) + row * A.nq + A.hit_dir[i], h.y);
     }
   }
   // hits of the rows swept inline (<= capacity here): HU independent chains
@@ -1044,7 +1059,7 @@ __global__ void k_lat_hits(LatArgs A) {
       if (i0 + k * stride >= ni) continue;
       const int c = (int)(h[k].x % C);
       const int64_t row = A.boff[r[k]] + __popcll(A.bmask[r[k]] & ((1ull << c) - 1ull));
-      atomicMin(reinterpret_cast<unsigned*>(A.q_out) + row * A.nq + dir[k], h[k].y);
+      if (row < A.out_row_cap) atomicMin(reinterpret_cast<unsigned*>(A.q_out) + row * A.nq + dir[k], h[k].y);
     }
   }
 }
@@ -1058,9 +1073,11 @@ __global__ void k_lat_pack(LatArgs A) {
   ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
   __shared__ int s_n[2];
-  const int64_t r = blockIdx.x;
+  const int64_t ncb = *A.n_cb_d;
+  for (int64_t r = blockIdx.x; r < ncb; r += gridDim.x) {
   const unsigned long long m = A.bmask[r];
   const int c = threadIdx.x, lane = c & 31, w = c >> 5;
+  if (A.boff[r] + __popcll(m) > A.out_row_cap || A.hoff[r] + A.hcount[r] > A.out_link_cap) continue;  // (uniform)
   const int k = __popcll(m & ((1ull << c) - 1ull));  // row of cell c within the block
   const int64_t row = A.boff[r] + k;
   const unsigned fl = ((m >> c) & 1ull) ? A.rows_out[row].y : 0u;
@@ -1079,6 +1096,8 @@ __global__ void k_lat_pack(LatArgs A) {
   int64_t o = A.hoff[r] + incl - __popc(fl);
   const float* q = A.q_out + row * A.nq;
   for (unsigned b = fl; b; b &= b - 1u) A.qp_out[o++] = q[__ffs(b) - 1];
+  if (C > 32) __syncthreads();  // s_n is rewritten by the next block
+  }
 }
 
 // Faces per warp of k_lat_faces: 16 lane pairs when faces are far smaller than
@@ -1234,6 +1253,7 @@ LatArgs make_args(ow_ctx* ctx) {
   A.hoff = (int64_t*)ctx->slot_ptr[SLOT_LAT_HOFFS];
   A.links_d = (unsigned long long*)(ctx->d_small + 51);
   A.face_next = (unsigned long long*)(ctx->d_small + 52);
+  A.out_row_cap = A.out_link_cap = INT64_MAX;
   return A;
 }
 
@@ -1247,13 +1267,18 @@ extern "C" int ow_lattice_links_count(ow_ctx* ctx, const ow_forest* f, int32_t l
                                       grid, h_dirs, n_dirs, d_flags, out_boundary, stream);
 }
 
-extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_leaves,
-                                            int64_t n_leaves, int64_t pos_lo, int64_t pos_hi, const float* d_coords,
-                                            int64_t n_faces, int64_t geom_key, const ow_grid* grid,
-                                            const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags,
-                                            int64_t* out_boundary, void* stream) {
+namespace {
+// d_nl (device-sized pass, ow_lattice_dev_count): the leaf count is read on the
+// device, n_leaves only bounds it (buffers and grids); the flag words are
+// cleared by k_lat_pos and nothing is read back (the caller reads the counts
+// after the pass and re-runs it on this synchronous path when a capacity was
+// short)
+int lat_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_leaves, int64_t n_leaves,
+              int64_t pos_lo, int64_t pos_hi, const float* d_coords, int64_t n_faces, int64_t geom_key,
+              const ow_grid* grid, const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags, int64_t* out_boundary,
+              cudaStream_t stream, const int64_t* d_nl) {
   (void)geom_key;
-  if (pos_lo < 0 || pos_hi > n_leaves || pos_lo > pos_hi) {
+  if (pos_lo < 0 || (pos_hi > n_leaves && !d_nl) || pos_lo > pos_hi) {
     ow_set_error("lattice: leaf range [%lld, %lld) outside [0, %lld)", (long long)pos_lo, (long long)pos_hi,
                  (long long)n_leaves);
     return OW_ERR_INVALID;
@@ -1302,7 +1327,7 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   const int64_t rcap = ctx->lat_row_cap, ucap = ctx->lat_unit_cap, icap = ctx->lat_ihit_cap;
   void* p;
   const int64_t nl = n_leaves;
-  OW_TRY(ow_slot(ctx, SLOT_LAT_POS, 4 * (size_t)f->n_blocks, s, &p));
+  OW_TRY(ow_slot(ctx, SLOT_LAT_POS, 4 * (size_t)(d_nl ? f->capacity : f->n_blocks), s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_HAS, (size_t)nl, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_CEN, 16 * (size_t)D * nl, s, &p));
   OW_TRY(ow_slot(ctx, SLOT_LAT_RANK, 4 * (size_t)nl, s, &p));
@@ -1328,12 +1353,13 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
     if (ctx->lat_grid_on) OW_TRY(ow_slot(ctx, SLOT_LAT_GRID, 4 * (size_t)cells, s, &p));
   }
   OW_TRY(ow_fill_async(ctx, ctx->d_small + 48, 0, 5 * 8, s));
-  OW_TRY(ow_fill_async(ctx, d_flags, 0, 4 * (size_t)n_leaves * C, s));
+  if (!d_nl) OW_TRY(ow_fill_async(ctx, d_flags, 0, 4 * (size_t)n_leaves * C, s));
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
   LatArgs A = make_args(ctx);
   if (A.grid) OW_TRY(ow_fill_async(ctx, A.grid, 0xFF, 4 * (size_t)A.gdim[0] * A.gdim[1] * A.gdim[2], s));
-  if (D == 3) ow_launch(k_lat_pos<3>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1]);
-  else ow_launch(k_lat_pos<2>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1]);
+  uint4* zf = d_nl ? reinterpret_cast<uint4*>(d_flags) : nullptr;
+  if (D == 3) ow_launch(k_lat_pos<3>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1], d_nl, zf);
+  else ow_launch(k_lat_pos<2>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1], d_nl, zf);
   // the sweep: k_lat_faces (rows; small rows tested inline) + k_lat_mt (large rows)
   OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
   const int fpw = faces_per_warp(ctx, D, n_faces, nl);
@@ -1355,7 +1381,7 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   } else {
     ctx->launches -= 1;
   }
-  if (ctx->lat_comm && ctx->lat_comm->world > 1) {
+  if (!d_nl && ctx->lat_comm && ctx->lat_comm->world > 1) {
     // multi-GPU: every rank swept the faces against its own leaf slice; the
     // flag words of the slices are all-gathered over peer memory.  A rank
     // whose own sweep outgrew its row / hit buffers re-runs it first (a local
@@ -1371,15 +1397,15 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
         ow_set_error("lattice: %lld link-face tests exceed one pass (2^31)", (long long)u0);
         return OW_ERR_CAPACITY;
       }
-      return ow_lattice_links_count_range(ctx, f, level, d_leaves, n_leaves, pos_lo, pos_hi, d_coords, n_faces,
-                                          geom_key, grid, h_dirs, n_dirs, d_flags, out_boundary, stream);
+      return lat_count(ctx, f, level, d_leaves, n_leaves, pos_lo, pos_hi, d_coords, n_faces, geom_key, grid, h_dirs,
+                       n_dirs, d_flags, out_boundary, stream, nullptr);
     }
     OW_TRY(ow_comm_allgather_words(ctx, ctx->lat_comm, d_flags, nullptr, pos_lo * C, pos_hi * C, nullptr, nl * C, s));
     if (D == 3) ow_launch(k_has_from_flags<3>, ow_blocks(nl, 8, 8 * OW_SMS), 256, 0, s, (const uint32_t*)d_flags, nl, A.has_pair);
     else ow_launch(k_has_from_flags<2>, ow_blocks(nl, 8, 8 * OW_SMS), 256, 0, s, (const uint32_t*)d_flags, nl, A.has_pair);
     OW_LAUNCHED(ctx);
   }
-  OW_TRY(ow::scan01(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s));
+  OW_TRY(ow::scan01(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s, d_nl));
   OW_PROF_END(ctx, PROF_LAT_SWEEP, s);
   if (D == 3) ow_launch(k_lat_bcount<3>, ow_blocks(nl, 8, 8 * OW_SMS), 256, 0, s, A);
   else ow_launch(k_lat_bcount<2>, ow_blocks(nl, 8, 8 * OW_SMS), 256, 0, s, A);
@@ -1387,6 +1413,7 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   OW_CHECK_LAUNCH();
   OW_TRY(scan(ctx, BcountLoad{A.bcount, A.n_cb_d}, BoffStore{(int64_t*)A.boff, A.n_cb_d}, nl, ctx->d_small + 35, s));
   OW_PROF_END(ctx, PROF_LATTICE, s);
+  if (d_nl) return OW_OK;  // (counts checked by the caller after the pass)
   // single readback: candidate blocks, (scan scratch), boundary cells, rows, units, links
   int64_t h[19];
   OW_TRY(ow_readback(ctx, ctx->d_small + 33, 19, h, s));
@@ -1405,8 +1432,8 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
       ow_set_error("lattice: %lld link-face tests exceed one pass (2^31)", (long long)n_units);
       return OW_ERR_CAPACITY;
     }
-    return ow_lattice_links_count_range(ctx, f, level, d_leaves, n_leaves, pos_lo, pos_hi, d_coords, n_faces,
-                                        geom_key, grid, h_dirs, n_dirs, d_flags, out_boundary, stream);
+    return lat_count(ctx, f, level, d_leaves, n_leaves, pos_lo, pos_hi, d_coords, n_faces, geom_key, grid, h_dirs,
+                     n_dirs, d_flags, out_boundary, stream, nullptr);
   }
   ctx->lat_ncb = n_cb;
   // statistics over both sweeps (rows of k_lat_mt + rows tested inline)
@@ -1415,6 +1442,59 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
   ctx->lat_boundary = nb;
   ctx->lat_links = n_links;
   *out_boundary = nb;
+  return OW_OK;
+}
+}  // namespace
+
+extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_leaves,
+                                            int64_t n_leaves, int64_t pos_lo, int64_t pos_hi, const float* d_coords,
+                                            int64_t n_faces, int64_t geom_key, const ow_grid* grid,
+                                            const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags,
+                                            int64_t* out_boundary, void* stream) {
+  return lat_count(ctx, f, level, d_leaves, n_leaves, pos_lo, pos_hi, d_coords, n_faces, geom_key, grid, h_dirs,
+                   n_dirs, d_flags, out_boundary, (cudaStream_t)stream, nullptr);
+}
+
+// Device-sized lattice stage of the fused pass: the finest leaves' count
+// *d_nl (<= nl_cap) is on the device; count (no readback) ...
+int ow_lattice_dev_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_leaves, const int64_t* d_nl,
+                         int64_t nl_cap, const float* d_coords, int64_t n_faces, const int8_t* h_dirs, int32_t n_dirs,
+                         uint32_t* d_flags, cudaStream_t s) {
+  int64_t nb = 0;
+  return lat_count(ctx, f, level, d_leaves, nl_cap, 0, INT64_MAX, d_coords, n_faces, -1, nullptr, h_dirs, n_dirs,
+                   d_flags, &nb, s, d_nl);
+}
+
+// ... then emit with the candidate-block count on the device: persistent grids
+// of ncb_grid CTAs, writes bounded by row_cap (cells, q, packed rows) and
+// link_cap (packed q).  The caller reads the counts afterwards.
+int ow_lattice_dev_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, int64_t row_cap, uint32_t* d_rows,
+                        float* d_q_packed, int64_t link_cap, int64_t ncb_grid, cudaStream_t s) {
+  LatArgs A = make_args(ctx);
+  A.cells_out = d_cells;
+  A.q_out = d_q;
+  A.rows_out = reinterpret_cast<uint2*>(d_rows);
+  A.qp_out = d_q_packed;
+  A.out_row_cap = row_cap;
+  A.out_link_cap = link_cap;
+  const int C = ctx->lat_forest.dim == 3 ? 64 : 16;
+  const int64_t nl = ctx->lat_leaves;  // (the bound)
+  const unsigned g = (unsigned)(ncb_grid < 1 ? 1 : (ncb_grid > nl ? (nl > 0 ? nl : 1) : ncb_grid));
+  OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
+  if (d_q_packed)
+    OW_TRY(scan(ctx, BcountLoad{A.hcount, A.n_cb_d}, BoffStore{A.hoff, A.n_cb_d}, nl, ctx->d_small + 36, s));
+  if (ctx->lat_forest.dim == 3) {
+    ow_launch(k_lat_emit<3>, g, C, 0, s, A);
+    ow_launch(k_lat_hits<3>, 8 * OW_SMS, 256, 0, s, A);
+    if (d_q_packed) ow_launch(k_lat_pack<3>, g, C, 0, s, A);
+  } else {
+    ow_launch(k_lat_emit<2>, g, C, 0, s, A);
+    ow_launch(k_lat_hits<2>, 8 * OW_SMS, 256, 0, s, A);
+    if (d_q_packed) ow_launch(k_lat_pack<2>, g, C, 0, s, A);
+  }
+  OW_PROF_END(ctx, PROF_LATTICE, s);
+  ctx->launches += d_q_packed ? 3 : 2;
+  OW_CHECK_LAUNCH();
   return OW_OK;
 }
 

@@ -151,8 +151,9 @@ struct MarkArgs {
 // the reference's cull holds no face that passes it.
 template <int D>
 __global__ void k_chunk_boxes(const int32_t* __restrict__ ids, int64_t n_entries, const float4* __restrict__ box,
-                              float4* cbox) {
+                              float4* cbox, const int64_t* d_n) {
   ow_pdl_wait();
+  if (d_n && *d_n < n_entries) n_entries = *d_n;  // entry count on the device (n_entries: its bound)
   // warp per chunk: independent loads, min / max (exact, order-free) by shuffles
   const int lane = threadIdx.x & 31;
   const int64_t n_chunks = (n_entries + 31) / 32;
@@ -700,7 +701,7 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
                    int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int32_t* d_bin_ids,
                    const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,
                    double reach, unsigned long long* out, cudaStream_t s, const int64_t* d_n_leaves,
-                   bool chunk_boxes_ready, const int64_t* d_slice) {
+                   bool chunk_boxes_ready, const int64_t* d_slice, const int64_t* d_bin_entries) {
   if (!(d_spec > 0.0f)) {
     ow_set_error("near-wall distance must be positive, got %g", (double)d_spec);
     return OW_ERR_INVALID;
@@ -752,8 +753,9 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   OW_TRY(ow_fill_async(ctx, ph, 0, 4 * (size_t)(n_leaves + (n_leaves & 1)) + 8, s));
   if (!chunk_boxes_ready) {  // the driver reuses them while the bins and face boxes are unchanged
     const int cg = ow_blocks((n_entries + 31) / 32, 4, 16 * OW_SMS);
-    if (f->dim == 3) ow_launch(k_chunk_boxes<3>, cg, 128, 0, s, d_bin_ids, n_entries, A.box, (float4*)pc);
-    else ow_launch(k_chunk_boxes<2>, cg, 128, 0, s, d_bin_ids, n_entries, A.box, (float4*)pc);
+    const int64_t* dn = binned ? d_bin_entries : nullptr;
+    if (f->dim == 3) ow_launch(k_chunk_boxes<3>, cg, 128, 0, s, d_bin_ids, n_entries, A.box, (float4*)pc, dn);
+    else ow_launch(k_chunk_boxes<2>, cg, 128, 0, s, d_bin_ids, n_entries, A.box, (float4*)pc, dn);
   }
   OW_PROF_BEGIN(ctx, PROF_MARK, s);
   // persistent past 4 waves (k_mark_blocks strides over the device leaf count)

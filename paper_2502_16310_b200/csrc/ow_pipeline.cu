@@ -154,6 +154,34 @@ extern "C" int ow_forest_init_root(ow_ctx* ctx, ow_forest* f, void* stream) {
 }
 
 namespace {
+// the device-resident loop's summary words (SUM_W per pass + the deepest
+// level's leaf count): host checks and results; DRV_RETRY when the forest
+// outgrew its capacity or a 2:1 cascade outran the device sweeps
+int drv_apply(ow_ctx* ctx, ow_forest* f, const int64_t* h, int passes, ow_nearwall_result* out) {
+  for (int level = 0; level < passes; ++level) {
+    const int64_t* w = h + SUM_W * level;
+    if (w[RS_INTER]) {
+      ow_set_error("level %d still carries intermediate marks; finish propagation first", level);
+      return OW_ERR_INVALID;
+    }
+    if (w[RS_MARKED] > 0 && level >= f->max_level) {
+      ow_set_error("refinement beyond max level %d", f->max_level);
+      return OW_ERR_INVALID;
+    }
+    if (w[RS_OVER] || w[7] > 0) return DRV_RETRY;
+    f->n_blocks = w[6];
+    out->marked_refined[level] = w[RS_MARKED];
+    out->n_split[level] = w[RS_SPLITS];
+    out->marked_detected[level] = w[8];
+    out->tests[level] = w[9];
+    out->evaluated[level] = w[10];
+    out->sphere_tests[level] = w[11];
+    out->box_culls[level] = w[12];
+  }
+  ctx->drv_spec_nl = h[SUM_W * passes];
+  return OW_OK;
+}
+
 // The level loop.  dev = false: the block count returns to the host after each
 // refinement (exact launch sizes; capacity overflows and deep 2:1 cascades are
 // finished on the host path, which grows the forest).  dev = true (fused pass
@@ -167,6 +195,9 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
                   const ow_grid* grid, const ow_nearwall_params* p, int32_t* d_bin_ids, int64_t bin_ids_capacity,
                   int32_t* d_bin_counts, int32_t* d_bin_offsets, ow_nearwall_result* out, cudaStream_t s, bool dev) {
   ctx->drv_spec_nl = -1;
+  // device-sized fused pass (g2g_device): bins are counted and emitted with
+  // their entry count on the device and nothing is read back here
+  const bool devpass = dev && ctx->dev_pass;
   ow_comm* comm = p->world > 1 ? p->comm : nullptr;
   if (p->world > 1 && !comm) dev = false;  // (the host exchange hook needs the leaf count on the host)
   if (comm && (comm->world != p->world || comm->rank != p->rank || !comm->open)) {
@@ -237,7 +268,9 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
   // face summary) happen first, so everything below runs without one and can
   // be replayed as a CUDA graph (ow_graph.cu)
   bool pre_counted = false;
-  if (dev && p->binned && p->reuse_bins) {
+  if (devpass) {
+    E = ctx->dev_e_cap;  // (the bound; the count stays on the device)
+  } else if (dev && p->binned && p->reuse_bins) {
     OW_TRY(record(se, 0, 0, s, ctx->no_stage_events));
     OW_TRY(count_bins());
     pre_counted = true;
@@ -258,9 +291,14 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
     bool fresh_bins = level == 0;  // chunk boxes of the bins (marking) need a rebuild
     if (p->binned && (!have_bins || !p->reuse_bins)) {
       fresh_bins = true;
-      if (!bins_counted) OW_TRY(count_bins());
-      bins_counted = false;
-      OW_TRY(ow_fill_bins_emit(ctx, grid, d_bin_ids, d_bin_counts, d_bin_offsets, s));
+      if (devpass) {
+        OW_TRY(ow_fill_bins_dev(ctx, grid, d_coords, n_faces, p->spacing, d_bin_counts, d_bin_ids, d_bin_offsets, E,
+                                s));
+      } else {
+        if (!bins_counted) OW_TRY(count_bins());
+        bins_counted = false;
+        OW_TRY(ow_fill_bins_emit(ctx, grid, d_bin_ids, d_bin_counts, d_bin_offsets, s));
+      }
       have_bins = true;
       out->bin_entries = E;
       out->bins_built += 1;
@@ -327,7 +365,8 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
       OW_TRY(ow_mark_launch(ctx, f, (const int32_t*)pl, n_host, d_coords, n_faces, geom_key,
                             p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
                             p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
-                            p->binned ? E : 0, p->d_spec, p->reach, dst, s, dn, !fresh_bins));
+                            p->binned ? E : 0, p->d_spec, p->reach, dst, s, dn, !fresh_bins, nullptr,
+                            devpass ? ctx->d_small + 5 : nullptr));
     }
     // ---- propagation (binned only): 1 + floor(d / min block length)
     OW_TRY(record(se, level, 2, s, ctx->no_stage_events));
@@ -405,30 +444,12 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
   } else {
     OW_TRY(device_part());
   }
-  if (dev && passes > 0) {
+  if (devpass) {
+    // (the caller reads the summary with its other words after the lattice work)
+  } else if (dev && passes > 0) {
     int64_t h[SUM_W * OW_MAX_PASSES + 1];
     OW_TRY(ow_readback(ctx, d_sum, SUM_W * passes + 1, h, s));
-    for (int level = 0; level < passes; ++level) {
-      const int64_t* w = h + SUM_W * level;
-      if (w[RS_INTER]) {
-        ow_set_error("level %d still carries intermediate marks; finish propagation first", level);
-        return OW_ERR_INVALID;
-      }
-      if (w[RS_MARKED] > 0 && level >= f->max_level) {
-        ow_set_error("refinement beyond max level %d", f->max_level);
-        return OW_ERR_INVALID;
-      }
-      if (w[RS_OVER] || w[7] > 0) return DRV_RETRY;
-      f->n_blocks = w[6];
-      out->marked_refined[level] = w[RS_MARKED];
-      out->n_split[level] = w[RS_SPLITS];
-      out->marked_detected[level] = w[8];
-      out->tests[level] = w[9];
-      out->evaluated[level] = w[10];
-      out->sphere_tests[level] = w[11];
-      out->box_culls[level] = w[12];
-    }
-    ctx->drv_spec_nl = h[SUM_W * passes];
+    OW_TRY(drv_apply(ctx, f, h, passes, out));
   } else if (passes > 0) {
     int64_t h[5 * OW_MAX_PASSES];
     OW_TRY(ow_readback(ctx, (const int64_t*)stats, 5 * passes, h, s));
@@ -538,10 +559,10 @@ int ow_faces_settle(ow_ctx* ctx, const int64_t* h6, cudaStream_t s) {
   return OW_OK;
 }
 
-extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces,
-                                   int64_t geom_key, ow_forest* f, const ow_grid* grid, const ow_g2g_params* p,
-                                   int32_t* d_bin_ids, int64_t bin_ids_capacity, int32_t* d_bin_counts,
-                                   int32_t* d_bin_offsets, ow_g2g_result* out, void* stream) {
+namespace {
+int g2g_sync(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces, int64_t geom_key, ow_forest* f,
+             const ow_grid* grid, const ow_g2g_params* p, int32_t* d_bin_ids, int64_t bin_ids_capacity,
+             int32_t* d_bin_counts, int32_t* d_bin_offsets, ow_g2g_result* out, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   memset(out, 0, sizeof(*out));
   out->faces.first_degenerate = out->faces.first_nonfinite = -1;
@@ -710,4 +731,301 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
   }
   OW_TRY(ow_lattice_stats(ctx, out->lattice_stats, stream));
   return ow_stage_times(ctx, &out->nw);  // host work overlapping the emit kernels
+}
+}  // namespace (g2g_sync)
+
+// ---------------------------------------------------------------------------
+// Device-sized pass: the whole geometry-to-grid pass is enqueued without a
+// host round trip — bins counted and emitted with their entry count on the
+// device, the level loop device-resident (a CUDA graph when replayable), the
+// lattice stage sized by the deepest level's leaf count on the device, emit
+// kernels striding over the candidate-block count — and ONE readback at the
+// end carries every count the host needs.  Launch sizes come from capacities
+// (the forest capacity, the caller's output buffers, the bin-entry and
+// lattice-row estimates of earlier passes); every kernel bounds its writes by
+// them.  The host then checks, in the reference's error order, the face
+// summary, the bin counts, the driver summary and the lattice counts; a pass
+// whose capacity or assumption (no slow bin faces, the near-wall reach
+// predicted from the domain, every level split) did not hold is re-run on the
+// synchronous path (g2g_sync), which also learns the larger capacities.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int G2G_RETRY = 1001;
+constexpr int G2G_WORDS = 34;  // [0, 8) bins, [8, 28) lattice (d_small 33..52), [28, 34) face summary
+
+// every word the host needs, written straight into mapped pinned host memory
+// (no copy-engine transfer after the last kernel): the driver summary, then
+// the bin, lattice and face words
+__global__ void k_g2g_summary(const int64_t* __restrict__ small, const int64_t* __restrict__ sum, int n_sum,
+                              volatile int64_t* dst) {
+  ow_pdl_wait();
+  for (int i = threadIdx.x; i < n_sum; i += blockDim.x) dst[i] = sum[i];
+  volatile int64_t* t = dst + n_sum;
+  const int k = threadIdx.x;
+  if (k < 8) t[k] = small[k];
+  if (k < 20) t[8 + k] = small[33 + k];
+  if (k < 6) t[28 + k] = small[56 + k];
+}
+
+__global__ void k_widen_dev(const int32_t* __restrict__ in, const int64_t* d_n, int64_t cap, int64_t* out) {
+  ow_pdl_wait();
+  const int64_t n = *d_n < cap ? *d_n : cap;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+// near-wall reach (nearwall.py:31-40) from the domain alone: equal to the
+// reference's value whenever no coordinate of the geometry exceeds the
+// domain's largest |bound| (checked against the face summary afterwards)
+double predicted_reach(const ow_forest* f, const ow_nearwall_params* nw) {
+  if (nw->reach > 0.0) return nw->reach;
+  double scale = 0.0;
+  for (int a = 0; a < f->dim; ++a) scale = fmax(scale, fmax(fabs(f->dmin[a]), fabs(f->dmin[a] + f->dext[a])));
+  return nw->d_spec64 + 1e-3 * fmax(1.0, fmax(scale, nw->d_spec64));
+}
+
+int g2g_device(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces, int64_t geom_key,
+               ow_forest* f, const ow_grid* grid, const ow_g2g_params* p, int32_t* d_bin_ids,
+               int64_t bin_ids_capacity, int32_t* d_bin_counts, int32_t* d_bin_offsets, ow_g2g_result* out,
+               cudaStream_t s) {
+  const int D = f->dim, C = D == 3 ? 64 : 16, Q = p->lattice_q;
+  const int passes = p->nw.n_levels - 1;
+  // capacities of this pass
+  const int64_t e_cap = ctx->dev_e_cap < bin_ids_capacity ? ctx->dev_e_cap : bin_ids_capacity;
+  int64_t nl_cap = f->capacity;
+  nl_cap = p->out_cap[OW_OUT_FLAGS] / (4 * C) < nl_cap ? p->out_cap[OW_OUT_FLAGS] / (4 * C) : nl_cap;
+  nl_cap = p->out_cap[OW_OUT_LEAVES] / 8 < nl_cap ? p->out_cap[OW_OUT_LEAVES] / 8 : nl_cap;
+  int64_t row_cap = p->out_cap[OW_OUT_CELLS] / 8;
+  row_cap = p->out_cap[OW_OUT_Q] / (4 * (int64_t)Q) < row_cap ? p->out_cap[OW_OUT_Q] / (4 * (int64_t)Q) : row_cap;
+  const bool packed = p->host_rows && p->host_q_packed && p->host_row_cap > 0 && p->host_link_cap > 0;
+  const bool host_forest = p->host_level && p->host_block_cap > 0;
+  const bool deferred = p->copy_done && packed && host_forest && p->dev_rows && p->dev_q_packed &&
+                        p->dev_row_cap > 0 && p->dev_link_cap > 0;
+  int64_t link_cap = INT64_MAX;
+  uint32_t* d_rows = nullptr;
+  float* d_qp = nullptr;
+  if (packed) {
+    row_cap = p->host_row_cap < row_cap ? p->host_row_cap : row_cap;
+    link_cap = p->host_link_cap;
+    if (deferred) {
+      row_cap = p->dev_row_cap < row_cap ? p->dev_row_cap : row_cap;
+      link_cap = p->dev_link_cap < link_cap ? p->dev_link_cap : link_cap;
+      d_rows = (uint32_t*)p->dev_rows;
+      d_qp = (float*)p->dev_q_packed;
+    } else {
+      void *pr, *pq;
+      OW_TRY(ow_slot(ctx, SLOT_LAT_RFLAGS, 8 * (size_t)row_cap, s, &pr));
+      OW_TRY(ow_slot(ctx, SLOT_LAT_QPACK, 4 * (size_t)link_cap, s, &pq));
+      d_rows = (uint32_t*)pr;
+      d_qp = (float*)pq;
+    }
+  }
+  if (e_cap < 1 || nl_cap < 1 || row_cap < 1) return G2G_RETRY;
+  // ---- the pass, enqueued without a host round trip
+  if (p->copy_done) OW_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)p->copy_done, 0));
+  if (d_records) OW_TRY(ow_stl_binary_to_soa(ctx, d_records, n_faces, d_coords, s));
+  OW_TRY(ow_face_check_launch(ctx, D, d_coords, n_faces, ctx->d_small + 56, s));
+  OW_TRY(ow_forest_init_root(ctx, f, s));
+  ow_nearwall_params nw = p->nw;
+  nw.reach = predicted_reach(f, &p->nw);
+  ctx->faces_pending = nullptr;
+  ctx->defer_stage_times = true;
+  ctx->no_stage_events = p->no_stage_times != 0;
+  ctx->dev_pass = true;
+  const int64_t e_cap_used = e_cap;
+  ctx->dev_e_cap = e_cap;  // (read by refine_driver)
+  int st = refine_driver(ctx, f, d_coords, n_faces, geom_key, grid, &nw, d_bin_ids, bin_ids_capacity, d_bin_counts,
+                         d_bin_offsets, &out->nw, s, true);
+  ctx->dev_pass = false;
+  if (st != OW_OK) return st;
+  void* drv = ctx->slot_ptr[SLOT_DRV_STATE];
+  int64_t* d_sum = (int64_t*)drv + 72 * passes + 8;
+  const int64_t* d_nl = d_sum + SUM_W * passes;  // the deepest level's leaf count (refine_driver)
+  const int32_t* leaves = (const int32_t*)ctx->slot_ptr[SLOT_DRV_LEAVES];
+  int64_t* leaves64 = (int64_t*)p->out_buf[OW_OUT_LEAVES];
+  uint32_t* flags = (uint32_t*)p->out_buf[OW_OUT_FLAGS];
+  ow_launch(k_widen_dev, ow_blocks(nl_cap, 256, 4 * OW_SMS), 256, 0, s, leaves, d_nl, nl_cap, leaves64);
+  OW_LAUNCHED(ctx);
+  ctx->lat_mean_extent = ctx->dev_mean_extent;
+  ctx->lat_comm = nullptr;
+  st = ow_lattice_dev_count(ctx, f, passes, leaves, d_nl, nl_cap, d_coords, n_faces, p->lattice_dirs, Q, flags, s);
+  ctx->lat_mean_extent = 0.0f;
+  OW_TRY(st);
+  const int64_t ncb_grid = ctx->dev_ncb > 0 ? ctx->dev_ncb : 4 * OW_SMS;
+  OW_TRY(ow_lattice_dev_emit(ctx, (int64_t*)p->out_buf[OW_OUT_CELLS], (float*)p->out_buf[OW_OUT_Q], row_cap, d_rows,
+                             d_qp, link_cap, ncb_grid, s));
+  // ---- the one readback: k_g2g_summary stores into pinned host memory
+  const int n_sum = SUM_W * passes + 1;
+  static_assert(128 + SUM_W * OW_MAX_PASSES + 1 + G2G_WORDS <= OW_PINNED_WORDS, "pinned summary area");
+  if (!ctx->h_pinned_dev) OW_CUDA(cudaHostGetDevicePointer((void**)&ctx->h_pinned_dev, ctx->h_pinned, 0));
+  ow_launch(k_g2g_summary, 1, 128, 0, s, (const int64_t*)ctx->d_small, (const int64_t*)d_sum, n_sum,
+            (volatile int64_t*)(ctx->h_pinned_dev + 128));
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  OW_CUDA(cudaStreamSynchronize(s));
+  int64_t h[SUM_W * OW_MAX_PASSES + 1], t[G2G_WORDS];
+  memcpy(h, ctx->h_pinned + 128, 8 * (size_t)n_sum);
+  memcpy(t, ctx->h_pinned + 128 + n_sum, sizeof(t));
+  // faces first (the reference's import order), then bins, driver, lattice
+  ow_nearwall_params nw_true = p->nw;
+  FacesState fs_state{out, f, &nw_true, n_faces};
+  ctx->faces_state = &fs_state;
+  ctx->faces_pending = ctx->d_small + 56;
+  st = ow_faces_settle(ctx, t + 28, s);
+  ctx->faces_state = nullptr;
+  ctx->faces_pending = nullptr;
+  ctx->defer_stage_times = false;
+  ctx->no_stage_events = false;
+  if (st != OW_OK) return st;
+  if (t[1] >= 0) {
+    ow_set_error("face sample outside binning domain (face %lld)", (long long)t[1]);
+    return OW_ERR_INVALID;
+  }
+  if (t[2]) {
+    ow_set_error("fill_bins: a face sample escaped its padded bin range (internal)");
+    return OW_ERR_INTERNAL;
+  }
+  const int64_t E = t[5];
+  ctx->dev_mean_extent = out->faces.mean_extent;
+  if (E > e_cap_used) ctx->dev_e_cap = E + E / 4 + 1024;
+  if (t[0] > 0 || E > e_cap_used || E > p->nw.overlap_factor * n_faces || nw_true.reach != nw.reach)
+    return G2G_RETRY;  // slow bin faces, short pair buffers, a capacity error or another reach
+  st = drv_apply(ctx, f, h, passes, &out->nw);
+  if (st == DRV_RETRY) return G2G_RETRY;
+  if (st != OW_OK) return st;
+  out->nw.n_passes = passes;
+  out->nw.bin_entries = E;
+  out->nw.bins_built = 1;
+  int finest = 0;
+  for (int l = 0; l < passes; ++l)
+    if (out->nw.n_split[l] > 0) finest = l + 1;
+  const int64_t nl = h[SUM_W * passes];
+  if (finest != passes || nl > nl_cap) return G2G_RETRY;
+  const int64_t* L = t + 8;  // d_small[33 + i]
+  const int64_t n_cb = L[0], nb = L[2], n_links = L[18];
+  const int64_t n_rows = (int64_t)((uint64_t)L[15] & ((1ull << 28) - 1)), n_units = (int64_t)((uint64_t)L[15] >> 28);
+  if (n_rows > ctx->lat_row_cap || n_units > ctx->lat_unit_cap || L[16] > ctx->lat_ihit_cap) {
+    // the sync path grows the row / hit lists (and re-runs the sweep)
+    return G2G_RETRY;
+  }
+  if (nb > row_cap || n_links > link_cap) return G2G_RETRY;
+  // ---- results
+  out->finest_level = finest;
+  out->n_finest_leaves = nl;
+  out->n_boundary = nb;
+  out->n_links = n_links;
+  ctx->lat_ncb = n_cb;
+  ctx->lat_rows = n_rows + (int64_t)((uint64_t)L[17] & ((1ull << 28) - 1));
+  ctx->lat_units = n_units + (int64_t)((uint64_t)L[17] >> 28);
+  ctx->lat_boundary = nb;
+  ctx->lat_links = n_links;
+  ctx->dev_ncb = n_cb;
+  out->lattice_stats[0] = n_cb;
+  out->lattice_stats[1] = ctx->lat_rows;
+  out->lattice_stats[2] = ctx->lat_units;
+  // host copies (the pass is complete on `s`): on the copy stream for a
+  // deferred caller, else on `s`
+  const int64_t nbk = f->n_blocks;
+  const bool fc = host_forest && p->host_block_cap >= nbk;
+  const bool rows_fit = packed && nb > 0;
+  if (fc || rows_fit || (!packed && p->host_cells && p->host_q && p->host_row_cap >= nb && nb > 0)) {
+    cudaStream_t cs = s;
+    if (deferred) {
+      if (!ctx->copy_stream) {
+        OW_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        OW_CUDA(cudaEventCreateWithFlags(&ctx->copy_ev[0], cudaEventDisableTiming));
+        OW_CUDA(cudaEventCreateWithFlags(&ctx->copy_ev[1], cudaEventDisableTiming));
+      }
+      cs = ctx->copy_stream;
+      OW_CUDA(cudaEventRecord(ctx->copy_ev[0], s));
+      OW_CUDA(cudaStreamWaitEvent(cs, ctx->copy_ev[0], 0));
+    }
+    if (fc) {
+      OW_CUDA(cudaMemcpyAsync(p->host_level, f->d_level, 2 * (size_t)nbk, cudaMemcpyDeviceToHost, cs));
+      for (int a = 0; a < D; ++a)
+        OW_CUDA(cudaMemcpyAsync(p->host_coord[a], f->d_coord[a], 4 * (size_t)nbk, cudaMemcpyDeviceToHost, cs));
+      OW_CUDA(cudaMemcpyAsync(p->host_parent, f->d_parent, 4 * (size_t)nbk, cudaMemcpyDeviceToHost, cs));
+      OW_CUDA(cudaMemcpyAsync(p->host_first_child, f->d_first_child, 4 * (size_t)nbk, cudaMemcpyDeviceToHost, cs));
+      OW_CUDA(cudaMemcpyAsync(p->host_marks, f->d_marks, (size_t)nbk, cudaMemcpyDeviceToHost, cs));
+      out->host_copied |= 1;
+    }
+    if (rows_fit) {
+      OW_CUDA(cudaMemcpyAsync(p->host_rows, d_rows, 8 * (size_t)nb, cudaMemcpyDeviceToHost, cs));
+      OW_CUDA(cudaMemcpyAsync(p->host_q_packed, d_qp, 4 * (size_t)n_links, cudaMemcpyDeviceToHost, cs));
+      out->host_copied |= deferred ? 4 | 8 : 4;
+    } else if (!packed && p->host_cells && p->host_q && p->host_row_cap >= nb && nb > 0) {
+      OW_CUDA(cudaMemcpyAsync(p->host_cells, p->out_buf[OW_OUT_CELLS], 8 * (size_t)nb, cudaMemcpyDeviceToHost, cs));
+      OW_CUDA(cudaMemcpyAsync(p->host_q, p->out_buf[OW_OUT_Q], 4 * (size_t)nb * Q, cudaMemcpyDeviceToHost, cs));
+      out->host_copied |= 2;
+    }
+    if (deferred) OW_CUDA(cudaEventRecord((cudaEvent_t)p->copy_done, cs));
+  }
+  if (p->copy_done && !deferred) OW_CUDA(cudaEventRecord((cudaEvent_t)p->copy_done, s));
+  return ow_stage_times(ctx, &out->nw);
+}
+
+bool g2g_device_eligible(const ow_ctx* ctx, const ow_forest* f, const ow_g2g_params* p) {
+  static const bool env_off = [] {
+    const char* e = getenv("OW_DEVICE_PASS");
+    return e && e[0] == '0';
+  }();
+  if (env_off || ctx->dev_disabled || ctx->dev_e_cap <= 0) return false;
+  if (p->nw.world > 1 || !p->nw.binned || !p->nw.reuse_bins || p->nw.n_levels < 2) return false;
+  if (p->lattice_q < 2 || !p->alloc) return false;
+  for (int k = 0; k < 4; ++k)
+    if (!p->out_buf[k] || p->out_cap[k] <= 0) return false;
+  if (ctx->prof && ctx->prof->enabled) return false;  // (profiled passes keep per-stage brackets)
+  return f->capacity > 0;
+}
+}  // namespace
+
+extern "C" int ow_set_device_pass(ow_ctx* ctx, int32_t enable) {
+  ctx->dev_disabled = enable ? 0 : 1;
+  return OW_OK;
+}
+
+extern "C" int ow_device_pass_stats(ow_ctx* ctx, int64_t* out2) {
+  out2[0] = ctx->dev_passes;
+  out2[1] = ctx->dev_fallbacks;
+  return OW_OK;
+}
+
+extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces,
+                                   int64_t geom_key, ow_forest* f, const ow_grid* grid, const ow_g2g_params* p,
+                                   int32_t* d_bin_ids, int64_t bin_ids_capacity, int32_t* d_bin_counts,
+                                   int32_t* d_bin_offsets, ow_g2g_result* out, void* stream) {
+  bool fell_back = false;
+  if (n_faces > 0 && g2g_device_eligible(ctx, f, p)) {
+    memset(out, 0, sizeof(*out));
+    out->faces.first_degenerate = out->faces.first_nonfinite = -1;
+    const int st = g2g_device(ctx, d_records, d_coords, n_faces, geom_key, f, grid, p, d_bin_ids, bin_ids_capacity,
+                              d_bin_counts, d_bin_offsets, out, (cudaStream_t)stream);
+    ctx->dev_pass = false;
+    ctx->faces_pending = nullptr;
+    ctx->faces_state = nullptr;
+    ctx->defer_stage_times = false;
+    ctx->no_stage_events = false;
+    if (st != G2G_RETRY) {
+      if (st == OW_OK) {
+        ctx->dev_passes++;
+        out->device_sized = 1;
+      }
+      return st;
+    }
+    ctx->dev_fallbacks++;
+    fell_back = true;
+    // (records already converted: the synchronous pass starts from the coordinates)
+    d_records = nullptr;
+  }
+  const int st = g2g_sync(ctx, d_records, d_coords, n_faces, geom_key, f, grid, p, d_bin_ids, bin_ids_capacity,
+                          d_bin_counts, d_bin_offsets, out, stream);
+  if (st == OW_OK) {  // capacities for the next device-sized pass
+    const int64_t E = out->nw.bin_entries;
+    const int64_t want = E + E / 4 + 1024;
+    if (ctx->dev_e_cap < want) ctx->dev_e_cap = want;
+    ctx->dev_ncb = out->lattice_stats[0];
+    ctx->dev_mean_extent = out->faces.mean_extent;
+    out->device_sized = fell_back ? 2 : 0;
+  }
+  return st;
 }

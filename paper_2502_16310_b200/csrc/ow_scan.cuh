@@ -324,8 +324,9 @@ constexpr int RS_WARPS = RS_THREADS / 32;
 
 template <int BITS, int ITEMS>
 __global__ void __launch_bounds__(RS_THREADS)
-k_radix_hist(const uint32_t* keys, int64_t n, int shift, int64_t n_tiles, int32_t* hist) {
+k_radix_hist(const uint32_t* keys, int64_t n, int shift, int64_t n_tiles, int32_t* hist, const int64_t* d_n) {
   ow_pdl_wait();
+  if (d_n && *d_n < n) n = *d_n;  // live length on the device (n: the buffers' bound)
   constexpr int DIG = 1 << BITS, TILE = RS_THREADS * ITEMS;
   __shared__ int h[DIG];
   for (int d = threadIdx.x; d < DIG; d += RS_THREADS) h[d] = 0;
@@ -343,8 +344,9 @@ k_radix_hist(const uint32_t* keys, int64_t n, int shift, int64_t n_tiles, int32_
 template <int BITS, int ITEMS>
 __global__ void __launch_bounds__(RS_THREADS)
 k_radix_scatter(const uint32_t* keys, const int32_t* vals, int64_t n, int shift, int64_t n_tiles,
-                const int32_t* hist_excl, uint32_t* keys_out, int32_t* vals_out) {
+                const int32_t* hist_excl, uint32_t* keys_out, int32_t* vals_out, const int64_t* d_n) {
   ow_pdl_wait();
+  if (d_n && *d_n < n) n = *d_n;
   constexpr int DIG = 1 << BITS, TILE = RS_THREADS * ITEMS, WARP_ITEMS = TILE / RS_WARPS;
   __shared__ int cnt[RS_WARPS][DIG];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -394,12 +396,13 @@ k_radix_scatter(const uint32_t* keys, const int32_t* vals, int64_t n, int shift,
 
 template <int BITS, int ITEMS>
 inline int radix_pass(ow_ctx* ctx, const uint32_t* ki, const int32_t* vi, uint32_t* ko, int32_t* vo, int64_t n,
-                      int shift, int64_t tiles, int32_t* hist, cudaStream_t s) {
-  ow_launch(k_radix_hist<BITS, ITEMS>, (unsigned)tiles, RS_THREADS, 0, s, ki, n, shift, tiles, hist);
+                      int shift, int64_t tiles, int32_t* hist, cudaStream_t s, const int64_t* d_n) {
+  ow_launch(k_radix_hist<BITS, ITEMS>, (unsigned)tiles, RS_THREADS, 0, s, ki, n, shift, tiles, hist, d_n);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   OW_TRY(scan(ctx, LoadArr<int32_t>{hist}, StoreExcl<int32_t>{hist}, (int64_t)(1 << BITS) * tiles, nullptr, s));
-  ow_launch(k_radix_scatter<BITS, ITEMS>, (unsigned)tiles, RS_THREADS, 0, s, ki, vi, n, shift, tiles, hist, ko, vo);
+  ow_launch(k_radix_scatter<BITS, ITEMS>, (unsigned)tiles, RS_THREADS, 0, s, ki, vi, n, shift, tiles, hist, ko, vo,
+            d_n);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;
@@ -407,13 +410,14 @@ inline int radix_pass(ow_ctx* ctx, const uint32_t* ki, const int32_t* vi, uint32
 
 template <int BITS>
 inline int radix_pass_items(ow_ctx* ctx, int items, const uint32_t* ki, const int32_t* vi, uint32_t* ko, int32_t* vo,
-                            int64_t n, int shift, int64_t tiles, int32_t* hist, cudaStream_t s) {
+                            int64_t n, int shift, int64_t tiles, int32_t* hist, cudaStream_t s,
+                            const int64_t* d_n) {
   switch (items) {
-    case 1: return radix_pass<BITS, 1>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s);
-    case 2: return radix_pass<BITS, 2>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s);
-    case 4: return radix_pass<BITS, 4>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s);
-    case 8: return radix_pass<BITS, 8>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s);
-    default: return radix_pass<BITS, 16>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s);
+    case 1: return radix_pass<BITS, 1>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s, d_n);
+    case 2: return radix_pass<BITS, 2>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s, d_n);
+    case 4: return radix_pass<BITS, 4>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s, d_n);
+    case 8: return radix_pass<BITS, 8>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s, d_n);
+    default: return radix_pass<BITS, 16>(ctx, ki, vi, ko, vo, n, shift, tiles, hist, s, d_n);
   }
 }
 
@@ -422,12 +426,13 @@ inline int radix_passes(int key_bits) { return key_bits <= 0 ? 0 : (key_bits + 9
 
 // Sort n pairs by the low `key_bits` bits of key, stably.  Input in (k0, v0);
 // the sorted result pointer pair is returned through (*rk, *rv), which is
-// either (k0, v0) or (k1, v1).
+// either (k0, v0) or (k1, v1).  d_n (optional): the live length min(n, *d_n)
+// is read on the device (n then only bounds the buffers and sizes the grid).
 inline int radix_sort_pairs(ow_ctx* ctx, uint32_t* k0, int32_t* v0, uint32_t* k1, int32_t* v1, int64_t n,
-                            int key_bits, uint32_t** rk, int32_t** rv, cudaStream_t s) {
+                            int key_bits, uint32_t** rk, int32_t** rv, cudaStream_t s, const int64_t* d_n = nullptr) {
   *rk = k0;
   *rv = v0;
-  if (n <= 1 || key_bits <= 0) return OW_OK;
+  if ((n <= 1 && !d_n) || n <= 0 || key_bits <= 0) return OW_OK;
   // fewest passes of 8..10-bit digits
   const int passes = radix_passes(key_bits);
   int bits = (key_bits + passes - 1) / passes;
@@ -443,9 +448,9 @@ inline int radix_sort_pairs(ow_ctx* ctx, uint32_t* k0, int32_t* v0, uint32_t* k1
   uint32_t *ki = k0, *ko = k1;
   int32_t *vi = v0, *vo = v1;
   for (int shift = 0; shift < key_bits; shift += bits) {
-    if (bits == 8) OW_TRY(radix_pass_items<8>(ctx, items, ki, vi, ko, vo, n, shift, tiles, hist, s));
-    else if (bits == 9) OW_TRY(radix_pass_items<9>(ctx, items, ki, vi, ko, vo, n, shift, tiles, hist, s));
-    else OW_TRY(radix_pass_items<10>(ctx, items, ki, vi, ko, vo, n, shift, tiles, hist, s));
+    if (bits == 8) OW_TRY(radix_pass_items<8>(ctx, items, ki, vi, ko, vo, n, shift, tiles, hist, s, d_n));
+    else if (bits == 9) OW_TRY(radix_pass_items<9>(ctx, items, ki, vi, ko, vo, n, shift, tiles, hist, s, d_n));
+    else OW_TRY(radix_pass_items<10>(ctx, items, ki, vi, ko, vo, n, shift, tiles, hist, s, d_n));
     uint32_t* tk = ki; ki = ko; ko = tk;
     int32_t* tv = vi; vi = vo; vo = tv;
   }

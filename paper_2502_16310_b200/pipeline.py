@@ -45,6 +45,7 @@ class GridPass:
     reran: bool = False  # the device-resident level loop outgrew the capacity; rerun with host sync
     host_copied: int = 0  # native host copies made (bit 0 forest, bit 2 packed rows, bit 3 deferred)
     done: object = None  # torch.cuda.Event of deferred host copies (run(defer=True)); None: already ordered
+    device_sized: int = 0  # 1: one device-sized pass (single readback); 2: it fell back to the synchronous pass
 
     def wait(self):
         """Block until the host copies of this pass are complete (the
@@ -307,7 +308,8 @@ class GridPlan:
         if host:
             hres = self._host_results(hbuf, int(out.host_copied), forest, links, int(out.n_links))
         done = self._done if int(out.host_copied) & 8 else None
-        return GridPass(geom, forest, result, links, hres, bool(out.reran), int(out.host_copied), done)
+        return GridPass(geom, forest, result, links, hres, bool(out.reran), int(out.host_copied), done,
+                        int(out.device_sized))
 
     def _host_results(self, hbuf, copied, forest, links, n_links):
         """Pinned host copies (the C side streamed whatever fit; the rest is

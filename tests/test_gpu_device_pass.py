@@ -1,0 +1,178 @@
+"""Device-sized fused passes (ow_pipeline.cu: g2g_device): after a plan's
+first pass has sized its output buffers, ``GridPlan.run`` enqueues the whole
+geometry-to-grid pass without a host round trip and reads every count back
+once at the end.  Each pass must equal the synchronous path array for array;
+a pass whose capacities or assumptions do not hold (more bin entries than the
+estimate, slow bin faces, a near-wall reach the domain does not predict,
+larger outputs) falls back to the synchronous pass and is still exact."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ow():
+    import paper_2502_16310_b200 as m
+    from paper_2502_16310_b200 import _build
+
+    _build.build()
+    return m
+
+
+def _records(tris):
+    import torch
+
+    from paper_2502_16310_b200 import shapes
+
+    data = shapes.binary_stl_bytes(tris)
+    return torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda(), int.from_bytes(data[80:84], "little")
+
+
+def _snapshot(gp):
+    out = dict(coords=gp.forest._coords.copy(), first_child=gp.forest._first_child.copy(),
+               parent=gp.forest._parent.copy(), level=gp.forest._level.copy(),
+               marks=gp.forest.marks.cpu().numpy().copy(), detected=list(gp.result.marked_detected),
+               refined=list(gp.result.marked_refined), tests=list(gp.result.cell_face_tests),
+               evaluated=list(gp.result.pairs_evaluated), entries=gp.result.bins.ids.numel(),
+               ids=gp.result.bins.ids.cpu().numpy().copy(), counts=gp.result.bins.counts.cpu().numpy().copy())
+    if gp.links is not None:
+        for name in ("leaves", "flags", "cells", "q"):
+            out[name] = getattr(gp.links, name).cpu().numpy().copy()
+    return out
+
+
+def _equal(a, b, tag):
+    assert a.keys() == b.keys()
+    for k in a:
+        if isinstance(a[k], np.ndarray):
+            np.testing.assert_array_equal(a[k], b[k], err_msg=f"{tag}: {k}")
+        else:
+            assert a[k] == b[k], (tag, k, a[k], b[k])
+
+
+def _run_both(ow, dom, root, params, lattice, inputs, stage_times=False):
+    """The same pass sequence through a device-sized plan and a synchronous one."""
+    import torch
+
+    from paper_2502_16310_b200 import _lib, pipeline
+
+    snaps, modes = [], []
+    for dev in (True, False):
+        _lib.set_device_pass(dev)
+        try:
+            plan = pipeline.GridPlan(dom, root, params, lattice, reuse_outputs=True, stage_times=stage_times)
+            run = []
+            for inp in inputs:
+                gp = plan.run(*inp) if isinstance(inp, tuple) else plan.run(geometry=inp)
+                torch.cuda.synchronize()
+                run.append(_snapshot(gp))
+                if dev:
+                    modes.append(gp.device_sized)
+            snaps.append(run)
+        finally:
+            _lib.set_device_pass(True)
+    for k, (a, b) in enumerate(zip(*snaps)):
+        _equal(a, b, f"pass {k}")
+    return modes
+
+
+def test_device_pass_matches_sync_3d(ow):
+    from paper_2502_16310_b200 import _lib, shapes
+
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8)
+    a = _records(shapes.icosphere_triangles(3))
+    b = _records(shapes.icosphere_triangles(3, radius=0.25))
+    c = _records(shapes.icosphere_triangles(4, radius=0.32))  # more entries / rows than the estimates
+    n0 = _lib.device_pass_stats()
+    modes = _run_both(ow, dom, (8, 8, 8), params, "D3Q19", [a, a, a, a, b, a, c, c, a])
+    assert modes[0] == 0  # the first pass sizes the outputs
+    assert modes[1:4] == [1, 1, 1]  # device-sized: eager, graph capture, graph replay
+    assert modes[-1] == 1
+    assert 2 in modes[6:8]  # the larger geometry outgrew an estimate once: synchronous re-run
+    n1 = _lib.device_pass_stats()
+    assert n1[0] - n0[0] >= 5
+
+
+def test_device_pass_matches_sync_stage_events_and_d3q27(ow):
+    """Stage-timing events on (the level loop runs eagerly, no graph) and a
+    27-direction lattice with 4 levels."""
+    from paper_2502_16310_b200 import shapes
+
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.05, n_levels=4, bins_per_axis=8)
+    a = _records(shapes.bumpy_sphere_triangles(40, 41))
+    modes = _run_both(ow, dom, (8, 8, 8), params, "D3Q27", [a, a, a], stage_times=True)
+    assert modes == [0, 1, 1]
+
+
+def test_device_pass_matches_sync_2d(ow):
+    dom = ow.Aabb(np.zeros(2), np.ones(2))
+    params = ow.NearWallParams(d_spec=0.1, n_levels=3, bins_per_axis=8)
+    g1 = ow.index_to_coords(ow.generate_circle((0.5, 0.5), 0.25, 256))
+    g2 = ow.index_to_coords(ow.generate_circle((0.45, 0.5), 0.3, 700))
+    modes = _run_both(ow, dom, (8, 8), params, "D2Q9", [g1, g1, g1, g2, g2, g1])
+    assert modes[1:3] == [1, 1]
+
+
+def test_device_pass_falls_back_on_slow_faces(ow):
+    """Faces spanning more bins than the bitmask path handles need the slow
+    path's readback: the device-sized attempt falls back, exactly."""
+    import torch
+
+    # a closed octahedron of 8 large faces: each spans many of the 16^3 bins
+    c, r = 0.5, 0.3
+    v = np.array([[c + r, c, c], [c - r, c, c], [c, c + r, c], [c, c - r, c], [c, c, c + r], [c, c, c - r]])
+    faces = [(0, 2, 4), (2, 1, 4), (1, 3, 4), (3, 0, 4), (2, 0, 5), (1, 2, 5), (3, 1, 5), (0, 3, 5)]
+    tris = np.array([[v[i] for i in f] for f in faces], np.float64)
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.05, n_levels=3, bins_per_axis=16, overlap_factor=1000)
+    a = _records(tris)
+    modes = _run_both(ow, dom, (8, 8, 8), params, "D3Q19", [a, a, a])
+    assert modes[1:] == [2, 2]
+    torch.cuda.synchronize()
+
+
+def test_device_pass_falls_back_on_reach(ow):
+    """A vertex slightly beyond the domain's largest |bound| (inside the
+    reference's 1e-6 tolerance) changes the near-wall reach the pass predicts
+    from the domain: fall back, exactly."""
+    from paper_2502_16310_b200 import shapes
+
+    tris = shapes.icosphere_triangles(2)
+    tris = np.concatenate([tris, np.array([[[0.999, 0.5, 0.5], [1.0 + 4e-7, 0.5, 0.5], [0.999, 0.51, 0.5]]])])
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8)
+    a = _records(tris)
+    modes = _run_both(ow, dom, (8, 8, 8), params, "D3Q19", [a, a])
+    assert modes[1] == 2
+
+
+def test_device_pass_errors_match_sync(ow):
+    """Invalid geometry through a device-sized plan raises the synchronous
+    path's error (message and type)."""
+    import torch
+
+    from paper_2502_16310_b200 import pipeline, shapes
+
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8)
+    plan = pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19", reuse_outputs=True, stage_times=False)
+    tris = shapes.icosphere_triangles(3)
+    rec, n = _records(tris)
+    plan.run(rec, n)
+    plan.run(rec, n)
+    bad = tris.copy()
+    bad[7, 1] = bad[7, 0]  # degenerate triangle 7
+    rb, nb = _records(bad)
+    with pytest.raises(ow.InvalidParameterError, match="degenerate"):
+        plan.run(rb, nb)
+    out = tris.copy() + 0.6  # outside the domain
+    ro, no = _records(out)
+    with pytest.raises(ow.InvalidParameterError, match="outside"):
+        plan.run(ro, no)
+    gp = plan.run(rec, n)  # and the plan recovers
+    torch.cuda.synchronize()
+    assert gp.device_sized == 1
