@@ -17,6 +17,7 @@
 // field would wrap, that first kernel clears the array.
 #include <string.h>
 
+#include <chrono>
 #include <functional>
 
 #include "ow_scan.cuh"
@@ -78,7 +79,17 @@ int ow_loop_graph(ow_ctx* ctx, bool ok, const GraphKey* key, cudaStream_t* ps, c
   }
   for (int i = 0; i < NG; ++i)
     if (ctx->loop_exec[i] && memcmp(ctx->loop_key[i], key, sizeof(GraphKey)) == 0) {
+      static const bool timed = getenv("OW_TIME_GRAPH") != nullptr;
+      const auto t0 = std::chrono::steady_clock::now();
       OW_CUDA(cudaGraphLaunch(ctx->loop_exec[i], s));
+      if (timed) {
+        static double acc = 0.0;
+        static int n = 0;
+        acc += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        if (++n % 20 == 0) fprintf(stderr, "graph launch: %.1f us host (mean of 20, %lld kernels)\n", acc / 20,
+                                   (long long)ctx->loop_launches[i]);
+        if (n % 20 == 0) acc = 0.0;
+      }
       ctx->launches += ctx->loop_launches[i];
       ctx->prep_key = -1;  // (the face-prep cache is not tracked across replays)
       return -1;

@@ -348,6 +348,31 @@ def test_lattice_links_vs_oracle(ow, case, inline_units):
         assert ll.n_boundary > 0
 
 
+@pytest.mark.parametrize("sub,root,lat", [(3, 8, "D3Q19"), (4, 8, "D3Q27"), (5, 16, "D3Q19")])
+def test_lattice_face_pass_shapes_agree(ow, sub, root, lat):
+    """The face pass shaped by the face extent (default) and with 4 or 16
+    faces per warp counts the same candidate blocks, rows and link-face tests
+    and produces identical flags, boundary rows and q."""
+    from paper_2502_16310_b200 import _lib, shapes
+
+    coords = np.ascontiguousarray(np.transpose(shapes.icosphere_triangles(sub).astype(np.float32), (1, 2, 0)))
+    geom = ow.CoordListGeometry(3, coords)
+    fg = ow.init_root_grid(domain(ow, 3), (root,) * 3)
+    ow.refine_near_wall(fg, geom, ow.NearWallParams(d_spec=0.05, n_levels=3, bins_per_axis=8))
+    out = []
+    for fpw in (-1, 4, 16):
+        _lib.call("ow_lattice_tune", _lib.ctx(), -1, fpw)
+        try:
+            ll = ow.build_lattice_links(fg, geom, None, lat)
+            out.append(([t.cpu().numpy() for t in (ll.leaves, ll.flags, ll.cells, ll.q)], _lib.lattice_stats()))
+        finally:
+            _lib.call("ow_lattice_tune", _lib.ctx(), -1, -1)
+    for arrs, stats in out[1:]:
+        assert stats == out[0][1]
+        for a, b in zip(arrs, out[0][0]):
+            np.testing.assert_array_equal(a, b)
+
+
 @pytest.mark.parametrize("case", ["wall_between", "wall_on_centres", "wall_at_link_end", "square2d"])
 def test_lattice_known_answers_on_gpu(ow, case):
     from oracle import forest as of
