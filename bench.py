@@ -154,43 +154,68 @@ def e2e_stream(plan, rec_host, n_faces, args, l2_flush, barrier):
     flushes = []
     passes = []
     slow, h2d_b, d2h_b = [], 0, 0
-    prev = None
+    prev = None  # (step, PendingGridPass) submitted, not yet finished by the host
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    h2d(-W)
-    for k in range(-W, K):
-        if k == 0:
-            if prev is not None:
-                prev.wait()  # warm-up results out of the way: the timed stream starts empty
-                prev = None
-            torch.cuda.synchronize()
-            start.record(cs)
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record(cs)
-        l2_flush()
-        f1.record(cs)
-        if k + 1 < K:  # step k+1's bytes start while step k computes (run() returns near a pass's end)
-            h2d(k + 1)
-        cs.wait_event(loaded[k % 2])
-        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        p0.record(cs)
-        gp = plans[k % 2].run(bufs[k % 2], n_faces, host=True, defer=True)
-        p1.record(cs)
-        consumed[k % 2].record(cs)
+
+    def finish(k, pend):
+        # the host finishes step k (its counts, errors, host copies) while
+        # step k+1 already runs on the device, then waits for step k-1's
+        # results to reach host memory (their copies overlapped step k)
+        nonlocal h2d_b, d2h_b
+        gp = pend.result()
         if k >= 0:
-            flushes.append((f0, f1))
-            passes.append((p0, p1))
             h2d_b = rec_host.numel()
             hres = gp.host
             d2h_b = sum(t.numel() * t.element_size() for k2, t in hres.items() if k2 != "coords")
             d2h_b += sum(t.numel() * t.element_size() for t in hres["coords"])
             if gp.reran or gp.host_copied & 5 != 5 or gp.done is None:
                 slow.append(k)
+        return gp
+
+    sync_steps = os.environ.get("OW_E2E_SYNC") == "1"
+    barrier()
+    h2d(-W)
+    done_prev = None
+    for k in range(-W, K):
+        if k == 0:
+            if prev is not None:
+                finish(*prev).wait()  # warm-up results out of the way: the timed stream starts empty
+                prev = None
+            if done_prev is not None:
+                done_prev.wait()
+                done_prev = None
+            torch.cuda.synchronize()
+            start.record(cs)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(cs)
+        l2_flush()
+        f1.record(cs)
+        if k + 1 < K:  # step k+1's bytes start while step k computes
+            h2d(k + 1)
+        cs.wait_event(loaded[k % 2])
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(cs)
+        pend = plans[k % 2].run_async(bufs[k % 2], n_faces, host=True, defer=True)
+        if sync_steps:  # (A/B: the host finishes each step before submitting the next)
+            pend.result()
+        p1.record(cs)
+        consumed[k % 2].record(cs)
+        if k >= 0:
+            flushes.append((f0, f1))
+            passes.append((p0, p1))
         if prev is not None:
-            prev.wait()  # the host has step k-1's results
-        prev = gp
-    if prev is not None and prev.done is not None:
-        cs.wait_event(prev.done)
+            gp = finish(*prev)  # step k-1, while step k runs
+            if done_prev is not None:
+                done_prev.wait()  # the host has step k-2's results
+            done_prev = gp
+        prev = (k, pend)
+    if prev is not None:
+        gp = finish(*prev)
+        if done_prev is not None:
+            done_prev.wait()
+        done_prev = gp
+    if done_prev is not None and done_prev.done is not None:
+        cs.wait_event(done_prev.done)
     end.record(cs)
     torch.cuda.synchronize()
     total = start.elapsed_time(end) - sum(a.elapsed_time(b) for a, b in flushes)
@@ -346,9 +371,10 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         if not text:
             e2e["slow_path_steps"] = slow_path
             e2e["pipeline"] = ("two GridPlans alternate: step k+1's STL bytes go host->device on a copy stream while "
-                               "step k computes, step k's results come back device->host on the library's copy "
-                               "stream (GridPlan.run(host=True, defer=True)) while step k+1 computes, and the host "
-                               "waits for step k's results (GridPass.wait()) after enqueueing step k+1; "
+                               "step k computes; step k+1 is submitted (GridPlan.run_async(host=True, defer=True)) "
+                               "before the host finishes step k (PendingGridPass.result(): its counts, checks and "
+                               "device->host copies on the library's copy stream, which overlap step k+1), and the "
+                               "host waits for step k-1's results (GridPass.wait()) after that; "
                                "ms_per_step = (device time from the first H2D to the last D2H - the L2 flushes "
                                "between passes) / steps; ms_step_* = per-pass compute-stream times")
 

@@ -315,6 +315,23 @@ int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, 
                         int64_t bin_ids_capacity, int32_t* d_bin_counts, int32_t* d_bin_offsets,
                         ow_g2g_result* out, void* stream);
 
+/* The same pass in two steps, so a stream of passes never waits for the host
+ * between passes: submit enqueues it (device-sized when eligible) and returns
+ * *ticket > 0 while it is in flight, or 0 when it already ran synchronously
+ * (`out` final); finish waits for its summary, checks it (the reference's
+ * errors), streams the host copies and fills `out` (a failed capacity or
+ * assumption re-runs the pass synchronously there).  Between the two calls
+ * the caller keeps every argument alive and unchanged; passes of other
+ * forests / outputs may be submitted meanwhile (at most 8 in flight). */
+int ow_geometry_to_grid_submit(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces,
+                               int64_t geom_key, ow_forest* f, const ow_grid* grid, const ow_g2g_params* params,
+                               int32_t* d_bin_ids, int64_t bin_ids_capacity, int32_t* d_bin_counts,
+                               int32_t* d_bin_offsets, ow_g2g_result* out, void* stream, int64_t* ticket);
+int ow_geometry_to_grid_finish(ow_ctx* ctx, int64_t ticket, float* d_coords, int64_t n_faces, int64_t geom_key,
+                               ow_forest* f, const ow_grid* grid, const ow_g2g_params* params, int32_t* d_bin_ids,
+                               int64_t bin_ids_capacity, int32_t* d_bin_counts, int32_t* d_bin_offsets,
+                               ow_g2g_result* out, void* stream);
+
 /* Device-sized fused passes (on by default once a pass has sized the caller's
  * output buffers): enable = 0 keeps ow_geometry_to_grid on the synchronous
  * path (a host round trip per size it needs).  Stats: [0] device-sized passes,

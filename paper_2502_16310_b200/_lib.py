@@ -193,6 +193,10 @@ _SIGS = {
     "ow_forest_init_root": [P, C.POINTER(ForestView), P],
     "ow_geometry_to_grid": [P, P, P, I64, I64, C.POINTER(ForestView), C.POINTER(Grid), C.POINTER(G2GParamsC), P, I64,
                             P, P, C.POINTER(G2GResultC), P],
+    "ow_geometry_to_grid_submit": [P, P, P, I64, I64, C.POINTER(ForestView), C.POINTER(Grid), C.POINTER(G2GParamsC),
+                                   P, I64, P, P, C.POINTER(G2GResultC), P, PI64],
+    "ow_geometry_to_grid_finish": [P, I64, P, I64, I64, C.POINTER(ForestView), C.POINTER(Grid), C.POINTER(G2GParamsC),
+                                   P, I64, P, P, C.POINTER(G2GResultC), P],
     "ow_refine_near_wall": [P, C.POINTER(ForestView), P, I64, I64, C.POINTER(Grid), C.POINTER(NearWallParamsC), P,
                             I64, P, P, C.POINTER(NearWallResultC), P],
     "ow_cell_face_links_count": [P, C.POINTER(ForestView), P, I64, P, I64, I64, C.POINTER(Grid), P, P, P, F32, F64,

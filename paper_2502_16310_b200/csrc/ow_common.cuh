@@ -185,6 +185,9 @@ struct ow_ctx {
   int64_t dev_ncb;                     // candidate blocks of the last pass (emit grid)
   float dev_mean_extent;               // face summary of the last pass (face-pass shape)
   int64_t dev_passes, dev_fallbacks;   // statistics
+  void* g2g_tickets;                   // passes in flight (ow_geometry_to_grid_submit / _finish)
+  int64_t* g2g_ring;                   // their summary areas: mapped pinned host memory ...
+  int64_t* g2g_ring_dev;               // ... and its device alias
 };
 
 // host-side inputs of the device-resident loop (a replay is valid only when
@@ -243,6 +246,8 @@ int ow_lattice_dev_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const i
                          uint32_t* d_flags, cudaStream_t s);
 int ow_lattice_dev_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, int64_t row_cap, uint32_t* d_rows,
                         float* d_q_packed, int64_t link_cap, int64_t ncb_grid, cudaStream_t s);
+
+void ow_g2g_release(ow_ctx* ctx);  // passes-in-flight table (ow_pipeline.cu)
 
 // fill_bins with the entry count left on the device (ow_binning.cu: fill_dev)
 int ow_fill_bins_dev(ow_ctx* ctx, const ow_grid* grid, const float* d_coords, int64_t n_faces, float spacing,

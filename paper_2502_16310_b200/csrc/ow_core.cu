@@ -76,6 +76,7 @@ extern "C" int ow_ctx_destroy(ow_ctx* c) {
           if (c->prof->ev[i][k][j]) cudaEventDestroy(c->prof->ev[i][k][j]);
     free(c->prof);
   }
+  ow_g2g_release(c);
   cudaFreeHost(c->h_pinned);
   cudaFree(c->d_small);
   free(c);

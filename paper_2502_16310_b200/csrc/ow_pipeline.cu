@@ -9,6 +9,7 @@
 // the scalars the algorithm needs to size the next step (leaf count, marks,
 // split / violator counts).
 #include <math.h>
+#include <stddef.h>
 #include <string.h>
 
 #include "ow_scan.cuh"
@@ -784,12 +785,31 @@ double predicted_reach(const ow_forest* f, const ow_nearwall_params* nw) {
   return nw->d_spec64 + 1e-3 * fmax(1.0, fmax(scale, nw->d_spec64));
 }
 
-int g2g_device(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces, int64_t geom_key,
+// One device-sized pass in flight: what its finish step needs besides the
+// caller's arguments (the capacities the pass was launched with, its summary
+// area and the event after its last kernel)
+struct G2GTicket {
+  int used;
+  cudaEvent_t ev;       // recorded after k_g2g_summary
+  int passes;
+  int64_t n_faces, e_cap, nl_cap, row_cap, link_cap, lat_row_cap, lat_unit_cap, lat_ihit_cap;
+  bool packed, host_forest, deferred;
+  uint32_t* d_rows;
+  float* d_qp;
+  double reach_pred;
+  int64_t* area;        // pinned summary words (host view)
+};
+constexpr int G2G_TICKETS = 8;
+constexpr int G2G_AREA = 512;  // int64 words per summary area
+
+// enqueue the whole pass; no host round trip
+int g2g_submit(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces, int64_t geom_key,
                ow_forest* f, const ow_grid* grid, const ow_g2g_params* p, int32_t* d_bin_ids,
                int64_t bin_ids_capacity, int32_t* d_bin_counts, int32_t* d_bin_offsets, ow_g2g_result* out,
-               cudaStream_t s) {
+               cudaStream_t s, G2GTicket* t) {
   const int D = f->dim, C = D == 3 ? 64 : 16, Q = p->lattice_q;
   const int passes = p->nw.n_levels - 1;
+  static_assert(SUM_W * OW_MAX_PASSES + 1 + G2G_WORDS <= G2G_AREA, "summary area");
   // capacities of this pass
   const int64_t e_cap = ctx->dev_e_cap < bin_ids_capacity ? ctx->dev_e_cap : bin_ids_capacity;
   int64_t nl_cap = f->capacity;
@@ -821,6 +841,18 @@ int g2g_device(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n
     }
   }
   if (e_cap < 1 || nl_cap < 1 || row_cap < 1) return G2G_RETRY;
+  if (!t->ev) OW_CUDA(cudaEventCreateWithFlags(&t->ev, cudaEventDisableTiming));
+  t->passes = passes;
+  t->n_faces = n_faces;
+  t->e_cap = e_cap;
+  t->nl_cap = nl_cap;
+  t->row_cap = row_cap;
+  t->link_cap = link_cap;
+  t->packed = packed;
+  t->host_forest = host_forest;
+  t->deferred = deferred;
+  t->d_rows = d_rows;
+  t->d_qp = d_qp;
   // ---- the pass, enqueued without a host round trip
   if (p->copy_done) OW_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)p->copy_done, 0));
   if (d_records) OW_TRY(ow_stl_binary_to_soa(ctx, d_records, n_faces, d_coords, s));
@@ -828,11 +860,11 @@ int g2g_device(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n
   OW_TRY(ow_forest_init_root(ctx, f, s));
   ow_nearwall_params nw = p->nw;
   nw.reach = predicted_reach(f, &p->nw);
+  t->reach_pred = nw.reach;
   ctx->faces_pending = nullptr;
   ctx->defer_stage_times = true;
   ctx->no_stage_events = p->no_stage_times != 0;
   ctx->dev_pass = true;
-  const int64_t e_cap_used = e_cap;
   ctx->dev_e_cap = e_cap;  // (read by refine_driver)
   int st = refine_driver(ctx, f, d_coords, n_faces, geom_key, grid, &nw, d_bin_ids, bin_ids_capacity, d_bin_counts,
                          d_bin_offsets, &out->nw, s, true);
@@ -851,44 +883,53 @@ int g2g_device(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n
   st = ow_lattice_dev_count(ctx, f, passes, leaves, d_nl, nl_cap, d_coords, n_faces, p->lattice_dirs, Q, flags, s);
   ctx->lat_mean_extent = 0.0f;
   OW_TRY(st);
+  // (the caps the finish step checks against: the lattice lists as sized now)
+  t->lat_row_cap = ctx->lat_row_cap;
+  t->lat_unit_cap = ctx->lat_unit_cap;
+  t->lat_ihit_cap = ctx->lat_ihit_cap;
   const int64_t ncb_grid = ctx->dev_ncb > 0 ? ctx->dev_ncb : 4 * OW_SMS;
   OW_TRY(ow_lattice_dev_emit(ctx, (int64_t*)p->out_buf[OW_OUT_CELLS], (float*)p->out_buf[OW_OUT_Q], row_cap, d_rows,
                              d_qp, link_cap, ncb_grid, s));
-  // ---- the one readback: k_g2g_summary stores into pinned host memory
-  const int n_sum = SUM_W * passes + 1;
-  static_assert(128 + SUM_W * OW_MAX_PASSES + 1 + G2G_WORDS <= OW_PINNED_WORDS, "pinned summary area");
-  if (!ctx->h_pinned_dev) OW_CUDA(cudaHostGetDevicePointer((void**)&ctx->h_pinned_dev, ctx->h_pinned, 0));
-  ow_launch(k_g2g_summary, 1, 128, 0, s, (const int64_t*)ctx->d_small, (const int64_t*)d_sum, n_sum,
-            (volatile int64_t*)(ctx->h_pinned_dev + 128));
+  // ---- every count the host needs, stored into this pass's pinned area
+  ow_launch(k_g2g_summary, 1, 128, 0, s, (const int64_t*)ctx->d_small, (const int64_t*)d_sum, SUM_W * passes + 1,
+            (volatile int64_t*)(ctx->g2g_ring_dev + (t->area - ctx->g2g_ring)));
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
-  OW_CUDA(cudaStreamSynchronize(s));
-  int64_t h[SUM_W * OW_MAX_PASSES + 1], t[G2G_WORDS];
-  memcpy(h, ctx->h_pinned + 128, 8 * (size_t)n_sum);
-  memcpy(t, ctx->h_pinned + 128 + n_sum, sizeof(t));
+  OW_CUDA(cudaEventRecord(t->ev, s));
+  return OW_OK;
+}
+
+// wait for the pass's summary, check it in the reference's error order, and
+// stream the host copies; G2G_RETRY: re-run on the synchronous path
+int g2g_finish(ow_ctx* ctx, ow_forest* f, const ow_g2g_params* p, ow_g2g_result* out, cudaStream_t s,
+               G2GTicket* t) {
+  const int D = f->dim, Q = p->lattice_q, passes = t->passes;
+  const int n_sum = SUM_W * passes + 1;
+  OW_CUDA(cudaEventSynchronize(t->ev));
+  int64_t h[SUM_W * OW_MAX_PASSES + 1], w[G2G_WORDS];
+  memcpy(h, t->area, 8 * (size_t)n_sum);
+  memcpy(w, t->area + n_sum, sizeof(w));
   // faces first (the reference's import order), then bins, driver, lattice
   ow_nearwall_params nw_true = p->nw;
-  FacesState fs_state{out, f, &nw_true, n_faces};
+  FacesState fs_state{out, f, &nw_true, t->n_faces};
   ctx->faces_state = &fs_state;
   ctx->faces_pending = ctx->d_small + 56;
-  st = ow_faces_settle(ctx, t + 28, s);
+  int st = ow_faces_settle(ctx, w + 28, s);
   ctx->faces_state = nullptr;
   ctx->faces_pending = nullptr;
-  ctx->defer_stage_times = false;
-  ctx->no_stage_events = false;
   if (st != OW_OK) return st;
-  if (t[1] >= 0) {
-    ow_set_error("face sample outside binning domain (face %lld)", (long long)t[1]);
+  if (w[1] >= 0) {
+    ow_set_error("face sample outside binning domain (face %lld)", (long long)w[1]);
     return OW_ERR_INVALID;
   }
-  if (t[2]) {
+  if (w[2]) {
     ow_set_error("fill_bins: a face sample escaped its padded bin range (internal)");
     return OW_ERR_INTERNAL;
   }
-  const int64_t E = t[5];
+  const int64_t E = w[5];
   ctx->dev_mean_extent = out->faces.mean_extent;
-  if (E > e_cap_used) ctx->dev_e_cap = E + E / 4 + 1024;
-  if (t[0] > 0 || E > e_cap_used || E > p->nw.overlap_factor * n_faces || nw_true.reach != nw.reach)
+  if (E > t->e_cap && ctx->dev_e_cap < E + E / 4 + 1024) ctx->dev_e_cap = E + E / 4 + 1024;
+  if (w[0] > 0 || E > t->e_cap || E > p->nw.overlap_factor * t->n_faces || nw_true.reach != t->reach_pred)
     return G2G_RETRY;  // slow bin faces, short pair buffers, a capacity error or another reach
   st = drv_apply(ctx, f, h, passes, &out->nw);
   if (st == DRV_RETRY) return G2G_RETRY;
@@ -900,15 +941,15 @@ int g2g_device(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n
   for (int l = 0; l < passes; ++l)
     if (out->nw.n_split[l] > 0) finest = l + 1;
   const int64_t nl = h[SUM_W * passes];
-  if (finest != passes || nl > nl_cap) return G2G_RETRY;
-  const int64_t* L = t + 8;  // d_small[33 + i]
+  if (finest != passes || nl > t->nl_cap) return G2G_RETRY;
+  const int64_t* L = w + 8;  // d_small[33 + i]
   const int64_t n_cb = L[0], nb = L[2], n_links = L[18];
   const int64_t n_rows = (int64_t)((uint64_t)L[15] & ((1ull << 28) - 1)), n_units = (int64_t)((uint64_t)L[15] >> 28);
-  if (n_rows > ctx->lat_row_cap || n_units > ctx->lat_unit_cap || L[16] > ctx->lat_ihit_cap) {
+  if (n_rows > t->lat_row_cap || n_units > t->lat_unit_cap || L[16] > t->lat_ihit_cap) {
     // the sync path grows the row / hit lists (and re-runs the sweep)
     return G2G_RETRY;
   }
-  if (nb > row_cap || n_links > link_cap) return G2G_RETRY;
+  if (nb > t->row_cap || n_links > t->link_cap) return G2G_RETRY;
   // ---- results
   out->finest_level = finest;
   out->n_finest_leaves = nl;
@@ -923,22 +964,21 @@ int g2g_device(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n
   out->lattice_stats[0] = n_cb;
   out->lattice_stats[1] = ctx->lat_rows;
   out->lattice_stats[2] = ctx->lat_units;
-  // host copies (the pass is complete on `s`): on the copy stream for a
-  // deferred caller, else on `s`
+  // host copies: on the copy stream after this pass's last kernel for a
+  // deferred caller (later passes may already be queued on `s`), else on `s`
   const int64_t nbk = f->n_blocks;
-  const bool fc = host_forest && p->host_block_cap >= nbk;
-  const bool rows_fit = packed && nb > 0;
-  if (fc || rows_fit || (!packed && p->host_cells && p->host_q && p->host_row_cap >= nb && nb > 0)) {
+  const bool fc = t->host_forest && p->host_block_cap >= nbk;
+  const bool rows_fit = t->packed && nb > 0;
+  if (fc || rows_fit || (!t->packed && p->host_cells && p->host_q && p->host_row_cap >= nb && nb > 0)) {
     cudaStream_t cs = s;
-    if (deferred) {
+    if (t->deferred) {
       if (!ctx->copy_stream) {
         OW_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         OW_CUDA(cudaEventCreateWithFlags(&ctx->copy_ev[0], cudaEventDisableTiming));
         OW_CUDA(cudaEventCreateWithFlags(&ctx->copy_ev[1], cudaEventDisableTiming));
       }
       cs = ctx->copy_stream;
-      OW_CUDA(cudaEventRecord(ctx->copy_ev[0], s));
-      OW_CUDA(cudaStreamWaitEvent(cs, ctx->copy_ev[0], 0));
+      OW_CUDA(cudaStreamWaitEvent(cs, t->ev, 0));
     }
     if (fc) {
       OW_CUDA(cudaMemcpyAsync(p->host_level, f->d_level, 2 * (size_t)nbk, cudaMemcpyDeviceToHost, cs));
@@ -950,18 +990,48 @@ int g2g_device(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n
       out->host_copied |= 1;
     }
     if (rows_fit) {
-      OW_CUDA(cudaMemcpyAsync(p->host_rows, d_rows, 8 * (size_t)nb, cudaMemcpyDeviceToHost, cs));
-      OW_CUDA(cudaMemcpyAsync(p->host_q_packed, d_qp, 4 * (size_t)n_links, cudaMemcpyDeviceToHost, cs));
-      out->host_copied |= deferred ? 4 | 8 : 4;
-    } else if (!packed && p->host_cells && p->host_q && p->host_row_cap >= nb && nb > 0) {
+      OW_CUDA(cudaMemcpyAsync(p->host_rows, t->d_rows, 8 * (size_t)nb, cudaMemcpyDeviceToHost, cs));
+      OW_CUDA(cudaMemcpyAsync(p->host_q_packed, t->d_qp, 4 * (size_t)n_links, cudaMemcpyDeviceToHost, cs));
+      out->host_copied |= t->deferred ? 4 | 8 : 4;
+    } else if (!t->packed && p->host_cells && p->host_q && p->host_row_cap >= nb && nb > 0) {
       OW_CUDA(cudaMemcpyAsync(p->host_cells, p->out_buf[OW_OUT_CELLS], 8 * (size_t)nb, cudaMemcpyDeviceToHost, cs));
       OW_CUDA(cudaMemcpyAsync(p->host_q, p->out_buf[OW_OUT_Q], 4 * (size_t)nb * Q, cudaMemcpyDeviceToHost, cs));
       out->host_copied |= 2;
     }
-    if (deferred) OW_CUDA(cudaEventRecord((cudaEvent_t)p->copy_done, cs));
+    if (t->deferred) OW_CUDA(cudaEventRecord((cudaEvent_t)p->copy_done, cs));
   }
-  if (p->copy_done && !deferred) OW_CUDA(cudaEventRecord((cudaEvent_t)p->copy_done, s));
+  if (p->copy_done && !t->deferred) OW_CUDA(cudaEventRecord((cudaEvent_t)p->copy_done, s));
   return ow_stage_times(ctx, &out->nw);
+}
+
+int ticket_get(ow_ctx* ctx, G2GTicket** out) {
+  if (!ctx->g2g_tickets) {
+    ctx->g2g_tickets = calloc(G2G_TICKETS, sizeof(G2GTicket));
+    if (!ctx->g2g_tickets) {
+      ow_set_error("geometry_to_grid: out of host memory");
+      return OW_ERR_INTERNAL;
+    }
+    OW_CUDA(cudaHostAlloc((void**)&ctx->g2g_ring, 8 * (size_t)G2G_AREA * G2G_TICKETS, cudaHostAllocMapped));
+    OW_CUDA(cudaHostGetDevicePointer((void**)&ctx->g2g_ring_dev, ctx->g2g_ring, 0));
+  }
+  G2GTicket* T = (G2GTicket*)ctx->g2g_tickets;
+  for (int i = 0; i < G2G_TICKETS; ++i)
+    if (!T[i].used) {
+      T[i].used = 1;
+      T[i].area = ctx->g2g_ring + (size_t)G2G_AREA * i;
+      *out = &T[i];
+      return OW_OK;
+    }
+  ow_set_error("geometry_to_grid: more than %d passes in flight on one context", G2G_TICKETS);
+  return OW_ERR_INVALID;
+}
+
+void g2g_reset_state(ow_ctx* ctx) {
+  ctx->dev_pass = false;
+  ctx->faces_pending = nullptr;
+  ctx->faces_state = nullptr;
+  ctx->defer_stage_times = false;
+  ctx->no_stage_events = false;
 }
 
 bool g2g_device_eligible(const ow_ctx* ctx, const ow_forest* f, const ow_g2g_params* p) {
@@ -979,6 +1049,19 @@ bool g2g_device_eligible(const ow_ctx* ctx, const ow_forest* f, const ow_g2g_par
 }
 }  // namespace
 
+// (ow_ctx_destroy) the in-flight table and the pinned summary areas
+void ow_g2g_release(ow_ctx* ctx) {
+  if (ctx->g2g_tickets) {
+    G2GTicket* T = (G2GTicket*)ctx->g2g_tickets;
+    for (int i = 0; i < G2G_TICKETS; ++i)
+      if (T[i].ev) cudaEventDestroy(T[i].ev);
+    free(ctx->g2g_tickets);
+    ctx->g2g_tickets = nullptr;
+  }
+  if (ctx->g2g_ring) cudaFreeHost(ctx->g2g_ring);
+  ctx->g2g_ring = ctx->g2g_ring_dev = nullptr;
+}
+
 extern "C" int ow_set_device_pass(ow_ctx* ctx, int32_t enable) {
   ctx->dev_disabled = enable ? 0 : 1;
   return OW_OK;
@@ -990,32 +1073,15 @@ extern "C" int ow_device_pass_stats(ow_ctx* ctx, int64_t* out2) {
   return OW_OK;
 }
 
-extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces,
-                                   int64_t geom_key, ow_forest* f, const ow_grid* grid, const ow_g2g_params* p,
-                                   int32_t* d_bin_ids, int64_t bin_ids_capacity, int32_t* d_bin_counts,
-                                   int32_t* d_bin_offsets, ow_g2g_result* out, void* stream) {
-  bool fell_back = false;
-  if (n_faces > 0 && g2g_device_eligible(ctx, f, p)) {
-    memset(out, 0, sizeof(*out));
-    out->faces.first_degenerate = out->faces.first_nonfinite = -1;
-    const int st = g2g_device(ctx, d_records, d_coords, n_faces, geom_key, f, grid, p, d_bin_ids, bin_ids_capacity,
-                              d_bin_counts, d_bin_offsets, out, (cudaStream_t)stream);
-    ctx->dev_pass = false;
-    ctx->faces_pending = nullptr;
-    ctx->faces_state = nullptr;
-    ctx->defer_stage_times = false;
-    ctx->no_stage_events = false;
-    if (st != G2G_RETRY) {
-      if (st == OW_OK) {
-        ctx->dev_passes++;
-        out->device_sized = 1;
-      }
-      return st;
-    }
+namespace {
+// the synchronous pass, after a device-sized attempt (fell_back) or instead of one
+int g2g_sync_learn(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces, int64_t geom_key,
+                   ow_forest* f, const ow_grid* grid, const ow_g2g_params* p, int32_t* d_bin_ids,
+                   int64_t bin_ids_capacity, int32_t* d_bin_counts, int32_t* d_bin_offsets, ow_g2g_result* out,
+                   void* stream, bool fell_back) {
+  if (fell_back) {
     ctx->dev_fallbacks++;
-    fell_back = true;
-    // (records already converted: the synchronous pass starts from the coordinates)
-    d_records = nullptr;
+    d_records = nullptr;  // (records already converted: the synchronous pass starts from the coordinates)
   }
   const int st = g2g_sync(ctx, d_records, d_coords, n_faces, geom_key, f, grid, p, d_bin_ids, bin_ids_capacity,
                           d_bin_counts, d_bin_offsets, out, stream);
@@ -1028,4 +1094,76 @@ extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float*
     out->device_sized = fell_back ? 2 : 0;
   }
   return st;
+}
+
+void g2g_out_init(ow_g2g_result* out) {
+  memset(out, 0, sizeof(*out));
+  out->faces.first_degenerate = out->faces.first_nonfinite = -1;
+}
+}  // namespace
+
+// Submit a pass without waiting for it (device-sized when eligible and no
+// stage events are requested): *ticket > 0 identifies the pass in flight and
+// ow_geometry_to_grid_finish completes it; *ticket = 0: the pass ran
+// synchronously and `out` is final.  Between submit and finish the caller
+// keeps every argument alive and unchanged and may submit passes of other
+// plans (other forests, parameters and outputs) on the same stream.
+extern "C" int ow_geometry_to_grid_submit(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces,
+                                          int64_t geom_key, ow_forest* f, const ow_grid* grid, const ow_g2g_params* p,
+                                          int32_t* d_bin_ids, int64_t bin_ids_capacity, int32_t* d_bin_counts,
+                                          int32_t* d_bin_offsets, ow_g2g_result* out, void* stream, int64_t* ticket) {
+  *ticket = 0;
+  g2g_out_init(out);
+  bool fell_back = false;
+  if (n_faces > 0 && g2g_device_eligible(ctx, f, p)) {
+    G2GTicket* t;
+    OW_TRY(ticket_get(ctx, &t));
+    const int st = g2g_submit(ctx, d_records, d_coords, n_faces, geom_key, f, grid, p, d_bin_ids, bin_ids_capacity,
+                              d_bin_counts, d_bin_offsets, out, (cudaStream_t)stream, t);
+    g2g_reset_state(ctx);
+    if (st == OW_OK) {
+      *ticket = 1 + (t - (G2GTicket*)ctx->g2g_tickets);
+      return OW_OK;
+    }
+    t->used = 0;
+    if (st != G2G_RETRY) return st;
+    fell_back = true;
+  }
+  return g2g_sync_learn(ctx, d_records, d_coords, n_faces, geom_key, f, grid, p, d_bin_ids, bin_ids_capacity,
+                        d_bin_counts, d_bin_offsets, out, stream, fell_back);
+}
+
+extern "C" int ow_geometry_to_grid_finish(ow_ctx* ctx, int64_t ticket, float* d_coords, int64_t n_faces,
+                                          int64_t geom_key, ow_forest* f, const ow_grid* grid, const ow_g2g_params* p,
+                                          int32_t* d_bin_ids, int64_t bin_ids_capacity, int32_t* d_bin_counts,
+                                          int32_t* d_bin_offsets, ow_g2g_result* out, void* stream) {
+  if (ticket <= 0) return OW_OK;  // (completed by the submit)
+  if (ticket > G2G_TICKETS || !ctx->g2g_tickets || !((G2GTicket*)ctx->g2g_tickets)[ticket - 1].used) {
+    ow_set_error("geometry_to_grid: unknown pass ticket %lld", (long long)ticket);
+    return OW_ERR_INVALID;
+  }
+  G2GTicket* t = (G2GTicket*)ctx->g2g_tickets + (ticket - 1);
+  const int st = g2g_finish(ctx, f, p, out, (cudaStream_t)stream, t);
+  t->used = 0;
+  g2g_reset_state(ctx);
+  if (st == OW_OK) {
+    ctx->dev_passes++;
+    out->device_sized = 1;
+    return OW_OK;
+  }
+  if (st != G2G_RETRY) return st;
+  g2g_out_init(out);
+  return g2g_sync_learn(ctx, nullptr, d_coords, n_faces, geom_key, f, grid, p, d_bin_ids, bin_ids_capacity,
+                        d_bin_counts, d_bin_offsets, out, stream, true);
+}
+
+extern "C" int ow_geometry_to_grid(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_faces,
+                                   int64_t geom_key, ow_forest* f, const ow_grid* grid, const ow_g2g_params* p,
+                                   int32_t* d_bin_ids, int64_t bin_ids_capacity, int32_t* d_bin_counts,
+                                   int32_t* d_bin_offsets, ow_g2g_result* out, void* stream) {
+  int64_t ticket = 0;
+  OW_TRY(ow_geometry_to_grid_submit(ctx, d_records, d_coords, n_faces, geom_key, f, grid, p, d_bin_ids,
+                                    bin_ids_capacity, d_bin_counts, d_bin_offsets, out, stream, &ticket));
+  return ow_geometry_to_grid_finish(ctx, ticket, d_coords, n_faces, geom_key, f, grid, p, d_bin_ids,
+                                    bin_ids_capacity, d_bin_counts, d_bin_offsets, out, stream);
 }

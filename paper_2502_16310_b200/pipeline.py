@@ -62,6 +62,52 @@ class GridPass:
         return unpack_q(h["flags"].numpy().view(np.uint32), h["q_packed"].numpy(), self.links.q.shape[1])
 
 
+class PendingGridPass:
+    """A submitted pass (``GridPlan.run_async``); ``result()`` waits for it
+    and returns its ``GridPass`` (the same object on every call; errors of
+    the pass are raised there)."""
+
+    def __init__(self, plan, state):
+        self._plan = plan
+        self._state = state
+        self._ticket = 0
+        self._gp = None
+        self._err = None
+
+    def result(self) -> GridPass:
+        if self._gp is None and self._err is None:
+            plan = self._plan
+            if plan._pending is self:
+                plan._pending = None
+            try:
+                self._gp = plan._finish(self._state, self._ticket)
+            except Exception as e:
+                self._err = e
+            self._state = None
+        if self._err is not None:
+            raise self._err
+        return self._gp
+
+
+class _outside_message:
+    """Re-raise the native 'outside the forest domain' error with the
+    geometry's extent (the reference's message)."""
+
+    def __init__(self, out, dim):
+        self.out, self.dim = out, dim
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, et, ev, tb):
+        if et is InvalidParameterError and self.out.outside_domain:
+            lo = np.array(self.out.faces.bbox_min[: self.dim], np.float32).astype(np.float64)
+            hi = np.array(self.out.faces.bbox_max[: self.dim], np.float32).astype(np.float64)
+            raise InvalidParameterError(
+                f"geometry spans {lo.tolist()}..{hi.tolist()}, outside the forest domain") from None
+        return False
+
+
 def unpack_q(row_flags: np.ndarray, q_packed: np.ndarray, nq: int) -> np.ndarray:
     """Packed boundary rows -> dense q: row r's set bits of ``row_flags[r]``, in
     ascending direction order, take the next entries of ``q_packed``."""
@@ -123,6 +169,7 @@ class GridPlan:
         self._setup = None  # (n_faces, _driver_setup result): the parts that depend on n_faces only
         self._gp0 = _lib.G2GParamsC()  # static fields of the call's parameter struct
         self._done = None  # torch.cuda.Event: the last pass's deferred host copies
+        self._pending = None  # the plan's submitted, unfinished pass (run_async)
         self._dev_rows = self._dev_qp = None  # device staging of the packed rows (deferred passes)
         if self.dirs is not None:
             self._gp0.lattice_q = len(self.dirs)
@@ -152,6 +199,12 @@ class GridPlan:
 
     def run(self, records: torch.Tensor | None = None, n_faces: int | None = None,
             geometry: CoordListGeometry | None = None, host: bool = False, defer: bool = False) -> GridPass:
+        """One pass, returned complete: ``run_async(...).result()``."""
+        return self.run_async(records, n_faces, geometry, host, defer).result()
+
+    def run_async(self, records: torch.Tensor | None = None, n_faces: int | None = None,
+                  geometry: CoordListGeometry | None = None, host: bool = False,
+                  defer: bool = False) -> "PendingGridPass":
         """Binary STL records (device uint8, 50 bytes per face, after the
         84-byte header) — or an existing ``geometry`` — to a refined forest and
         its finest-level lattice links.
@@ -169,7 +222,18 @@ class GridPlan:
         them, so they overlap whatever is enqueued next (another plan's pass:
         alternate two plans to stream geometries); ``GridPass.wait()`` blocks
         until they are done.  The plan's next pass waits for them on the
-        device before it rewrites its outputs."""
+        device before it rewrites its outputs.
+
+        ``run_async`` submits the pass and returns a ``PendingGridPass``
+        without waiting for the device (when the pass can run device-sized:
+        from a plan's second pass on, without stage-timing events);
+        ``.result()`` waits for it and returns the ``GridPass``.  Passes of
+        other plans may be submitted in between, so a stream of geometries
+        through two alternating plans keeps the GPU fed while the host
+        finishes the previous pass.  A plan's pending pass is finished before
+        its next one is submitted."""
+        if self._pending is not None:
+            self._pending.result()
         if geometry is None and records is None:
             raise InvalidParameterError("geometry_to_grid needs STL records or a geometry")
         dim = self.dim
@@ -264,20 +328,36 @@ class GridPlan:
         out = _lib.G2GResultC()
         g, bins_t = st["g"], st["bins_t"]
         v = forest.view()
-        try:
-            _lib.call("ow_geometry_to_grid", _lib.ctx(), _lib.ptr(records) if geometry is None else None,
-                      _lib.ptr(coords), nf, next(_geom_keys), C.byref(v), C.byref(g) if g is not None else None,
-                      C.byref(gp), _lib.ptr(bins_t[0]) if bins_t else None, st["cap"],
-                      _lib.ptr(bins_t[1]) if bins_t else None, _lib.ptr(bins_t[2]) if bins_t else None,
-                      C.byref(out), _lib.stream())
-        except InvalidParameterError:
-            if out.outside_domain:
-                lo = np.array(out.faces.bbox_min[:dim], np.float32).astype(np.float64)
-                hi = np.array(out.faces.bbox_max[:dim], np.float32).astype(np.float64)
-                raise InvalidParameterError(
-                    f"geometry spans {lo.tolist()}..{hi.tolist()}, outside the forest domain") from None
-            raise
-        finally:
+        args = (_lib.ptr(coords), nf, next(_geom_keys), C.byref(v), C.byref(g) if g is not None else None,
+                C.byref(gp), _lib.ptr(bins_t[0]) if bins_t else None, st["cap"],
+                _lib.ptr(bins_t[1]) if bins_t else None, _lib.ptr(bins_t[2]) if bins_t else None,
+                C.byref(out), _lib.stream())
+        ticket = C.c_int64(0)
+        pending = PendingGridPass(self, (forest, v, out, st, gp, g, bins_t, coords, geometry, hbuf, host, args))
+        with _outside_message(out, dim):
+            try:
+                _lib.call("ow_geometry_to_grid_submit", _lib.ctx(), _lib.ptr(records) if geometry is None else None,
+                          *args, C.byref(ticket))
+            except Exception:
+                _driver_done(forest, out.nw)
+                raise
+        pending._ticket = int(ticket.value)
+        if pending._ticket == 0 or self.stage_times:  # (stage events live in the context: finish now)
+            pending.result()
+        else:
+            self._pending = pending
+        return pending
+
+    def _finish(self, state, ticket):
+        forest, v, out, st, gp, g, bins_t, coords, geometry, hbuf, host, args = state
+        dim = self.dim
+        if ticket:
+            with _outside_message(out, dim):
+                try:
+                    _lib.call("ow_geometry_to_grid_finish", _lib.ctx(), ticket, *args)
+                finally:
+                    _driver_done(forest, out.nw)
+        else:
             _driver_done(forest, out.nw)
         geom = geometry if geometry is not None else CoordListGeometry._validated(dim, coords, out.faces)
         result = _driver_result(forest, self.params, st, out.nw)

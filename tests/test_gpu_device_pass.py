@@ -176,3 +176,45 @@ def test_device_pass_errors_match_sync(ow):
     gp = plan.run(rec, n)  # and the plan recovers
     torch.cuda.synchronize()
     assert gp.device_sized == 1
+
+
+def test_run_async_two_plans_stream(ow):
+    """run_async: two plans alternate over a stream of geometries with the
+    next pass submitted before the previous one is finished (the e2e bench's
+    pipeline); every pass's device arrays and host copies equal a fresh
+    synchronous pass's, including a pass that outgrows its plan's estimates
+    (finished on the synchronous path after the next pass was submitted)."""
+    import torch
+
+    from paper_2502_16310_b200 import pipeline, shapes
+
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8)
+    geoms = [shapes.icosphere_triangles(s, radius=r) for s, r in
+             ((3, 0.3), (3, 0.3), (3, 0.25), (3, 0.3), (3, 0.3), (4, 0.32), (3, 0.3), (4, 0.32), (3, 0.3))]
+    recs = [_records(t) for t in geoms]
+    refs = []
+    for rec, n in recs:
+        r = pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19").run(rec, n, host=True)
+        torch.cuda.synchronize()
+        refs.append((_snapshot(r), {k: (v.clone() if isinstance(v, torch.Tensor) else [c.clone() for c in v])
+                                    for k, v in r.host.items()}))
+    plans = [pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19", reuse_outputs=True, stage_times=False)
+             for _ in range(2)]
+    prev, modes = None, []
+    for k, (rec, n) in enumerate(recs):
+        pend = plans[k % 2].run_async(rec, n, host=True, defer=True)
+        if prev is not None:
+            j, p = prev
+            g = p.result()
+            g.wait()
+            modes.append(g.device_sized)
+            _equal(_snapshot(g), refs[j][0], f"pass {j}")
+            for key in ("level", "parent", "first_child", "marks", "cells", "flags", "q_packed"):
+                assert torch.equal(g.host[key], refs[j][1][key]), (j, key)
+        prev = (k, pend)
+    j, p = prev
+    g = p.result()
+    g.wait()
+    _equal(_snapshot(g), refs[j][0], f"pass {j}")
+    assert 1 in modes and 2 in modes
