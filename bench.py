@@ -261,11 +261,17 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     plan = pipeline.GridPlan(dom, (cfg["root"],) * dim, params, cfg["lattice"], reuse_outputs=True, comm=comm,
                              stage_times=False)
 
-    def step(records):
+    def submit(records):
         # fused native pass: STL records (C1: the resident text-primitive
-        # geometry) -> grid -> lattice links (ow_geometry_to_grid)
-        gp = plan.run(geometry=geom_dev) if text else plan.run(records, n_faces)
+        # geometry) -> grid -> lattice links (ow_geometry_to_grid_submit)
+        return plan.run_async(geometry=geom_dev) if text else plan.run_async(records, n_faces)
+
+    def done(pend):
+        gp = pend.result()  # (the host's checks and results: ow_geometry_to_grid_finish)
         return gp.result, gp.forest, gp.links
+
+    def step(records):
+        return done(submit(records))
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
@@ -285,7 +291,8 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     n_boundary = ll.n_boundary
 
     # ---- value: inputs resident in HBM
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
+    fallback_steps = []
     gc.collect()
     gc.disable()  # no collector pauses inside the timed regions (re-enabled after e2e)
     launches0 = _lib.launches()
@@ -294,12 +301,16 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         for k in range(args.steps):
             l2_flush()
             ev[k][0].record()
-            res, forest, ll = step(rec_dev if not text else None)
-            ev[k][1].record()
+            pend = submit(rec_dev if not text else None)
+            ev[k][1].record()  # after the submitted pass's last kernel
+            res, forest, ll = done(pend)
+            ev[k][2].record()  # (a pass that fell back to the synchronous path is timed to here)
+            if pend.result().device_sized == 2:
+                fallback_steps.append(k)
         barrier()
     launches = _lib.launches() - launches0
     lat_stats = _lib.lattice_stats()
-    ms = sum(a.elapsed_time(b) for a, b in ev)
+    ms = sum(e0.elapsed_time(e2 if k in fallback_steps else e1) for k, (e0, e1, e2) in enumerate(ev))
     # per-kernel-family device times (roofline): the same steps again with the
     # library's CUDA-event brackets on, outside the timed loop above
     _lib.profile(True)
@@ -463,6 +474,10 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         "data": "synthetic (procedural geometry, deterministic)",
         # (main() sets "config" to bench_config(): the same object as the reference arm's)
         "run": {"cell_face_tests_per_step": T_step, "pairs_evaluated_per_step": evaluated,
+                "value_timing": ("per pass: CUDA events before the submit and after its last kernel "
+                                 "(GridPlan.run_async); the host's finish step runs after; a pass that fell "
+                                 "back to the synchronous path is timed through its finish"),
+                "fallback_steps": fallback_steps,
                 "blocks_per_level": blocks, "boundary_cells": n_boundary,
                 "parallelism": (f"octree-block shards x{world}: work-balanced marking slices and finest-leaf "
                                 f"lattice slices per rank, marks / statistics / flag words / q rows exchanged "
