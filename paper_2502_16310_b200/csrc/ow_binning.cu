@@ -530,6 +530,27 @@ int fill_emit(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, int32_t* i
   return OW_OK;
 }
 
+// offsets of the device-sized fill_bins: when the entry count outgrew the
+// pair buffers (e_cap) the bins are emptied instead (counts and offsets 0), so
+// nothing downstream indexes entries that were never written; the host sees
+// the count after the pass and re-runs it with room
+struct GuardLoad {
+  const int32_t* counts;
+  const int64_t* d_e;
+  int64_t cap;
+  __device__ int64_t operator()(int64_t i) const { return *d_e <= cap ? (int64_t)counts[i] : 0; }
+};
+struct GuardStore {
+  int32_t* offsets;
+  int32_t* counts;
+  const int64_t* d_e;
+  int64_t cap;
+  __device__ void operator()(int64_t i, int64_t e, int64_t) const {
+    offsets[i] = (int32_t)e;
+    if (*d_e > cap) counts[i] = 0;
+  }
+};
+
 // Device-sized fill_bins (fused pass, ow_pipeline.cu): count, face offsets,
 // emission and the stable sort with the entry count left on the device
 // (small[5]); e_cap bounds the pair buffers and sizes the sort's grid.  The
@@ -577,7 +598,8 @@ int fill_dev(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, in
     ow_set_error("fill_bins: sort ended outside the id buffer (internal)");
     return OW_ERR_INTERNAL;
   }
-  OW_TRY(scan(ctx, ow::LoadArr<int32_t>{counts}, ow::StoreExcl<int32_t>{offsets}, n_bins, nullptr, s));
+  OW_TRY(scan(ctx, GuardLoad{counts, small + 5, e_cap}, GuardStore{offsets, counts, small + 5, e_cap}, n_bins, nullptr,
+              s));
   ctx->bins_faces = n;
   ctx->bins_entries = -1;  // (on the device)
   ctx->bins_slow = 0;

@@ -1278,7 +1278,7 @@ int lat_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_l
               const ow_grid* grid, const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags, int64_t* out_boundary,
               cudaStream_t stream, const int64_t* d_nl) {
   (void)geom_key;
-  if (pos_lo < 0 || (pos_hi > n_leaves && !d_nl) || pos_lo > pos_hi) {
+  if (pos_lo < 0 || pos_hi > n_leaves || pos_lo > pos_hi) {
     ow_set_error("lattice: leaf range [%lld, %lld) outside [0, %lld)", (long long)pos_lo, (long long)pos_hi,
                  (long long)n_leaves);
     return OW_ERR_INVALID;
@@ -1461,8 +1461,10 @@ int ow_lattice_dev_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const i
                          int64_t nl_cap, const float* d_coords, int64_t n_faces, const int8_t* h_dirs, int32_t n_dirs,
                          uint32_t* d_flags, cudaStream_t s) {
   int64_t nb = 0;
-  return lat_count(ctx, f, level, d_leaves, nl_cap, 0, INT64_MAX, d_coords, n_faces, -1, nullptr, h_dirs, n_dirs,
-                   d_flags, &nb, s, d_nl);
+  // (positions >= nl_cap are rejected by the face pass: a stale leaf position
+  // of an earlier pass can then never index past this pass's buffers)
+  return lat_count(ctx, f, level, d_leaves, nl_cap, 0, nl_cap, d_coords, n_faces, -1, nullptr, h_dirs, n_dirs, d_flags,
+                   &nb, s, d_nl);
 }
 
 // ... then emit with the candidate-block count on the device: persistent grids

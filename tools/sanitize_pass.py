@@ -30,4 +30,25 @@ plan = pipeline.GridPlan(ow.Aabb(np.zeros(3), np.ones(3)), (8, 8, 8),
 for _ in range(2):
     gp = plan.run(rec, n, host=True)
 torch.cuda.synchronize()
-print("sanitize pass OK:", f.blocks_per_level(), ll.n_boundary, gp.forest.blocks_per_level(), gp.links.n_boundary)
+# device-sized passes (single readback, graph capture and replay) through two
+# plans with the next pass submitted before the previous one is finished, a
+# pass that outgrows the estimates (synchronous fallback) and deferred copies
+plans = [pipeline.GridPlan(ow.Aabb(np.zeros(3), np.ones(3)), (8, 8, 8),
+                           ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8), "D3Q19", reuse_outputs=True,
+                           stage_times=False) for _ in range(2)]
+big = shapes.binary_stl_bytes(shapes.icosphere_triangles(4, radius=0.32))
+recs = [(rec, n)] * 4 + [(torch.frombuffer(bytearray(big[84:]), dtype=torch.uint8).cuda(),
+                          int.from_bytes(big[80:84], "little"))] * 2 + [(rec, n)] * 2
+prev, modes = None, []
+for k, (r, nn) in enumerate(recs):
+    pend = plans[k % 2].run_async(r, nn, host=True, defer=True)
+    if prev is not None:
+        g = prev.result()
+        g.wait()
+        modes.append(g.device_sized)
+    prev = pend
+g = prev.result()
+g.wait()
+torch.cuda.synchronize()
+print("sanitize pass OK:", f.blocks_per_level(), ll.n_boundary, gp.forest.blocks_per_level(), gp.links.n_boundary,
+      "device-sized modes", modes + [g.device_sized])
