@@ -382,7 +382,7 @@ int ow_lattice_links_n_links(ow_ctx* ctx, int64_t* out);
 /* Tuning / testing knobs of the lattice sweep (results never depend on them):
  * rows of more than `inline_units` cells are tested by the unit-balanced
  * k_lat_mt pass, the others inside the face pass (default 64: all inline);
- * faces_per_warp (4 or 8) fixes the face pass's lane groups (default: chosen
+ * faces_per_warp (1, 2, 4, 8, 16 or 32; 3D) fixes the face pass's lane groups (default: chosen
  * from the mean face size against the finest block).  Negative = default. */
 int ow_lattice_tune(ow_ctx* ctx, int32_t inline_units, int32_t faces_per_warp);
 

@@ -1110,7 +1110,7 @@ int faces_per_warp(const ow_ctx* ctx, int D, int64_t n_faces, int64_t n_leaves) 
     return e ? atoi(e) : 0;
   }();
   if (ctx->lat_fpw) return ctx->lat_fpw;
-  if (env == 4 || env == 8 || env == 16 || env == 32) return env;
+  if (env == 1 || env == 2 || env == 4 || env == 8 || env == 16 || env == 32) return env;
   if (ctx->lat_mean_extent > 0.0f) {  // measured (C2-C5 sweep): 8 wins at 0.17 and 0.28 blocks, 4 at 0.69 and 0.94
     const ow_forest* f = &ctx->lat_forest;
     double q = INFINITY;
@@ -1118,7 +1118,9 @@ int faces_per_warp(const ow_ctx* ctx, int D, int64_t n_faces, int64_t n_leaves) 
     // (C5 sweep: 16 faces per warp 1.75 ms vs 8 1.82 vs 32 1.84 at 0.15 blocks;
     // C2 at 0.6-1 blocks: 4 0.098 ms vs 16 0.164)
     const double r = (double)ctx->lat_mean_extent / q;
-    return r < 0.25 ? 16 : (r < 0.5 ? 8 : 4);
+    // (round 2 sweep, 1/2/4/8/16: C2 0.093 ms at 2 vs 0.098 at 4, C3 0.514 vs 0.528;
+    // C4 0.56 at 8; C5 1.75 at 16 vs 1.82 at 8)
+    return r < 0.25 ? 16 : (r < 0.5 ? 8 : 2);
   }
   return n_faces > 4 * n_leaves ? 8 : 4;
 }
@@ -1367,6 +1369,8 @@ int lat_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_l
     if (fpw == 32) ow_launch(k_lat_faces<3, 32>, lat_face_grid<3, 32>(n_faces), 128, 0, s, A);
     else if (fpw == 16) ow_launch(k_lat_faces<3, 16>, lat_face_grid<3, 16>(n_faces), 128, 0, s, A);
     else if (fpw == 8) ow_launch(k_lat_faces<3, 8>, lat_face_grid<3, 8>(n_faces), 128, 0, s, A);
+    else if (fpw == 2) ow_launch(k_lat_faces<3, 2>, lat_face_grid<3, 2>(n_faces), 128, 0, s, A);
+    else if (fpw == 1) ow_launch(k_lat_faces<3, 1>, lat_face_grid<3, 1>(n_faces), 128, 0, s, A);
     else ow_launch(k_lat_faces<3, 4>, lat_face_grid<3, 4>(n_faces), 128, 0, s, A);
   } else {
     if (fpw == 8) ow_launch(k_lat_faces<2, 8>, lat_face_grid<2, 8>(n_faces), 128, 0, s, A);
@@ -1557,9 +1561,9 @@ extern "C" int ow_lattice_links_emit_packed(ow_ctx* ctx, int64_t* d_cells, float
 // k_lat_mt, the others inside k_lat_faces; faces_per_warp 4 or 8 fixes the
 // face-pass shape.  Negative values restore the defaults.
 extern "C" int ow_lattice_tune(ow_ctx* ctx, int32_t inline_units, int32_t faces_per_warp) {
-  if (faces_per_warp > 0 && faces_per_warp != 4 && faces_per_warp != 8 && faces_per_warp != 16 &&
-      faces_per_warp != 32) {
-    ow_set_error("lattice: faces_per_warp must be 4, 8, 16 or 32, got %d", faces_per_warp);
+  if (faces_per_warp > 0 && faces_per_warp != 1 && faces_per_warp != 2 && faces_per_warp != 4 &&
+      faces_per_warp != 8 && faces_per_warp != 16 && faces_per_warp != 32) {
+    ow_set_error("lattice: faces_per_warp must be 1, 2, 4, 8, 16 or 32, got %d", faces_per_warp);
     return OW_ERR_INVALID;
   }
   ctx->lat_inline_set = inline_units >= 0;

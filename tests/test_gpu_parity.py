@@ -360,7 +360,7 @@ def test_lattice_face_pass_shapes_agree(ow, sub, root, lat):
     fg = ow.init_root_grid(domain(ow, 3), (root,) * 3)
     ow.refine_near_wall(fg, geom, ow.NearWallParams(d_spec=0.05, n_levels=3, bins_per_axis=8))
     out = []
-    for fpw in (-1, 4, 16):
+    for fpw in (-1, 1, 2, 4, 16):
         _lib.call("ow_lattice_tune", _lib.ctx(), -1, fpw)
         try:
             ll = ow.build_lattice_links(fg, geom, None, lat)
