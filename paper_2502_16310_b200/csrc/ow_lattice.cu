@@ -958,6 +958,7 @@ __global__ void k_lat_bcount(LatArgs A) {
   // persistent warps over the candidate blocks (their count is on the device;
   // a grid over every leaf launched ~7x more CTAs than there is work at C5)
   const int64_t ncb = *A.n_cb_d;
+  unsigned long long links_acc = 0;  // (one atomic per warp at the end, not per block)
   for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < ncb;
        r += (int64_t)gridDim.x * (blockDim.x >> 5)) {
   const int64_t pos = A.cand_blocks[r];
@@ -976,9 +977,10 @@ __global__ void k_lat_bcount(LatArgs A) {
     A.bcount[r] = __popcll(m);
     A.hcount[r] = links;
     A.bmask[r] = m;
-    if (links) atomicAdd(A.links_d, (unsigned long long)links);
+    links_acc += (unsigned long long)links;
   }
   }
+  if ((threadIdx.x & 31) == 0 && links_acc) atomicAdd(A.links_d, links_acc);
 }
 
 // boundary rows in (block, cell) order: cells and q rows (-1 where the link

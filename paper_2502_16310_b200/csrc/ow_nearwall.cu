@@ -371,7 +371,8 @@ __device__ __forceinline__ void flush_counts(const MarkArgs& A, MarkCounts& cn, 
 
 template <int D, bool BINNED>
 __device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M, MarkSmem<D>& S, int64_t pos,
-                                           int lane, int wid);
+                                           int lane, int wid, MarkCounts& cn, unsigned long long& t_acc,
+                                           unsigned long long& marked);
 
 // persistent over the level's leaves (the count may live on the device)
 template <int D, bool BINNED, int MINB = 6>
@@ -381,13 +382,24 @@ __global__ void __launch_bounds__(MARK_THREADS, MINB) k_mark_blocks(MarkArgs A, 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t lo = A.d_slice ? A.d_slice[0] : 0;
   const int64_t n = A.d_slice ? A.d_slice[1] : (A.d_n ? *A.d_n : A.n_leaves);
+  // statistics accumulate per warp over its blocks: one atomic per counter
+  // and warp at the end (per block they were same-address atomics from every
+  // warp of the grid: 1.6 M of them at C5)
+  MarkCounts cn;
+  unsigned long long t_acc = 0, marked = 0;
   for (int64_t pos = lo + (int64_t)blockIdx.x * MARK_WARPS + wid; pos < n; pos += (int64_t)gridDim.x * MARK_WARPS)
-    mark_block<D, BINNED>(A, M, S, pos, lane, wid);
+    mark_block<D, BINNED>(A, M, S, pos, lane, wid, cn, t_acc, marked);
+  flush_counts(A, cn, lane);
+  if (lane == 0) {
+    if (t_acc) atomicAdd(&A.out[1], t_acc);
+    if (marked) atomicAdd(&A.out[0], marked);
+  }
 }
 
 template <int D, bool BINNED>
 __device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M, MarkSmem<D>& S, int64_t pos,
-                                           int lane, int wid) {
+                                           int lane, int wid, MarkCounts& cn, unsigned long long& t_acc,
+                                           unsigned long long& marked) {
   constexpr int CPL = D == 3 ? 2 : 1;
   const int id = A.leaves[pos];
   double blo[3], bhi[3];
@@ -401,11 +413,10 @@ __device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M
     if (bin[k] >= 0) t += BINNED ? (unsigned long long)A.bin_counts[bin[k]] : (unsigned long long)A.n_faces;
   // algorithmic test count T, one atomic per warp
   for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-  if (lane == 0) atomicAdd(&A.out[1], t);
+  t_acc += t;  // (every lane holds the sum; lane 0's is flushed)
   if (A.F.marks[id] == OW_MARKED) return;
   const double reach2 = DMUL(A.reach, A.reach);
   const float r2 = FMUL(A.d, A.d);
-  MarkCounts cn;
   bool pend[CPL];
 #pragma unroll
   for (int k = 0; k < CPL; ++k) pend[k] = bin[k] >= 0;
@@ -477,11 +488,10 @@ __device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M
       }
     }
   }
-  flush_counts(A, cn, lane);
   if (lane == 0) {
     if (hit && atomicOr(&M.hit[pos], 1u) == 0u) {
       A.F.marks[id] = OW_MARKED;
-      atomicAdd(&A.out[0], 1ull);
+      ++marked;
     }
   }
 }

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import itertools
+import threading
 import struct
 from dataclasses import dataclass
 
@@ -28,15 +29,17 @@ _keys = itertools.count(1)
 
 
 def _require(ok, message):
+    """Raise InvalidParameterError(message) unless ok; ``message`` may be a
+    callable so array formatting only happens on failure."""
     if not ok:
-        raise InvalidParameterError(message)
+        raise InvalidParameterError(message() if callable(message) else message)
 
 
 def as_point(p, dim):
     """float64 point of exactly ``dim`` finite components (geometry.py:16-25)."""
     a = np.asarray(p, dtype=np.float64).ravel()
     _require(a.size == dim, f"expected a {dim}-component point, got {a.size}")
-    _require(bool(np.isfinite(a).all()), f"point has non-finite components: {a}")
+    _require(bool(np.isfinite(a).all()), lambda: f"point has non-finite components: {a}")
     return a
 
 
@@ -51,7 +54,7 @@ class Aabb:
         lo, hi = (np.asarray(c, dtype=np.float64).ravel() for c in (self.min, self.max))
         _require(lo.shape == hi.shape, "aabb min/max dimension mismatch")
         _require(bool(np.isfinite(lo).all() and np.isfinite(hi).all()), "aabb has non-finite corners")
-        _require(not bool((lo > hi).any()), f"aabb min {lo} exceeds max {hi}")
+        _require(not bool((lo > hi).any()), lambda: f"aabb min {lo} exceeds max {hi}")
         self.min, self.max = lo, hi
 
     @property
@@ -284,14 +287,42 @@ def import_text_primitives(path, dim=None):
     return parse_text_primitives(text, path=path, dim=dim)
 
 
+_staging = threading.local()
+
+
+def _to_device(a: np.ndarray, slot: int, dev) -> torch.Tensor:
+    """Host array -> device tensor through a reusable pinned staging buffer
+    (per thread and slot), stream-ordered and without a host synchronisation
+    (a pageable copy would wait for the device); the buffer is refilled only
+    after its previous copy has completed."""
+    bufs = getattr(_staging, "bufs", None)
+    if bufs is None:
+        bufs = _staging.bufs = {}
+    a = np.ascontiguousarray(a)
+    ent = bufs.get(slot)
+    if ent is None or ent[0].numel() < a.nbytes:
+        ent = (torch.empty(max(a.nbytes, 1 << 16), dtype=torch.uint8, pin_memory=True), torch.cuda.Event())
+        bufs[slot] = ent
+    else:
+        ent[1].synchronize()
+    buf, ev = ent
+    host = buf[: a.nbytes].numpy()
+    host[:] = a.reshape(-1).view(np.uint8)
+    out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=dev)
+    out.view(-1).view(torch.uint8).copy_(buf[: a.nbytes], non_blocking=True)
+    ev.record()
+    return out
+
+
 def index_to_coords(g: IndexedGeometry) -> CoordListGeometry:
-    """Indexed mesh -> device coordinate list; pure gather on the GPU."""
+    """Indexed mesh -> device coordinate list; pure gather on the GPU (the
+    vertices and faces go host -> device stream-ordered, no host wait)."""
     dev = _lib.device()
     n = g.n_faces
     out = torch.empty((g.dim, g.dim, n), dtype=torch.float32, device=dev)
     if n:
-        v = torch.from_numpy(np.ascontiguousarray(g.vertices)).to(dev)
-        fc = torch.from_numpy(np.ascontiguousarray(g.faces)).to(dev)
+        v = _to_device(g.vertices, 0, dev)
+        fc = _to_device(g.faces, 1, dev)
         _lib.call("ow_index_to_coords", _lib.ctx(), g.dim, _lib.ptr(v), _lib.ptr(fc), n, _lib.ptr(out), _lib.stream())
     return CoordListGeometry(g.dim, out)
 
