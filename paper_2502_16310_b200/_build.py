@@ -74,6 +74,9 @@ def _compile(src, obj, extra, verbose):
 
 
 def build(force=False, verbose=False, extra=()):
+    # OW_NVCC_EXTRA: extra nvcc flags for A/B experiments (e.g. -DOW_MARK_CG=2);
+    # they enter the fingerprint, so the default build is restored without them
+    extra = (*extra, *os.environ.get("OW_NVCC_EXTRA", "").split())
     if not force and up_to_date(extra):
         return LIB
     objdir = os.path.join(HERE, "build")

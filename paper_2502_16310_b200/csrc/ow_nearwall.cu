@@ -199,7 +199,10 @@ __global__ void k_chunk_boxes(const int32_t* __restrict__ ids, int64_t n_entries
 // is one the reference evaluates (same culls), so marks are bit-exact even
 // where the predicate is ill-conditioned.
 constexpr int MARK_WARPS = MARK_THREADS / 32;
-constexpr int CG = 4;  // chunks swept inline by the block pass
+#ifndef OW_MARK_CG
+#define OW_MARK_CG 4
+#endif
+constexpr int CG = OW_MARK_CG;  // chunks swept inline by the block pass
 
 struct MarkCounts {
   unsigned long long evaluated = 0, spheres = 0, culls = 0;

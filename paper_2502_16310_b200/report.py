@@ -3,7 +3,7 @@ pipeline, with its CSV schema (report.py:16-41).  Figures (matplotlib) are
 out of scope; the CSV is the canonical artifact.
 
 A sweep is also the C3 benchmark configuration of BASELINE.json (bunny-scale
-STL, 4 levels, bin-density sweep): ``bench.py --sweep`` runs it.
+STL, 4 levels, bin-density sweep): ``tools/sweep_c3.py`` runs it (``profiles/r01_sweep_c3.csv``).
 """
 
 from __future__ import annotations
