@@ -38,7 +38,7 @@ with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CPU,
     torch.cuda.synchronize()
 prof.export_chrome_trace(out)
 ev = json.load(open(out))["traceEvents"]
-steps = sorted([e for e in ev if e.get("name") == "step" and e.get("ph") == "X"], key=lambda e: e["ts"])
+steps = sorted([e for e in ev if e.get("name") == "step" and e.get("ph") == "X" and e.get("cat") == "user_annotation"], key=lambda e: e["ts"])
 s = steps[-1]
 t0, t1 = s["ts"], s["ts"] + s["dur"]
 rows = []

@@ -59,7 +59,7 @@ with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CPU, tor
 prof.export_chrome_trace(out)
 ev = json.load(open(out))["traceEvents"]
 kern = sorted([e for e in ev if e.get("cat") in ("kernel", "gpu_memset", "gpu_memcpy")], key=lambda e: e["ts"])
-steps_ev = sorted([e for e in ev if e.get("name") == "step" and e.get("ph") == "X"], key=lambda e: e["ts"])
+steps_ev = sorted([e for e in ev if e.get("name") == "step" and e.get("ph") == "X" and e.get("cat") == "user_annotation"], key=lambda e: e["ts"])
 s = steps_ev[-1]
 t0, t1 = s["ts"], s["ts"] + s["dur"]
 ks = [k for k in kern if t0 <= k["ts"] <= t1]
