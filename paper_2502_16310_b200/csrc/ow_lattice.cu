@@ -26,7 +26,8 @@
 //   k_lat_mt     : (rows above a tunable size only; not launched by default)
 //                  one thread per (row, cell) unit, load-balanced over rows
 //                  staged in shared memory, the same test.
-//   k_lat_bcount + scan : boundary rows in (block, cell) order.
+//   k_lat_bscan  : boundary cells per candidate block and their row offsets
+//                  in (block, cell) order (one look-back scan).
 //   k_lat_emit + k_lat_hits : cells, q rows (-1 / min t via atomicMin).
 #include "ow_scan.cuh"
 #include <stdlib.h>
@@ -949,38 +950,95 @@ __global__ void __launch_bounds__(MT_THREADS) k_lat_mt(LatArgs A) {
   }
 }
 
-// boundary cells per candidate block (warp per block): count + cell mask
+// Boundary cells of each candidate block and their row offsets in one pass
+// (a single-pass scan with decoupled look-back over tiles of 256 candidate
+// blocks, ow_scan.cuh): a thread per candidate block reads its flag words
+// (16-byte loads, all in flight), forms the boundary-cell mask, the cell
+// count and the link count; the tile's counts are scanned and the rows of
+// the blocks before it come from the look-back.  Writes bmask / bcount /
+// hcount / boff per candidate, the row total into *nb_total and the links
+// into A.links_d (one atomic per warp).
+constexpr int BSCAN_THREADS = 256;
 template <int D>
-__global__ void k_lat_bcount(LatArgs A) {
+__global__ void __launch_bounds__(BSCAN_THREADS)
+k_lat_bscan(LatArgs A, int64_t* boff, int64_t n_bound, int64_t* nb_total, unsigned long long* status,
+            unsigned long long epoch, const unsigned long long* d_epoch_base) {
   ow_pdl_wait();
+  if (d_epoch_base) epoch += *d_epoch_base * ow::GRAPH_SITES;  // inside a CUDA graph (ow_graph.cu)
   constexpr int C = D == 3 ? 64 : 16;
-  const int lane = threadIdx.x & 31;
-  // persistent warps over the candidate blocks (their count is on the device;
-  // a grid over every leaf launched ~7x more CTAs than there is work at C5)
-  const int64_t ncb = *A.n_cb_d;
-  unsigned long long links_acc = 0;  // (one atomic per warp at the end, not per block)
-  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < ncb;
-       r += (int64_t)gridDim.x * (blockDim.x >> 5)) {
-  const int64_t pos = A.cand_blocks[r];
+  constexpr int W = BSCAN_THREADS / 32;
+  __shared__ int64_t s_w[W];
+  __shared__ int64_t s_pre;
+  const int64_t ncb = *A.n_cb_d < n_bound ? *A.n_cb_d : n_bound;
+  const int64_t tile = blockIdx.x;
+  if (tile > 0 && tile * BSCAN_THREADS >= ncb) return;  // (past the candidates: nobody looks back here)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r = tile * BSCAN_THREADS + threadIdx.x;
   unsigned long long m = 0;
   int links = 0;
+  if (r < ncb) {
+    const uint4* fp = reinterpret_cast<const uint4*>(A.flags + (int64_t)A.cand_blocks[r] * C);
+    uint4 w[C / 4];
 #pragma unroll
-  for (int k = 0; k < (C + 31) / 32; ++k) {
-    const int c = lane + 32 * k;
-    const unsigned fl = c < C ? A.flags[pos * C + c] : 0u;
-    const unsigned b = __ballot_sync(0xffffffffu, fl != 0);
-    m |= (unsigned long long)b << (32 * k);
-    links += __popc(fl);
+    for (int k = 0; k < C / 4; ++k) w[k] = fp[k];
+#pragma unroll
+    for (int k = 0; k < C / 4; ++k) {
+      m |= (unsigned long long)((unsigned)(w[k].x != 0u) | (unsigned)(w[k].y != 0u) << 1 |
+                                (unsigned)(w[k].z != 0u) << 2 | (unsigned)(w[k].w != 0u) << 3)
+           << (4 * k);
+      links += __popc(w[k].x) + __popc(w[k].y) + __popc(w[k].z) + __popc(w[k].w);
+    }
   }
-  links = __reduce_add_sync(0xffffffffu, links);
-  if (lane == 0) {
-    A.bcount[r] = __popcll(m);
-    A.hcount[r] = links;
+  const int bc = __popcll(m);
+  int x = bc;  // warp inclusive scan of the cell counts
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[warp] = x;
+  const int lsum = __reduce_add_sync(0xffffffffu, links);
+  if (lane == 0 && lsum) atomicAdd(A.links_d, (unsigned long long)lsum);
+  __syncthreads();
+  if (warp == 0) {
+    int64_t y = lane < W ? s_w[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < W; o <<= 1) {
+      const int64_t z = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += z;
+    }
+    const int64_t agg = __shfl_sync(0xffffffffu, y, W - 1);
+    const int64_t wex = y - (lane < W ? s_w[lane] : 0);
+    const int64_t prefix = ow::lookback(status, tile, agg, epoch, lane);
+    __syncwarp();
+    if (lane < W) s_w[lane] = prefix + wex;
+    if (lane == 0) s_pre = prefix;
+  }
+  __syncthreads();
+  const int64_t e = s_w[warp] + (x - bc);
+  if (r < ncb) {
+    boff[r] = e;
     A.bmask[r] = m;
-    links_acc += (unsigned long long)links;
+    A.bcount[r] = bc;
+    A.hcount[r] = links;
+    if (r == ncb - 1) *nb_total = e + bc;
   }
-  }
-  if ((threadIdx.x & 31) == 0 && links_acc) atomicAdd(A.links_d, links_acc);
+  if (ncb == 0 && threadIdx.x == 0) *nb_total = 0;
+  (void)s_pre;
+}
+
+// tiles / launch of k_lat_bscan over at most n_bound candidate blocks
+template <int D>
+int lat_bscan(ow_ctx* ctx, const LatArgs& A, int64_t n_bound, int64_t* nb_total, cudaStream_t s) {
+  const int64_t tiles = n_bound > 0 ? (n_bound + BSCAN_THREADS - 1) / BSCAN_THREADS : 1;
+  unsigned long long* status;
+  unsigned long long epoch;
+  OW_TRY(ow::scan_status(ctx, tiles, s, &status, &epoch));
+  ow_launch(k_lat_bscan<D>, (unsigned)tiles, BSCAN_THREADS, 0, s, A, (int64_t*)A.boff, n_bound, nb_total, status, epoch,
+            (const unsigned long long*)(ctx->capturing ? ctx->d_graph_epoch : nullptr));
+  OW_LAUNCHED(ctx);
+  OW_CHECK_LAUNCH();
+  return OW_OK;
 }
 
 // boundary rows in (block, cell) order: cells and q rows (-1 where the link
@@ -1378,14 +1436,13 @@ int lat_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_l
     if (fpw == 8) ow_launch(k_lat_faces<2, 8>, lat_face_grid<2, 8>(n_faces), 128, 0, s, A);
     else ow_launch(k_lat_faces<2, 4>, lat_face_grid<2, 4>(n_faces), 128, 0, s, A);
   }
-  ctx->launches += 2;
+  ctx->launches += 2;  // (k_lat_pos, the face pass)
   OW_CHECK_LAUNCH();
   const int64_t tiles_max = ucap / MT_TILE + 1;
   if (!inline_all) {  // (every row inline: no k_lat_mt rows, and k_lat_hits sees zero units)
     if (D == 3) ow_launch(k_lat_mt<3>, ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s, A);
     else ow_launch(k_lat_mt<2>, ow_blocks(tiles_max, 1, 6 * OW_SMS), MT_THREADS, 0, s, A);
-  } else {
-    ctx->launches -= 1;
+    OW_LAUNCHED(ctx);
   }
   if (!d_nl && ctx->lat_comm && ctx->lat_comm->world > 1) {
     // multi-GPU: every rank swept the faces against its own leaf slice; the
@@ -1413,11 +1470,8 @@ int lat_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_l
   }
   OW_TRY(ow::scan01(ctx, CandLoad{A.has_pair}, CandStore{A.cand_rank, A.cand_blocks}, nl, ctx->d_small + 33, s, d_nl));
   OW_PROF_END(ctx, PROF_LAT_SWEEP, s);
-  if (D == 3) ow_launch(k_lat_bcount<3>, ow_blocks(nl, 8, 8 * OW_SMS), 256, 0, s, A);
-  else ow_launch(k_lat_bcount<2>, ow_blocks(nl, 8, 8 * OW_SMS), 256, 0, s, A);
-  ctx->launches += 2;
-  OW_CHECK_LAUNCH();
-  OW_TRY(scan(ctx, BcountLoad{A.bcount, A.n_cb_d}, BoffStore{(int64_t*)A.boff, A.n_cb_d}, nl, ctx->d_small + 35, s));
+  if (D == 3) OW_TRY(lat_bscan<3>(ctx, A, nl, ctx->d_small + 35, s));
+  else OW_TRY(lat_bscan<2>(ctx, A, nl, ctx->d_small + 35, s));
   OW_PROF_END(ctx, PROF_LATTICE, s);
   if (d_nl) return OW_OK;  // (counts checked by the caller after the pass)
   // single readback: candidate blocks, (scan scratch), boundary cells, rows, units, links
