@@ -287,6 +287,8 @@ int ow_readback(ow_ctx* ctx, const int64_t* d_src, int n, int64_t* h_dst, cudaSt
 int ow_faces_settle(ow_ctx* ctx, const int64_t* h6, cudaStream_t s);
 void ow_face_summary_from(const int64_t* h, int64_t n, ow_face_summary* out);
 int ow_face_check_launch(ow_ctx* ctx, int32_t dim, const float* d_coords, int64_t n, int64_t* dst, cudaStream_t s);
+int ow_stl_to_soa_checked(ow_ctx* ctx, const uint8_t* d_records, int64_t n, float* d_coords, int64_t* dst,
+                          cudaStream_t s);
 
 // bracket device work of kernel family `id` with events when profiling is on
 void ow_prof_mark(ow_ctx* ctx, int id, int end, cudaStream_t s);

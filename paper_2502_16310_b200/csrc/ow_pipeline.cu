@@ -575,10 +575,11 @@ int g2g_sync(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n_f
   // deferred host copies of this caller's previous pass still read its
   // outputs: the device waits for them before anything is rewritten
   if (p->copy_done) OW_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)p->copy_done, 0));
-  if (d_records) OW_TRY(ow_stl_binary_to_soa(ctx, d_records, n_faces, d_coords, stream));
   // the face check's summary is read with the first bin-count readback (one
   // host round trip less) and validated there, before anything depends on it
-  OW_TRY(ow_face_check_launch(ctx, D, d_coords, n_faces, ctx->d_small + 56, s));
+  // (with STL records: fused into the record -> SoA pass)
+  if (d_records && D == 3) OW_TRY(ow_stl_to_soa_checked(ctx, d_records, n_faces, d_coords, ctx->d_small + 56, s));
+  else OW_TRY(ow_face_check_launch(ctx, D, d_coords, n_faces, ctx->d_small + 56, s));
   OW_TRY(ow_forest_init_root(ctx, f, stream));
   ow_nearwall_params nw = p->nw;
   FacesState fs_state{out, f, &nw, n_faces};
@@ -855,8 +856,8 @@ int g2g_submit(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n
   t->d_qp = d_qp;
   // ---- the pass, enqueued without a host round trip
   if (p->copy_done) OW_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)p->copy_done, 0));
-  if (d_records) OW_TRY(ow_stl_binary_to_soa(ctx, d_records, n_faces, d_coords, s));
-  OW_TRY(ow_face_check_launch(ctx, D, d_coords, n_faces, ctx->d_small + 56, s));
+  if (d_records && D == 3) OW_TRY(ow_stl_to_soa_checked(ctx, d_records, n_faces, d_coords, ctx->d_small + 56, s));
+  else OW_TRY(ow_face_check_launch(ctx, D, d_coords, n_faces, ctx->d_small + 56, s));
   OW_TRY(ow_forest_init_root(ctx, f, s));
   ow_nearwall_params nw = p->nw;
   nw.reach = predicted_reach(f, &p->nw);
