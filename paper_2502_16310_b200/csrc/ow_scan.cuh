@@ -219,15 +219,22 @@ int scan(ow_ctx* ctx, Load load, Store store, int64_t n, int64_t* d_total, cudaS
 // per thread; ranks come from ballots, so values never leave registers.
 constexpr int C01_ITEMS = 16;
 constexpr int C01_TILE = SCAN_THREADS * C01_ITEMS;
+// small compactions (the level loop's leaf / split / violator lists: up to a
+// few 100 k elements) use 1 024-element tiles instead: 4x the CTAs in flight
+// for the same elements, so the dependent loads of the predicates overlap
+constexpr int C01_ITEMS_SMALL = 4;
+constexpr int64_t C01_SMALL_MAX = int64_t(1) << 20;
 
-template <class Load, class Store>
+template <class Load, class Store, int ITEMS = C01_ITEMS>
 __global__ void __launch_bounds__(SCAN_THREADS, 6)
 k_scan01(Load load, Store store, int64_t n, const int64_t* d_n, unsigned long long* status, int64_t* total_out,
          unsigned long long epoch, const unsigned long long* d_epoch_base) {
   ow_pdl_wait();
   if (d_epoch_base) epoch += *d_epoch_base * GRAPH_SITES;  // inside a CUDA graph (ow_graph.cu)
   constexpr int W = SCAN_THREADS / 32;
-  static_assert(C01_ITEMS * W == 128, "warp 0 holds 4 counts per lane");
+  constexpr int C01_TILE = SCAN_THREADS * ITEMS;
+  constexpr int C01_ITEMS = ITEMS;
+  static_assert(C01_ITEMS * W == 128 || C01_ITEMS * W == 32, "warp 0 holds 4 or 1 counts per lane");
   __shared__ int s_cnt[C01_ITEMS * W];  // per (item k, warp) in element order -> exclusive ranks
   __shared__ int64_t s_pre;
   const int64_t tile = blockIdx.x;
@@ -253,19 +260,31 @@ k_scan01(Load load, Store store, int64_t n, const int64_t* d_n, unsigned long lo
   if (lane < C01_ITEMS) s_cnt[lane * W + warp] = c;
   __syncthreads();
   if (warp == 0) {
-    const int a0 = s_cnt[4 * lane], a1 = s_cnt[4 * lane + 1], a2 = s_cnt[4 * lane + 2], a3 = s_cnt[4 * lane + 3];
-    const int s4 = a0 + a1 + a2 + a3;
-    int x = s4;
+    int x;
+    if constexpr (C01_ITEMS * W == 128) {
+      const int a0 = s_cnt[4 * lane], a1 = s_cnt[4 * lane + 1], a2 = s_cnt[4 * lane + 2], a3 = s_cnt[4 * lane + 3];
+      const int s4 = a0 + a1 + a2 + a3;
+      x = s4;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      const int ex = x - s4;
+      s_cnt[4 * lane] = ex;
+      s_cnt[4 * lane + 1] = ex + a0;
+      s_cnt[4 * lane + 2] = ex + a0 + a1;
+      s_cnt[4 * lane + 3] = ex + a0 + a1 + a2;
+    } else {
+      const int a0 = s_cnt[lane];
+      x = a0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      s_cnt[lane] = x - a0;
     }
-    const int ex = x - s4;
-    s_cnt[4 * lane] = ex;
-    s_cnt[4 * lane + 1] = ex + a0;
-    s_cnt[4 * lane + 2] = ex + a0 + a1;
-    s_cnt[4 * lane + 3] = ex + a0 + a1 + a2;
     const int64_t agg = __shfl_sync(0xffffffffu, x, 31);
     const int64_t prefix = lookback(status, tile, agg, epoch, lane);
     if (lane == 0) {
@@ -291,12 +310,19 @@ int scan01(ow_ctx* ctx, Load load, Store store, int64_t n, int64_t* d_total, cud
     if (d_total) OW_CUDA(cudaMemsetAsync(d_total, 0, sizeof(int64_t), s));
     return OW_OK;
   }
-  const int64_t tiles = (n + C01_TILE - 1) / C01_TILE;
+  const bool small = n <= C01_SMALL_MAX;
+  const int64_t tile = (int64_t)SCAN_THREADS * (small ? C01_ITEMS_SMALL : C01_ITEMS);
+  const int64_t tiles = (n + tile - 1) / tile;
   unsigned long long* status;
   unsigned long long epoch;
   OW_TRY(scan_status(ctx, tiles, s, &status, &epoch));
-  ow_launch(k_scan01<Load, Store>, (unsigned)tiles, SCAN_THREADS, 0, s, load, store, n, d_n, status, d_total, epoch,
-            (const unsigned long long*)(ctx->capturing ? ctx->d_graph_epoch : nullptr));
+  const unsigned long long* base = (const unsigned long long*)(ctx->capturing ? ctx->d_graph_epoch : nullptr);
+  if (small)
+    ow_launch(k_scan01<Load, Store, C01_ITEMS_SMALL>, (unsigned)tiles, SCAN_THREADS, 0, s, load, store, n, d_n, status,
+              d_total, epoch, base);
+  else
+    ow_launch(k_scan01<Load, Store, C01_ITEMS>, (unsigned)tiles, SCAN_THREADS, 0, s, load, store, n, d_n, status,
+              d_total, epoch, base);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;
