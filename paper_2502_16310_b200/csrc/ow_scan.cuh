@@ -89,10 +89,11 @@ __device__ __forceinline__ int64_t lookback(unsigned long long* status, int64_t 
 // scans only, no CTA barrier; the re-read hits L2) and stores.  One tile per
 // CTA would make the look-back chain grow with n / SCAN_TILE and dominate:
 // when tiles are cheap every tile looks back at once.
-template <class Load, class Store>
+template <class Load, class Store, int ITEMS = SCAN_ITEMS>
 __global__ void __launch_bounds__(SCAN_THREADS)
 k_scan(Load load, Store store, int64_t n, int64_t n_chunks, int64_t chunk, unsigned long long* status,
        int64_t* total_out, unsigned long long epoch, const unsigned long long* d_epoch_base) {
+  constexpr int SCAN_ITEMS = ITEMS;  // (shadows the default: small scans take 2 per thread)
   ow_pdl_wait();
   if (d_epoch_base) epoch += *d_epoch_base * GRAPH_SITES;  // inside a CUDA graph (ow_graph.cu)
   constexpr int W = SCAN_THREADS / 32;
@@ -198,16 +199,24 @@ int scan(ow_ctx* ctx, Load load, Store store, int64_t n, int64_t* d_total, cudaS
     if (d_total) OW_CUDA(cudaMemsetAsync(d_total, 0, sizeof(int64_t), s));
     return OW_OK;
   }
-  // chunks of whole tiles, at most SCAN_MAX_CHUNKS of them
-  const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  // chunks of whole tiles, at most SCAN_MAX_CHUNKS of them (tiles of 2 elements
+  // per thread below 1 M elements: 4x the CTAs in flight for small scans)
+  const bool small = n <= (int64_t(1) << 20);
+  const int64_t tile = (int64_t)SCAN_THREADS * (small ? 2 : SCAN_ITEMS);
+  const int64_t tiles = (n + tile - 1) / tile;
   const int64_t per = (tiles + SCAN_MAX_CHUNKS - 1) / SCAN_MAX_CHUNKS;
-  const int64_t chunk = per * SCAN_TILE;
+  const int64_t chunk = per * tile;
   const int64_t n_chunks = (n + chunk - 1) / chunk;
   unsigned long long* status;
   unsigned long long epoch;
   OW_TRY(scan_status(ctx, n_chunks, s, &status, &epoch));
-  ow_launch(k_scan<Load, Store>, (unsigned)n_chunks, SCAN_THREADS, 0, s, load, store, n, n_chunks, chunk, status, d_total,
-            epoch, (const unsigned long long*)(ctx->capturing ? ctx->d_graph_epoch : nullptr));
+  const unsigned long long* base = (const unsigned long long*)(ctx->capturing ? ctx->d_graph_epoch : nullptr);
+  if (small)
+    ow_launch(k_scan<Load, Store, 2>, (unsigned)n_chunks, SCAN_THREADS, 0, s, load, store, n, n_chunks, chunk, status,
+              d_total, epoch, base);
+  else
+    ow_launch(k_scan<Load, Store, SCAN_ITEMS>, (unsigned)n_chunks, SCAN_THREADS, 0, s, load, store, n, n_chunks, chunk,
+              status, d_total, epoch, base);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   return OW_OK;
