@@ -263,7 +263,7 @@ constexpr int RS_MAX_ITERS = 26;
 int ow_forest_leaves_dev(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t* d_out, int64_t* d_count,
                          cudaStream_t s, const int64_t* d_nb = nullptr);
 int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, const int64_t* d_n, int64_t n_bound,
-                     int32_t rounds, cudaStream_t s);
+                     int32_t rounds, cudaStream_t s, bool tags = false);
 int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64_t* d_st, cudaStream_t s,
                   int64_t* d_nb = nullptr);
 int ow_rebalance_host(ow_ctx* ctx, ow_forest* f, int64_t f0, int64_t* n_split, cudaStream_t s);

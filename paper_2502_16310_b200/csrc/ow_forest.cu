@@ -138,11 +138,17 @@ __global__ void k_violators(ForestC F, int64_t f0, int64_t f1, uint8_t* flag) {
   if (F.first_child[node] < 0 && depth < lv - 1) flag[node] = 1;
 }
 
+// a mark that counts as MARKED in a propagation round: MARKED, or a round tag
+// of an earlier round of the device loop (3 <= m < below, ow_propagate_dev)
+__device__ __forceinline__ bool counts_marked(int8_t m, int below) {
+  return m == OW_MARKED || (m >= 3 && m < below);
+}
+
 // any MARKED leaf on the face of region (L, nc) facing the query block
-__device__ bool side_has_marked(const ForestC& F, int L, const int32_t* nc, int s) {
+__device__ bool side_has_marked(const ForestC& F, int L, const int32_t* nc, int s, int below = 0) {
   int depth;
   int node = locate(F, L, nc, &depth);
-  if (F.first_child[node] < 0) return F.marks[node] == OW_MARKED;
+  if (F.first_child[node] < 0) return counts_marked(F.marks[node], below);
   const int ax = s >> 1;
   const int want = (s & 1) ? 0 : 1;  // neighbour on + side: its children on the min face
   int stack[64];
@@ -152,7 +158,7 @@ __device__ bool side_has_marked(const ForestC& F, int L, const int32_t* nc, int 
     int b = stack[--sp];
     int fc = F.first_child[b];
     if (fc < 0) {
-      if (F.marks[b] == OW_MARKED) return true;
+      if (counts_marked(F.marks[b], below)) return true;
       continue;
     }
     for (int ci = (1 << F.dim) - 1; ci >= 0; --ci)
@@ -439,7 +445,14 @@ struct FlagCompactClear {  // compaction that also clears the flags it consumed
   }
 };
 
-__global__ void k_prop_gather_dev(ForestC F, const int32_t* __restrict__ leaves, const int64_t* n) {
+// One propagation round of the device loop (nearwall.py:321-366) without
+// its promote step: a NONE leaf with a face neighbour that counts as MARKED
+// (MARKED, or tagged in an earlier round) gets this round's tag 3 + r, which
+// the same round never counts — so every round sees exactly the marks the
+// reference's round does, and one promote after the last round turns the
+// tags into MARKED (rounds + 1 launches instead of 2 rounds).
+__global__ void k_prop_gather_dev(ForestC F, const int32_t* __restrict__ leaves, const int64_t* n, int tag,
+                                  int below) {
   ow_pdl_wait();
   const int64_t nn = *n;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
@@ -450,8 +463,8 @@ __global__ void k_prop_gather_dev(ForestC F, const int32_t* __restrict__ leaves,
     for (int s = 0; s < 2 * F.dim; ++s) {
       int32_t nc[3];
       if (!side_target(F, L, c, s, nc)) continue;
-      if (side_has_marked(F, L, nc, s)) {
-        F.marks[id] = OW_INTERMEDIATE;
+      if (side_has_marked(F, L, nc, s, below)) {
+        F.marks[id] = (int8_t)tag;
         break;
       }
     }
@@ -463,7 +476,7 @@ __global__ void k_prop_promote_dev(int8_t* marks, const int32_t* __restrict__ le
   const int64_t nn = *n;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
     const int id = leaves[i];
-    if (marks[id] == OW_INTERMEDIATE) marks[id] = OW_MARKED;
+    if (marks[id] >= OW_INTERMEDIATE) marks[id] = OW_MARKED;  // (INTERMEDIATE or this level's round tags)
   }
 }
 
@@ -480,14 +493,23 @@ int ow_forest_leaves_dev(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t
 }
 
 int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, const int64_t* d_n, int64_t n_bound,
-                     int32_t rounds, cudaStream_t s) {
+                     int32_t rounds, cudaStream_t s, bool tags) {
   if (n_bound <= 0 || rounds <= 0) return OW_OK;
   ForestC F = make_forestc(f);
   OW_PROF_BEGIN(ctx, PROF_PROP, s);
+  // tags (a fresh forest, no INTERMEDIATE marks before the level's marking):
+  // round tags 3 .. 3 + rounds - 1 stay inside int8 (a promote every 100
+  // rounds restarts them; the reference's rounds are 1 + floor(d / block
+  // length)).  Else the reference's round as is: INTERMEDIATE, then promote.
   for (int r = 0; r < rounds; ++r) {
-    ow_launch(k_prop_gather_dev, ow_blocks(n_bound, 128, 16 * OW_SMS), 128, 0, s, F, d_leaves, d_n);
-    ow_launch(k_prop_promote_dev, ow_blocks(n_bound, 256, 8 * OW_SMS), 256, 0, s, F.marks, d_leaves, d_n);
-    ctx->launches += 2;
+    const int tag = tags ? 3 + r % 100 : OW_INTERMEDIATE;
+    ow_launch(k_prop_gather_dev, ow_blocks(n_bound, 128, 16 * OW_SMS), 128, 0, s, F, d_leaves, d_n, tag,
+              tags ? tag : 0);
+    ctx->launches += 1;
+    if (!tags || r % 100 == 99 || r + 1 == rounds) {
+      ow_launch(k_prop_promote_dev, ow_blocks(n_bound, 256, 8 * OW_SMS), 256, 0, s, F.marks, d_leaves, d_n);
+      ctx->launches += 1;
+    }
   }
   OW_PROF_END(ctx, PROF_PROP, s);
   OW_CHECK_LAUNCH();

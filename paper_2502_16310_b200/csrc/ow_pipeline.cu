@@ -378,7 +378,8 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
         bl = b < bl ? b : bl;
       }
       const int rounds = 1 + (int)floor(p->d_spec64 / bl);
-      OW_TRY(ow_propagate_dev(ctx, f, (const int32_t*)pl, dn, n_host, rounds, s));
+      // (the device-resident loop starts from a fresh root grid: round tags)
+      OW_TRY(ow_propagate_dev(ctx, f, (const int32_t*)pl, dn, n_host, rounds, s, dev));
     }
     // ---- refinement on the device; one readback of its state per level
     OW_TRY(record(se, level, 3, s, ctx->no_stage_events));
