@@ -425,6 +425,14 @@ __global__ void k_small_init(int64_t* small) {
   if (threadIdx.x < 8) small[threadIdx.x] = (threadIdx.x == 1 || threadIdx.x == 3) ? -1 : 0;
 }
 
+// the same and the bin counts cleared, one launch (device-sized fill_bins)
+__global__ void k_bins_init(int64_t* small, int32_t* counts, int64_t n_bins) {
+  ow_pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x < 8) small[threadIdx.x] = (threadIdx.x == 1 || threadIdx.x == 3) ? -1 : 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_bins; i += (int64_t)gridDim.x * blockDim.x)
+    counts[i] = 0;
+}
+
 template <int D>
 int fill_count(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, int32_t* counts, int64_t n_bins,
                int64_t* out_entries, int64_t* out_outside, cudaStream_t s) {
@@ -567,8 +575,7 @@ int fill_dev(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, in
   OW_TRY(ow_slot(ctx, SLOT_BIN_SLOW, 4 * (size_t)n, s, &psl));
   OW_TRY(ow_slot(ctx, SLOT_BIN_MID, 4 * (size_t)n, s, &pmid));
   int64_t* small = ctx->d_small;
-  OW_TRY(ow_fill_async(ctx, counts, 0, 4 * (size_t)n_bins, s));
-  ow_launch(k_small_init, 1, 32, 0, s, small);
+  ow_launch(k_bins_init, ow_blocks(n_bins, 256, 4 * OW_SMS), 256, 0, s, small, counts, n_bins);
   ow_launch(k_count_fast<D>, ow_blocks(n, 256), 256, 0, s, g, c, n, (unsigned long long*)pm, (int32_t*)pnb, counts,
             (int32_t*)pmid, small);
   ow_launch(k_count_walk<D>, ow_blocks(n, 256, 8 * OW_SMS), 256, 0, s, g, c, n, h, (const int32_t*)pmid,

@@ -243,7 +243,7 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
 // device-sized lattice stage of the fused pass (ow_lattice.cu)
 int ow_lattice_dev_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_leaves, const int64_t* d_nl,
                          int64_t nl_cap, const float* d_coords, int64_t n_faces, const int8_t* h_dirs, int32_t n_dirs,
-                         uint32_t* d_flags, cudaStream_t s);
+                         uint32_t* d_flags, cudaStream_t s, int64_t* d_leaves64);
 int ow_lattice_dev_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, int64_t row_cap, uint32_t* d_rows,
                         float* d_q_packed, int64_t link_cap, int64_t ncb_grid, cudaStream_t s);
 

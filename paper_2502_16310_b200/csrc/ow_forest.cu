@@ -355,15 +355,23 @@ namespace {
 // [RS_NR + k] block count before split k, [RS_CR + k] length of split list k
 // (layout constants RS_* in ow_common.cuh)
 
-__global__ void k_rs_init(int64_t* st, int64_t n, const int64_t* nd) {
+// refine state init (CTA 0) and the violator flags cleared (grid-stride, 16
+// bytes per store: flag is 8-byte aligned scratch of cap + 8 bytes)
+__global__ void k_rs_init(int64_t* st, int64_t n, const int64_t* nd, uint8_t* flag, int64_t cap) {
   ow_pdl_wait();
-  if (nd) n = *nd;
-  for (int i = threadIdx.x; i < RS_WORDS; i += blockDim.x) st[i] = 0;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    st[RS_NR] = n;
-    st[RS_RESUME] = n;
+  if (blockIdx.x == 0) {
+    if (nd) n = *nd;
+    for (int i = threadIdx.x; i < RS_WORDS; i += blockDim.x) st[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      st[RS_NR] = n;
+      st[RS_RESUME] = n;
+    }
   }
+  const int64_t words = (cap + 15) / 16;
+  uint4* f4 = reinterpret_cast<uint4*>(flag);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
+    f4[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 
 // Split k of a device-driven refine: list k (length cnt[k]) splits into ids
@@ -534,10 +542,9 @@ int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64
   const int64_t n = f->n_blocks, cap = f->capacity;
   void *pl, *pf;
   OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(cap + 1), s, &pl));
-  OW_TRY(ow_slot(ctx, SLOT_FOREST_FLAG, (size_t)cap + 8, s, &pf));
+  OW_TRY(ow_slot(ctx, SLOT_FOREST_FLAG, (size_t)cap + 16, s, &pf));
   OW_PROF_BEGIN(ctx, PROF_REFINE, s);
-  ow_launch(k_rs_init, 1, 64, 0, s, d_st, n, d_nb);
-  OW_TRY(ow_fill_async(ctx, pf, 0, (size_t)cap, s));
+  ow_launch(k_rs_init, ow_blocks((cap + 15) / 16, 256, 2 * OW_SMS), 256, 0, s, d_st, n, d_nb, (uint8_t*)pf, cap);
   OW_TRY(scan01(ctx, SplitLoad{make_forestc(f), level, d_st + RS_INTER}, CompactStore{(int32_t*)pl},
                 d_nb ? cap : n, d_st + RS_CR, s, d_nb));
   const ow_forest fv = *f;

@@ -112,7 +112,7 @@ struct LatArgs {
 template <int D>
 __global__ void k_lat_pos(ForestC F, int level, const int32_t* __restrict__ leaves, int64_t n, int32_t* pos_of,
                           uint8_t* has_pair, float* cen, int32_t* grid, int g0, int g1, const int64_t* d_n,
-                          uint4* zero_flags) {
+                          uint4* zero_flags, int64_t* widen) {
   ow_pdl_wait();
   if (d_n && *d_n < n) n = *d_n;  // device-sized pass: the leaf count lives on the device
   if (zero_flags)  // ... and the flag words of those leaves are cleared here (no separate fill)
@@ -126,6 +126,7 @@ __global__ void k_lat_pos(ForestC F, int level, const int32_t* __restrict__ leav
     const int id = leaves[i];
     pos_of[id] = (int32_t)i;
     has_pair[i] = 0;
+    if (widen) widen[i] = id;  // (device-sized pass: the int64 leaf output)
     if (grid) {  // finest leaves are the blocks of `level` with no children: one lattice cell each
       int64_t lin = F.coord[D - 1][id];
       if (D == 3) lin = lin * g1 + F.coord[1][id];
@@ -1338,7 +1339,7 @@ namespace {
 int lat_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_leaves, int64_t n_leaves,
               int64_t pos_lo, int64_t pos_hi, const float* d_coords, int64_t n_faces, int64_t geom_key,
               const ow_grid* grid, const int8_t* h_dirs, int32_t n_dirs, uint32_t* d_flags, int64_t* out_boundary,
-              cudaStream_t stream, const int64_t* d_nl) {
+              cudaStream_t stream, const int64_t* d_nl, int64_t* widen_out = nullptr) {
   (void)geom_key;
   if (pos_lo < 0 || pos_hi > n_leaves || pos_lo > pos_hi) {
     ow_set_error("lattice: leaf range [%lld, %lld) outside [0, %lld)", (long long)pos_lo, (long long)pos_hi,
@@ -1420,8 +1421,8 @@ int lat_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_l
   LatArgs A = make_args(ctx);
   if (A.grid) OW_TRY(ow_fill_async(ctx, A.grid, 0xFF, 4 * (size_t)A.gdim[0] * A.gdim[1] * A.gdim[2], s));
   uint4* zf = d_nl ? reinterpret_cast<uint4*>(d_flags) : nullptr;
-  if (D == 3) ow_launch(k_lat_pos<3>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1], d_nl, zf);
-  else ow_launch(k_lat_pos<2>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1], d_nl, zf);
+  if (D == 3) ow_launch(k_lat_pos<3>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1], d_nl, zf, widen_out);
+  else ow_launch(k_lat_pos<2>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1], d_nl, zf, widen_out);
   // the sweep: k_lat_faces (rows; small rows tested inline) + k_lat_mt (large rows)
   OW_PROF_BEGIN(ctx, PROF_LAT_SWEEP, s);
   const int fpw = faces_per_warp(ctx, D, n_faces, nl);
@@ -1519,12 +1520,12 @@ extern "C" int ow_lattice_links_count_range(ow_ctx* ctx, const ow_forest* f, int
 // *d_nl (<= nl_cap) is on the device; count (no readback) ...
 int ow_lattice_dev_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_leaves, const int64_t* d_nl,
                          int64_t nl_cap, const float* d_coords, int64_t n_faces, const int8_t* h_dirs, int32_t n_dirs,
-                         uint32_t* d_flags, cudaStream_t s) {
+                         uint32_t* d_flags, cudaStream_t s, int64_t* d_leaves64) {
   int64_t nb = 0;
   // (positions >= nl_cap are rejected by the face pass: a stale leaf position
   // of an earlier pass can then never index past this pass's buffers)
   return lat_count(ctx, f, level, d_leaves, nl_cap, 0, nl_cap, d_coords, n_faces, -1, nullptr, h_dirs, n_dirs, d_flags,
-                   &nb, s, d_nl);
+                   &nb, s, d_nl, d_leaves64);
 }
 
 // ... then emit with the candidate-block count on the device: persistent grids

@@ -61,8 +61,13 @@ int64_t overflow_total(const int32_t* h_counts, int64_t n_bins, int64_t bin_frac
   return acc;
 }
 
-__global__ void k_set_i64(int64_t* p, int64_t v) {
-  ow_pdl_wait(); *p = v; }
+// the level loop's statistics cleared and (device-resident loop) the block
+// count set, one launch
+__global__ void k_loop_init(unsigned long long* stats, int n_stats, int64_t* d_nb, int64_t nb) {
+  ow_pdl_wait();
+  for (int i = threadIdx.x; i < n_stats; i += blockDim.x) stats[i] = 0ull;
+  if (threadIdx.x == 0 && d_nb) *d_nb = nb;
+}
 
 // ---- multi-GPU marking shards ("balanced by work") --------
 // Work of a leaf block: 1 + the faces of the bin holding its centre (the
@@ -281,11 +286,8 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
   auto device_part = [&]() -> int {
   bool bins_counted = pre_counted;
   have_bins = false;
-  OW_TRY(ow_fill_async(ctx, stats, 0, 40 * (size_t)passes, s));
-  if (dev) {
-    ow_launch(k_set_i64, 1, 1, 0, s, d_nb, f->n_blocks);
-    OW_LAUNCHED(ctx);
-  }
+  ow_launch(k_loop_init, 1, 128, 0, s, (unsigned long long*)stats, 5 * passes, dev ? d_nb : nullptr, f->n_blocks);
+  OW_LAUNCHED(ctx);
   for (int level = 0; level < passes; ++level) {
     // ---- bin_setup
     if (!(pre_counted && level == 0)) OW_TRY(record(se, level, 0, s, ctx->no_stage_events));
@@ -770,13 +772,6 @@ __global__ void k_g2g_summary(const int64_t* __restrict__ small, const int64_t* 
   if (k < 6) t[28 + k] = small[56 + k];
 }
 
-__global__ void k_widen_dev(const int32_t* __restrict__ in, const int64_t* d_n, int64_t cap, int64_t* out) {
-  ow_pdl_wait();
-  const int64_t n = *d_n < cap ? *d_n : cap;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = in[i];
-}
-
 // near-wall reach (nearwall.py:31-40) from the domain alone: equal to the
 // reference's value whenever no coordinate of the geometry exceeds the
 // domain's largest |bound| (checked against the face summary afterwards)
@@ -878,11 +873,11 @@ int g2g_submit(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n
   const int32_t* leaves = (const int32_t*)ctx->slot_ptr[SLOT_DRV_LEAVES];
   int64_t* leaves64 = (int64_t*)p->out_buf[OW_OUT_LEAVES];
   uint32_t* flags = (uint32_t*)p->out_buf[OW_OUT_FLAGS];
-  ow_launch(k_widen_dev, ow_blocks(nl_cap, 256, 4 * OW_SMS), 256, 0, s, leaves, d_nl, nl_cap, leaves64);
-  OW_LAUNCHED(ctx);
   ctx->lat_mean_extent = ctx->dev_mean_extent;
   ctx->lat_comm = nullptr;
-  st = ow_lattice_dev_count(ctx, f, passes, leaves, d_nl, nl_cap, d_coords, n_faces, p->lattice_dirs, Q, flags, s);
+  // (k_lat_pos also writes the int64 leaf output)
+  st = ow_lattice_dev_count(ctx, f, passes, leaves, d_nl, nl_cap, d_coords, n_faces, p->lattice_dirs, Q, flags, s,
+                            leaves64);
   ctx->lat_mean_extent = 0.0f;
   OW_TRY(st);
   // (the caps the finish step checks against: the lattice lists as sized now)
