@@ -259,6 +259,15 @@ int ow_stage_times(ow_ctx* ctx, ow_nearwall_result* out);
 // ring state per pass (int64 words, see ow_refine_dev)
 enum { RS_INTER = 0, RS_OVER, RS_MARKED, RS_SPLITS, RS_RESUME, RS_OVER_FIRST, RS_NR = 8, RS_CR = 36, RS_WORDS = 64 };
 constexpr int RS_MAX_ITERS = 26;
+// 2:1 violator sweeps after splitting the MARKED leaves of `level` (children
+// at level + 1; the forest was balanced before): a violator of a block at
+// depth c has depth < c - 1, so sweep k (k >= 1) can only find leaves at depth
+// <= level - k — at most `level` sweeps find any, one more verifies that none
+// is left (the driver re-runs on the host path if it finds one).  Level 0
+// needs none: no leaf is shallower than 0.
+__host__ __device__ __forceinline__ int refine_sweeps(int level) {
+  return level == 0 ? 0 : (level + 1 < RS_MAX_ITERS ? level + 1 : RS_MAX_ITERS);
+}
 // device-driven forest steps of the native driver (ow_forest.cu)
 int ow_forest_leaves_dev(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t* d_out, int64_t* d_count,
                          cudaStream_t s, const int64_t* d_nb = nullptr);

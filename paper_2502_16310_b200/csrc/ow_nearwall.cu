@@ -773,7 +773,11 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   OW_PROF_BEGIN(ctx, PROF_MARK, s);
   // persistent past 4 waves (k_mark_blocks strides over the device leaf count)
   const int64_t nblk = (n_leaves + MARK_WARPS - 1) / MARK_WARPS;
-  dim3 grd((unsigned)(nblk < 24 * OW_SMS ? nblk : 24 * OW_SMS));
+  static const int64_t per_sm = [] {  // CTAs per SM of the block pass grid (OW_MARK_CTAS_PER_SM: A/B)
+    const char* e = getenv("OW_MARK_CTAS_PER_SM");
+    return e && atoi(e) > 0 ? (int64_t)atoi(e) : (int64_t)24;
+  }();
+  dim3 grd((unsigned)(nblk < per_sm * OW_SMS ? nblk : per_sm * OW_SMS));
   const int gi = 8 * OW_SMS;
   if (f->dim == 3) {
     if (binned) {

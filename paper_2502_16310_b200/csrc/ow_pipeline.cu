@@ -132,11 +132,11 @@ __global__ void k_drv_summary(const int64_t* drv, const unsigned long long* stat
   ow_pdl_wait();
   for (int p = threadIdx.x; p < passes; p += blockDim.x) {
     const int64_t* rs = drv + 72 * p + 8;
-    const int it = p + 2 < RS_MAX_ITERS ? p + 2 : RS_MAX_ITERS;
+    const int it = refine_sweeps(p);
     int64_t* o = sum + SUM_W * p;
     for (int k = 0; k < 6; ++k) o[k] = rs[k];
     o[6] = rs[RS_NR + it + 1];
-    o[7] = rs[RS_CR + it];
+    o[7] = it > 0 ? rs[RS_CR + it] : 0;  // (the last violator sweep's list; none at level 0)
     for (int k = 0; k < 5; ++k) o[8 + k] = (int64_t)stats[5 * p + k];
   }
 }
@@ -388,7 +388,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
     // splits that would not fit the current capacity are detected on the device
     // and finished below on the host path, which grows the forest
     // a cascade of splits descends at least one level per sweep
-    const int iters = level + 2 < RS_MAX_ITERS ? level + 2 : RS_MAX_ITERS;
+    const int iters = refine_sweeps(level);
     OW_TRY(ow_refine_dev(ctx, f, level, iters, rs, s, d_nb));
     OW_TRY(record(se, level, 4, s, ctx->no_stage_events));
     if (dev) {
@@ -406,7 +406,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
       return OW_ERR_INVALID;
     }
     int64_t n_split = h[3], n_marked = h[2];
-    const int64_t n_final = h[8 + iters + 1], last_cnt = h[36 + iters];
+    const int64_t n_final = h[8 + iters + 1], last_cnt = iters > 0 ? h[36 + iters] : 0;
     if (h[1] && h[5]) {
       // the MARKED list itself did not fit: refine synchronously (grows the forest)
       OW_TRY(ow_refine_marked_counted(ctx, f, level, &n_split, &n_marked, s));
