@@ -260,21 +260,23 @@ int ow_stage_times(ow_ctx* ctx, ow_nearwall_result* out);
 enum { RS_INTER = 0, RS_OVER, RS_MARKED, RS_SPLITS, RS_RESUME, RS_OVER_FIRST, RS_NR = 8, RS_CR = 36, RS_WORDS = 64 };
 constexpr int RS_MAX_ITERS = 26;
 // 2:1 violator sweeps after splitting the MARKED leaves of `level` (children
-// at level + 1; the forest was balanced before): a violator of a block at
-// depth c has depth < c - 1, so sweep k (k >= 1) can only find leaves at depth
-// <= level - k — at most `level` sweeps find any, one more verifies that none
-// is left (the driver re-runs on the host path if it finds one).  Level 0
-// needs none: no leaf is shallower than 0.
+// at level + 1): a violator of a block at depth c has depth < c - 1, and the
+// children of a violator at depth v are at depth v + 1, so sweep k (k >= 1) can
+// only find leaves at depth <= level - k.  `level` sweeps therefore finish
+// every cascade (none at level 0: no leaf is shallower than 0); only a level
+// past RS_MAX_ITERS needs the last sweep's list checked (then the host path
+// finishes the cascade).
 __host__ __device__ __forceinline__ int refine_sweeps(int level) {
-  return level == 0 ? 0 : (level + 1 < RS_MAX_ITERS ? level + 1 : RS_MAX_ITERS);
+  return level < RS_MAX_ITERS ? level : RS_MAX_ITERS;
 }
+__host__ __device__ __forceinline__ bool refine_sweeps_exact(int level) { return level < RS_MAX_ITERS; }
 // device-driven forest steps of the native driver (ow_forest.cu)
 int ow_forest_leaves_dev(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t* d_out, int64_t* d_count,
                          cudaStream_t s, const int64_t* d_nb = nullptr);
 int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, const int64_t* d_n, int64_t n_bound,
                      int32_t rounds, cudaStream_t s, bool tags = false);
 int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64_t* d_st, cudaStream_t s,
-                  int64_t* d_nb = nullptr);
+                  int64_t* d_nb = nullptr, int32_t* next_leaves = nullptr, int64_t* next_count = nullptr);
 int ow_rebalance_host(ow_ctx* ctx, ow_forest* f, int64_t f0, int64_t* n_split, cudaStream_t s);
 
 // refine_marked returning the MARKED-leaf count of the split pass as well

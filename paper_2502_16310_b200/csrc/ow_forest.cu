@@ -378,8 +378,11 @@ __global__ void k_rs_init(int64_t* st, int64_t n, const int64_t* nd, uint8_t* fl
 // n[k] + 2^D r + ci; one thread publishes n[k+1].  A list that does not fit
 // the capacity is dropped (n[k+1] = n[k]) and the frontier to resume from is
 // recorded; the MARKED list (k = 0) is not split beyond max_level.
+// next_leaves / next_count (device-resident loop, k = 0): the children of
+// this split are exactly the leaves of level + 1 at the next marking pass, a
+// contiguous id range in ascending order — written here, no compaction
 __global__ void k_split_ring(ow_forest f, const int32_t* __restrict__ list, int64_t* st, int k, int beyond_max,
-                             int64_t* nb_out) {
+                             int64_t* nb_out, int32_t* next_leaves, int64_t* next_count) {
   ow_pdl_wait();
   const int nc = 1 << f.dim;
   const int64_t base = st[RS_NR + k];
@@ -401,6 +404,7 @@ __global__ void k_split_ring(ow_forest f, const int32_t* __restrict__ list, int6
       st[RS_RESUME] = base;  // frontier of the newest children
     }
     if (nb_out) *nb_out = st[RS_NR + k + 1];
+    if (next_count) *next_count = over ? 0 : nc * m;
   }
   if (over) return;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m * nc; t += (int64_t)gridDim.x * blockDim.x) {
@@ -408,6 +412,7 @@ __global__ void k_split_ring(ow_forest f, const int32_t* __restrict__ list, int6
     const int ci = (int)(t % nc);
     const int p = list[r];
     const int64_t id = base + t;
+    if (next_leaves) next_leaves[t] = (int32_t)id;
     f.d_level[id] = (int16_t)(f.d_level[p] + 1);
     for (int a = 0; a < f.dim; ++a) f.d_coord[a][id] = 2 * f.d_coord[a][p] + ((ci >> a) & 1);
     f.d_parent[id] = p;
@@ -536,7 +541,7 @@ int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, c
 // final count written back to *d_nb, so f->n_blocks is stale until the caller
 // reads it.
 int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64_t* d_st, cudaStream_t s,
-                  int64_t* d_nb) {
+                  int64_t* d_nb, int32_t* next_leaves, int64_t* next_count) {
   if (iters > RS_MAX_ITERS) iters = RS_MAX_ITERS;
   const int nc = 1 << f->dim;
   const int64_t n = f->n_blocks, cap = f->capacity;
@@ -550,7 +555,7 @@ int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64
   const ow_forest fv = *f;
   const int sg = ow_blocks(cap * nc, 256, 8 * OW_SMS);
   ow_launch(k_split_ring, sg, 256, 0, s, fv, (const int32_t*)pl, d_st, 0, level >= f->max_level,
-                                   iters == 0 ? d_nb : nullptr);
+            iters == 0 ? d_nb : nullptr, next_leaves, next_count);
   ctx->launches += 2;
   ForestC F = make_forestc(f);
   F.n = cap;
@@ -561,7 +566,8 @@ int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64
     // violator flags of blocks [0, n[k]) (n[k] on the device; 0 after a sweep without splits)
     OW_TRY(scan01(ctx, FlagLoad{(const uint8_t*)pf}, FlagCompactClear{(int32_t*)pl, (uint8_t*)pf}, cap,
                   d_st + RS_CR + k, s, scan_n));
-    ow_launch(k_split_ring, sg, 256, 0, s, fv, (const int32_t*)pl, d_st, k, 0, k == iters ? d_nb : nullptr);
+    ow_launch(k_split_ring, sg, 256, 0, s, fv, (const int32_t*)pl, d_st, k, 0, k == iters ? d_nb : nullptr,
+              (int32_t*)nullptr, (int64_t*)nullptr);
     ctx->launches += 2;
   }
   OW_PROF_END(ctx, PROF_REFINE, s);

@@ -136,7 +136,7 @@ __global__ void k_drv_summary(const int64_t* drv, const unsigned long long* stat
     int64_t* o = sum + SUM_W * p;
     for (int k = 0; k < 6; ++k) o[k] = rs[k];
     o[6] = rs[RS_NR + it + 1];
-    o[7] = it > 0 ? rs[RS_CR + it] : 0;  // (the last violator sweep's list; none at level 0)
+    o[7] = refine_sweeps_exact(p) ? 0 : rs[RS_CR + it];  // (a cascade the sweeps may not have finished)
     for (int k = 0; k < 5; ++k) o[8 + k] = (int64_t)stats[5 * p + k];
   }
 }
@@ -319,7 +319,9 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
       // sharded marking on the device: slices balanced by per-leaf work, the
       // rank marks its slice, then the marks and the statistics are exchanged
       // over peer memory (ow_comm.cu) — no host round trip
-      OW_TRY(ow_forest_leaves_dev(ctx, f, level, (int32_t*)pl, dn, s, d_nb));
+      // (device-resident loop: the leaves of level >= 1 were written by the
+      // previous level's split, ow_refine_dev next_leaves)
+      if (level == 0 || !dev) OW_TRY(ow_forest_leaves_dev(ctx, f, level, (int32_t*)pl, dn, s, d_nb));
       void* psl;
       OW_TRY(ow_slot(ctx, SLOT_DRV_SLICE, 8 * (size_t)(n_host + 8), s, &psl));
       int64_t* wpre = (int64_t*)psl + 8;
@@ -363,8 +365,9 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
       OW_CUDA(cudaStreamSynchronize(s));
     } else {
       // leaf count stays on the device: marking is launched for n_host blocks
-      // (an upper bound) and every warp checks the exact count
-      OW_TRY(ow_forest_leaves_dev(ctx, f, level, (int32_t*)pl, dn, s, d_nb));
+      // (an upper bound) and every warp checks the exact count (the leaves of
+      // level >= 1 were written by the previous level's split)
+      if (level == 0 || !dev) OW_TRY(ow_forest_leaves_dev(ctx, f, level, (int32_t*)pl, dn, s, d_nb));
       OW_TRY(ow_mark_launch(ctx, f, (const int32_t*)pl, n_host, d_coords, n_faces, geom_key,
                             p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
                             p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
@@ -389,7 +392,10 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
     // and finished below on the host path, which grows the forest
     // a cascade of splits descends at least one level per sweep
     const int iters = refine_sweeps(level);
-    OW_TRY(ow_refine_dev(ctx, f, level, iters, rs, s, d_nb));
+    // device-resident loop: the split of this level's MARKED leaves writes the
+    // next level's leaf list (its children, a contiguous id range) and count
+    int64_t* next_count = !dev ? nullptr : (level + 1 < passes ? (int64_t*)drv + 72 * (level + 1) : d_sum + SUM_W * passes);
+    OW_TRY(ow_refine_dev(ctx, f, level, iters, rs, s, d_nb, dev ? (int32_t*)pl : nullptr, next_count));
     OW_TRY(record(se, level, 4, s, ctx->no_stage_events));
     if (dev) {
       out->n_passes = level + 1;
@@ -406,7 +412,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
       return OW_ERR_INVALID;
     }
     int64_t n_split = h[3], n_marked = h[2];
-    const int64_t n_final = h[8 + iters + 1], last_cnt = iters > 0 ? h[36 + iters] : 0;
+    const int64_t n_final = h[8 + iters + 1], last_cnt = refine_sweeps_exact(level) ? 0 : h[36 + iters];
     if (h[1] && h[5]) {
       // the MARKED list itself did not fit: refine synchronously (grows the forest)
       OW_TRY(ow_refine_marked_counted(ctx, f, level, &n_split, &n_marked, s));
@@ -420,10 +426,8 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
     out->n_passes = level + 1;
   }
   if (dev && passes > 0) {
-    // leaves of the deepest level (the lattice level whenever the last pass split)
-    void* pl;
-    OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(f->capacity + 1), s, &pl));
-    OW_TRY(ow_forest_leaves_dev(ctx, f, passes, (int32_t*)pl, d_sum + SUM_W * passes, s, d_nb));
+    // (the leaves of the deepest level, the lattice level whenever the last
+    // pass split, were written by that pass's split into SLOT_DRV_LEAVES)
     ow_launch(k_drv_summary, 1, 32, 0, s, (const int64_t*)drv, (const unsigned long long*)stats, passes, d_sum);
     OW_LAUNCHED(ctx);
   }
