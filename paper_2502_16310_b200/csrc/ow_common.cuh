@@ -274,9 +274,10 @@ __host__ __device__ __forceinline__ bool refine_sweeps_exact(int level) { return
 int ow_forest_leaves_dev(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t* d_out, int64_t* d_count,
                          cudaStream_t s, const int64_t* d_nb = nullptr);
 int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, const int64_t* d_n, int64_t n_bound,
-                     int32_t rounds, cudaStream_t s, bool tags = false);
+                     int32_t rounds, cudaStream_t s, bool tags = false, bool defer_promote = false);
 int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64_t* d_st, cudaStream_t s,
-                  int64_t* d_nb = nullptr, int32_t* next_leaves = nullptr, int64_t* next_count = nullptr);
+                  int64_t* d_nb = nullptr, int32_t* next_leaves = nullptr, int64_t* next_count = nullptr,
+                  const int32_t* promote_leaves = nullptr, const int64_t* promote_n = nullptr);
 int ow_rebalance_host(ow_ctx* ctx, ow_forest* f, int64_t f0, int64_t* n_split, cudaStream_t s);
 
 // refine_marked returning the MARKED-leaf count of the split pass as well
@@ -299,7 +300,20 @@ int ow_faces_settle(ow_ctx* ctx, const int64_t* h6, cudaStream_t s);
 void ow_face_summary_from(const int64_t* h, int64_t n, ow_face_summary* out);
 int ow_face_check_launch(ow_ctx* ctx, int32_t dim, const float* d_coords, int64_t n, int64_t* dst, cudaStream_t s);
 int ow_stl_to_soa_checked(ow_ctx* ctx, const uint8_t* d_records, int64_t n, float* d_coords, int64_t* dst,
-                          cudaStream_t s);
+                          cudaStream_t s, bool init_summary = true);
+// the face summary's initial words (as k_face_check_init), for a kernel that
+// initialises them itself (the fused pass's first kernel)
+__device__ __forceinline__ void ow_face_summary_init_words(int64_t* small) {
+  small[0] = -1;  // 0xfff.. as unsigned = "none"
+  small[1] = -1;
+  float* fs = (float*)(small + 2);
+  for (int a = 0; a < 3; ++a) {
+    fs[a] = INFINITY;
+    fs[3 + a] = -INFINITY;
+  }
+  fs[6] = 0.0f;
+  fs[7] = 0.0f;
+}
 
 // bracket device work of kernel family `id` with events when profiling is on
 void ow_prof_mark(ow_ctx* ctx, int id, int end, cudaStream_t s);

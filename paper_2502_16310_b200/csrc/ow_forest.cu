@@ -357,8 +357,18 @@ namespace {
 
 // refine state init (CTA 0) and the violator flags cleared (grid-stride, 16
 // bytes per store: flag is 8-byte aligned scratch of cap + 8 bytes)
-__global__ void k_rs_init(int64_t* st, int64_t n, const int64_t* nd, uint8_t* flag, int64_t cap) {
+// (+ the deferred last promote of the level's propagation rounds: round tags
+// of the leaves -> MARKED, ow_propagate_dev)
+__global__ void k_rs_init(int64_t* st, int64_t n, const int64_t* nd, uint8_t* flag, int64_t cap,
+                          int8_t* marks, const int32_t* __restrict__ promote_leaves, const int64_t* promote_n) {
   ow_pdl_wait();
+  if (promote_leaves) {
+    const int64_t pn = *promote_n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pn; i += (int64_t)gridDim.x * blockDim.x) {
+      const int id = promote_leaves[i];
+      if (marks[id] >= OW_INTERMEDIATE) marks[id] = OW_MARKED;
+    }
+  }
   if (blockIdx.x == 0) {
     if (nd) n = *nd;
     for (int i = threadIdx.x; i < RS_WORDS; i += blockDim.x) st[i] = 0;
@@ -506,7 +516,7 @@ int ow_forest_leaves_dev(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t
 }
 
 int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, const int64_t* d_n, int64_t n_bound,
-                     int32_t rounds, cudaStream_t s, bool tags) {
+                     int32_t rounds, cudaStream_t s, bool tags, bool defer_promote) {
   if (n_bound <= 0 || rounds <= 0) return OW_OK;
   ForestC F = make_forestc(f);
   OW_PROF_BEGIN(ctx, PROF_PROP, s);
@@ -519,7 +529,7 @@ int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, c
     ow_launch(k_prop_gather_dev, ow_blocks(n_bound, 128, 16 * OW_SMS), 128, 0, s, F, d_leaves, d_n, tag,
               tags ? tag : 0);
     ctx->launches += 1;
-    if (!tags || r % 100 == 99 || r + 1 == rounds) {
+    if (!tags || r % 100 == 99 || (r + 1 == rounds && !defer_promote)) {
       ow_launch(k_prop_promote_dev, ow_blocks(n_bound, 256, 8 * OW_SMS), 256, 0, s, F.marks, d_leaves, d_n);
       ctx->launches += 1;
     }
@@ -541,7 +551,8 @@ int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, c
 // final count written back to *d_nb, so f->n_blocks is stale until the caller
 // reads it.
 int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64_t* d_st, cudaStream_t s,
-                  int64_t* d_nb, int32_t* next_leaves, int64_t* next_count) {
+                  int64_t* d_nb, int32_t* next_leaves, int64_t* next_count, const int32_t* promote_leaves,
+                  const int64_t* promote_n) {
   if (iters > RS_MAX_ITERS) iters = RS_MAX_ITERS;
   const int nc = 1 << f->dim;
   const int64_t n = f->n_blocks, cap = f->capacity;
@@ -549,7 +560,8 @@ int ow_refine_dev(ow_ctx* ctx, ow_forest* f, int32_t level, int32_t iters, int64
   OW_TRY(ow_slot(ctx, SLOT_FOREST_LIST, 4 * (size_t)(cap + 1), s, &pl));
   OW_TRY(ow_slot(ctx, SLOT_FOREST_FLAG, (size_t)cap + 16, s, &pf));
   OW_PROF_BEGIN(ctx, PROF_REFINE, s);
-  ow_launch(k_rs_init, ow_blocks((cap + 15) / 16, 256, 2 * OW_SMS), 256, 0, s, d_st, n, d_nb, (uint8_t*)pf, cap);
+  ow_launch(k_rs_init, ow_blocks((cap + 15) / 16, 256, 2 * OW_SMS), 256, 0, s, d_st, n, d_nb, (uint8_t*)pf, cap,
+            f->d_marks, promote_leaves, promote_n);
   OW_TRY(scan01(ctx, SplitLoad{make_forestc(f), level, d_st + RS_INTER}, CompactStore{(int32_t*)pl},
                 d_nb ? cap : n, d_st + RS_CR, s, d_nb));
   const ow_forest fv = *f;

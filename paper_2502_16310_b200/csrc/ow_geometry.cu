@@ -287,13 +287,15 @@ void ow_face_summary_from(const int64_t* h, int64_t n, ow_face_summary* out) {
 
 // fused pass: STL records -> coordinates + the face check into d_small[dst, dst + 6)
 int ow_stl_to_soa_checked(ow_ctx* ctx, const uint8_t* d_records, int64_t n, float* d_coords, int64_t* dst,
-                          cudaStream_t s) {
+                          cudaStream_t s, bool init_summary) {
   if (n < 0 || (n > 0 && (!d_records || !d_coords)) || ((uintptr_t)d_records & 1) != 0) {
     ow_set_error("ow_stl_binary_to_soa: bad arguments (records must be 2-byte aligned)");
     return OW_ERR_INVALID;
   }
-  ow_launch(k_face_check_init, 1, 1, 0, s, dst);
-  OW_LAUNCHED(ctx);
+  if (init_summary) {  // (else the caller initialised the summary words: ow_face_summary_init_words)
+    ow_launch(k_face_check_init, 1, 1, 0, s, dst);
+    OW_LAUNCHED(ctx);
+  }
   if (n > 0) {
     OW_PROF_BEGIN(ctx, PROF_STL, s);
     ow_launch(k_stl_to_soa_check, ow_blocks(n, STL_TILE, 8 * OW_SMS), STL_TILE, 0, s, (const uint16_t*)d_records, n,

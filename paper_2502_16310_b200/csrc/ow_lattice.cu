@@ -109,6 +109,16 @@ struct LatArgs {
   int64_t out_row_cap, out_link_cap;
 };
 
+// d_small[48..53) = 0 (row / hit / statistics / link counters, face queue)
+// and the dense lattice table (int32, slot 16-byte aligned, 4 words per uint4)
+// filled with -1
+__global__ void k_lat_init(int64_t* counters, uint4* grid, int64_t n4) {
+  ow_pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x < 5) counters[threadIdx.x] = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
+    grid[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+}
+
 template <int D>
 __global__ void k_lat_pos(ForestC F, int level, const int32_t* __restrict__ leaves, int64_t n, int32_t* pos_of,
                           uint8_t* has_pair, float* cen, int32_t* grid, int g0, int g1, const int64_t* d_n,
@@ -1415,11 +1425,15 @@ int lat_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_l
     ctx->lat_grid_on = cells <= (int64_t(1) << 26) && !getenv("OW_LAT_NO_GRID");
     if (ctx->lat_grid_on) OW_TRY(ow_slot(ctx, SLOT_LAT_GRID, 4 * (size_t)cells, s, &p));
   }
-  OW_TRY(ow_fill_async(ctx, ctx->d_small + 48, 0, 5 * 8, s));
   if (!d_nl) OW_TRY(ow_fill_async(ctx, d_flags, 0, 4 * (size_t)n_leaves * C, s));
   OW_PROF_BEGIN(ctx, PROF_LATTICE, s);
   LatArgs A = make_args(ctx);
-  if (A.grid) OW_TRY(ow_fill_async(ctx, A.grid, 0xFF, 4 * (size_t)A.gdim[0] * A.gdim[1] * A.gdim[2], s));
+  {  // the sweep's counters cleared and the dense lattice table set to -1, one launch
+    const int64_t cells = A.grid ? (int64_t)A.gdim[0] * A.gdim[1] * A.gdim[2] : 0;
+    ow_launch(k_lat_init, ow_blocks((cells + 3) / 4, 256, 8 * OW_SMS), 256, 0, s, ctx->d_small + 48,
+              reinterpret_cast<uint4*>(A.grid), (cells + 3) / 4);
+    OW_LAUNCHED(ctx);
+  }
   uint4* zf = d_nl ? reinterpret_cast<uint4*>(d_flags) : nullptr;
   if (D == 3) ow_launch(k_lat_pos<3>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1], d_nl, zf, widen_out);
   else ow_launch(k_lat_pos<2>, ow_blocks(nl, 256, 8 * OW_SMS), 256, 0, s, A.F, level, d_leaves, nl, A.pos_of, A.has_pair, A.cen, A.grid, A.gdim[0], A.gdim[1], d_nl, zf, widen_out);

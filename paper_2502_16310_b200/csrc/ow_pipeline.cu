@@ -18,8 +18,9 @@ namespace {
 
 using ow::scan;
 
-__global__ void k_root_init(ow_forest f, int64_t r) {
+__global__ void k_root_init(ow_forest f, int64_t r, int64_t* face_summary) {
   ow_pdl_wait();
+  if (face_summary && blockIdx.x == 0 && threadIdx.x == 0) ow_face_summary_init_words(face_summary);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= r) return;
   int64_t rem = i;
@@ -128,22 +129,27 @@ __global__ void k_slice_bounds(const int64_t* __restrict__ e, const int64_t* d_n
 constexpr int SUM_W = 13;  // [0..6) RS_INTER..RS_OVER_FIRST, [6] final blocks, [7] last sweep's list, [8..13) stats
 constexpr int DRV_RETRY = 1000;  // internal: rerun the pass with per-level host sync
 
+// the SUM_W summary words of pass p from its ring state and statistics
+template <class Out>
+__device__ __forceinline__ void drv_summary_pass(const int64_t* drv, const unsigned long long* stats, int p, Out o) {
+  const int64_t* rs = drv + 72 * p + 8;
+  const int it = refine_sweeps(p);
+  for (int k = 0; k < 6; ++k) o[k] = rs[k];
+  o[6] = rs[RS_NR + it + 1];
+  o[7] = refine_sweeps_exact(p) ? 0 : rs[RS_CR + it];  // (a cascade the sweeps may not have finished)
+  for (int k = 0; k < 5; ++k) o[8 + k] = (int64_t)stats[5 * p + k];
+}
+
 __global__ void k_drv_summary(const int64_t* drv, const unsigned long long* stats, int passes, int64_t* sum) {
   ow_pdl_wait();
-  for (int p = threadIdx.x; p < passes; p += blockDim.x) {
-    const int64_t* rs = drv + 72 * p + 8;
-    const int it = refine_sweeps(p);
-    int64_t* o = sum + SUM_W * p;
-    for (int k = 0; k < 6; ++k) o[k] = rs[k];
-    o[6] = rs[RS_NR + it + 1];
-    o[7] = refine_sweeps_exact(p) ? 0 : rs[RS_CR + it];  // (a cascade the sweeps may not have finished)
-    for (int k = 0; k < 5; ++k) o[8 + k] = (int64_t)stats[5 * p + k];
-  }
+  for (int p = threadIdx.x; p < passes; p += blockDim.x) drv_summary_pass(drv, stats, p, sum + SUM_W * p);
 }
 
 }  // namespace
 
-extern "C" int ow_forest_init_root(ow_ctx* ctx, ow_forest* f, void* stream) {
+namespace {
+// root grid (+ the fused pass's face summary words initialised in the same launch)
+int init_root(ow_ctx* ctx, ow_forest* f, void* stream, int64_t* face_summary) {
   cudaStream_t s = (cudaStream_t)stream;
   int64_t r = 1;
   for (int a = 0; a < f->dim; ++a) r *= f->root[a];
@@ -152,11 +158,16 @@ extern "C" int ow_forest_init_root(ow_ctx* ctx, ow_forest* f, void* stream) {
                  (long long)f->capacity);
     return OW_ERR_INVALID;
   }
-  ow_launch(k_root_init, ow_blocks(r, 256), 256, 0, s, *f, r);
+  ow_launch(k_root_init, ow_blocks(r, 256), 256, 0, s, *f, r, face_summary);
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
   f->n_blocks = r;
   return OW_OK;
+}
+}  // namespace
+
+extern "C" int ow_forest_init_root(ow_ctx* ctx, ow_forest* f, void* stream) {
+  return init_root(ctx, f, stream, nullptr);
 }
 
 namespace {
@@ -376,15 +387,17 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
     }
     // ---- propagation (binned only): 1 + floor(d / min block length)
     OW_TRY(record(se, level, 2, s, ctx->no_stage_events));
+    int rounds = 0;
     if (p->binned) {
       double bl = INFINITY;
       for (int a = 0; a < f->dim; ++a) {
         const double b = f->dext[a] / (double)((int64_t)f->root[a] << level);
         bl = b < bl ? b : bl;
       }
-      const int rounds = 1 + (int)floor(p->d_spec64 / bl);
+      rounds = 1 + (int)floor(p->d_spec64 / bl);
       // (the device-resident loop starts from a fresh root grid: round tags)
-      OW_TRY(ow_propagate_dev(ctx, f, (const int32_t*)pl, dn, n_host, rounds, s, dev));
+      // (its last promote is deferred into the refine's init kernel)
+      OW_TRY(ow_propagate_dev(ctx, f, (const int32_t*)pl, dn, n_host, rounds, s, dev, dev));
     }
     // ---- refinement on the device; one readback of its state per level
     OW_TRY(record(se, level, 3, s, ctx->no_stage_events));
@@ -395,7 +408,8 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
     // device-resident loop: the split of this level's MARKED leaves writes the
     // next level's leaf list (its children, a contiguous id range) and count
     int64_t* next_count = !dev ? nullptr : (level + 1 < passes ? (int64_t*)drv + 72 * (level + 1) : d_sum + SUM_W * passes);
-    OW_TRY(ow_refine_dev(ctx, f, level, iters, rs, s, d_nb, dev ? (int32_t*)pl : nullptr, next_count));
+    OW_TRY(ow_refine_dev(ctx, f, level, iters, rs, s, d_nb, dev ? (int32_t*)pl : nullptr, next_count,
+                         dev && p->binned && rounds > 0 ? (const int32_t*)pl : nullptr, dn));
     OW_TRY(record(se, level, 4, s, ctx->no_stage_events));
     if (dev) {
       out->n_passes = level + 1;
@@ -427,9 +441,12 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
   }
   if (dev && passes > 0) {
     // (the leaves of the deepest level, the lattice level whenever the last
-    // pass split, were written by that pass's split into SLOT_DRV_LEAVES)
-    ow_launch(k_drv_summary, 1, 32, 0, s, (const int64_t*)drv, (const unsigned long long*)stats, passes, d_sum);
-    OW_LAUNCHED(ctx);
+    // pass split, were written by that pass's split into SLOT_DRV_LEAVES; a
+    // device-sized pass forms the summary in its own last kernel)
+    if (!devpass) {
+      ow_launch(k_drv_summary, 1, 32, 0, s, (const int64_t*)drv, (const unsigned long long*)stats, passes, d_sum);
+      OW_LAUNCHED(ctx);
+    }
   }
   return OW_OK;
   };  // device_part
@@ -765,10 +782,12 @@ constexpr int G2G_WORDS = 34;  // [0, 8) bins, [8, 28) lattice (d_small 33..52),
 // every word the host needs, written straight into mapped pinned host memory
 // (no copy-engine transfer after the last kernel): the driver summary, then
 // the bin, lattice and face words
-__global__ void k_g2g_summary(const int64_t* __restrict__ small, const int64_t* __restrict__ sum, int n_sum,
-                              volatile int64_t* dst) {
+__global__ void k_g2g_summary(const int64_t* __restrict__ small, const int64_t* __restrict__ drv,
+                              const unsigned long long* __restrict__ stats, int passes, volatile int64_t* dst) {
   ow_pdl_wait();
-  for (int i = threadIdx.x; i < n_sum; i += blockDim.x) dst[i] = sum[i];
+  for (int p = threadIdx.x; p < passes; p += blockDim.x) drv_summary_pass(drv, stats, p, dst + SUM_W * p);
+  const int n_sum = SUM_W * passes + 1;
+  if (threadIdx.x == 0) dst[n_sum - 1] = drv[72 * passes + 8 + SUM_W * passes];  // the deepest level's leaves
   volatile int64_t* t = dst + n_sum;
   const int k = threadIdx.x;
   if (k < 8) t[k] = small[k];
@@ -856,9 +875,13 @@ int g2g_submit(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n
   t->d_qp = d_qp;
   // ---- the pass, enqueued without a host round trip
   if (p->copy_done) OW_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)p->copy_done, 0));
-  if (d_records && D == 3) OW_TRY(ow_stl_to_soa_checked(ctx, d_records, n_faces, d_coords, ctx->d_small + 56, s));
-  else OW_TRY(ow_face_check_launch(ctx, D, d_coords, n_faces, ctx->d_small + 56, s));
-  OW_TRY(ow_forest_init_root(ctx, f, s));
+  if (d_records && D == 3) {  // root grid + face summary words in one launch, then the fused import
+    OW_TRY(init_root(ctx, f, s, ctx->d_small + 56));
+    OW_TRY(ow_stl_to_soa_checked(ctx, d_records, n_faces, d_coords, ctx->d_small + 56, s, false));
+  } else {
+    OW_TRY(ow_face_check_launch(ctx, D, d_coords, n_faces, ctx->d_small + 56, s));
+    OW_TRY(ow_forest_init_root(ctx, f, s));
+  }
   ow_nearwall_params nw = p->nw;
   nw.reach = predicted_reach(f, &p->nw);
   t->reach_pred = nw.reach;
@@ -892,7 +915,8 @@ int g2g_submit(ow_ctx* ctx, const uint8_t* d_records, float* d_coords, int64_t n
   OW_TRY(ow_lattice_dev_emit(ctx, (int64_t*)p->out_buf[OW_OUT_CELLS], (float*)p->out_buf[OW_OUT_Q], row_cap, d_rows,
                              d_qp, link_cap, ncb_grid, s));
   // ---- every count the host needs, stored into this pass's pinned area
-  ow_launch(k_g2g_summary, 1, 128, 0, s, (const int64_t*)ctx->d_small, (const int64_t*)d_sum, SUM_W * passes + 1,
+  ow_launch(k_g2g_summary, 1, 128, 0, s, (const int64_t*)ctx->d_small, (const int64_t*)drv,
+            (const unsigned long long*)ctx->slot_ptr[SLOT_DRV_STATS], passes,
             (volatile int64_t*)(ctx->g2g_ring_dev + (t->area - ctx->g2g_ring)));
   OW_LAUNCHED(ctx);
   OW_CHECK_LAUNCH();
