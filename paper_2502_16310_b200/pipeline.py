@@ -188,6 +188,16 @@ class GridPlan:
         if self.dirs is not None:
             self._gp0.alloc = self._alloc_cb
 
+    def __del__(self):
+        # a submitted pass holds a ticket on the context: finish it (its
+        # results are dropped with the plan)
+        pend = getattr(self, "_pending", None)
+        if pend is not None:
+            try:
+                pend.result()
+            except Exception:  # pragma: no cover - nothing to report to at collection time
+                pass
+
     def _new_out(self, what, nbytes):
         dt = _OUT_DTYPES[what]
         t = torch.empty(max(nbytes, 0) // (8 if dt in (torch.int64,) else 4), dtype=dt, device=self.dev)

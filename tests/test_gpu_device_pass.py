@@ -218,3 +218,41 @@ def test_run_async_two_plans_stream(ow):
     g.wait()
     _equal(_snapshot(g), refs[j][0], f"pass {j}")
     assert 1 in modes and 2 in modes
+
+
+def test_run_async_same_plan_and_in_flight_limit(ow):
+    """A plan's pending pass is finished before its next submit (results of
+    both equal synchronous passes); at most 8 passes may be in flight on one
+    context — a 9th submit raises, and the pending ones still finish exactly."""
+    import torch
+
+    from paper_2502_16310_b200 import pipeline, shapes
+
+    dom = ow.Aabb(np.zeros(3), np.ones(3))
+    params = ow.NearWallParams(d_spec=0.06, n_levels=3, bins_per_axis=8)
+    rec, n = _records(shapes.icosphere_triangles(3))
+    ref = _snapshot(pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19").run(rec, n))
+    plan = pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19", reuse_outputs=True, stage_times=False)
+    plan.run(rec, n)
+    p1 = plan.run_async(rec, n)
+    p2 = plan.run_async(rec, n)  # finishes p1 first
+    g1 = p1.result()
+    assert g1.device_sized == 1
+    g2 = p2.result()
+    torch.cuda.synchronize()
+    _equal(_snapshot(g2), ref, "same plan")
+    plans = [pipeline.GridPlan(dom, (8, 8, 8), params, "D3Q19", reuse_outputs=True, stage_times=False)
+             for _ in range(9)]
+    for p in plans:
+        p.run(rec, n)  # (sizes every plan's outputs)
+    pend = [p.run_async(rec, n) for p in plans[:8]]
+    with pytest.raises(ow.InvalidParameterError, match="in flight"):
+        plans[8].run_async(rec, n)
+    for q in pend:
+        g = q.result()
+        assert g.device_sized == 1
+    torch.cuda.synchronize()
+    _equal(_snapshot(g), ref, "after the in-flight limit")
+    g9 = plans[8].run(rec, n)
+    torch.cuda.synchronize()
+    _equal(_snapshot(g9), ref, "the refused plan afterwards")
