@@ -40,6 +40,8 @@ __global__ void k_graph_begin(unsigned long long* base, unsigned long long* stat
 }
 }  // namespace
 
+void loop_key_slots(GraphKey* k, const ow_ctx* ctx);
+
 void make_loop_key(GraphKey* k, const ow_ctx* ctx, const ow_forest* f, const float* d_coords, int64_t n_faces,
                    const ow_grid* grid, const ow_nearwall_params* p, const int32_t* ids, const int32_t* counts,
                    const int32_t* offsets, int64_t E, const void* stats, const void* drv) {
@@ -56,10 +58,32 @@ void make_loop_key(GraphKey* k, const ow_ctx* ctx, const ow_forest* f, const flo
   k->stats = stats;
   k->drv = drv;
   k->dev = ctx->dev_pass ? 1 : 0;
+  loop_key_slots(k, ctx);
+}
+
+// scratch slots the captured loop never touches (the lattice stage and the
+// cell-face links run after it): left out of the key, so their growth after
+// the loop does not defeat the capture of the next pass
+static bool slot_outside_loop(int i) {
+  switch (i) {
+    case SLOT_SCAN_STATUS_G:  // (allocated by the capture itself)
+    case SLOT_LINK_CNT: case SLOT_LINK_OFF: case SLOT_LINK_CELLOFF: case SLOT_LINK_LEAVES:
+    case SLOT_LAT_BCOUNT: case SLOT_LAT_BOFFS: case SLOT_LAT_LEAVES: case SLOT_LAT_RANK: case SLOT_LAT_POS:
+    case SLOT_LAT_HAS: case SLOT_LAT_CEN: case SLOT_LAT_REC: case SLOT_LAT_ROWS: case SLOT_LAT_ROWOFF:
+    case SLOT_LAT_TILEROW: case SLOT_LAT_HITS: case SLOT_LAT_HITDIR: case SLOT_LAT_TILEHITS: case SLOT_LAT_IHITS:
+    case SLOT_LAT_IHITDIR: case SLOT_LAT_BMASK: case SLOT_LAT_HCOUNT: case SLOT_LAT_HOFFS: case SLOT_LAT_RFLAGS:
+    case SLOT_LAT_QPACK: case SLOT_LAT_GRID: case SLOT_MISC:
+      return true;
+    default:
+      return false;
+  }
+}
+
+void loop_key_slots(GraphKey* k, const ow_ctx* ctx) {
   for (int i = 0; i < SLOT_COUNT; ++i) {
-    if (i == SLOT_SCAN_STATUS_G) continue;  // (allocated by the capture itself)
-    k->slot_ptr[i] = ctx->slot_ptr[i];
-    k->slot_bytes[i] = ctx->slot_bytes[i];
+    const bool out = slot_outside_loop(i);
+    k->slot_ptr[i] = out ? nullptr : ctx->slot_ptr[i];
+    k->slot_bytes[i] = out ? 0 : ctx->slot_bytes[i];
   }
 }
 
@@ -98,13 +122,21 @@ int ow_loop_graph(ow_ctx* ctx, bool ok, const GraphKey* key, cudaStream_t* ps, c
   for (int i = 0; i < NG; ++i)
     if (memcmp(ctx->eager_key[i], key, sizeof(GraphKey)) == 0) ek = i;
   if (ek < 0) {
-    // first pass with these inputs: run eagerly (it sizes every scratch slot)
-    *ctx->eager_key[ctx->eager_next] = *key;
-    ctx->eager_next = (ctx->eager_next + 1) % NG;
-    return body();
+    // first pass with these inputs: run eagerly (it sizes every scratch slot);
+    // the key is recorded with the slots as this pass left them, so the next
+    // pass with the same inputs is captured even when this one grew scratch
+    if (getenv("OW_DEBUG_GRAPH")) fprintf(stderr, "ow graph: eager pass (dev=%d)\n", key->dev);
+    const int e = ctx->eager_next;
+    *ctx->eager_key[e] = *key;
+    ctx->eager_next = (e + 1) % NG;
+    const int st = body();
+    loop_key_slots(ctx->eager_key[e], ctx);
+    return st;
   }
   // second pass with the same inputs: capture the loop, then launch it
   memset(ctx->eager_key[ek], 0, sizeof(GraphKey));  // (one capture attempt per eager pass)
+  static const bool dbg = getenv("OW_DEBUG_GRAPH") != nullptr;
+  if (dbg) fprintf(stderr, "ow graph: capture attempt (dev=%d)\n", key->dev);
   if (!ctx->d_graph_epoch) {
     OW_CUDA(cudaMalloc((void**)&ctx->d_graph_epoch, 64));
     OW_CUDA(cudaMemsetAsync(ctx->d_graph_epoch, 0, 64, s));
@@ -137,6 +169,7 @@ int ow_loop_graph(ow_ctx* ctx, bool ok, const GraphKey* key, cudaStream_t* ps, c
   const bool good = st == OW_OK && ce == cudaSuccess && graph && !ctx->capture_failed &&
                     ctx->graph_site <= MAX_SITES;
   if (!good) {
+    if (dbg) fprintf(stderr, "ow graph: capture failed (%s)\n", ow_last_error());
     if (graph) cudaGraphDestroy(graph);
     ctx->launches = launches0;
     if (st != OW_OK && !ctx->capture_failed) return st;

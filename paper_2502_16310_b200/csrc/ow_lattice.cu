@@ -91,6 +91,7 @@ struct LatArgs {
   unsigned long long* ihit_d;  // device inline-hit counter (may exceed the capacity)
   unsigned long long* iru_d;   // inline (units << RU_ROW_BITS | rows), statistics
   int inline_units;            // rows of more cells go to k_lat_mt (OW_INLINE_UNITS overrides; tuning)
+  int lane_rows;               // batches whose rows have at most this many cells: a row per lane (0: off)
   int32_t* bcount;          // [n_cb] boundary cells per candidate block
   int32_t* hcount;          // [n_cb] boundary links (set flag bits) per candidate block
   int64_t* hoff;            // [n_cb] packed-q offsets
@@ -685,6 +686,74 @@ __global__ void __launch_bounds__(128) k_lat_faces(LatArgs A) {
       const int se = si - us;
       iru += ((unsigned long long)S << RU_ROW_BITS) + (unsigned long long)__popc(__ballot_sync(0xffffffffu, us > 0));
       if (!S) continue;
+      // Batches of short rows (every row at most lane_rows cells: the common
+      // case for faces far smaller than the finest blocks) skip the staging
+      // below: each lane tests its own row's cells, one per warp step, with
+      // the row's frame-permuted vertices and cell box in registers.
+      if (D == 3 && A.lane_rows > 0) {
+        const int umax = __reduce_max_sync(0xffffffffu, us);
+        if (umax <= A.lane_rows) {
+          float4 V[3];
+          int b0[3] = {0, 0, 0}, e0 = 1, e1 = 1, d = 0;
+          unsigned kx = 0, ky = 0, kz = 0;
+          const float* cp = A.cen;
+          if (us > 0) {
+            const unsigned w = (unsigned)row.z;
+            d = (int)(w & 31u);
+            const unsigned fr = s_frame[d];
+            kx = fr & 3u;
+            ky = (fr >> 2) & 3u;
+            kz = (fr >> 4) & 3u;
+            const float* F = reinterpret_cast<const float*>(s_face[wid][row.y - fbase]);
+            const float4 sh = s_shear[d];
+            V[0] = make_float4(F[kx], F[ky], F[kz], sh.x);
+            V[1] = make_float4(F[4 + kx], F[4 + ky], F[4 + kz], sh.y);
+            V[2] = make_float4(F[8 + kx], F[8 + ky], F[8 + kz], sh.z);
+            const unsigned k3[3] = {kx, ky, kz};
+            int ex[3];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              const unsigned ra = (w >> (5 + 4 * k3[q])) & 0xFu;  // i0 | (ext-1) << 2 of axis k3[q]
+              b0[q] = (int)(ra & 3u);
+              ex[q] = (int)(ra >> 2) + 1;
+            }
+            e0 = ex[0];
+            e1 = ex[1];
+            cp = A.cen + (int64_t)row.x * 12;
+          } else {
+            V[0] = V[1] = V[2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          }
+          for (int k = 0; k < umax; ++k) {
+            bool cand = false;
+            WtNum num{0.0f, 0.0f};
+            unsigned cellg = 0;
+            if (k < us) {
+              const int q0 = div_small(k, e0);
+              const int c0 = b0[0] + (k - q0 * e0);
+              const int j2 = div_small(q0, e1);
+              const int c1 = b0[1] + (q0 - j2 * e1), c2 = b0[2] + j2;
+              const float x0 = __ldg(cp + kx * 4 + c0), x1 = __ldg(cp + ky * 4 + c1), x2 = __ldg(cp + kz * 4 + c2);
+              cellg = (unsigned)row.x * (unsigned)C + (unsigned)(c0 << (2 * kx) | c1 << (2 * ky) | c2 << (2 * kz));
+              cand = wt_cand_perm(x0, x1, x2, V, num);
+            }
+            const unsigned cm = __ballot_sync(0xffffffffu, cand);
+            if (cm) {
+              if (cand) {
+                const int kk = nc + __popc(cm & lanemask_lt());
+                s_cnum[wid][kk] = num;
+                s_cmeta[wid][kk] = make_uint2(cellg, (unsigned)d);
+              }
+              nc += __popc(cm);
+              __syncwarp();
+              if (nc >= 32) {
+                nh = drain_cands(A, s_cnum[wid], s_cmeta[wid], nc, 32, s_hit[wid], s_hdir[wid], nh, lane);
+                nc -= 32;
+              }
+            }
+          }
+          continue;
+        }
+      }
       // Stage the batch's rows in the row's own watertight frame: the face's
       // vertices permuted to (kx, ky, kz) with the shears in .w, the leaf's
       // cell centres per permuted axis, and the cell box along the permuted
@@ -1319,6 +1388,13 @@ LatArgs make_args(ow_ctx* ctx) {
   A.ihit_d = (unsigned long long*)(ctx->d_small + 49);
   A.iru_d = (unsigned long long*)(ctx->d_small + 50);
   A.inline_units = inline_units_setting(ctx);
+  {
+    static const int lr = [] {  // OW_LAT_LANE_ROWS overrides (A/B)
+      const char* e = getenv("OW_LAT_LANE_ROWS");
+      return e ? atoi(e) : 0;
+    }();
+    A.lane_rows = lr;
+  }
   A.bcount = (int32_t*)ctx->slot_ptr[SLOT_LAT_BCOUNT];
   A.bmask = (unsigned long long*)ctx->slot_ptr[SLOT_LAT_BMASK];
   A.boff = (const int64_t*)ctx->slot_ptr[SLOT_LAT_BOFFS];
