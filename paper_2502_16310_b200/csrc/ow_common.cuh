@@ -232,7 +232,12 @@ int ow_comm_exchange_marks(ow_ctx* ctx, ow_comm* c, const int32_t* d_leaves, int
                            const int64_t* d_n, int64_t n_bound, unsigned long long* d_stats, int n_stats,
                            cudaStream_t s);
 
-// one marking pass without a host round trip: stats accumulate in d_out[0..2]
+// marking statistics per pass: [0] marked, [1] tests T, [2] evaluated,
+// [3] sphere tests, [4] box culls, [5] the pass's (block, chunk) item counter
+constexpr int MARK_STATS = 6;
+
+// one marking pass without a host round trip: stats accumulate in d_out[0..5)
+// (d_out[5]: the item counter, zero on entry like the statistics)
 int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves, const float* d_coords,
                    int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int32_t* d_bin_ids,
                    const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,

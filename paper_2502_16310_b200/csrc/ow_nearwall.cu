@@ -405,6 +405,7 @@ __device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M
                                            unsigned long long& marked) {
   constexpr int CPL = D == 3 ? 2 : 1;
   const int id = A.leaves[pos];
+  if (lane == 0) M.hit[pos] = 0u;  // (this warp owns the block's hit word in this kernel; k_mark_items reads it after)
   double blo[3], bhi[3];
   float p[CPL][3];
   int bin[CPL];
@@ -760,10 +761,10 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   A.d_slice = d_slice;
   MarkItems M;
   M.items = (int4*)pi;
-  M.n_items = (unsigned long long*)((unsigned*)ph + n_leaves + (n_leaves & 1));  // after the hit words
+  M.n_items = out + 5;  // (zeroed with the statistics; the hit words are cleared by k_mark_blocks per block)
   M.cap = cap;
   M.hit = (unsigned*)ph;
-  OW_TRY(ow_fill_async(ctx, ph, 0, 4 * (size_t)(n_leaves + (n_leaves & 1)) + 8, s));
+
   if (!chunk_boxes_ready) {  // the driver reuses them while the bins and face boxes are unchanged
     const int cg = ow_blocks((n_entries + 31) / 32, 4, 16 * OW_SMS);
     const int64_t* dn = binned ? d_bin_entries : nullptr;
@@ -811,7 +812,7 @@ extern "C" int ow_mark_near_wall(ow_ctx* ctx, ow_forest* f, const int32_t* d_lea
                                  int64_t* out_tests, int64_t* out_evaluated, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   unsigned long long* out = (unsigned long long*)(ctx->d_small + 16);
-  OW_CUDA(cudaMemsetAsync(out, 0, 5 * 8, s));
+  OW_CUDA(cudaMemsetAsync(out, 0, MARK_STATS * 8, s));
   OW_TRY(ow_mark_launch(ctx, f, d_leaves, n_leaves, d_coords, n_faces, geom_key, grid, d_bin_ids, d_bin_counts,
                         d_bin_offsets, n_bin_entries, d_spec, reach, out, s));
   int64_t h[3];

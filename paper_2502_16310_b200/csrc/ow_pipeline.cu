@@ -137,7 +137,7 @@ __device__ __forceinline__ void drv_summary_pass(const int64_t* drv, const unsig
   for (int k = 0; k < 6; ++k) o[k] = rs[k];
   o[6] = rs[RS_NR + it + 1];
   o[7] = refine_sweeps_exact(p) ? 0 : rs[RS_CR + it];  // (a cascade the sweeps may not have finished)
-  for (int k = 0; k < 5; ++k) o[8 + k] = (int64_t)stats[5 * p + k];
+  for (int k = 0; k < 5; ++k) o[8 + k] = (int64_t)stats[MARK_STATS * p + k];
 }
 
 __global__ void k_drv_summary(const int64_t* drv, const unsigned long long* stats, int passes, int64_t* sum) {
@@ -247,7 +247,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
   int64_t E = 0;
   const int passes = p->n_levels - 1;
   void *stats, *drv;
-  OW_TRY(ow_slot(ctx, SLOT_DRV_STATS, 40 * (size_t)passes, s, &stats));
+  OW_TRY(ow_slot(ctx, SLOT_DRV_STATS, 8 * MARK_STATS * (size_t)passes, s, &stats));
   // [72 * pass] ring state | [72 * passes] device block count | summary
   OW_TRY(ow_slot(ctx, SLOT_DRV_STATE, 8 * (72 * (size_t)passes + 16 + SUM_W * (size_t)passes), s, &drv));
   // the bin count of fill_bins with its host checks (one readback: the entry
@@ -297,7 +297,8 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
   auto device_part = [&]() -> int {
   bool bins_counted = pre_counted;
   have_bins = false;
-  ow_launch(k_loop_init, 1, 128, 0, s, (unsigned long long*)stats, 5 * passes, dev ? d_nb : nullptr, f->n_blocks);
+  ow_launch(k_loop_init, 1, 128, 0, s, (unsigned long long*)stats, MARK_STATS * passes, dev ? d_nb : nullptr,
+            f->n_blocks);
   OW_LAUNCHED(ctx);
   for (int level = 0; level < passes; ++level) {
     // ---- bin_setup
@@ -325,7 +326,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
     OW_TRY(ow_slot(ctx, SLOT_DRV_LEAVES, 4 * (size_t)(n_host + 1), s, &pl));
     int64_t* dn = (int64_t*)drv + 72 * level;  // [0] leaves at level, [8..72) refine state
     int64_t* rs = dn + 8;
-    unsigned long long* dst = (unsigned long long*)stats + 5 * level;
+    unsigned long long* dst = (unsigned long long*)stats + MARK_STATS * level;
     if (comm) {
       // sharded marking on the device: slices balanced by per-leaf work, the
       // rank marks its slice, then the marks and the statistics are exchanged
@@ -477,13 +478,13 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
     OW_TRY(drv_apply(ctx, f, h, passes, out));
   } else if (passes > 0) {
     int64_t h[5 * OW_MAX_PASSES];
-    OW_TRY(ow_readback(ctx, (const int64_t*)stats, 5 * passes, h, s));
+    OW_TRY(ow_readback(ctx, (const int64_t*)stats, MARK_STATS * passes, h, s));
     for (int level = 0; level < out->n_passes; ++level) {
-      out->marked_detected[level] = h[5 * level];
-      out->tests[level] = h[5 * level + 1];
-      out->evaluated[level] = h[5 * level + 2];
-      out->sphere_tests[level] = h[5 * level + 3];
-      out->box_culls[level] = h[5 * level + 4];
+      out->marked_detected[level] = h[MARK_STATS * level];
+      out->tests[level] = h[MARK_STATS * level + 1];
+      out->evaluated[level] = h[MARK_STATS * level + 2];
+      out->sphere_tests[level] = h[MARK_STATS * level + 3];
+      out->box_culls[level] = h[MARK_STATS * level + 4];
     }
   }
   if (!ctx->defer_stage_times) return ow_stage_times(ctx, out);
