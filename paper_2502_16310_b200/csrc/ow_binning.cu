@@ -567,7 +567,7 @@ struct GuardStore {
 // pass and re-runs it on the synchronous path when one fails.
 template <int D>
 int fill_dev(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, int32_t* counts, int32_t* ids,
-             int32_t* offsets, int64_t n_bins, int64_t e_cap, cudaStream_t s) {
+             int32_t* offsets, int64_t n_bins, int64_t e_cap, cudaStream_t s, bool init) {
   void *pm, *pnb, *pfo, *psl, *pmid;
   OW_TRY(ow_slot(ctx, SLOT_BIN_MASK, 8 * (size_t)n, s, &pm));
   OW_TRY(ow_slot(ctx, SLOT_BIN_NB, 4 * (size_t)n, s, &pnb));
@@ -575,12 +575,15 @@ int fill_dev(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, in
   OW_TRY(ow_slot(ctx, SLOT_BIN_SLOW, 4 * (size_t)n, s, &psl));
   OW_TRY(ow_slot(ctx, SLOT_BIN_MID, 4 * (size_t)n, s, &pmid));
   int64_t* small = ctx->d_small;
-  ow_launch(k_bins_init, ow_blocks(n_bins, 256, 4 * OW_SMS), 256, 0, s, small, counts, n_bins);
+  if (init) {  // (else the caller's first kernel cleared them: k_loop_init)
+    ow_launch(k_bins_init, ow_blocks(n_bins, 256, 4 * OW_SMS), 256, 0, s, small, counts, n_bins);
+    OW_LAUNCHED(ctx);
+  }
   ow_launch(k_count_fast<D>, ow_blocks(n, 256), 256, 0, s, g, c, n, (unsigned long long*)pm, (int32_t*)pnb, counts,
             (int32_t*)pmid, small);
   ow_launch(k_count_walk<D>, ow_blocks(n, 256, 8 * OW_SMS), 256, 0, s, g, c, n, h, (const int32_t*)pmid,
             (unsigned long long*)pm, (int32_t*)pnb, counts, (int32_t*)psl, small);
-  ctx->launches += 3;
+  ctx->launches += 2;
   OW_CHECK_LAUNCH();
   OW_TRY(scan(ctx, ow::LoadArr<int32_t>{(const int32_t*)pnb}, ow::StoreExcl<int32_t>{(int32_t*)pfo}, n, small + 5, s));
   void *pk0, *pv0, *pk1, *pv1;
@@ -620,15 +623,15 @@ int fill_dev(ow_ctx* ctx, const GridC& g, const float* c, int64_t n, float h, in
 }  // namespace
 
 int ow_fill_bins_dev(ow_ctx* ctx, const ow_grid* grid, const float* d_coords, int64_t n_faces, float spacing,
-                     int32_t* d_counts, int32_t* d_ids, int32_t* d_offsets, int64_t e_cap, cudaStream_t s) {
+                     int32_t* d_counts, int32_t* d_ids, int32_t* d_offsets, int64_t e_cap, cudaStream_t s, bool init) {
   GridC g = make_gridc(grid);
   int64_t n_bins = 1;
   for (int a = 0; a < grid->dim; ++a) n_bins *= grid->bins_per_axis;
   OW_PROF_BEGIN(ctx, PROF_BINS, s);
   const int st = grid->dim == 2 ? fill_dev<2>(ctx, g, d_coords, n_faces, spacing, d_counts, d_ids, d_offsets, n_bins,
-                                              e_cap, s)
+                                              e_cap, s, init)
                                 : fill_dev<3>(ctx, g, d_coords, n_faces, spacing, d_counts, d_ids, d_offsets, n_bins,
-                                              e_cap, s);
+                                              e_cap, s, init);
   OW_PROF_END(ctx, PROF_BINS, s);
   return st;
 }

@@ -256,7 +256,8 @@ void ow_g2g_release(ow_ctx* ctx);  // passes-in-flight table (ow_pipeline.cu)
 
 // fill_bins with the entry count left on the device (ow_binning.cu: fill_dev)
 int ow_fill_bins_dev(ow_ctx* ctx, const ow_grid* grid, const float* d_coords, int64_t n_faces, float spacing,
-                     int32_t* d_counts, int32_t* d_ids, int32_t* d_offsets, int64_t e_cap, cudaStream_t s);
+                     int32_t* d_counts, int32_t* d_ids, int32_t* d_offsets, int64_t e_cap, cudaStream_t s,
+                     bool init = true);
 
 int ow_stage_times(ow_ctx* ctx, ow_nearwall_result* out);
 

@@ -64,10 +64,18 @@ int64_t overflow_total(const int32_t* h_counts, int64_t n_bins, int64_t bin_frac
 
 // the level loop's statistics cleared and (device-resident loop) the block
 // count set, one launch
-__global__ void k_loop_init(unsigned long long* stats, int n_stats, int64_t* d_nb, int64_t nb) {
+// (+ the device-sized pass's bin counts and count words, k_bins_init's work)
+__global__ void k_loop_init(unsigned long long* stats, int n_stats, int64_t* d_nb, int64_t nb, int32_t* counts,
+                            int64_t n_bins, int64_t* small) {
   ow_pdl_wait();
-  for (int i = threadIdx.x; i < n_stats; i += blockDim.x) stats[i] = 0ull;
-  if (threadIdx.x == 0 && d_nb) *d_nb = nb;
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < n_stats; i += blockDim.x) stats[i] = 0ull;
+    if (threadIdx.x == 0 && d_nb) *d_nb = nb;
+    if (small && threadIdx.x < 8) small[threadIdx.x] = (threadIdx.x == 1 || threadIdx.x == 3) ? -1 : 0;
+  }
+  if (counts)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_bins; i += (int64_t)gridDim.x * blockDim.x)
+      counts[i] = 0;
 }
 
 // ---- multi-GPU marking shards ("balanced by work") --------
@@ -297,8 +305,10 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
   auto device_part = [&]() -> int {
   bool bins_counted = pre_counted;
   have_bins = false;
-  ow_launch(k_loop_init, 1, 128, 0, s, (unsigned long long*)stats, MARK_STATS * passes, dev ? d_nb : nullptr,
-            f->n_blocks);
+  const bool init_bins = devpass && p->binned;  // (fill_dev then skips its own init)
+  ow_launch(k_loop_init, init_bins ? ow_blocks(n_bins, 256, 4 * OW_SMS) : 1, init_bins ? 256 : 128, 0, s,
+            (unsigned long long*)stats, MARK_STATS * passes, dev ? d_nb : nullptr, f->n_blocks,
+            init_bins ? d_bin_counts : nullptr, n_bins, init_bins ? ctx->d_small : nullptr);
   OW_LAUNCHED(ctx);
   for (int level = 0; level < passes; ++level) {
     // ---- bin_setup
@@ -308,7 +318,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
       fresh_bins = true;
       if (devpass) {
         OW_TRY(ow_fill_bins_dev(ctx, grid, d_coords, n_faces, p->spacing, d_bin_counts, d_bin_ids, d_bin_offsets, E,
-                                s));
+                                s, level > 0 || !init_bins));
       } else {
         if (!bins_counted) OW_TRY(count_bins());
         bins_counted = false;
