@@ -27,7 +27,7 @@ constexpr int PREP_THREADS = 128;
 
 // Per-face terms of marking: FP32 box, bounding sphere and predicate payload.
 // Records are assembled in shared memory and leave as contiguous float4 runs
-// (a thread's own 192-byte payload record would be a 16-byte scatter per lane).
+// (a thread's own 112-byte payload record would be a 16-byte scatter per lane).
 template <int D>
 __global__ void __launch_bounds__(PREP_THREADS) k_face_prep(const float* __restrict__ c, int64_t n, float d,
                                                             double reach, float4* box, float4* sph, float4* pay) {
@@ -143,6 +143,7 @@ struct MarkArgs {
   float d;
   double reach;
   unsigned long long* out;  // [0] marked, [1] tests, [2] evaluated, [3] sphere tests, [4] box culls
+  int prefilter;            // k_mark_blocks: lane-level empty-bin prefilter (OW_MARK_PREFILTER=0: off, A/B)
 };
 
 // Union box of the face boxes of bin-CSR entries [32 g, 32 g + 32) (entries of
@@ -334,12 +335,14 @@ __device__ __forceinline__ bool sweep_chunks(const MarkArgs& A, MarkSmem<D>& S, 
   // sphere prefilter over (face, own cell) with the sphere broadcast from shared
   // memory; survivors are buffered and then evaluated 32 at a time
   int npairs = 0;
+  unsigned nact = 0;  // the lane's cells in this bin: sphere tests per face (counted once per exit)
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) nact += act[k] ? 1u : 0u;
   for (int fi = 0; fi < nf; ++fi) {
     const float4 sp = S.sph[wid][fi];
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       const bool pass = act[k] && sphere_ok<D>(p[k], sp);
-      cn.spheres += act[k];
       const unsigned m = __ballot_sync(0xffffffffu, pass);
       if (pass) S.pair[wid][npairs + __popc(m & lanemask_lt())] = (unsigned short)((fi << 6) | (lane + 32 * k));
       npairs += __popc(m);
@@ -347,11 +350,15 @@ __device__ __forceinline__ bool sweep_chunks(const MarkArgs& A, MarkSmem<D>& S, 
     if (npairs > PAIR_CAP - 64) {  // buffer nearly full: evaluate what we have
       __syncwarp();
       cn.evaluated += lane == 0 ? npairs : 0;
-      if (eval_pairs<D>(A, S, wid, lane, npairs, r2)) return true;
+      if (eval_pairs<D>(A, S, wid, lane, npairs, r2)) {
+        cn.spheres += (unsigned long long)nact * (unsigned)(fi + 1);
+        return true;
+      }
       npairs = 0;
       __syncwarp();
     }
   }
+  cn.spheres += (unsigned long long)nact * (unsigned)nf;
   __syncwarp();
   cn.evaluated += lane == 0 ? npairs : 0;
   const bool hit = eval_pairs<D>(A, S, wid, lane, npairs, r2);
@@ -377,6 +384,47 @@ __device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M
                                            int lane, int wid, MarkCounts& cn, unsigned long long& t_acc,
                                            unsigned long long& marked);
 
+// Lane-level prefilter of one leaf block (binned marking): false when every
+// bin its cells fall in is empty.  Such a block adds nothing to T (its cells'
+// bin counts are all 0) and has no candidate to test, so skipping it is exact.
+// The cells' bins along an axis lie between the bins of its first and last
+// cell centres (centres and bin_axis are monotone in the index), and those two
+// centres are formed with block_cells' exact FP64 ops; a bin box of more than
+// 64 bins is not scanned (the block takes the full path).
+template <int D>
+__device__ __forceinline__ bool block_may_hit(const MarkArgs& A, int id) {
+  const int L = A.F.level[id];
+  int b0[3] = {0, 0, 0}, nb[3] = {1, 1, 1};
+  int total = 1;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const double q = block_len(A.F, a, L);
+    const double blo = DADD(A.F.dmin[a], DMUL((double)A.F.coord[a][id], q));
+    // u = (i + 0.5) / 4 for the first and last cell: 0.125 and 0.875 (exact)
+    const float p0 = __double2float_rn(DADD(blo, DMUL(0.125, q)));
+    const float p3 = __double2float_rn(DADD(blo, DMUL(0.875, q)));
+    b0[a] = bin_axis(p0, A.g.min32[a], A.g.len32[a], A.g.B);
+    nb[a] = bin_axis(p3, A.g.min32[a], A.g.len32[a], A.g.B) - b0[a] + 1;
+    total *= nb[a];
+  }
+  if (total > 64) return true;
+  int any = 0;
+  for (int k = 0; k < total; ++k) {
+    int r = k, lin = 0, mul = 1;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const int i = r % nb[a];
+      r /= nb[a];
+      lin += (b0[a] + i) * mul;
+      mul *= A.g.B;
+    }
+    any |= __ldg(A.bin_counts + lin);
+  }
+  return any != 0;
+}
+
+static __device__ __forceinline__ bool mark_prefilter_on(const MarkArgs& A) { return A.prefilter != 0; }
+
 // persistent over the level's leaves (the count may live on the device)
 template <int D, bool BINNED, int MINB = 6>
 __global__ void __launch_bounds__(MARK_THREADS, MINB) k_mark_blocks(MarkArgs A, MarkItems M) {
@@ -390,8 +438,29 @@ __global__ void __launch_bounds__(MARK_THREADS, MINB) k_mark_blocks(MarkArgs A, 
   // warp of the grid: 1.6 M of them at C5)
   MarkCounts cn;
   unsigned long long t_acc = 0, marked = 0;
-  for (int64_t pos = lo + (int64_t)blockIdx.x * MARK_WARPS + wid; pos < n; pos += (int64_t)gridDim.x * MARK_WARPS)
-    mark_block<D, BINNED>(A, M, S, pos, lane, wid, cn, t_acc, marked);
+  const int64_t G = (int64_t)gridDim.x * MARK_WARPS, gw = (int64_t)blockIdx.x * MARK_WARPS + wid;
+  if (BINNED && mark_prefilter_on(A) && n - lo > G) {
+    // several blocks per warp: the warp's blocks (the same strided set as
+    // below) are prefiltered 32 at a time, one per lane, and only blocks with
+    // a non-empty bin take the warp-wide path (C5 level 0: most of the 64^3
+    // root blocks lie in empty bins, and each was one dependent-load chain)
+    for (int64_t k0 = 0; lo + gw + k0 * G < n; k0 += 32) {
+      const int64_t pos = lo + gw + (k0 + lane) * G;
+      bool need = false;
+      if (pos < n) {
+        need = block_may_hit<D>(A, A.leaves[pos]);
+        if (!need) M.hit[pos] = 0u;
+      }
+      unsigned m = __ballot_sync(0xffffffffu, need);
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        mark_block<D, BINNED>(A, M, S, lo + gw + (k0 + j) * G, lane, wid, cn, t_acc, marked);
+      }
+    }
+  } else {
+    for (int64_t pos = lo + gw; pos < n; pos += G) mark_block<D, BINNED>(A, M, S, pos, lane, wid, cn, t_acc, marked);
+  }
   flush_counts(A, cn, lane);
   if (lane == 0) {
     if (t_acc) atomicAdd(&A.out[1], t_acc);
@@ -747,6 +816,13 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   A.d = d_spec;
   A.reach = reach;
   A.out = out;
+  {
+    static const int pf = [] {
+      const char* e = getenv("OW_MARK_PREFILTER");
+      return e ? atoi(e) : 1;
+    }();
+    A.prefilter = pf;
+  }
   const int64_t n_entries = binned ? n_bin_entries : n_faces;
   void *pc, *pi, *ph;
   OW_TRY(ow_slot(ctx, SLOT_MARK_CBOX, 32 * (size_t)((n_entries + 31) / 32 + 1), s, &pc));
@@ -778,7 +854,13 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
     const char* e = getenv("OW_MARK_CTAS_PER_SM");
     return e && atoi(e) > 0 ? (int64_t)atoi(e) : (int64_t)24;
   }();
-  dim3 grd((unsigned)(nblk < per_sm * OW_SMS ? nblk : per_sm * OW_SMS));
+  static const int64_t max_ctas = [] {  // OW_MARK_MAX_CTAS: total cap (tests: many blocks per warp)
+    const char* e = getenv("OW_MARK_MAX_CTAS");
+    return e && atoi(e) > 0 ? (int64_t)atoi(e) : (int64_t)0;
+  }();
+  int64_t ng = nblk < per_sm * OW_SMS ? nblk : per_sm * OW_SMS;
+  if (max_ctas > 0 && ng > max_ctas) ng = max_ctas;
+  dim3 grd((unsigned)ng);
   const int gi = 8 * OW_SMS;
   if (f->dim == 3) {
     if (binned) {

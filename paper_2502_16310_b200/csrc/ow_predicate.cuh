@@ -1,24 +1,36 @@
 // FP32 near-face predicate (Algorithm 1 of arXiv 2502.16310) with the
 // reference's exact operation order: octowall/distance.py:167-245.
 //
-// Per-face terms (edge vectors, squared lengths, unit edges, unit normal,
-// in-plane edge normals n x e_k, slab anchors v0 -+ d*n) are precomputed once
-// per (geometry, d) by k_face_prep with the same float32 operations the
-// reference evaluates per pair; reusing them is bit-safe because each is a
-// pure function of the face and d.  Per pair the predicate costs 130 FP32
-// operations (3 IEEE divisions), SURVEY.md §8(d).
+// Per-face terms (unit normal, unit edges, slab anchors v0 -+ d*n) are
+// precomputed once per (geometry, d) by k_face_prep with the same float32
+// operations the reference evaluates per pair; the cheap ones (edge vectors,
+// squared edge lengths, in-plane edge normals n x e_k) are re-formed per pair
+// from the stored operands by the same operations.  Either way each term is a
+// pure function of the face and d, so the predicate is bit-identical to the
+// per-pair evaluation.  Per pair the predicate costs 130 FP32 operations (3
+// IEEE divisions), SURVEY.md §8(d).
 #pragma once
 
 #include "ow_common.cuh"
 
-// payload float4 layout (3D, 12 x float4 = 192 B per face):
-//  [k]     k=0..2 : v_k.xyz, el2_k          (v_k vertex, el2_k = |v_{k+1}-v_k|^2)
-//  [3+k]          : e_k.xyz, n.(x|y|z)_k    (e_k = v_{k+1}-v_k; unit normal component k)
-//  [6+k]          : eh_k.xyz, alo.(x|y|z)_k (eh_k = e_k/|e_k|; alo = v0 - d*n)
-//  [9+k]          : m_k.xyz, ahi.(x|y|z)_k  (m_k = n x eh_k; ahi = v0 + d*n)
+// payload float4 layout (3D, 7 x float4 = 112 B per face):
+//  [k]     k=0..2 : v_k.xyz, n_k            (v_k vertex; unit normal component k)
+//  [3+k]          : eh_k.xyz, alo_k         (eh_k = e_k/|e_k|, e_k = v_{k+1}-v_k; alo = v0 - d*n)
+//  [6]            : ahi.xyz, 0              (ahi = v0 + d*n)
+// (e_k, |e_k|^2 and m_k = n x eh_k are re-formed by near_tri: 51 FP32
+// operations per pair instead of 80 B more per face written by k_face_prep and
+// read by every evaluated pair; C5 writes 5.2 M payloads per pass)
 // 2D (3 x float4 = 48 B): [a.xy b.xy] [e.xy el2 0] [eh.xy 0 0]
-constexpr int PAY3 = 12;
+constexpr int PAY3 = 7;
 constexpr int PAY2 = 3;
+
+// in-plane edge normal m = n x eh (distance.py:203-205), the op order of the
+// reference's np.cross
+__device__ __forceinline__ void edge_normal(const float* nn, float ex, float ey, float ez, float* m) {
+  m[0] = FSUB(FMUL(nn[1], ez), FMUL(nn[2], ey));
+  m[1] = FSUB(FMUL(nn[2], ex), FMUL(nn[0], ez));
+  m[2] = FSUB(FMUL(nn[0], ey), FMUL(nn[1], ex));
+}
 
 template <int D>
 __device__ __forceinline__ void face_prep_one(const float* __restrict__ c, int64_t n, int64_t f, float d,
@@ -44,23 +56,16 @@ __device__ __forceinline__ void face_prep_one(const float* __restrict__ c, int64
     float nz = FSUB(FMUL(ux, wy), FMUL(uy, wx));
     float nl = FSQRT(dot3f(nx, ny, nz, nx, ny, nz));
     float nn[3] = {FDIV(nx, nl), FDIV(ny, nl), FDIV(nz, nl)};
-    float m[3][3];
-    for (int k = 0; k < 3; ++k) {  // distance.py:203-205
-      m[k][0] = FSUB(FMUL(nn[1], eh[k][2]), FMUL(nn[2], eh[k][1]));
-      m[k][1] = FSUB(FMUL(nn[2], eh[k][0]), FMUL(nn[0], eh[k][2]));
-      m[k][2] = FSUB(FMUL(nn[0], eh[k][1]), FMUL(nn[1], eh[k][0]));
-    }
     float alo[3], ahi[3];
     for (int a = 0; a < 3; ++a) {  // distance.py:210-211: (a - d*n), (a + d*n)
       alo[a] = FSUB(v[0][a], FMUL(d, nn[a]));
       ahi[a] = FADD(v[0][a], FMUL(d, nn[a]));
     }
     for (int k = 0; k < 3; ++k) {
-      pay[k] = make_float4(v[k][0], v[k][1], v[k][2], el2[k]);
-      pay[3 + k] = make_float4(e[k][0], e[k][1], e[k][2], nn[k]);
-      pay[6 + k] = make_float4(eh[k][0], eh[k][1], eh[k][2], alo[k]);
-      pay[9 + k] = make_float4(m[k][0], m[k][1], m[k][2], ahi[k]);
+      pay[k] = make_float4(v[k][0], v[k][1], v[k][2], nn[k]);
+      pay[3 + k] = make_float4(eh[k][0], eh[k][1], eh[k][2], alo[k]);
     }
+    pay[6] = make_float4(ahi[0], ahi[1], ahi[2], 0.0f);
   } else {
     float ax = c[0 * n + f], ay = c[1 * n + f], bx = c[2 * n + f], by = c[3 * n + f];
     float ex = FSUB(bx, ax), ey = FSUB(by, ay);
@@ -74,14 +79,14 @@ __device__ __forceinline__ void face_prep_one(const float* __restrict__ c, int64
 
 // 3D predicate on a prepared face; r2 = d*d (float32).
 __device__ __forceinline__ bool near_tri(const float4* __restrict__ P, float px, float py, float pz, float r2) {
-  float4 V[3], E[3], H[3], M[3];
+  float4 V[3], H[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     V[k] = P[k];
-    E[k] = P[3 + k];
-    H[k] = P[6 + k];
-    M[k] = P[9 + k];
+    H[k] = P[3 + k];
   }
+  const float4 AH = P[6];
+  const float nn[3] = {V[0].w, V[1].w, V[2].w};
   float w[3][3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -90,28 +95,30 @@ __device__ __forceinline__ bool near_tri(const float4* __restrict__ P, float px,
     w[k][2] = FSUB(V[k].z, pz);
   }
   bool hit = false;
+  bool inside = true;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const float* W = w[k];
     const float* Wn = w[(k + 1) % 3];  // b - p, identical to the reference's (bx - px)
-    float ex = E[k].x, ey = E[k].y, ez = E[k].z;
+    const float4 Vn = V[(k + 1) % 3];
+    // edge vector and squared length, k_face_prep's operations (v_{k+1} - v_k)
+    float ex = FSUB(Vn.x, V[k].x), ey = FSUB(Vn.y, V[k].y), ez = FSUB(Vn.z, V[k].z);
+    float el2 = dot3f(ex, ey, ez, ex, ey, ez);
     float ball = dot3f(W[0], W[1], W[2], W[0], W[1], W[2]);
     float cx = FSUB(FMUL(ey, W[2]), FMUL(ez, W[1]));
     float cy = FSUB(FMUL(ez, W[0]), FMUL(ex, W[2]));
     float cz = FSUB(FMUL(ex, W[1]), FMUL(ey, W[0]));
-    float d2 = FDIV(dot3f(cx, cy, cz, cx, cy, cz), V[k].w);
+    float d2 = FDIV(dot3f(cx, cy, cz, cx, cy, cz), el2);
     float de1 = -dot3f(W[0], W[1], W[2], H[k].x, H[k].y, H[k].z);
     float de2 = dot3f(Wn[0], Wn[1], Wn[2], H[k].x, H[k].y, H[k].z);
     hit |= (ball <= r2) | ((d2 <= r2) & (de1 >= 0.0f) & (de2 >= 0.0f));
+    // prism interior: (p - a_k) . m_k >= 0, with p - a_k == -(a_k - p) exactly
+    float m[3];
+    edge_normal(nn, H[k].x, H[k].y, H[k].z, m);
+    inside &= -dot3f(W[0], W[1], W[2], m[0], m[1], m[2]) >= 0.0f;
   }
-  // prism interior: (p - a_k) . m_k >= 0, with p - a_k == -(a_k - p) exactly
-  bool inside = true;
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
-    inside &= -dot3f(w[k][0], w[k][1], w[k][2], M[k].x, M[k].y, M[k].z) >= 0.0f;
-  float nx = E[0].w, ny = E[1].w, nz = E[2].w;
-  float lo = -dot3f(FSUB(H[0].w, px), FSUB(H[1].w, py), FSUB(H[2].w, pz), nx, ny, nz);
-  float hi = dot3f(FSUB(M[0].w, px), FSUB(M[1].w, py), FSUB(M[2].w, pz), nx, ny, nz);
+  float lo = -dot3f(FSUB(H[0].w, px), FSUB(H[1].w, py), FSUB(H[2].w, pz), nn[0], nn[1], nn[2]);
+  float hi = dot3f(FSUB(AH.x, px), FSUB(AH.y, py), FSUB(AH.z, pz), nn[0], nn[1], nn[2]);
   return hit | (inside & (lo >= 0.0f) & (hi >= 0.0f));
 }
 

@@ -1084,3 +1084,71 @@ def test_pdl_off_matches_pdl_on(ow, tmp_path):
     for k in out["1"].files:
         np.testing.assert_array_equal(out["1"][k], out["0"][k], err_msg=k)
     assert len(out["1"]["cells"]) > 0
+
+
+_PREFILTER_SCRIPT = r"""
+import glob, json, os, sys, numpy as np, torch
+sys.path.insert(0, sys.argv[2])
+sys.path.insert(0, os.path.join(sys.argv[2], "tests"))
+import paper_2502_16310_b200 as ow
+from paper_2502_16310_b200 import pipeline, shapes
+import golden_util as gu
+from test_gpu_parity import domain, geom_of
+stats = {}
+for path in gu.files("pipe_"):  # every golden pipeline, bit-exact under this process's launch knobs
+    g = gu.load(path)
+    geom = geom_of(ow, g)
+    dim = geom.dim
+    f = ow.init_root_grid(domain(ow, dim), (int(g["root"]),) * dim)
+    params = ow.NearWallParams(d_spec=float(g["d_spec"]), n_levels=int(g["n_levels"]),
+                               strategy=str(g["strategy"]), bins_per_axis=int(g["bins_per_axis"]))
+    res = ow.refine_near_wall(f, geom, params)
+    assert res.marked_detected == g["marked_detected"].tolist(), path
+    assert res.marked_refined == g["marked_refined"].tolist(), path
+    np.testing.assert_array_equal(f._coords, g["coords"], err_msg=path)
+    np.testing.assert_array_equal(f.marks.cpu().numpy(), g["marks"], err_msg=path)
+    # T per pass (algorithmic); the evaluated / sphere / cull counts depend on
+    # when another warp's hit ends a block's remaining items, so not compared
+    stats[os.path.basename(path)] = list(map(int, res.cell_face_tests))
+data = shapes.binary_stl_bytes(shapes.icosphere_triangles(4))
+n = int.from_bytes(data[80:84], "little")
+rec = torch.frombuffer(bytearray(data[84:]), dtype=torch.uint8).cuda()
+plan = pipeline.GridPlan(ow.Aabb(np.zeros(3), np.ones(3)), (16, 16, 16),
+                         ow.NearWallParams(d_spec=0.05, n_levels=3, bins_per_axis=8), "D3Q19")
+for _ in range(3):  # sizing, device-sized, graph replay
+    gp = plan.run(rec, n)
+f, ll = gp.forest, gp.links
+np.savez(sys.argv[1], level=f._level, coords=f._coords, parent=f._parent, marks=f.marks.cpu().numpy(),
+         flags=ll.flags.cpu().numpy(), q=ll.q.cpu().numpy())
+json.dump(stats, open(sys.argv[1] + ".json", "w"))
+"""
+
+
+def test_mark_prefilter_many_blocks_per_warp(ow, tmp_path):
+    """The block pass prefilters a warp's leaf blocks one per lane when it has
+    more than one (only blocks with a non-empty bin take the warp-wide path).
+    With the grid capped at 2 CTAs (8 warps: every level has many blocks per
+    warp) the golden pipelines stay bit-exact with their statistics equal to
+    the same capped run without the prefilter, and the fused pass is array for
+    array the default launch's."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out, st = {}, {}
+    for tag, env in (("pf", {"OW_MARK_MAX_CTAS": "2", "OW_MARK_PREFILTER": "1"}),
+                     ("nopf", {"OW_MARK_MAX_CTAS": "2", "OW_MARK_PREFILTER": "0"}),
+                     ("default", {})):
+        path = str(tmp_path / f"{tag}.npz")
+        e = dict(os.environ, **env)
+        r = subprocess.run([sys.executable, "-c", _PREFILTER_SCRIPT, path, repo], env=e, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        out[tag] = np.load(path)
+        st[tag] = json.load(open(path + ".json"))
+    assert st["pf"] == st["nopf"] == st["default"]
+    for tag in ("pf", "nopf"):
+        for k in out["default"].files:
+            np.testing.assert_array_equal(out[tag][k], out["default"][k], err_msg=f"{tag}:{k}")
