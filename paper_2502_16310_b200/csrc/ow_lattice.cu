@@ -1389,9 +1389,12 @@ LatArgs make_args(ow_ctx* ctx) {
   A.iru_d = (unsigned long long*)(ctx->d_small + 50);
   A.inline_units = inline_units_setting(ctx);
   {
+    // batches whose rows all have at most 2 cells skip the staging (A/B on one
+    // B200, OW_LAT_LANE_ROWS 0-4, tools/ab_lat.sh: C5 sweep 1.909 -> 1.846 ms
+    // at 2, C2 / C3 / C4 within noise; 4 is slower again at C5)
     static const int lr = [] {  // OW_LAT_LANE_ROWS overrides (A/B)
       const char* e = getenv("OW_LAT_LANE_ROWS");
-      return e ? atoi(e) : 0;
+      return e ? atoi(e) : 2;
     }();
     A.lane_rows = lr;
   }
