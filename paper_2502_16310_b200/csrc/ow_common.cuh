@@ -234,7 +234,7 @@ int ow_comm_exchange_marks(ow_ctx* ctx, ow_comm* c, const int32_t* d_leaves, int
 
 // marking statistics per pass: [0] marked, [1] tests T, [2] evaluated,
 // [3] sphere tests, [4] box culls, [5] the pass's (block, chunk) item counter
-constexpr int MARK_STATS = 6;
+constexpr int MARK_STATS = 8;  // marked, T, evaluated, spheres, culls, items, block-pass counter, -
 
 // one marking pass without a host round trip: stats accumulate in d_out[0..5)
 // (d_out[5]: the item counter, zero on entry like the statistics)

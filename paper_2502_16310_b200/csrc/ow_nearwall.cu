@@ -144,6 +144,7 @@ struct MarkArgs {
   double reach;
   unsigned long long* out;  // [0] marked, [1] tests, [2] evaluated, [3] sphere tests, [4] box culls
   int prefilter;            // k_mark_blocks: lane-level empty-bin prefilter (OW_MARK_PREFILTER=0: off, A/B)
+  int dyn;                  // k_mark_blocks: dynamic schedule over out[6] (OW_MARK_DYN, A/B)
 };
 
 // Union box of the face boxes of bin-CSR entries [32 g, 32 g + 32) (entries of
@@ -439,7 +440,39 @@ __global__ void __launch_bounds__(MARK_THREADS, MINB) k_mark_blocks(MarkArgs A, 
   MarkCounts cn;
   unsigned long long t_acc = 0, marked = 0;
   const int64_t G = (int64_t)gridDim.x * MARK_WARPS, gw = (int64_t)blockIdx.x * MARK_WARPS + wid;
-  if (BINNED && mark_prefilter_on(A) && n - lo > G) {
+  if (A.dyn) {
+    // dynamic schedule: warps take runs of K consecutive leaf positions from a
+    // per-pass counter (out[6]); the next run is reserved before the current
+    // one is swept, so the atomic's round trip hides behind the work
+    const int64_t total = n - lo;
+    int64_t K = total / (G * 8);
+    K = K < 1 ? 1 : (K > 32 ? 32 : K);
+    unsigned long long nxt = 0;
+    if (lane == 0) nxt = atomicAdd(&A.out[6], (unsigned long long)K);
+    nxt = __shfl_sync(0xffffffffu, nxt, 0);
+    while ((int64_t)nxt < total) {
+      const int64_t base = lo + (int64_t)nxt;
+      unsigned long long nn = 0;
+      if (lane == 0) nn = atomicAdd(&A.out[6], (unsigned long long)K);
+      if (BINNED && K > 1 && mark_prefilter_on(A)) {
+        const int64_t pos = base + lane;
+        bool need = false;
+        if (lane < K && pos < n) {
+          need = block_may_hit<D>(A, A.leaves[pos]);
+          if (!need) M.hit[pos] = 0u;
+        }
+        unsigned m = __ballot_sync(0xffffffffu, need);
+        while (m) {
+          const int j = __ffs(m) - 1;
+          m &= m - 1;
+          mark_block<D, BINNED>(A, M, S, base + j, lane, wid, cn, t_acc, marked);
+        }
+      } else {
+        for (int64_t j = 0; j < K && base + j < n; ++j) mark_block<D, BINNED>(A, M, S, base + j, lane, wid, cn, t_acc, marked);
+      }
+      nxt = __shfl_sync(0xffffffffu, nn, 0);
+    }
+  } else if (BINNED && mark_prefilter_on(A) && n - lo > G) {
     // several blocks per warp: the warp's blocks (the same strided set as
     // below) are prefiltered 32 at a time, one per lane, and only blocks with
     // a non-empty bin take the warp-wide path (C5 level 0: most of the 64^3
@@ -822,6 +855,14 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
       return e ? atoi(e) : 1;
     }();
     A.prefilter = pf;
+    // dynamic block schedule (A/B on one B200, tools/ab_markdyn.sh, with 12
+    // CTAs per SM: C2 0.321 -> 0.319 ms, C3 1.570 -> 1.523, C4 2.180 -> 2.105,
+    // C5 3.577 -> 3.554; the static stride's best grid was 24 per SM)
+    static const int dy = [] {
+      const char* e = getenv("OW_MARK_DYN");
+      return e ? atoi(e) : 1;
+    }();
+    A.dyn = dy;
   }
   const int64_t n_entries = binned ? n_bin_entries : n_faces;
   void *pc, *pi, *ph;
@@ -848,11 +889,11 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
     else ow_launch(k_chunk_boxes<2>, cg, 128, 0, s, d_bin_ids, n_entries, A.box, (float4*)pc, dn);
   }
   OW_PROF_BEGIN(ctx, PROF_MARK, s);
-  // persistent past 4 waves (k_mark_blocks strides over the device leaf count)
+  // two waves of CTAs (k_mark_blocks takes its blocks from a per-pass counter)
   const int64_t nblk = (n_leaves + MARK_WARPS - 1) / MARK_WARPS;
   static const int64_t per_sm = [] {  // CTAs per SM of the block pass grid (OW_MARK_CTAS_PER_SM: A/B)
     const char* e = getenv("OW_MARK_CTAS_PER_SM");
-    return e && atoi(e) > 0 ? (int64_t)atoi(e) : (int64_t)24;
+    return e && atoi(e) > 0 ? (int64_t)atoi(e) : (int64_t)12;
   }();
   static const int64_t max_ctas = [] {  // OW_MARK_MAX_CTAS: total cap (tests: many blocks per warp)
     const char* e = getenv("OW_MARK_MAX_CTAS");

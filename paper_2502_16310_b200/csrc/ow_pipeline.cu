@@ -487,7 +487,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
     OW_TRY(ow_readback(ctx, d_sum, SUM_W * passes + 1, h, s));
     OW_TRY(drv_apply(ctx, f, h, passes, out));
   } else if (passes > 0) {
-    int64_t h[5 * OW_MAX_PASSES];
+    int64_t h[MARK_STATS * OW_MAX_PASSES];
     OW_TRY(ow_readback(ctx, (const int64_t*)stats, MARK_STATS * passes, h, s));
     for (int level = 0; level < out->n_passes; ++level) {
       out->marked_detected[level] = h[MARK_STATS * level];

@@ -1126,7 +1126,9 @@ json.dump(stats, open(sys.argv[1] + ".json", "w"))
 
 def test_mark_prefilter_many_blocks_per_warp(ow, tmp_path):
     """The block pass prefilters a warp's leaf blocks one per lane when it has
-    more than one (only blocks with a non-empty bin take the warp-wide path).
+    more than one (only blocks with a non-empty bin take the warp-wide path),
+    under the dynamic schedule (runs of K blocks from a counter) and the
+    static stride (OW_MARK_DYN=0).
     With the grid capped at 2 CTAs (8 warps: every level has many blocks per
     warp) the golden pipelines stay bit-exact with their statistics equal to
     the same capped run without the prefilter, and the fused pass is array for
@@ -1140,6 +1142,7 @@ def test_mark_prefilter_many_blocks_per_warp(ow, tmp_path):
     out, st = {}, {}
     for tag, env in (("pf", {"OW_MARK_MAX_CTAS": "2", "OW_MARK_PREFILTER": "1"}),
                      ("nopf", {"OW_MARK_MAX_CTAS": "2", "OW_MARK_PREFILTER": "0"}),
+                     ("static", {"OW_MARK_MAX_CTAS": "2", "OW_MARK_DYN": "0"}),
                      ("default", {})):
         path = str(tmp_path / f"{tag}.npz")
         e = dict(os.environ, **env)
@@ -1148,7 +1151,7 @@ def test_mark_prefilter_many_blocks_per_warp(ow, tmp_path):
         assert r.returncode == 0, r.stderr[-3000:]
         out[tag] = np.load(path)
         st[tag] = json.load(open(path + ".json"))
-    assert st["pf"] == st["nopf"] == st["default"]
-    for tag in ("pf", "nopf"):
+    assert st["pf"] == st["nopf"] == st["static"] == st["default"]
+    for tag in ("pf", "nopf", "static"):
         for k in out["default"].files:
             np.testing.assert_array_equal(out[tag][k], out["default"][k], err_msg=f"{tag}:{k}")
