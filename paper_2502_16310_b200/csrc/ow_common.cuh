@@ -243,7 +243,7 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
                    const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,
                    double reach, unsigned long long* d_out, cudaStream_t s,
                    const int64_t* d_n_leaves = nullptr, bool chunk_boxes_ready = false,
-                   const int64_t* d_slice = nullptr, const int64_t* d_bin_entries = nullptr);
+                   const int64_t* d_slice = nullptr, const int64_t* d_bin_entries = nullptr, int level = -1);
 
 // device-sized lattice stage of the fused pass (ow_lattice.cu)
 int ow_lattice_dev_count(ow_ctx* ctx, const ow_forest* f, int32_t level, const int32_t* d_leaves, const int64_t* d_nl,

@@ -219,18 +219,18 @@ struct MarkItems {
 
 constexpr int PAIR_CAP = 256;  // sphere-passing (face, cell) pairs buffered per warp
 
-template <int D>
+template <int D, int CGN = CG>
 struct MarkSmem {
   static constexpr int C = D == 3 ? 64 : 16;
-  int cand[MARK_WARPS][32 * CG];
-  float4 sph[MARK_WARPS][32 * CG];
+  int cand[MARK_WARPS][32 * CGN];
+  float4 sph[MARK_WARPS][32 * CGN];
   float p[MARK_WARPS][C][D];                  // cell centres of the warp's block
   unsigned short pair[MARK_WARPS][PAIR_CAP];  // face index << 6 | cell
 };
 
 // cell centres of the lane's cells into the warp's shared table
-template <int D>
-__device__ __forceinline__ void share_cells(MarkSmem<D>& S, int wid, int lane, const float (*p)[3]) {
+template <int D, int CGN>
+__device__ __forceinline__ void share_cells(MarkSmem<D, CGN>& S, int wid, int lane, const float (*p)[3]) {
   constexpr int C = D == 3 ? 64 : 16;
   constexpr int CPL = D == 3 ? 2 : 1;
 #pragma unroll
@@ -243,8 +243,8 @@ __device__ __forceinline__ void share_cells(MarkSmem<D>& S, int wid, int lane, c
 
 // full predicate on the buffered pairs, 32 in parallel (their payload loads
 // overlap); true on a hit
-template <int D>
-__device__ __forceinline__ bool eval_pairs(const MarkArgs& A, MarkSmem<D>& S, int wid, int lane, int npairs, float r2) {
+template <int D, int CGN>
+__device__ __forceinline__ bool eval_pairs(const MarkArgs& A, MarkSmem<D, CGN>& S, int wid, int lane, int npairs, float r2) {
   constexpr int PW = D == 3 ? PAY3 : PAY2;
   for (int k0 = 0; k0 < npairs; k0 += 32) {
     bool h = false;
@@ -300,29 +300,29 @@ __device__ __forceinline__ void block_cells(const MarkArgs& A, int id, int lane,
 // cells (centres in registers, act = cell lies in this bin) against the
 // broadcast bounding sphere, and runs the full predicate on the survivors.
 // True on a hit (checked after every face: a mark is an OR).
-template <int D, bool BINNED>
-__device__ __forceinline__ bool sweep_chunks(const MarkArgs& A, MarkSmem<D>& S, int wid, int lane, const int64_t* gc,
+template <int D, bool BINNED, int CGN>
+__device__ __forceinline__ bool sweep_chunks(const MarkArgs& A, MarkSmem<D, CGN>& S, int wid, int lane, const int64_t* gc,
                                              int64_t off, int64_t cnt, const double* blo, const double* bhi,
                                              double reach2, float r2, const float (*p)[3], const bool* act,
                                              MarkCounts& cn) {
   constexpr int CPL = D == 3 ? 2 : 1;
-  int fv[CG];
-  bool fok[CG];
+  int fv[CGN];
+  bool fok[CGN];
 #pragma unroll
-  for (int j = 0; j < CG; ++j) {  // independent loads: the id -> box chains overlap
+  for (int j = 0; j < CGN; ++j) {  // independent loads: the id -> box chains overlap
     const int64_t e = gc[j] * 32 + lane;
     fok[j] = gc[j] >= 0 && e >= off && e < off + cnt;
     fv[j] = fok[j] ? (BINNED ? A.bin_ids[e] : (int)e) : 0;
   }
 #pragma unroll
-  for (int j = 0; j < CG; ++j)
+  for (int j = 0; j < CGN; ++j)
     if (fok[j]) {
       ++cn.culls;
       fok[j] = box_ok<D>(blo, bhi, A.box[2 * (int64_t)fv[j]], A.box[2 * (int64_t)fv[j] + 1], reach2);
     }
   int nf = 0;
 #pragma unroll
-  for (int j = 0; j < CG; ++j) {
+  for (int j = 0; j < CGN; ++j) {
     const unsigned fm = __ballot_sync(0xffffffffu, fok[j]);
     if (fok[j]) {
       const int r = nf + __popc(fm & lanemask_lt());
@@ -351,7 +351,7 @@ __device__ __forceinline__ bool sweep_chunks(const MarkArgs& A, MarkSmem<D>& S, 
     if (npairs > PAIR_CAP - 64) {  // buffer nearly full: evaluate what we have
       __syncwarp();
       cn.evaluated += lane == 0 ? npairs : 0;
-      if (eval_pairs<D>(A, S, wid, lane, npairs, r2)) {
+      if (eval_pairs<D, CGN>(A, S, wid, lane, npairs, r2)) {
         cn.spheres += (unsigned long long)nact * (unsigned)(fi + 1);
         return true;
       }
@@ -362,7 +362,7 @@ __device__ __forceinline__ bool sweep_chunks(const MarkArgs& A, MarkSmem<D>& S, 
   cn.spheres += (unsigned long long)nact * (unsigned)nf;
   __syncwarp();
   cn.evaluated += lane == 0 ? npairs : 0;
-  const bool hit = eval_pairs<D>(A, S, wid, lane, npairs, r2);
+  const bool hit = eval_pairs<D, CGN>(A, S, wid, lane, npairs, r2);
   __syncwarp();
   return hit;
 }
@@ -380,8 +380,8 @@ __device__ __forceinline__ void flush_counts(const MarkArgs& A, MarkCounts& cn, 
   }
 }
 
-template <int D, bool BINNED>
-__device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M, MarkSmem<D>& S, int64_t pos,
+template <int D, bool BINNED, int CGN>
+__device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M, MarkSmem<D, CGN>& S, int64_t pos,
                                            int lane, int wid, MarkCounts& cn, unsigned long long& t_acc,
                                            unsigned long long& marked);
 
@@ -427,10 +427,10 @@ __device__ __forceinline__ bool block_may_hit(const MarkArgs& A, int id) {
 static __device__ __forceinline__ bool mark_prefilter_on(const MarkArgs& A) { return A.prefilter != 0; }
 
 // persistent over the level's leaves (the count may live on the device)
-template <int D, bool BINNED, int MINB = 6>
+template <int D, bool BINNED, int MINB = 6, int CGN = CG>
 __global__ void __launch_bounds__(MARK_THREADS, MINB) k_mark_blocks(MarkArgs A, MarkItems M) {
   ow_pdl_wait();
-  __shared__ MarkSmem<D> S;
+  __shared__ MarkSmem<D, CGN> S;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t lo = A.d_slice ? A.d_slice[0] : 0;
   const int64_t n = A.d_slice ? A.d_slice[1] : (A.d_n ? *A.d_n : A.n_leaves);
@@ -465,10 +465,10 @@ __global__ void __launch_bounds__(MARK_THREADS, MINB) k_mark_blocks(MarkArgs A, 
         while (m) {
           const int j = __ffs(m) - 1;
           m &= m - 1;
-          mark_block<D, BINNED>(A, M, S, base + j, lane, wid, cn, t_acc, marked);
+          mark_block<D, BINNED, CGN>(A, M, S, base + j, lane, wid, cn, t_acc, marked);
         }
       } else {
-        for (int64_t j = 0; j < K && base + j < n; ++j) mark_block<D, BINNED>(A, M, S, base + j, lane, wid, cn, t_acc, marked);
+        for (int64_t j = 0; j < K && base + j < n; ++j) mark_block<D, BINNED, CGN>(A, M, S, base + j, lane, wid, cn, t_acc, marked);
       }
       nxt = __shfl_sync(0xffffffffu, nn, 0);
     }
@@ -488,11 +488,11 @@ __global__ void __launch_bounds__(MARK_THREADS, MINB) k_mark_blocks(MarkArgs A, 
       while (m) {
         const int j = __ffs(m) - 1;
         m &= m - 1;
-        mark_block<D, BINNED>(A, M, S, lo + gw + (k0 + j) * G, lane, wid, cn, t_acc, marked);
+        mark_block<D, BINNED, CGN>(A, M, S, lo + gw + (k0 + j) * G, lane, wid, cn, t_acc, marked);
       }
     }
   } else {
-    for (int64_t pos = lo + gw; pos < n; pos += G) mark_block<D, BINNED>(A, M, S, pos, lane, wid, cn, t_acc, marked);
+    for (int64_t pos = lo + gw; pos < n; pos += G) mark_block<D, BINNED, CGN>(A, M, S, pos, lane, wid, cn, t_acc, marked);
   }
   flush_counts(A, cn, lane);
   if (lane == 0) {
@@ -501,8 +501,8 @@ __global__ void __launch_bounds__(MARK_THREADS, MINB) k_mark_blocks(MarkArgs A, 
   }
 }
 
-template <int D, bool BINNED>
-__device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M, MarkSmem<D>& S, int64_t pos,
+template <int D, bool BINNED, int CGN>
+__device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M, MarkSmem<D, CGN>& S, int64_t pos,
                                            int lane, int wid, MarkCounts& cn, unsigned long long& t_acc,
                                            unsigned long long& marked) {
   constexpr int CPL = D == 3 ? 2 : 1;
@@ -512,7 +512,7 @@ __device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M
   float p[CPL][3];
   int bin[CPL];
   block_cells<D, BINNED>(A, id, lane, blo, bhi, p, bin);
-  share_cells<D>(S, wid, lane, p);
+  share_cells<D, CGN>(S, wid, lane, p);
   unsigned long long t = 0;
 #pragma unroll
   for (int k = 0; k < CPL; ++k)
@@ -558,16 +558,16 @@ __device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M
       unsigned cm = __ballot_sync(0xffffffffu, cok);
       if (cm && inline_left) {
         inline_left = false;
-        int64_t gc[CG];
+        int64_t gc[CGN];
 #pragma unroll
-        for (int j = 0; j < CG; ++j) {
+        for (int j = 0; j < CGN; ++j) {
           gc[j] = -1;
           if (cm) {
             gc[j] = gb + __ffs(cm) - 1;
             cm &= cm - 1;
           }
         }
-        hit = sweep_chunks<D, BINNED>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, p, act, cn);
+        hit = sweep_chunks<D, BINNED, CGN>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, p, act, cn);
         if (hit) break;
       }
       if (cm) {  // the rest: (block, chunk, bin) items for the flat pass
@@ -579,16 +579,16 @@ __device__ __forceinline__ void mark_block(const MarkArgs& A, const MarkItems& M
         } else {
           // item list full: this warp sweeps its remaining chunks itself
           while (cm && !hit) {
-            int64_t gc[CG];
+            int64_t gc[CGN];
 #pragma unroll
-            for (int j = 0; j < CG; ++j) {
+            for (int j = 0; j < CGN; ++j) {
               gc[j] = -1;
               if (cm) {
                 gc[j] = gb + __ffs(cm) - 1;
                 cm &= cm - 1;
               }
             }
-            hit = sweep_chunks<D, BINNED>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, p, act, cn);
+            hit = sweep_chunks<D, BINNED, CGN>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, p, act, cn);
           }
         }
       }
@@ -628,7 +628,7 @@ __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_items(MarkArgs A, Mark
     float p[CPL][3];
     int bin[CPL];
     block_cells<D, BINNED>(A, id, lane, blo, bhi, p, bin);
-    share_cells<D>(S, wid, lane, p);
+    share_cells<D, CG>(S, wid, lane, p);
     bool act[CPL];
 #pragma unroll
     for (int k = 0; k < CPL; ++k) act[k] = bin[k] >= 0 && (!BINNED || bin[k] == b);
@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(MARK_THREADS, 6) k_mark_items(MarkArgs A, Mark
 #pragma unroll
     for (int j = 0; j < CG; ++j) gc[j] = j == 0 ? (int64_t)item.y : -1;
     const bool hit =
-        sweep_chunks<D, BINNED>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, p, act, cn);
+        sweep_chunks<D, BINNED, CG>(A, S, wid, lane, gc, off, cnt, blo, bhi, reach2, r2, p, act, cn);
     if (hit && lane == 0 && atomicOr(&M.hit[pos], 1u) == 0u) {
       A.F.marks[id] = OW_MARKED;
       ++marked;
@@ -813,11 +813,23 @@ static int mark_minb() {
   }();
   return v;
 }
+// first level whose 3D binned block pass sweeps 8 chunks inline
+// (OW_MARK_CG8_FROM: A/B, 99 = never; tools/ab_markcg8.sh on one B200: from
+// level 2, C3 1.521 -> 1.439 ms, C4 2.100 -> 2.026; C2 / C5 mark levels 0-1
+// only, where 8 inline chunks were slower: C2 0.319 -> 0.328 and C5 3.54 ->
+// 3.73 ms with 8 on every level)
+static int mark_cg8_from() {
+  static const int v = [] {
+    const char* e = getenv("OW_MARK_CG8_FROM");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
 int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n_leaves, const float* d_coords,
                    int64_t n_faces, int64_t geom_key, const ow_grid* grid, const int32_t* d_bin_ids,
                    const int32_t* d_bin_counts, const int32_t* d_bin_offsets, int64_t n_bin_entries, float d_spec,
                    double reach, unsigned long long* out, cudaStream_t s, const int64_t* d_n_leaves,
-                   bool chunk_boxes_ready, const int64_t* d_slice, const int64_t* d_bin_entries) {
+                   bool chunk_boxes_ready, const int64_t* d_slice, const int64_t* d_bin_entries, int level) {
   if (!(d_spec > 0.0f)) {
     ow_set_error("near-wall distance must be positive, got %g", (double)d_spec);
     return OW_ERR_INVALID;
@@ -905,7 +917,10 @@ int ow_mark_launch(ow_ctx* ctx, ow_forest* f, const int32_t* d_leaves, int64_t n
   const int gi = 8 * OW_SMS;
   if (f->dim == 3) {
     if (binned) {
-      if (mark_minb() == 8) ow_launch(k_mark_blocks<3, true, 8>, grd, MARK_THREADS, 0, s, A, M);
+      // inline chunks per block: 8 from level mark_cg8_from() on (deeper
+      // levels: small blocks inside large bins), 4 above
+      if (level >= mark_cg8_from()) ow_launch(k_mark_blocks<3, true, 6, 8>, grd, MARK_THREADS, 0, s, A, M);
+      else if (mark_minb() == 8) ow_launch(k_mark_blocks<3, true, 8>, grd, MARK_THREADS, 0, s, A, M);
       else if (mark_minb() == 7) ow_launch(k_mark_blocks<3, true, 7>, grd, MARK_THREADS, 0, s, A, M);
       else ow_launch(k_mark_blocks<3, true>, grd, MARK_THREADS, 0, s, A, M);
       ow_launch(k_mark_items<3, true>, gi, MARK_THREADS, 0, s, A, M);

@@ -357,7 +357,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
       OW_TRY(ow_mark_launch(ctx, f, (const int32_t*)pl, n_host, d_coords, n_faces, geom_key,
                             p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
                             p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
-                            p->binned ? E : 0, p->d_spec, p->reach, dst, s, dn, !fresh_bins, slice));
+                            p->binned ? E : 0, p->d_spec, p->reach, dst, s, dn, !fresh_bins, slice, nullptr, level));
       OW_TRY(ow_comm_exchange_marks(ctx, comm, (const int32_t*)pl, f->d_marks, slice, dn, n_host, dst, 5, s));
     } else if (p->world > 1) {
       // sharded marking: each rank marks a contiguous slice, then the exchange
@@ -371,7 +371,8 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
       OW_TRY(ow_mark_launch(ctx, f, (const int32_t*)pl + lo, hi - lo, d_coords, n_faces, geom_key,
                             p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
                             p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
-                            p->binned ? E : 0, p->d_spec, p->reach, dst, s, nullptr, !fresh_bins));
+                            p->binned ? E : 0, p->d_spec, p->reach, dst, s, nullptr, !fresh_bins, nullptr, nullptr,
+                            level));
       if (!p->exchange) {
         ow_set_error("refine_near_wall: world > 1 needs an exchange callback");
         return OW_ERR_INVALID;
@@ -394,7 +395,7 @@ int refine_driver(ow_ctx* ctx, ow_forest* f, const float* d_coords, int64_t n_fa
                             p->binned ? grid : nullptr, p->binned ? d_bin_ids : nullptr,
                             p->binned ? d_bin_counts : nullptr, p->binned ? d_bin_offsets : nullptr,
                             p->binned ? E : 0, p->d_spec, p->reach, dst, s, dn, !fresh_bins, nullptr,
-                            devpass ? ctx->d_small + 5 : nullptr));
+                            devpass ? ctx->d_small + 5 : nullptr, level));
     }
     // ---- propagation (binned only): 1 + floor(d / min block length)
     OW_TRY(record(se, level, 2, s, ctx->no_stage_events));
