@@ -185,7 +185,9 @@ __global__ void k_chunk_boxes(const int32_t* __restrict__ ids, int64_t n_entries
 }
 
 // Marking, two flat passes so no block's work is one long serial chain:
-//  k_mark_blocks : warp per leaf block.  Cell centres (FP64 -> one FP32
+//  k_mark_blocks : warp per leaf block (runs of blocks taken from a per-pass
+//                  counter; runs of several blocks are first prefiltered one
+//                  block per lane, block_may_hit).  Cell centres (FP64 -> one FP32
 //                  rounding) and bins, the algorithmic test count T; per
 //                  distinct bin of its cells, the 32-entry bin chunks whose union
 //                  box passes the reference's FP64 box cull.  The first CG
@@ -204,7 +206,7 @@ constexpr int MARK_WARPS = MARK_THREADS / 32;
 #ifndef OW_MARK_CG
 #define OW_MARK_CG 4
 #endif
-constexpr int CG = OW_MARK_CG;  // chunks swept inline by the block pass
+constexpr int CG = OW_MARK_CG;  // chunks swept inline by the block pass (levels 0-1; 8 from mark_cg8_from())
 
 struct MarkCounts {
   unsigned long long evaluated = 0, spheres = 0, culls = 0;
