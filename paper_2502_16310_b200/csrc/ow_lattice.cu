@@ -1125,32 +1125,58 @@ int lat_bscan(ow_ctx* ctx, const LatArgs& A, int64_t n_bound, int64_t* nb_total,
 // misses; flagged entries start at +big and receive min t from k_lat_hits).
 // CTA per candidate block: the block's q rows are one contiguous run, written
 // linearly (coalesced) from the flags staged in shared memory.
+// The loop is software-pipelined: the header (mask, block, row offset) of the
+// CTA's block two iterations ahead and the flag word of the next one are
+// loaded before the current block is written, so the two dependent loads of
+// a block overlap the stores of the ones before it.
 template <int D>
 __global__ void k_lat_emit(LatArgs A) {
   ow_pdl_wait();
   constexpr int C = D == 3 ? 64 : 16;
   __shared__ unsigned s_fl[C];
   const int64_t ncb = *A.n_cb_d;
-  for (int64_t r = blockIdx.x; r < ncb; r += gridDim.x) {
-  const unsigned long long m = A.bmask[r];
   const int c = threadIdx.x;
-  const int64_t pos = A.cand_blocks[r];
-  const int64_t row0 = A.boff[r];
-  const int nrow = __popcll(m), nq = A.nq;
-  if (row0 + nrow > A.out_row_cap) continue;  // (uniform per CTA; the host re-runs with room)
-  if ((m >> c) & 1ull) {
-    const int k = __popcll(m & ((1ull << c) - 1ull));
-    s_fl[k] = A.flags[pos * C + c];
-    A.cells_out[row0 + k] = pos * C + c;
-    if (A.rows_out) A.rows_out[row0 + k] = make_uint2((unsigned)(pos * C + c), s_fl[k]);
-  }
-  __syncthreads();
-  float* q = A.q_out + row0 * nq;
-  for (int i = c; i < nrow * nq; i += C) {
-    const int k = i / nq, d = i - k * nq;
-    q[i] = ((s_fl[k] >> d) & 1u) ? __uint_as_float(0x7f7f7f7fu) : -1.0f;
-  }
-  __syncthreads();  // s_fl is rewritten by the next block
+  const int nq = A.nq;
+  const int64_t G = gridDim.x;
+  struct Hdr {
+    unsigned long long m;
+    int64_t pos, row0;
+  };
+  auto header = [&](int64_t r) {
+    Hdr h{0ull, 0, 0};
+    if (r < ncb) h = Hdr{A.bmask[r], (int64_t)A.cand_blocks[r], A.boff[r]};
+    return h;
+  };
+  auto flag = [&](int64_t r, const Hdr& h) {
+    return (r < ncb && ((h.m >> c) & 1ull)) ? A.flags[h.pos * C + c] : 0u;
+  };
+  int64_t r = blockIdx.x;
+  Hdr h0 = header(r), h1 = header(r + G);
+  unsigned f0 = flag(r, h0);
+  for (; r < ncb; r += G) {
+    const Hdr h2 = header(r + 2 * G);  // two blocks ahead
+    const unsigned f1 = flag(r + G, h1);  // the next block's flag word
+    const unsigned long long m = h0.m;
+    const int64_t pos = h0.pos, row0 = h0.row0;
+    const int nrow = __popcll(m);
+    if (row0 + nrow <= A.out_row_cap) {  // (uniform per CTA; past the cap the host re-runs with room)
+      if ((m >> c) & 1ull) {
+        const int k = __popcll(m & ((1ull << c) - 1ull));
+        s_fl[k] = f0;
+        A.cells_out[row0 + k] = pos * C + c;
+        if (A.rows_out) A.rows_out[row0 + k] = make_uint2((unsigned)(pos * C + c), f0);
+      }
+      __syncthreads();
+      float* q = A.q_out + row0 * nq;
+      for (int i = c; i < nrow * nq; i += C) {
+        const int k = i / nq, d = i - k * nq;
+        q[i] = ((s_fl[k] >> d) & 1u) ? __uint_as_float(0x7f7f7f7fu) : -1.0f;
+      }
+      __syncthreads();  // s_fl is rewritten by the next block
+    }
+    h0 = h1;
+    h1 = h2;
+    f0 = f1;
   }
 }
 
@@ -1283,6 +1309,19 @@ unsigned lat_face_grid(int64_t n_faces) {
   const int64_t need = (n_faces + 4 * FPW - 1) / (4 * FPW);
   const int64_t cap = (int64_t)per_sm * OW_SMS;
   return (unsigned)(need < cap ? need : cap);
+}
+
+// k_lat_emit: resident CTAs only (32 per SM of 64 / 16 threads), so each CTA
+// walks several candidate blocks and its software pipeline has work to
+// overlap (OW_LAT_EMIT_CTAS_PER_SM: A/B, 0 = one CTA per candidate block)
+unsigned emit_grid(unsigned g) {
+  static const int per_sm = [] {
+    const char* e = getenv("OW_LAT_EMIT_CTAS_PER_SM");
+    return e ? atoi(e) : 32;
+  }();
+  if (per_sm <= 0) return g;
+  const unsigned cap = (unsigned)per_sm * OW_SMS;
+  return g < cap ? g : cap;
 }
 
 int inline_units_setting(const ow_ctx* ctx) {
@@ -1640,11 +1679,11 @@ int ow_lattice_dev_emit(ow_ctx* ctx, int64_t* d_cells, float* d_q, int64_t row_c
   if (d_q_packed)
     OW_TRY(scan(ctx, BcountLoad{A.hcount, A.n_cb_d}, BoffStore{A.hoff, A.n_cb_d}, nl, ctx->d_small + 36, s));
   if (ctx->lat_forest.dim == 3) {
-    ow_launch(k_lat_emit<3>, g, C, 0, s, A);
+    ow_launch(k_lat_emit<3>, emit_grid(g), C, 0, s, A);
     ow_launch(k_lat_hits<3>, 8 * OW_SMS, 256, 0, s, A);
     if (d_q_packed) ow_launch(k_lat_pack<3>, g, C, 0, s, A);
   } else {
-    ow_launch(k_lat_emit<2>, g, C, 0, s, A);
+    ow_launch(k_lat_emit<2>, emit_grid(g), C, 0, s, A);
     ow_launch(k_lat_hits<2>, 8 * OW_SMS, 256, 0, s, A);
     if (d_q_packed) ow_launch(k_lat_pack<2>, g, C, 0, s, A);
   }
@@ -1681,10 +1720,10 @@ extern "C" int ow_lattice_links_emit_packed(ow_ctx* ctx, int64_t* d_cells, float
     OW_TRY(scan(ctx, ow::LoadArr<int32_t>{A.hcount}, ow::StoreExcl<int64_t>{A.hoff}, ctx->lat_ncb,
                 ctx->d_small + 36, s));
   if (ctx->lat_forest.dim == 3) {
-    ow_launch(k_lat_emit<3>, (unsigned)ctx->lat_ncb, C, 0, s, A);
+    ow_launch(k_lat_emit<3>, emit_grid((unsigned)ctx->lat_ncb), C, 0, s, A);
     ow_launch(k_lat_hits<3>, 8 * OW_SMS, 256, 0, s, A);
   } else {
-    ow_launch(k_lat_emit<2>, (unsigned)ctx->lat_ncb, C, 0, s, A);
+    ow_launch(k_lat_emit<2>, emit_grid((unsigned)ctx->lat_ncb), C, 0, s, A);
     ow_launch(k_lat_hits<2>, 8 * OW_SMS, 256, 0, s, A);
   }
   if (ctx->lat_comm && ctx->lat_comm->world > 1) {
