@@ -474,10 +474,31 @@ struct FlagCompactClear {  // compaction that also clears the flags it consumed
 // the same round never counts — so every round sees exactly the marks the
 // reference's round does, and one promote after the last round turns the
 // tags into MARKED (rounds + 1 launches instead of 2 rounds).
+// (levels of at most side_max leaves: a thread per (leaf, side), so a leaf's
+// up to 2D neighbour descents run in parallel instead of one after another;
+// every side that finds a marked neighbour writes the same tag, and
+// counts_marked never counts this round's tag, so the result is the per-leaf
+// loop's.  Larger levels keep a thread per leaf: they fill the GPU anyway
+// and the per-leaf early exit saves descents)
 __global__ void k_prop_gather_dev(ForestC F, const int32_t* __restrict__ leaves, const int64_t* n, int tag,
-                                  int below) {
+                                  int below, int64_t side_max) {
   ow_pdl_wait();
   const int64_t nn = *n;
+  if (nn <= side_max) {
+    const int ns = 2 * F.dim;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn * ns;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int id = leaves[i / ns];
+      const int sd = (int)(i % ns);
+      if (F.marks[id] != OW_NONE) continue;
+      const int L = F.level[id];
+      int32_t c[3] = {F.coord[0][id], F.dim > 1 ? F.coord[1][id] : 0, F.dim > 2 ? F.coord[2][id] : 0};
+      int32_t nc[3];
+      if (!side_target(F, L, c, sd, nc)) continue;
+      if (side_has_marked(F, L, nc, sd, below)) F.marks[id] = (int8_t)tag;
+    }
+    return;
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
     const int id = leaves[i];
     if (F.marks[id] != OW_NONE) continue;
@@ -515,6 +536,19 @@ int ow_forest_leaves_dev(ow_ctx* ctx, const ow_forest* f, int32_t level, int32_t
   return scan01(ctx, LeafLoad{f->d_level, f->d_first_child, level}, CompactStore{d_out}, f->n_blocks, d_count, s);
 }
 
+// largest level whose propagation gather runs a thread per (leaf, side)
+// (OW_PROP_SIDES_MAX, A/B; 0: always per leaf).  tools/ab_prop.sh on one
+// B200, per (leaf, side) on every level vs per leaf: C1 0.287 -> 0.252 ms,
+// C2 0.320 -> 0.311, C3 1.454 -> 1.431, C4 2.050 -> 2.034, but C5 (levels of
+// 262 144 and 178 112 leaves) 3.559 -> 3.574
+static int64_t prop_side_max() {
+  static const int64_t v = [] {
+    const char* e = getenv("OW_PROP_SIDES_MAX");
+    return e ? (int64_t)atoll(e) : (int64_t)131072;
+  }();
+  return v;
+}
+
 int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, const int64_t* d_n, int64_t n_bound,
                      int32_t rounds, cudaStream_t s, bool tags, bool defer_promote) {
   if (n_bound <= 0 || rounds <= 0) return OW_OK;
@@ -526,8 +560,8 @@ int ow_propagate_dev(ow_ctx* ctx, const ow_forest* f, const int32_t* d_leaves, c
   // length)).  Else the reference's round as is: INTERMEDIATE, then promote.
   for (int r = 0; r < rounds; ++r) {
     const int tag = tags ? 3 + r % 100 : OW_INTERMEDIATE;
-    ow_launch(k_prop_gather_dev, ow_blocks(n_bound, 128, 16 * OW_SMS), 128, 0, s, F, d_leaves, d_n, tag,
-              tags ? tag : 0);
+    ow_launch(k_prop_gather_dev, ow_blocks(n_bound * 2 * f->dim, 128, 16 * OW_SMS), 128, 0, s, F, d_leaves, d_n, tag,
+              tags ? tag : 0, prop_side_max());
     ctx->launches += 1;
     if (!tags || r % 100 == 99 || (r + 1 == rounds && !defer_promote)) {
       ow_launch(k_prop_promote_dev, ow_blocks(n_bound, 256, 8 * OW_SMS), 256, 0, s, F.marks, d_leaves, d_n);
